@@ -1,0 +1,244 @@
+"""CPU ORACLE for the Sphinx selective-refinement hot path — TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and the ``cpu_baseline`` /
+``--impl reference`` legs of ``bench.py`` may import this package.  The product
+path (``paper_2511_18672_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in ``sphinx_oracle.c`` (plain C99, fp64, cited per
+function against PAPER.md / SPEC.md).  This module only marshals numpy arrays
+through ctypes.
+
+Parity status per function:
+  pixel_mask / maxpool / tile_blocks / block_mask   pinned (TV-1..5, brute force)
+  eq2 / select_k / start_step                       pinned (TV-6..8);
+                                                    the k-logic TABLE values are parity unpinned
+                                                    (Fig. k_logic is an image)
+  compact                                           pinned (popcount, brute-force order, identity)
+  noise                                             pinned (TV-9..11, Monte Carlo)
+  conv3x3_blocks / conv3x3_dense                    pinned (shift kernels, torch fp64 conv2d, linearity)
+  scatter                                           pinned (density 0/1, composition O7)
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
+SRC_FULL, SRC_COMPACT = 0, 1
+
+
+class KLogic(ctypes.Structure):
+    """Mirror of ``oracle_klogic``."""
+    _fields_ = [("m", ctypes.c_int32), ("thr", ctypes.c_double * 16),
+                ("step", ctypes.c_int32 * 16), ("fallback_k", ctypes.c_int32),
+                ("k_max", ctypes.c_int32)]
+
+
+def make_klogic(thr, steps, fallback_k=0, k_max=40):
+    lg = KLogic()
+    lg.m = len(thr)
+    for i, (t, s) in enumerate(zip(thr, steps)):
+        lg.thr[i] = float(t)
+        lg.step[i] = int(s)
+    lg.fallback_k = fallback_k
+    lg.k_max = k_max
+    return lg
+
+
+def build(force=False):
+    """Compile liboracle.so with gcc (no CUDA headers, no fast-math, no FMA contraction)."""
+    src = os.path.join(_HERE, "sphinx_oracle.c")
+    if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(src):
+        return _SO
+    cmd = ["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+           "-fno-fast-math", "-o", _SO, src, "-lm"]
+    subprocess.check_call(cmd)
+    return _SO
+
+
+def load():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        I = ctypes.c_int
+        F = ctypes.c_float
+        D = ctypes.c_double
+        sig = {
+            "oracle_pixel_mask": [P, P, P, F, I, I, I, P],
+            "oracle_maxpool": [P, I, I, I, I, P],
+            "oracle_tile_blocks": [P, I, I, I, I, P],
+            "oracle_block_mask": [P, P, P, F, I, I, I, I, I, I, P, P],
+            "oracle_start_step": [P, P, P, P, P, D, P, I, I, P],
+            "oracle_compact": [P, I, I, I, P, I, I, P, P],
+            "oracle_noise": [P, P, P, P, I, I, I, I, I, P, I, P, P, I],
+            "oracle_conv3x3_blocks": [P, P, P, I, I, I, I, I, I, P, I, P, P, I],
+            "oracle_conv3x3_dense": [P, P, P, I, I, I, I, I, P, P, I],
+            "oracle_scatter": [P, I, P, P, I, I, I, I, I, I, P, P, I, P, I],
+        }
+        for name, args in sig.items():
+            fn = getattr(_lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        _lib.oracle_eq2.argtypes = [D, D, D, D]
+        _lib.oracle_eq2.restype = D
+        _lib.oracle_select_k.argtypes = [P, D]
+        _lib.oracle_select_k.restype = ctypes.c_int32
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dt):
+    return None if a is None else np.ascontiguousarray(a, dtype=dt)
+
+
+def _check(rc, name):
+    if rc != 0:
+        raise ValueError(f"{name}: invalid argument (rc={rc})")
+
+
+def level_dims(hp, wp, f, b, n_levels):
+    """Geometry only: (H_l, W_l, Hb_l, Wb_l) per level (/f then /2 per level)."""
+    out = []
+    h, w = hp // f, wp // f
+    for l in range(n_levels):
+        out.append((h, w, -(-h // b), -(-w // b)))
+        h, w = h // 2, w // 2
+    return out
+
+
+def pixel_mask(O, U, tau_u, tau_o):
+    lib = load()
+    O = _c(O, np.float32); U = _c(U, np.float32); tau_u = _c(tau_u, np.float32)
+    n, hp, wp = O.shape
+    m = np.zeros((n, hp, wp), np.uint8)
+    _check(lib.oracle_pixel_mask(_p(O), _p(U), _p(tau_u), tau_o, n, hp, wp, _p(m)), "pixel_mask")
+    return m
+
+
+def maxpool(grid, f):
+    lib = load()
+    g = _c(grid, np.uint8)
+    n, h, w = g.shape
+    out = np.zeros((n, h // f, w // f), np.uint8)
+    _check(lib.oracle_maxpool(_p(g), n, h, w, f, _p(out)), "maxpool")
+    return out
+
+
+def tile_blocks(grid, b):
+    lib = load()
+    g = _c(grid, np.uint8)
+    n, h, w = g.shape
+    out = np.zeros((n, -(-h // b), -(-w // b)), np.uint8)
+    _check(lib.oracle_tile_blocks(_p(g), n, h, w, b, _p(out)), "tile_blocks")
+    return out
+
+
+def block_mask(O, U, tau_u, tau_o, f, b, n_levels):
+    """Returns (list of per-level u8 masks [n,Hb,Wb], counts int32 [n, n_levels])."""
+    lib = load()
+    O = _c(O, np.float32); U = _c(U, np.float32); tau_u = _c(tau_u, np.float32)
+    n, hp, wp = O.shape
+    dims = level_dims(hp, wp, f, b, n_levels)
+    sizes = [n * hb * wb for (_, _, hb, wb) in dims]
+    flat = np.zeros(sum(sizes), np.uint8)
+    counts = np.zeros((n, n_levels), np.int32)
+    _check(lib.oracle_block_mask(_p(O), _p(U), _p(tau_u), tau_o, n, hp, wp, f, b, n_levels,
+                                 _p(flat), _p(counts)), "block_mask")
+    masks, off = [], 0
+    for (sz, (_, _, hb, wb)) in zip(sizes, dims):
+        masks.append(flat[off:off + sz].reshape(n, hb, wb).copy())
+        off += sz
+    return masks, counts
+
+
+def eq2(c0, c1, t, gamma):
+    return load().oracle_eq2(c0, c1, t, gamma)
+
+
+def select_k(logic, r):
+    return load().oracle_select_k(ctypes.byref(logic), r)
+
+
+def start_step(q, c0, c1, t, gamma, logics, logic_id=None):
+    lib = load()
+    q = _c(q, np.float32); c0 = _c(c0, np.float32); c1 = _c(c1, np.float32); t = _c(t, np.float32)
+    lid = _c(logic_id, np.int32)
+    n = q.shape[0]
+    arr = (KLogic * len(logics))(*logics)
+    k = np.zeros(n, np.int32)
+    _check(lib.oracle_start_step(_p(q), _p(c0), _p(c1), _p(t), _p(lid), gamma,
+                                 ctypes.cast(arr, ctypes.c_void_p), len(logics), n, _p(k)),
+           "start_step")
+    return k
+
+
+def compact(mask, k=None, u=0, select=SELECT_ACTIVE, shape=None):
+    lib = load()
+    m = _c(mask, np.uint8) if mask is not None else None
+    n, hb, wb = m.shape if m is not None else shape
+    kk = _c(k, np.int32)
+    ids = np.zeros(max(n * hb * wb, 1), np.int32)
+    cnt = np.zeros(1, np.int32)
+    _check(lib.oracle_compact(_p(m), n, hb, wb, _p(kk), int(u), select, _p(ids), _p(cnt)), "compact")
+    return ids[:cnt[0]].copy()
+
+
+def noise(x0, eps, xt_in, b, ids, step, abar):
+    lib = load()
+    x0 = _c(x0, np.float32); eps = _c(eps, np.float32); xt_in = _c(xt_in, np.float32)
+    ids = _c(ids, np.int32); step = _c(step, np.int32); abar = _c(abar, np.float32)
+    n, h, w, c = x0.shape
+    out = np.zeros(x0.shape, np.float64)
+    _check(lib.oracle_noise(_p(x0), _p(eps), _p(xt_in), _p(out), n, h, w, c, b,
+                            _p(ids), len(ids), _p(step), _p(abar), len(abar) - 1), "noise")
+    return out
+
+
+def conv3x3_blocks(x_bf16bits, w_bf16bits, bias, b, ids, n_threads=0, y_init=None):
+    """x: uint16 [n,h,w,cin] bf16 bits; w: uint16 [cout,3,3,cin]; returns (y, absacc) fp64.
+    Pixels outside listed blocks hold y_init (default NaN) / NaN."""
+    lib = load()
+    x = _c(x_bf16bits, np.uint16); w = _c(w_bf16bits, np.uint16)
+    bias = _c(bias, np.float32); ids = _c(ids, np.int32)
+    n, h, wd, cin = x.shape
+    cout = w.shape[0]
+    y = np.full((n, h, wd, cout), np.nan) if y_init is None else np.array(y_init, np.float64)
+    a = np.full((n, h, wd, cout), np.nan)
+    _check(lib.oracle_conv3x3_blocks(_p(x), _p(w), _p(bias), n, h, wd, cin, cout, b,
+                                     _p(ids), len(ids), _p(y), _p(a), n_threads), "conv3x3_blocks")
+    return y, a
+
+
+def conv3x3_dense(x_bf16bits, w_bf16bits, bias, n_threads=0):
+    lib = load()
+    x = _c(x_bf16bits, np.uint16); w = _c(w_bf16bits, np.uint16); bias = _c(bias, np.float32)
+    n, h, wd, cin = x.shape
+    cout = w.shape[0]
+    y = np.zeros((n, h, wd, cout)); a = np.zeros((n, h, wd, cout))
+    _check(lib.oracle_conv3x3_dense(_p(x), _p(w), _p(bias), n, h, wd, cin, cout,
+                                    _p(y), _p(a), n_threads), "conv3x3_dense")
+    return y, a
+
+
+def scatter(src, cache, b, mask=None, k=None, u=0, ids=None, src_layout=SRC_FULL):
+    """Bit copy; src/cache any 2- or 4-byte dtype, NHWC (or COMPACT [count,b,b,c])."""
+    lib = load()
+    cache = np.ascontiguousarray(cache)
+    src = np.ascontiguousarray(src, dtype=cache.dtype)
+    n, h, w, c = cache.shape
+    out = np.empty_like(cache)
+    m = _c(mask, np.uint8); kk = _c(k, np.int32); ids = _c(ids, np.int32)
+    cnt = 0 if ids is None else len(ids)
+    _check(lib.oracle_scatter(_p(src), src_layout, _p(cache), _p(out), cache.dtype.itemsize,
+                              n, h, w, c, b, _p(m), _p(kk), int(u), _p(ids), cnt), "scatter")
+    return out

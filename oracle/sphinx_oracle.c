@@ -1,0 +1,368 @@
+/*
+ * sphinx_oracle.c — CPU ORACLE (test infrastructure only; see sphinx_oracle.h).
+ *
+ * Plain C99, fp64, scalar loops in the paper's order.  No blocking, fusion or
+ * reordering beyond what the definitions state.  OpenMP is used only to run
+ * independent output pixels of the convolution concurrently; every output
+ * element is still the same strictly ordered sum.
+ */
+#include "sphinx_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define BAD (-1)
+
+/* ---------------------------------------------------------------- a1 ---- */
+
+/* Alg1 line 9: M_op = 1[O < tau_o]; line 10: M = M_op v M_blur.
+ * P:447 "Pixels with opacity values below 0.5 or identified as blurry are selected".
+ * Reading R-9: a NaN is never "confident", so !(o >= tau_o) and !(u <= tau). */
+int oracle_pixel_mask(const float* O, const float* U, const float* tau_u, float tau_o,
+                      int n, int hp, int wp, uint8_t* m) {
+  if (!O || !m || n <= 0 || hp <= 0 || wp <= 0) return BAD;
+  if (!(tau_o >= 0.0f && tau_o <= 1.0f)) return BAD;
+  if (U && !tau_u) return BAD;
+  for (int i = 0; i < n; ++i) {
+    for (int y = 0; y < hp; ++y) {
+      for (int x = 0; x < wp; ++x) {
+        size_t p = ((size_t)i * hp + y) * wp + x;
+        int m_op = !(O[p] >= tau_o);
+        int m_blur = 0;
+        if (U) m_blur = !(U[p] <= tau_u[i]);
+        m[p] = (uint8_t)(m_op || m_blur);
+      }
+    }
+  }
+  return 0;
+}
+
+/* P:489 "the confidence mask is downsampled using max-pooling at each layer";
+ * S:246 non-overlapping window, 1 iff any input pixel is 1. */
+int oracle_maxpool(const uint8_t* in, int n, int h, int w, int f, uint8_t* out) {
+  if (!in || !out || n <= 0 || h <= 0 || w <= 0 || f <= 0) return BAD;
+  if (h % f != 0 || w % f != 0) return BAD;
+  int ho = h / f, wo = w / f;
+  for (int i = 0; i < n; ++i)
+    for (int y = 0; y < ho; ++y)
+      for (int x = 0; x < wo; ++x) {
+        uint8_t v = 0;
+        for (int dy = 0; dy < f; ++dy)
+          for (int dx = 0; dx < f; ++dx)
+            if (in[((size_t)i * h + y * f + dy) * w + x * f + dx]) v = 1;
+        out[((size_t)i * ho + y) * wo + x] = v;
+      }
+  return 0;
+}
+
+/* P:352 "tiles the feature maps into blocks ... Each block is marked for
+ * refinement if it contains at least one pixel within the refinement mask";
+ * S:253 last row/col blocks may be smaller (reading R-2). */
+int oracle_tile_blocks(const uint8_t* grid, int n, int h, int w, int b, uint8_t* out) {
+  if (!grid || !out || n <= 0 || h <= 0 || w <= 0 || b <= 0) return BAD;
+  int hb = (h + b - 1) / b, wb = (w + b - 1) / b;
+  for (int i = 0; i < n; ++i)
+    for (int by = 0; by < hb; ++by)
+      for (int bx = 0; bx < wb; ++bx) {
+        uint8_t v = 0;
+        for (int y = by * b; y < by * b + b && y < h; ++y)
+          for (int x = bx * b; x < bx * b + b && x < w; ++x)
+            if (grid[((size_t)i * h + y) * w + x]) v = 1;
+        out[((size_t)i * hb + by) * wb + bx] = v;
+      }
+  return 0;
+}
+
+int oracle_block_mask(const float* O, const float* U, const float* tau_u, float tau_o,
+                      int n, int hp, int wp, int f, int b, int n_levels,
+                      uint8_t* masks, int32_t* counts) {
+  if (!O || !masks || n <= 0 || hp <= 0 || wp <= 0 || f <= 0 || b <= 0) return BAD;
+  if (n_levels < 1 || n_levels > 4) return BAD;
+  if (hp % f != 0 || wp % f != 0) return BAD;
+  int h0 = hp / f, w0 = wp / f;
+  int div = 1 << (n_levels - 1);
+  if (h0 % div != 0 || w0 % div != 0) return BAD;
+
+  size_t npx = (size_t)n * hp * wp;
+  uint8_t* pix = (uint8_t*)malloc(npx);
+  uint8_t* cur = (uint8_t*)malloc((size_t)n * h0 * w0);
+  uint8_t* nxt = (uint8_t*)malloc((size_t)n * h0 * w0);
+  if (!pix || !cur || !nxt) { free(pix); free(cur); free(nxt); return -2; }
+  int rc = oracle_pixel_mask(O, U, tau_u, tau_o, n, hp, wp, pix); /* Alg1 lines 9-10 */
+  if (rc == 0) rc = oracle_maxpool(pix, n, hp, wp, f, cur);      /* VAE /8 */
+  size_t off = 0;
+  int hl = h0, wl = w0;
+  for (int l = 0; rc == 0 && l < n_levels; ++l) {
+    if (l > 0) { /* UNet level l: max-pool by 2 */
+      rc = oracle_maxpool(cur, n, hl, wl, 2, nxt);
+      hl /= 2; wl /= 2;
+      uint8_t* t = cur; cur = nxt; nxt = t;
+      if (rc) break;
+    }
+    int hb = (hl + b - 1) / b, wb = (wl + b - 1) / b;
+    rc = oracle_tile_blocks(cur, n, hl, wl, b, masks + off);
+    if (rc) break;
+    if (counts) {
+      for (int i = 0; i < n; ++i) {
+        int32_t c = 0;
+        for (int j = 0; j < hb * wb; ++j) c += masks[off + (size_t)i * hb * wb + j];
+        counts[i * n_levels + l] = c;
+      }
+    }
+    off += (size_t)n * hb * wb;
+  }
+  free(pix); free(cur); free(nxt);
+  return rc;
+}
+
+/* ---------------------------------------------------------------- a2 ---- */
+
+/* Eq. 2: Q* = c0 + (c1 - c0) f(t); f = t^gamma if c1 >= c0,
+ * else 1 - (1 - t)^gamma.  Literal transcription (reading R-11). */
+double oracle_eq2(double c0, double c1, double t, double gamma) {
+  double f;
+  if (c1 >= c0) f = pow(t, gamma);
+  else f = 1.0 - pow(1.0 - t, gamma);
+  return c0 + (c1 - c0) * f;
+}
+
+/* S:143 k = steps[i] for the largest i with thresholds[i] <= r (left-closed,
+ * S:166); fallback_k if r is below all; clamp to k_max ("largest k=40"). */
+int32_t oracle_select_k(const oracle_klogic* lg, double r) {
+  int32_t k = lg->fallback_k;
+  for (int i = 0; i < lg->m; ++i)
+    if (lg->thr[i] <= r) k = lg->step[i];
+  if (k > lg->k_max) k = lg->k_max;
+  return k;
+}
+
+int oracle_start_step(const float* q, const float* c0, const float* c1, const float* t,
+                      const int32_t* logic_id, double gamma,
+                      const oracle_klogic* logics, int n_logics, int n, int32_t* k) {
+  if (!q || !c0 || !c1 || !t || !logics || !k || n <= 0 || n_logics < 1) return BAD;
+  if (!(gamma > 0.0 && gamma <= 1.0)) return BAD;
+  for (int j = 0; j < n_logics; ++j) {
+    const oracle_klogic* lg = &logics[j];
+    if (lg->m < 1 || lg->m > 16) return BAD;
+    for (int i = 1; i < lg->m; ++i)
+      if (!(lg->thr[i - 1] < lg->thr[i]) || lg->step[i - 1] > lg->step[i]) return BAD;
+  }
+  for (int i = 0; i < n; ++i) {
+    int lid = logic_id ? logic_id[i] : 0;
+    double ti = (double)t[i];
+    if (lid < 0 || lid >= n_logics || !(ti >= 0.0 && ti <= 1.0)) { k[i] = -1; continue; }
+    double qs = oracle_eq2((double)c0[i], (double)c1[i], ti, gamma); /* Alg1 line 4 */
+    if (!(qs > 0.0)) { k[i] = -1; continue; }
+    double r = (double)q[i] / qs;                                    /* Alg1 line 5 */
+    if (r != r) { k[i] = -1; continue; }
+    k[i] = oracle_select_k(&logics[lid], r);                         /* Alg1 line 6 */
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- a3 ---- */
+
+int oracle_compact(const uint8_t* mask, int n, int hb, int wb, const int32_t* k, int u,
+                   int select, int32_t* ids, int32_t* count) {
+  if (!ids || !count || n <= 0 || hb <= 0 || wb <= 0) return BAD;
+  if (select < 0 || select > 2) return BAD;
+  if (select == 0 && !mask) return BAD;
+  if (select == 1 && !k) return BAD;
+  int32_t c = 0;
+  for (int i = 0; i < n; ++i)
+    for (int by = 0; by < hb; ++by)
+      for (int bx = 0; bx < wb; ++bx) {
+        int32_t id = (i * hb + by) * wb + bx;
+        int take;
+        if (select == 0)      /* A_u = 1[k <= u] (Alg1 line 17) and M (Alg1 line 18) */
+          take = mask[id] && (!k || (k[i] >= 0 && k[i] <= u));
+        else if (select == 1) /* frames not in A_u are resampled (Alg1 line 19) */
+          take = k[i] > u;
+        else
+          take = !k || k[i] >= 0;
+        if (take) ids[c++] = id;
+      }
+  *count = c;
+  return 0;
+}
+
+/* ---------------------------------------------------------------- a4 ---- */
+
+/* add_noise (Alg1 lines 12, 19): z_u = sqrt(abar[u]) z0 + sqrt(1 - abar[u]) eps
+ * (BASELINE north_star).  u = 0 noisiest, u = S clean. */
+int oracle_noise(const float* x0, const float* eps, const float* xt_in, double* out,
+                 int n, int h, int w, int c, int b, const int32_t* ids, int count,
+                 const int32_t* step, const float* abar, int total_steps) {
+  if (!x0 || !eps || !xt_in || !out || !step || !abar) return BAD;
+  if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || b <= 0 || count < 0 || total_steps < 2) return BAD;
+  if (count > 0 && !ids) return BAD;
+  size_t total = (size_t)n * h * w * c;
+  for (size_t e = 0; e < total; ++e) out[e] = (double)xt_in[e];
+  int hb = (h + b - 1) / b, wb = (w + b - 1) / b;
+  for (int j = 0; j < count; ++j) {
+    int id = ids[j];
+    int i = id / (hb * wb), by = (id / wb) % hb, bx = id % wb;
+    int u = step[i];
+    if (u < 0 || u > total_steps) continue; /* left untouched */
+    double ab = (double)abar[u];
+    double a = sqrt(ab), s = sqrt(1.0 - ab);
+    for (int y = by * b; y < by * b + b && y < h; ++y)
+      for (int x = bx * b; x < bx * b + b && x < w; ++x)
+        for (int ch = 0; ch < c; ++ch) {
+          size_t e = (((size_t)i * h + y) * w + x) * c + ch;
+          out[e] = a * (double)x0[e] + s * (double)eps[e];
+        }
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- a5 ---- */
+
+static double bf16_to_double(uint16_t v) {
+  uint32_t bits = (uint32_t)v << 16; /* bf16 is the top half of an IEEE binary32 */
+  float f;
+  memcpy(&f, &bits, sizeof f);
+  return (double)f;
+}
+
+/* y[n,p,co] = bias[co] + sum_{dy,dx} sum_ci W[co,dy+1,dx+1,ci] x[n,p+(dy,dx),ci],
+ * x = 0 outside the image (reading R-17).  Order: taps row-major, then ci. */
+static void conv_pixel(const double* xd, const double* wd, const float* bias,
+                       int i, int y, int x, int h, int w, int cin, int cout,
+                       double* yo, double* ao) {
+  for (int co = 0; co < cout; ++co) {
+    double acc = bias ? (double)bias[co] : 0.0;
+    double aab = bias ? fabs((double)bias[co]) : 0.0;
+    for (int ky = 0; ky < 3; ++ky) {
+      int yy = y + ky - 1;
+      if (yy < 0 || yy >= h) continue;
+      for (int kx = 0; kx < 3; ++kx) {
+        int xx = x + kx - 1;
+        if (xx < 0 || xx >= w) continue;
+        const double* xp = xd + (((size_t)i * h + yy) * w + xx) * cin;
+        const double* wp = wd + (((size_t)co * 3 + ky) * 3 + kx) * cin;
+        for (int ci = 0; ci < cin; ++ci) {
+          double p = wp[ci] * xp[ci];
+          acc += p;
+          aab += fabs(p);
+        }
+      }
+    }
+    yo[co] = acc;
+    if (ao) ao[co] = aab;
+  }
+}
+
+static double* widen(const uint16_t* v, size_t cnt) {
+  double* d = (double*)malloc(cnt * sizeof(double));
+  if (!d) return NULL;
+  for (size_t j = 0; j < cnt; ++j) d[j] = bf16_to_double(v[j]);
+  return d;
+}
+
+int oracle_conv3x3_blocks(const uint16_t* x, const uint16_t* wt, const float* bias,
+                          int n, int h, int w, int cin, int cout, int b,
+                          const int32_t* ids, int count, double* y, double* absacc,
+                          int n_threads) {
+  if (!x || !wt || !y || n <= 0 || h <= 0 || w <= 0 || cin <= 0 || cout <= 0 || b <= 0) return BAD;
+  if (count < 0 || (count > 0 && !ids)) return BAD;
+  int hb = (h + b - 1) / b, wb = (w + b - 1) / b;
+  for (int j = 0; j < count; ++j)
+    if (ids[j] < 0 || ids[j] >= n * hb * wb) return BAD;
+  double* xd = widen(x, (size_t)n * h * w * cin);
+  double* wd = widen(wt, (size_t)cout * 9 * cin);
+  if (!xd || !wd) { free(xd); free(wd); return -2; }
+  long total = (long)count * b * b;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (long q = 0; q < total; ++q) {
+    int j = (int)(q / (b * b));
+    int p = (int)(q % (b * b));
+    int id = ids[j];
+    int i = id / (hb * wb), by = (id / wb) % hb, bx = id % wb;
+    int yy = by * b + p / b, xx = bx * b + p % b;
+    if (yy >= h || xx >= w) continue; /* truncated edge block (reading R-2) */
+    size_t o = (((size_t)i * h + yy) * w + xx) * cout;
+    conv_pixel(xd, wd, bias, i, yy, xx, h, w, cin, cout, y + o, absacc ? absacc + o : NULL);
+  }
+  free(xd); free(wd);
+  return 0;
+}
+
+int oracle_conv3x3_dense(const uint16_t* x, const uint16_t* wt, const float* bias,
+                         int n, int h, int w, int cin, int cout,
+                         double* y, double* absacc, int n_threads) {
+  if (!x || !wt || !y || n <= 0 || h <= 0 || w <= 0 || cin <= 0 || cout <= 0) return BAD;
+  double* xd = widen(x, (size_t)n * h * w * cin);
+  double* wd = widen(wt, (size_t)cout * 9 * cin);
+  if (!xd || !wd) { free(xd); free(wd); return -2; }
+  long total = (long)n * h * w;
+#ifdef _OPENMP
+  if (n_threads > 0) omp_set_num_threads(n_threads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (long q = 0; q < total; ++q) {
+    int i = (int)(q / ((long)h * w));
+    int yy = (int)((q / w) % h), xx = (int)(q % w);
+    size_t o = (size_t)q * cout;
+    conv_pixel(xd, wd, bias, i, yy, xx, h, w, cin, cout, y + o, absacc ? absacc + o : NULL);
+  }
+  free(xd); free(wd);
+  return 0;
+}
+
+/* ---------------------------------------------------------------- a6 ---- */
+
+/* P:352 "reuses cached latents from the last full denoising step for unrefined
+ * regions".  A pixel takes src iff its block is refined. */
+int oracle_scatter(const void* src, int src_layout, const void* cache, void* out, int elem_bytes,
+                   int n, int h, int w, int c, int b,
+                   const uint8_t* mask, const int32_t* k, int u,
+                   const int32_t* ids, int count) {
+  if (!src || !cache || !out || n <= 0 || h <= 0 || w <= 0 || c <= 0 || b <= 0) return BAD;
+  if (elem_bytes != 2 && elem_bytes != 4) return BAD;
+  if (src_layout != 0 && src_layout != 1) return BAD;
+  if (src_layout == 0 && !mask) return BAD;
+  if (src_layout == 1 && (count < 0 || (count > 0 && !ids))) return BAD;
+  int hb = (h + b - 1) / b, wb = (w + b - 1) / b;
+  size_t px_bytes = (size_t)c * elem_bytes;
+  const uint8_t* s = (const uint8_t*)src;
+  const uint8_t* ca = (const uint8_t*)cache;
+  uint8_t* o = (uint8_t*)out;
+  /* start from the cache everywhere ... */
+  memcpy(o, ca, (size_t)n * h * w * px_bytes);
+  if (src_layout == 0) {
+    /* ... and take src on every pixel of an active block */
+    for (int i = 0; i < n; ++i)
+      for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+          int id = (i * hb + y / b) * wb + x / b;
+          int act = mask[id] && (!k || (k[i] >= 0 && k[i] <= u));
+          if (act) {
+            size_t e = (((size_t)i * h + y) * w + x) * px_bytes;
+            memcpy(o + e, s + e, px_bytes);
+          }
+        }
+  } else {
+    for (int j = 0; j < count; ++j) {
+      int id = ids[j];
+      if (id < 0 || id >= n * hb * wb) return BAD;
+      int i = id / (hb * wb), by = (id / wb) % hb, bx = id % wb;
+      for (int py = 0; py < b; ++py)
+        for (int px = 0; px < b; ++px) {
+          int y = by * b + py, x = bx * b + px;
+          if (y >= h || x >= w) continue;
+          size_t e = (((size_t)i * h + y) * w + x) * px_bytes;
+          size_t se = (((size_t)j * b + py) * b + px) * px_bytes;
+          memcpy(o + e, s + se, px_bytes);
+        }
+    }
+  }
+  return 0;
+}

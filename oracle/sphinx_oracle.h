@@ -1,0 +1,113 @@
+/*
+ * sphinx_oracle.h — CPU ORACLE for the Sphinx selective-refinement hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load liboracle.so.
+ * The product path (paper_2511_18672_b200/, libsphinx.so) never links,
+ * imports or executes anything in this directory, and this directory shares
+ * no code, header, table or constant with it.
+ *
+ * Plain, slow, obviously-correct C99, fp64 for every floating-point step,
+ * compiled with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ * Citation keys: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n,
+ * "Alg1 line k" = the k-th statement of Algorithm 1, readings R-n =
+ * DESIGN.md §3.
+ *
+ * Every function returns 0 on success and a negative value on invalid
+ * arguments ("invalid-argument").
+ */
+#ifndef SPHINX_ORACLE_H
+#define SPHINX_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* k-decision logic K_c (Fig. k_logic). */
+typedef struct {
+  int32_t m;            /* number of cut points, 1..16 */
+  double thr[16];       /* strictly ascending ratio cut points, left-closed */
+  int32_t step[16];     /* start steps, non-decreasing */
+  int32_t fallback_k;   /* k when r < thr[0] */
+  int32_t k_max;        /* clamp (40) */
+} oracle_klogic;
+
+/* O1a. Pixel refinement mask M = M_op OR M_blur (Alg1 lines 9-10).
+ * M_op = 1[O < tau_o] ("below 0.5"); M_blur = 1[U > tau_u[n]] (P:348,
+ * "1 indicates blurry").  NaN flags the pixel (reading R-9).  U may be NULL. */
+int oracle_pixel_mask(const float* O, const float* U, const float* tau_u, float tau_o,
+                      int n, int hp, int wp, uint8_t* m);
+
+/* O1b. Non-overlapping f x f max-pool of a binary grid ("downsampled using
+ * max-pooling at each layer").  Requires h % f == 0 and w % f == 0. */
+int oracle_maxpool(const uint8_t* in, int n, int h, int w, int f, uint8_t* out);
+
+/* O1c. SBNet-style block tiling ("marked for refinement if it contains at
+ * least one pixel"): block (by,bx) of b x b cells is 1 iff any cell
+ * of it is 1.  Edge blocks are truncated (reading R-2).  out: [n][ceil(h/b)][ceil(w/b)]. */
+int oracle_tile_blocks(const uint8_t* grid, int n, int h, int w, int b, uint8_t* out);
+
+/* O1. The composite step a1, in the paper's order: pixel mask -> max-pool by
+ * the VAE factor f ("downsampled by a factor of 8") -> max-pool by 2 per
+ * UNet level -> block tiling per level.  masks: concatenation of the
+ * n_levels block masks [n][Hb_l][Wb_l]; counts: [n][n_levels] or NULL. */
+int oracle_block_mask(const float* O, const float* U, const float* tau_u, float tau_o,
+                      int n, int hp, int wp, int f, int b, int n_levels,
+                      uint8_t* masks, int32_t* counts);
+
+/* O2. Start step (Alg1 lines 4-6; Eq. 2 at P:270-281; ratio P:268; k-logic P:288).
+ * All arithmetic in fp64.  k[i] = -1 for invalid per-frame input
+ * (t outside [0,1], Q* <= 0 or NaN; reading R-15).  logic_id may be NULL. */
+int oracle_start_step(const float* q, const float* c0, const float* c1, const float* t,
+                      const int32_t* logic_id, double gamma,
+                      const oracle_klogic* logics, int n_logics, int n, int32_t* k);
+
+/* Eq. 2 alone, for pins. */
+double oracle_eq2(double c0, double c1, double t, double gamma);
+/* k-logic lookup alone. */
+int32_t oracle_select_k(const oracle_klogic* lg, double r);
+
+/* O3. Compaction (P:352 batched blocks; Alg1 lines 17, 19).
+ * select: 0 = ACTIVE (mask && (k==NULL || 0<=k[n]<=u)),
+ *         1 = INACTIVE_FRAMES (k!=NULL && k[n] > u), 2 = ALL (k==NULL || k[n] >= 0).
+ * ids ascending flat (n*hb+by)*wb+bx; *count = list length. */
+int oracle_compact(const uint8_t* mask, int n, int hb, int wb, const int32_t* k, int u,
+                   int select, int32_t* ids, int32_t* count);
+
+/* O4. Forward noise on listed blocks (Alg1 lines 12, 19):
+ * x_t = sqrt(abar[u_n]) x0 + sqrt(1 - abar[u_n]) eps, fp64, abar widened from fp32.
+ * NHWC [n][h][w][c]; out (double) receives xt_in for elements not listed. */
+int oracle_noise(const float* x0, const float* eps, const float* xt_in, double* out,
+                 int n, int h, int w, int c, int b, const int32_t* ids, int count,
+                 const int32_t* step, const float* abar, int total_steps);
+
+/* O5. 3x3 / stride 1 / zero-pad 1 convolution on the exact bf16 values
+ * (inputs are bf16 bit patterns), fp64 accumulation, for every real pixel of
+ * every listed block ("batched convolution over selected blocks").
+ * x: [n][h][w][cin], wt: [cout][3][3][cin], bias: [cout] fp32 or NULL.
+ * y, absacc: double [n][h][w][cout]; only listed pixels are written;
+ * absacc = sum |w*x| (the tolerance scale, north_star). */
+int oracle_conv3x3_blocks(const uint16_t* x, const uint16_t* wt, const float* bias,
+                          int n, int h, int w, int cin, int cout, int b,
+                          const int32_t* ids, int count, double* y, double* absacc,
+                          int n_threads);
+
+/* O5'. The textbook dense convolution over all pixels (same definition). */
+int oracle_conv3x3_dense(const uint16_t* x, const uint16_t* wt, const float* bias,
+                         int n, int h, int w, int cin, int cout,
+                         double* y, double* absacc, int n_threads);
+
+/* O6. Cached scatter ("reuses cached latents ... for unrefined regions"):
+ * out = active(block) ? src : cache, bit copy of elem_bytes per element.
+ * src_layout 0 = FULL NHWC, active from mask/k/u exactly as oracle_compact ACTIVE;
+ * src_layout 1 = COMPACT [count][b][b][c] in ids order, active = listed. */
+int oracle_scatter(const void* src, int src_layout, const void* cache, void* out, int elem_bytes,
+                   int n, int h, int w, int c, int b,
+                   const uint8_t* mask, const int32_t* k, int u,
+                   const int32_t* ids, int count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

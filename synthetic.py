@@ -1,0 +1,183 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU parity tests and bench.py.
+
+This module holds NONE of the method's arithmetic: it only draws random
+tensors with the shapes, value distributions and spatial structure of the
+paper's workloads (DESIGN.md §5 "input recipe").  Both the oracle and the CUDA
+path receive exactly these arrays.
+
+Workload shapes: SEVA 576x576 images -> 72x72 latent (/8),
+21 frames = 2 inputs + 19 targets, UNet levels 72x72x320,
+36x36x640, 18x18x1280 (BASELINE configs[2]).  Opacity follows SPEC's toy
+disocclusion recipe: background U(0.8,1.0), low-opacity ellipses
+U(0,0.4).
+"""
+import hashlib
+import math
+
+import numpy as np
+
+BASE_SEED = 7  # SPEC's example seed
+
+
+def rng(*names):
+    """Independent PCG64 stream per (BASE_SEED, names...)."""
+    h = hashlib.sha256(repr((BASE_SEED,) + tuple(names)).encode()).digest()
+    return np.random.Generator(np.random.PCG64(int.from_bytes(h[:8], "little")))
+
+
+def to_bf16_bits(a):
+    """float32 -> bf16 bit patterns (round to nearest even), as uint16."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    rounded = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    nan = np.isnan(a)
+    out = rounded.astype(np.uint16)
+    out[nan] = 0x7FC0
+    return out
+
+
+def bf16_bits_to_f32(b):
+    return (np.ascontiguousarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+# ------------------------------------------------------------ block choice ---
+
+def choose_cells(rg, hb, wb, n_active, pattern="clustered"):
+    """Pick n_active cells of an hb x wb grid. 'clustered' grows 4-connected blobs from
+    random seeds (disocclusions are contiguous regions); 'scattered' is uniform;
+    'checker' is a checkerboard (halo worst case)."""
+    n_active = int(max(0, min(n_active, hb * wb)))
+    sel = np.zeros((hb, wb), bool)
+    if n_active == 0:
+        return sel
+    if pattern == "scattered":
+        idx = rg.choice(hb * wb, n_active, replace=False)
+        sel.flat[idx] = True
+        return sel
+    if pattern == "checker":
+        cand = [(y, x) for y in range(hb) for x in range(wb) if (y + x) % 2 == 0]
+        cand += [(y, x) for y in range(hb) for x in range(wb) if (y + x) % 2 == 1]
+        for (y, x) in cand[:n_active]:
+            sel[y, x] = True
+        return sel
+    # clustered
+    frontier = []
+    n_blobs = max(1, n_active // 12)
+    while sel.sum() < n_active:
+        if not frontier or len(frontier) == 0 or rg.random() < 1.0 / (4 * n_blobs):
+            free = np.flatnonzero(~sel.ravel())
+            c = free[rg.integers(len(free))]
+            y, x = divmod(int(c), wb)
+        else:
+            y, x = frontier.pop(rg.integers(len(frontier)))
+            if sel[y, x]:
+                continue
+        sel[y, x] = True
+        for dy, dx in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+            yy, xx = y + dy, x + dx
+            if 0 <= yy < hb and 0 <= xx < wb and not sel[yy, xx]:
+                frontier.append((yy, xx))
+    return sel
+
+
+def opacity_maps(n, hp, wp, cell_px, densities, pattern="clustered", tag="opacity"):
+    """Opacity O [n,hp,wp] fp32.  For frame i, round(densities[i]*cells) cells of
+    cell_px x cell_px pixels (cell_px = b*f, one level-0 block footprint) receive one
+    low-opacity ellipse U(0,0.4) strictly inside them; everything else U(0.8,1.0)."""
+    rg = rng(tag, n, hp, wp, cell_px, pattern)
+    O = rg.uniform(0.8, 1.0, size=(n, hp, wp)).astype(np.float32)
+    hb, wb = -(-hp // cell_px), -(-wp // cell_px)
+    cells = []
+    for i in range(n):
+        d = float(densities[i] if np.ndim(densities) else densities)
+        sel = choose_cells(rg, hb, wb, round(d * hb * wb), pattern)
+        cells.append(sel)
+        for (cy, cx) in zip(*np.nonzero(sel)):
+            y0, x0 = cy * cell_px, cx * cell_px
+            hh, ww = min(cell_px, hp - y0), min(cell_px, wp - x0)
+            ry = max(0.5, rg.uniform(0.15, 0.5) * hh)
+            rx = max(0.5, rg.uniform(0.15, 0.5) * ww)
+            my = rg.uniform(ry, max(ry, hh - ry)) if hh > 1 else 0.0
+            mx = rg.uniform(rx, max(rx, ww - rx)) if ww > 1 else 0.0
+            yy, xx = np.mgrid[0:hh, 0:ww]
+            inside = ((yy + 0.5 - my) / ry) ** 2 + ((xx + 0.5 - mx) / rx) ** 2 <= 1.0
+            if not inside.any():
+                inside[min(int(my), hh - 1), min(int(mx), ww - 1)] = True
+            patch = O[i, y0:y0 + hh, x0:x0 + ww]
+            patch[inside] = rg.uniform(0.0, 0.4, size=int(inside.sum())).astype(np.float32)
+    return O, np.stack(cells)
+
+
+def uncertainty_maps(n, hp, wp, cell_px, cells, frac_blobs=0.3, tag="uncert"):
+    """Uncertainty U [n,hp,wp] in U(0,0.6) with a 0.9 blob inside a fraction of the
+    already-chosen cells, plus per-frame threshold tau_u = 0.7 (reading R-10: the
+    Otsu producer is NEXT-2, so tau_u is an input)."""
+    rg = rng(tag, n, hp, wp, cell_px)
+    U = rg.uniform(0.0, 0.6, size=(n, hp, wp)).astype(np.float32)
+    for i in range(n):
+        for (cy, cx) in zip(*np.nonzero(cells[i])):
+            if rg.random() < frac_blobs:
+                y = cy * cell_px + rg.integers(min(cell_px, hp - cy * cell_px))
+                x = cx * cell_px + rg.integers(min(cell_px, wp - cx * cell_px))
+                U[i, y, x] = 0.9
+    tau_u = np.full(n, 0.7, np.float32)
+    return U, tau_u
+
+
+# ------------------------------------------------------------ tensors -------
+
+def features_bf16(shape, tag):
+    """x ~ N(0,1) rounded to bf16 (bit patterns)."""
+    return to_bf16_bits(rng("feat", tag, shape).standard_normal(shape, dtype=np.float32))
+
+
+def weights_bf16(cout, cin, tag):
+    """W ~ N(0, 1/(9 cin)) in OHWI [cout][3][3][cin] (reading R-19), bf16 bits."""
+    w = rng("w", tag, cout, cin).standard_normal((cout, 3, 3, cin), dtype=np.float32)
+    return to_bf16_bits(w * np.float32(1.0 / math.sqrt(9 * cin)))
+
+
+def bias_f32(cout, tag):
+    return (rng("bias", tag, cout).standard_normal(cout, dtype=np.float32) * np.float32(0.01))
+
+
+def latents_f32(shape, tag):
+    return rng("lat", tag, shape).standard_normal(shape, dtype=np.float32)
+
+
+def abar_cosine(S=50):
+    """S:43 cosine table abar[u] = cos^2((pi/2)(1-u/S)*0.98), u=0 noisiest.
+    abar[S] = cos^2(0) = 1, so SPEC's renormalisation is a no-op (reading R-5)."""
+    u = np.arange(S + 1, dtype=np.float64)
+    a = np.cos((math.pi / 2) * (1.0 - u / S) * 0.98) ** 2
+    return a.astype(np.float32)
+
+
+def abar_linear(S=50):
+    """S:43 linear table abar[0] = 0.01 -> abar[S] = 1."""
+    return np.linspace(0.01, 1.0, S + 1).astype(np.float32)
+
+
+def request_scores(n_frames=21, c0=62.0, c1=66.0, tag="req"):
+    """Per-frame (q, c0, c1, t) for one request: frames 0 and n-1 are the input views
+    (2 inputs), targets t_i = i/(n-1).  q follows a U-shaped quality dip
+    toward the middle (Fig. avg_k): q_i = mean(c0,c1)(1 - 0.2 sin(pi t)) + noise."""
+    rg = rng("scores", tag, n_frames)
+    t = np.arange(n_frames, dtype=np.float64) / (n_frames - 1)
+    base = 0.5 * (c0 + c1)
+    q = base * (1.0 - 0.2 * np.sin(math.pi * t)) + 0.6 * rg.standard_normal(n_frames)
+    return (q.astype(np.float32), np.full(n_frames, c0, np.float32),
+            np.full(n_frames, c1, np.float32), t.astype(np.float32))
+
+
+def request_densities(n_frames=21, mean=0.25, lo=0.05, hi=0.60):
+    """Per-frame level-0 block density, proportional to sin(pi t), clipped, rescaled to
+    the requested mean (frames far from the inputs have more disocclusion)."""
+    t = np.arange(n_frames) / (n_frames - 1)
+    d = np.sin(math.pi * t) + 0.05
+    for _ in range(50):
+        d = np.clip(d * (mean / max(d.mean(), 1e-9)), lo, hi)
+    return d
+
+
+SPEC_KLOGIC = dict(thr=[0.85, 0.92, 0.97], steps=[10, 25, 40], fallback_k=0, k_max=40)

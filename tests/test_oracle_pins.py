@@ -1,0 +1,351 @@
+"""Pins the CPU oracle to what the paper, SPEC and mathematics fix (no GPU).
+
+Each test names the passage or property it checks.  None of them re-types the
+oracle's formula: they use worked values (tests/golden/worked_examples.json),
+closed forms, brute force on tiny inputs, library routines (torch fp64
+conv2d), exact invariants, or Monte-Carlo statistics.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synthetic as syn
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+
+
+# ------------------------------------------------------------------ a1 masks
+
+@pytest.mark.parametrize("case", GOLD["block_mask"], ids=lambda c: c["name"])
+def test_block_mask_worked_examples(case):
+    O = np.ones((case["n"], case["hp"], case["wp"]), np.float32)
+    for (y, x, v) in case["pixels"]:
+        O[0, y, x] = np.nan if v == "nan" else v
+    masks, counts = oracle.block_mask(O, None, None, 0.5, case["f"], case["b"], case["levels"])
+    for l, want in enumerate(case["ids"]):
+        assert np.flatnonzero(masks[l]).tolist() == want, (case["cite"], l)
+        assert counts[0, l] == len(want)
+
+
+def test_opacity_mask_spec_row():
+    g = GOLD["opacity_mask_spec"]
+    O = np.array([[g["row"]]], np.float32)
+    assert oracle.pixel_mask(O, None, None, g["tau_o"])[0, 0].tolist() == g["mask"]
+
+
+def test_opacity_mask_trivial_and_union():
+    ones = np.ones((2, 4, 4), np.float32)
+    assert oracle.pixel_mask(ones, None, None, 0.5).sum() == 0
+    assert oracle.pixel_mask(0 * ones, None, None, 0.5).all()
+    # M = M_op OR M_blur (Alg1 line 10): blur full, opacity empty -> full
+    U = np.ones((2, 4, 4), np.float32)
+    tau = np.full(2, 0.5, np.float32)
+    assert oracle.pixel_mask(ones, U, tau, 0.5).all()
+    # strict '>' for the blur map (reading R-8): U == tau is not blurry
+    assert oracle.pixel_mask(ones, 0.5 * U, tau, 0.5).sum() == 0
+    # disjoint single pixels -> exactly two set pixels
+    O = ones.copy(); O[0, 1, 1] = 0.0
+    U2 = np.zeros_like(ones); U2[0, 2, 3] = 1.0
+    assert oracle.pixel_mask(O, U2, tau, 0.5).sum() == 2
+    with pytest.raises(ValueError):
+        oracle.pixel_mask(ones, None, None, 1.5)
+
+
+def test_maxpool_spec_examples():
+    m = np.zeros((1, 8, 8), np.uint8); m[0, 3, 5] = 1
+    assert oracle.maxpool(m, 8).tolist() == [[[1]]]
+    assert oracle.maxpool(np.zeros((1, 16, 16), np.uint8), 4).sum() == 0
+    rg = syn.rng("pin-maxpool")
+    for _ in range(200):
+        g = (rg.random((1, 16, 16)) < 0.05).astype(np.uint8)
+        assert np.array_equal(oracle.maxpool(oracle.maxpool(g, 2), 2), oracle.maxpool(g, 4))
+    with pytest.raises(ValueError):
+        oracle.maxpool(np.zeros((1, 6, 6), np.uint8), 4)
+
+
+def test_tile_blocks_spec_and_brute_force():
+    assert oracle.tile_blocks(np.ones((1, 8, 8), np.uint8), 4).sum() == 4
+    g = np.zeros((1, 9, 9), np.uint8); g[0, 8, 2] = 1
+    t = oracle.tile_blocks(g, 4)
+    assert t.shape == (1, 3, 3) and t.sum() == 1 and t[0, 2, 0] == 1        # S:257, edge block
+    rg = syn.rng("pin-tile")
+    for _ in range(50):
+        h, w, b = rg.integers(1, 30), rg.integers(1, 30), int(rg.integers(1, 9))
+        g = (rg.random((2, h, w)) < 0.03).astype(np.uint8)
+        want = np.zeros((2, -(-h // b), -(-w // b)), np.uint8)
+        for i in range(2):
+            for by in range(want.shape[1]):
+                for bx in range(want.shape[2]):
+                    want[i, by, bx] = g[i, by * b:(by + 1) * b, bx * b:(bx + 1) * b].any()
+        assert np.array_equal(oracle.tile_blocks(g, b), want)
+
+
+def test_block_mask_exhaustive_config1_patterns():
+    """All 2^16 block patterns of config-1 geometry (16x16, f=1, b=4): paint one
+    flagged pixel at a random spot of every chosen block; the oracle must return
+    exactly the pattern (coverage + no false positives)."""
+    n = 1 << 16
+    pat = ((np.arange(n)[:, None] >> np.arange(16)[None, :]) & 1).astype(bool)  # [n,16]
+    rg = syn.rng("pin-exhaustive")
+    O = rg.uniform(0.5, 1.0, size=(n, 16, 16)).astype(np.float32)  # 0.5 itself is not flagged
+    oy = rg.integers(0, 4, size=(n, 16)); ox = rg.integers(0, 4, size=(n, 16))
+    fi, bi = np.nonzero(pat)
+    by, bx = bi // 4, bi % 4
+    O[fi, by * 4 + oy[fi, bi], bx * 4 + ox[fi, bi]] = rg.uniform(0, 0.4999, size=len(fi))
+    masks, counts = oracle.block_mask(O, None, None, 0.5, 1, 4, 1)
+    assert np.array_equal(masks[0].reshape(n, 16).astype(bool), pat)
+    assert np.array_equal(counts[:, 0], pat.sum(1))
+
+
+def test_block_mask_pyramid_nesting_and_counts():
+    """Coarser levels never drop a refined region (S:232 'every coarser level >=
+    max-pool of the finer'): with b=8 and /2 per level, a level-l block covers the
+    2x2 level-(l-1) blocks below it (edge blocks truncated), so it is their OR."""
+    n = 3
+    O, cells = syn.opacity_maps(n, 576, 576, 64, [0.05, 0.25, 0.6], "scattered", tag="pin-pyr")
+    U, tau = syn.uncertainty_maps(n, 576, 576, 64, cells, tag="pin-pyr")
+    masks, counts = oracle.block_mask(O, U, tau, 0.5, 8, 8, 3)
+    assert [m.shape for m in masks] == [(n, 9, 9), (n, 5, 5), (n, 3, 3)]
+    # level 0 equals the cells the generator painted (each painted cell has >= 1 flagged px,
+    # unpainted cells have opacity >= 0.8 and uncertainty blobs only inside painted cells)
+    assert np.array_equal(masks[0].astype(bool), cells)
+    for l in (1, 2):
+        fine, coarse = masks[l - 1], masks[l]
+        for i in range(n):
+            for by in range(coarse.shape[1]):
+                for bx in range(coarse.shape[2]):
+                    assert coarse[i, by, bx] == fine[i, 2 * by:2 * by + 2, 2 * bx:2 * bx + 2].any()
+    for l in range(3):
+        assert np.array_equal(counts[:, l], masks[l].reshape(n, -1).sum(1))
+
+
+# --------------------------------------------------------------- a2 start step
+
+@pytest.mark.parametrize("case", GOLD["eq2"], ids=lambda c: c["cite"][:12])
+def test_eq2_worked(case):
+    got = oracle.eq2(case["c0"], case["c1"], case["t"], case["gamma"])
+    assert abs(got - case["expect"]) <= case["tol"], case["cite"]
+
+
+def test_eq2_gamma1_is_linear_and_endpoints():
+    for t in np.linspace(0, 1, 100):
+        for (c0, c1) in ((60.0, 70.0), (70.0, 60.0), (55.5, 55.5)):
+            assert abs(oracle.eq2(c0, c1, t, 1.0) - (c0 + (c1 - c0) * t)) <= 1e-12
+    for g in (0.1, 0.5, 0.9, 1.0):                                         # f(0)=0, f(1)=1
+        for (c0, c1) in ((60.0, 70.0), (70.0, 60.0)):
+            assert oracle.eq2(c0, c1, 0.0, g) == c0
+            assert oracle.eq2(c0, c1, 1.0, g) == c1
+
+
+def test_select_k_spec_and_monotone():
+    g = GOLD["select_k"]
+    lg = oracle.make_klogic(g["logic"]["thr"], g["logic"]["steps"], g["logic"]["fallback_k"],
+                            g["logic"]["k_max"])
+    for c in g["cases"]:
+        assert oracle.select_k(lg, c["r"]) == c["k"], c["cite"]
+    ks = [oracle.select_k(lg, r) for r in np.linspace(0, 2, 2001)]       # S:157 monotone
+    assert all(a <= b for a, b in zip(ks, ks[1:]))
+    big = oracle.make_klogic([0.5, 0.9], [30, 48], 0, 40)                  # S:160 never above k_max
+    assert max(oracle.select_k(big, r) for r in np.linspace(0, 2, 101)) == 40
+
+
+def test_start_step_fp32_tie_cases():
+    lg = oracle.make_klogic(**{k: v for k, v in syn.SPEC_KLOGIC.items() if k in ("thr",)},
+                            steps=syn.SPEC_KLOGIC["steps"])
+    for c in GOLD["start_step_fp32"]:
+        q = np.float32(0.97 * 65) if c["q"] == "fp32(0.97*65)" else np.float32(c["q"])
+        k = oracle.start_step([q], [c["c0"]], [c["c1"]], [c["t"]], c["gamma"], [lg])
+        assert k[0] == c["k"], c["cite"]
+
+
+def test_start_step_invalid_and_logic_id():
+    lg0 = oracle.make_klogic([0.85, 0.92, 0.97], [10, 25, 40])
+    lg1 = oracle.make_klogic([0.5], [5], 1, 40)
+    k = oracle.start_step([60, 60, 60, 60], [60, 0, 60, 60], [70, 0, 70, 70],
+                          [1.5, 0.5, 0.5, 0.5], 0.5, [lg0, lg1], logic_id=[0, 0, 1, 2])
+    # t outside [0,1] -> -1; Q* = 0 -> -1; logic 1 -> 5; bad logic id -> -1
+    assert k.tolist() == [-1, -1, 5, -1]
+
+
+# ---------------------------------------------------------------- a3 compaction
+
+def test_compact_brute_force_and_selections():
+    rg = syn.rng("pin-compact")
+    for trial in range(30):
+        n, hb, wb = int(rg.integers(1, 6)), int(rg.integers(1, 10)), int(rg.integers(1, 10))
+        m = (rg.random((n, hb, wb)) < rg.random()).astype(np.uint8)
+        k = rg.integers(-1, 45, size=n).astype(np.int32)
+        u = int(rg.integers(0, 50))
+        ids = oracle.compact(m, k, u)
+        elig = (k >= 0) & (k <= u)                                          # Alg1 line 17
+        want = np.flatnonzero((m.astype(bool) & elig[:, None, None]).ravel())
+        assert np.array_equal(ids, want)
+        assert len(ids) == int((m * elig[:, None, None]).sum())
+        inact = oracle.compact(m, k, u, oracle.SELECT_INACTIVE_FRAMES)      # Alg1 line 19
+        assert np.array_equal(inact, np.flatnonzero(np.repeat(k > u, hb * wb)))
+        allb = oracle.compact(None, k, u, oracle.SELECT_ALL, shape=(n, hb, wb))
+        assert np.array_equal(allb, np.flatnonzero(np.repeat(k >= 0, hb * wb)))
+    m = np.ones((3, 5, 5), np.uint8)
+    assert np.array_equal(oracle.compact(m), np.arange(75))                 # density 1 -> identity
+    assert len(oracle.compact(0 * m)) == 0                                  # density 0 -> empty
+
+
+# --------------------------------------------------------------------- a4 noise
+
+@pytest.mark.parametrize("case", GOLD["noise"], ids=lambda c: c["name"])
+def test_noise_worked(case):
+    abar = syn.abar_linear(case["S"]) if case["schedule"] == "linear" else syn.abar_cosine(case["S"])
+    x0 = np.full((1, 4, 4, 2), case["x0"], np.float32)
+    eps = np.full_like(x0, case["eps"])
+    out = oracle.noise(x0, eps, np.zeros_like(x0), 4, [0], [case["u"]], abar)
+    assert np.all(np.abs(out - case["expect"]) <= case["tol"]), case["cite"]
+
+
+def test_noise_clean_endpoint_and_untouched():
+    abar = syn.abar_cosine(50)
+    x0 = syn.latents_f32((2, 9, 9, 4), "pin-n-x0")
+    eps = syn.latents_f32((2, 9, 9, 4), "pin-n-eps")
+    xt = syn.latents_f32((2, 9, 9, 4), "pin-n-xt")
+    out = oracle.noise(x0, eps, xt, 4, [0, 1, 2, 3, 4, 5, 6, 7, 8, 9], [50, 10], abar)
+    assert np.array_equal(out[0].astype(np.float32), x0[0])                 # S:306, frame 0 all listed
+    # frame 1: only block ids 9 (=frame1 block (0,0)) listed -> rest untouched, bitwise
+    touched = np.zeros((9, 9), bool); touched[0:4, 0:4] = True
+    assert np.array_equal(out[1][~touched].astype(np.float32), xt[1][~touched])
+    assert not np.array_equal(out[1][touched].astype(np.float32), xt[1][touched])
+
+
+def test_noise_monte_carlo_marginals():
+    """S:308 / S:577: over 10 000 draws, mean within 3 sigma of sqrt(abar)z0 and
+    variance within 5% of 1-abar, at u in {0,10,25,40}."""
+    abar = syn.abar_cosine(50)
+    z0 = np.float32(0.7)
+    draws = 10000
+    x0 = np.full((1, 1, draws, 1), z0, np.float32)
+    eps = syn.rng("pin-mc").standard_normal((1, 1, draws, 1)).astype(np.float32)
+    for u in (0, 10, 25, 40):
+        out = oracle.noise(x0, eps, np.zeros_like(x0), draws, [0], [u], abar).ravel()
+        a = float(abar[u])
+        sigma = math.sqrt((1 - a) / draws)
+        assert abs(out.mean() - math.sqrt(a) * z0) <= 3 * sigma
+        assert abs(out.var() / (1 - a) - 1) <= 0.05
+
+
+# ---------------------------------------------------------------------- a5 conv
+
+def _shift_weights(c, ky, kx):
+    w = np.zeros((c, 3, 3, c), np.float32)
+    for i in range(c):
+        w[i, ky, kx, i] = 1.0
+    return syn.to_bf16_bits(w)
+
+
+@pytest.mark.parametrize("ky,kx", [(a, c) for a in range(3) for c in range(3)])
+def test_conv_shift_kernels_exact(ky, kx):
+    """W = delta(co=ci) delta(tap) gives y(p) = x(p + (ky-1, kx-1)) exactly, zero
+    outside the image (TV-12/13), across block boundaries and ragged edges."""
+    n, h, w, c, b = 2, 10, 11, 8, 4
+    x = syn.features_bf16((n, h, w, c), "pin-shift")
+    xf = syn.bf16_bits_to_f32(x).astype(np.float64)
+    want = np.zeros((n, h, w, c))
+    dy, dx = ky - 1, kx - 1
+    for yy in range(h):
+        for xx in range(w):
+            if 0 <= yy + dy < h and 0 <= xx + dx < w:
+                want[:, yy, xx] = xf[:, yy + dy, xx + dx]
+    y, a = oracle.conv3x3_dense(x, _shift_weights(c, ky, kx), None)
+    assert np.array_equal(y, want)
+    hb, wb = -(-h // b), -(-w // b)
+    ids = np.arange(0, n * hb * wb, 2)
+    ys, _ = oracle.conv3x3_blocks(x, _shift_weights(c, ky, kx), None, b, ids)
+    listed = np.zeros((n, h, w), bool)
+    for id_ in ids:
+        i, r = divmod(int(id_), hb * wb)
+        by, bx = divmod(r, wb)
+        listed[i, by * b:(by + 1) * b, bx * b:(bx + 1) * b] = True
+    assert np.array_equal(ys[listed], want[listed])
+    assert np.isnan(ys[~listed]).all()
+
+
+def test_conv_dense_matches_torch_fp64():
+    """Library sanity check: torch.nn.functional.conv2d in fp64 on CPU."""
+    torch = pytest.importorskip("torch")
+    n, h, w, cin, cout = 2, 9, 7, 24, 16
+    x = syn.features_bf16((n, h, w, cin), "pin-torch")
+    wt = syn.weights_bf16(cout, cin, "pin-torch")
+    bias = syn.bias_f32(cout, "pin-torch")
+    y, a = oracle.conv3x3_dense(x, wt, bias)
+    xt = torch.from_numpy(syn.bf16_bits_to_f32(x).astype(np.float64)).permute(0, 3, 1, 2)
+    wtt = torch.from_numpy(syn.bf16_bits_to_f32(wt).astype(np.float64)).permute(0, 3, 1, 2)
+    ref = torch.nn.functional.conv2d(xt, wtt, torch.from_numpy(bias.astype(np.float64)), padding=1)
+    ref = ref.permute(0, 2, 3, 1).numpy()
+    assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(a)
+    assert np.all(a >= np.abs(y - bias) - 1e-12)
+
+
+def test_conv_zero_input_bias_and_abs_sum():
+    n, h, w, c = 1, 5, 6, 8
+    zero = np.zeros((n, h, w, c), np.uint16)
+    bias = syn.bias_f32(c, "pin-zero")
+    y, _ = oracle.conv3x3_dense(zero, syn.weights_bf16(c, c, "pin-zero"), bias)
+    assert np.array_equal(y, np.broadcast_to(bias.astype(np.float64), y.shape))
+    # non-negative operands: sum |w x| == sum w x exactly (same order, no cancellation)
+    xp = syn.to_bf16_bits(np.abs(syn.bf16_bits_to_f32(syn.features_bf16((n, h, w, c), "pz"))))
+    wp = syn.to_bf16_bits(np.abs(syn.bf16_bits_to_f32(syn.weights_bf16(c, c, "pz"))))
+    y, a = oracle.conv3x3_dense(xp, wp, None)
+    assert np.array_equal(y, a)
+
+
+def test_conv_blocks_equal_dense_on_listed_pixels():
+    """P:352 / S:326: block-sparse output equals the dense conv on active blocks."""
+    n, h, w, c, b = 2, 18, 18, 16, 8
+    x = syn.features_bf16((n, h, w, c), "pin-bd")
+    wt = syn.weights_bf16(c, c, "pin-bd")
+    bias = syn.bias_f32(c, "pin-bd")
+    yd, ad = oracle.conv3x3_dense(x, wt, bias)
+    ids = np.array([0, 4, 8, 9, 13, 17])  # includes truncated edge blocks (3x3 grid)
+    ys, as_ = oracle.conv3x3_blocks(x, wt, bias, b, ids)
+    got = ~np.isnan(ys[..., 0])
+    assert got.sum() == sum(min(b, h - (r // 3) * b) * min(b, w - (r % 3) * b)
+                            for r in (i % 9 for i in ids))
+    assert np.array_equal(ys[got], yd[got]) and np.array_equal(as_[got], ad[got])
+
+
+# ------------------------------------------------------------------- a6 scatter
+
+def test_scatter_density_0_1_and_composition():
+    n, h, w, c, b = 2, 18, 18, 8, 8
+    src = syn.features_bf16((n, h, w, c), "pin-sc-src")
+    cache = syn.features_bf16((n, h, w, c), "pin-sc-cache")
+    m0 = np.zeros((n, 3, 3), np.uint8)
+    assert np.array_equal(oracle.scatter(src, cache, b, mask=m0), cache)        # density 0
+    m1 = np.ones((n, 3, 3), np.uint8)
+    assert np.array_equal(oracle.scatter(src, cache, b, mask=m1), src)          # density 1
+    k = np.array([5, 30], np.int32)
+    out = oracle.scatter(src, cache, b, mask=m1, k=k, u=10)                     # frame 1 inactive
+    assert np.array_equal(out[0], src[0]) and np.array_equal(out[1], cache[1])
+    # O7: scatter(conv_sparse(x), cache) == where(active, dense(x), cache)
+    rg = syn.rng("pin-o7")
+    m = (rg.random((n, 3, 3)) < 0.5).astype(np.uint8)
+    ids = oracle.compact(m)
+    x = syn.features_bf16((n, h, w, c), "pin-o7x")
+    wt = syn.weights_bf16(c, c, "pin-o7")
+    cache32 = syn.latents_f32((n, h, w, c), "pin-o7c")
+    ys, _ = oracle.conv3x3_blocks(x, wt, None, b, ids, y_init=cache32.astype(np.float64))
+    yd, _ = oracle.conv3x3_dense(x, wt, None)
+    act = np.kron(m, np.ones((1, b, b), np.uint8))[:, :h, :w].astype(bool)
+    want = np.where(act[..., None], yd.astype(np.float32), cache32)
+    got = oracle.scatter(ys.astype(np.float32), cache32, b, mask=m)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    # COMPACT source layout gives the same result
+    comp = np.zeros((len(ids), b, b, c), np.float32)
+    for j, id_ in enumerate(ids):
+        i, r = divmod(int(id_), 9)
+        by, bx = divmod(r, 3)
+        blk = ys[i, by * b:(by + 1) * b, bx * b:(bx + 1) * b].astype(np.float32)
+        comp[j, :blk.shape[0], :blk.shape[1]] = blk
+    got2 = oracle.scatter(comp, cache32, b, ids=ids, src_layout=oracle.SRC_COMPACT)
+    assert np.array_equal(got2.view(np.uint32), want.view(np.uint32))
