@@ -1,0 +1,226 @@
+/*
+ * sphinx.h — C ABI of the B200-native (sm_100a) Sphinx selective-refinement hot path.
+ *
+ * Paper: "Sphinx: Efficiently Serving Novel View Synthesis using Regression-Guided
+ * Selective Refinement" (arXiv 2511.18672).  Citation keys: P:n = PAPER.md line n,
+ * S:n = SPEC.md line n, "Alg1 line k" = k-th statement of Algorithm 1,
+ * R-n = reading n in DESIGN.md §3.
+ *
+ * The five entry points are the five steps of the hot path (BASELINE north_star):
+ *   (1) sphinx_block_mask      per-pixel maps -> per-level block masks + per-frame start step
+ *   (2) sphinx_compact_blocks  block mask (+ frame eligibility) -> ascending block-id list
+ *   (3) sphinx_noise_inject    x_t = sqrt(abar) x0 + sqrt(1-abar) eps on listed blocks
+ *   (4) sphinx_sparse_conv3x3  halo gather + 3x3 implicit GEMM (tcgen05/TMEM) on listed blocks
+ *   (5) sphinx_scatter_cached  out = active ? computed : latent cache
+ *
+ * CONVENTIONS (all entry points)
+ *  - Ownership: every array pointer is caller-owned memory.  "device" pointers must be
+ *    CUDA device (or managed) memory of the current device; "host" pointers are read
+ *    synchronously before return.  The library never allocates, frees or retains
+ *    caller pointers after it returns.
+ *  - Asynchrony: arguments visible on the host are validated synchronously; the work is
+ *    then enqueued on `stream` (NULL = legacy default stream) with no implicit
+ *    synchronisation.  No call reads device memory on the host (device counts stay on
+ *    the device), so every call is CUDA-graph capturable.
+ *  - Errors: a non-zero sphinx_status is returned before anything is enqueued, except
+ *    SPHINX_ERR_CUDA which may follow a failed launch.  Per-frame data errors that live
+ *    in device memory cannot be reported synchronously; they are encoded in outputs as
+ *    documented per call (start_step = -1).
+ *  - Layouts: feature maps and latents are NHWC, C innermost (channels-last), densely
+ *    packed.  Block (n, by, bx) of a level with Hb x Wb blocks has flat id
+ *    (n*Hb + by)*Wb + bx (S:192 frame-major, row-major; R-20).  Edge blocks are
+ *    truncated at the image border (R-2).
+ *  - Determinism: outputs are bit-reproducible run to run: no floating-point
+ *    atomics, list order defined by the flat id.
+ *  - Thread safety: no global mutable state besides the thread-local last CUDA error.
+ */
+#ifndef SPHINX_H
+#define SPHINX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SPHINX_API __attribute__((visibility("default")))
+#else
+#define SPHINX_API
+#endif
+
+typedef struct CUstream_st* sphinx_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  SPHINX_OK = 0,
+  SPHINX_ERR_INVALID_ARGUMENT = 1, /* null pointer, non-positive size, inconsistent dims,
+                                      tau_o outside [0,1], gamma outside (0,1], bad k-logic,
+                                      S < 2 ... */
+  SPHINX_ERR_UNSUPPORTED = 2,      /* valid but not implemented on sm_100a (e.g. C % 8 != 0,
+                                      block > 16); there is no fallback */
+  SPHINX_ERR_CUDA = 3,             /* launch / driver failure: see sphinx_last_cuda_error() */
+  SPHINX_ERR_DEVICE = 4            /* current device is not sm_100 */
+} sphinx_status;
+
+typedef enum { SPHINX_BF16 = 0, SPHINX_F32 = 1 } sphinx_dtype;
+
+/* Which blocks compaction selects (Alg1 lines 17-19). */
+typedef enum {
+  SPHINX_SELECT_ACTIVE = 0,          /* mask == 1 and 0 <= k[n] <= u: A_u = 1[k <= u] (Alg1 line 17) */
+  SPHINX_SELECT_INACTIVE_FRAMES = 1, /* every block of frames with k[n] > u: resampled (Alg1 line 19) */
+  SPHINX_SELECT_ALL = 2              /* every block of frames with k[n] >= 0 (or all if k == NULL) */
+} sphinx_select;
+
+typedef enum { SPHINX_SRC_FULL = 0, SPHINX_SRC_COMPACT = 1 } sphinx_src_layout;
+
+/* k-decision logic K_c (Fig. k_logic).
+ * k = step[i] for the largest i with thr[i] <= r (left-closed); fallback_k when
+ * r < thr[0]; then min(k, k_max) ("We set the largest k=40"). */
+typedef struct {
+  int32_t m;         /* number of cut points, 1..16 */
+  double thr[16];    /* strictly ascending ratio cut points */
+  int32_t step[16];  /* non-decreasing start steps */
+  int32_t fallback_k;
+  int32_t k_max;
+} sphinx_klogic;
+
+#define SPHINX_MAX_LOGICS 8
+
+/* Per-frame inputs of the start-step map (Alg1 lines 3-6; Eq. 2). */
+typedef struct {
+  const float* q_reg;        /* [N] device: no-reference score Q_reg of the regression frame */
+  const float* c0;           /* [N] device: score of input view I0 of the frame's request */
+  const float* c1;           /* [N] device: score of input view I1 */
+  const float* t;            /* [N] device: normalised target position t in [0,1] (Eq. 2; R-12) */
+  const int32_t* logic_id;   /* [N] device: cluster index c selecting the k-logic, or NULL = 0;
+                                a negative id marks a conditioning (input) frame: k = -1 (R-14) */
+  float gamma;               /* Eq. 2 exponent, in (0,1] */
+  const sphinx_klogic* logics; /* host array of n_logics tables, copied by value into the launch */
+  int32_t n_logics;          /* 1..SPHINX_MAX_LOGICS */
+} sphinx_start_args;
+
+SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
+SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
+#define SPHINX_ABI_VERSION 1
+
+/* ---------------------------------------------------------------------------------
+ * (1) Block mask + start step.
+ * P:346 opacity mask M_op = 1[O < tau_o] ("opacity values below 0.5");
+ * P:348 blur mask (1 = blurry) from the uncertainty map U and per-frame Otsu
+ * threshold tau_u[n] (R-10: tau_u is an input); P:350 M = M_op OR M_blur;
+ * P:489 M is max-pooled by the VAE factor f and by 2 at every UNet level;
+ * P:352 block (n,by,bx) of level l is active iff it contains >= 1 masked cell.
+ * Equivalently: active iff some pixel (i,j) with by*b*f*2^l <= i < (by+1)*b*f*2^l
+ * (clipped to Hp), same for j, has !(O >= tau_o) || (U && !(U <= tau_u[n]))
+ * (NaN refines, R-9; strict inequalities, R-8).
+ *
+ * opacity       [N][Hp][Wp] fp32 device.
+ * uncertainty   [N][Hp][Wp] fp32 device, or NULL (then tau_u is ignored).
+ * tau_u         [N] fp32 device.
+ * tau_o         opacity threshold in [0,1] (0.5).
+ * px_per_cell   f: image pixels per level-0 latent cell (8 = VAE factor; 1 allowed).
+ * block         b in cells, same at every level, 1..64.
+ * n_levels      1..4; level l has H_l = (Hp/f) >> l; requires Hp % f == 0 and
+ *               (Hp/f) % 2^(n_levels-1) == 0 (and the same for W).
+ * block_mask    HOST array of n_levels DEVICE pointers; level l is u8 [N][ceil(H_l/b)][ceil(W_l/b)]
+ *               and receives 0/1.
+ * active_count  [N][n_levels] int32 device, or NULL.
+ * ss            host struct or NULL (skip the start-step map).
+ * start_step    [N] int32 device out (required if ss != NULL): k_n = K_c(q/Q*) per Alg1 lines 4-6
+ *               in fp64; -1 if t outside [0,1], Q* <= 0 / NaN, or logic_id out of range (R-15).
+ *               gamma == 1 and gamma == 0.5 use t and sqrt(t) (exact); other gamma use pow (R-16).
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_block_mask(const float* opacity, const float* uncertainty, const float* tau_u,
+                                float tau_o, int32_t n, int32_t hp, int32_t wp,
+                                int32_t px_per_cell, int32_t block, int32_t n_levels,
+                                uint8_t* const* block_mask, int32_t* active_count,
+                                const sphinx_start_args* ss, int32_t* start_step,
+                                sphinx_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
+ * (2) Compaction ("batched convolution over selected blocks").
+ * Emits, in ascending flat-id order, the ids of the blocks selected by `select`
+ * (see sphinx_select; k[n] < 0 excludes frame n from every selection, R-14), and
+ * writes their number to *count.  The count stays on the device.
+ *
+ * block_mask   u8 [N][hb][wb] device (may be NULL only for SELECT_INACTIVE_FRAMES / SELECT_ALL).
+ * start_step   int32 [N] device or NULL (all frames eligible; required for INACTIVE_FRAMES).
+ * step_u       the denoising step u of Alg1's loop.
+ * block_ids    int32 [N*hb*wb] device out (capacity = N*hb*wb).
+ * count        int32 device scalar out.
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_compact_blocks(const uint8_t* block_mask, int32_t n, int32_t hb, int32_t wb,
+                                    const int32_t* start_step, int32_t step_u, sphinx_select select,
+                                    int32_t* block_ids, int32_t* count, sphinx_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
+ * (3) Forward noise on listed blocks (Alg1 line 12 add_noise(Z0, k_min); line 19
+ * resampling of inactive frames to u+1; formula S:303 / north_star):
+ *   x_t = sqrt(abar[u_n]) * x0 + sqrt(1 - abar[u_n]) * eps     (fp32)
+ * for every element of every real pixel of every listed block; every other element of
+ * x_t is left untouched.  u = 0 is the noisiest step, u = S clean (R-5).
+ *
+ * x0, eps, x_t  NHWC fp32 [N][h][w][c] device; x_t may alias x0 (in place).
+ * block_ids/count/capacity  a list produced by sphinx_compact_blocks for this geometry.
+ * step          int32 [N] device: u_n per frame; a frame with u_n outside [0,S] is left untouched.
+ * abar          fp32 [S+1] device; total_steps = S >= 2.  eps is caller-generated (R-6).
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_noise_inject(const float* x0, const float* eps, float* x_t,
+                                  int32_t n, int32_t h, int32_t w, int32_t c, int32_t block,
+                                  const int32_t* block_ids, const int32_t* count, int32_t capacity,
+                                  const int32_t* step, const float* abar, int32_t total_steps,
+                                  sphinx_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
+ * (4) Block-sparse 3x3 convolution ("tiles the feature maps into blocks ...
+ * enables batched convolution over selected blocks"):
+ *   y[n,p,co] = bias[co] + sum_{dy,dx in {-1,0,1}} sum_ci W[co][dy+1][dx+1][ci] * x[n,p+(dy,dx),ci]
+ * with x = 0 outside the image (R-17), computed (bf16 x bf16, fp32 accumulation on the
+ * tcgen05 tensor cores) for every real pixel of every listed block and written into the
+ * full-resolution y at its own position (the scatter of computed blocks is fused).
+ * Halo pixels are read from the full map as-is: inactive blocks there hold cached values
+ * (P:352 latent reuse).  Pixels of unlisted blocks are NOT written (persistent-buffer
+ * mode: pre-fill y with the cache, R-17).
+ *
+ * x      bf16 NHWC [N][h][w][c_in] device, 16-byte aligned.
+ * w      bf16 [c_out][3][3][c_in] device (OHWI, R-19; torch OIHW -> permute(0,2,3,1)).
+ * bias   fp32 [c_out] device or NULL.
+ * y      NHWC [N][h][w][c_out] device, y_dtype bf16 or fp32; must not alias x.
+ * c_in % 8 == 0, c_out % 8 == 0, block in {4, 8}  (else SPHINX_ERR_UNSUPPORTED).
+ * block_ids/count/capacity  list from sphinx_compact_blocks (capacity = N*Hb*Wb upper bound).
+ * workspace  reserved (pass NULL, 0); sphinx_conv_workspace_size returns 0 in ABI v1.
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, const float* bias,
+                                    void* y, sphinx_dtype y_dtype,
+                                    int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+                                    int32_t block, const int32_t* block_ids, const int32_t* count,
+                                    int32_t capacity, void* workspace, size_t workspace_bytes,
+                                    sphinx_stream_t stream);
+SPHINX_API size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+                                  int32_t block);
+
+/* ---------------------------------------------------------------------------------
+ * (5) Cached scatter ("reuses cached latents from the last full denoising step for
+ * unrefined regions"):  out[n,y,x,:] = active(n, y/b, x/b) ? src[...] : cache[n,y,x,:]
+ * as a bit copy (NaN payloads and -0 preserved).
+ *
+ * src_layout FULL:    src NHWC [N][h][w][c]; active(n,by,bx) = block_mask[n][by][bx] &&
+ *                     (start_step == NULL || 0 <= start_step[n] <= step_u)  (same predicate as
+ *                     SELECT_ACTIVE).  out may alias src: then only inactive blocks are written.
+ * src_layout COMPACT: src [count][b][b][c] holds the listed blocks in list order
+ *                     (block_ids/count required, ascending); active = listed.
+ * cache, out  NHWC device; dtype selects the element width (bf16 = 2 B, fp32 = 4 B);
+ *             c * elem_size must be a multiple of 16 bytes; out must not alias cache.
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_scatter_cached(const void* src, sphinx_src_layout src_layout,
+                                    const void* cache, void* out, sphinx_dtype dtype,
+                                    int32_t n, int32_t h, int32_t w, int32_t c, int32_t block,
+                                    const uint8_t* block_mask, const int32_t* start_step,
+                                    int32_t step_u, const int32_t* block_ids, const int32_t* count,
+                                    sphinx_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHINX_H */

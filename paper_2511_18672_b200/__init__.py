@@ -1,0 +1,227 @@
+"""Python binding of libsphinx.so — the B200-native Sphinx selective-refinement hot path.
+
+Argument marshalling only: every step runs in the CUDA kernels behind the C ABI
+(include/sphinx.h).  PyTorch supplies device memory and streams.  There is no
+CPU or PyTorch fallback: if the library is missing or the device is not sm_100,
+every call raises.
+
+Functions carry the C names:
+    sphinx_block_mask       step 1  (Alg1 lines 4-10; Eq. 2)
+    sphinx_compact_blocks   step 2  (Alg1 lines 17, 19)
+    sphinx_noise_inject     step 3  (Alg1 lines 12, 19)
+    sphinx_sparse_conv3x3   step 4
+    sphinx_scatter_cached   step 5
+"""
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "libsphinx.so")
+
+OK, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_DEVICE = 0, 1, 2, 3, 4
+BF16, F32 = 0, 1
+SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
+SRC_FULL, SRC_COMPACT = 0, 1
+MAX_LOGICS = 8
+ABI_VERSION = 1
+EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
+           "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
+           "sphinx_conv_workspace_size", "sphinx_scatter_cached")
+
+_lib = None
+
+
+class SphinxError(RuntimeError):
+    def __init__(self, fn, status, cuda_err=0):
+        names = {1: "INVALID_ARGUMENT", 2: "UNSUPPORTED", 3: "CUDA", 4: "DEVICE"}
+        super().__init__(f"{fn}: SPHINX_ERR_{names.get(status, status)}"
+                         + (f" (cudaError {cuda_err})" if status == ERR_CUDA else ""))
+        self.status = status
+
+
+class KLogic(ctypes.Structure):
+    """sphinx_klogic."""
+    _fields_ = [("m", ctypes.c_int32), ("thr", ctypes.c_double * 16),
+                ("step", ctypes.c_int32 * 16), ("fallback_k", ctypes.c_int32),
+                ("k_max", ctypes.c_int32)]
+
+
+class StartArgs(ctypes.Structure):
+    """sphinx_start_args (Alg1 lines 3-6)."""
+    _fields_ = [("q_reg", ctypes.c_void_p), ("c0", ctypes.c_void_p), ("c1", ctypes.c_void_p),
+                ("t", ctypes.c_void_p), ("logic_id", ctypes.c_void_p), ("gamma", ctypes.c_float),
+                ("logics", ctypes.c_void_p), ("n_logics", ctypes.c_int32)]
+
+
+def make_klogic(thr, steps, fallback_k=0, k_max=40):
+    lg = KLogic()
+    lg.m = len(thr)
+    for i, (t, s) in enumerate(zip(thr, steps)):
+        lg.thr[i] = float(t)
+        lg.step[i] = int(s)
+    lg.fallback_k = int(fallback_k)
+    lg.k_max = int(k_max)
+    return lg
+
+
+def load(path=SO_PATH):
+    """Loads libsphinx.so (raises if absent: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libsphinx.so not built at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    P, I, F, Z = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float, ctypes.c_size_t
+    sig = {
+        "sphinx_abi_version": ([], I),
+        "sphinx_last_cuda_error": ([], I),
+        "sphinx_block_mask": ([P, P, P, F, I, I, I, I, I, I, P, P, P, P, P], I),
+        "sphinx_compact_blocks": ([P, I, I, I, P, I, I, P, P, P], I),
+        "sphinx_noise_inject": ([P, P, P, I, I, I, I, I, P, P, I, P, P, I, P], I),
+        "sphinx_sparse_conv3x3": ([P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_conv_workspace_size": ([I, I, I, I, I, I], Z),
+        "sphinx_scatter_cached": ([P, I, P, P, I, I, I, I, I, I, P, P, I, P, P, P], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.sphinx_abi_version() != ABI_VERSION:
+        raise RuntimeError("libsphinx ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _chk(fn, rc):
+    if rc != OK:
+        raise SphinxError(fn, rc, load().sphinx_last_cuda_error() if rc == ERR_CUDA else 0)
+
+
+def _dev(t, dtype, name):
+    import torch
+    if t is None:
+        return
+    if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise ValueError(f"{name}: expected a contiguous CUDA {dtype} tensor")
+
+
+def sphinx_block_mask(opacity, uncertainty, tau_u, tau_o, px_per_cell, block, block_masks,
+                      active_count=None, start=None, start_step=None, stream=None):
+    """Step 1.  opacity/uncertainty [N,Hp,Wp] fp32; block_masks: list of u8 [N,Hb_l,Wb_l]
+    (one per level); start: dict(q_reg, c0, c1, t, gamma, logics=[KLogic], logic_id=None)."""
+    import torch
+    _dev(opacity, torch.float32, "opacity")
+    _dev(uncertainty, torch.float32, "uncertainty")
+    _dev(tau_u, torch.float32, "tau_u")
+    for m in block_masks:
+        _dev(m, torch.uint8, "block_mask")
+    _dev(active_count, torch.int32, "active_count")
+    n, hp, wp = opacity.shape
+    L = len(block_masks)
+    masks = (ctypes.c_void_p * L)(*[m.data_ptr() for m in block_masks])
+    ss = None
+    keep = []
+    if start is not None:
+        logics = (KLogic * len(start["logics"]))(*start["logics"])
+        keep.append(logics)
+        for k in ("q_reg", "c0", "c1", "t"):
+            _dev(start[k], torch.float32, k)
+        _dev(start.get("logic_id"), torch.int32, "logic_id")
+        _dev(start_step, torch.int32, "start_step")
+        ss = StartArgs(start["q_reg"].data_ptr(), start["c0"].data_ptr(), start["c1"].data_ptr(),
+                       start["t"].data_ptr(),
+                       start["logic_id"].data_ptr() if start.get("logic_id") is not None else None,
+                       float(start["gamma"]), ctypes.cast(logics, ctypes.c_void_p), len(start["logics"]))
+        keep.append(ss)
+    rc = load().sphinx_block_mask(_ptr(opacity), _ptr(uncertainty), _ptr(tau_u), float(tau_o),
+                                  n, hp, wp, int(px_per_cell), int(block), L,
+                                  ctypes.cast(masks, ctypes.c_void_p), _ptr(active_count),
+                                  ctypes.byref(ss) if ss is not None else None, _ptr(start_step),
+                                  _stream(stream))
+    _chk("sphinx_block_mask", rc)
+
+
+def sphinx_compact_blocks(block_mask, start_step, step_u, select, block_ids, count, shape=None,
+                          stream=None):
+    """Step 2.  block_mask u8 [N,Hb,Wb] (or None with shape=(N,Hb,Wb)); block_ids int32 [N*Hb*Wb];
+    count int32 [1] (stays on the device)."""
+    import torch
+    _dev(block_mask, torch.uint8, "block_mask")
+    _dev(start_step, torch.int32, "start_step")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, hb, wb = block_mask.shape if block_mask is not None else shape
+    if block_ids.numel() < n * hb * wb:
+        raise ValueError("block_ids capacity < N*Hb*Wb")
+    rc = load().sphinx_compact_blocks(_ptr(block_mask), n, hb, wb, _ptr(start_step), int(step_u),
+                                      int(select), _ptr(block_ids), _ptr(count), _stream(stream))
+    _chk("sphinx_compact_blocks", rc)
+
+
+def sphinx_noise_inject(x0, eps, x_t, block, block_ids, count, step, abar, capacity=None,
+                        stream=None):
+    """Step 3.  x0/eps/x_t NHWC fp32 [N,H,W,C]; step int32 [N]; abar fp32 [S+1]."""
+    import torch
+    for t, nm in ((x0, "x0"), (eps, "eps"), (x_t, "x_t"), (abar, "abar")):
+        _dev(t, torch.float32, nm)
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    _dev(step, torch.int32, "step")
+    n, h, w, c = x0.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = load().sphinx_noise_inject(_ptr(x0), _ptr(eps), _ptr(x_t), n, h, w, c, int(block),
+                                    _ptr(block_ids), _ptr(count), int(cap), _ptr(step), _ptr(abar),
+                                    abar.numel() - 1, _stream(stream))
+    _chk("sphinx_noise_inject", rc)
+
+
+def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None, stream=None):
+    """Step 4.  x bf16 NHWC [N,H,W,Cin]; w bf16 [Cout,3,3,Cin]; bias fp32 [Cout] or None;
+    y NHWC [N,H,W,Cout] bf16 or fp32 (only listed blocks are written)."""
+    import torch
+    _dev(x, torch.bfloat16, "x")
+    _dev(w, torch.bfloat16, "w")
+    _dev(bias, torch.float32, "bias")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    if y.dtype not in (torch.bfloat16, torch.float32) or not (y.is_cuda and y.is_contiguous()):
+        raise ValueError("y: contiguous CUDA bf16/fp32")
+    n, h, wd, cin = x.shape
+    cout = w.shape[0]
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = load().sphinx_sparse_conv3x3(_ptr(x), _ptr(w), _ptr(bias), _ptr(y),
+                                      F32 if y.dtype == torch.float32 else BF16,
+                                      n, h, wd, cin, cout, int(block), _ptr(block_ids), _ptr(count),
+                                      int(cap), None, 0, _stream(stream))
+    _chk("sphinx_sparse_conv3x3", rc)
+
+
+def sphinx_scatter_cached(src, cache, out, block, block_mask=None, start_step=None, step_u=0,
+                          block_ids=None, count=None, src_layout=SRC_FULL, stream=None):
+    """Step 5.  out = active ? src : cache (bit copy); NHWC bf16 or fp32."""
+    import torch
+    if cache.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("cache: bf16/fp32")
+    for t, nm in ((src, "src"), (cache, "cache"), (out, "out")):
+        _dev(t, cache.dtype, nm)
+    _dev(block_mask, torch.uint8, "block_mask")
+    _dev(start_step, torch.int32, "start_step")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, h, w, c = cache.shape
+    rc = load().sphinx_scatter_cached(_ptr(src), int(src_layout), _ptr(cache), _ptr(out),
+                                      F32 if cache.dtype == torch.float32 else BF16,
+                                      n, h, w, c, int(block), _ptr(block_mask), _ptr(start_step),
+                                      int(step_u), _ptr(block_ids), _ptr(count), _stream(stream))
+    _chk("sphinx_scatter_cached", rc)

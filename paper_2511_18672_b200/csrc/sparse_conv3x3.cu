@@ -1,0 +1,393 @@
+// sparse_conv3x3.cu — step (4): halo gather + 3x3 implicit GEMM on listed blocks,
+// tcgen05 tensor cores with TMEM accumulators, TMA operand staging (sm_100a).
+//
+// "tiles the feature maps into blocks ... enables batched convolution over
+// selected blocks, amortizing memory and compute overhead while preserving spatial
+// correlation across boundaries"; P:333 spatial ResNet layers act per frame.
+//
+// GEMM view:  M = pixels of listed blocks (b*b per block),
+// N = C_out, K = 9 * C_in ordered (tap, channel) to match the OHWI weights.
+//  - A tile (128 x 64): 128 / b^2 blocks; for every (tap, 64-channel chunk) each
+//    block's rows are ONE 4-D TMA box {64 ch, b, b, 1} of the NHWC map at the
+//    tap-shifted origin (bx*b+dx-1, by*b+dy-1).  The box lands as b^2 rows of
+//    128 B in the canonical K-major SWIZZLE_128B layout, and TMA's out-of-bound
+//    zero fill IS the conv's zero padding (image borders) and the ragged edge.
+//  - B tile (BN x 64): 3-D TMA box {64 ch, 1 tap, BN} of W viewed as [C_out][9][C_in].
+//  - One elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=BN,
+//    K=16) x 4 per stage into a TMEM accumulator; tcgen05.commit releases the smem
+//    stage (empty barrier) and, after the last K step, hands the accumulator to the
+//    epilogue.  Two TMEM accumulators (2*BN columns) let the epilogue of tile i
+//    overlap the main loop of tile i+1.
+//  - Epilogue: 4 warps tcgen05.ld their 32 TMEM lanes (= 32 pixels), add bias, and
+//    store straight into the full-resolution NHWC output at each pixel's own
+//    position (the scatter of computed blocks is fused; unlisted pixels untouched).
+//  - Persistent CTAs (grid = #SMs) walk the tile list in a static stride; the tile
+//    count comes from the device-side block count, so no host synchronisation.
+//  Warp roles (192 threads): w0 TMA producer, w1 TMEM allocator + MMA issuer,
+//  w2..w5 epilogue.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace sphinx {
+
+constexpr int kBM = 128;          // MMA M: pixels per tile
+constexpr int kBK = 64;           // channels per K chunk: 128 B rows, SWIZZLE_128B
+constexpr int kStageA = kBM * kBK * 2;  // 16 KB
+constexpr int kThreads = 192;
+
+struct ConvParams {
+  const int32_t* ids;
+  const int32_t* count;
+  const float* bias;
+  void* y;
+  int y_f32;
+  int h, w, cout, b, hb, wb;
+  int kc;         // 64-channel chunks per tap
+  int n_tiles_n;  // tiles along C_out
+  int bpt;        // blocks per 128-row tile = 128 / b^2
+};
+
+template <int BN>
+struct ConvCfg {
+  static constexpr int kStageB = BN * kBK * 2;
+  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr uint32_t kTmemCols = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                        : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
+  static constexpr int kSmem = 1024 + kStages * (kStageA + kStageB) + kBarBytes;
+};
+
+__device__ __forceinline__ void decode_block(int id, int hb, int wb, int& n, int& by, int& bx) {
+  n = id / (hb * wb);
+  const int r = id - n * hb * wb;
+  by = r / wb;
+  bx = r - by * wb;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                             const __grid_constant__ CUtensorMap tmB, const ConvParams p) {
+  using Cfg = ConvCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * kStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kStageB);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int count = *p.count;
+  const int m_tiles = (count + p.bpt - 1) / p.bpt;
+  const int total = m_tiles * p.n_tiles_n;
+  const int ksteps = 9 * p.kc;
+  const int bb = p.b * p.b;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      const uint64_t pol_a = policy_evict_normal();
+      const uint64_t pol_b = policy_evict_last();
+      const uint32_t stage_bytes = (uint32_t)(kStageA + Cfg::kStageB);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
+        int bn_[8], by_[8], bx_[8];
+        for (int i = 0; i < p.bpt; ++i) {
+          const int j = min(mt * p.bpt + i, count - 1);  // pad a short last tile with a real block
+          decode_block(__ldg(p.ids + j), p.hb, p.wb, bn_[i], by_[i], bx_[i]);
+        }
+        for (int tap = 0; tap < 9; ++tap) {
+          const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+          for (int kc = 0; kc < p.kc; ++kc) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], stage_bytes);
+            uint8_t* a_dst = sA + stage * kStageA;
+            for (int i = 0; i < p.bpt; ++i)
+              tma_load_4d(&tmA, &full[stage], a_dst + i * bb * 128, kc * kBK,
+                          bx_[i] * p.b + dx, by_[i] * p.b + dy, bn_[i], pol_a);
+            tma_load_3d(&tmB, &full[stage], sB + stage * Cfg::kStageB, kc * kBK, tap, nt * BN,
+                        pol_b);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int ks = 0; ks < ksteps; ++ks) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * kStageA);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::kStageB);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(a_addr + k * 32, 1024);
+            const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 1024);
+            tc_mma_bf16(d_tmem, ad, bd, idesc, (ks | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
+      const int bi = row / bb, pp = row - bi * bb;
+      const int j = mt * p.bpt + bi;
+      bool valid = (bi < p.bpt) && (j < count);
+      size_t pix = 0;
+      if (valid) {
+        int n, by, bx;
+        decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
+        const int yy = by * p.b + pp / p.b, xx = bx * p.b + pp % p.b;
+        valid = (yy < p.h) && (xx < p.w);
+        pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
+        tc_wait_ld();
+        const int co = nt * BN + c0;
+        if (valid) {
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (p.bias) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (co + i < p.cout) v[i] += __ldg(p.bias + co + i);
+          }
+          if (p.y_f32) {
+            float* yp = static_cast<float*>(p.y) + pix + co;
+#pragma unroll
+            for (int g = 0; g < 32; g += 4)
+              if (co + g < p.cout)
+                *reinterpret_cast<float4*>(yp + g) = make_float4(v[g], v[g + 1], v[g + 2], v[g + 3]);
+          } else {
+            __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + pix + co;
+#pragma unroll
+            for (int g = 0; g < 32; g += 8) {
+              if (co + g < p.cout) {
+                uint4 pk;
+                __nv_bfloat162 t0 = __floats2bfloat162_rn(v[g + 0], v[g + 1]);
+                __nv_bfloat162 t1 = __floats2bfloat162_rn(v[g + 2], v[g + 3]);
+                __nv_bfloat162 t2 = __floats2bfloat162_rn(v[g + 4], v[g + 5]);
+                __nv_bfloat162 t3 = __floats2bfloat162_rn(v[g + 6], v[g + 7]);
+                pk.x = *reinterpret_cast<uint32_t*>(&t0);
+                pk.y = *reinterpret_cast<uint32_t*>(&t1);
+                pk.z = *reinterpret_cast<uint32_t*>(&t2);
+                pk.w = *reinterpret_cast<uint32_t*>(&t3);
+                *reinterpret_cast<uint4*>(yp + g) = pk;
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                      const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t get_encode_tiled() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
+  }
+  return fn;
+}
+
+template <int BN>
+static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p,
+                               int grid, cudaStream_t s) {
+  using Cfg = ConvCfg<BN>;
+  static bool attr_set = false;  // per-process; attribute is per function, per device
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(sparse_conv3x3_tc_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    attr_set = true;
+  }
+  sparse_conv3x3_tc_kernel<BN><<<grid, kThreads, Cfg::kSmem, s>>>(ta, tb, p);
+  SPHINX_CHECK_LAUNCH();
+  return SPHINX_OK;
+}
+
+// Widest tile that minimises padded output columns (ties -> wider).
+static int pick_bn(int cout) {
+  const int cands[] = {256, 160, 128, 64, 32};
+  int best = 32, best_pad = 1 << 30;
+  for (int bn : cands) {
+    const int pad = cdiv(cout, bn) * bn;
+    if (pad < best_pad) {
+      best_pad = pad;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+}  // namespace sphinx
+
+using namespace sphinx;
+
+extern "C" size_t sphinx_conv_workspace_size(int32_t, int32_t, int32_t, int32_t, int32_t,
+                                             int32_t) {
+  return 0;
+}
+
+extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, const float* bias,
+                                               void* y, sphinx_dtype y_dtype, int32_t n, int32_t h,
+                                               int32_t w_, int32_t c_in, int32_t c_out,
+                                               int32_t block, const int32_t* block_ids,
+                                               const int32_t* count, int32_t capacity,
+                                               void* workspace, size_t workspace_bytes,
+                                               sphinx_stream_t stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (!x || !w || !y || !block_ids || !count) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (n <= 0 || h <= 0 || w_ <= 0 || c_in <= 0 || c_out <= 0 || block <= 0 || capacity < 0)
+    return SPHINX_ERR_INVALID_ARGUMENT;
+  if (y_dtype != SPHINX_BF16 && y_dtype != SPHINX_F32) return SPHINX_ERR_INVALID_ARGUMENT;
+  const int hb = cdiv(h, block), wb = cdiv(w_, block);
+  if ((int64_t)capacity > (int64_t)n * hb * wb) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (c_in % 8 || c_out % 8 || (block != 4 && block != 8)) return SPHINX_ERR_UNSUPPORTED;
+  if (!aligned16(x) || !aligned16(w) || !aligned16(y)) return SPHINX_ERR_UNSUPPORTED;
+  int sms = 0;
+  sphinx_status st = check_device(&sms);
+  if (st != SPHINX_OK) return st;
+  if (capacity == 0) return SPHINX_OK;
+  PFN_encodeTiled_t enc = get_encode_tiled();
+  if (!enc) return cuda_fail(cudaErrorNotSupported);
+
+  CUtensorMap ta, tb;
+  {
+    const cuuint64_t dims[4] = {(cuuint64_t)c_in, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
+    const cuuint64_t strides[3] = {(cuuint64_t)c_in * 2, (cuuint64_t)w_ * c_in * 2,
+                                   (cuuint64_t)h * w_ * c_in * 2};
+    const cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)block, (cuuint32_t)block, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
+  }
+  const int bn = pick_bn(c_out);
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)c_in, 9, (cuuint64_t)c_out};
+    const cuuint64_t strides[2] = {(cuuint64_t)c_in * 2, (cuuint64_t)9 * c_in * 2};
+    const cuuint32_t box[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)bn};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
+  }
+  ConvParams p;
+  p.ids = block_ids;
+  p.count = count;
+  p.bias = bias;
+  p.y = y;
+  p.y_f32 = y_dtype == SPHINX_F32;
+  p.h = h;
+  p.w = w_;
+  p.cout = c_out;
+  p.b = block;
+  p.hb = hb;
+  p.wb = wb;
+  p.kc = cdiv(c_in, kBK);
+  p.n_tiles_n = cdiv(c_out, bn);
+  p.bpt = kBM / (block * block);
+  const long long max_tiles = (long long)cdiv(capacity, p.bpt) * p.n_tiles_n;
+  const int grid = (int)(max_tiles < sms ? max_tiles : sms);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  switch (bn) {
+    case 256: return launch_bn<256>(ta, tb, p, grid, s);
+    case 160: return launch_bn<160>(ta, tb, p, grid, s);
+    case 128: return launch_bn<128>(ta, tb, p, grid, s);
+    case 64: return launch_bn<64>(ta, tb, p, grid, s);
+    default: return launch_bn<32>(ta, tb, p, grid, s);
+  }
+}

@@ -1,0 +1,48 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/sphinx.h
+declares, and rejects invalid host-visible arguments before touching a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2511_18672_b200 as sp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    hdr = open(os.path.join(ROOT, "include", "sphinx.h")).read()
+    return sorted(set(re.findall(r"SPHINX_API\s+[\w\s\*]+?\b(sphinx_\w+)\s*\(", hdr)))
+
+
+def test_header_and_binding_agree():
+    assert _declared() == sorted(sp.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = sp.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert lib.sphinx_abi_version() == sp.ABI_VERSION
+
+
+def test_invalid_arguments_rejected_on_host():
+    lib = sp.load()
+    null = None
+    # n = 0 (S:44 invalid-argument), before any device query
+    assert lib.sphinx_compact_blocks(null, 0, 9, 9, null, 0, 0, null, null, null) == sp.ERR_INVALID_ARGUMENT
+    assert lib.sphinx_compact_blocks(null, 1, 9, 9, null, 0, 0, ctypes.c_void_p(16),
+                                     ctypes.c_void_p(16), null) == sp.ERR_INVALID_ARGUMENT  # ACTIVE needs mask
+    assert lib.sphinx_noise_inject(null, null, null, 1, 8, 8, 4, 8, null, null, 1, null, null, 50,
+                                   null) == sp.ERR_INVALID_ARGUMENT
+    # tau_o outside [0,1]
+    masks = (ctypes.c_void_p * 1)(16)
+    assert lib.sphinx_block_mask(ctypes.c_void_p(16), null, null, 1.5, 1, 16, 16, 1, 4, 1,
+                                 ctypes.cast(masks, ctypes.c_void_p), null, null, null,
+                                 null) == sp.ERR_INVALID_ARGUMENT
+    # channels not a multiple of 8 -> unsupported (no fallback)
+    p = ctypes.c_void_p(1024)
+    assert lib.sphinx_sparse_conv3x3(p, p, null, p, sp.F32, 1, 16, 16, 12, 32, 4, p, p, 16, null, 0,
+                                     null) == sp.ERR_UNSUPPORTED
+    assert lib.sphinx_conv_workspace_size(1, 16, 16, 32, 32, 4) == 0

@@ -1,0 +1,295 @@
+"""GPU parity: every C-ABI entry point against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE north_star): masks, counts, id lists, start steps and scatter bit-exact;
+conv |y - y_ref| <= 1e-3 * sum|w x| + 1e-6 per element (fp32 output); noise within
+1e-6 relative to |a x0| + |s eps| (reading R-3).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synthetic as syn
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+dev = "cuda"
+
+
+def T(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(dev)
+
+
+def bf16(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(dev)
+
+
+def gpu_block_mask(sp, O, U, tau_u, tau_o, f, b, L, start=None):
+    n, hp, wp = O.shape
+    dims = oracle.level_dims(hp, wp, f, b, L)
+    masks = [torch.full((n, hb, wb), 7, dtype=torch.uint8, device=dev) for (_, _, hb, wb) in dims]
+    counts = torch.full((n, L), -5, dtype=torch.int32, device=dev)
+    k = torch.full((n,), -9, dtype=torch.int32, device=dev) if start else None
+    sp.sphinx_block_mask(T(O), None if U is None else T(U), None if tau_u is None else T(tau_u),
+                         tau_o, f, b, masks, counts, start, k)
+    torch.cuda.synchronize()
+    return [m.cpu().numpy() for m in masks], counts.cpu().numpy(), None if k is None else k.cpu().numpy()
+
+
+def gpu_compact(sp, mask, k, u, select=0, shape=None):
+    n, hb, wb = mask.shape if mask is not None else shape
+    ids = torch.full((n * hb * wb,), -7, dtype=torch.int32, device=dev)
+    cnt = torch.full((1,), -1, dtype=torch.int32, device=dev)
+    sp.sphinx_compact_blocks(None if mask is None else T(mask), None if k is None else T(k, torch.int32),
+                             u, select, ids, cnt, shape=(n, hb, wb))
+    c = int(cnt.item())
+    return ids, cnt, ids[:c].cpu().numpy()
+
+
+# ----------------------------------------------------------------- step 1
+
+@pytest.mark.parametrize("case", GOLD["block_mask"], ids=lambda c: c["name"])
+def test_block_mask_worked_examples(sphinx, case):
+    O = np.ones((case["n"], case["hp"], case["wp"]), np.float32)
+    for (y, x, v) in case["pixels"]:
+        O[0, y, x] = np.nan if v == "nan" else v
+    masks, counts, _ = gpu_block_mask(sphinx, O, None, None, 0.5, case["f"], case["b"], case["levels"])
+    for l, want in enumerate(case["ids"]):
+        assert np.flatnonzero(masks[l]).tolist() == want
+
+
+@pytest.mark.parametrize("geom", [
+    dict(n=4, hp=16, wp=16, f=1, b=4, L=1, d=[0.25, 0.0, 1.0, 0.5]),     # configs[0] geometry
+    dict(n=3, hp=18, wp=18, f=1, b=8, L=1, d=[0.3, 0.6, 1.0]),           # scalar path, ragged
+    dict(n=21, hp=576, wp=576, f=8, b=8, L=3, d=list(syn.request_densities(21))),  # configs[2]
+    dict(n=2, hp=64, wp=96, f=2, b=4, L=3, d=[0.1, 0.4]),
+])
+@pytest.mark.parametrize("pattern", ["clustered", "scattered"])
+def test_block_mask_vs_oracle(sphinx, geom, pattern):
+    n, hp, wp, f, b, L = geom["n"], geom["hp"], geom["wp"], geom["f"], geom["b"], geom["L"]
+    O, cells = syn.opacity_maps(n, hp, wp, b * f, geom["d"], pattern, tag=f"gm{hp}{wp}")
+    U, tau = syn.uncertainty_maps(n, hp, wp, b * f, cells, tag=f"gm{hp}{wp}")
+    O[0, 0, 1] = np.nan
+    U[-1, hp - 1, wp - 1] = tau[-1]  # equality: not blurry
+    for uu, tt in ((U, tau), (None, None)):
+        want_m, want_c = oracle.block_mask(O, uu, tt, 0.5, f, b, L)
+        got_m, got_c, _ = gpu_block_mask(sphinx, O, uu, tt, 0.5, f, b, L)
+        for l in range(L):
+            assert np.array_equal(got_m[l], want_m[l]), l
+        assert np.array_equal(got_c, want_c)
+
+
+def test_start_steps_vs_oracle(sphinx):
+    lg0 = oracle.make_klogic(**{"thr": syn.SPEC_KLOGIC["thr"], "steps": syn.SPEC_KLOGIC["steps"]})
+    lg1 = oracle.make_klogic([0.6, 0.8, 0.9, 1.0], [5, 15, 30, 45], 2, 40)
+    glg = [sphinx.make_klogic(syn.SPEC_KLOGIC["thr"], syn.SPEC_KLOGIC["steps"]),
+           sphinx.make_klogic([0.6, 0.8, 0.9, 1.0], [5, 15, 30, 45], 2, 40)]
+    reqs = [syn.request_scores(21, c0, c1, tag=f"r{i}") for i, (c0, c1) in
+            enumerate([(62, 66), (70, 58), (50, 50), (64, 61)])]
+    q, c0, c1, t = (np.concatenate([r[j] for r in reqs]) for j in range(4))
+    n = len(q)
+    # tie cases TV-6..8 and invalid inputs appended
+    q = np.concatenate([q, np.float32([61.75, 59.8, np.float32(0.97 * 65), 60, 60])])
+    c0 = np.concatenate([c0, np.float32([60, 60, 60, 0, 60])])
+    c1 = np.concatenate([c1, np.float32([70, 70, 70, 0, 70])])
+    t = np.concatenate([t, np.float32([0.25, 0.25, 0.25, 0.5, 1.5])])
+    lid = (np.arange(len(q)) % 2).astype(np.int32)
+    lid[n:] = 0
+    O = np.ones((len(q), 16, 16), np.float32)
+    for gamma in (0.5, 1.0, 0.7):
+        want = oracle.start_step(q, c0, c1, t, gamma, [lg0, lg1], logic_id=lid)
+        start = dict(q_reg=T(q), c0=T(c0), c1=T(c1), t=T(t), gamma=gamma, logics=glg,
+                     logic_id=T(lid))
+        _, _, k = gpu_block_mask(sphinx, O, None, None, 0.5, 1, 4, 1, start=start)
+        assert np.array_equal(k, want), gamma
+        assert k[n:].tolist() == [25, 10, 25, -1, -1] or gamma != 0.5
+
+
+# ----------------------------------------------------------------- step 2
+
+def test_compact_vs_oracle(sphinx):
+    rg = syn.rng("gpu-compact")
+    for (n, hb, wb) in [(1, 4, 4), (21, 9, 9), (168, 9, 9), (168, 5, 5), (3, 1, 1), (7, 33, 31)]:
+        for dens in (0.0, 0.05, 0.25, 1.0):
+            m = (rg.random((n, hb, wb)) < dens).astype(np.uint8)
+            k = rg.integers(-1, 45, size=n).astype(np.int32)
+            for u in (0, 25, 49):
+                for sel in (0, 1, 2):
+                    if sel == 0:
+                        for kk in (k, None):
+                            _, _, got = gpu_compact(sphinx, m, kk, u, sel)
+                            assert np.array_equal(got, oracle.compact(m, kk, u, sel))
+                    else:
+                        _, _, got = gpu_compact(sphinx, None, k, u, sel, shape=(n, hb, wb))
+                        assert np.array_equal(got, oracle.compact(None, k, u, sel, shape=(n, hb, wb)))
+
+
+# ----------------------------------------------------------------- step 3
+
+@pytest.mark.parametrize("shape,b", [((1, 16, 16, 4), 4), ((21, 72, 72, 4), 8), ((3, 36, 36, 4), 8),
+                                     ((2, 18, 18, 3), 8)])
+def test_noise_vs_oracle(sphinx, shape, b):
+    n, h, w, c = shape
+    hb, wb = -(-h // b), -(-w // b)
+    rg = syn.rng("gpu-noise", shape)
+    m = (rg.random((n, hb, wb)) < 0.4).astype(np.uint8)
+    ids = oracle.compact(m)
+    step = rg.integers(-1, 52, size=n).astype(np.int32)  # includes out-of-range u: untouched
+    abar = syn.abar_cosine(50)
+    x0, eps, xt = (syn.latents_f32(shape, f"gn{j}") for j in range(3))
+    want = oracle.noise(x0, eps, xt, b, ids, step, abar)
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, None, 0)
+    out = T(xt)
+    sphinx.sphinx_noise_inject(T(x0), T(eps), out, b, g_ids, g_cnt, T(step), T(abar))
+    got = out.cpu().numpy()
+    touched = want != xt.astype(np.float64)
+    assert np.array_equal(got[~touched], xt[~touched])
+    # tolerance relative to the term magnitudes |a x0| + |s eps| (reading R-3)
+    u = np.clip(step, 0, 50)
+    a = np.sqrt(abar[u].astype(np.float64))[:, None, None, None]
+    s = np.sqrt(1.0 - abar[u].astype(np.float64))[:, None, None, None]
+    scale = np.abs(a * x0) + np.abs(s * eps)
+    assert np.all(np.abs(got - want) <= 1e-6 * scale + 1e-30)
+    # in place (x_t aliases x0)
+    inplace = T(x0)
+    sphinx.sphinx_noise_inject(inplace, T(eps), inplace, b, g_ids, g_cnt, T(step), T(abar))
+    want2 = oracle.noise(x0, eps, x0, b, ids, step, abar)
+    assert np.all(np.abs(inplace.cpu().numpy() - want2) <= 1e-6 * scale + 1e-30)
+
+
+# ----------------------------------------------------------------- step 4
+
+def _conv_check(sphinx, n, h, w, cin, cout, b, density, pattern, tag, out_dtype=torch.float32,
+                bias=True, weights=None, x_bits=None, sample_ids=None):
+    hb, wb = -(-h // b), -(-w // b)
+    x = syn.features_bf16((n, h, w, cin), tag) if x_bits is None else x_bits
+    wt = syn.weights_bf16(cout, cin, tag) if weights is None else weights
+    bs = syn.bias_f32(cout, tag) if bias else None
+    rg = syn.rng("conv-mask", tag)
+    m = np.stack([syn.choose_cells(rg, hb, wb, round(density * hb * wb), pattern) for _ in range(n)])
+    m = m.astype(np.uint8)
+    ids_all = oracle.compact(m)
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, None, 0)
+    sentinel = -12345.0
+    y = torch.full((n, h, w, cout), sentinel, dtype=out_dtype, device=dev)
+    sphinx.sphinx_sparse_conv3x3(bf16(x), bf16(wt), None if bs is None else T(bs), y, b, g_ids, g_cnt)
+    torch.cuda.synchronize()
+    got = y.float().cpu().numpy().astype(np.float64)
+    check_ids = ids_all if sample_ids is None else ids_all[sample_ids(len(ids_all))]
+    want, acc = oracle.conv3x3_blocks(x, wt, bs, b, check_ids)
+    listed = ~np.isnan(want[..., 0])
+    tol = 1e-3 * acc[listed] + 1e-6
+    if out_dtype == torch.bfloat16:
+        tol = tol + 2.0 ** -8 * np.abs(want[listed])
+    err = np.abs(got[listed] - want[listed])
+    assert np.all(err <= tol), f"max err/tol {np.max(err / tol)}"
+    if sample_ids is None:  # unlisted pixels untouched
+        assert np.all(got[~listed] == np.float64(np.float32(sentinel)) if out_dtype == torch.float32
+                      else got[~listed] == float(torch.tensor(sentinel, dtype=out_dtype).float()))
+    return err, tol
+
+
+def test_conv_config0(sphinx):
+    """configs[0]: 1 frame, 16x16x32, 3x3 32->32, block 4, 25% active."""
+    _conv_check(sphinx, 1, 16, 16, 32, 32, 4, 0.25, "scattered", "cfg0")
+
+
+@pytest.mark.parametrize("h,c,pattern,dens", [(72, 320, "clustered", 0.25), (36, 640, "scattered", 0.4),
+                                              (18, 1280, "checker", 0.5), (72, 320, "checker", 1.0)])
+def test_conv_unet_levels(sphinx, h, c, pattern, dens):
+    """configs[1]/[2] geometries: 72x72x320, 36x36x640 (ragged 5x5 blocks), 18x18x1280."""
+    _conv_check(sphinx, 2, h, h, c, c, 8, dens, pattern, f"lvl{h}")
+
+
+@pytest.mark.parametrize("cin,cout,b", [(64, 64, 8), (128, 32, 4), (320, 160, 8), (8, 16, 4),
+                                        (96, 264, 8)])
+def test_conv_shapes_bf16_out(sphinx, cin, cout, b):
+    _conv_check(sphinx, 3, 20, 28, cin, cout, b, 0.5, "scattered", f"shape{cin}{cout}",
+                out_dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("ky,kx", [(0, 0), (1, 1), (2, 1), (0, 2)])
+def test_conv_shift_kernels_exact(sphinx, ky, kx):
+    """TV-12/13: a shift kernel reproduces the shifted input exactly, incl. halos across
+    blocks (active and inactive neighbours) and zero padding at the border."""
+    n, h, w, c, b = 2, 18, 18, 64, 8
+    wt = np.zeros((c, 3, 3, c), np.float32)
+    for i in range(c):
+        wt[i, ky, kx, i] = 1.0
+    err, _ = _conv_check(sphinx, n, h, w, c, c, b, 0.6, "scattered", "shift", bias=False,
+                         weights=syn.to_bf16_bits(wt))
+    assert np.all(err == 0)
+
+
+def test_conv_density_zero_and_count_zero(sphinx):
+    n, h, w, c, b = 1, 16, 16, 32, 4
+    g_ids, g_cnt, got = gpu_compact(sphinx, np.zeros((n, 4, 4), np.uint8), None, 0)
+    assert len(got) == 0
+    y = torch.full((n, h, w, c), 3.0, device=dev)
+    sphinx.sphinx_sparse_conv3x3(bf16(syn.features_bf16((n, h, w, c), "z")),
+                                 bf16(syn.weights_bf16(c, c, "z")), None, y, b, g_ids, g_cnt)
+    assert torch.all(y == 3.0)
+
+
+def test_conv_full_size_sampled(sphinx):
+    """BASELINE configs[3] size at level 1 (168 frames x 72x72x320, 25%): sampled blocks."""
+    _conv_check(sphinx, 168, 72, 72, 320, 320, 8, 0.25, "clustered", "full168",
+                sample_ids=lambda m: np.linspace(0, m - 1, 24).astype(int))
+
+
+# ----------------------------------------------------------------- step 5
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_scatter_vs_oracle(sphinx, dtype):
+    n, h, w, c, b = 5, 36, 36, 64, 8
+    hb, wb = 5, 5
+    rg = syn.rng("gpu-scatter", dtype)
+    m = (rg.random((n, hb, wb)) < 0.4).astype(np.uint8)
+    k = np.array([0, 10, 30, -1, 45], np.int32)
+    u = 25
+    if dtype == "bf16":
+        src, cache = syn.features_bf16((n, h, w, c), "s1"), syn.features_bf16((n, h, w, c), "s2")
+        src[0, 0, 0, 0] = 0x7FC1  # NaN payload
+        src[0, 0, 0, 1] = 0x8000  # -0
+        tt = lambda a: bf16(a)
+        back = lambda t: t.view(torch.int16).cpu().numpy().view(np.uint16)
+    else:
+        src, cache = syn.latents_f32((n, h, w, c), "s1"), syn.latents_f32((n, h, w, c), "s2")
+        tt = lambda a: T(a)
+        back = lambda t: t.cpu().numpy()
+    want = oracle.scatter(src, cache, b, mask=m, k=k, u=u)
+    out = tt(np.zeros_like(cache))
+    sphinx.sphinx_scatter_cached(tt(src), tt(cache), out, b, block_mask=T(m), start_step=T(k), step_u=u)
+    assert np.array_equal(back(out).view(np.uint8), want.view(np.uint8))
+    # in place: out aliases src -> only inactive blocks written
+    s2 = tt(src)
+    sphinx.sphinx_scatter_cached(s2, tt(cache), s2, b, block_mask=T(m), start_step=T(k), step_u=u)
+    assert np.array_equal(back(s2).view(np.uint8), want.view(np.uint8))
+    # COMPACT layout
+    ids = oracle.compact(m, k, u)
+    comp = np.zeros((max(len(ids), 1), b, b, c), cache.dtype)
+    for j, id_ in enumerate(ids):
+        i, r = divmod(int(id_), hb * wb)
+        by, bx = divmod(r, wb)
+        blk = src[i, by * b:(by + 1) * b, bx * b:(bx + 1) * b]
+        comp[j, :blk.shape[0], :blk.shape[1]] = blk
+    want_c = oracle.scatter(comp, cache, b, ids=ids, src_layout=oracle.SRC_COMPACT)
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, k, u)
+    out2 = tt(np.zeros_like(cache))
+    sphinx.sphinx_scatter_cached(tt(comp), tt(cache), out2, b, block_ids=g_ids, count=g_cnt,
+                                 src_layout=sphinx.SRC_COMPACT)
+    assert np.array_equal(back(out2).view(np.uint8), want_c.view(np.uint8))
+    assert np.array_equal(want_c.view(np.uint8), want.view(np.uint8))
+
+
+def test_invalid_arguments_raise(sphinx):
+    with pytest.raises(sphinx.SphinxError):
+        sphinx.sphinx_block_mask(T(np.ones((1, 16, 16), np.float32)), None, None, 2.0, 1, 4,
+                                 [torch.zeros((1, 4, 4), dtype=torch.uint8, device=dev)])
