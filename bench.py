@@ -61,6 +61,7 @@ def make_request(seed_tag):
     h0 = HP // F
     req["x0"] = syn.latents_f32((N_FRAMES, h0, h0, 4), f"x0{seed_tag}")
     req["eps"] = syn.latents_f32((N_FRAMES, h0, h0, 4), f"eps{seed_tag}")
+    req["lat_cache"] = syn.latents_f32((N_FRAMES, h0, h0, 4), f"lc{seed_tag}")
     for l, (h, c) in enumerate(LEVELS):
         req[f"feat{l}"] = syn.features_bf16((N_FRAMES, h, h, c), f"x{l}{seed_tag}")
         req[f"cache{l}"] = syn.features_bf16((N_FRAMES, h, h, c), f"c{l}{seed_tag}")
@@ -96,11 +97,13 @@ class GpuStep:
         self.cnt_in = torch.empty((1,), dtype=torch.int32, device=dev)
         self.step_u1 = torch.full((n,), U_STEP + 1, dtype=torch.int32, device=dev)
         self.zt = torch.empty_like(self.d["x0"])
-        self.y = [self.d[f"cache{l}"].clone() for l in range(3)]   # persistent buffers
+        # persistent buffers (R-17): pre-filled with the cache once (the full step's job), the
+        # conv epilogue then writes only active blocks, i.e. the feature-level scatter is fused
+        self.y = [self.d[f"cache{l}"].clone() for l in range(3)]
         self.z = [self.d[f"cache{l}"].clone() for l in range(3)]
-        self.out = [torch.empty_like(self.d[f"cache{l}"]) for l in range(3)]
+        self.lat_out = torch.empty_like(self.d["x0"])
         self.logics = [sp.make_klogic(syn.SPEC_KLOGIC["thr"], syn.SPEC_KLOGIC["steps"])]
-        self.launches_per_step = 2 + 4 + 2 + 3 * CONVS_PER_LEVEL + 3
+        self.launches_per_step = 2 + 4 + 2 + 3 * CONVS_PER_LEVEL + 1
         self.conv_events = None
 
     def run(self, conv_events=None):
@@ -126,8 +129,10 @@ class GpuStep:
                 if conv_events is not None:
                     conv_events[l][j][1].record()
                 src = dst
-            sp.sphinx_scatter_cached(src, d[f"cache{l}"], self.out[l], B, block_mask=self.masks[l],
-                                     start_step=self.k, step_u=U_STEP)
+        # step 5 at latent resolution: refined latent blocks from this step, the latent cache of
+        # the last full step everywhere else (P:352 spatial latent reuse)
+        sp.sphinx_scatter_cached(self.zt, d["lat_cache"], self.lat_out, B, block_mask=self.masks[0],
+                                 start_step=self.k, step_u=U_STEP)
 
     def active_stats(self):
         """Algorithmic FLOPs of the step's convs: real active pixels x 2*9*Cin*Cout."""
@@ -243,6 +248,52 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0
     return out
 
 
+def capture_step(torch, st, with_conv_events):
+    """Captures one step into a CUDA graph (launch-bound chain of ~15 kernels).  Conv launches
+    are bracketed by external event-record nodes so their device time is measured inside the
+    replayed graph."""
+    conv_ev = None
+    if with_conv_events:
+        conv_ev = [[[torch.cuda.Event(enable_timing=True, external=True),
+                     torch.cuda.Event(enable_timing=True, external=True)]
+                    for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            st.run()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        st.run(conv_ev)
+    torch.cuda.synchronize()
+    return g, conv_ev
+
+
+def scatter_bandwidth(torch, st, reps=20):
+    """Out-of-place cached scatter of the level-0 feature map (bf16 [21,72,72,320]): 2 x map bytes
+    per launch (read src-or-cache, write out), HBM roofline.  L2 flushed before each launch."""
+    d = st.d
+    out = torch.empty_like(d["cache0"])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=out.device)
+    ts = []
+    for i in range(reps + 3):
+        flush.fill_(0.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st.sp.sphinx_scatter_cached(st.z[0], d["cache0"], out, B, block_mask=st.masks[0], start_step=st.k,
+                                    step_u=U_STEP)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(e0.elapsed_time(e1))
+    t = statistics.median(ts)
+    nbytes = 2 * out.numel() * out.element_size()
+    return {"kernel": "scatter_full_kernel", "shape": list(out.shape), "ms": round(t, 5),
+            "algorithmic_bytes": nbytes, "gbs": round(nbytes / (t * 1e-3) / 1e9, 1)}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -259,13 +310,17 @@ def run_gpu(args):
     hbm, tc_peak, tc_sust, peak_kind = peaks()
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    try:
+        g, conv_ev = capture_step(torch, st, with_conv_events=True)
+        graph_note = "CUDA graph replay, conv launches timed by captured external events"
+    except Exception as e:  # event nodes unsupported: time the convs outside the graph
+        g, _ = capture_step(torch, st, with_conv_events=False)
+        conv_ev, graph_note = None, f"CUDA graph replay; conv events unsupported in capture ({type(e).__name__})"
     for _ in range(max(args.warmup, 3)):
-        st.run()
+        g.replay()
         flush.fill_(1.0)
     torch.cuda.synchronize()
     flops, px_l, blocks_l = st.active_stats()
-    conv_ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-                for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
     step_ms, conv_ms = [], [[[] for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
     stop = threading.Event()
     clk_lines = []
@@ -275,22 +330,38 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    for _ in range(args.steps):
+    reps = max(1, args.steps)
+    for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        st.run(conv_ev)
+        g.replay()
         e1.record()
         flush.fill_(1.0)  # L2 flush between timed steps (outside the e0..e1 window)
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        for l in range(3):
-            for j in range(CONVS_PER_LEVEL):
-                conv_ms[l][j].append(conv_ev[l][j][0].elapsed_time(conv_ev[l][j][1]))
+        if conv_ev is not None:
+            for l in range(3):
+                for j in range(CONVS_PER_LEVEL):
+                    conv_ms[l][j].append(conv_ev[l][j][0].elapsed_time(conv_ev[l][j][1]))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # keep sampling clocks through a sustained stretch so the record is not 3 samples long
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        g.replay()
+        torch.cuda.synchronize()
     stop.set()
     th.join(timeout=3)
+    if conv_ev is None:  # eager fallback for per-conv timing
+        ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+               for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
+        for _ in range(reps):
+            st.run(ev)
+            torch.cuda.synchronize()
+            for l in range(3):
+                for j in range(CONVS_PER_LEVEL):
+                    conv_ms[l][j].append(ev[l][j][0].elapsed_time(ev[l][j][1]))
     ms = statistics.mean(step_ms)
     if world > 1:
         t = torch.tensor([ms, float(flops)], dtype=torch.float64, device=dev)
@@ -303,7 +374,6 @@ def run_gpu(args):
         ms_all, flops_all = ms, float(flops)
     value = flops_all / (ms_all * 1e-3) / 1e12
 
-    # dominant kernel: the level-1 (72x72x320) sparse conv — report each level's conv
     per_level = []
     for l, (h, c) in enumerate(LEVELS):
         t_l = statistics.mean([statistics.mean(conv_ms[l][j]) for j in range(CONVS_PER_LEVEL)])
@@ -312,66 +382,69 @@ def run_gpu(args):
                           "real_px": px_l[l], "conv_ms": round(t_l, 5),
                           "tflops": round(f_l / (t_l * 1e-3) / 1e12, 2)})
     conv_total_ms = sum(p["conv_ms"] for p in per_level) * CONVS_PER_LEVEL
+    # dominant kernel = the conv launch family with the largest share of the step
     dom = max(per_level, key=lambda p: p["conv_ms"])
     dom_flops = dom["real_px"] * 2 * 9 * LEVELS[dom["level"]][1] ** 2
     achieved = dom_flops / (dom["conv_ms"] * 1e-3) / 1e12
+    all_conv_tflops = flops / (conv_total_ms * 1e-3) / 1e12
 
-    # e2e: same step through the public API with host buffers, H2D + D2H inside the timing
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(torch, st, req, dev, args, flops)
-
+    e2e = None if args.no_e2e else run_e2e(torch, st, g, req, dev, args, flops)
     sweep = None
     if rank == 0 and not args.no_sweep:
         sweep = density_sweep(torch, st.sp, dev)
+    scat = scatter_bandwidth(torch, st) if rank == 0 else None
+    if scat is not None:
+        scat["hbm_frac"] = round(scat["gbs"] / hbm, 4)
 
     if rank == 0:
         cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(req, bounded_s=args.cpu_seconds)
         line = {
             "metric": "block-sparse conv effective TFLOP/s & speedup vs dense at 10/25/50% density",
-            "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": reps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_all, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "configs[2]: 21-frame request, 3 UNet levels (72x72x320, 36x36x640, "
                                    "18x18x1280), per-frame adaptive start steps, mean level-0 density 25%; "
-                                   "per rank at N>1 (weak scaling)",
+                                   "one request per rank at N>1 (weak scaling)",
                        "frames_per_rank": N_FRAMES, "image": [HP, HP], "block": B, "u": U_STEP,
                        "convs_per_level": CONVS_PER_LEVEL, "active_blocks_per_level": blocks_l,
                        "density_per_level": [round(blocks_l[l] / (N_FRAMES * st.dims[l][1] ** 2), 4)
                                              for l in range(3)],
-                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"dp{world}"},
-            "gpu_launches": st.launches_per_step * args.steps,
+                       "l2": "flushed between timed steps (256 MB write)", "timing": graph_note,
+                       "parallelism": f"dp{world}"},
+            "gpu_launches": st.launches_per_step * reps,
             "roofline": {"bound": "tensor", "kernel": "sparse_conv3x3_tc_kernel (level %d)" % dom["level"],
                          "achieved": round(achieved, 2), "peak": tc_peak, "unit": "TFLOP/s",
                          "frac": round(achieved / tc_peak, 4), "peak_kind": f"{peak_kind} bf16 burst",
                          "frac_sustained": round(achieved / tc_sust, 4) if tc_sust else None,
-                         "traffic": None, "conv_share_of_step": round(conv_total_ms / ms_all, 4)},
+                         "traffic": None, "all_convs_tflops": round(all_conv_tflops, 2),
+                         "conv_share_of_step": round(conv_total_ms / ms_all, 4)},
             "conv_levels": per_level,
+            "scatter_bandwidth": scat,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "density_sweep": sweep,
             "paper_context": "1.8x average end-to-end speedup vs diffusion-only on 4x A40 (P:34, P:445); "
                              "context only, not this metric",
+            "clocks": summarize_clocks(clk_lines),
         }
-        stop2 = summarize_clocks(clk_lines)
-        line["clocks"] = stop2
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def run_e2e(torch, st, req, dev, args, flops):
-    """Inputs copied from pinned host memory each step, final outputs copied back."""
-    in_keys = ["O", "U", "tau_u", "q", "c0", "c1", "t", "x0", "eps", "lid", "feat0", "feat1", "feat2",
-               "cache0", "cache1", "cache2"]
-    in_keys = list(dict.fromkeys(in_keys))
+def run_e2e(torch, st, g, req, dev, args, flops):
+    """Same step through the public API with HOST buffers: every step copies its inputs from
+    pinned host memory (H2D) and reads its outputs back (D2H), all inside the timed region."""
+    in_keys = ["O", "U", "tau_u", "q", "c0", "c1", "t", "x0", "eps", "lid", "lat_cache", "feat0", "feat1",
+               "feat2"]
     host = {k: torch.from_numpy(np.ascontiguousarray(req[k].view(np.int16) if req[k].dtype == np.uint16
                                                      else req[k])).pin_memory() for k in in_keys}
-    out_host = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in st.out]
-    zt_host = torch.empty(st.zt.shape, dtype=st.zt.dtype).pin_memory()
+    outs = [st.z[l] for l in range(3)] + [st.lat_out]
+    out_host = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
     h2d = sum(h.numel() * h.element_size() for h in host.values())
-    d2h = sum(o.numel() * o.element_size() for o in out_host) + zt_host.numel() * 4
+    d2h = sum(o.numel() * o.element_size() for o in out_host)
 
     def step():
         for k, h in host.items():
@@ -380,10 +453,9 @@ def run_e2e(torch, st, req, dev, args, flops):
                 dst.view(torch.int16).copy_(h, non_blocking=True)
             else:
                 dst.copy_(h, non_blocking=True)
-        st.run()
-        for o, oh in zip(st.out, out_host):
+        g.replay()
+        for o, oh in zip(outs, out_host):
             oh.copy_(o, non_blocking=True)
-        zt_host.copy_(st.zt, non_blocking=True)
 
     for _ in range(2):
         step()
@@ -398,7 +470,8 @@ def run_e2e(torch, st, req, dev, args, flops):
     ms = e0.elapsed_time(e1) / reps
     return {"value": round(flops / (ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "note": "conv weights resident on device (model state); per-step inputs and outputs cross PCIe"}
+            "note": "conv weights resident on device (model state); per-step maps, features and latents "
+                    "H2D, refined feature maps + latent D2H"}
 
 
 # ----------------------------------------------------------------- CPU oracle arm
@@ -417,6 +490,7 @@ def oracle_step_sample(req, max_blocks_per_level):
     z = oracle.noise(req["x0"], req["eps"], req["x0"], B, ids[0], k, req["abar"])
     z = oracle.noise(req["x0"], req["eps"], z.astype(np.float32), B, inact,
                      np.full(N_FRAMES, U_STEP + 1, np.int32), req["abar"])
+    oracle.scatter(z.astype(np.float32), req["lat_cache"], B, mask=masks[0], k=k, u=U_STEP)
     flops = 0
     for l, (h, c) in enumerate(LEVELS):
         sub = ids[l][:max_blocks_per_level]
@@ -425,17 +499,20 @@ def oracle_step_sample(req, max_blocks_per_level):
         r = sub % (hb * hb)
         px = int((np.minimum(B, h - (r // hb) * B) * np.minimum(B, h - (r % hb) * B)).sum())
         flops += px * 2 * 9 * c * c
-        ysc = np.where(np.isnan(y), 0, y).astype(np.float32)
-        oracle.scatter(ysc, syn.bf16_bits_to_f32(req[f"cache{l}"]), B, mask=masks[l], k=k, u=U_STEP)
     return time.perf_counter() - t0, flops
+
+
+def calibrate_blocks(req, seconds):
+    """Blocks per level so that one oracle step sample takes about `seconds`."""
+    t1, _ = oracle_step_sample(req, 1)
+    t3, _ = oracle_step_sample(req, 3)
+    slope = max((t3 - t1) / 2, 1e-3)
+    return int(max(1, min(4000, 1 + (seconds - t1) / slope)))
 
 
 def cpu_baseline(req, bounded_s=15.0):
     cores = os.cpu_count()
-    # calibrate the sample so the oracle runs ~bounded_s seconds
-    t1, f1 = oracle_step_sample(req, 2)
-    rate = f1 / max(t1, 1e-3)
-    nb = int(max(2, min(200, bounded_s * rate / max(f1 / 2, 1) / 3)))
+    nb = calibrate_blocks(req, bounded_s)
     t, f = oracle_step_sample(req, nb)
     return {"value": round(f / t / 1e12, 8), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
             "seconds": round(t, 2),
@@ -449,9 +526,7 @@ def run_reference(args):
         return
     req = make_request("r0")
     cores = os.cpu_count()
-    t1, f1 = oracle_step_sample(req, 2)
-    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
-    nb = int(max(2, min(200, per_step_budget * (f1 / max(t1, 1e-3)) / max(f1 / 2, 1) / 3)))
+    nb = calibrate_blocks(req, 150.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
         oracle_step_sample(req, nb)
     ts, fl = [], 0

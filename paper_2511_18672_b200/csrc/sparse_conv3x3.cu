@@ -28,6 +28,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -50,14 +52,20 @@ struct ConvParams {
   int bpt;        // blocks per 128-row tile = 128 / b^2
 };
 
-template <int BN>
+template <int BN, int CG>
 struct ConvCfg {
-  static constexpr int kStageB = BN * kBK * 2;
-  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kBNc = BN / CG;  // B rows (output channels) held by this CTA
+  static constexpr int kStageB = kBNc * kBK * 2;
+  static constexpr int kStageBytes = kStageA + kStageB;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kMaxSmem = 232448;  // 227 KB opt-in per CTA
+  static constexpr int kStagesFit = (kMaxSmem - 1024 - kBarBytes) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr uint32_t kTmemCols = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
-  static constexpr int kSmem = 1024 + kStages * (kStageA + kStageB) + kBarBytes;
+  static constexpr int kSmem = 1024 + kStages * kStageBytes + kBarBytes;
+  static_assert(kStages >= 3, "pipeline too shallow");
+  static_assert((2 * kStages + 4) * 8 + 4 <= kBarBytes, "barrier area");
 };
 
 __device__ __forceinline__ void decode_block(int id, int hb, int wb, int& n, int& by, int& bx) {
@@ -67,11 +75,17 @@ __device__ __forceinline__ void decode_block(int id, int hb, int wb, int& n, int
   bx = r - by * wb;
 }
 
-template <int BN>
+// CG = 1: one CTA per 128 x BN tile, tcgen05.mma.cta_group::1 (M = 128).
+// CG = 2: a CTA pair (cluster of 2) per 256 x BN tile, tcgen05.mma.cta_group::2 (M = 256):
+//   each CTA TMA-loads its own 128 rows of A and its half (BN/2 rows) of B; the leader
+//   (rank 0) waits for both halves on its full barrier and issues the MMAs; commits are
+//   multicast to both CTAs' barriers; each CTA's epilogue drains its own TMEM lanes and
+//   arrives on the leader's accumulator-empty barrier.  B traffic per SM halves.
+template <int BN, int CG, int BLK>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, const ConvParams p) {
-  using Cfg = ConvCfg<BN>;
+  using Cfg = ConvCfg<BN, CG>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -85,11 +99,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+  const int cluster_id = blockIdx.x / CG, n_clusters = gridDim.x / CG;
   const int count = *p.count;
-  const int m_tiles = (count + p.bpt - 1) / p.bpt;
+  constexpr int BPT = kBM / (BLK * BLK);  // blocks per CTA tile (2 at b=8, 8 at b=4)
+  constexpr int bb = BLK * BLK;
+  const int bpt_pair = BPT * CG;  // blocks per (pair) tile
+  const int m_tiles = (count + bpt_pair - 1) / bpt_pair;
   const int total = m_tiles * p.n_tiles_n;
   const int ksteps = 9 * p.kc;
-  const int bb = p.b * p.b;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -100,42 +118,63 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CG);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_cg2<Cfg::kTmemCols>(tmem_slot);
+    else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs) =====================
     if (elect_one()) {
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = policy_evict_last();
-      const uint32_t stage_bytes = (uint32_t)(kStageA + Cfg::kStageB);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cluster_id; t < total; t += n_clusters) {
         const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
-        int bn_[8], by_[8], bx_[8];
-        for (int i = 0; i < p.bpt; ++i) {
-          const int j = min(mt * p.bpt + i, count - 1);  // pad a short last tile with a real block
-          decode_block(__ldg(p.ids + j), p.hb, p.wb, bn_[i], by_[i], bx_[i]);
+        // TMA origin of every block of this CTA's half of the tile (kept in registers)
+        int cx[BPT], cy[BPT], cn[BPT];
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+          // pad a short last tile with a real block (its rows are computed, never stored)
+          const int j = min(mt * bpt_pair + rank * BPT + i, count - 1);
+          int n, by, bx;
+          decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
+          cn[i] = n;
+          cy[i] = by * BLK - 1;
+          cx[i] = bx * BLK - 1;
         }
+        const int n0 = nt * BN + rank * Cfg::kBNc;
         for (int tap = 0; tap < 9; ++tap) {
-          const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+          const int dy = tap / 3, dx = tap - 3 * (tap / 3);
           for (int kc = 0; kc < p.kc; ++kc) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], stage_bytes);
             uint8_t* a_dst = sA + stage * kStageA;
-            for (int i = 0; i < p.bpt; ++i)
-              tma_load_4d(&tmA, &full[stage], a_dst + i * bb * 128, kc * kBK,
-                          bx_[i] * p.b + dx, by_[i] * p.b + dy, bn_[i], pol_a);
-            tma_load_3d(&tmB, &full[stage], sB + stage * Cfg::kStageB, kc * kBK, tap, nt * BN,
-                        pol_b);
+            uint8_t* b_dst = sB + stage * Cfg::kStageB;
+            if constexpr (CG == 1) {
+              mbar_arrive_expect_tx(&full[stage], (uint32_t)Cfg::kStageBytes);
+#pragma unroll
+              for (int i = 0; i < BPT; ++i)
+                tma_load_4d(&tmA, &full[stage], a_dst + i * bb * 128, kc * kBK, cx[i] + dx,
+                            cy[i] + dy, cn[i], pol_a);
+              tma_load_3d(&tmB, &full[stage], b_dst, kc * kBK, tap, n0, pol_b);
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], (uint32_t)(2 * Cfg::kStageBytes));
+              const uint32_t bar = leader_addr(&full[stage]);
+#pragma unroll
+              for (int i = 0; i < BPT; ++i)
+                tma_load_4d_cg2(&tmA, bar, a_dst + i * bb * 128, kc * kBK, cx[i] + dx, cy[i] + dy,
+                                cn[i], pol_a);
+              tma_load_3d_cg2(&tmB, bar, b_dst, kc * kBK, tap, n0, pol_b);
+            }
             if (++stage == S) {
               stage = 0;
               phase ^= 1;
@@ -145,14 +184,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (rank == 0 && elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cluster_id; t < total; t += n_clusters) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -165,15 +204,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = umma_desc_sw128(a_addr + k * 32, 1024);
             const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 1024);
-            tc_mma_bf16(d_tmem, ad, bd, idesc, (ks | k) != 0 ? 1u : 0u);
+            if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc, (ks | k) != 0 ? 1u : 0u);
+            else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc, (ks | k) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);
+          if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_cg2_mc(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_cg2_mc(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -181,21 +221,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..5, both CTAs) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = cluster_id; t < total; t += n_clusters) {
       const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
       const int bi = row / bb, pp = row - bi * bb;
-      const int j = mt * p.bpt + bi;
-      bool valid = (bi < p.bpt) && (j < count);
+      const int j = mt * bpt_pair + rank * BPT + bi;
+      bool valid = (bi < BPT) && (j < count);
       size_t pix = 0;
       if (valid) {
         int n, by, bx;
         decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
-        const int yy = by * p.b + pp / p.b, xx = bx * p.b + pp % p.b;
+        const int yy = by * BLK + pp / BLK, xx = bx * BLK + pp % BLK;
         valid = (yy < p.h) && (xx < p.w);
         pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
       }
@@ -244,7 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_cluster(leader_addr(&tempty[acc]));
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -252,9 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    if constexpr (CG == 2) tmem_dealloc_cg2<Cfg::kTmemCols>(tmem_base);
+    else tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -279,20 +324,40 @@ static PFN_encodeTiled_t get_encode_tiled() {
   return fn;
 }
 
-template <int BN>
+template <int BN, int CG, int BLK>
 static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p,
                                int grid, cudaStream_t s) {
-  using Cfg = ConvCfg<BN>;
-  static bool attr_set = false;  // per-process; attribute is per function, per device
+  using Cfg = ConvCfg<BN, CG>;
+  auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK>;
+  static bool attr_set = false;  // per process; the attribute is per function
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(sparse_conv3x3_tc_kernel<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return cuda_fail(e);
     attr_set = true;
   }
-  sparse_conv3x3_tc_kernel<BN><<<grid, kThreads, Cfg::kSmem, s>>>(ta, tb, p);
-  SPHINX_CHECK_LAUNCH();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
+}
+
+template <int BN>
+static sphinx_status launch_cg(int cg, const CUtensorMap& ta, const CUtensorMap& tb,
+                               const ConvParams& p, int grid, cudaStream_t s) {
+  if (p.b == 8)
+    return cg == 2 ? launch_bn<BN, 2, 8>(ta, tb, p, grid, s) : launch_bn<BN, 1, 8>(ta, tb, p, grid, s);
+  return cg == 2 ? launch_bn<BN, 2, 4>(ta, tb, p, grid, s) : launch_bn<BN, 1, 4>(ta, tb, p, grid, s);
 }
 
 // Widest tile that minimises padded output columns (ties -> wider).
@@ -355,10 +420,13 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
   }
   const int bn = pick_bn(c_out);
+  // CTA-pair (cta_group::2) unless overridden: halves the weight traffic per SM
+  int cg = 2;
+  if (const char* env = getenv("SPHINX_CONV_CG")) cg = atoi(env) == 1 ? 1 : 2;
   {
     const cuuint64_t dims[3] = {(cuuint64_t)c_in, 9, (cuuint64_t)c_out};
     const cuuint64_t strides[2] = {(cuuint64_t)c_in * 2, (cuuint64_t)9 * c_in * 2};
-    const cuuint32_t box[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)bn};
+    const cuuint32_t box[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)(bn / cg)};
     const cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides,
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -380,14 +448,15 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.kc = cdiv(c_in, kBK);
   p.n_tiles_n = cdiv(c_out, bn);
   p.bpt = kBM / (block * block);
-  const long long max_tiles = (long long)cdiv(capacity, p.bpt) * p.n_tiles_n;
-  const int grid = (int)(max_tiles < sms ? max_tiles : sms);
+  const long long max_tiles = (long long)cdiv(capacity, p.bpt * cg) * p.n_tiles_n;
+  const int max_clusters = sms / cg;
+  const int grid = cg * (int)(max_tiles < max_clusters ? max_tiles : max_clusters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (bn) {
-    case 256: return launch_bn<256>(ta, tb, p, grid, s);
-    case 160: return launch_bn<160>(ta, tb, p, grid, s);
-    case 128: return launch_bn<128>(ta, tb, p, grid, s);
-    case 64: return launch_bn<64>(ta, tb, p, grid, s);
-    default: return launch_bn<32>(ta, tb, p, grid, s);
+    case 256: return launch_cg<256>(cg, ta, tb, p, grid, s);
+    case 160: return launch_cg<160>(cg, ta, tb, p, grid, s);
+    case 128: return launch_cg<128>(cg, ta, tb, p, grid, s);
+    case 64: return launch_cg<64>(cg, ta, tb, p, grid, s);
+    default: return launch_cg<32>(cg, ta, tb, p, grid, s);
   }
 }

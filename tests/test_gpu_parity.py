@@ -166,6 +166,13 @@ def test_noise_vs_oracle(sphinx, shape, b):
 
 # ----------------------------------------------------------------- step 4
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "pair"], autouse=False)
+def conv_cg(request, monkeypatch):
+    """Runs a conv test with the 1-SM (cta_group::1) and the CTA-pair (cta_group::2) kernels."""
+    monkeypatch.setenv("SPHINX_CONV_CG", str(request.param))
+    return request.param
+
+
 def _conv_check(sphinx, n, h, w, cin, cout, b, density, pattern, tag, out_dtype=torch.float32,
                 bias=True, weights=None, x_bits=None, sample_ids=None):
     hb, wb = -(-h // b), -(-w // b)
@@ -196,27 +203,27 @@ def _conv_check(sphinx, n, h, w, cin, cout, b, density, pattern, tag, out_dtype=
     return err, tol
 
 
-def test_conv_config0(sphinx):
+def test_conv_config0(sphinx, conv_cg):
     """configs[0]: 1 frame, 16x16x32, 3x3 32->32, block 4, 25% active."""
     _conv_check(sphinx, 1, 16, 16, 32, 32, 4, 0.25, "scattered", "cfg0")
 
 
 @pytest.mark.parametrize("h,c,pattern,dens", [(72, 320, "clustered", 0.25), (36, 640, "scattered", 0.4),
                                               (18, 1280, "checker", 0.5), (72, 320, "checker", 1.0)])
-def test_conv_unet_levels(sphinx, h, c, pattern, dens):
+def test_conv_unet_levels(sphinx, conv_cg, h, c, pattern, dens):
     """configs[1]/[2] geometries: 72x72x320, 36x36x640 (ragged 5x5 blocks), 18x18x1280."""
     _conv_check(sphinx, 2, h, h, c, c, 8, dens, pattern, f"lvl{h}")
 
 
 @pytest.mark.parametrize("cin,cout,b", [(64, 64, 8), (128, 32, 4), (320, 160, 8), (8, 16, 4),
                                         (96, 264, 8)])
-def test_conv_shapes_bf16_out(sphinx, cin, cout, b):
+def test_conv_shapes_bf16_out(sphinx, conv_cg, cin, cout, b):
     _conv_check(sphinx, 3, 20, 28, cin, cout, b, 0.5, "scattered", f"shape{cin}{cout}",
                 out_dtype=torch.bfloat16)
 
 
 @pytest.mark.parametrize("ky,kx", [(0, 0), (1, 1), (2, 1), (0, 2)])
-def test_conv_shift_kernels_exact(sphinx, ky, kx):
+def test_conv_shift_kernels_exact(sphinx, conv_cg, ky, kx):
     """TV-12/13: a shift kernel reproduces the shifted input exactly, incl. halos across
     blocks (active and inactive neighbours) and zero padding at the border."""
     n, h, w, c, b = 2, 18, 18, 64, 8
@@ -228,7 +235,7 @@ def test_conv_shift_kernels_exact(sphinx, ky, kx):
     assert np.all(err == 0)
 
 
-def test_conv_density_zero_and_count_zero(sphinx):
+def test_conv_density_zero_and_count_zero(sphinx, conv_cg):
     n, h, w, c, b = 1, 16, 16, 32, 4
     g_ids, g_cnt, got = gpu_compact(sphinx, np.zeros((n, 4, 4), np.uint8), None, 0)
     assert len(got) == 0
@@ -238,7 +245,7 @@ def test_conv_density_zero_and_count_zero(sphinx):
     assert torch.all(y == 3.0)
 
 
-def test_conv_full_size_sampled(sphinx):
+def test_conv_full_size_sampled(sphinx, conv_cg):
     """BASELINE configs[3] size at level 1 (168 frames x 72x72x320, 25%): sampled blocks."""
     _conv_check(sphinx, 168, 72, 72, 320, 320, 8, 0.25, "clustered", "full168",
                 sample_ids=lambda m: np.linspace(0, m - 1, 24).astype(int))
