@@ -190,25 +190,30 @@ def summarize_clocks(lines):
             "samples": len(sm)}
 
 
-def time_dense_cudnn(torch, x, w, reps=20):
-    """cuDNN dense 3x3 conv (channels_last bf16, fp32 accumulate) — the dense bar."""
-    xn = x.permute(0, 3, 1, 2)  # NHWC storage viewed as NCHW channels_last
-    wn = w.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
+def graph_time(torch, fn, reps=20):
+    """Device time per call: `reps` calls captured in one CUDA graph and replayed (no host
+    launch overhead in the measurement)."""
     for _ in range(3):
-        torch.nn.functional.conv2d(xn, wn, padding=1)
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
-    for _ in range(reps):
-        torch.nn.functional.conv2d(xn, wn, padding=1)
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
 
 
 def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0.50, 0.75, 1.0)):
-    """configs[1]: 72x72x320, block 8, density sweep (1 frame, and the 21-frame batched variant):
-    own sparse conv vs own dense (all blocks) vs cuDNN dense."""
+    """configs[1]: 72x72x320, block 8, density sweep 5-100% (1 frame, and the 21-frame batched
+    variant): own sparse conv vs own dense launch (all blocks listed) vs cuDNN dense
+    (torch conv2d, channels_last bf16, fp32 accumulate).  Graph-replay device time, L2-warm."""
     h, c = 72, 320
     hb = 9
     out = []
@@ -216,7 +221,10 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0
         x = torch.from_numpy(syn.features_bf16((nf, h, h, c), "sweep").view(np.int16)).view(torch.bfloat16).to(dev)
         w = torch.from_numpy(syn.weights_bf16(c, c, "sweep").view(np.int16)).view(torch.bfloat16).to(dev)
         y = torch.zeros((nf, h, h, c), dtype=torch.bfloat16, device=dev)
-        t_cudnn = time_dense_cudnn(torch, x, w)
+        xn = x.permute(0, 3, 1, 2)
+        wn = w.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
+        t_cudnn = graph_time(torch, lambda: torch.nn.functional.conv2d(xn, wn, padding=1))
+        sp.conv_workspace(c, dev)
         rows = []
         for d in list(dens):
             rg = syn.rng("sweep-mask", nf, d)
@@ -224,17 +232,7 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0
             ids_np = np.flatnonzero(m.ravel()).astype(np.int32)
             ids = torch.from_numpy(ids_np).to(dev)
             cnt = torch.tensor([len(ids_np)], dtype=torch.int32, device=dev)
-            for _ in range(3):
-                sp.sphinx_sparse_conv3x3(x, w, None, y, B, ids, cnt)
-            reps = 20
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(reps):
-                sp.sphinx_sparse_conv3x3(x, w, None, y, B, ids, cnt)
-            e1.record()
-            torch.cuda.synchronize()
-            t = e0.elapsed_time(e1) / reps
+            t = graph_time(torch, lambda: sp.sphinx_sparse_conv3x3(x, w, None, y, B, ids, cnt))
             flops = len(ids_np) * 64 * 2 * 9 * c * c
             rows.append({"density": round(len(ids_np) / (nf * 81), 4), "active_blocks": int(len(ids_np)),
                          "sparse_ms": round(t, 5), "eff_tflops": round(flops / t / 1e9, 2)})
@@ -243,8 +241,11 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0
         for r in rows:
             r["speedup_vs_dense"] = round(t_dense / r["sparse_ms"], 3)
             r["speedup_vs_cudnn"] = round(t_cudnn / r["sparse_ms"], 3)
+            r["efficiency_S_times_d"] = round(r["speedup_vs_dense"] * r["density"], 3)
         out.append({"frames": nf, "shape": [nf, h, h, c], "dense_cudnn_ms": round(t_cudnn, 5),
-                    "dense_own_ms": round(t_own_dense, 5), "rows": rows})
+                    "dense_cudnn_tflops": round(nf * h * h * 2 * 9 * c * c / t_cudnn / 1e9, 1),
+                    "dense_own_ms": round(t_own_dense, 5), "rows": rows,
+                    "timing": "CUDA-graph replay of 20 launches, L2-warm"})
     return out
 
 

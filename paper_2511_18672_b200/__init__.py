@@ -186,9 +186,27 @@ def sphinx_noise_inject(x0, eps, x_t, block, block_ids, count, step, abar, capac
     _chk("sphinx_noise_inject", rc)
 
 
-def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None, stream=None):
+_ws_cache = {}
+
+
+def conv_workspace(c_out, device):
+    """Zero-initialised split-K workspace for convs with c_out output channels on `device`
+    (allocated once and cached; the kernel leaves its counters zeroed).  Memory only."""
+    key = (device, c_out)
+    ws = _ws_cache.get(key)
+    if ws is None:
+        import torch
+        n = int(load().sphinx_conv_workspace_size(1, 1, 1, 8, int(c_out), 8))
+        ws = _ws_cache[key] = torch.zeros(n, dtype=torch.uint8, device=device)
+    return ws
+
+
+def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None, stream=None,
+                          workspace=None):
     """Step 4.  x bf16 NHWC [N,H,W,Cin]; w bf16 [Cout,3,3,Cin]; bias fp32 [Cout] or None;
-    y NHWC [N,H,W,Cout] bf16 or fp32 (only listed blocks are written)."""
+    y NHWC [N,H,W,Cout] bf16 or fp32 (only listed blocks are written).
+    workspace: None = a cached zeroed split-K workspace for this device, False = no split-K,
+    or a caller-owned zero-initialised uint8 CUDA tensor (one per stream)."""
     import torch
     _dev(x, torch.bfloat16, "x")
     _dev(w, torch.bfloat16, "w")
@@ -200,10 +218,13 @@ def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None,
     n, h, wd, cin = x.shape
     cout = w.shape[0]
     cap = block_ids.numel() if capacity is None else capacity
+    if workspace is None:
+        workspace = conv_workspace(cout, y.device)
+    ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
     rc = load().sphinx_sparse_conv3x3(_ptr(x), _ptr(w), _ptr(bias), _ptr(y),
                                       F32 if y.dtype == torch.float32 else BF16,
                                       n, h, wd, cin, cout, int(block), _ptr(block_ids), _ptr(count),
-                                      int(cap), None, 0, _stream(stream))
+                                      int(cap), ws_ptr, ws_bytes, _stream(stream))
     _chk("sphinx_sparse_conv3x3", rc)
 
 

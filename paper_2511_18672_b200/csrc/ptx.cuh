@@ -232,3 +232,17 @@ __device__ __forceinline__ void tc_commit_cg2_mc(uint64_t* bar) {
 }
 
 }  // namespace sphinx
+
+namespace sphinx {
+// 1-D bulk copy global -> shared (async proxy), completion on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+}  // namespace sphinx

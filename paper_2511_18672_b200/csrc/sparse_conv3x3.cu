@@ -50,14 +50,40 @@ struct ConvParams {
   int kc;         // 64-channel chunks per tap
   int n_tiles_n;  // tiles along C_out
   int bpt;        // blocks per 128-row tile = 128 / b^2
+  // split-K workspace (NULL = never split): per-(tile, split) fp32 partial tiles and one
+  // arrival counter per (tile, CTA of the pair); counters are zero between launches.
+  float* ws_part;
+  int32_t* ws_cnt;
+  int ws_slots;    // partial-tile slots available
+  int ws_tiles;    // counter capacity in tiles
 };
+
+// Split-K factor chosen ON THE DEVICE from the device-side tile count (CUDA-graph safe).
+// Splitting is used only when all (tile, split) units fit in ONE round of the co-resident
+// persistent grid (units <= clusters), which makes the split CTAs' rendezvous safe; among
+// those S, minimise ksteps/S + kRedCost (the fixed cost of the partial-tile exchange).
+// Every CTA evaluates the same pure function of the count.
+__device__ __forceinline__ int choose_split(int tiles, int n_clusters, int ksteps, const ConvParams& p) {
+  constexpr int kMinSteps = 4, kRedCost = 6, kMaxSplit = 16;
+  if (p.ws_part == nullptr || tiles <= 0 || tiles > p.ws_tiles || tiles * 2 > n_clusters) return 1;
+  int best = 1, best_cost = ksteps * 1000;
+  for (int sk = 2; sk <= kMaxSplit; ++sk) {
+    if (ksteps / sk < kMinSteps || tiles * sk > n_clusters || tiles * sk > p.ws_slots) break;
+    const int cost = ksteps * 1000 / sk + kRedCost * 1000;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = sk;
+    }
+  }
+  return best;
+}
 
 template <int BN, int CG>
 struct ConvCfg {
   static constexpr int kBNc = BN / CG;  // B rows (output channels) held by this CTA
   static constexpr int kStageB = kBNc * kBK * 2;
   static constexpr int kStageBytes = kStageA + kStageB;
-  static constexpr int kBarBytes = 256;
+  static constexpr int kBarBytes = 256 + kBM * 8;  // barriers + split-K pixel table
   static constexpr int kMaxSmem = 232448;  // 227 KB opt-in per CTA
   static constexpr int kStagesFit = (kMaxSmem - 1024 - kBarBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
@@ -65,7 +91,8 @@ struct ConvCfg {
                                         : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kSmem = 1024 + kStages * kStageBytes + kBarBytes;
   static_assert(kStages >= 3, "pipeline too shallow");
-  static_assert((2 * kStages + 4) * 8 + 4 <= kBarBytes, "barrier area");
+  static_assert((2 * kStages + 5) * 8 + 8 <= 256, "barrier area");
+  static_assert(kStages * kStageBytes >= (kBM + 16) * BN * 4, "split-K staging must fit the ring");
 };
 
 __device__ __forceinline__ void decode_block(int id, int hb, int wb, int& n, int& by, int& bx) {
@@ -73,6 +100,43 @@ __device__ __forceinline__ void decode_block(int id, int hb, int wb, int& n, int
   const int r = id - n * hb * wb;
   by = r / wb;
   bx = r - by * wb;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// 32 consecutive output channels [co, co+32) of one pixel: + bias, fp32 or bf16 store.
+__device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix, int co, float (&v)[32]) {
+  if (p.bias) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (co + i < p.cout) v[i] += __ldg(p.bias + co + i);
+  }
+  if (p.y_f32) {
+    float* yp = static_cast<float*>(p.y) + pix + co;
+#pragma unroll
+    for (int g = 0; g < 32; g += 4)
+      if (co + g < p.cout)
+        *reinterpret_cast<float4*>(yp + g) = make_float4(v[g], v[g + 1], v[g + 2], v[g + 3]);
+  } else {
+    __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + pix + co;
+#pragma unroll
+    for (int g = 0; g < 32; g += 8) {
+      if (co + g < p.cout) {
+        uint4 pk;
+        __nv_bfloat162 t0 = __floats2bfloat162_rn(v[g + 0], v[g + 1]);
+        __nv_bfloat162 t1 = __floats2bfloat162_rn(v[g + 2], v[g + 3]);
+        __nv_bfloat162 t2 = __floats2bfloat162_rn(v[g + 4], v[g + 5]);
+        __nv_bfloat162 t3 = __floats2bfloat162_rn(v[g + 6], v[g + 7]);
+        pk.x = *reinterpret_cast<uint32_t*>(&t0);
+        pk.y = *reinterpret_cast<uint32_t*>(&t1);
+        pk.z = *reinterpret_cast<uint32_t*>(&t2);
+        pk.w = *reinterpret_cast<uint32_t*>(&t3);
+        *reinterpret_cast<uint4*>(yp + g) = pk;
+      }
+    }
+  }
 }
 
 // CG = 1: one CTA per 128 x BN tile, tcgen05.mma.cta_group::1 (M = 128).
@@ -96,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
+  uint64_t* red_bar = tempty + 2;  // split-K partial staging barrier (one use per launch)
+  // split-K: element offset of each tile row's output pixel (-1 = not stored), 8-byte aligned
+  long long* pix_tab = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
@@ -106,8 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int bb = BLK * BLK;
   const int bpt_pair = BPT * CG;  // blocks per (pair) tile
   const int m_tiles = (count + bpt_pair - 1) / bpt_pair;
-  const int total = m_tiles * p.n_tiles_n;
+  const int tiles = m_tiles * p.n_tiles_n;
   const int ksteps = 9 * p.kc;
+  const int nsplit = choose_split(tiles, n_clusters, ksteps, p);
+  const int total = tiles * nsplit;  // work units: (tile, k-split), split fastest
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -120,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
     }
+    mbar_init(red_bar, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -138,8 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_b = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < total; t += n_clusters) {
+      for (int u = cluster_id; u < total; u += n_clusters) {
+        const int t = u / nsplit, sk = u - t * nsplit;
         const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
+        const int ks0 = sk * ksteps / nsplit, ks1 = (sk + 1) * ksteps / nsplit;
         // TMA origin of every block of this CTA's half of the tile (kept in registers)
         int cx[BPT], cy[BPT], cn[BPT];
 #pragma unroll
@@ -153,9 +225,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           cx[i] = bx * BLK - 1;
         }
         const int n0 = nt * BN + rank * Cfg::kBNc;
-        for (int tap = 0; tap < 9; ++tap) {
-          const int dy = tap / 3, dx = tap - 3 * (tap / 3);
-          for (int kc = 0; kc < p.kc; ++kc) {
+        int tap = ks0 / p.kc, kc = ks0 - (ks0 / p.kc) * p.kc;
+        for (int ks = ks0; ks < ks1; ++ks) {
+          {
+            const int dy = tap / 3, dx = tap - 3 * (tap / 3);
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* a_dst = sA + stage * kStageA;
             uint8_t* b_dst = sB + stage * Cfg::kStageB;
@@ -179,6 +252,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               stage = 0;
               phase ^= 1;
             }
+            if (++kc == p.kc) {
+              kc = 0;
+              ++tap;
+            }
           }
         }
       }
@@ -191,11 +268,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster_id; t < total; t += n_clusters) {
+      for (int u = cluster_id; u < total; u += n_clusters) {
+        const int sk = u - (u / nsplit) * nsplit;
+        const int ks0 = sk * ksteps / nsplit, ks1 = (sk + 1) * ksteps / nsplit;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        for (int ks = 0; ks < ksteps; ++ks) {
+        for (int ks = ks0; ks < ks1; ++ks) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * kStageA);
@@ -204,8 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = umma_desc_sw128(a_addr + k * 32, 1024);
             const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 1024);
-            if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc, (ks | k) != 0 ? 1u : 0u);
-            else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc, (ks | k) != 0 ? 1u : 0u);
+            const uint32_t accum = (ks != ks0 || k != 0) ? 1u : 0u;
+            if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc, accum);
+            else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc, accum);
           }
           if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_cg2_mc(&empty[stage]);
           if (++stage == S) {
@@ -226,7 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cluster_id; t < total; t += n_clusters) {
+    for (int u = cluster_id; u < total; u += n_clusters) {
+      const int t = u / nsplit, sk = u - t * nsplit;
       const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
       const int bi = row / bb, pp = row - bi * bb;
       const int j = mt * bpt_pair + rank * BPT + bi;
@@ -239,6 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         valid = (yy < p.h) && (xx < p.w);
         pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
       }
+      float* part = nullptr;
+      if (nsplit > 1)
+        part = p.ws_part + (((size_t)(t * nsplit + sk) * CG + rank) * kBM + row) * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -246,40 +330,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
         tc_wait_ld();
-        const int co = nt * BN + c0;
-        if (valid) {
+        if (nsplit > 1) {
+          // split-K: park this split's fp32 partial row in the workspace
+#pragma unroll
+          for (int g = 0; g < 32; g += 4)
+            __stcg(reinterpret_cast<float4*>(part + c0 + g),
+                   make_float4(__uint_as_float(r[g]), __uint_as_float(r[g + 1]),
+                               __uint_as_float(r[g + 2]), __uint_as_float(r[g + 3])));
+        } else if (valid) {
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (p.bias) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (co + i < p.cout) v[i] += __ldg(p.bias + co + i);
-          }
-          if (p.y_f32) {
-            float* yp = static_cast<float*>(p.y) + pix + co;
-#pragma unroll
-            for (int g = 0; g < 32; g += 4)
-              if (co + g < p.cout)
-                *reinterpret_cast<float4*>(yp + g) = make_float4(v[g], v[g + 1], v[g + 2], v[g + 3]);
-          } else {
-            __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + pix + co;
-#pragma unroll
-            for (int g = 0; g < 32; g += 8) {
-              if (co + g < p.cout) {
-                uint4 pk;
-                __nv_bfloat162 t0 = __floats2bfloat162_rn(v[g + 0], v[g + 1]);
-                __nv_bfloat162 t1 = __floats2bfloat162_rn(v[g + 2], v[g + 3]);
-                __nv_bfloat162 t2 = __floats2bfloat162_rn(v[g + 4], v[g + 5]);
-                __nv_bfloat162 t3 = __floats2bfloat162_rn(v[g + 6], v[g + 7]);
-                pk.x = *reinterpret_cast<uint32_t*>(&t0);
-                pk.y = *reinterpret_cast<uint32_t*>(&t1);
-                pk.z = *reinterpret_cast<uint32_t*>(&t2);
-                pk.w = *reinterpret_cast<uint32_t*>(&t3);
-                *reinterpret_cast<uint4*>(yp + g) = pk;
-              }
-            }
-          }
+          store_row_chunk(p, pix, nt * BN + c0, v);
         }
       }
       tc_fence_before();
@@ -291,6 +353,77 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+      if (nsplit > 1) {
+        // Rendezvous of the nsplit units of tile t (all co-resident in this single round),
+        // then each reduces a 1/nsplit slice of the rows, summing partials in split order
+        // (deterministic), with coalesced float4 loads across the epilogue threads.
+        pix_tab[row] = valid ? (long long)pix : -1ll;
+        __threadfence();
+        named_bar_sync(1, 128);
+        int* arrive = p.ws_cnt + (t * CG + rank) * 2;
+        if (row == 0) {
+          atomicAdd(arrive, 1);
+          int seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
+            if (seen < nsplit) __nanosleep(64);
+          } while (seen < nsplit);
+        }
+        named_bar_sync(1, 128);
+        const int r0 = sk * kBM / nsplit, r1 = (sk + 1) * kBM / nsplit;
+        const uint32_t slice_bytes = (uint32_t)((r1 - r0) * BN * 4);
+        const float* base = p.ws_part + (((size_t)(t * nsplit) * CG + rank) * kBM + r0) * BN;
+        const size_t split_stride = (size_t)CG * kBM * BN;
+        float* stage_buf = reinterpret_cast<float*>(sA);  // the operand ring is idle now
+        if (row == 0) {
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(red_bar, slice_bytes * (uint32_t)nsplit);
+          for (int s2 = 0; s2 < nsplit; ++s2)
+            bulk_g2s(stage_buf + (size_t)s2 * (r1 - r0) * BN, base + s2 * split_stride, slice_bytes,
+                     red_bar);
+        }
+        mbar_wait(red_bar, 0);
+        constexpr int kV = BN / 4;  // float4 per row
+        const int n_el = (r1 - r0) * kV;
+        const float4* sb = reinterpret_cast<const float4*>(stage_buf);
+        for (int e = row; e < n_el; e += 128) {
+          const int rr = r0 + e / kV, c4 = e - (e / kV) * kV;
+          const long long px = pix_tab[rr];
+          if (px < 0) continue;
+          float4 acc4 = sb[e];
+          for (int s2 = 1; s2 < nsplit; ++s2) {
+            const float4 a = sb[s2 * n_el + e];
+            acc4.x += a.x; acc4.y += a.y; acc4.z += a.z; acc4.w += a.w;
+          }
+          const int co = nt * BN + c4 * 4;
+          if (co < p.cout) {
+            if (p.bias) {
+              acc4.x += __ldg(p.bias + co); acc4.y += __ldg(p.bias + co + 1);
+              acc4.z += __ldg(p.bias + co + 2); acc4.w += __ldg(p.bias + co + 3);
+            }
+            if (p.y_f32) {
+              *reinterpret_cast<float4*>(static_cast<float*>(p.y) + px + co) = acc4;
+            } else {
+              __nv_bfloat162 t0 = __floats2bfloat162_rn(acc4.x, acc4.y);
+              __nv_bfloat162 t1 = __floats2bfloat162_rn(acc4.z, acc4.w);
+              uint2 pk;
+              pk.x = *reinterpret_cast<uint32_t*>(&t0);
+              pk.y = *reinterpret_cast<uint32_t*>(&t1);
+              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.y) + px + co) = pk;
+            }
+          }
+        }
+        // departure: the last unit to leave re-zeroes both counters for the next launch
+        named_bar_sync(1, 128);
+        if (row == 0) {
+          const int old = atomicAdd(arrive + 1, 1);
+          if (old == nsplit - 1) {
+            arrive[0] = 0;
+            arrive[1] = 0;
+            __threadfence();
+          }
+        }
       }
     }
   }
@@ -378,9 +511,23 @@ static int pick_bn(int cout) {
 
 using namespace sphinx;
 
-extern "C" size_t sphinx_conv_workspace_size(int32_t, int32_t, int32_t, int32_t, int32_t,
-                                             int32_t) {
-  return 0;
+// Split-K workspace: [kCntBytes of int32 arrival counters][partial-tile slots].
+constexpr size_t kCntBytes = 4096;
+
+static size_t slot_bytes(int cg, int bn) { return (size_t)cg * kBM * bn * sizeof(float); }
+
+extern "C" size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, int32_t c_in,
+                                             int32_t c_out, int32_t block) {
+  (void)n; (void)h; (void)w_; (void)c_in; (void)block;
+  if (c_out <= 0) return 0;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+  }
+  // one slot per SM (two rounds of CTA pairs), sized for the CTA-pair kernel
+  return kCntBytes + (size_t)sms * slot_bytes(2, pick_bn(c_out));
 }
 
 extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, const float* bias,
@@ -390,9 +537,8 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
                                                const int32_t* count, int32_t capacity,
                                                void* workspace, size_t workspace_bytes,
                                                sphinx_stream_t stream) {
-  (void)workspace;
-  (void)workspace_bytes;
   if (!x || !w || !y || !block_ids || !count) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u)) return SPHINX_ERR_INVALID_ARGUMENT;
   if (n <= 0 || h <= 0 || w_ <= 0 || c_in <= 0 || c_out <= 0 || block <= 0 || capacity < 0)
     return SPHINX_ERR_INVALID_ARGUMENT;
   if (y_dtype != SPHINX_BF16 && y_dtype != SPHINX_F32) return SPHINX_ERR_INVALID_ARGUMENT;
@@ -448,9 +594,22 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.kc = cdiv(c_in, kBK);
   p.n_tiles_n = cdiv(c_out, bn);
   p.bpt = kBM / (block * block);
+  p.ws_part = nullptr;
+  p.ws_cnt = nullptr;
+  p.ws_slots = 0;
+  p.ws_tiles = 0;
+  bool allow_split = true;
+  if (const char* env = getenv("SPHINX_CONV_SPLIT")) allow_split = atoi(env) != 0;
+  if (allow_split && workspace && workspace_bytes >= kCntBytes + slot_bytes(cg, bn)) {
+    p.ws_cnt = static_cast<int32_t*>(workspace);
+    p.ws_part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kCntBytes);
+    p.ws_slots = (int)((workspace_bytes - kCntBytes) / slot_bytes(cg, bn));
+    p.ws_tiles = (int)(kCntBytes / (2 * sizeof(int32_t))) / cg;
+  }
   const long long max_tiles = (long long)cdiv(capacity, p.bpt * cg) * p.n_tiles_n;
   const int max_clusters = sms / cg;
-  const int grid = cg * (int)(max_tiles < max_clusters ? max_tiles : max_clusters);
+  const long long want = p.ws_part ? max_tiles * 16 : max_tiles;  // split-K may multiply units
+  const int grid = cg * (int)(want < max_clusters ? want : max_clusters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (bn) {
     case 256: return launch_cg<256>(cg, ta, tb, p, grid, s);

@@ -166,10 +166,13 @@ def test_noise_vs_oracle(sphinx, shape, b):
 
 # ----------------------------------------------------------------- step 4
 
-@pytest.fixture(params=[1, 2], ids=["cta1", "pair"], autouse=False)
+@pytest.fixture(params=[(1, 0), (2, 0), (1, 1), (2, 1)], ids=["cta1", "pair", "cta1-splitk", "pair-splitk"])
 def conv_cg(request, monkeypatch):
-    """Runs a conv test with the 1-SM (cta_group::1) and the CTA-pair (cta_group::2) kernels."""
-    monkeypatch.setenv("SPHINX_CONV_CG", str(request.param))
+    """Runs a conv test with the 1-SM (cta_group::1) and the CTA-pair (cta_group::2) kernels,
+    each without and with device-chosen split-K."""
+    cg, split = request.param
+    monkeypatch.setenv("SPHINX_CONV_CG", str(cg))
+    monkeypatch.setenv("SPHINX_CONV_SPLIT", str(split))
     return request.param
 
 
@@ -243,6 +246,29 @@ def test_conv_density_zero_and_count_zero(sphinx, conv_cg):
     sphinx.sphinx_sparse_conv3x3(bf16(syn.features_bf16((n, h, w, c), "z")),
                                  bf16(syn.weights_bf16(c, c, "z")), None, y, b, g_ids, g_cnt)
     assert torch.all(y == 3.0)
+
+
+def test_conv_deterministic_and_split_consistent(sphinx, monkeypatch):
+    """S:350 bit-reproducible; split-K (fixed-order fp32 reduction) agrees with one pass
+    within the conv tolerance on a latency-bound shape where the device picks S > 1."""
+    n, h, c, b = 1, 18, 1280, 8
+    x = bf16(syn.features_bf16((n, h, h, c), "det"))
+    w = bf16(syn.weights_bf16(c, c, "det"))
+    m = np.zeros((n, 3, 3), np.uint8); m[0, 0, :] = 1; m[0, 2, 2] = 1
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, None, 0)
+    outs = []
+    for split in ("1", "1", "0"):
+        monkeypatch.setenv("SPHINX_CONV_SPLIT", split)
+        y = torch.zeros((n, h, h, c), dtype=torch.float32, device=dev)
+        sphinx.sphinx_sparse_conv3x3(x, w, None, y, b, g_ids, g_cnt)
+        outs.append(y.cpu().numpy())
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    xb = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    wb = w.view(torch.int16).cpu().numpy().view(np.uint16)
+    want, acc = oracle.conv3x3_blocks(xb, wb, None, b, oracle.compact(m))
+    listed = ~np.isnan(want[..., 0])
+    for o in outs:
+        assert np.all(np.abs(o[listed] - want[listed]) <= 1e-3 * acc[listed] + 1e-6)
 
 
 def test_conv_full_size_sampled(sphinx, conv_cg):

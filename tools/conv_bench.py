@@ -17,13 +17,19 @@ import synthetic as syn  # noqa: E402
 
 
 def timed(fn, reps):
+    """Device time per launch: `reps` launches captured in one CUDA graph, replayed."""
     for _ in range(3):
         fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
-    for _ in range(reps):
-        fn()
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
@@ -36,6 +42,7 @@ def main():
     ap.add_argument("--dens", type=float, nargs="+", default=[0.05, 0.1, 0.25, 0.5, 1.0])
     ap.add_argument("--levels", type=int, nargs="+", default=[0, 1, 2])
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--split", type=int, nargs="+", default=[0, 1])
     a = ap.parse_args()
     sp.load()
     dev = torch.device("cuda")
@@ -51,6 +58,7 @@ def main():
             xn = x.permute(0, 3, 1, 2)
             wn = w.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
             t_cudnn = timed(lambda: torch.nn.functional.conv2d(xn, wn, padding=1), a.reps)
+            sp.conv_workspace(c, dev)
             dense_flops = nf * h * h * 2 * 9 * c * c
             for d in a.dens:
                 rg = syn.rng("mbmask", nf, li, d)
@@ -63,11 +71,13 @@ def main():
                 ids = torch.from_numpy(ids_np).to(dev)
                 cnt = torch.tensor([len(ids_np)], dtype=torch.int32, device=dev)
                 for cg in a.cg:
+                  for split in a.split:
                     os.environ["SPHINX_CONV_CG"] = str(cg)
+                    os.environ["SPHINX_CONV_SPLIT"] = str(split)
                     t = timed(lambda: sp.sphinx_sparse_conv3x3(x, w, None, y, 8, ids, cnt), a.reps)
                     f = px * 2 * 9 * c * c
                     print(json.dumps({"frames": nf, "level": li, "shape": [h, c], "density": round(len(ids_np) / (nf * hb * hb), 3),
-                                      "cg": cg, "ms": round(t, 5), "eff_tflops": round(f / t / 1e9, 1),
+                                      "cg": cg, "split": split, "ms": round(t, 5), "eff_tflops": round(f / t / 1e9, 1),
                                       "cudnn_ms": round(t_cudnn, 5), "cudnn_tflops": round(dense_flops / t_cudnn / 1e9, 1),
                                       "speedup_vs_cudnn": round(t_cudnn / t, 3)}), flush=True)
 
