@@ -137,13 +137,15 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
 
 // UMMA shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B
 // (64 bf16 of K), 8-row core groups at stride `sbo_bytes`, version 1 (sm_100).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t sbo_bytes) {
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t sbo_bytes,
+                                                    uint32_t bo_mode = 1) {
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);          // start address   [0,14)
   d |= (uint64_t)(1) << 16;                             // LBO (unused for SW128 K-major) [16,30)
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;     // SBO             [32,46)
   d |= (uint64_t)1 << 46;                               // version = 1     [46,48)
-  d |= (uint64_t)((smem_addr >> 7) & 0x7) << 49;        // base offset     [49,52)
+  if (bo_mode == 1) d |= (uint64_t)((smem_addr >> 7) & 0x7) << 49;  // base offset [49,52)
+  if (bo_mode == 2) d |= (uint64_t)1 << 52;             // lbo mode = 1 (absolute) [52]
   d |= (uint64_t)2 << 61;                               // SWIZZLE_128B    [61,64)
   return d;
 }

@@ -56,6 +56,8 @@ struct ConvParams {
   int32_t* ws_cnt;
   int ws_slots;    // partial-tile slots available
   int ws_tiles;    // counter capacity in tiles
+  int halo;        // 1: halo-staged A operand (b = 8)
+  uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
 };
 
 // Split-K factor chosen ON THE DEVICE from the device-side tile count (CUDA-graph safe).
@@ -63,8 +65,10 @@ struct ConvParams {
 // persistent grid (units <= clusters), which makes the split CTAs' rendezvous safe; among
 // those S, minimise ksteps/S + kRedCost (the fixed cost of the partial-tile exchange).
 // Every CTA evaluates the same pure function of the count.
-__device__ __forceinline__ int choose_split(int tiles, int n_clusters, int ksteps, const ConvParams& p) {
-  constexpr int kMinSteps = 4, kRedCost = 6, kMaxSplit = 16;
+__device__ __forceinline__ int choose_split(int tiles, int n_clusters, int ksteps, int max_split,
+                                           const ConvParams& p) {
+  constexpr int kMinSteps = 4, kRedCost = 6;
+  const int kMaxSplit = max_split < 16 ? max_split : 16;
   if (p.ws_part == nullptr || tiles <= 0 || tiles > p.ws_tiles || tiles * 2 > n_clusters) return 1;
   int best = 1, best_cost = ksteps * 1000;
   for (int sk = 2; sk <= kMaxSplit; ++sk) {
@@ -78,21 +82,37 @@ __device__ __forceinline__ int choose_split(int tiles, int n_clusters, int kstep
   return best;
 }
 
-template <int BN, int CG>
+// Shared-memory plan.  Per-tap mode (HALO = false): a ring of kStages stages, each the A tile
+// of one (tap, 64-ch chunk) [128 rows x 128 B] plus its B tile [BN/CG rows x 128 B].
+// Halo mode (HALO = true, b = 8): an A ring of kANum slots, each holding the (b+2)^2 halos of
+// the CTA's BPT blocks for one 64-ch chunk, stored as halo rows of 10 px in 2048-B slots
+// ordered [y][block] (so the 8-row UMMA core groups are 1024-B aligned at stride 2048 and a
+// tap (dy,dx) is the start shift dy*BPT*2048 + dx*128), plus a B ring of kBNum (tap, chunk) tiles.
+template <int BN, int CG, bool HALO>
 struct ConvCfg {
   static constexpr int kBNc = BN / CG;  // B rows (output channels) held by this CTA
   static constexpr int kStageB = kBNc * kBK * 2;
   static constexpr int kStageBytes = kStageA + kStageB;
-  static constexpr int kBarBytes = 256 + kBM * 8;  // barriers + split-K pixel table
-  static constexpr int kMaxSmem = 232448;  // 227 KB opt-in per CTA
-  static constexpr int kStagesFit = (kMaxSmem - 1024 - kBarBytes) / kStageBytes;
+  static constexpr int kBarBytes = 512 + kBM * 8;  // barriers + split-K pixel table
+  static constexpr int kMaxSmem = 232448;          // 227 KB opt-in per CTA
+  static constexpr int kAvail = kMaxSmem - 1024 - kBarBytes;
+  // per-tap mode
+  static constexpr int kStagesFit = kAvail / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  // halo mode (BPT = 2 blocks of 8x8)
+  static constexpr int kHaloRow = 2048;
+  static constexpr int kASlot = 10 * 2 * kHaloRow;
+  static constexpr int kANum = 2;
+  static constexpr int kBNumFit = (kAvail - kANum * kASlot) / kStageB;
+  static constexpr int kBNum = kBNumFit > 16 ? 16 : kBNumFit;
+  static constexpr int kRingBytes = HALO ? kANum * kASlot + kBNum * kStageB : kStages * kStageBytes;
+  static constexpr int kNumBars = HALO ? kANum + kBNum : kStages;
   static constexpr uint32_t kTmemCols = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int kSmem = 1024 + kStages * kStageBytes + kBarBytes;
-  static_assert(kStages >= 3, "pipeline too shallow");
-  static_assert((2 * kStages + 5) * 8 + 8 <= 256, "barrier area");
-  static_assert(kStages * kStageBytes >= (kBM + 16) * BN * 4, "split-K staging must fit the ring");
+  static constexpr int kSmem = 1024 + kRingBytes + kBarBytes;
+  static_assert(HALO ? kBNum >= 4 : kStages >= 3, "pipeline too shallow");
+  static_assert((2 * kNumBars + 5) * 8 + 8 <= 512, "barrier area");
+  static_assert(kRingBytes >= (kBM + 16) * BN * 4, "split-K staging must fit the ring");
 };
 
 __device__ __forceinline__ void decode_block(int id, int hb, int wb, int& n, int& by, int& bx) {
@@ -145,25 +165,27 @@ __device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix,
 //   (rank 0) waits for both halves on its full barrier and issues the MMAs; commits are
 //   multicast to both CTAs' barriers; each CTA's epilogue drains its own TMEM lanes and
 //   arrives on the leader's accumulator-empty barrier.  B traffic per SM halves.
-template <int BN, int CG, int BLK>
+template <int BN, int CG, int BLK, bool HALO>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB, const ConvParams p) {
-  using Cfg = ConvCfg<BN, CG>;
+  using Cfg = ConvCfg<BN, CG, HALO>;
+  static_assert(!HALO || BLK == 8, "halo staging needs 8x8 blocks");
   constexpr int S = Cfg::kStages;
+  constexpr int NB = Cfg::kNumBars;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + S * kStageA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * Cfg::kStageB);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
+  uint8_t* sB = smem + (HALO ? Cfg::kANum * Cfg::kASlot : S * kStageA);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes);
+  uint64_t* empty = full + NB;
+  uint64_t* tfull = empty + NB;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
   uint64_t* red_bar = tempty + 2;  // split-K partial staging barrier (one use per launch)
   // split-K: element offset of each tile row's output pixel (-1 = not stored), 8-byte aligned
-  long long* pix_tab = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(full) + 256);
+  long long* pix_tab = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(full) + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
@@ -175,13 +197,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int m_tiles = (count + bpt_pair - 1) / bpt_pair;
   const int tiles = m_tiles * p.n_tiles_n;
   const int ksteps = 9 * p.kc;
-  const int nsplit = choose_split(tiles, n_clusters, ksteps, p);
+  // halo mode splits K at 64-channel chunk boundaries (all 9 taps of a chunk stay together)
+  const int nsplit = choose_split(tiles, n_clusters, ksteps, HALO ? p.kc : 16, p);
   const int total = tiles * nsplit;  // work units: (tile, k-split), split fastest
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < NB; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -208,6 +231,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_b = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      if constexpr (HALO) {
+        int bs = 0;  // B ring position
+        uint32_t bph = 0;
+        for (int u = cluster_id; u < total; u += n_clusters) {
+          const int t = u / nsplit, sk = u - t * nsplit;
+          const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
+          const int kc0 = sk * p.kc / nsplit, kc1 = (sk + 1) * p.kc / nsplit;
+          int cx[BPT], cy[BPT], cn[BPT];
+#pragma unroll
+          for (int i = 0; i < BPT; ++i) {
+            const int j = min(mt * bpt_pair + rank * BPT + i, count - 1);
+            int n, by, bx;
+            decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
+            cn[i] = n;
+            cy[i] = by * BLK - 1;
+            cx[i] = bx * BLK - 1;
+          }
+          const int n0 = nt * BN + rank * Cfg::kBNc;
+          constexpr uint32_t kABytes = BPT * 10 * 10 * 128;  // real halo bytes per CTA
+          for (int kc = kc0; kc < kc1; ++kc) {
+            // A: the chunk's halos, one TMA row box {64 ch, 10 px} per halo row per block
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* a_dst = sA + stage * Cfg::kASlot;
+            if constexpr (CG == 1) {
+              mbar_arrive_expect_tx(&full[stage], kABytes);
+#pragma unroll
+              for (int yy = 0; yy < 10; ++yy)
+#pragma unroll
+                for (int i = 0; i < BPT; ++i)
+                  tma_load_4d(&tmA, &full[stage], a_dst + (yy * BPT + i) * Cfg::kHaloRow, kc * kBK,
+                              cx[i], cy[i] + yy, cn[i], pol_a);
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kABytes);
+              const uint32_t bar = leader_addr(&full[stage]);
+#pragma unroll
+              for (int yy = 0; yy < 10; ++yy)
+#pragma unroll
+                for (int i = 0; i < BPT; ++i)
+                  tma_load_4d_cg2(&tmA, bar, a_dst + (yy * BPT + i) * Cfg::kHaloRow, kc * kBK,
+                                  cx[i], cy[i] + yy, cn[i], pol_a);
+            }
+            if (++stage == Cfg::kANum) {
+              stage = 0;
+              phase ^= 1;
+            }
+            // B: one (tap, chunk) weight tile per tap
+            for (int tap = 0; tap < 9; ++tap) {
+              uint64_t* bf = &full[Cfg::kANum + bs];
+              mbar_wait(&empty[Cfg::kANum + bs], bph ^ 1);
+              uint8_t* b_dst = sB + bs * Cfg::kStageB;
+              if constexpr (CG == 1) {
+                mbar_arrive_expect_tx(bf, (uint32_t)Cfg::kStageB);
+                tma_load_3d(&tmB, bf, b_dst, kc * kBK, tap, n0, pol_b);
+              } else {
+                if (rank == 0) mbar_arrive_expect_tx(bf, (uint32_t)(2 * Cfg::kStageB));
+                tma_load_3d_cg2(&tmB, leader_addr(bf), b_dst, kc * kBK, tap, n0, pol_b);
+              }
+              if (++bs == Cfg::kBNum) {
+                bs = 0;
+                bph ^= 1;
+              }
+            }
+          }
+        }
+      } else
       for (int u = cluster_id; u < total; u += n_clusters) {
         const int t = u / nsplit, sk = u - t * nsplit;
         const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
@@ -268,6 +356,54 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      if constexpr (HALO) {
+        int bs = 0;
+        uint32_t bph = 0;
+        for (int u = cluster_id; u < total; u += n_clusters) {
+          const int sk = u - (u / nsplit) * nsplit;
+          const int kc0 = sk * p.kc / nsplit, kc1 = (sk + 1) * p.kc / nsplit;
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+          for (int kc = kc0; kc < kc1; ++kc) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a_base = smem_u32(sA + stage * Cfg::kASlot);
+            for (int tap = 0; tap < 9; ++tap) {
+              const int dy = tap / 3, dx = tap - 3 * (tap / 3);
+              mbar_wait(&full[Cfg::kANum + bs], bph);
+              tc_fence_after();
+              // tap (dy,dx): group g = 2*py + block at a_start + g*2048, row k = pixel px + dx
+              const uint32_t a_start = a_base + (uint32_t)(dy * BPT * Cfg::kHaloRow + dx * 128);
+              const uint32_t b_addr = smem_u32(sB + bs * Cfg::kStageB);
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k) {
+                const uint64_t ad = umma_desc_sw128(a_start + k * 32, Cfg::kHaloRow, p.desc_bo);
+                const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 1024);
+                const uint32_t accum = (kc != kc0 || tap != 0 || k != 0) ? 1u : 0u;
+                if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc, accum);
+                else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc, accum);
+              }
+              if constexpr (CG == 1) tc_commit(&empty[Cfg::kANum + bs]);
+              else tc_commit_cg2_mc(&empty[Cfg::kANum + bs]);
+              if (++bs == Cfg::kBNum) {
+                bs = 0;
+                bph ^= 1;
+              }
+            }
+            if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_cg2_mc(&empty[stage]);
+            if (++stage == Cfg::kANum) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          if constexpr (CG == 1) tc_commit(&tfull[acc]); else tc_commit_cg2_mc(&tfull[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+      } else
       for (int u = cluster_id; u < total; u += n_clusters) {
         const int sk = u - (u / nsplit) * nsplit;
         const int ks0 = sk * ksteps / nsplit, ks1 = (sk + 1) * ksteps / nsplit;
@@ -309,14 +445,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = cluster_id; u < total; u += n_clusters) {
       const int t = u / nsplit, sk = u - t * nsplit;
       const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
-      const int bi = row / bb, pp = row - bi * bb;
+      // tile row -> (block, pixel): per-tap mode rows are block-major (b^2 rows per block);
+      // halo mode rows are [py][block][px] (8-row groups g = py*BPT + block)
+      const int bi = HALO ? (row >> 3) % BPT : row / bb;
+      const int ry = HALO ? (row >> 3) / BPT : (row - bi * bb) / BLK;
+      const int rx = HALO ? (row & 7) : (row - bi * bb) % BLK;
       const int j = mt * bpt_pair + rank * BPT + bi;
       bool valid = (bi < BPT) && (j < count);
       size_t pix = 0;
       if (valid) {
         int n, by, bx;
         decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
-        const int yy = by * BLK + pp / BLK, xx = bx * BLK + pp % BLK;
+        const int yy = by * BLK + ry, xx = bx * BLK + rx;
         valid = (yy < p.h) && (xx < p.w);
         pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
       }
@@ -457,11 +597,11 @@ static PFN_encodeTiled_t get_encode_tiled() {
   return fn;
 }
 
-template <int BN, int CG, int BLK>
+template <int BN, int CG, int BLK, bool HALO>
 static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p,
                                int grid, cudaStream_t s) {
-  using Cfg = ConvCfg<BN, CG>;
-  auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK>;
+  using Cfg = ConvCfg<BN, CG, HALO>;
+  auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK, HALO>;
   static bool attr_set = false;  // per process; the attribute is per function
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
@@ -488,9 +628,14 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
 template <int BN>
 static sphinx_status launch_cg(int cg, const CUtensorMap& ta, const CUtensorMap& tb,
                                const ConvParams& p, int grid, cudaStream_t s) {
+  if (p.b == 8 && p.halo)
+    return cg == 2 ? launch_bn<BN, 2, 8, true>(ta, tb, p, grid, s)
+                   : launch_bn<BN, 1, 8, true>(ta, tb, p, grid, s);
   if (p.b == 8)
-    return cg == 2 ? launch_bn<BN, 2, 8>(ta, tb, p, grid, s) : launch_bn<BN, 1, 8>(ta, tb, p, grid, s);
-  return cg == 2 ? launch_bn<BN, 2, 4>(ta, tb, p, grid, s) : launch_bn<BN, 1, 4>(ta, tb, p, grid, s);
+    return cg == 2 ? launch_bn<BN, 2, 8, false>(ta, tb, p, grid, s)
+                   : launch_bn<BN, 1, 8, false>(ta, tb, p, grid, s);
+  return cg == 2 ? launch_bn<BN, 2, 4, false>(ta, tb, p, grid, s)
+                 : launch_bn<BN, 1, 4, false>(ta, tb, p, grid, s);
 }
 
 // Widest tile that minimises padded output columns (ties -> wider).
@@ -553,22 +698,27 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   PFN_encodeTiled_t enc = get_encode_tiled();
   if (!enc) return cuda_fail(cudaErrorNotSupported);
 
+  const int bn = pick_bn(c_out);
+  // CTA-pair (cta_group::2) unless overridden: halves the weight traffic per SM
+  int cg = 2;
+  if (const char* env = getenv("SPHINX_CONV_CG")) cg = atoi(env) == 1 ? 1 : 2;
+  // halo-staged A for 8x8 blocks unless overridden: each activation read once per chunk
+  int halo = block == 8 ? 1 : 0;
+  if (const char* env = getenv("SPHINX_CONV_HALO")) halo = halo && atoi(env) != 0;
   CUtensorMap ta, tb;
   {
     const cuuint64_t dims[4] = {(cuuint64_t)c_in, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
     const cuuint64_t strides[3] = {(cuuint64_t)c_in * 2, (cuuint64_t)w_ * c_in * 2,
                                    (cuuint64_t)h * w_ * c_in * 2};
-    const cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)block, (cuuint32_t)block, 1};
+    // per-tap: the b x b block window; halo: one halo row of b+2 pixels
+    const cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)(halo ? block + 2 : block),
+                               (cuuint32_t)(halo ? 1 : block), 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
   }
-  const int bn = pick_bn(c_out);
-  // CTA-pair (cta_group::2) unless overridden: halves the weight traffic per SM
-  int cg = 2;
-  if (const char* env = getenv("SPHINX_CONV_CG")) cg = atoi(env) == 1 ? 1 : 2;
   {
     const cuuint64_t dims[3] = {(cuuint64_t)c_in, 9, (cuuint64_t)c_out};
     const cuuint64_t strides[2] = {(cuuint64_t)c_in * 2, (cuuint64_t)9 * c_in * 2};
@@ -594,6 +744,9 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.kc = cdiv(c_in, kBK);
   p.n_tiles_n = cdiv(c_out, bn);
   p.bpt = kBM / (block * block);
+  p.halo = halo;
+  p.desc_bo = 0;  // measured: the SW128 phase comes from absolute smem address bits
+  if (const char* env = getenv("SPHINX_DESC_BO")) p.desc_bo = (uint32_t)atoi(env);
   p.ws_part = nullptr;
   p.ws_cnt = nullptr;
   p.ws_slots = 0;

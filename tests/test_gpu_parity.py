@@ -166,13 +166,15 @@ def test_noise_vs_oracle(sphinx, shape, b):
 
 # ----------------------------------------------------------------- step 4
 
-@pytest.fixture(params=[(1, 0), (2, 0), (1, 1), (2, 1)], ids=["cta1", "pair", "cta1-splitk", "pair-splitk"])
+@pytest.fixture(params=[(1, 0, 1), (2, 0, 1), (1, 1, 1), (2, 1, 1), (2, 0, 0), (2, 1, 0)],
+                ids=["cta1", "pair", "cta1-splitk", "pair-splitk", "pair-pertap", "pair-pertap-splitk"])
 def conv_cg(request, monkeypatch):
     """Runs a conv test with the 1-SM (cta_group::1) and the CTA-pair (cta_group::2) kernels,
-    each without and with device-chosen split-K."""
-    cg, split = request.param
+    without and with device-chosen split-K, with halo-staged (b=8 default) and per-tap A."""
+    cg, split, halo = request.param
     monkeypatch.setenv("SPHINX_CONV_CG", str(cg))
     monkeypatch.setenv("SPHINX_CONV_SPLIT", str(split))
+    monkeypatch.setenv("SPHINX_CONV_HALO", str(halo))
     return request.param
 
 

@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--levels", type=int, nargs="+", default=[0, 1, 2])
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--split", type=int, nargs="+", default=[0, 1])
+    ap.add_argument("--halo", type=int, nargs="+", default=[1])
     a = ap.parse_args()
     sp.load()
     dev = torch.device("cuda")
@@ -72,12 +73,14 @@ def main():
                 cnt = torch.tensor([len(ids_np)], dtype=torch.int32, device=dev)
                 for cg in a.cg:
                   for split in a.split:
+                   for halo in a.halo:
+                    os.environ["SPHINX_CONV_HALO"] = str(halo)
                     os.environ["SPHINX_CONV_CG"] = str(cg)
                     os.environ["SPHINX_CONV_SPLIT"] = str(split)
                     t = timed(lambda: sp.sphinx_sparse_conv3x3(x, w, None, y, 8, ids, cnt), a.reps)
                     f = px * 2 * 9 * c * c
                     print(json.dumps({"frames": nf, "level": li, "shape": [h, c], "density": round(len(ids_np) / (nf * hb * hb), 3),
-                                      "cg": cg, "split": split, "ms": round(t, 5), "eff_tflops": round(f / t / 1e9, 1),
+                                      "cg": cg, "split": split, "halo": halo, "ms": round(t, 5), "eff_tflops": round(f / t / 1e9, 1),
                                       "cudnn_ms": round(t_cudnn, 5), "cudnn_tflops": round(dense_flops / t_cudnn / 1e9, 1),
                                       "speedup_vs_cudnn": round(t_cudnn / t, 3)}), flush=True)
 
