@@ -224,7 +224,7 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0
         xn = x.permute(0, 3, 1, 2)
         wn = w.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
         t_cudnn = graph_time(torch, lambda: torch.nn.functional.conv2d(xn, wn, padding=1))
-        sp.conv_workspace(c, dev)
+        sp.conv_workspace(c, dev, nf, h, h, B)
         rows = []
         for d in list(dens):
             rg = syn.rng("sweep-mask", nf, d)

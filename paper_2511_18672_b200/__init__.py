@@ -189,15 +189,16 @@ def sphinx_noise_inject(x0, eps, x_t, block, block_ids, count, step, abar, capac
 _ws_cache = {}
 
 
-def conv_workspace(c_out, device):
-    """Zero-initialised split-K workspace for convs with c_out output channels on `device`
-    (allocated once and cached; the kernel leaves its counters zeroed).  Memory only."""
-    key = (device, c_out)
+def conv_workspace(c_out, device, n=1, h=1, w=1, block=8):
+    """Zero-initialised workspace (split-K counters + partial tiles, edge-class plan) for a conv
+    of this geometry on `device`, allocated once and cached (the kernel leaves its counters
+    zeroed).  Memory only: no computation happens here."""
+    key = (device, c_out, n, h, w, block)
     ws = _ws_cache.get(key)
     if ws is None:
         import torch
-        n = int(load().sphinx_conv_workspace_size(1, 1, 1, 8, int(c_out), 8))
-        ws = _ws_cache[key] = torch.zeros(n, dtype=torch.uint8, device=device)
+        nbytes = int(load().sphinx_conv_workspace_size(int(n), int(h), int(w), 8, int(c_out), int(block)))
+        ws = _ws_cache[key] = torch.zeros(nbytes, dtype=torch.uint8, device=device)
     return ws
 
 
@@ -219,7 +220,7 @@ def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None,
     cout = w.shape[0]
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = conv_workspace(cout, y.device)
+        workspace = conv_workspace(cout, y.device, n, h, wd, block)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
     rc = load().sphinx_sparse_conv3x3(_ptr(x), _ptr(w), _ptr(bias), _ptr(y),
                                       F32 if y.dtype == torch.float32 else BF16,

@@ -248,3 +248,15 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 }  // namespace sphinx
+
+namespace sphinx {
+// 4-D TMA load with the completion mbarrier given as a shared::cluster address.
+__device__ __forceinline__ void tma_load_4d_bar(const CUtensorMap* m, uint32_t bar, void* dst, int c0,
+                                                int c1, int c2, int c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+      : "memory");
+}
+}  // namespace sphinx

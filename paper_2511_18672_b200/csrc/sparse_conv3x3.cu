@@ -57,6 +57,12 @@ struct ConvParams {
   int ws_slots;    // partial-tile slots available
   int ws_tiles;    // counter capacity in tiles
   int halo;        // 1: halo-staged A operand (b = 8)
+  // edge-class packing (halo mode, H % 8 or W % 8 != 0): the plan kernel writes the list
+  // partitioned into full / bottom-edge / right-edge blocks (each ascending) and the counts
+  const int32_t* plan_ids;   // [capacity] or NULL (no plan: every block is "full")
+  const int32_t* plan_meta;  // [3] = {n_full, n_bottom, n_right}
+  int rb, cr;                // valid rows of bottom-edge blocks, valid cols of right-edge blocks
+  int bpt_b, bpt_r;          // blocks per CTA tile of the two edge classes
   uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
 };
 
@@ -88,7 +94,7 @@ __device__ __forceinline__ int choose_split(int tiles, int n_clusters, int kstep
 // the CTA's BPT blocks for one 64-ch chunk, stored as halo rows of 10 px in 2048-B slots
 // ordered [y][block] (so the 8-row UMMA core groups are 1024-B aligned at stride 2048 and a
 // tap (dy,dx) is the start shift dy*BPT*2048 + dx*128), plus a B ring of kBNum (tap, chunk) tiles.
-template <int BN, int CG, bool HALO>
+template <int BN, int CG, bool HALO, bool EDGE = false>
 struct ConvCfg {
   static constexpr int kBNc = BN / CG;  // B rows (output channels) held by this CTA
   static constexpr int kStageB = kBNc * kBK * 2;
@@ -101,7 +107,8 @@ struct ConvCfg {
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   // halo mode (BPT = 2 blocks of 8x8)
   static constexpr int kHaloRow = 2048;
-  static constexpr int kASlot = 10 * 2 * kHaloRow;
+  // full-block tiles use 10 lines x 2 blocks; edge tiles up to 8 blocks: 32 line slots
+  static constexpr int kASlot = (EDGE ? 32 : 20) * kHaloRow;
   static constexpr int kANum = 2;
   static constexpr int kBNumFit = (kAvail - kANum * kASlot) / kStageB;
   static constexpr int kBNum = kBNumFit > 16 ? 16 : kBNumFit;
@@ -110,7 +117,7 @@ struct ConvCfg {
   static constexpr uint32_t kTmemCols = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kSmem = 1024 + kRingBytes + kBarBytes;
-  static_assert(HALO ? kBNum >= 4 : kStages >= 3, "pipeline too shallow");
+  static_assert(HALO ? kBNum >= 3 : kStages >= 3, "pipeline too shallow");
   static_assert((2 * kNumBars + 5) * 8 + 8 <= 512, "barrier area");
   static_assert(kRingBytes >= (kBM + 16) * BN * 4, "split-K staging must fit the ring");
 };
@@ -159,17 +166,51 @@ __device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix,
   }
 }
 
+// Halo-mode tile geometry.  Tiles are enumerated class-major: full 8x8 blocks (2 per CTA,
+// 10 halo rows each), then bottom-edge blocks (rb valid rows: rb+2 halo rows, up to 8 per
+// CTA), then right-edge blocks (cr valid columns, loaded as rb+2... columns: the tile is
+// "transposed", its 8-row UMMA groups run down a pixel column).
+struct HaloTile {
+  int bpt;       // blocks per CTA tile
+  int lines;     // halo lines (rows, or columns if tr) loaded per block
+  int tr;        // 1: column-oriented (right-edge class)
+  int j0;        // index of this CTA's first block in the class list
+  int nblk;      // blocks in the class
+  const int32_t* list;
+};
+
+template <int CG>
+__device__ __forceinline__ HaloTile halo_tile(int mt, int rank, int nF, int nB, const int32_t* list,
+                                              int nR, const ConvParams& p) {
+  HaloTile g;
+  const int mF = (nF + 2 * CG - 1) / (2 * CG);
+  const int mB = (nB + p.bpt_b * CG - 1) / (p.bpt_b * CG);
+  int local;
+  if (mt < mF) {
+    g.bpt = 2; g.lines = 10; g.tr = 0; g.nblk = nF; g.list = list; local = mt;
+  } else if (mt < mF + mB) {
+    g.bpt = p.bpt_b; g.lines = p.rb + 2; g.tr = 0; g.nblk = nB; g.list = list + nF; local = mt - mF;
+  } else {
+    g.bpt = p.bpt_r; g.lines = p.cr + 2; g.tr = 1; g.nblk = nR; g.list = list + nF + nB;
+    local = mt - mF - mB;
+  }
+  g.j0 = local * g.bpt * CG + rank * g.bpt;
+  return g;
+}
+
 // CG = 1: one CTA per 128 x BN tile, tcgen05.mma.cta_group::1 (M = 128).
 // CG = 2: a CTA pair (cluster of 2) per 256 x BN tile, tcgen05.mma.cta_group::2 (M = 256):
 //   each CTA TMA-loads its own 128 rows of A and its half (BN/2 rows) of B; the leader
 //   (rank 0) waits for both halves on its full barrier and issues the MMAs; commits are
 //   multicast to both CTAs' barriers; each CTA's epilogue drains its own TMEM lanes and
 //   arrives on the leader's accumulator-empty barrier.  B traffic per SM halves.
-template <int BN, int CG, int BLK, bool HALO>
+template <int BN, int CG, int BLK, bool HALO, bool EDGE>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
-                             const __grid_constant__ CUtensorMap tmB, const ConvParams p) {
-  using Cfg = ConvCfg<BN, CG, HALO>;
+                             const __grid_constant__ CUtensorMap tmB,
+                             const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+  using Cfg = ConvCfg<BN, CG, HALO, EDGE>;
+  static_assert(!EDGE || HALO, "edge packing is a halo-mode feature");
   static_assert(!HALO || BLK == 8, "halo staging needs 8x8 blocks");
   constexpr int S = Cfg::kStages;
   constexpr int NB = Cfg::kNumBars;
@@ -194,7 +235,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int BPT = kBM / (BLK * BLK);  // blocks per CTA tile (2 at b=8, 8 at b=4)
   constexpr int bb = BLK * BLK;
   const int bpt_pair = BPT * CG;  // blocks per (pair) tile
-  const int m_tiles = (count + bpt_pair - 1) / bpt_pair;
+  // class counts (edge packing) -- without a plan every listed block is a "full" block
+  const int32_t* list = (EDGE && p.plan_ids) ? p.plan_ids : p.ids;
+  const int nF = (EDGE && p.plan_ids) ? __ldg(p.plan_meta + 0) : count;
+  const int nB = (EDGE && p.plan_ids) ? __ldg(p.plan_meta + 1) : 0;
+  const int nR = (EDGE && p.plan_ids) ? __ldg(p.plan_meta + 2) : 0;
+  const int m_tiles = HALO ? (nF + 2 * CG - 1) / (2 * CG) +
+                                 (nB + p.bpt_b * CG - 1) / (p.bpt_b * CG) +
+                                 (nR + p.bpt_r * CG - 1) / (p.bpt_r * CG)
+                           : (count + bpt_pair - 1) / bpt_pair;
   const int tiles = m_tiles * p.n_tiles_n;
   const int ksteps = 9 * p.kc;
   // halo mode splits K at 64-channel chunk boundaries (all 9 taps of a chunk stay together)
@@ -238,39 +287,43 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int t = u / nsplit, sk = u - t * nsplit;
           const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
           const int kc0 = sk * p.kc / nsplit, kc1 = (sk + 1) * p.kc / nsplit;
-          int cx[BPT], cy[BPT], cn[BPT];
+          const HaloTile g = halo_tile<CG>(mt, rank, nF, nB, list, nR, p);
+          int cx[8], cy[8], cn[8];
 #pragma unroll
-          for (int i = 0; i < BPT; ++i) {
-            const int j = min(mt * bpt_pair + rank * BPT + i, count - 1);
-            int n, by, bx;
-            decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
+          for (int i = 0; i < 8; ++i) {
+            // pad a short tile with a real block of the same class (computed, never stored)
+            const int j = min(g.j0 + i, g.nblk - 1);
+            int n = 0, by = 0, bx = 0;
+            if (i < g.bpt) decode_block(__ldg(g.list + j), p.hb, p.wb, n, by, bx);
             cn[i] = n;
             cy[i] = by * BLK - 1;
             cx[i] = bx * BLK - 1;
           }
           const int n0 = nt * BN + rank * Cfg::kBNc;
-          constexpr uint32_t kABytes = BPT * 10 * 10 * 128;  // real halo bytes per CTA
+          const uint32_t a_bytes = (uint32_t)(g.lines * g.bpt * 10 * 128);  // real halo bytes
           for (int kc = kc0; kc < kc1; ++kc) {
-            // A: the chunk's halos, one TMA row box {64 ch, 10 px} per halo row per block
+            // A: the chunk's halos, one TMA line box {64 ch, 10 px} per halo line per block;
+            // line l of block i lands in 2048-B slot (l * bpt + i)
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* a_dst = sA + stage * Cfg::kASlot;
+            uint32_t bar;
             if constexpr (CG == 1) {
-              mbar_arrive_expect_tx(&full[stage], kABytes);
-#pragma unroll
-              for (int yy = 0; yy < 10; ++yy)
-#pragma unroll
-                for (int i = 0; i < BPT; ++i)
-                  tma_load_4d(&tmA, &full[stage], a_dst + (yy * BPT + i) * Cfg::kHaloRow, kc * kBK,
-                              cx[i], cy[i] + yy, cn[i], pol_a);
+              mbar_arrive_expect_tx(&full[stage], a_bytes);
+              bar = smem_u32(&full[stage]);
             } else {
-              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kABytes);
-              const uint32_t bar = leader_addr(&full[stage]);
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * a_bytes);
+              bar = leader_addr(&full[stage]);
+            }
+            for (int l = 0; l < g.lines; ++l) {
 #pragma unroll
-              for (int yy = 0; yy < 10; ++yy)
-#pragma unroll
-                for (int i = 0; i < BPT; ++i)
-                  tma_load_4d_cg2(&tmA, bar, a_dst + (yy * BPT + i) * Cfg::kHaloRow, kc * kBK,
-                                  cx[i], cy[i] + yy, cn[i], pol_a);
+              for (int i = 0; i < 8; ++i) {
+                if (i >= g.bpt) break;
+                uint8_t* dst = a_dst + (l * g.bpt + i) * Cfg::kHaloRow;
+                const CUtensorMap* tm = g.tr ? &tmC : &tmA;
+                const int xx = g.tr ? cx[i] + l : cx[i], yy = g.tr ? cy[i] : cy[i] + l;
+                if constexpr (CG == 1) tma_load_4d_bar(tm, bar, dst, kc * kBK, xx, yy, cn[i], pol_a);
+                else tma_load_4d_cg2(tm, bar, dst, kc * kBK, xx, yy, cn[i], pol_a);
+              }
             }
             if (++stage == Cfg::kANum) {
               stage = 0;
@@ -360,8 +413,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int bs = 0;
         uint32_t bph = 0;
         for (int u = cluster_id; u < total; u += n_clusters) {
-          const int sk = u - (u / nsplit) * nsplit;
+          const int t = u / nsplit, sk = u - t * nsplit;
           const int kc0 = sk * p.kc / nsplit, kc1 = (sk + 1) * p.kc / nsplit;
+          const HaloTile g = halo_tile<CG>(t / p.n_tiles_n, 0, nF, nB, list, nR, p);
+          const uint32_t line_stride = (uint32_t)(g.bpt * Cfg::kHaloRow);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -373,8 +428,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int dy = tap / 3, dx = tap - 3 * (tap / 3);
               mbar_wait(&full[Cfg::kANum + bs], bph);
               tc_fence_after();
-              // tap (dy,dx): group g = 2*py + block at a_start + g*2048, row k = pixel px + dx
-              const uint32_t a_start = a_base + (uint32_t)(dy * BPT * Cfg::kHaloRow + dx * 128);
+              // tap (dy,dx): 8-row group q*bpt + block at a_start + group*2048; rows run along
+              // the halo line, so the along-line shift is 128 B per pixel and the cross-line
+              // shift is one line (bpt slots); transposed tiles swap the roles of dy and dx
+              const int major = g.tr ? dx : dy, minor = g.tr ? dy : dx;
+              const uint32_t a_start = a_base + (uint32_t)major * line_stride + (uint32_t)(minor * 128);
               const uint32_t b_addr = smem_u32(sB + bs * Cfg::kStageB);
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k) {
@@ -446,16 +504,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t = u / nsplit, sk = u - t * nsplit;
       const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
       // tile row -> (block, pixel): per-tap mode rows are block-major (b^2 rows per block);
-      // halo mode rows are [py][block][px] (8-row groups g = py*BPT + block)
-      const int bi = HALO ? (row >> 3) % BPT : row / bb;
-      const int ry = HALO ? (row >> 3) / BPT : (row - bi * bb) / BLK;
-      const int rx = HALO ? (row & 7) : (row - bi * bb) % BLK;
-      const int j = mt * bpt_pair + rank * BPT + bi;
-      bool valid = (bi < BPT) && (j < count);
+      // halo mode rows are [line q][block][8 px along the line] (group = q * bpt + block)
+      int bi, ry, rx, j, nblk;
+      const int32_t* lst;
+      if constexpr (HALO) {
+        const HaloTile g = halo_tile<CG>(mt, rank, nF, nB, list, nR, p);
+        bi = (row >> 3) % g.bpt;
+        const int q = (row >> 3) / g.bpt;
+        ry = g.tr ? (row & 7) : q;
+        rx = g.tr ? q : (row & 7);
+        j = g.j0 + bi;
+        nblk = g.nblk;
+        lst = g.list;
+      } else {
+        bi = row / bb;
+        ry = (row - bi * bb) / BLK;
+        rx = (row - bi * bb) % BLK;
+        j = mt * bpt_pair + rank * BPT + bi;
+        nblk = count;
+        lst = p.ids;
+      }
+      bool valid = (bi < (HALO ? 8 : BPT)) && (j < nblk);
       size_t pix = 0;
       if (valid) {
         int n, by, bx;
-        decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
+        decode_block(__ldg(lst + j), p.hb, p.wb, n, by, bx);
         const int yy = by * BLK + ry, xx = bx * BLK + rx;
         valid = (yy < p.h) && (xx < p.w);
         pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
@@ -576,6 +649,55 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Edge-class plan (halo mode on maps with H % 8 or W % 8 != 0): partitions the ascending list
+// into full, bottom-edge (incl. corner) and right-edge blocks, each kept ascending, with
+// warp-ballot / popc prefix sums in one CTA (latency-bound: <= a few thousand ids).
+__global__ void __launch_bounds__(1024) conv_plan_kernel(const int32_t* __restrict__ ids,
+                                                         const int32_t* __restrict__ count, int hb,
+                                                         int wb, int has_b, int has_r,
+                                                         int32_t* __restrict__ plan_ids,
+                                                         int32_t* __restrict__ meta) {
+  __shared__ int warp_off[32];
+  __shared__ int round_total;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int cnt = *count;
+  int base = 0;
+  for (int cls = 0; cls < 3; ++cls) {
+    const int cls_base = base;
+    for (int start = 0; start < cnt; start += blockDim.x) {
+      const int j = start + threadIdx.x;
+      bool take = false;
+      int id = 0;
+      if (j < cnt) {
+        id = __ldg(ids + j);
+        const int r = id % (hb * wb), by = r / wb, bx = r - (r / wb) * wb;
+        const bool bottom = has_b && by == hb - 1, right = has_r && bx == wb - 1;
+        take = (bottom ? 1 : (right ? 2 : 0)) == cls;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      const int pre = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) warp_off[warp] = __popc(bal);
+      __syncthreads();
+      if (warp == 0) {
+        const int v = lane < nwarps ? warp_off[lane] : 0;
+        int incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += o;
+        }
+        if (lane < nwarps) warp_off[lane] = incl - v;
+        if (lane == 31) round_total = incl;
+      }
+      __syncthreads();
+      if (take) plan_ids[base + warp_off[warp] + pre] = id;
+      base += round_total;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) meta[cls] = base - cls_base;
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -597,11 +719,11 @@ static PFN_encodeTiled_t get_encode_tiled() {
   return fn;
 }
 
-template <int BN, int CG, int BLK, bool HALO>
-static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const ConvParams& p,
-                               int grid, cudaStream_t s) {
-  using Cfg = ConvCfg<BN, CG, HALO>;
-  auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK, HALO>;
+template <int BN, int CG, int BLK, bool HALO, bool EDGE = false>
+static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                               const ConvParams& p, int grid, cudaStream_t s) {
+  using Cfg = ConvCfg<BN, CG, HALO, EDGE>;
+  auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK, HALO, EDGE>;
   static bool attr_set = false;  // per process; the attribute is per function
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
@@ -620,22 +742,25 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }
 
 template <int BN>
 static sphinx_status launch_cg(int cg, const CUtensorMap& ta, const CUtensorMap& tb,
-                               const ConvParams& p, int grid, cudaStream_t s) {
+                               const CUtensorMap& tc, const ConvParams& p, int grid, cudaStream_t s) {
+  if (p.b == 8 && p.halo && p.plan_ids)
+    return cg == 2 ? launch_bn<BN, 2, 8, true, true>(ta, tb, tc, p, grid, s)
+                   : launch_bn<BN, 1, 8, true, true>(ta, tb, tc, p, grid, s);
   if (p.b == 8 && p.halo)
-    return cg == 2 ? launch_bn<BN, 2, 8, true>(ta, tb, p, grid, s)
-                   : launch_bn<BN, 1, 8, true>(ta, tb, p, grid, s);
+    return cg == 2 ? launch_bn<BN, 2, 8, true>(ta, tb, tc, p, grid, s)
+                   : launch_bn<BN, 1, 8, true>(ta, tb, tc, p, grid, s);
   if (p.b == 8)
-    return cg == 2 ? launch_bn<BN, 2, 8, false>(ta, tb, p, grid, s)
-                   : launch_bn<BN, 1, 8, false>(ta, tb, p, grid, s);
-  return cg == 2 ? launch_bn<BN, 2, 4, false>(ta, tb, p, grid, s)
-                 : launch_bn<BN, 1, 4, false>(ta, tb, p, grid, s);
+    return cg == 2 ? launch_bn<BN, 2, 8, false>(ta, tb, tc, p, grid, s)
+                   : launch_bn<BN, 1, 8, false>(ta, tb, tc, p, grid, s);
+  return cg == 2 ? launch_bn<BN, 2, 4, false>(ta, tb, tc, p, grid, s)
+                 : launch_bn<BN, 1, 4, false>(ta, tb, tc, p, grid, s);
 }
 
 // Widest tile that minimises padded output columns (ties -> wider).
@@ -656,15 +781,18 @@ static int pick_bn(int cout) {
 
 using namespace sphinx;
 
-// Split-K workspace: [kCntBytes of int32 arrival counters][partial-tile slots].
+// Workspace: [kCntBytes of int32 split-K arrival counters][plan meta (256 B)]
+//            [plan ids: capacity int32, padded to 256 B][split-K partial-tile slots].
 constexpr size_t kCntBytes = 4096;
+static size_t plan_bytes(long long capacity) { return 256 + (((size_t)capacity * 4 + 255) & ~(size_t)255); }
 
 static size_t slot_bytes(int cg, int bn) { return (size_t)cg * kBM * bn * sizeof(float); }
 
 extern "C" size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, int32_t c_in,
                                              int32_t c_out, int32_t block) {
-  (void)n; (void)h; (void)w_; (void)c_in; (void)block;
-  if (c_out <= 0) return 0;
+  (void)c_in;
+  if (c_out <= 0 || n <= 0 || h <= 0 || w_ <= 0 || block <= 0) return 0;
+  const long long capacity = (long long)n * cdiv(h, block) * cdiv(w_, block);
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) {
@@ -672,7 +800,7 @@ extern "C" size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, i
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
   }
   // one slot per SM (two rounds of CTA pairs), sized for the CTA-pair kernel
-  return kCntBytes + (size_t)sms * slot_bytes(2, pick_bn(c_out));
+  return kCntBytes + plan_bytes(capacity) + (size_t)sms * slot_bytes(2, pick_bn(c_out));
 }
 
 extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, const float* bias,
@@ -705,7 +833,7 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   // halo-staged A for 8x8 blocks unless overridden: each activation read once per chunk
   int halo = block == 8 ? 1 : 0;
   if (const char* env = getenv("SPHINX_CONV_HALO")) halo = halo && atoi(env) != 0;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc;
   {
     const cuuint64_t dims[4] = {(cuuint64_t)c_in, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
     const cuuint64_t strides[3] = {(cuuint64_t)c_in * 2, (cuuint64_t)w_ * c_in * 2,
@@ -717,6 +845,12 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
     CUresult r = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides,
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
+    // halo columns (transposed right-edge tiles): one pixel wide, b+2 tall
+    const cuuint32_t boxc[4] = {(cuuint32_t)kBK, 1, (cuuint32_t)(block + 2), 1};
+    r = enc(&tc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, boxc, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
   }
   {
@@ -751,12 +885,26 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.ws_cnt = nullptr;
   p.ws_slots = 0;
   p.ws_tiles = 0;
-  bool allow_split = true;
+  p.plan_ids = nullptr;
+  p.plan_meta = nullptr;
+  p.rb = h % 8;
+  p.cr = w_ % 8;
+  p.bpt_b = p.rb ? (16 / p.rb < 8 ? 16 / p.rb : 8) : 8;
+  p.bpt_r = p.cr ? (16 / p.cr < 8 ? 16 / p.cr : 8) : 8;
+  const size_t pl_bytes = plan_bytes(capacity);
+  bool allow_split = true, allow_edge = true;
   if (const char* env = getenv("SPHINX_CONV_SPLIT")) allow_split = atoi(env) != 0;
-  if (allow_split && workspace && workspace_bytes >= kCntBytes + slot_bytes(cg, bn)) {
-    p.ws_cnt = static_cast<int32_t*>(workspace);
-    p.ws_part = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kCntBytes);
-    p.ws_slots = (int)((workspace_bytes - kCntBytes) / slot_bytes(cg, bn));
+  if (const char* env = getenv("SPHINX_CONV_EDGE")) allow_edge = atoi(env) != 0;
+  const bool ws_ok = workspace && workspace_bytes >= kCntBytes + pl_bytes;
+  uint8_t* ws8 = static_cast<uint8_t*>(workspace);
+  if (ws_ok && allow_edge && halo && (p.rb || p.cr)) {
+    p.plan_meta = reinterpret_cast<int32_t*>(ws8 + kCntBytes);
+    p.plan_ids = reinterpret_cast<int32_t*>(ws8 + kCntBytes + 256);
+  }
+  if (allow_split && ws_ok && workspace_bytes >= kCntBytes + pl_bytes + slot_bytes(cg, bn)) {
+    p.ws_cnt = reinterpret_cast<int32_t*>(ws8);
+    p.ws_part = reinterpret_cast<float*>(ws8 + kCntBytes + pl_bytes);
+    p.ws_slots = (int)((workspace_bytes - kCntBytes - pl_bytes) / slot_bytes(cg, bn));
     p.ws_tiles = (int)(kCntBytes / (2 * sizeof(int32_t))) / cg;
   }
   const long long max_tiles = (long long)cdiv(capacity, p.bpt * cg) * p.n_tiles_n;
@@ -764,11 +912,17 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   const long long want = p.ws_part ? max_tiles * 16 : max_tiles;  // split-K may multiply units
   const int grid = cg * (int)(want < max_clusters ? want : max_clusters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (p.plan_ids) {
+    conv_plan_kernel<<<1, 1024, 0, s>>>(block_ids, count, hb, wb, p.rb != 0, p.cr != 0,
+                                        const_cast<int32_t*>(p.plan_ids),
+                                        const_cast<int32_t*>(p.plan_meta));
+    SPHINX_CHECK_LAUNCH();
+  }
   switch (bn) {
-    case 256: return launch_cg<256>(cg, ta, tb, p, grid, s);
-    case 160: return launch_cg<160>(cg, ta, tb, p, grid, s);
-    case 128: return launch_cg<128>(cg, ta, tb, p, grid, s);
-    case 64: return launch_cg<64>(cg, ta, tb, p, grid, s);
-    default: return launch_cg<32>(cg, ta, tb, p, grid, s);
+    case 256: return launch_cg<256>(cg, ta, tb, tc, p, grid, s);
+    case 160: return launch_cg<160>(cg, ta, tb, tc, p, grid, s);
+    case 128: return launch_cg<128>(cg, ta, tb, tc, p, grid, s);
+    case 64: return launch_cg<64>(cg, ta, tb, tc, p, grid, s);
+    default: return launch_cg<32>(cg, ta, tb, tc, p, grid, s);
   }
 }

@@ -166,15 +166,19 @@ def test_noise_vs_oracle(sphinx, shape, b):
 
 # ----------------------------------------------------------------- step 4
 
-@pytest.fixture(params=[(1, 0, 1), (2, 0, 1), (1, 1, 1), (2, 1, 1), (2, 0, 0), (2, 1, 0)],
-                ids=["cta1", "pair", "cta1-splitk", "pair-splitk", "pair-pertap", "pair-pertap-splitk"])
+@pytest.fixture(params=[(1, 0, 1, 1), (2, 0, 1, 1), (1, 1, 1, 1), (2, 1, 1, 1), (2, 1, 1, 0),
+                        (2, 0, 0, 0), (2, 1, 0, 0)],
+                ids=["cta1", "pair", "cta1-splitk", "pair-splitk", "pair-splitk-noedge", "pair-pertap",
+                     "pair-pertap-splitk"])
 def conv_cg(request, monkeypatch):
     """Runs a conv test with the 1-SM (cta_group::1) and the CTA-pair (cta_group::2) kernels,
-    without and with device-chosen split-K, with halo-staged (b=8 default) and per-tap A."""
-    cg, split, halo = request.param
+    without and with device-chosen split-K, with halo-staged (b=8 default, with and without
+    edge-class packing) and per-tap A."""
+    cg, split, halo, edge = request.param
     monkeypatch.setenv("SPHINX_CONV_CG", str(cg))
     monkeypatch.setenv("SPHINX_CONV_SPLIT", str(split))
     monkeypatch.setenv("SPHINX_CONV_HALO", str(halo))
+    monkeypatch.setenv("SPHINX_CONV_EDGE", str(edge))
     return request.param
 
 
@@ -225,6 +229,15 @@ def test_conv_unet_levels(sphinx, conv_cg, h, c, pattern, dens):
 def test_conv_shapes_bf16_out(sphinx, conv_cg, cin, cout, b):
     _conv_check(sphinx, 3, 20, 28, cin, cout, b, 0.5, "scattered", f"shape{cin}{cout}",
                 out_dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("h,w", [(17, 9), (20, 28), (13, 11), (22, 15), (19, 23), (14, 30)])
+@pytest.mark.parametrize("pattern", ["checker", "scattered"])
+def test_conv_ragged_edges(sphinx, conv_cg, h, w, pattern):
+    """Every remainder H % 8, W % 8 in 1..7: bottom-edge, right-edge and corner blocks (the
+    edge-class packing of the halo kernel) against the oracle, bf16 and fp32 outputs."""
+    for dt in (torch.float32, torch.bfloat16):
+        _conv_check(sphinx, 3, h, w, 64, 96, 8, 0.6, pattern, f"rag{h}x{w}{pattern}", out_dtype=dt)
 
 
 @pytest.mark.parametrize("ky,kx", [(0, 0), (1, 1), (2, 1), (0, 2)])

@@ -59,7 +59,7 @@ def main():
             xn = x.permute(0, 3, 1, 2)
             wn = w.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
             t_cudnn = timed(lambda: torch.nn.functional.conv2d(xn, wn, padding=1), a.reps)
-            sp.conv_workspace(c, dev)
+            sp.conv_workspace(c, dev, nf, h, h, 8)
             dense_flops = nf * h * h * 2 * 9 * c * c
             for d in a.dens:
                 rg = syn.rng("mbmask", nf, li, d)
