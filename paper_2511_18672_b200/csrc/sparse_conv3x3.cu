@@ -166,6 +166,24 @@ __device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix,
   }
 }
 
+// Work unit u -> (tile, k-split index, splits of that tile, split-tile slot).
+struct Unit {
+  int t, sk, ns, slot;
+};
+__device__ __forceinline__ Unit decode_unit(int u, int n_full, int nsplit) {
+  Unit r;
+  if (u < n_full) {
+    r.t = u; r.sk = 0; r.ns = 1; r.slot = 0;
+  } else {
+    const int v = u - n_full;
+    r.slot = v / nsplit;
+    r.t = n_full + r.slot;
+    r.sk = v - r.slot * nsplit;
+    r.ns = nsplit;
+  }
+  return r;
+}
+
 // Halo-mode tile geometry.  Tiles are enumerated class-major: full 8x8 blocks (2 per CTA,
 // 10 halo rows each), then bottom-edge blocks (rb valid rows: rb+2 halo rows, up to 8 per
 // CTA), then right-edge blocks (cr valid columns, loaded as rb+2... columns: the tile is
@@ -247,8 +265,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tiles = m_tiles * p.n_tiles_n;
   const int ksteps = 9 * p.kc;
   // halo mode splits K at 64-channel chunk boundaries (all 9 taps of a chunk stay together)
-  const int nsplit = choose_split(tiles, n_clusters, ksteps, HALO ? p.kc : 16, p);
-  const int total = tiles * nsplit;  // work units: (tile, k-split), split fastest
+  // Full waves of tiles run unsplit; the last partial wave (rem tiles) is split nsplit ways
+  // along K so that it fills one co-resident round (tail split-K).  Halo mode splits at
+  // 64-channel chunk boundaries (the 9 taps of a chunk stay together).
+  const int rem = tiles - (tiles / n_clusters) * n_clusters;
+  const int nsplit = rem > 0 ? choose_split(rem, n_clusters, ksteps, HALO ? p.kc : 16, p) : 1;
+  const int n_full = nsplit > 1 ? tiles - rem : tiles;
+  const int total = n_full + (nsplit > 1 ? rem * nsplit : 0);  // work units
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -284,9 +307,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int bs = 0;  // B ring position
         uint32_t bph = 0;
         for (int u = cluster_id; u < total; u += n_clusters) {
-          const int t = u / nsplit, sk = u - t * nsplit;
+          const Unit U = decode_unit(u, n_full, nsplit);
+          const int t = U.t;
           const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
-          const int kc0 = sk * p.kc / nsplit, kc1 = (sk + 1) * p.kc / nsplit;
+          const int kc0 = U.sk * p.kc / U.ns, kc1 = (U.sk + 1) * p.kc / U.ns;
           const HaloTile g = halo_tile<CG>(mt, rank, nF, nB, list, nR, p);
           int cx[8], cy[8], cn[8];
 #pragma unroll
@@ -350,9 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else
       for (int u = cluster_id; u < total; u += n_clusters) {
-        const int t = u / nsplit, sk = u - t * nsplit;
+        const Unit U = decode_unit(u, n_full, nsplit);
+        const int t = U.t;
         const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
-        const int ks0 = sk * ksteps / nsplit, ks1 = (sk + 1) * ksteps / nsplit;
+        const int ks0 = U.sk * ksteps / U.ns, ks1 = (U.sk + 1) * ksteps / U.ns;
         // TMA origin of every block of this CTA's half of the tile (kept in registers)
         int cx[BPT], cy[BPT], cn[BPT];
 #pragma unroll
@@ -413,9 +438,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int bs = 0;
         uint32_t bph = 0;
         for (int u = cluster_id; u < total; u += n_clusters) {
-          const int t = u / nsplit, sk = u - t * nsplit;
-          const int kc0 = sk * p.kc / nsplit, kc1 = (sk + 1) * p.kc / nsplit;
-          const HaloTile g = halo_tile<CG>(t / p.n_tiles_n, 0, nF, nB, list, nR, p);
+          const Unit U = decode_unit(u, n_full, nsplit);
+          const int kc0 = U.sk * p.kc / U.ns, kc1 = (U.sk + 1) * p.kc / U.ns;
+          const HaloTile g = halo_tile<CG>(U.t / p.n_tiles_n, 0, nF, nB, list, nR, p);
           const uint32_t line_stride = (uint32_t)(g.bpt * Cfg::kHaloRow);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
@@ -463,8 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else
       for (int u = cluster_id; u < total; u += n_clusters) {
-        const int sk = u - (u / nsplit) * nsplit;
-        const int ks0 = sk * ksteps / nsplit, ks1 = (sk + 1) * ksteps / nsplit;
+        const Unit U = decode_unit(u, n_full, nsplit);
+        const int ks0 = U.sk * ksteps / U.ns, ks1 = (U.sk + 1) * ksteps / U.ns;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -501,7 +526,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cluster_id; u < total; u += n_clusters) {
-      const int t = u / nsplit, sk = u - t * nsplit;
+      const Unit U = decode_unit(u, n_full, nsplit);
+      const int t = U.t, sk = U.sk, ns = U.ns;
       const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
       // tile row -> (block, pixel): per-tap mode rows are block-major (b^2 rows per block);
       // halo mode rows are [line q][block][8 px along the line] (group = q * bpt + block)
@@ -534,8 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
       }
       float* part = nullptr;
-      if (nsplit > 1)
-        part = p.ws_part + (((size_t)(t * nsplit + sk) * CG + rank) * kBM + row) * BN;
+      if (ns > 1)
+        part = p.ws_part + (((size_t)(U.slot * ns + sk) * CG + rank) * kBM + row) * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -543,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
         tc_wait_ld();
-        if (nsplit > 1) {
+        if (ns > 1) {
           // split-K: park this split's fp32 partial row in the workspace
 #pragma unroll
           for (int g = 0; g < 32; g += 4)
@@ -567,32 +593,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc = 0;
         acc_phase ^= 1;
       }
-      if (nsplit > 1) {
-        // Rendezvous of the nsplit units of tile t (all co-resident in this single round),
+      if (ns > 1) {
+        // Rendezvous of the ns units of tile t (all co-resident in this single round),
         // then each reduces a 1/nsplit slice of the rows, summing partials in split order
         // (deterministic), with coalesced float4 loads across the epilogue threads.
         pix_tab[row] = valid ? (long long)pix : -1ll;
         __threadfence();
         named_bar_sync(1, 128);
-        int* arrive = p.ws_cnt + (t * CG + rank) * 2;
+        int* arrive = p.ws_cnt + (U.slot * CG + rank) * 2;
         if (row == 0) {
           atomicAdd(arrive, 1);
           int seen;
           do {
             asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
-            if (seen < nsplit) __nanosleep(64);
-          } while (seen < nsplit);
+            if (seen < ns) __nanosleep(64);
+          } while (seen < ns);
         }
         named_bar_sync(1, 128);
-        const int r0 = sk * kBM / nsplit, r1 = (sk + 1) * kBM / nsplit;
+        const int r0 = sk * kBM / ns, r1 = (sk + 1) * kBM / ns;
         const uint32_t slice_bytes = (uint32_t)((r1 - r0) * BN * 4);
-        const float* base = p.ws_part + (((size_t)(t * nsplit) * CG + rank) * kBM + r0) * BN;
+        const float* base = p.ws_part + (((size_t)(U.slot * ns) * CG + rank) * kBM + r0) * BN;
         const size_t split_stride = (size_t)CG * kBM * BN;
         float* stage_buf = reinterpret_cast<float*>(sA);  // the operand ring is idle now
         if (row == 0) {
           fence_proxy_async_global();
-          mbar_arrive_expect_tx(red_bar, slice_bytes * (uint32_t)nsplit);
-          for (int s2 = 0; s2 < nsplit; ++s2)
+          mbar_arrive_expect_tx(red_bar, slice_bytes * (uint32_t)ns);
+          for (int s2 = 0; s2 < ns; ++s2)
             bulk_g2s(stage_buf + (size_t)s2 * (r1 - r0) * BN, base + s2 * split_stride, slice_bytes,
                      red_bar);
         }
@@ -605,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const long long px = pix_tab[rr];
           if (px < 0) continue;
           float4 acc4 = sb[e];
-          for (int s2 = 1; s2 < nsplit; ++s2) {
+          for (int s2 = 1; s2 < ns; ++s2) {
             const float4 a = sb[s2 * n_el + e];
             acc4.x += a.x; acc4.y += a.y; acc4.z += a.z; acc4.w += a.w;
           }
@@ -631,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, 128);
         if (row == 0) {
           const int old = atomicAdd(arrive + 1, 1);
-          if (old == nsplit - 1) {
+          if (old == ns - 1) {
             arrive[0] = 0;
             arrive[1] = 0;
             __threadfence();
