@@ -364,13 +364,9 @@ def run_gpu(args):
                 for j in range(CONVS_PER_LEVEL):
                     conv_ms[l][j].append(ev[l][j][0].elapsed_time(ev[l][j][1]))
     ms = statistics.mean(step_ms)
-    if world > 1:
-        t = torch.tensor([ms, float(flops)], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
-        ms_all, flops_all = float(tmax[0]), float(tsum[1])
+    if world > 1:  # whole-job throughput: sum of the work / max over ranks of the step time
+        from paper_2511_18672_b200 import dist as sdist
+        ms_all, flops_all = sdist.reduce_step(ms, flops, device=dev)
     else:
         ms_all, flops_all = ms, float(flops)
     value = flops_all / (ms_all * 1e-3) / 1e12
@@ -433,6 +429,20 @@ def run_gpu(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_profile():
+    """Minimal run for ncu: the captured step graph replayed twice; only the step's kernels
+    (and the graph-capture warm-up's) appear in the launch list."""
+    import torch
+    torch.cuda.set_device(0)
+    st = GpuStep(make_request("r0"), torch.device("cuda", 0))
+    g, _ = capture_step(torch, st, with_conv_events=False)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    print(json.dumps({"profile": "done", "launches_per_step": st.launches_per_step}))
 
 
 def run_e2e(torch, st, g, req, dev, args, flops):
@@ -561,9 +571,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--profile", action="store_true",
+                    help="ncu mode: capture the step graph, replay it twice (warm-up + profiled), exit")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.profile:
+        run_profile()
     else:
         run_gpu(args)
 
