@@ -189,7 +189,13 @@ SPHINX_API sphinx_status sphinx_noise_inject(const float* x0, const float* eps, 
  * y      NHWC [N][h][w][c_out] device, y_dtype bf16 or fp32; must not alias x.
  * c_in % 8 == 0, c_out % 8 == 0, block in {4, 8}  (else SPHINX_ERR_UNSUPPORTED).
  * block_ids/count/capacity  list from sphinx_compact_blocks (capacity = N*Hb*Wb upper bound).
- * workspace  reserved (pass NULL, 0); sphinx_conv_workspace_size returns 0 in ABI v1.
+ * workspace  device scratch of sphinx_conv_workspace_size(...) bytes, 256-byte aligned, ZERO-
+ *            INITIALISED ONCE by the caller (the kernel leaves it zeroed); one per stream.  It
+ *            holds the split-K arrival counters and fp32 partial tiles (used when the device-side
+ *            block count leaves the last wave of tiles partial: the tail is split along K and
+ *            reduced in a fixed order, so results stay bit-reproducible) and, for maps with
+ *            H % 8 or W % 8 != 0, the edge-class plan (full / bottom-edge / right-edge blocks).
+ *            NULL disables both (the conv is still complete and exact, only slower).
  * ------------------------------------------------------------------------------- */
 SPHINX_API sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, const float* bias,
                                     void* y, sphinx_dtype y_dtype,

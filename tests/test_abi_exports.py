@@ -45,4 +45,8 @@ def test_invalid_arguments_rejected_on_host():
     p = ctypes.c_void_p(1024)
     assert lib.sphinx_sparse_conv3x3(p, p, null, p, sp.F32, 1, 16, 16, 12, 32, 4, p, p, 16, null, 0,
                                      null) == sp.ERR_UNSUPPORTED
-    assert lib.sphinx_conv_workspace_size(1, 16, 16, 32, 32, 4) == 0
+    # workspace: split-K counters + edge plan (capacity ids) + partial tiles; grows with N
+    small = lib.sphinx_conv_workspace_size(1, 16, 16, 32, 32, 4)
+    big = lib.sphinx_conv_workspace_size(168, 16, 16, 32, 32, 4)
+    assert small > 4096 and big - small >= (168 - 1) * 16 * 4 - 256
+    assert lib.sphinx_conv_workspace_size(0, 16, 16, 32, 32, 4) == 0
