@@ -311,12 +311,17 @@ def run_gpu(args):
     hbm, tc_peak, tc_sust, peak_kind = peaks()
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    # The step is timed on an event-free graph (event nodes would break the PDL chain between
+    # kernels); a second graph with external event nodes around each conv gives the per-conv
+    # device times used for the roofline.
+    g, _ = capture_step(torch, st, with_conv_events=False)
     try:
-        g, conv_ev = capture_step(torch, st, with_conv_events=True)
-        graph_note = "CUDA graph replay, conv launches timed by captured external events"
+        g_ev, conv_ev = capture_step(torch, st, with_conv_events=True)
+        graph_note = ("CUDA graph replay (event-free graph for the step; conv launches timed by "
+                      "captured external events in a second graph)")
     except Exception as e:  # event nodes unsupported: time the convs outside the graph
-        g, _ = capture_step(torch, st, with_conv_events=False)
-        conv_ev, graph_note = None, f"CUDA graph replay; conv events unsupported in capture ({type(e).__name__})"
+        g_ev, conv_ev = None, None
+        graph_note = f"CUDA graph replay; conv events unsupported in capture ({type(e).__name__})"
     for _ in range(max(args.warmup, 3)):
         g.replay()
         flush.fill_(1.0)
@@ -337,24 +342,30 @@ def run_gpu(args):
         e0.record()
         g.replay()
         e1.record()
-        flush.fill_(1.0)  # L2 flush between timed steps (outside the e0..e1 window)
+        if not args.no_flush:
+            flush.fill_(1.0)  # L2 flush between timed steps (outside the e0..e1 window)
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        if conv_ev is not None:
-            for l in range(3):
-                for j in range(CONVS_PER_LEVEL):
-                    conv_ms[l][j].append(conv_ev[l][j][0].elapsed_time(conv_ev[l][j][1]))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # keep sampling clocks through a sustained stretch so the record is not 3 samples long
+    # per-conv device times (same cold-L2 protocol), then a sustained stretch for the clocks
+    for _ in range(reps):
+        if g_ev is not None:
+            g_ev.replay()
+            torch.cuda.synchronize()
+            for l in range(3):
+                for j in range(CONVS_PER_LEVEL):
+                    conv_ms[l][j].append(conv_ev[l][j][0].elapsed_time(conv_ev[l][j][1]))
+        if not args.no_flush:
+            flush.fill_(1.0)
     t_end = time.time() + 1.0
     while time.time() < t_end:
         g.replay()
         torch.cuda.synchronize()
     stop.set()
     th.join(timeout=3)
-    if conv_ev is None:  # eager fallback for per-conv timing
+    if g_ev is None:  # eager fallback for per-conv timing
         ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
                for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
         for _ in range(reps):
@@ -377,6 +388,7 @@ def run_gpu(args):
         f_l = px_l[l] * 2 * 9 * c * c
         per_level.append({"level": l, "shape": [N_FRAMES, h, h, c], "active_blocks": blocks_l[l],
                           "real_px": px_l[l], "conv_ms": round(t_l, 5),
+                          "conv_ms_each": [round(statistics.mean(conv_ms[l][j]), 5) for j in range(CONVS_PER_LEVEL)],
                           "tflops": round(f_l / (t_l * 1e-3) / 1e12, 2)})
     conv_total_ms = sum(p["conv_ms"] for p in per_level) * CONVS_PER_LEVEL
     # dominant kernel = the conv launch family with the largest share of the step
@@ -385,6 +397,12 @@ def run_gpu(args):
     achieved = dom_flops / (dom["conv_ms"] * 1e-3) / 1e12
     all_conv_tflops = flops / (conv_total_ms * 1e-3) / 1e12
 
+    # the same conv calls timed in isolation (graph of 20 back-to-back launches, L2-warm)
+    iso = []
+    for l in range(3):
+        d = st.d
+        iso.append(round(graph_time(torch, lambda: st.sp.sphinx_sparse_conv3x3(
+            d[f"feat{l}"], d[f"w{l}0"], d[f"b{l}0"], st.y[l], B, st.ids[l], st.cnt[l])), 5))
     e2e = None if args.no_e2e else run_e2e(torch, st, g, req, dev, args, flops)
     sweep = None
     if rank == 0 and not args.no_sweep:
@@ -407,7 +425,8 @@ def run_gpu(args):
                        "convs_per_level": CONVS_PER_LEVEL, "active_blocks_per_level": blocks_l,
                        "density_per_level": [round(blocks_l[l] / (N_FRAMES * st.dims[l][1] ** 2), 4)
                                              for l in range(3)],
-                       "l2": "flushed between timed steps (256 MB write)", "timing": graph_note,
+                       "l2": ("NOT flushed (diagnostic --no-flush)" if args.no_flush else
+                              "flushed between timed steps (256 MB write)"), "timing": graph_note,
                        "parallelism": f"dp{world}"},
             "gpu_launches": st.launches_per_step * reps,
             "roofline": {"bound": "tensor", "kernel": "sparse_conv3x3_tc_kernel (level %d)" % dom["level"],
@@ -417,6 +436,7 @@ def run_gpu(args):
                          "traffic": None, "all_convs_tflops": round(all_conv_tflops, 2),
                          "conv_share_of_step": round(conv_total_ms / ms_all, 4)},
             "conv_levels": per_level,
+            "conv_isolated_ms": iso,
             "scatter_bandwidth": scat,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -571,6 +591,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-flush", action="store_true", help="diagnostic: keep L2 warm between steps")
     ap.add_argument("--profile", action="store_true",
                     help="ncu mode: capture the step graph, replay it twice (warm-up + profiled), exit")
     args = ap.parse_args()

@@ -33,6 +33,14 @@ sphinx_status check_device(int* sm_count) {
   return cached_ok ? SPHINX_OK : SPHINX_ERR_DEVICE;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SPHINX_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 }  // namespace sphinx
 
 extern "C" int32_t sphinx_abi_version(void) { return SPHINX_ABI_VERSION; }

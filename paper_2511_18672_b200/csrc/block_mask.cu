@@ -27,6 +27,8 @@ __global__ void __launch_bounds__(512) block_mask_l0_kernel(
     const float* __restrict__ O, const float* __restrict__ U, const float* __restrict__ tau_u,
     float tau_o, int hp, int wp, int cell_px, int hb0, int wb0, int rows_per_cta, int splits,
     uint8_t* __restrict__ mask0) {
+  pdl_wait();
+  pdl_trigger();
   const int cta = blockIdx.x;
   const int s = cta % splits;
   const int rest = cta / splits;
@@ -100,6 +102,8 @@ __global__ void __launch_bounds__(256) block_mask_tail_kernel(
     const float* __restrict__ q, const float* __restrict__ c0, const float* __restrict__ c1,
     const float* __restrict__ t, const int32_t* __restrict__ logic_id,
     int32_t* __restrict__ start_step) {
+  pdl_wait();
+  pdl_trigger();
   const int n = blockIdx.x;
   const int hb0 = lv.hb[0], wb0 = lv.wb[0];
   const uint8_t* m0 = lv.mask[0] + (size_t)n * hb0 * wb0;
@@ -197,19 +201,18 @@ extern "C" sphinx_status sphinx_block_mask(const float* opacity, const float* un
   int splits = cdiv(cell_px, rows_per_cta);
   const dim3 block(bdx, bdy);
   const int grid = n * hb0 * splits;
-  if (vec)
-    block_mask_l0_kernel<4><<<grid, block, 0, s>>>(opacity, uncertainty, tau_u, tau_o, hp, wp,
-                                                   cell_px, hb0, wb0, rows_per_cta, splits,
-                                                   block_mask[0]);
-  else
-    block_mask_l0_kernel<1><<<grid, block, 0, s>>>(opacity, uncertainty, tau_u, tau_o, hp, wp,
-                                                   cell_px, hb0, wb0, rows_per_cta, splits,
-                                                   block_mask[0]);
-  SPHINX_CHECK_LAUNCH();
-  block_mask_tail_kernel<<<n, 256, 0, s>>>(lv, n_levels, active_count, ks,
-                                           ss ? ss->q_reg : nullptr, ss ? ss->c0 : nullptr,
-                                           ss ? ss->c1 : nullptr, ss ? ss->t : nullptr,
-                                           ss ? ss->logic_id : nullptr, start_step);
-  SPHINX_CHECK_LAUNCH();
+  uint8_t* m0 = block_mask[0];
+  e = launch_k(vec ? block_mask_l0_kernel<4> : block_mask_l0_kernel<1>, dim3(grid), block, 0, s,
+               opacity, uncertainty, tau_u, tau_o, (int)hp, (int)wp, cell_px, hb0, wb0, rows_per_cta,
+               splits, m0);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const float* q = ss ? ss->q_reg : nullptr;
+  const float* c0 = ss ? ss->c0 : nullptr;
+  const float* c1 = ss ? ss->c1 : nullptr;
+  const float* tt = ss ? ss->t : nullptr;
+  const int32_t* lid = ss ? ss->logic_id : nullptr;
+  e = launch_k(block_mask_tail_kernel, dim3(n), dim3(256), 0, s, lv, (int)n_levels, active_count, ks,
+               q, c0, c1, tt, lid, start_step);
+  if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }

@@ -15,6 +15,8 @@ __global__ void __launch_bounds__(1024) compact_kernel(const uint8_t* __restrict
                                                        int u, int select,
                                                        int32_t* __restrict__ ids,
                                                        int32_t* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int warp_off[32];
   __shared__ int round_total;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -75,8 +77,9 @@ extern "C" sphinx_status sphinx_compact_blocks(const uint8_t* block_mask, int32_
   if ((int64_t)n * hb * wb > (int64_t)1 << 30) return SPHINX_ERR_UNSUPPORTED;
   sphinx_status st = check_device();
   if (st != SPHINX_OK) return st;
-  compact_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      block_mask, n, hb * wb, start_step, step_u, (int)select, block_ids, count);
-  SPHINX_CHECK_LAUNCH();
+  cudaError_t e = launch_k(compact_kernel, dim3(1), dim3(1024), 0,
+                           reinterpret_cast<cudaStream_t>(stream), block_mask, (int)n, (int)(hb * wb),
+                           start_step, (int)step_u, (int)select, block_ids, count);
+  if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }

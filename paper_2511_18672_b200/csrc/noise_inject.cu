@@ -22,6 +22,8 @@ __global__ void __launch_bounds__(256) noise_kernel(const float* __restrict__ x0
                                                     const int32_t* __restrict__ count,
                                                     const int32_t* __restrict__ step,
                                                     const float* __restrict__ abar, int S) {
+  pdl_wait();
+  pdl_trigger();
   const int cnt = *count;
   const int vpp = c / V;              // vectors per pixel
   const int per_block = b * b * vpp;  // vectors per (padded) block
@@ -86,12 +88,9 @@ extern "C" sphinx_status sphinx_noise_inject(const float* x0, const float* eps, 
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (vec)
-    noise_kernel<4><<<(int)blocks, 256, 0, s>>>(x0, eps, x_t, h, w, c, b, hb, wb, block_ids, count,
-                                                step, abar, total_steps);
-  else
-    noise_kernel<1><<<(int)blocks, 256, 0, s>>>(x0, eps, x_t, h, w, c, b, hb, wb, block_ids, count,
-                                                step, abar, total_steps);
-  SPHINX_CHECK_LAUNCH();
+  cudaError_t e = launch_k(vec ? noise_kernel<4> : noise_kernel<1>, dim3((unsigned)blocks), dim3(256),
+                           0, s, x0, eps, x_t, (int)h, (int)w, (int)c, (int)b, hb, wb, block_ids,
+                           count, step, abar, (int)total_steps);
+  if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }

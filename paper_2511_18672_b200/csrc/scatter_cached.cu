@@ -1,30 +1,35 @@
 // scatter_cached.cu — step (5): out = active(block) ? src : latent cache (bit copy).
 //
 // P:352 "reuses cached latents from the last full denoising step for unrefined
-// regions".  HBM-bound copy.  One CTA per (frame, pixel row): in NHWC the b
-// pixels of one block on one row are a contiguous b*C*elem-byte segment, so each
-// segment is a coalesced run of 16-byte words taken wholesale from src or cache.
-// The element type never passes through a float conversion (NaN payloads, -0 kept).
+// regions".  HBM-bound copy, 2 x map bytes (read src-or-cache, write out).
+// FULL layout: a flat grid-stride loop over the 16-byte words of the NHWC map (coalesced for
+// any C); COMPACT layout: one CTA per (frame, pixel row), each block's row segment taken from
+// its compact slot (binary search of the ascending list) or from the cache.  The element
+// type never passes through a float conversion (NaN payloads, -0 kept).
 #include "common.cuh"
 
 namespace sphinx {
 
+// One thread per 16-byte word of the map; consecutive threads cover consecutive words of a
+// pixel row, so each warp's accesses are coalesced whatever C is (4 fp32 latent channels or
+// 640 bf16 feature channels).
 __global__ void __launch_bounds__(256) scatter_full_kernel(
     const int4* src, const int4* __restrict__ cache, int4* out, int h, int w, int px_vec, int b,
     int hb, int wb, const uint8_t* __restrict__ mask, const int32_t* __restrict__ k, int u,
-    int in_place) {
-  const int n = blockIdx.x / h, y = blockIdx.x - (blockIdx.x / h) * h, by = y / b;
-  const int kf = k ? __ldg(k + n) : 0;
-  const bool frame_ok = !k || (kf >= 0 && kf <= u);
-  const size_t row = ((size_t)n * h + y) * w;
-  for (int bx = 0; bx < wb; ++bx) {
-    const bool act = frame_ok && mask[((size_t)n * hb + by) * wb + bx];
+    int in_place, long long total) {
+  pdl_wait();
+  pdl_trigger();
+  const int row_vec = w * px_vec;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / row_vec;  // = n * h + y
+    const int xv = (int)(e - row * row_vec);
+    const int n = (int)(row / h), y = (int)(row - (long long)n * h);
+    const int x = xv / px_vec;
+    const int kf = k ? __ldg(k + n) : 0;
+    const bool act = (!k || (kf >= 0 && kf <= u)) && mask[((size_t)n * hb + y / b) * wb + x / b];
     if (in_place && act) continue;
-    const int x0 = bx * b, npx = min(b, w - x0);
-    const size_t base = (row + x0) * px_vec;
-    const int nv = npx * px_vec;
-    const int4* sp = act ? src : cache;
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) out[base + i] = sp[base + i];
+    out[e] = act ? src[e] : __ldg(cache + e);
   }
 }
 
@@ -32,6 +37,8 @@ __global__ void __launch_bounds__(256) scatter_compact_kernel(
     const int4* __restrict__ src, const int4* __restrict__ cache, int4* __restrict__ out, int h,
     int w, int px_vec, int b, int hb, int wb, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
   const int n = blockIdx.x / h, y = blockIdx.x - (blockIdx.x / h) * h;
   const int by = y / b, py = y - by * b;
   const int cnt = *count;
@@ -88,14 +95,23 @@ extern "C" sphinx_status sphinx_scatter_cached(const void* src, sphinx_src_layou
   const int hb = cdiv(h, b), wb = cdiv(w, b);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int grid = n * h;
-  if (src_layout == SPHINX_SRC_FULL)
-    scatter_full_kernel<<<grid, 256, 0, s>>>(
-        static_cast<const int4*>(src), static_cast<const int4*>(cache), static_cast<int4*>(out), h,
-        w, px_vec, b, hb, wb, block_mask, start_step, step_u, out == src ? 1 : 0);
-  else
-    scatter_compact_kernel<<<grid, 256, 0, s>>>(
-        static_cast<const int4*>(src), static_cast<const int4*>(cache), static_cast<int4*>(out), h,
-        w, px_vec, b, hb, wb, block_ids, count);
-  SPHINX_CHECK_LAUNCH();
+  if (src_layout == SPHINX_SRC_FULL) {
+    int sms = 148;
+    check_device(&sms);
+    const long long total = (long long)n * h * w * px_vec;
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
+    cudaError_t e = launch_k(scatter_full_kernel, dim3((unsigned)blocks), dim3(256), 0, s,
+                             static_cast<const int4*>(src), static_cast<const int4*>(cache),
+                             static_cast<int4*>(out), (int)h, (int)w, px_vec, (int)b, hb, wb,
+                             block_mask, start_step, (int)step_u, out == src ? 1 : 0, total);
+    if (e != cudaSuccess) return cuda_fail(e);
+  } else {
+    cudaError_t e = launch_k(scatter_compact_kernel, dim3(grid), dim3(256), 0, s,
+                             static_cast<const int4*>(src), static_cast<const int4*>(cache),
+                             static_cast<int4*>(out), (int)h, (int)w, px_vec, (int)b, hb, wb,
+                             block_ids, count);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
   return SPHINX_OK;
 }

@@ -64,6 +64,7 @@ struct ConvParams {
   int rb, cr;                // valid rows of bottom-edge blocks, valid cols of right-edge blocks
   int bpt_b, bpt_r;          // blocks per CTA tile of the two edge classes
   uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
+  int a_ahead;       // halo chunks the A cursor may run ahead of the B cursor (1..kANum-1)
 };
 
 // Split-K factor chosen ON THE DEVICE from the device-side tile count (CUDA-graph safe).
@@ -91,9 +92,11 @@ __device__ __forceinline__ int choose_split(int tiles, int n_clusters, int kstep
 // Shared-memory plan.  Per-tap mode (HALO = false): a ring of kStages stages, each the A tile
 // of one (tap, 64-ch chunk) [128 rows x 128 B] plus its B tile [BN/CG rows x 128 B].
 // Halo mode (HALO = true, b = 8): an A ring of kANum slots, each holding the (b+2)^2 halos of
-// the CTA's BPT blocks for one 64-ch chunk, stored as halo rows of 10 px in 2048-B slots
-// ordered [y][block] (so the 8-row UMMA core groups are 1024-B aligned at stride 2048 and a
-// tap (dy,dx) is the start shift dy*BPT*2048 + dx*128), plus a B ring of kBNum (tap, chunk) tiles.
+// the CTA's blocks for one 64-ch chunk, stored densely as halo lines of 10 px x 128 B
+// (1280 B) ordered [line][block]; the 8-row UMMA core groups sit at stride 1280 B and a tap
+// (dy,dx) is the start shift dy*bpt*1280 + dx*128.  Valid because the SW128 XOR phase is
+// derived from absolute smem address bits (measured: base-offset field 0), exactly as TMA
+// writes it.  Plus a B ring of kBNum (tap, chunk) weight tiles.
 template <int BN, int CG, bool HALO, bool EDGE = false>
 struct ConvCfg {
   static constexpr int kBNc = BN / CG;  // B rows (output channels) held by this CTA
@@ -106,13 +109,16 @@ struct ConvCfg {
   static constexpr int kStagesFit = kAvail / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   // halo mode (BPT = 2 blocks of 8x8)
-  static constexpr int kHaloRow = 2048;
-  // full-block tiles use 10 lines x 2 blocks; edge tiles up to 8 blocks: 32 line slots
+  static constexpr int kHaloRow = 1280;
+  // full-block tiles: 10 lines x 2 blocks (+ the UMMA over-read of padding groups stays inside);
+  // edge tiles up to 8 blocks: 32 line slots
   static constexpr int kASlot = (EDGE ? 32 : 20) * kHaloRow;
-  static constexpr int kANum = 2;
-  static constexpr int kBNumFit = (kAvail - kANum * kASlot) / kStageB;
+  static constexpr int kANum = 3;
+  static constexpr int kBNumFit = (kAvail - kANum * kASlot - 1024) / kStageB;
   static constexpr int kBNum = kBNumFit > 16 ? 16 : kBNumFit;
-  static constexpr int kRingBytes = HALO ? kANum * kASlot + kBNum * kStageB : kStages * kStageBytes;
+  // halo A ring padded to 1 KB so the B ring (SW128, 1024-B atoms) stays aligned
+  static constexpr int kARing = (kANum * kASlot + 1023) / 1024 * 1024;
+  static constexpr int kRingBytes = HALO ? kARing + kBNum * kStageB : kStages * kStageBytes;
   static constexpr int kNumBars = HALO ? kANum + kBNum : kStages;
   static constexpr uint32_t kTmemCols = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (HALO ? Cfg::kANum * Cfg::kASlot : S * kStageA);
+  uint8_t* sB = smem + (HALO ? Cfg::kARing : S * kStageA);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes);
   uint64_t* empty = full + NB;
   uint64_t* tfull = empty + NB;
@@ -249,6 +255,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
   const int cluster_id = blockIdx.x / CG, n_clusters = gridDim.x / CG;
+  // ---- setup that needs no upstream data (overlaps the previous kernel's tail under PDL)
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if constexpr (EDGE) tma_prefetch(&tmC);
+    for (int s = 0; s < NB; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4 * CG);
+    }
+    mbar_init(red_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_cg2<Cfg::kTmemCols>(tmem_slot);
+    else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // ids, count, plan and x are produced upstream
+  pdl_trigger();
   const int count = *p.count;
   constexpr int BPT = kBM / (BLK * BLK);  // blocks per CTA tile (2 at b=8, 8 at b=4)
   constexpr int bb = BLK * BLK;
@@ -273,28 +305,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_full = nsplit > 1 ? tiles - rem : tiles;
   const int total = n_full + (nsplit > 1 ? rem * nsplit : 0);  // work units
 
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    for (int s = 0; s < NB; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);
-    }
-    mbar_init(red_bar, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    if constexpr (CG == 2) tmem_alloc_cg2<Cfg::kTmemCols>(tmem_slot);
-    else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
-  }
-  tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -304,30 +314,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       if constexpr (HALO) {
-        int bs = 0;  // B ring position
-        uint32_t bph = 0;
-        for (int u = cluster_id; u < total; u += n_clusters) {
-          const Unit U = decode_unit(u, n_full, nsplit);
-          const int t = U.t;
-          const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
-          const int kc0 = U.sk * p.kc / U.ns, kc1 = (U.sk + 1) * p.kc / U.ns;
-          const HaloTile g = halo_tile<CG>(mt, rank, nF, nB, list, nR, p);
-          int cx[8], cy[8], cn[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            // pad a short tile with a real block of the same class (computed, never stored)
-            const int j = min(g.j0 + i, g.nblk - 1);
-            int n = 0, by = 0, bx = 0;
-            if (i < g.bpt) decode_block(__ldg(g.list + j), p.hb, p.wb, n, by, bx);
-            cn[i] = n;
-            cy[i] = by * BLK - 1;
-            cx[i] = bx * BLK - 1;
+        // Two cursors over this CTA's flattened (unit, chunk) sequence: the A cursor (halo
+        // loads) runs up to kAhead chunks ahead of the B cursor (weight tiles), so a chunk's
+        // halo is requested long before its 9 taps' MMAs need it.  Before issuing B(c) the
+        // producer may wait only on A slots the MMA frees while consuming B(c-1) or earlier
+        // (otherwise the MMA would stall on B(c)): kAhead <= kANum - 1.
+        struct Cur {
+          int u, kc, kc1;  // unit, chunk, end chunk of the unit
+        };
+        auto cur_begin = [&](int u) {
+          Cur c{u, 0, 0};
+          if (u < total) {
+            const Unit U = decode_unit(u, n_full, nsplit);
+            c.kc = U.sk * p.kc / U.ns;
+            c.kc1 = (U.sk + 1) * p.kc / U.ns;
           }
-          const int n0 = nt * BN + rank * Cfg::kBNc;
-          const uint32_t a_bytes = (uint32_t)(g.lines * g.bpt * 10 * 128);  // real halo bytes
-          for (int kc = kc0; kc < kc1; ++kc) {
-            // A: the chunk's halos, one TMA line box {64 ch, 10 px} per halo line per block;
-            // line l of block i lands in 2048-B slot (l * bpt + i)
+          return c;
+        };
+        auto cur_next = [&](Cur& c) {
+          if (++c.kc >= c.kc1) c = cur_begin(c.u + n_clusters);
+        };
+        Cur ca = cur_begin(cluster_id), cb = ca;
+        const int kAhead = p.a_ahead;
+        int a_unit = -1;  // unit whose blocks are decoded in cx/cy/cn
+        int b_unit = -1, b_n0 = 0;
+        HaloTile g{};
+        int cx[8], cy[8], cn[8];
+        int ahead = 0;  // chunks the A cursor is ahead of the B cursor
+        int bs = 0;     // B ring position
+        uint32_t bph = 0;
+        while (cb.u < total) {
+          // ---- A: issue halos up to kANum-1 chunks ahead of the current B chunk
+          while (ca.u < total && ahead < kAhead) {
+            if (ca.u != a_unit) {  // new tile: decode its blocks once (kept in registers)
+              a_unit = ca.u;
+              const Unit U = decode_unit(ca.u, n_full, nsplit);
+              g = halo_tile<CG>(U.t / p.n_tiles_n, rank, nF, nB, list, nR, p);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                // pad a short tile with a real block of the same class (computed, never stored)
+                const int j = min(g.j0 + i, g.nblk - 1);
+                int n = 0, by = 0, bx = 0;
+                if (i < g.bpt) decode_block(__ldg(g.list + j), p.hb, p.wb, n, by, bx);
+                cn[i] = n;
+                cy[i] = by * BLK - 1;
+                cx[i] = bx * BLK - 1;
+              }
+            }
+            const uint32_t a_bytes = (uint32_t)(g.lines * g.bpt * 10 * 128);  // real halo bytes
+            // line l of block i lands in the (l * bpt + i)-th 1280-B line of the slot
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* a_dst = sA + stage * Cfg::kASlot;
             uint32_t bar;
@@ -345,25 +380,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* dst = a_dst + (l * g.bpt + i) * Cfg::kHaloRow;
                 const CUtensorMap* tm = g.tr ? &tmC : &tmA;
                 const int xx = g.tr ? cx[i] + l : cx[i], yy = g.tr ? cy[i] : cy[i] + l;
-                if constexpr (CG == 1) tma_load_4d_bar(tm, bar, dst, kc * kBK, xx, yy, cn[i], pol_a);
-                else tma_load_4d_cg2(tm, bar, dst, kc * kBK, xx, yy, cn[i], pol_a);
+                if constexpr (CG == 1) tma_load_4d_bar(tm, bar, dst, ca.kc * kBK, xx, yy, cn[i], pol_a);
+                else tma_load_4d_cg2(tm, bar, dst, ca.kc * kBK, xx, yy, cn[i], pol_a);
               }
             }
             if (++stage == Cfg::kANum) {
               stage = 0;
               phase ^= 1;
             }
-            // B: one (tap, chunk) weight tile per tap
+            cur_next(ca);
+            ++ahead;
+          }
+          // ---- B: one (tap, chunk) weight tile per tap of the B cursor's chunk
+          {
+            if (cb.u != b_unit) {
+              b_unit = cb.u;
+              const Unit U = decode_unit(cb.u, n_full, nsplit);
+              b_n0 = (U.t - (U.t / p.n_tiles_n) * p.n_tiles_n) * BN + rank * Cfg::kBNc;
+            }
+            const int n0 = b_n0;
             for (int tap = 0; tap < 9; ++tap) {
               uint64_t* bf = &full[Cfg::kANum + bs];
               mbar_wait(&empty[Cfg::kANum + bs], bph ^ 1);
               uint8_t* b_dst = sB + bs * Cfg::kStageB;
               if constexpr (CG == 1) {
                 mbar_arrive_expect_tx(bf, (uint32_t)Cfg::kStageB);
-                tma_load_3d(&tmB, bf, b_dst, kc * kBK, tap, n0, pol_b);
+                tma_load_3d(&tmB, bf, b_dst, cb.kc * kBK, tap, n0, pol_b);
               } else {
                 if (rank == 0) mbar_arrive_expect_tx(bf, (uint32_t)(2 * Cfg::kStageB));
-                tma_load_3d_cg2(&tmB, leader_addr(bf), b_dst, kc * kBK, tap, n0, pol_b);
+                tma_load_3d_cg2(&tmB, leader_addr(bf), b_dst, cb.kc * kBK, tap, n0, pol_b);
               }
               if (++bs == Cfg::kBNum) {
                 bs = 0;
@@ -371,6 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          cur_next(cb);
+          --ahead;
         }
       } else
       for (int u = cluster_id; u < total; u += n_clusters) {
@@ -683,45 +730,61 @@ __global__ void __launch_bounds__(1024) conv_plan_kernel(const int32_t* __restri
                                                          int wb, int has_b, int has_r,
                                                          int32_t* __restrict__ plan_ids,
                                                          int32_t* __restrict__ meta) {
-  __shared__ int warp_off[32];
-  __shared__ int round_total;
+  pdl_wait();
+  pdl_trigger();
+  // pass 1: class totals (so the class sub-lists' offsets are known); pass 2: scatter, with
+  // one ballot per class per round giving each id its in-class rank (order = list order)
+  __shared__ int tot[3];
+  __shared__ int warp_off[3][32];
+  __shared__ int round_tot[3];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int cnt = *count;
-  int base = 0;
-  for (int cls = 0; cls < 3; ++cls) {
-    const int cls_base = base;
-    for (int start = 0; start < cnt; start += blockDim.x) {
-      const int j = start + threadIdx.x;
-      bool take = false;
-      int id = 0;
-      if (j < cnt) {
-        id = __ldg(ids + j);
-        const int r = id % (hb * wb), by = r / wb, bx = r - (r / wb) * wb;
-        const bool bottom = has_b && by == hb - 1, right = has_r && bx == wb - 1;
-        take = (bottom ? 1 : (right ? 2 : 0)) == cls;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, take);
-      const int pre = __popc(bal & ((1u << lane) - 1u));
-      if (lane == 0) warp_off[warp] = __popc(bal);
-      __syncthreads();
-      if (warp == 0) {
-        const int v = lane < nwarps ? warp_off[lane] : 0;
-        int incl = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int o = __shfl_up_sync(0xffffffffu, incl, d);
-          if (lane >= d) incl += o;
-        }
-        if (lane < nwarps) warp_off[lane] = incl - v;
-        if (lane == 31) round_total = incl;
-      }
-      __syncthreads();
-      if (take) plan_ids[base + warp_off[warp] + pre] = id;
-      base += round_total;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) meta[cls] = base - cls_base;
+  if (threadIdx.x < 3) tot[threadIdx.x] = 0;
+  __syncthreads();
+  auto cls_of = [&](int id) {
+    const int r = id % (hb * wb), by = r / wb, bx = r - (r / wb) * wb;
+    return (has_b && by == hb - 1) ? 1 : ((has_r && bx == wb - 1) ? 2 : 0);
+  };
+  int local[3] = {0, 0, 0};
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) ++local[cls_of(__ldg(ids + j))];
+  for (int c = 0; c < 3; ++c) {
+    int v = local[c];
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane == 0 && v) atomicAdd(&tot[c], v);
   }
+  __syncthreads();
+  int base[3] = {0, tot[0], tot[0] + tot[1]};
+  for (int start = 0; start < cnt; start += blockDim.x) {
+    const int j = start + threadIdx.x;
+    int id = 0, c = -1;
+    if (j < cnt) {
+      id = __ldg(ids + j);
+      c = cls_of(id);
+    }
+    int pre = 0;
+    for (int k = 0; k < 3; ++k) {
+      const unsigned bal = __ballot_sync(0xffffffffu, c == k);
+      if (c == k) pre = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) warp_off[k][warp] = __popc(bal);
+    }
+    __syncthreads();
+    if (warp < 3) {  // warp k scans class k's per-warp counts
+      const int v = lane < nwarps ? warp_off[warp][lane] : 0;
+      int incl = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += o;
+      }
+      if (lane < nwarps) warp_off[warp][lane] = incl - v;
+      if (lane == 31) round_tot[warp] = incl;
+    }
+    __syncthreads();
+    if (c >= 0) plan_ids[base[c] + warp_off[c][warp] + pre] = id;
+    for (int k = 0; k < 3; ++k) base[k] += round_tot[k];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) meta[threadIdx.x] = tot[threadIdx.x];
 }
 
 // ------------------------------------------------------------------ host side
@@ -761,13 +824,15 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
@@ -905,6 +970,8 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.n_tiles_n = cdiv(c_out, bn);
   p.bpt = kBM / (block * block);
   p.halo = halo;
+  p.a_ahead = 2;
+  if (const char* env = getenv("SPHINX_A_AHEAD")) p.a_ahead = atoi(env) < 1 ? 1 : (atoi(env) > 2 ? 2 : atoi(env));
   p.desc_bo = 0;  // measured: the SW128 phase comes from absolute smem address bits
   if (const char* env = getenv("SPHINX_DESC_BO")) p.desc_bo = (uint32_t)atoi(env);
   p.ws_part = nullptr;
@@ -939,10 +1006,10 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   const int grid = cg * (int)(want < max_clusters ? want : max_clusters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (p.plan_ids) {
-    conv_plan_kernel<<<1, 1024, 0, s>>>(block_ids, count, hb, wb, p.rb != 0, p.cr != 0,
-                                        const_cast<int32_t*>(p.plan_ids),
-                                        const_cast<int32_t*>(p.plan_meta));
-    SPHINX_CHECK_LAUNCH();
+    cudaError_t e = launch_k(conv_plan_kernel, dim3(1), dim3(1024), 0, s, block_ids, count, hb, wb,
+                             (int)(p.rb != 0), (int)(p.cr != 0), const_cast<int32_t*>(p.plan_ids),
+                             const_cast<int32_t*>(p.plan_meta));
+    if (e != cudaSuccess) return cuda_fail(e);
   }
   switch (bn) {
     case 256: return launch_cg<256>(cg, ta, tb, tc, p, grid, s);
