@@ -38,6 +38,32 @@ MEAN_DENSITY = 0.25
 CONVS_PER_LEVEL = 2
 
 
+def ncu_traffic(kernel_sig):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes) of the conv launches whose
+    name contains kernel_sig, from the newest committed `ncu --set full` capture
+    (profiles/*_conv_full_raw.csv).  Returns (bytes or None, source file)."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_conv_full_raw.csv")))
+    if not files:
+        return None, None
+    rows = list(csv.reader(open(files[-1])))
+    if len(rows) < 3:
+        return None, None
+    hdr, units = rows[0], rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    vals = []
+    for r in rows[2:]:
+        if kernel_sig not in r[idx["Kernel Name"]]:
+            continue
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(r[idx[m]].replace(",", "")) * scale.get(units[idx[m]], 1)
+        vals.append(tot)
+    return (round(sum(vals) / len(vals)) if vals else None), os.path.basename(files[-1])
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -396,6 +422,8 @@ def run_gpu(args):
     dom_flops = dom["real_px"] * 2 * 9 * LEVELS[dom["level"]][1] ** 2
     achieved = dom_flops / (dom["conv_ms"] * 1e-3) / 1e12
     all_conv_tflops = flops / (conv_total_ms * 1e-3) / 1e12
+    bn_sig = {0: "<160, 2, 8, 1, 0>", 1: "<160, 2, 8, 1, 1>", 2: "<256, 2, 8, 1, 1>"}[dom["level"]]
+    traffic, traffic_src = ncu_traffic(bn_sig)
 
     # the same conv calls timed in isolation (graph of 20 back-to-back launches, L2-warm)
     iso = []
@@ -433,7 +461,8 @@ def run_gpu(args):
                          "achieved": round(achieved, 2), "peak": tc_peak, "unit": "TFLOP/s",
                          "frac": round(achieved / tc_peak, 4), "peak_kind": f"{peak_kind} bf16 burst",
                          "frac_sustained": round(achieved / tc_sust, 4) if tc_sust else None,
-                         "traffic": None, "all_convs_tflops": round(all_conv_tflops, 2),
+                         "traffic": traffic, "traffic_unit": "bytes per launch (dram read+write)",
+                         "traffic_source": traffic_src, "all_convs_tflops": round(all_conv_tflops, 2),
                          "conv_share_of_step": round(conv_total_ms / ms_all, 4)},
             "conv_levels": per_level,
             "conv_isolated_ms": iso,
