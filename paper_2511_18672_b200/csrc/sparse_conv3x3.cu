@@ -65,6 +65,7 @@ struct ConvParams {
   int bpt_b, bpt_r;          // blocks per CTA tile of the two edge classes
   uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
   int a_ahead;       // halo chunks the A cursor may run ahead of the B cursor (1..kANum-1)
+  int allow_streamk; // halo mode may use stream-K when it shortens the makespan
 };
 
 // Split-K factor chosen ON THE DEVICE from the device-side tile count (CUDA-graph safe).
@@ -124,7 +125,9 @@ struct ConvCfg {
                                         : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kSmem = 1024 + kRingBytes + kBarBytes;
   static_assert(HALO ? kBNum >= 3 : kStages >= 3, "pipeline too shallow");
-  static_assert((2 * kNumBars + 5) * 8 + 8 <= 512, "barrier area");
+  static_assert((2 * kNumBars + 6) * 8 + 8 <= 512, "barrier area");
+  // stream-K owner staging: 2 buffers x kMaxParts parts x (32 cols x 128 rows fp32)
+  static constexpr int kMaxParts = (kRingBytes / (2 * 32 * kBM * 4)) < 6 ? (kRingBytes / (2 * 32 * kBM * 4)) : 6;
   static_assert(kRingBytes >= (kBM + 16) * BN * 4, "split-K staging must fit the ring");
 };
 
@@ -190,6 +193,50 @@ __device__ __forceinline__ Unit decode_unit(int u, int n_full, int nsplit) {
   return r;
 }
 
+// A CTA's work as a sequence of segments (tile, chunk range [k0, k1), role).
+//  mode 0: units u = cluster + i * clusters: unsplit tiles (FULL) then the tail split units
+//          (SPLIT: co-resident rendezvous, distributed fixed-order reduction).
+//  mode 1: stream-K (halo mode): cluster c owns the contiguous range [c*W/C, (c+1)*W/C) of
+//          the flattened (tile, chunk) space, W = tiles * KC.  A tile cut by range boundaries
+//          has one OWNER (the cluster holding its chunk 0; that segment is the LAST of the
+//          owner's range) and PART contributors (each such segment is the FIRST of its range):
+//          parts park fp32 partials and signal, never wait; the owner waits at its very end,
+//          adds the parts in cluster order (deterministic) and stores.
+enum SegRole { kFull = 0, kSplit = 1, kPart = 2, kOwner = 3 };
+struct Seg {
+  int t, k0, k1, role, sk, ns, slot;
+};
+struct SegIter {
+  int mode, cluster, C, total, n_full, nsplit, kc;
+  long long x, hi, W;
+  __device__ __forceinline__ bool get(Seg& g) {
+    if (mode == 0) {
+      if (x >= total) return false;
+      const Unit U = decode_unit((int)x, n_full, nsplit);
+      g.t = U.t; g.sk = U.sk; g.ns = U.ns; g.slot = U.slot;
+      g.k0 = U.sk * kc / U.ns;
+      g.k1 = (U.sk + 1) * kc / U.ns;
+      g.role = U.ns > 1 ? kSplit : kFull;
+      return true;
+    }
+    if (x >= hi) return false;
+    g.t = (int)(x / kc);
+    g.k0 = (int)(x - (long long)g.t * kc);
+    g.k1 = (int)min((long long)kc, g.k0 + (hi - x));
+    g.role = (g.k0 == 0 && g.k1 == kc) ? kFull : (g.k0 == 0 ? kOwner : kPart);
+    g.sk = 0; g.ns = 1; g.slot = cluster;
+    return true;
+  }
+  __device__ __forceinline__ void next(const Seg& g) {
+    if (mode == 0) x += C;
+    else x += g.k1 - g.k0;
+  }
+};
+// cluster whose stream-K range contains flattened position xx: max{c : floor(c*W/C) <= xx}
+__device__ __forceinline__ int sk_cluster_of(long long xx, long long W, int C) {
+  return (int)(((xx + 1) * C - 1) / W);
+}
+
 // Halo-mode tile geometry.  Tiles are enumerated class-major: full 8x8 blocks (2 per CTA,
 // 10 halo rows each), then bottom-edge blocks (rb valid rows: rb+2 halo rows, up to 8 per
 // CTA), then right-edge blocks (cr valid columns, loaded as rb+2... columns: the tile is
@@ -247,8 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + NB;
   uint64_t* tfull = empty + NB;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
-  uint64_t* red_bar = tempty + 2;  // split-K partial staging barrier (one use per launch)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  uint64_t* red_bar = tempty + 2;  // [2] split-K / stream-K partial staging barriers
   // split-K: element offset of each tile row's output pixel (-1 = not stored), 8-byte aligned
   long long* pix_tab = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(full) + 512);
 
@@ -268,7 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
     }
-    mbar_init(red_bar, 1);
+    mbar_init(&red_bar[0], 1);
+    mbar_init(&red_bar[1], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -304,6 +352,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nsplit = rem > 0 ? choose_split(rem, n_clusters, ksteps, HALO ? p.kc : 16, p) : 1;
   const int n_full = nsplit > 1 ? tiles - rem : tiles;
   const int total = n_full + (nsplit > 1 ? rem * nsplit : 0);  // work units
+  // stream-K (halo mode) when it shortens the makespan (in chunk units, ~1 chunk of fixup)
+  int sk_mode = 0;
+  const long long Wk = (long long)tiles * p.kc;
+  if (HALO && p.ws_part != nullptr && p.allow_streamk && Wk >= n_clusters &&
+      n_clusters <= p.ws_slots && n_clusters * CG * 2 <= 1024) {
+    const long long q = Wk / n_clusters;  // chunks per cluster (floor)
+    // measured: the tail split's rendezvous + reduction costs ~2 chunks, stream-K's fixup ~1;
+    // stream-K is taken only on a clear modelled win (it measured worse at model ties)
+    const long long cost0 = nsplit > 1 ? (long long)(tiles / n_clusters) * p.kc + p.kc / nsplit + 2
+                                       : (long long)((tiles + n_clusters - 1) / n_clusters) * p.kc;
+    const long long cost1 = (Wk + n_clusters - 1) / n_clusters + 2;
+    if ((cost1 < cost0 || p.allow_streamk == 2) && (p.kc + q - 1) / q <= Cfg::kMaxParts) sk_mode = 1;
+  }
+  SegIter it0;
+  it0.mode = sk_mode; it0.cluster = cluster_id; it0.C = n_clusters; it0.total = total;
+  it0.n_full = n_full; it0.nsplit = nsplit; it0.kc = p.kc; it0.W = Wk;
+  it0.x = sk_mode ? (long long)cluster_id * Wk / n_clusters : cluster_id;
+  it0.hi = sk_mode ? (long long)(cluster_id + 1) * Wk / n_clusters : 0;
 
 
   if (warp == 0) {
@@ -320,36 +386,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         // producer may wait only on A slots the MMA frees while consuming B(c-1) or earlier
         // (otherwise the MMA would stall on B(c)): kAhead <= kANum - 1.
         struct Cur {
-          int u, kc, kc1;  // unit, chunk, end chunk of the unit
+          SegIter it;
+          Seg g;
+          int ok, kc;
         };
-        auto cur_begin = [&](int u) {
-          Cur c{u, 0, 0};
-          if (u < total) {
-            const Unit U = decode_unit(u, n_full, nsplit);
-            c.kc = U.sk * p.kc / U.ns;
-            c.kc1 = (U.sk + 1) * p.kc / U.ns;
-          }
-          return c;
+        auto cur_init = [&](Cur& c) {
+          c.it = it0;
+          c.ok = c.it.get(c.g);
+          c.kc = c.ok ? c.g.k0 : 0;
         };
         auto cur_next = [&](Cur& c) {
-          if (++c.kc >= c.kc1) c = cur_begin(c.u + n_clusters);
+          if (++c.kc >= c.g.k1) {
+            c.it.next(c.g);
+            c.ok = c.it.get(c.g);
+            c.kc = c.ok ? c.g.k0 : 0;
+          }
         };
-        Cur ca = cur_begin(cluster_id), cb = ca;
+        Cur ca, cb;
+        cur_init(ca);
+        cur_init(cb);
         const int kAhead = p.a_ahead;
-        int a_unit = -1;  // unit whose blocks are decoded in cx/cy/cn
-        int b_unit = -1, b_n0 = 0;
+        long long a_seg = -1;  // segment whose blocks are decoded in cx/cy/cn
+        long long b_seg = -1;
+        int b_n0 = 0;
         HaloTile g{};
         int cx[8], cy[8], cn[8];
         int ahead = 0;  // chunks the A cursor is ahead of the B cursor
         int bs = 0;     // B ring position
         uint32_t bph = 0;
-        while (cb.u < total) {
-          // ---- A: issue halos up to kANum-1 chunks ahead of the current B chunk
-          while (ca.u < total && ahead < kAhead) {
-            if (ca.u != a_unit) {  // new tile: decode its blocks once (kept in registers)
-              a_unit = ca.u;
-              const Unit U = decode_unit(ca.u, n_full, nsplit);
-              g = halo_tile<CG>(U.t / p.n_tiles_n, rank, nF, nB, list, nR, p);
+        while (cb.ok) {
+          // ---- A: issue halos up to kAhead chunks ahead of the current B chunk
+          while (ca.ok && ahead < kAhead) {
+            if (ca.it.x != a_seg) {  // new segment: decode its blocks once (kept in registers)
+              a_seg = ca.it.x;
+              g = halo_tile<CG>(ca.g.t / p.n_tiles_n, rank, nF, nB, list, nR, p);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 // pad a short tile with a real block of the same class (computed, never stored)
@@ -393,10 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // ---- B: one (tap, chunk) weight tile per tap of the B cursor's chunk
           {
-            if (cb.u != b_unit) {
-              b_unit = cb.u;
-              const Unit U = decode_unit(cb.u, n_full, nsplit);
-              b_n0 = (U.t - (U.t / p.n_tiles_n) * p.n_tiles_n) * BN + rank * Cfg::kBNc;
+            if (cb.it.x != b_seg) {
+              b_seg = cb.it.x;
+              b_n0 = (cb.g.t - (cb.g.t / p.n_tiles_n) * p.n_tiles_n) * BN + rank * Cfg::kBNc;
             }
             const int n0 = b_n0;
             for (int tap = 0; tap < 9; ++tap) {
@@ -484,10 +553,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (HALO) {
         int bs = 0;
         uint32_t bph = 0;
-        for (int u = cluster_id; u < total; u += n_clusters) {
-          const Unit U = decode_unit(u, n_full, nsplit);
-          const int kc0 = U.sk * p.kc / U.ns, kc1 = (U.sk + 1) * p.kc / U.ns;
-          const HaloTile g = halo_tile<CG>(U.t / p.n_tiles_n, 0, nF, nB, list, nR, p);
+        SegIter it = it0;
+        Seg sg;
+        for (; it.get(sg); it.next(sg)) {
+          const int kc0 = sg.k0, kc1 = sg.k1;
+          const HaloTile g = halo_tile<CG>(sg.t / p.n_tiles_n, 0, nF, nB, list, nR, p);
           const uint32_t line_stride = (uint32_t)(g.bpt * Cfg::kHaloRow);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
@@ -572,9 +642,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = cluster_id; u < total; u += n_clusters) {
-      const Unit U = decode_unit(u, n_full, nsplit);
-      const int t = U.t, sk = U.sk, ns = U.ns;
+    SegIter it = it0;
+    Seg sg;
+    for (; it.get(sg); it.next(sg)) {
+      const int t = sg.t, sk = sg.sk, ns = sg.ns;
+      const Unit U{sg.t, sg.sk, sg.ns, sg.slot};
       const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
       // tile row -> (block, pixel): per-tap mode rows are block-major (b^2 rows per block);
       // halo mode rows are [line q][block][8 px along the line] (group = q * bpt + block)
@@ -609,25 +681,79 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* part = nullptr;
       if (ns > 1)
         part = p.ws_part + (((size_t)(U.slot * ns + sk) * CG + rank) * kBM + row) * BN;
+      // stream-K part: column-major [BN][128] slot of this cluster (coalesced per column)
+      float* skpart = (sg.role == kPart)
+                          ? p.ws_part + ((size_t)cluster_id * CG + rank) * kBM * BN + row : nullptr;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (sg.role == kOwner) {
+        // ---- stream-K owner: wait for the parts of tile t, then add them chunk by chunk
+        const int c_last = sk_cluster_of((long long)(t + 1) * p.kc - 1, Wk, n_clusters);
+        const int n_parts = c_last - cluster_id;
+        int* cnt = p.ws_cnt + (cluster_id * CG + rank) * 2;
+        if (row == 0) {
+          int seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+            if (seen < n_parts) __nanosleep(64);
+          } while (seen < n_parts);
+          fence_proxy_async_global();
+        }
+        named_bar_sync(1, 128);
+        float* stage_buf = reinterpret_cast<float*>(sA);  // the operand ring is idle now
+        const uint32_t chunk_bytes = 32u * kBM * 4u;          // 32 columns x 128 rows, fp32
+        auto stage_chunk = [&](int c0, int buf) {             // issued by row 0 only
+          mbar_arrive_expect_tx(&red_bar[buf], chunk_bytes * (uint32_t)n_parts);
+          for (int j = 0; j < n_parts; ++j)
+            bulk_g2s(stage_buf + ((size_t)buf * Cfg::kMaxParts + j) * 32 * kBM,
+                     p.ws_part + ((size_t)(cluster_id + 1 + j) * CG + rank) * kBM * BN + (size_t)c0 * kBM,
+                     chunk_bytes, &red_bar[buf]);
+        };
+        if (row == 0) stage_chunk(0, 0);
+        uint32_t rph0 = 0, rph1 = 0;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
-        tc_wait_ld();
-        if (ns > 1) {
-          // split-K: park this split's fp32 partial row in the workspace
-#pragma unroll
-          for (int g = 0; g < 32; g += 4)
-            __stcg(reinterpret_cast<float4*>(part + c0 + g),
-                   make_float4(__uint_as_float(r[g]), __uint_as_float(r[g + 1]),
-                               __uint_as_float(r[g + 2]), __uint_as_float(r[g + 3])));
-        } else if (valid) {
+        for (int c0 = 0, ci = 0; c0 < BN; c0 += 32, ++ci) {
+          const int buf = ci & 1;
+          if (row == 0 && c0 + 32 < BN) stage_chunk(c0 + 32, buf ^ 1);  // prefetch next chunk
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
+          tc_wait_ld();
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          store_row_chunk(p, pix, nt * BN + c0, v);
+          mbar_wait(&red_bar[buf], buf ? rph1 : rph0);
+          if (buf) rph1 ^= 1; else rph0 ^= 1;
+          for (int j = 0; j < n_parts; ++j) {
+            const float* src = stage_buf + ((size_t)buf * Cfg::kMaxParts + j) * 32 * kBM + row;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += src[i * kBM];  // lanes = consecutive rows
+          }
+          if (valid) store_row_chunk(p, pix, nt * BN + c0, v);
+          named_bar_sync(1, 128);  // every thread done with buf before it is refilled
+        }
+        if (row == 0) cnt[0] = 0;  // leave the counter zeroed for the next launch
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
+          tc_wait_ld();
+          if (sg.role == kPart) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) __stcg(skpart + (size_t)(c0 + i) * kBM, __uint_as_float(r[i]));
+          } else if (ns > 1) {
+            // split-K: park this split's fp32 partial row in the workspace
+#pragma unroll
+            for (int g = 0; g < 32; g += 4)
+              __stcg(reinterpret_cast<float4*>(part + c0 + g),
+                     make_float4(__uint_as_float(r[g]), __uint_as_float(r[g + 1]),
+                                 __uint_as_float(r[g + 2]), __uint_as_float(r[g + 3])));
+          } else if (valid) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            store_row_chunk(p, pix, nt * BN + c0, v);
+          }
         }
       }
       tc_fence_before();
@@ -639,6 +765,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+      if (sg.role == kPart) {
+        // publish this part to the tile's owner (never waits)
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (row == 0) {
+          const int owner = sk_cluster_of((long long)t * p.kc, Wk, n_clusters);
+          atomicAdd(p.ws_cnt + (owner * CG + rank) * 2, 1);
+        }
       }
       if (ns > 1) {
         // Rendezvous of the ns units of tile t (all co-resident in this single round),
@@ -971,6 +1106,8 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.bpt = kBM / (block * block);
   p.halo = halo;
   p.a_ahead = 2;
+  p.allow_streamk = 1;
+  if (const char* env = getenv("SPHINX_CONV_STREAMK")) p.allow_streamk = atoi(env);  // 2 = force
   if (const char* env = getenv("SPHINX_A_AHEAD")) p.a_ahead = atoi(env) < 1 ? 1 : (atoi(env) > 2 ? 2 : atoi(env));
   p.desc_bo = 0;  // measured: the SW128 phase comes from absolute smem address bits
   if (const char* env = getenv("SPHINX_DESC_BO")) p.desc_bo = (uint32_t)atoi(env);

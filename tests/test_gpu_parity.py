@@ -166,15 +166,17 @@ def test_noise_vs_oracle(sphinx, shape, b):
 
 # ----------------------------------------------------------------- step 4
 
-@pytest.fixture(params=[(1, 0, 1, 1), (2, 0, 1, 1), (1, 1, 1, 1), (2, 1, 1, 1), (2, 1, 1, 0),
-                        (2, 0, 0, 0), (2, 1, 0, 0)],
+@pytest.fixture(params=[(1, 0, 1, 1, 1), (2, 0, 1, 1, 1), (1, 1, 1, 1, 1), (2, 1, 1, 1, 1),
+                        (2, 1, 1, 0, 1), (2, 0, 0, 0, 1), (2, 1, 0, 0, 1), (2, 1, 1, 1, 2),
+                        (1, 1, 1, 1, 2)],
                 ids=["cta1", "pair", "cta1-splitk", "pair-splitk", "pair-splitk-noedge", "pair-pertap",
-                     "pair-pertap-splitk"])
+                     "pair-pertap-splitk", "pair-streamk", "cta1-streamk"])
 def conv_cg(request, monkeypatch):
     """Runs a conv test with the 1-SM (cta_group::1) and the CTA-pair (cta_group::2) kernels,
     without and with device-chosen split-K, with halo-staged (b=8 default, with and without
-    edge-class packing) and per-tap A."""
-    cg, split, halo, edge = request.param
+    edge-class packing) and per-tap A, and with stream-K forced where feasible."""
+    cg, split, halo, edge, streamk = request.param
+    monkeypatch.setenv("SPHINX_CONV_STREAMK", str(streamk))
     monkeypatch.setenv("SPHINX_CONV_CG", str(cg))
     monkeypatch.setenv("SPHINX_CONV_SPLIT", str(split))
     monkeypatch.setenv("SPHINX_CONV_HALO", str(halo))
