@@ -17,6 +17,8 @@ Parity status per function:
   noise                                             pinned (TV-9..11, Monte Carlo)
   conv3x3_blocks / conv3x3_dense                    pinned (shift kernels, torch fp64 conv2d, linearity)
   scatter                                           pinned (density 0/1, composition O7)
+  ddim_step (NEXT-1)                                pinned (S:315 collapse to the clean latent,
+                                                    S:316 flat segment, eps-direction invariant)
 """
 import ctypes
 import os
@@ -81,6 +83,7 @@ def load():
             "oracle_conv3x3_blocks": [P, P, P, I, I, I, I, I, I, P, I, P, P, I],
             "oracle_conv3x3_dense": [P, P, P, I, I, I, I, I, P, P, I],
             "oracle_scatter": [P, I, P, P, I, I, I, I, I, I, P, P, I, P, I],
+            "oracle_ddim_step": [P, P, P, I, I, I, I, I, P, I, I, P, I],
         }
         for name, args in sig.items():
             fn = getattr(_lib, name)
@@ -241,4 +244,16 @@ def scatter(src, cache, b, mask=None, k=None, u=0, ids=None, src_layout=SRC_FULL
     cnt = 0 if ids is None else len(ids)
     _check(lib.oracle_scatter(_p(src), src_layout, _p(cache), _p(out), cache.dtype.itemsize,
                               n, h, w, c, b, _p(m), _p(kk), int(u), _p(ids), cnt), "scatter")
+    return out
+
+
+def ddim_step(z, x0_hat, b, ids, u, abar):
+    """NEXT-1 DDIM update on listed blocks, fp64; unlisted elements = z."""
+    lib = load()
+    z = _c(z, np.float32); x0_hat = _c(x0_hat, np.float32); ids = _c(ids, np.int32)
+    abar = _c(abar, np.float32)
+    n, h, w, c = z.shape
+    out = np.zeros(z.shape, np.float64)
+    _check(lib.oracle_ddim_step(_p(z), _p(x0_hat), _p(out), n, h, w, c, b, _p(ids), len(ids), int(u),
+                                _p(abar), len(abar) - 1), "ddim_step")
     return out

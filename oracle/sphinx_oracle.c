@@ -366,3 +366,34 @@ int oracle_scatter(const void* src, int src_layout, const void* cache, void* out
   }
   return 0;
 }
+
+/* -------------------------------------------------------------- NEXT-1 ---- */
+
+/* S:312 ddim_full_step / partial_step update: eps_hat = (z - sqrt(abar[u]) x0_hat) /
+ * sqrt(1 - abar[u]); z' = sqrt(abar[u+1]) x0_hat + sqrt(1 - abar[u+1]) eps_hat (eta = 0).
+ * Written in that order, in fp64. */
+int oracle_ddim_step(const float* z, const float* x0_hat, double* out, int n, int h, int w, int c,
+                     int b, const int32_t* ids, int count, int u, const float* abar,
+                     int total_steps) {
+  if (!z || !x0_hat || !out || !abar || n <= 0 || h <= 0 || w <= 0 || c <= 0 || b <= 0) return BAD;
+  if (count < 0 || (count > 0 && !ids) || total_steps < 2) return BAD;
+  if (u < 0 || u >= total_steps) return BAD;
+  size_t total = (size_t)n * h * w * c;
+  for (size_t e = 0; e < total; ++e) out[e] = (double)z[e];
+  int hb = (h + b - 1) / b, wb = (w + b - 1) / b;
+  double a0 = sqrt((double)abar[u]), s0 = sqrt(1.0 - (double)abar[u]);
+  double a1 = sqrt((double)abar[u + 1]), s1 = sqrt(1.0 - (double)abar[u + 1]);
+  for (int j = 0; j < count; ++j) {
+    int id = ids[j];
+    if (id < 0 || id >= n * hb * wb) return BAD;
+    int i = id / (hb * wb), by = (id / wb) % hb, bx = id % wb;
+    for (int y = by * b; y < by * b + b && y < h; ++y)
+      for (int x = bx * b; x < bx * b + b && x < w; ++x)
+        for (int ch = 0; ch < c; ++ch) {
+          size_t e = (((size_t)i * h + y) * w + x) * c + ch;
+          double eps_hat = ((double)z[e] - a0 * (double)x0_hat[e]) / s0;
+          out[e] = a1 * (double)x0_hat[e] + s1 * eps_hat;
+        }
+  }
+  return 0;
+}

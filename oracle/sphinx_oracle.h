@@ -107,6 +107,14 @@ int oracle_scatter(const void* src, int src_layout, const void* cache, void* out
                    const uint8_t* mask, const int32_t* k, int u,
                    const int32_t* ids, int count);
 
+/* NEXT-1. Deterministic DDIM update (eta = 0) on listed blocks (Alg1 line 18 D.partial_step's
+ * latent update): eps_hat = (z - sqrt(abar[u]) x0_hat) / sqrt(1 - abar[u]);
+ * z' = sqrt(abar[u+1]) x0_hat + sqrt(1 - abar[u+1]) eps_hat, fp64 (abar widened from fp32).
+ * 0 <= u < S.  out (double) receives z for elements not listed. */
+int oracle_ddim_step(const float* z, const float* x0_hat, double* out, int n, int h, int w, int c,
+                     int b, const int32_t* ids, int count, int u, const float* abar,
+                     int total_steps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -349,3 +349,56 @@ def test_scatter_density_0_1_and_composition():
         comp[j, :blk.shape[0], :blk.shape[1]] = blk
     got2 = oracle.scatter(comp, cache32, b, ids=ids, src_layout=oracle.SRC_COMPACT)
     assert np.array_equal(got2.view(np.uint32), want.view(np.uint32))
+
+
+# ------------------------------------------------------------- NEXT-1 DDIM update
+
+def test_ddim_collapses_to_clean_latent():
+    """with x0_hat = the true clean latent, running u from k to S collapses z to x0
+    (within 1e-5), for the cosine and linear schedules and several start steps."""
+    x0 = syn.latents_f32((2, 16, 16, 4), "ddim-x0")
+    eps = syn.latents_f32((2, 16, 16, 4), "ddim-eps")
+    ids = np.arange(2 * 16)  # every 4x4 block
+    for abar in (syn.abar_cosine(50), syn.abar_linear(50)):
+        for k in (0, 10, 25, 40, 49):
+            z = oracle.noise(x0, eps, x0, 4, ids, [k, k], abar).astype(np.float32)
+            for u in range(k, 50):
+                z = oracle.ddim_step(z, x0, 4, ids, u, abar).astype(np.float32)
+            assert np.max(np.abs(z - x0)) <= 1e-5
+
+
+def test_ddim_flat_segment_identity_and_last_step():
+    z = syn.latents_f32((1, 8, 8, 4), "ddim-z")
+    xh = syn.latents_f32((1, 8, 8, 4), "ddim-xh")
+    ids = np.arange(4)
+    abar = syn.abar_cosine(50).copy()
+    abar[11] = abar[10]                          # S:316 hypothetical flat segment
+    out = oracle.ddim_step(z, xh, 4, ids, 10, abar)
+    assert np.max(np.abs(out - z)) <= 1e-12
+    out = oracle.ddim_step(z, xh, 4, ids, 49, syn.abar_cosine(50))  # abar[S] = 1 -> x0_hat
+    assert np.array_equal(out, xh.astype(np.float64))
+
+
+def test_ddim_preserves_noise_direction_and_untouched():
+    """eta = 0: if z = sqrt(abar_u) x0_hat + sqrt(1-abar_u) e then z' = sqrt(abar_u+1) x0_hat +
+    sqrt(1-abar_u+1) e (up to the fp32 rounding of z); unlisted blocks keep z bitwise."""
+    abar = syn.abar_cosine(50)
+    xh = syn.latents_f32((2, 12, 12, 4), "ddim-dir-x")
+    e = syn.latents_f32((2, 12, 12, 4), "ddim-dir-e")
+    for u in (0, 13, 37, 48):
+        a0, s0 = np.sqrt(np.float64(abar[u])), np.sqrt(1 - np.float64(abar[u]))
+        a1, s1 = np.sqrt(np.float64(abar[u + 1])), np.sqrt(1 - np.float64(abar[u + 1]))
+        z = (a0 * xh + s0 * e).astype(np.float32)
+        ids = np.array([0, 4, 8, 9, 17])          # 3x3 blocks of 4 per frame, ragged
+        out = oracle.ddim_step(z, xh, 4, ids, u, abar)
+        want = a1 * xh + s1 * e
+        listed = np.zeros((2, 12, 12), bool)
+        for id_ in ids:
+            i, r = divmod(int(id_), 9)
+            by, bx = divmod(r, 3)
+            listed[i, by * 4:(by + 1) * 4, bx * 4:(bx + 1) * 4] = True
+        tol = 1e-6 * (s1 / s0) * np.abs(z) + 1e-12
+        assert np.all(np.abs(out - want)[listed] <= tol[listed])
+        assert np.array_equal(out[~listed].astype(np.float32), z[~listed])
+    with pytest.raises(ValueError):
+        oracle.ddim_step(z, xh, 4, [0], 50, abar)  # u must be < S
