@@ -226,6 +226,23 @@ SPHINX_API sphinx_status sphinx_scatter_cached(const void* src, sphinx_src_layou
                                     int32_t step_u, const int32_t* block_ids, const int32_t* count,
                                     sphinx_stream_t stream);
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-1. Partial-step latent update (Alg1 line 18; deterministic DDIM, eta = 0):
+ *   eps_hat = (z - sqrt(abar[u]) x0_hat) / sqrt(1 - abar[u])
+ *   z_out   = sqrt(abar[u+1]) x0_hat + sqrt(1 - abar[u+1]) eps_hat          (fp32)
+ * for every element of every real pixel of every listed block (the refined blocks of the
+ * active frames); other elements of z_out are untouched.  Inactive frames are resampled
+ * with sphinx_noise_inject at step u+1 (Alg1 line 19).
+ * z, x0_hat, z_out  NHWC fp32 [N][h][w][c] device; z_out may alias z.
+ * step_u            0 <= u < total_steps (u = 0 noisiest).
+ * abar              HOST fp32 [S+1] (read synchronously: the step is a scalar of the loop).
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_ddim_step(const float* z, const float* x0_hat, float* z_out,
+                                          int32_t n, int32_t h, int32_t w, int32_t c, int32_t block,
+                                          const int32_t* block_ids, const int32_t* count,
+                                          int32_t capacity, int32_t step_u, const float* abar,
+                                          int32_t total_steps, sphinx_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,8 @@ Parity status per function:
   scatter                                           pinned (density 0/1, composition O7)
   ddim_step (NEXT-1)                                pinned (S:315 collapse to the clean latent,
                                                     S:316 flat segment, eps-direction invariant)
+  laplacian_var / box_smooth / otsu / uncertainty   pinned (S:201-213 examples, brute-force Otsu
+    (NEXT-2)                                        argmax, variance identities)
 """
 import ctypes
 import os
@@ -84,6 +86,11 @@ def load():
             "oracle_conv3x3_dense": [P, P, P, I, I, I, I, I, P, P, I],
             "oracle_scatter": [P, I, P, P, I, I, I, I, I, I, P, P, I, P, I],
             "oracle_ddim_step": [P, P, P, I, I, I, I, I, P, I, I, P, I],
+            "oracle_laplacian_var": [P, I, I, I, I, P],
+            "oracle_box_smooth": [P, I, I, I, I, P],
+            "oracle_otsu": [P, ctypes.c_long, P],
+            "oracle_otsu_f64": [P, ctypes.c_long, P],
+            "oracle_uncertainty": [P, I, I, I, I, I, P, P],
         }
         for name, args in sig.items():
             fn = getattr(_lib, name)
@@ -257,3 +264,49 @@ def ddim_step(z, x0_hat, b, ids, u, abar):
     _check(lib.oracle_ddim_step(_p(z), _p(x0_hat), _p(out), n, h, w, c, b, _p(ids), len(ids), int(u),
                                 _p(abar), len(abar) - 1), "ddim_step")
     return out
+
+
+def laplacian_var(rgb, window=7):
+    lib = load()
+    rgb = _c(rgb, np.float32)
+    n, h, w, _ = rgb.shape
+    B = np.zeros((n, h, w))
+    _check(lib.oracle_laplacian_var(_p(rgb), n, h, w, window, _p(B)), "laplacian_var")
+    return B
+
+
+def box_smooth(x, k=5):
+    lib = load()
+    x = _c(x, np.float64)
+    n, h, w = x.shape
+    out = np.zeros_like(x)
+    _check(lib.oracle_box_smooth(_p(x), n, h, w, k, _p(out)), "box_smooth")
+    return out
+
+
+def otsu(values):
+    """tau for one grid (float32 values, the kernel's precision) -- NEXT-2c."""
+    lib = load()
+    v = _c(values, np.float32).ravel()
+    tau = np.zeros(1, np.float32)
+    _check(lib.oracle_otsu(_p(v), v.size, _p(tau)), "otsu")
+    return float(tau[0])
+
+
+def otsu_f64(values):
+    lib = load()
+    v = _c(values, np.float64).ravel()
+    tau = np.zeros(1, np.float32)
+    _check(lib.oracle_otsu_f64(_p(v), v.size, _p(tau)), "otsu_f64")
+    return float(tau[0])
+
+
+def uncertainty(rgb, window=7, smooth=5):
+    """(U fp64 [n,h,w], tau fp32 [n]) -- NEXT-2."""
+    lib = load()
+    rgb = _c(rgb, np.float32)
+    n, h, w, _ = rgb.shape
+    U = np.zeros((n, h, w))
+    tau = np.zeros(n, np.float32)
+    _check(lib.oracle_uncertainty(_p(rgb), n, h, w, window, smooth, _p(U), _p(tau)), "uncertainty")
+    return U, tau

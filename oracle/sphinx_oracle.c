@@ -397,3 +397,158 @@ int oracle_ddim_step(const float* z, const float* x0_hat, double* out, int n, in
   }
   return 0;
 }
+
+/* -------------------------------------------------------------- NEXT-2 ---- */
+
+static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+int oracle_laplacian_var(const float* rgb, int n, int h, int w, int window, double* B) {
+  if (!rgb || !B || n <= 0 || h <= 0 || w <= 0) return BAD;
+  if (window < 3 || window % 2 == 0) return BAD; /* S:199 even window -> invalid */
+  size_t plane = (size_t)h * w;
+  double* Y = (double*)malloc(plane * sizeof(double));
+  double* L = (double*)malloc(plane * sizeof(double));
+  if (!Y || !L) { free(Y); free(L); return -2; }
+  int r = window / 2;
+  for (int i = 0; i < n; ++i) {
+    /* luminance (R-23) */
+    for (size_t p = 0; p < plane; ++p) {
+      const float* px = rgb + ((size_t)i * plane + p) * 3;
+      Y[p] = 0.299 * (double)px[0] + 0.587 * (double)px[1] + 0.114 * (double)px[2];
+    }
+    /* 3x3 Laplacian with edge replication */
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) {
+        double up = Y[(size_t)clampi(y - 1, 0, h - 1) * w + x];
+        double dn = Y[(size_t)clampi(y + 1, 0, h - 1) * w + x];
+        double lf = Y[(size_t)y * w + clampi(x - 1, 0, w - 1)];
+        double rt = Y[(size_t)y * w + clampi(x + 1, 0, w - 1)];
+        L[(size_t)y * w + x] = up + dn + lf + rt - 4.0 * Y[(size_t)y * w + x];
+      }
+    /* population variance over the window (two-pass: mean, then mean squared deviation) */
+    double cnt = (double)window * window;
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) {
+        double mean = 0.0;
+        for (int dy = -r; dy <= r; ++dy)
+          for (int dx = -r; dx <= r; ++dx)
+            mean += L[(size_t)clampi(y + dy, 0, h - 1) * w + clampi(x + dx, 0, w - 1)];
+        mean /= cnt;
+        double var = 0.0;
+        for (int dy = -r; dy <= r; ++dy)
+          for (int dx = -r; dx <= r; ++dx) {
+            double d = L[(size_t)clampi(y + dy, 0, h - 1) * w + clampi(x + dx, 0, w - 1)] - mean;
+            var += d * d;
+          }
+        B[(size_t)i * plane + (size_t)y * w + x] = var / cnt;
+      }
+  }
+  free(Y); free(L);
+  return 0;
+}
+
+int oracle_box_smooth(const double* in, int n, int h, int w, int k, double* out) {
+  if (!in || !out || n <= 0 || h <= 0 || w <= 0 || k < 1 || k % 2 == 0) return BAD;
+  int r = k / 2;
+  size_t plane = (size_t)h * w;
+  for (int i = 0; i < n; ++i)
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) {
+        double s = 0.0;
+        for (int dy = -r; dy <= r; ++dy)
+          for (int dx = -r; dx <= r; ++dx)
+            s += in[(size_t)i * plane + (size_t)clampi(y + dy, 0, h - 1) * w + clampi(x + dx, 0, w - 1)];
+        out[(size_t)i * plane + (size_t)y * w + x] = s / ((double)k * k);
+      }
+  return 0;
+}
+
+typedef unsigned __int128 u128;
+
+/* Between-class variance of the split after bin k, exactly:  with n0, n1 the class counts,
+ * N = n0 + n1, S0 the sum of class-0 bin indices and S the total, sigma_b^2 * N^2 =
+ * (n0 S - N S0)^2 / (n0 n1).  Returned as quotient + remainder over den = n0 n1. */
+static void otsu_score(const long long* hist, int k, long long N, long long S, u128* q, u128* rem,
+                       u128* den) {
+  long long n0 = 0, s0 = 0;
+  for (int i = 0; i <= k; ++i) { n0 += hist[i]; s0 += (long long)i * hist[i]; }
+  long long n1 = N - n0;
+  if (n0 == 0 || n1 == 0) { *q = 0; *rem = 0; *den = 1; return; }
+  __int128 d = (__int128)n0 * S - (__int128)N * s0;
+  u128 num = (u128)(d < 0 ? -d : d);
+  num = num * num;
+  *den = (u128)n0 * (u128)n1;
+  *q = num / *den;
+  *rem = num % *den;
+}
+
+static int otsu_from_hist(const long long* hist, float vmax, float* tau) {
+  long long N = 0, S = 0;
+  int nonempty = 0;
+  for (int i = 0; i < 256; ++i) { N += hist[i]; S += (long long)i * hist[i]; nonempty += hist[i] > 0; }
+  if (N <= 0) return BAD;
+  if (nonempty <= 1) { *tau = vmax; return 0; } /* constant grid: nothing above */
+  int best = 0;
+  u128 bq, br, bd;
+  otsu_score(hist, 0, N, S, &bq, &br, &bd);
+  for (int k = 1; k < 255; ++k) {
+    u128 q, r, d;
+    otsu_score(hist, k, N, S, &q, &r, &d);
+    /* strictly greater only: ties go to the smaller k */
+    if (q > bq || (q == bq && r * bd > br * d)) { best = k; bq = q; br = r; bd = d; }
+  }
+  *tau = (float)(best + 1) / 256.0f;
+  return 0;
+}
+
+static int bin_of(double v) {
+  /* bin i = (i/256, (i+1)/256]; v * 256 is exact in binary floating point */
+  double t = ceil(v * 256.0) - 1.0;
+  if (t < 0.0) t = 0.0;
+  if (t > 255.0) t = 255.0;
+  return (int)t;
+}
+
+int oracle_otsu(const float* values, long count, float* tau) {
+  if (!values || !tau || count <= 0) return BAD;
+  long long hist[256] = {0};
+  float vmax = values[0];
+  for (long j = 0; j < count; ++j) {
+    hist[bin_of((double)values[j])]++;
+    if (values[j] > vmax) vmax = values[j];
+  }
+  return otsu_from_hist(hist, vmax, tau);
+}
+
+int oracle_otsu_f64(const double* values, long count, float* tau) {
+  if (!values || !tau || count <= 0) return BAD;
+  long long hist[256] = {0};
+  double vmax = values[0];
+  for (long j = 0; j < count; ++j) {
+    hist[bin_of(values[j])]++;
+    if (values[j] > vmax) vmax = values[j];
+  }
+  return otsu_from_hist(hist, (float)vmax, tau);
+}
+
+int oracle_uncertainty(const float* rgb, int n, int h, int w, int window, int smooth, double* U,
+                       float* tau) {
+  if (!rgb || !U || !tau || n <= 0 || h <= 0 || w <= 0) return BAD;
+  size_t plane = (size_t)h * w;
+  double* B = (double*)malloc((size_t)n * plane * sizeof(double));
+  if (!B) return -2;
+  int rc = oracle_laplacian_var(rgb, n, h, w, window, B);         /* Alg1 line 7 */
+  if (rc == 0) rc = oracle_box_smooth(B, n, h, w, smooth, U);     /* "smoothed" */
+  for (int i = 0; rc == 0 && i < n; ++i) {
+    double* u = U + (size_t)i * plane;
+    double lo = u[0], hi = u[0];
+    for (size_t p = 0; p < plane; ++p) { if (u[p] < lo) lo = u[p]; if (u[p] > hi) hi = u[p]; }
+    for (size_t p = 0; p < plane; ++p) {
+      double nrm = hi > lo ? (u[p] - lo) / (hi - lo) : 0.0;       /* "normalized" */
+      u[p] = 1.0 - nrm;                                           /* "inverted" */
+    }
+    rc = oracle_otsu_f64(u, (long)plane, &tau[i]);                /* Alg1 line 8 "otsu" */
+  }
+  free(B);
+  return rc;
+}

@@ -115,6 +115,31 @@ int oracle_ddim_step(const float* z, const float* x0_hat, double* out, int n, in
                      int b, const int32_t* ids, int count, int u, const float* abar,
                      int total_steps);
 
+/* NEXT-2a. Laplacian blur map (Alg1 line 7 laplacian_var):
+ * luminance Y = 0.299 R + 0.587 G + 0.114 B (reading R-23) of NHWC rgb [n][h][w][3] ->
+ * 3x3 Laplacian [[0,1,0],[1,-4,1],[0,1,0]] with edge replication -> population variance of the
+ * Laplacian over the window x window neighbourhood (edge replication).  fp64 out [n][h][w].
+ * window odd >= 3. */
+int oracle_laplacian_var(const float* rgb, int n, int h, int w, int window, double* B);
+
+/* NEXT-2b. k x k box mean with edge replication ("smoothed"; S:217 5x5). */
+int oracle_box_smooth(const double* in, int n, int h, int w, int k, double* out);
+
+/* NEXT-2c. Otsu threshold of `count` values in [0,1] (Alg1 line 8; S:205-214;
+ * reading R-24): 256 bins, bin i = (i/256, (i+1)/256] (bin 0 also holds 0); split after bin
+ * k (class 0 = bins <= k, i.e. v <= (k+1)/256), between-class variance maximised EXACTLY
+ * (integer histogram, 128-bit rational comparison), ties to the smaller k; tau = (k+1)/256.
+ * Degenerate (one non-empty bin): tau = max value, so no value is above it. */
+int oracle_otsu(const float* values, long count, float* tau);
+int oracle_otsu_f64(const double* values, long count, float* tau);
+
+/* NEXT-2. The uncertainty producer (Alg1 lines 7-8; "smoothed, normalized, and
+ * inverted, followed by Otsu"): B = laplacian_var(rgb), S = box(B, smooth), per frame
+ * N = (S - min S)/(max S - min S) (constant -> 0), U = 1 - N, tau[n] = otsu(U[n]).
+ * U fp64 [n][h][w]; tau fp32 [n].  The blur mask is U > tau (1 = blurry). */
+int oracle_uncertainty(const float* rgb, int n, int h, int w, int window, int smooth, double* U,
+                       float* tau);
+
 #ifdef __cplusplus
 }
 #endif

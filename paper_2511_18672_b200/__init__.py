@@ -26,7 +26,7 @@ MAX_LOGICS = 8
 ABI_VERSION = 1
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
-           "sphinx_conv_workspace_size", "sphinx_scatter_cached")
+           "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step")
 
 _lib = None
 
@@ -82,6 +82,7 @@ def load(path=SO_PATH):
         "sphinx_sparse_conv3x3": ([P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_conv_workspace_size": ([I, I, I, I, I, I], Z),
         "sphinx_scatter_cached": ([P, I, P, P, I, I, I, I, I, I, P, P, I, P, P, P], I),
+        "sphinx_ddim_step": ([P, P, P, I, I, I, I, I, P, P, I, I, P, I, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -247,3 +248,22 @@ def sphinx_scatter_cached(src, cache, out, block, block_mask=None, start_step=No
                                       n, h, w, c, int(block), _ptr(block_mask), _ptr(start_step),
                                       int(step_u), _ptr(block_ids), _ptr(count), _stream(stream))
     _chk("sphinx_scatter_cached", rc)
+
+
+def sphinx_ddim_step(z, x0_hat, z_out, block, block_ids, count, step_u, abar_host, capacity=None,
+                     stream=None):
+    """NEXT-1 (Alg1 line 18, S:312).  z/x0_hat/z_out NHWC fp32 [N,H,W,C] on the device;
+    abar_host: numpy fp32 [S+1] (host: the step u is a loop scalar)."""
+    import numpy as np
+    import torch
+    for t, nm in ((z, "z"), (x0_hat, "x0_hat"), (z_out, "z_out")):
+        _dev(t, torch.float32, nm)
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    ab = np.ascontiguousarray(abar_host, dtype=np.float32)
+    n, h, w, c = z.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = load().sphinx_ddim_step(_ptr(z), _ptr(x0_hat), _ptr(z_out), n, h, w, c, int(block),
+                                 _ptr(block_ids), _ptr(count), int(cap), int(step_u),
+                                 ab.ctypes.data_as(ctypes.c_void_p), len(ab) - 1, _stream(stream))
+    _chk("sphinx_ddim_step", rc)

@@ -343,3 +343,28 @@ def test_invalid_arguments_raise(sphinx):
     with pytest.raises(sphinx.SphinxError):
         sphinx.sphinx_block_mask(T(np.ones((1, 16, 16), np.float32)), None, None, 2.0, 1, 4,
                                  [torch.zeros((1, 4, 4), dtype=torch.uint8, device=dev)])
+
+
+# ----------------------------------------------------------------- NEXT-1 DDIM update
+
+@pytest.mark.parametrize("shape,b", [((21, 72, 72, 4), 8), ((3, 18, 18, 4), 8), ((2, 16, 16, 3), 4)])
+@pytest.mark.parametrize("u", [0, 17, 40, 49])
+def test_ddim_step_vs_oracle(sphinx, shape, b, u):
+    n, h, w, c = shape
+    hb, wb = -(-h // b), -(-w // b)
+    rg = syn.rng("gpu-ddim", shape, u)
+    m = (rg.random((n, hb, wb)) < 0.4).astype(np.uint8)
+    ids = oracle.compact(m)
+    abar = syn.abar_cosine(50)
+    z, xh = syn.latents_f32(shape, "gd-z"), syn.latents_f32(shape, "gd-x")
+    want = oracle.ddim_step(z, xh, b, ids, u, abar)
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, None, 0)
+    out = T(z)  # in place: z_out aliases z
+    sphinx.sphinx_ddim_step(out, T(xh), out, b, g_ids, g_cnt, u, abar)
+    got = out.cpu().numpy()
+    a0, s0 = np.sqrt(np.float64(abar[u])), np.sqrt(1 - np.float64(abar[u]))
+    a1, s1 = np.sqrt(np.float64(abar[u + 1])), np.sqrt(1 - np.float64(abar[u + 1]))
+    tol = 1e-6 * (np.abs(a1 * xh) + (s1 / s0) * (np.abs(z) + np.abs(a0 * xh))) + 1e-30
+    assert np.all(np.abs(got - want) <= tol), np.max(np.abs(got - want) / tol)
+    untouched = want == z.astype(np.float64)
+    assert np.array_equal(got[untouched], z[untouched])

@@ -402,3 +402,101 @@ def test_ddim_preserves_noise_direction_and_untouched():
         assert np.array_equal(out[~listed].astype(np.float32), z[~listed])
     with pytest.raises(ValueError):
         oracle.ddim_step(z, xh, 4, [0], 50, abar)  # u must be < S
+
+
+# ------------------------------------------------------- NEXT-2 uncertainty producer
+
+def _rgb(shape, tag):
+    return syn.rng("rgb", tag, shape).uniform(0, 1, size=shape + (3,)).astype(np.float32)
+
+
+def test_laplacian_var_constant_and_point():
+    """S:201 constant image -> all-zero map; S:202 a single bright pixel -> the map is largest
+    around it and exactly zero where the window cannot see the Laplacian's support."""
+    const = np.full((1, 12, 9, 3), 0.37, np.float32)
+    assert np.all(oracle.laplacian_var(const, 7) == 0.0)
+    img = np.zeros((1, 21, 21, 3), np.float32)
+    img[0, 10, 10, :] = 1.0
+    B = oracle.laplacian_var(img, 7)[0]
+    yy, xx = np.mgrid[0:21, 0:21]
+    cheb = np.maximum(np.abs(yy - 10), np.abs(xx - 10))
+    assert np.all(B[cheb > 4] == 0.0) and np.all(B[cheb <= 3] > 0)
+    assert B.argmax() // 21 in range(6, 15)
+    # mirror symmetry of the configuration (to summation-order rounding)
+    assert np.allclose(B, B[::-1, ::-1], rtol=1e-12, atol=0) and np.allclose(B, B.T, rtol=1e-12, atol=0)
+    for k in range(20):  # S:203 non-negative
+        assert oracle.laplacian_var(_rgb((2, 17, 13), f"nn{k}"), 3 + 2 * (k % 3)).min() >= 0.0
+    with pytest.raises(ValueError):
+        oracle.laplacian_var(img, 6)  # S:199 even window
+
+
+def test_laplacian_var_and_box_match_scipy_ndimage():
+    """Library cross-check: scipy.ndimage.laplace / uniform_filter with mode='nearest'
+    (= edge replication) give the same Laplacian variance and box mean in fp64."""
+    nd = pytest.importorskip("scipy.ndimage")
+    rgb = _rgb((2, 23, 31), "scipy")
+    Y = rgb.astype(np.float64) @ np.array([0.299, 0.587, 0.114])
+    for win in (3, 7):
+        B = oracle.laplacian_var(rgb, win)
+        for i in range(2):
+            L = nd.laplace(Y[i], mode="nearest")
+            m1 = nd.uniform_filter(L, win, mode="nearest")
+            m2 = nd.uniform_filter(L * L, win, mode="nearest")
+            assert np.max(np.abs(B[i] - (m2 - m1 * m1))) <= 1e-9 * max(1.0, m2.max())
+    S = oracle.box_smooth(B, 5)
+    for i in range(2):
+        assert np.max(np.abs(S[i] - nd.uniform_filter(B[i], 5, mode="nearest"))) <= 1e-12 * B.max()
+
+
+def _brute_otsu(v):
+    """Exhaustive search over the 255 splits of the 256-bin histogram (bin i = (i/256,(i+1)/256],
+    R-24), between-class variance in fp64, first maximum."""
+    b = np.clip(np.ceil(v.astype(np.float64) * 256) - 1, 0, 255).astype(int)
+    if len(np.unique(b)) == 1:
+        return float(v.max())
+    best, bk = -1.0, 0
+    for k in range(255):
+        c0, c1 = b[b <= k], b[b > k]
+        if len(c0) == 0 or len(c1) == 0:
+            s = 0.0
+        else:
+            w0, w1 = len(c0) / len(b), len(c1) / len(b)
+            s = w0 * w1 * (c0.mean() - c1.mean()) ** 2
+        if s > best:
+            best, bk = s, k
+    return (bk + 1) / 256.0
+
+
+def test_otsu_spec_examples_and_brute_force():
+    v = np.concatenate([np.full(500, 0.1), np.full(500, 0.9)]).astype(np.float32)   # S:211
+    tau = oracle.otsu(v)
+    assert 0.1 < tau <= 0.9 and np.array_equal(v > tau, np.arange(1000) >= 500)
+    assert oracle.otsu(np.full(64, 0.5, np.float32)) == 0.5                          # S:212
+    assert not np.any(np.full(64, 0.5, np.float32) > 0.5)
+    rg = syn.rng("pin-otsu")
+    for t in range(50):                                                                # S:213
+        kind = t % 3
+        if kind == 0:
+            v = rg.random(400)
+        elif kind == 1:
+            v = np.concatenate([rg.normal(0.3, 0.05, 300), rg.normal(0.7, 0.1, 200)])
+        else:
+            v = rg.beta(0.5, 2.0, 700)
+        v = np.clip(v, 0, 1).astype(np.float32)
+        assert oracle.otsu(v) == np.float32(_brute_otsu(v)), t
+    with pytest.raises(ValueError):
+        oracle.otsu(np.zeros(0, np.float32))
+
+
+def test_uncertainty_blur_mask_properties():
+    """S:219 constant map -> empty mask; S:220 half sharp checkerboard / half flat gray ->
+    the mask (U > tau: 1 = blurry) covers the flat half and not the sharp half (>= 95%)."""
+    U, tau = oracle.uncertainty(np.full((1, 32, 32, 3), 0.4, np.float32))
+    assert np.all(U == 1.0) and tau[0] == 1.0 and not np.any(U > tau[0])
+    img = np.full((1, 64, 64, 3), 0.5, np.float32)
+    yy, xx = np.mgrid[0:64, 0:32]
+    img[0, :, :32, :] = ((yy + xx) % 2)[..., None].astype(np.float32)
+    U, tau = oracle.uncertainty(img)
+    m = U[0] > tau[0]
+    assert m[:, 40:].mean() >= 0.95 and m[:, :24].mean() <= 0.05
+    assert set(np.unique(m)) <= {False, True}
