@@ -243,6 +243,28 @@ SPHINX_API sphinx_status sphinx_ddim_step(const float* z, const float* x0_hat, f
                                           int32_t capacity, int32_t step_u, const float* abar,
                                           int32_t total_steps, sphinx_stream_t stream);
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-2. Uncertainty (blur) producer feeding step (1) (Alg1 lines 7-8; "smoothed,
+ * normalized, and inverted, followed by Otsu thresholding"; constants S:196-222, R-23/R-24):
+ *   Y = 0.299 R + 0.587 G + 0.114 B; L = 3x3 Laplacian [[0,1,0],[1,-4,1],[0,1,0]] (edge
+ *   replication); V = population variance of L over window x window (edge replication);
+ *   S = smooth x smooth box mean of V; U = 1 - (S - min S)/(max S - min S) per frame
+ *   (constant S -> U = 1); tau_u[n] = Otsu over 256 bins, bin i = (i/256, (i+1)/256],
+ *   exact between-class-variance argmax, ties to the lower split, tau = (k+1)/256; a frame
+ *   whose U occupies one bin gets tau = 1 (= max U: no pixel is blurry).
+ * The outputs are exactly sphinx_block_mask's (uncertainty, tau_u): blurry iff U > tau_u.
+ * rgb          NHWC fp32 [N][h][w][3] device (the regression frames X, values in [0,1]).
+ * window       odd, 3..15 (SPEC default 7); smooth: odd, 1..15 (SPEC default 5).
+ * uncertainty  fp32 [N][h][w] device out; tau_u: fp32 [N] device out.
+ * workspace    device scratch of sphinx_uncertainty_workspace_size(N) bytes (re-initialised
+ *              by every call on `stream`).
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_uncertainty_map(const float* rgb, int32_t n, int32_t h, int32_t w,
+                                                int32_t window, int32_t smooth, float* uncertainty,
+                                                float* tau_u, void* workspace, size_t workspace_bytes,
+                                                sphinx_stream_t stream);
+SPHINX_API size_t sphinx_uncertainty_workspace_size(int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,8 @@ MAX_LOGICS = 8
 ABI_VERSION = 1
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
-           "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step")
+           "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
+           "sphinx_uncertainty_map", "sphinx_uncertainty_workspace_size")
 
 _lib = None
 
@@ -83,6 +84,8 @@ def load(path=SO_PATH):
         "sphinx_conv_workspace_size": ([I, I, I, I, I, I], Z),
         "sphinx_scatter_cached": ([P, I, P, P, I, I, I, I, I, I, P, P, I, P, P, P], I),
         "sphinx_ddim_step": ([P, P, P, I, I, I, I, I, P, P, I, I, P, I, P], I),
+        "sphinx_uncertainty_map": ([P, I, I, I, I, I, P, P, P, Z, P], I),
+        "sphinx_uncertainty_workspace_size": ([I], Z),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -267,3 +270,25 @@ def sphinx_ddim_step(z, x0_hat, z_out, block, block_ids, count, step_u, abar_hos
                                  _ptr(block_ids), _ptr(count), int(cap), int(step_u),
                                  ab.ctypes.data_as(ctypes.c_void_p), len(ab) - 1, _stream(stream))
     _chk("sphinx_ddim_step", rc)
+
+
+def sphinx_uncertainty_map(rgb, uncertainty, tau_u, window=7, smooth=5, workspace=None, stream=None):
+    """NEXT-2 (Alg1 lines 7-8).  rgb NHWC fp32 [N,H,W,3] -> uncertainty fp32 [N,H,W],
+    tau_u fp32 [N] (the inputs of sphinx_block_mask).  workspace: uint8 CUDA tensor or None
+    (a cached one per device is used)."""
+    import torch
+    _dev(rgb, torch.float32, "rgb")
+    _dev(uncertainty, torch.float32, "uncertainty")
+    _dev(tau_u, torch.float32, "tau_u")
+    n, h, w, c = rgb.shape
+    if c != 3:
+        raise ValueError("rgb: [N,H,W,3]")
+    if workspace is None:
+        key = ("unc", rgb.device, n)
+        workspace = _ws_cache.get(key)
+        if workspace is None:
+            nbytes = int(load().sphinx_uncertainty_workspace_size(int(n)))
+            workspace = _ws_cache[key] = torch.zeros(nbytes, dtype=torch.uint8, device=rgb.device)
+    rc = load().sphinx_uncertainty_map(_ptr(rgb), n, h, w, int(window), int(smooth), _ptr(uncertainty),
+                                       _ptr(tau_u), _ptr(workspace), workspace.numel(), _stream(stream))
+    _chk("sphinx_uncertainty_map", rc)

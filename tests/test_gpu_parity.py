@@ -368,3 +368,65 @@ def test_ddim_step_vs_oracle(sphinx, shape, b, u):
     assert np.all(np.abs(got - want) <= tol), np.max(np.abs(got - want) / tol)
     untouched = want == z.astype(np.float64)
     assert np.array_equal(got[untouched], z[untouched])
+
+
+# ----------------------------------------------------------- NEXT-2 uncertainty producer
+
+def _rgb_frames(n, h, w, tag):
+    """Synthetic regression frames: smooth gradients + sharp texture + flat (blurry) patches."""
+    rg = syn.rng("gpu-rgb", tag, n, h, w)
+    yy, xx = np.mgrid[0:h, 0:w].astype(np.float32)
+    out = np.empty((n, h, w, 3), np.float32)
+    for i in range(n):
+        base = 0.5 + 0.3 * np.sin(yy / (7 + i)) * np.cos(xx / (11 + i))
+        tex = rg.random((h, w)).astype(np.float32) * 0.4
+        blur = np.zeros((h, w), bool)
+        for _ in range(3):
+            cy, cx, r = rg.integers(0, h), rg.integers(0, w), rg.integers(h // 10 + 2, h // 4 + 3)
+            blur |= (yy - cy) ** 2 + (xx - cx) ** 2 < r * r
+        img = np.where(blur, base, base + tex - 0.2)
+        out[i] = np.clip(np.stack([img, img * 0.9, img * 1.1], -1), 0, 1)
+    return out
+
+
+@pytest.mark.parametrize("n,h,w,win,sm", [(2, 64, 64, 7, 5), (3, 576, 576, 7, 5), (2, 37, 53, 3, 1),
+                                          (1, 40, 30, 9, 3)])
+def test_uncertainty_map_vs_oracle(sphinx, n, h, w, win, sm):
+    rgb = _rgb_frames(n, h, w, f"{h}x{w}")
+    U_ref, _ = oracle.uncertainty(rgb, win, sm)
+    U = torch.empty((n, h, w), dtype=torch.float32, device=dev)
+    tau = torch.empty((n,), dtype=torch.float32, device=dev)
+    sphinx.sphinx_uncertainty_map(T(rgb), U, tau, win, sm)
+    Ug, tg = U.cpu().numpy(), tau.cpu().numpy()
+    # fp32 stencil (two-pass variance, box mean) and normalisation vs fp64: the map lives in
+    # [0,1] and the fp32 rounding of S relative to the frame's range (max S - min S) stays
+    # ~1e-6; 1e-4 absolute leaves two decades of margin (reading R-24)
+    assert np.max(np.abs(Ug - U_ref)) <= 1e-4
+    # the Otsu decision is taken in the kernel's precision: the oracle's exact Otsu on the
+    # GPU's own U must give the GPU's tau bit for bit
+    for i in range(n):
+        assert tg[i] == np.float32(oracle.otsu(Ug[i])), i
+    assert Ug.min() >= 0.0 and Ug.max() == 1.0
+
+
+def test_uncertainty_map_degenerate_and_semantics(sphinx):
+    # S:219 constant frame -> U == 1, tau == 1 -> empty blur mask
+    rgb = np.full((2, 24, 24, 3), 0.3, np.float32)
+    U = torch.empty((2, 24, 24), dtype=torch.float32, device=dev)
+    tau = torch.empty((2,), dtype=torch.float32, device=dev)
+    sphinx.sphinx_uncertainty_map(T(rgb), U, tau)
+    assert torch.all(U == 1.0) and torch.all(tau == 1.0)
+    # S:220 half sharp checkerboard / half flat gray: blurry = flat half
+    img = np.full((1, 64, 64, 3), 0.5, np.float32)
+    yy, xx = np.mgrid[0:64, 0:32]
+    img[0, :, :32, :] = ((yy + xx) % 2)[..., None]
+    U = torch.empty((1, 64, 64), dtype=torch.float32, device=dev)
+    tau = torch.empty((1,), dtype=torch.float32, device=dev)
+    sphinx.sphinx_uncertainty_map(T(img), U, tau)
+    m = (U > tau[0]).cpu().numpy()[0]
+    assert m[:, 40:].mean() >= 0.95 and m[:, :24].mean() <= 0.05
+    # chained into step 1: the produced (U, tau) drive sphinx_block_mask exactly like the oracle
+    O = np.ones((1, 64, 64), np.float32)
+    masks, counts, _ = gpu_block_mask(sphinx, O, U.cpu().numpy(), tau.cpu().numpy(), 0.5, 1, 8, 1)
+    want, _ = oracle.block_mask(O, U.cpu().numpy(), tau.cpu().numpy(), 0.5, 1, 8, 1)
+    assert np.array_equal(masks[0], want[0])
