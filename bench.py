@@ -298,27 +298,54 @@ def capture_step(torch, st, with_conv_events):
     return g, conv_ev
 
 
-def scatter_bandwidth(torch, st, reps=20):
-    """Out-of-place cached scatter of the level-0 feature map (bf16 [21,72,72,320]): 2 x map bytes
-    per launch (read src-or-cache, write out), HBM roofline.  L2 flushed before each launch."""
-    d = st.d
-    out = torch.empty_like(d["cache0"])
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=out.device)
-    ts = []
-    for i in range(reps + 3):
-        flush.fill_(0.0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        st.sp.sphinx_scatter_cached(st.z[0], d["cache0"], out, B, block_mask=st.masks[0], start_step=st.k,
-                                    step_u=U_STEP)
-        e1.record()
-        torch.cuda.synchronize()
-        if i >= 3:
-            ts.append(e0.elapsed_time(e1))
-    t = statistics.median(ts)
-    nbytes = 2 * out.numel() * out.element_size()
-    return {"kernel": "scatter_full_kernel", "shape": list(out.shape), "ms": round(t, 5),
-            "algorithmic_bytes": nbytes, "gbs": round(nbytes / (t * 1e-3) / 1e9, 1)}
+def memory_kernels(torch, st, req, reps=10):
+    """HBM-bound / latency-bound kernels timed one launch at a time after an L2 flush (cold),
+    CUDA events on the launching stream; algorithmic bytes / time vs the measured HBM peak.
+    Includes the NEXT rows (DDIM update, uncertainty producer) measured beside the step."""
+    sp, d, dev = st.sp, st.d, st.dev
+    hbm = peaks()[0]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def timed(fn):
+        ts = []
+        for i in range(reps + 2):
+            flush.fill_(0.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    out = {}
+    def row(name, ms, nbytes, note):
+        out[name] = {"ms": round(ms, 5), "algorithmic_bytes": int(nbytes),
+                     "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1), "hbm_frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4),
+                     "bytes": note}
+    n, hp = N_FRAMES, HP
+    start = dict(q_reg=d["q"], c0=d["c0"], c1=d["c1"], t=d["t"], gamma=GAMMA, logics=st.logics, logic_id=d["lid"])
+    ms = timed(lambda: sp.sphinx_block_mask(d["O"], d["U"], d["tau_u"], 0.5, F, B, st.masks, st.counts, start, st.k))
+    row("block_mask", ms, n * hp * hp * 8, "two fp32 maps read (8 B/px)")
+    cnt = int(st.cnt[0].item())
+    ms = timed(lambda: sp.sphinx_compact_blocks(st.masks[0], st.k, U_STEP, sp.SELECT_ACTIVE, st.ids[0], st.cnt[0]))
+    out["compact_blocks"] = {"ms": round(ms, 5), "entries": n * 81, "bound": "latency (one CTA)"}
+    ms = timed(lambda: sp.sphinx_noise_inject(d["x0"], d["eps"], st.zt, B, st.ids[0], st.cnt[0], st.k, d["abar"]))
+    row("noise_inject", ms, cnt * 64 * 4 * 12, "12 B per active latent element (x0, eps in; x_t out)")
+    out0 = torch.empty_like(d["cache0"])
+    ms = timed(lambda: sp.sphinx_scatter_cached(st.z[0], d["cache0"], out0, B, block_mask=st.masks[0],
+                                                start_step=st.k, step_u=U_STEP))
+    row("scatter_cached_level0_features", ms, 2 * out0.numel() * 2, "2 x map bytes (21x72x72x320 bf16)")
+    zo = torch.empty_like(st.zt)
+    ms = timed(lambda: sp.sphinx_ddim_step(st.zt, d["x0"], zo, B, st.ids[0], st.cnt[0], U_STEP, req["abar"]))
+    row("ddim_step (NEXT-1)", ms, cnt * 64 * 4 * 12, "12 B per active latent element (z, x0_hat in; z' out)")
+    rgb = torch.rand((n, hp, hp, 3), device=dev, dtype=torch.float32)
+    U = torch.empty((n, hp, hp), device=dev, dtype=torch.float32)
+    tau = torch.empty((n,), device=dev, dtype=torch.float32)
+    ms = timed(lambda: sp.sphinx_uncertainty_map(rgb, U, tau))
+    row("uncertainty_map (NEXT-2)", ms, n * hp * hp * 16, "rgb read 12 B/px + U write 4 B/px (algorithmic)")
+    return out
 
 
 def run_gpu(args):
@@ -435,9 +462,7 @@ def run_gpu(args):
     sweep = None
     if rank == 0 and not args.no_sweep:
         sweep = density_sweep(torch, st.sp, dev)
-    scat = scatter_bandwidth(torch, st) if rank == 0 else None
-    if scat is not None:
-        scat["hbm_frac"] = round(scat["gbs"] / hbm, 4)
+    mem = memory_kernels(torch, st, req) if rank == 0 else None
 
     if rank == 0:
         cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(req, bounded_s=args.cpu_seconds)
@@ -466,7 +491,7 @@ def run_gpu(args):
                          "conv_share_of_step": round(conv_total_ms / ms_all, 4)},
             "conv_levels": per_level,
             "conv_isolated_ms": iso,
-            "scatter_bandwidth": scat,
+            "memory_kernels": mem,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "density_sweep": sweep,

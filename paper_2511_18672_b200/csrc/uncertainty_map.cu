@@ -10,9 +10,10 @@
 //   tau[n] = Otsu over a 256-bin histogram of U (bin i = (i/256, (i+1)/256]), exact argmax.
 // U and tau are exactly the (uncertainty, tau_u) inputs of sphinx_block_mask (U > tau blurry).
 //
-// Kernels: (1) fused stencil per 32x32 tile: Y, L, V, S staged in shared memory over the
-// tile + halo (radius 1 + window/2 + smooth/2), S written to the output buffer and per-frame
-// min/max folded with integer atomics (S >= 0, so float bits order as ints); (2) normalise +
+// Kernels: (1) fused stencil per 32x32 tile: Y, L, V (separable fp64 window sums), S
+// (separable box) staged in shared memory over the tile + halo (radius 1 + window/2 +
+// smooth/2), S written to the output buffer and per-frame min/max folded with integer
+// atomics (S >= 0, so float bits order as ints); (2) normalise +
 // invert in place and a per-CTA shared histogram folded into the per-frame histogram
 // (integer atomics: deterministic); (3) one CTA per frame: the exact Otsu argmax.
 #include "common.cuh"
@@ -23,78 +24,104 @@ constexpr int kUT = 32;  // output tile edge
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Every stage works on the in-image rectangle its consumer needs and reads the previous stage
+// with image-clamped coordinates (edge replication of each stage's input, exactly as defined):
+//   S rows [sy0, sy1)  <- V rows [vy0, vy1) = [max(0, sy0-rs), min(h, sy1+rs))
+//   V rows [vy0, vy1)  <- L rows [ly0, ly1) = [max(0, vy0-rv), min(h, vy1+rv))
+//   L rows [ly0, ly1)  <- Y rows [yy0, yy1) = [max(0, ly0-1), min(h, ly1+1))      (same in x)
+// The window variance uses separable fp32 row/column sums of L and L^2:
+//   V = E[L^2] - E[L]^2 over the (2rv+1)^2 window.  The cancellation error is
+//   ~ 2^-23 E[L^2]; for images in [0,1] the Laplacian of a window with small variance but a
+//   large mean (constant curvature) is itself small, so after min-max normalisation the error
+//   stays ~1e-6 (parity tolerance 1e-4 vs the fp64 two-pass oracle, tests/test_gpu_parity).
 __global__ void __launch_bounds__(256) lapvar_smooth_kernel(const float* __restrict__ rgb, int h, int w,
                                                             int rv, int rs, float* __restrict__ S_out,
                                                             int* __restrict__ minmax) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ float sm[];
+  extern __shared__ __align__(16) unsigned char smraw[];
   const int n = blockIdx.z;
-  const int y0 = blockIdx.y * kUT, x0 = blockIdx.x * kUT;
-  const int R = rs + rv + 1;
-  const int NY = kUT + 2 * R, NL = kUT + 2 * (rs + rv), NV = kUT + 2 * rs;
-  float* Ys = sm;                 // Ys[a][b] = Y(clamp(y0-R+a), clamp(x0-R+b))
-  float* Ls = Ys + NY * NY;       // Ls[a][b] = L(clamp(y0-rs-rv+a), clamp(x0-rs-rv+b))
-  float* Vs = Ls + NL * NL;       // Vs[a][b] = V(clamp(y0-rs+a), clamp(x0-rs+b))
+  const int sy0 = blockIdx.y * kUT, sx0 = blockIdx.x * kUT;
+  const int sy1 = min(h, sy0 + kUT), sx1 = min(w, sx0 + kUT);
+  const int vy0 = max(0, sy0 - rs), vy1 = min(h, sy1 + rs), vx0 = max(0, sx0 - rs), vx1 = min(w, sx1 + rs);
+  const int ly0 = max(0, vy0 - rv), ly1 = min(h, vy1 + rv), lx0 = max(0, vx0 - rv), lx1 = min(w, vx1 + rv);
+  const int yy0 = max(0, ly0 - 1), yy1 = min(h, ly1 + 1), yx0 = max(0, lx0 - 1), yx1 = min(w, lx1 + 1);
+  const int YW = yx1 - yx0, LW = lx1 - lx0, VW = vx1 - vx0, SW = sx1 - sx0;
+  const int YH = yy1 - yy0, LH = ly1 - ly0, VH = vy1 - vy0, SH = sy1 - sy0;
+  // smem carve-up (max extents for T=32, r<=7: Y 62x62, L 60x60, rowsums 60x46 x2 fp64, V 46x46,
+  // S-rowsums 46x32)
+  float* R1 = reinterpret_cast<float*>(smraw);              // [LH][VW] sum_dx L
+  float* R2 = R1 + LH * VW;                                 // [LH][VW] sum_dx L^2
+  float* Ys = reinterpret_cast<float*>(R2 + LH * VW);       // [YH][YW]
+  float* Ls = Ys + YH * YW;                                 // [LH][LW]
+  float* Vs = Ls + LH * LW;                                 // [VH][VW]
+  float* Ts = Vs + VH * VW;                                 // [VH][SW] sum_dx V (box rows)
   const size_t plane = (size_t)h * w;
   const float* img = rgb + (size_t)n * plane * 3;
-  for (int i = threadIdx.x; i < NY * NY; i += blockDim.x) {
-    const int a = i / NY, b = i - (i / NY) * NY;
-    const int yy = clampi(y0 - R + a, 0, h - 1), xx = clampi(x0 - R + b, 0, w - 1);
-    const float* px = img + ((size_t)yy * w + xx) * 3;
-    Ys[i] = 0.299f * __ldg(px) + 0.587f * __ldg(px + 1) + 0.114f * __ldg(px + 2);
-  }
-  __syncthreads();
-  // L at the (clamped) image position p, from Y at clamp(p +- 1): index = image coord - (y0 - R)
-  for (int i = threadIdx.x; i < NL * NL; i += blockDim.x) {
-    const int a = i / NL, b = i - (i / NL) * NL;
-    const int py = clampi(y0 - rs - rv + a, 0, h - 1), px = clampi(x0 - rs - rv + b, 0, w - 1);
-    const int cy = py - (y0 - R), cx = px - (x0 - R);
-    const int uy = clampi(py - 1, 0, h - 1) - (y0 - R), dy = clampi(py + 1, 0, h - 1) - (y0 - R);
-    const int lx = clampi(px - 1, 0, w - 1) - (x0 - R), rx = clampi(px + 1, 0, w - 1) - (x0 - R);
-    Ls[i] = Ys[uy * NY + cx] + Ys[dy * NY + cx] + Ys[cy * NY + lx] + Ys[cy * NY + rx] -
-            4.0f * Ys[cy * NY + cx];
-  }
-  __syncthreads();
-  // V at the (clamped) position p: two-pass variance of L(clamp(p + d)), d in [-rv, rv]^2
-  const float inv_cnt = 1.0f / (float)((2 * rv + 1) * (2 * rv + 1));
-  for (int i = threadIdx.x; i < NV * NV; i += blockDim.x) {
-    const int a = i / NV, b = i - (i / NV) * NV;
-    const int py = clampi(y0 - rs + a, 0, h - 1), px = clampi(x0 - rs + b, 0, w - 1);
-    float mean = 0.0f;
-    for (int ddy = -rv; ddy <= rv; ++ddy) {
-      const int ly = clampi(py + ddy, 0, h - 1) - (y0 - rs - rv);
-      for (int ddx = -rv; ddx <= rv; ++ddx)
-        mean += Ls[ly * NL + clampi(px + ddx, 0, w - 1) - (x0 - rs - rv)];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int a = wid; a < YH; a += nw)
+    for (int c = lane; c < YW; c += 32) {
+      const float* px = img + ((size_t)(yy0 + a) * w + (yx0 + c)) * 3;
+      Ys[a * YW + c] = 0.299f * __ldg(px) + 0.587f * __ldg(px + 1) + 0.114f * __ldg(px + 2);
     }
-    mean *= inv_cnt;
-    float var = 0.0f;
-    for (int ddy = -rv; ddy <= rv; ++ddy) {
-      const int ly = clampi(py + ddy, 0, h - 1) - (y0 - rs - rv);
-      for (int ddx = -rv; ddx <= rv; ++ddx) {
-        const float d = Ls[ly * NL + clampi(px + ddx, 0, w - 1) - (x0 - rs - rv)] - mean;
-        var = fmaf(d, d, var);
+  __syncthreads();
+  for (int a = wid; a < LH; a += nw)
+   for (int c = lane; c < LW; c += 32) {
+    const int i = a * LW + c;
+    const int py = ly0 + a, px = lx0 + c;  // in-image position; neighbours clamped to the image
+    const int cy = py - yy0, cx = px - yx0;
+    const int uy = max(py - 1, 0) - yy0, dy = min(py + 1, h - 1) - yy0;
+    const int lx = max(px - 1, 0) - yx0, rx = min(px + 1, w - 1) - yx0;
+    Ls[i] = Ys[uy * YW + cx] + Ys[dy * YW + cx] + Ys[cy * YW + lx] + Ys[cy * YW + rx] - 4.0f * Ys[cy * YW + cx];
+   }
+  __syncthreads();
+  for (int a = wid; a < LH; a += nw)  // horizontal window sums of L and L^2
+    for (int c = lane; c < VW; c += 32) {
+      const int px = vx0 + c;
+      float s1 = 0.0f, s2 = 0.0f;
+      for (int d = -rv; d <= rv; ++d) {
+        const float l = Ls[a * LW + min(max(px + d, 0), w - 1) - lx0];
+        s1 += l;
+        s2 = fmaf(l, l, s2);
       }
+      R1[a * VW + c] = s1;
+      R2[a * VW + c] = s2;
     }
-    Vs[i] = var * inv_cnt;
-  }
   __syncthreads();
-  // S = box mean of V(clamp(y + d)); per-CTA min/max of S
+  const float inv_cnt = 1.0f / (float)((2 * rv + 1) * (2 * rv + 1));
+  for (int a = wid; a < VH; a += nw)  // vertical window sums -> variance
+    for (int c = lane; c < VW; c += 32) {
+      const int py = vy0 + a;
+      float s1 = 0.0f, s2 = 0.0f;
+      for (int d = -rv; d <= rv; ++d) {
+        const int r = min(max(py + d, 0), h - 1) - ly0;
+        s1 += R1[r * VW + c];
+        s2 += R2[r * VW + c];
+      }
+      const float m = s1 * inv_cnt;
+      Vs[a * VW + c] = fmaxf(fmaf(-m, m, s2 * inv_cnt), 0.0f);
+    }
+  __syncthreads();
+  for (int a = wid; a < VH; a += nw)  // box: horizontal sums of V
+    for (int c = lane; c < SW; c += 32) {
+      const int px = sx0 + c;
+      float s1 = 0.0f;
+      for (int d = -rs; d <= rs; ++d) s1 += Vs[a * VW + min(max(px + d, 0), w - 1) - vx0];
+      Ts[a * SW + c] = s1;
+    }
+  __syncthreads();
   const float inv_box = 1.0f / (float)((2 * rs + 1) * (2 * rs + 1));
   float lo = 3.0e38f, hi = 0.0f;
-  for (int i = threadIdx.x; i < kUT * kUT; i += blockDim.x) {
-    const int y = y0 + i / kUT, x = x0 + (i % kUT);
-    if (y >= h || x >= w) continue;
-    float sacc = 0.0f;
-    for (int ddy = -rs; ddy <= rs; ++ddy) {
-      const int vy = clampi(y + ddy, 0, h - 1) - (y0 - rs);
-      for (int ddx = -rs; ddx <= rs; ++ddx) sacc += Vs[vy * NV + clampi(x + ddx, 0, w - 1) - (x0 - rs)];
-    }
-    const float sv = sacc * inv_box;
-    S_out[(size_t)n * plane + (size_t)y * w + x] = sv;
+  for (int a = wid; a < SH; a += nw)  // box: vertical sums -> S
+   for (int c = lane; c < SW; c += 32) {
+    const int py = sy0 + a;
+    float s1 = 0.0f;
+    for (int d = -rs; d <= rs; ++d) s1 += Ts[(min(max(py + d, 0), h - 1) - vy0) * SW + c];
+    const float sv = s1 * inv_box;
+    S_out[(size_t)n * plane + (size_t)py * w + sx0 + c] = sv;
     lo = fminf(lo, sv);
     hi = fmaxf(hi, sv);
-  }
+   }
   for (int d = 16; d > 0; d >>= 1) {
     lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, d));
     hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, d));
@@ -169,17 +196,20 @@ __global__ void __launch_bounds__(256) otsu_kernel(const int* __restrict__ hist,
     sr[k] = 0;
     sd[k] = 1;
   }
+  __shared__ int sk[256];
+  sk[k] = k;
   __syncthreads();
-  if (k == 0) {
-    if (nonempty <= 1) {
-      tau[n] = 1.0f;
-      return;
+  // tree argmax; a candidate with the larger score wins, on ties the smaller split index
+  for (int off = 128; off > 0; off >>= 1) {
+    if (k < off) {
+      const int a = sk[k], b = sk[k + off];
+      const bool b_better = sq[b] > sq[a] || (sq[b] == sq[a] && sr[b] * sd[a] > sr[a] * sd[b]) ||
+                            (sq[b] == sq[a] && sr[b] * sd[a] == sr[a] * sd[b] && b < a);
+      if (b_better) sk[k] = b;
     }
-    int best = 0;
-    for (int j = 1; j < 255; ++j)
-      if (sq[j] > sq[best] || (sq[j] == sq[best] && sr[j] * sd[best] > sr[best] * sd[j])) best = j;
-    tau[n] = (float)(best + 1) / 256.0f;
+    __syncthreads();
   }
+  if (k == 0) tau[n] = nonempty <= 1 ? 1.0f : (float)(sk[0] + 1) / 256.0f;
 }
 
 }  // namespace sphinx
@@ -214,10 +244,11 @@ extern "C" sphinx_status sphinx_uncertainty_map(const float* rgb, int32_t n, int
   if (e != cudaSuccess) return cuda_fail(e);
   const int rv = window / 2, rs = smooth / 2, R = rs + rv + 1;
   const int NY = kUT + 2 * R, NL = kUT + 2 * (rs + rv), NV = kUT + 2 * rs;
-  const size_t smem = (size_t)(NY * NY + NL * NL + NV * NV) * sizeof(float);
+  const size_t smem = (size_t)NL * NV * 2 * sizeof(float) +
+                      (size_t)(NY * NY + NL * NL + NV * NV + NV * kUT) * sizeof(float);
   static bool attr_set = false;
   if (!attr_set) {
-    e = cudaFuncSetAttribute(lapvar_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    e = cudaFuncSetAttribute(lapvar_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return cuda_fail(e);
     attr_set = true;
   }
