@@ -114,7 +114,8 @@ struct ConvCfg {
   // full-block tiles: 10 lines x 2 blocks (+ the UMMA over-read of padding groups stays inside);
   // edge tiles up to 8 blocks: 32 line slots
   static constexpr int kASlot = (EDGE ? 32 : 20) * kHaloRow;
-  static constexpr int kANum = 3;
+  // edge kernels at >= 128 B rows per CTA keep 2 halo slots so the weight ring stays deep
+  static constexpr int kANum = (EDGE && kBNc >= 128) ? 2 : 3;
   static constexpr int kBNumFit = (kAvail - kANum * kASlot - 1024) / kStageB;
   static constexpr int kBNum = kBNumFit > 16 ? 16 : kBNumFit;
   // halo A ring padded to 1 KB so the B ring (SW128, 1024-B atoms) stays aligned
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         Cur ca, cb;
         cur_init(ca);
         cur_init(cb);
-        const int kAhead = p.a_ahead;
+        const int kAhead = p.a_ahead < Cfg::kANum - 1 ? p.a_ahead : Cfg::kANum - 1;
         long long a_seg = -1;  // segment whose blocks are decoded in cx/cy/cn
         long long b_seg = -1;
         int b_n0 = 0;
