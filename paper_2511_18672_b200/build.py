@@ -28,17 +28,23 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, trace=False):
+    """trace=True builds the dev-only timeline variant libsphinx_trace.so (-DSPHINX_TRACE)."""
+    so = SO.replace("libsphinx.so", "libsphinx_trace.so") if trace else SO
+    if not trace and not force and not _stale():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
-        ["-I", os.path.join(ROOT, "include"), "-o", SO + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+        (["-DSPHINX_TRACE"] if trace else []) + \
+        ["-I", os.path.join(ROOT, "include"), "-o", so + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":
+    if "--trace" in sys.argv:
+        print(build(trace=True))
+        sys.exit(0)
     build(force=True, verbose="-v" in sys.argv)
     print(SO)

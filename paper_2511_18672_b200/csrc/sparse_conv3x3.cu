@@ -38,7 +38,30 @@ namespace sphinx {
 constexpr int kBM = 128;          // MMA M: pixels per tile
 constexpr int kBK = 64;           // channels per K chunk: 128 B rows, SWIZZLE_128B
 constexpr int kStageA = kBM * kBK * 2;  // 16 KB
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;
+constexpr int kAWarp = 6;  // halo mode: the halo (A) producer warp when the producers are split
+
+#ifdef SPHINX_TRACE
+// Dev-only timeline trace (libsphinx_trace.so): globaltimer stamps per CTA of one launch.
+// slots: 0 entry, 1 after pdl_wait, 2 first MMA, 3 last MMA commit, 4 epilogue done, 5 exit,
+//        6 chunks issued by the MMA warp, 7 B producer done, 8 first A issued, 9 first B issued,
+//        10 first A full (MMA), 11 last accumulator ready (epilogue), 12 epilogue tiles,
+//        13 sum of TMEM-drain durations, 14 last TMEM-drain duration (ns).
+__device__ unsigned long long g_conv_trace[1024 * 16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CONV_TRACE(k, v) \
+  do {                   \
+    if (p.trace) g_conv_trace[blockIdx.x * 16 + (k)] = (v); \
+  } while (0)
+#else
+#define CONV_TRACE(k, v) \
+  do {                   \
+  } while (0)
+#endif
 
 struct ConvParams {
   const int32_t* ids;
@@ -64,6 +87,9 @@ struct ConvParams {
   int rb, cr;                // valid rows of bottom-edge blocks, valid cols of right-edge blocks
   int bpt_b, bpt_r;          // blocks per CTA tile of the two edge classes
   uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
+  int trace;         // SPHINX_TRACE builds: record this launch's timeline
+  int dbg;           // SPHINX_TRACE builds: 1 = skip epilogue global stores, 2 = skip bias
+  int a_warp;        // halo mode: 1 = halos issued by their own producer warp
   int a_ahead;       // halo chunks the A cursor may run ahead of the B cursor (1..kANum-1)
   int allow_streamk; // halo mode may use stream-K when it shortens the makespan
 };
@@ -103,7 +129,8 @@ struct ConvCfg {
   static constexpr int kBNc = BN / CG;  // B rows (output channels) held by this CTA
   static constexpr int kStageB = kBNc * kBK * 2;
   static constexpr int kStageBytes = kStageA + kStageB;
-  static constexpr int kBarBytes = 512 + kBM * 8;  // barriers + split-K pixel table
+  // barriers + split-K pixel table + per-accumulator bias slices (2 x 256 fp32)
+  static constexpr int kBarBytes = 512 + kBM * 8 + 2 * 256 * 4;
   static constexpr int kMaxSmem = 232448;          // 227 KB opt-in per CTA
   static constexpr int kAvail = kMaxSmem - 1024 - kBarBytes;
   // per-tap mode
@@ -144,12 +171,27 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 }
 
 // 32 consecutive output channels [co, co+32) of one pixel: + bias, fp32 or bf16 store.
-__device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix, int co, float (&v)[32]) {
-  if (p.bias) {
+__device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix, int co, float (&v)[32],
+                                                const float* sb) {
+  // sb: this chunk's 32 bias values in shared memory (zero-padded): broadcast LDS.128, no
+  // predicated global loads queued behind the previous chunk's stores
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (co + i < p.cout) v[i] += __ldg(p.bias + co + i);
+  for (int i = 0; i < 32; i += 4) {
+    const float4 b4 = *reinterpret_cast<const float4*>(sb + i);
+    v[i] += b4.x;
+    v[i + 1] += b4.y;
+    v[i + 2] += b4.z;
+    v[i + 3] += b4.w;
   }
+#ifdef SPHINX_TRACE
+  if (p.dbg & 1) {
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc += v[i];
+    if (acc == 12345.678f) static_cast<float*>(p.y)[pix] = acc;  // keep the values live
+    return;
+  }
+#endif
   if (p.y_f32) {
     float* yp = static_cast<float*>(p.y) + pix + co;
 #pragma unroll
@@ -299,8 +341,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* red_bar = tempty + 2;  // [2] split-K / stream-K partial staging barriers
   // split-K: element offset of each tile row's output pixel (-1 = not stored), 8-byte aligned
   long long* pix_tab = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(full) + 512);
+  // bias of the tile held in accumulator a: s_bias[a * 256 + column] (0 beyond cout / no bias)
+  float* s_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512 + kBM * 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SPHINX_TRACE
+  if (threadIdx.x == 0) CONV_TRACE(0, gtimer());
+#endif
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
   const int cluster_id = blockIdx.x / CG, n_clusters = gridDim.x / CG;
   // ---- setup that needs no upstream data (overlaps the previous kernel's tail under PDL)
@@ -330,6 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // ids, count, plan and x are produced upstream
   pdl_trigger();
+#ifdef SPHINX_TRACE
+  if (threadIdx.x == 0) CONV_TRACE(1, gtimer());
+#endif
   const int count = *p.count;
   constexpr int BPT = kBM / (BLK * BLK);  // blocks per CTA tile (2 at b=8, 8 at b=4)
   constexpr int bb = BLK * BLK;
@@ -373,8 +423,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   it0.hi = sk_mode ? (long long)(cluster_id + 1) * Wk / n_clusters : 0;
 
 
-  if (warp == 0) {
-    // ===================== TMA producer (both CTAs) =====================
+  if (warp == 0 || (HALO && warp == kAWarp)) {
+    // ===================== TMA producers (both CTAs) =====================
+    // halo mode: warp 0 issues the weight (B) tiles and warp kAWarp the halos (A), so the two
+    // streams of TMA issues overlap (a single issuing thread caps the per-SM TMA op rate)
     if (elect_one()) {
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = policy_evict_last();
@@ -415,9 +467,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         int ahead = 0;  // chunks the A cursor is ahead of the B cursor
         int bs = 0;     // B ring position
         uint32_t bph = 0;
-        while (cb.ok) {
-          // ---- A: issue halos up to kAhead chunks ahead of the current B chunk
-          while (ca.ok && ahead < kAhead) {
+#ifdef SPHINX_TRACE
+        bool tr_a = false, tr_b = false;
+#endif
+        const bool split = p.a_warp != 0;
+        const bool doA = split ? warp == kAWarp : warp == 0;
+        const bool doB = warp == 0;
+        while (doB ? cb.ok : ca.ok) {
+          // ---- A: issue halos up to kAhead chunks ahead of the current B chunk (split: the A
+          // thread runs on its own, bounded only by the A ring)
+          while (doA && ca.ok && (split || ahead < kAhead)) {
             if (ca.it.x != a_seg) {  // new segment: decode its blocks once (kept in registers)
               a_seg = ca.it.x;
               g = halo_tile<CG>(ca.g.t / p.n_tiles_n, rank, nF, nB, list, nR, p);
@@ -455,6 +514,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else tma_load_4d_cg2(tm, bar, dst, ca.kc * kBK, xx, yy, cn[i], pol_a);
               }
             }
+#ifdef SPHINX_TRACE
+            if (!tr_a) {
+              CONV_TRACE(8, gtimer());
+              tr_a = true;
+            }
+#endif
             if (++stage == Cfg::kANum) {
               stage = 0;
               phase ^= 1;
@@ -462,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cur_next(ca);
             ++ahead;
           }
+          if (!doB) break;
           // ---- B: one (tap, chunk) weight tile per tap of the B cursor's chunk
           {
             if (cb.it.x != b_seg) {
@@ -480,6 +546,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (rank == 0) mbar_arrive_expect_tx(bf, (uint32_t)(2 * Cfg::kStageB));
                 tma_load_3d_cg2(&tmB, leader_addr(bf), b_dst, cb.kc * kBK, tap, n0, pol_b);
               }
+#ifdef SPHINX_TRACE
+              if (!tr_b) {
+                CONV_TRACE(9, gtimer());
+                tr_b = true;
+              }
+#endif
               if (++bs == Cfg::kBNum) {
                 bs = 0;
                 bph ^= 1;
@@ -489,7 +561,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           cur_next(cb);
           --ahead;
         }
-      } else
+#ifdef SPHINX_TRACE
+        if (doB) CONV_TRACE(7, gtimer());
+#endif
+      } else if (warp == 0)
       for (int u = cluster_id; u < total; u += n_clusters) {
         const Unit U = decode_unit(u, n_full, nsplit);
         const int t = U.t;
@@ -556,8 +631,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t bph = 0;
         SegIter it = it0;
         Seg sg;
+#ifdef SPHINX_TRACE
+        int n_chunks = 0;
+        bool first = true;
+#endif
         for (; it.get(sg); it.next(sg)) {
           const int kc0 = sg.k0, kc1 = sg.k1;
+#ifdef SPHINX_TRACE
+          n_chunks += kc1 - kc0;
+#endif
           const HaloTile g = halo_tile<CG>(sg.t / p.n_tiles_n, 0, nF, nB, list, nR, p);
           const uint32_t line_stride = (uint32_t)(g.bpt * Cfg::kHaloRow);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -566,11 +648,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kc = kc0; kc < kc1; ++kc) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
+#ifdef SPHINX_TRACE
+            if (first) CONV_TRACE(10, gtimer());
+#endif
             const uint32_t a_base = smem_u32(sA + stage * Cfg::kASlot);
             for (int tap = 0; tap < 9; ++tap) {
               const int dy = tap / 3, dx = tap - 3 * (tap / 3);
               mbar_wait(&full[Cfg::kANum + bs], bph);
               tc_fence_after();
+#ifdef SPHINX_TRACE
+              if (first) {
+                CONV_TRACE(2, gtimer());
+                first = false;
+              }
+#endif
               // tap (dy,dx): 8-row group q*bpt + block at a_start + group*2048; rows run along
               // the halo line, so the along-line shift is 128 B per pixel and the cross-line
               // shift is one line (bpt slots); transposed tiles swap the roles of dy and dx
@@ -604,6 +695,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc_phase ^= 1;
           }
         }
+#ifdef SPHINX_TRACE
+        CONV_TRACE(3, gtimer());
+        CONV_TRACE(6, (unsigned long long)n_chunks);
+#endif
       } else
       for (int u = cluster_id; u < total; u += n_clusters) {
         const Unit U = decode_unit(u, n_full, nsplit);
@@ -637,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp < kAWarp) {
     // ===================== epilogue (warps 2..5, both CTAs) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
@@ -685,8 +780,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // stream-K part: column-major [BN][128] slot of this cluster (coalesced per column)
       float* skpart = (sg.role == kPart)
                           ? p.ws_part + ((size_t)cluster_id * CG + rank) * kBM * BN + row : nullptr;
+      {
+        // this tile's bias slice -> s_bias[acc] (the slot was last read two tiles ago, before
+        // the previous tile's barrier below)
+        float* sb = s_bias + acc * 256;
+        const int nb = p.bias ? min(BN, p.cout - nt * BN) : 0;
+        for (int c = row; c < BN; c += kBM) sb[c] = c < nb ? __ldg(p.bias + nt * BN + c) : 0.f;
+        named_bar_sync(1, 128);
+      }
+      const float* sbt = s_bias + acc * 256;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+#ifdef SPHINX_TRACE
+      if (warp == 2 && lane == 0) {
+        CONV_TRACE(11, gtimer());
+        if (p.trace) ++g_conv_trace[blockIdx.x * 16 + 12];
+      }
+#endif
       if (sg.role == kOwner) {
         // ---- stream-K owner: wait for the parts of tile t, then add them chunk by chunk
         const int c_last = sk_cluster_of((long long)(t + 1) * p.kc - 1, Wk, n_clusters);
@@ -729,7 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] += src[i * kBM];  // lanes = consecutive rows
           }
-          if (valid) store_row_chunk(p, pix, nt * BN + c0, v);
+          if (valid) store_row_chunk(p, pix, nt * BN + c0, v, sbt + c0);
           named_bar_sync(1, 128);  // every thread done with buf before it is refilled
         }
         if (row == 0) cnt[0] = 0;  // leave the counter zeroed for the next launch
@@ -753,12 +863,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             float v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-            store_row_chunk(p, pix, nt * BN + c0, v);
+            store_row_chunk(p, pix, nt * BN + c0, v, sbt + c0);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
+#ifdef SPHINX_TRACE
+      if (warp == 2 && lane == 0 && p.trace) {
+        const unsigned long long d = gtimer() - g_conv_trace[blockIdx.x * 16 + 11];
+        g_conv_trace[blockIdx.x * 16 + 13] += d;
+        g_conv_trace[blockIdx.x * 16 + 14] = d;
+      }
+#endif
       if (lane == 0) {
         if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
         else mbar_arrive_cluster(leader_addr(&tempty[acc]));
@@ -820,10 +937,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const int co = nt * BN + c4 * 4;
           if (co < p.cout) {
-            if (p.bias) {
-              acc4.x += __ldg(p.bias + co); acc4.y += __ldg(p.bias + co + 1);
-              acc4.z += __ldg(p.bias + co + 2); acc4.w += __ldg(p.bias + co + 3);
-            }
+            const float4 b4 = *reinterpret_cast<const float4*>(sbt + c4 * 4);
+            acc4.x += b4.x; acc4.y += b4.y; acc4.z += b4.z; acc4.w += b4.w;
             if (p.y_f32) {
               *reinterpret_cast<float4*>(static_cast<float*>(p.y) + px + co) = acc4;
             } else {
@@ -849,8 +964,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+#ifdef SPHINX_TRACE
+  if (warp == 2 && lane == 0) CONV_TRACE(4, gtimer());
+#endif
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();
+#ifdef SPHINX_TRACE
+  if (threadIdx.x == 0) CONV_TRACE(5, gtimer());
+#endif
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 2) tmem_dealloc_cg2<Cfg::kTmemCols>(tmem_base);
@@ -1107,6 +1228,19 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.bpt = kBM / (block * block);
   p.halo = halo;
   p.a_ahead = 2;
+  p.a_warp = 1;
+  p.trace = 0;
+  p.dbg = 0;
+#ifdef SPHINX_TRACE
+  if (const char* env = getenv("SPHINX_DBG")) p.dbg = atoi(env);
+  {
+    static int launch_no = 0;
+    const char* env = getenv("SPHINX_TRACE_LAUNCH");
+    p.trace = env && atoi(env) == launch_no;
+    ++launch_no;
+  }
+#endif
+  if (const char* env = getenv("SPHINX_A_WARP")) p.a_warp = atoi(env);
   p.allow_streamk = 1;
   if (const char* env = getenv("SPHINX_CONV_STREAMK")) p.allow_streamk = atoi(env);  // 2 = force
   if (const char* env = getenv("SPHINX_A_AHEAD")) p.a_ahead = atoi(env) < 1 ? 1 : (atoi(env) > 2 ? 2 : atoi(env));
@@ -1157,3 +1291,14 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
     default: return launch_cg<32>(cg, ta, tb, tc, p, grid, s);
   }
 }
+
+#ifdef SPHINX_TRACE
+extern "C" SPHINX_API int sphinx_debug_conv_trace_reset() {
+  static unsigned long long zero[1024 * 16] = {};
+  return cudaMemcpyToSymbol(sphinx::g_conv_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+extern "C" SPHINX_API int sphinx_debug_conv_trace(unsigned long long* host, int n_ctas) {
+  return cudaMemcpyFromSymbol(host, sphinx::g_conv_trace, sizeof(unsigned long long) * 16 * n_ctas) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif
