@@ -46,8 +46,9 @@ constexpr int kAWarp = 6;  // halo mode: the halo (A) producer warp when the pro
 // slots: 0 entry, 1 after pdl_wait, 2 first MMA, 3 last MMA commit, 4 epilogue done, 5 exit,
 //        6 chunks issued by the MMA warp, 7 B producer done, 8 first A issued, 9 first B issued,
 //        10 first A full (MMA), 11 last accumulator ready (epilogue), 12 epilogue tiles,
-//        13 sum of TMEM-drain durations, 14 last TMEM-drain duration (ns).
-__device__ unsigned long long g_conv_trace[1024 * 16];
+//        13 sum of TMEM-drain durations, 14 last TMEM-drain duration (ns), 15 setup done,
+//        16 split partial parked, 17 split rendezvous done, 18 split reduction done, 19 ns.
+__device__ unsigned long long g_conv_trace[1024 * 24];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -55,7 +56,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define CONV_TRACE(k, v) \
   do {                   \
-    if (p.trace) g_conv_trace[blockIdx.x * 16 + (k)] = (v); \
+    if (p.trace) g_conv_trace[blockIdx.x * 24 + (k)] = (v); \
   } while (0)
 #else
 #define CONV_TRACE(k, v) \
@@ -339,8 +340,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   uint64_t* red_bar = tempty + 2;  // [2] split-K / stream-K partial staging barriers
-  // split-K: element offset of each tile row's output pixel (-1 = not stored), 8-byte aligned
-  long long* pix_tab = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(full) + 512);
   // bias of the tile held in accumulator a: s_bias[a * 256 + column] (0 beyond cout / no bias)
   float* s_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512 + kBM * 8);
 
@@ -423,6 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   it0.hi = sk_mode ? (long long)(cluster_id + 1) * Wk / n_clusters : 0;
 
 
+#ifdef SPHINX_TRACE
+  if (threadIdx.x == 0) CONV_TRACE(15, gtimer());
+#endif
   if (warp == 0 || (HALO && warp == kAWarp)) {
     // ===================== TMA producers (both CTAs) =====================
     // halo mode: warp 0 issues the weight (B) tiles and warp kAWarp the halos (A), so the two
@@ -774,9 +776,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         valid = (yy < p.h) && (xx < p.w);
         pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
       }
+      // split-K part: column-major [BN][128] (lanes = consecutive rows: coalesced)
       float* part = nullptr;
-      if (ns > 1)
-        part = p.ws_part + (((size_t)(U.slot * ns + sk) * CG + rank) * kBM + row) * BN;
+      if (ns > 1) part = p.ws_part + ((size_t)(U.slot * ns + sk) * CG + rank) * kBM * BN + row;
       // stream-K part: column-major [BN][128] slot of this cluster (coalesced per column)
       float* skpart = (sg.role == kPart)
                           ? p.ws_part + ((size_t)cluster_id * CG + rank) * kBM * BN + row : nullptr;
@@ -794,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef SPHINX_TRACE
       if (warp == 2 && lane == 0) {
         CONV_TRACE(11, gtimer());
-        if (p.trace) ++g_conv_trace[blockIdx.x * 16 + 12];
+        if (p.trace) ++g_conv_trace[blockIdx.x * 24 + 12];
       }
 #endif
       if (sg.role == kOwner) {
@@ -853,12 +855,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) __stcg(skpart + (size_t)(c0 + i) * kBM, __uint_as_float(r[i]));
           } else if (ns > 1) {
-            // split-K: park this split's fp32 partial row in the workspace
+            // split-K: park this split's fp32 partial (column-major, coalesced)
 #pragma unroll
-            for (int g = 0; g < 32; g += 4)
-              __stcg(reinterpret_cast<float4*>(part + c0 + g),
-                     make_float4(__uint_as_float(r[g]), __uint_as_float(r[g + 1]),
-                                 __uint_as_float(r[g + 2]), __uint_as_float(r[g + 3])));
+            for (int i = 0; i < 32; ++i) __stcg(part + (size_t)(c0 + i) * kBM, __uint_as_float(r[i]));
           } else if (valid) {
             float v[32];
 #pragma unroll
@@ -871,9 +870,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
 #ifdef SPHINX_TRACE
       if (warp == 2 && lane == 0 && p.trace) {
-        const unsigned long long d = gtimer() - g_conv_trace[blockIdx.x * 16 + 11];
-        g_conv_trace[blockIdx.x * 16 + 13] += d;
-        g_conv_trace[blockIdx.x * 16 + 14] = d;
+        const unsigned long long d = gtimer() - g_conv_trace[blockIdx.x * 24 + 11];
+        g_conv_trace[blockIdx.x * 24 + 13] += d;
+        g_conv_trace[blockIdx.x * 24 + 14] = d;
       }
 #endif
       if (lane == 0) {
@@ -897,9 +896,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Rendezvous of the ns units of tile t (all co-resident in this single round),
         // then each reduces a 1/nsplit slice of the rows, summing partials in split order
         // (deterministic), with coalesced float4 loads across the epilogue threads.
-        pix_tab[row] = valid ? (long long)pix : -1ll;
         __threadfence();
         named_bar_sync(1, 128);
+#ifdef SPHINX_TRACE
+        if (row == 0) {
+          CONV_TRACE(16, gtimer());
+          CONV_TRACE(19, (unsigned long long)ns);
+        }
+#endif
         int* arrive = p.ws_cnt + (U.slot * CG + rank) * 2;
         if (row == 0) {
           atomicAdd(arrive, 1);
@@ -910,49 +914,65 @@ __global__ void __launch_bounds__(kThreads, 1)
           } while (seen < ns);
         }
         named_bar_sync(1, 128);
-        const int r0 = sk * kBM / ns, r1 = (sk + 1) * kBM / ns;
-        const uint32_t slice_bytes = (uint32_t)((r1 - r0) * BN * 4);
-        const float* base = p.ws_part + (((size_t)(U.slot * ns) * CG + rank) * kBM + r0) * BN;
+#ifdef SPHINX_TRACE
+        if (row == 0) CONV_TRACE(17, gtimer());
+#endif
+        // this unit reduces output columns [c0s, c1s) (multiples of 8) of all 128 rows: from every
+        // part that column range is one contiguous column-major block -> one bulk copy each
+        const int c0s = (sk * (BN / 8) / ns) * 8, c1s = ((sk + 1) * (BN / 8) / ns) * 8;
+        const int ncol = c1s - c0s;
+        const uint32_t slice_bytes = (uint32_t)(ncol * kBM * 4);
+        const float* base = p.ws_part + ((size_t)(U.slot * ns) * CG + rank) * kBM * BN + (size_t)c0s * kBM;
         const size_t split_stride = (size_t)CG * kBM * BN;
         float* stage_buf = reinterpret_cast<float*>(sA);  // the operand ring is idle now
-        if (row == 0) {
+        if ((size_t)ns * slice_bytes > (size_t)Cfg::kRingBytes) __trap();  // never at BN <= 256
+        if (row == 0 && ncol > 0) {
           fence_proxy_async_global();
           mbar_arrive_expect_tx(red_bar, slice_bytes * (uint32_t)ns);
           for (int s2 = 0; s2 < ns; ++s2)
-            bulk_g2s(stage_buf + (size_t)s2 * (r1 - r0) * BN, base + s2 * split_stride, slice_bytes,
-                     red_bar);
+            bulk_g2s(stage_buf + (size_t)s2 * ncol * kBM, base + s2 * split_stride, slice_bytes, red_bar);
         }
-        mbar_wait(red_bar, 0);
-        constexpr int kV = BN / 4;  // float4 per row
-        const int n_el = (r1 - r0) * kV;
-        const float4* sb = reinterpret_cast<const float4*>(stage_buf);
-        for (int e = row; e < n_el; e += 128) {
-          const int rr = r0 + e / kV, c4 = e - (e / kV) * kV;
-          const long long px = pix_tab[rr];
-          if (px < 0) continue;
-          float4 acc4 = sb[e];
-          for (int s2 = 1; s2 < ns; ++s2) {
-            const float4 a = sb[s2 * n_el + e];
-            acc4.x += a.x; acc4.y += a.y; acc4.z += a.z; acc4.w += a.w;
-          }
-          const int co = nt * BN + c4 * 4;
-          if (co < p.cout) {
-            const float4 b4 = *reinterpret_cast<const float4*>(sbt + c4 * 4);
-            acc4.x += b4.x; acc4.y += b4.y; acc4.z += b4.z; acc4.w += b4.w;
-            if (p.y_f32) {
-              *reinterpret_cast<float4*>(static_cast<float*>(p.y) + px + co) = acc4;
-            } else {
-              __nv_bfloat162 t0 = __floats2bfloat162_rn(acc4.x, acc4.y);
-              __nv_bfloat162 t1 = __floats2bfloat162_rn(acc4.z, acc4.w);
-              uint2 pk;
-              pk.x = *reinterpret_cast<uint32_t*>(&t0);
-              pk.y = *reinterpret_cast<uint32_t*>(&t1);
-              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.y) + px + co) = pk;
+        if (ncol > 0) {
+          mbar_wait(red_bar, 0);
+          if (valid) {
+            // thread = row (its own pixel); partials summed in split order (deterministic)
+            for (int c = 0; c < ncol; c += 8) {
+              const int co = nt * BN + c0s + c;
+              if (co >= p.cout) break;
+              float v8[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v8[i] = stage_buf[(size_t)(c + i) * kBM + row];
+              for (int s2 = 1; s2 < ns; ++s2) {
+                const float* sp = stage_buf + (size_t)s2 * ncol * kBM;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v8[i] += sp[(size_t)(c + i) * kBM + row];
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v8[i] += sbt[c0s + c + i];
+              if (p.y_f32) {
+                float* yp = static_cast<float*>(p.y) + pix + co;
+                *reinterpret_cast<float4*>(yp) = make_float4(v8[0], v8[1], v8[2], v8[3]);
+                *reinterpret_cast<float4*>(yp + 4) = make_float4(v8[4], v8[5], v8[6], v8[7]);
+              } else {
+                uint4 pk;
+                __nv_bfloat162 t0 = __floats2bfloat162_rn(v8[0], v8[1]);
+                __nv_bfloat162 t1 = __floats2bfloat162_rn(v8[2], v8[3]);
+                __nv_bfloat162 t2 = __floats2bfloat162_rn(v8[4], v8[5]);
+                __nv_bfloat162 t3 = __floats2bfloat162_rn(v8[6], v8[7]);
+                pk.x = *reinterpret_cast<uint32_t*>(&t0);
+                pk.y = *reinterpret_cast<uint32_t*>(&t1);
+                pk.z = *reinterpret_cast<uint32_t*>(&t2);
+                pk.w = *reinterpret_cast<uint32_t*>(&t3);
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + pix + co) = pk;
+              }
             }
           }
         }
         // departure: the last unit to leave re-zeroes both counters for the next launch
         named_bar_sync(1, 128);
+#ifdef SPHINX_TRACE
+        if (row == 0) CONV_TRACE(18, gtimer());
+#endif
         if (row == 0) {
           const int old = atomicAdd(arrive + 1, 1);
           if (old == ns - 1) {
@@ -1294,11 +1314,11 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
 
 #ifdef SPHINX_TRACE
 extern "C" SPHINX_API int sphinx_debug_conv_trace_reset() {
-  static unsigned long long zero[1024 * 16] = {};
+  static unsigned long long zero[1024 * 24] = {};
   return cudaMemcpyToSymbol(sphinx::g_conv_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
 }
 extern "C" SPHINX_API int sphinx_debug_conv_trace(unsigned long long* host, int n_ctas) {
-  return cudaMemcpyFromSymbol(host, sphinx::g_conv_trace, sizeof(unsigned long long) * 16 * n_ctas) ==
+  return cudaMemcpyFromSymbol(host, sphinx::g_conv_trace, sizeof(unsigned long long) * 24 * n_ctas) ==
                  cudaSuccess ? 0 : -1;
 }
 #endif

@@ -28,8 +28,8 @@ for _ in range(3):
 torch.cuda.synchronize()
 base = 3 * n_conv
 sms = torch.cuda.get_device_properties(0).multi_processor_count
-buf = (ctypes.c_ulonglong * (sms * 16))()
-zero = (ctypes.c_ulonglong * (sms * 16))()
+buf = (ctypes.c_ulonglong * (sms * 24))()
+zero = (ctypes.c_ulonglong * (sms * 24))()
 for j in range(n_conv):
     lib.sphinx_debug_conv_trace_reset()
     os.environ["SPHINX_TRACE_LAUNCH"] = str(base + j)
@@ -37,7 +37,7 @@ for j in range(n_conv):
     torch.cuda.synchronize()
     base += n_conv
     assert lib.sphinx_debug_conv_trace(buf, sms) == 0
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(sms, 16).astype(np.int64)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(sms, 24).astype(np.int64)
     live = a[:, 0] > 0
     a = a[live]
     t0 = a[:, 0].min()
@@ -46,12 +46,19 @@ for j in range(n_conv):
     chunks = a[lead, 6]
     print(f"conv {j} (level {j // bench.CONVS_PER_LEVEL}): {live.sum()} CTAs, "
           f"kernel span {(a[:, 5].max() - t0) / 1e3:.1f} us")
-    for name, c in (("entry", 0), ("after pdl_wait", 1), ("first A issued", 8), ("first B issued", 9),
+    for name, c in (("entry", 0), ("after pdl_wait", 1), ("setup done", 15), ("first A issued", 8), ("first B issued", 9),
                     ("first A full", 10), ("first MMA", 2), ("last MMA", 3), ("last acc ready", 11),
-                    ("epilogue done", 4), ("exit", 5), ("B producer done", 7)):
+                    ("epilogue done", 4), ("exit", 5), ("B producer done", 7),
+                    ("split parked", 16), ("split rendezvous", 17), ("split reduced", 18)):
         v = rel(c)[a[:, c] > 0]
         if len(v):
             print(f"   {name:16s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f}")
+    sp_ = a[:, 16] > 0
+    if sp_.any():
+        print(f"   split units: {sp_.sum()} CTAs, ns {np.unique(a[sp_, 19])}; last acc->parked med "
+              f"{np.median((a[sp_, 16] - a[sp_, 11]) / 1e3):.2f} us, parked->rendezvous med "
+              f"{np.median((a[sp_, 17] - a[sp_, 16]) / 1e3):.2f} us (max {np.max((a[sp_, 17] - a[sp_, 16]) / 1e3):.2f}), "
+              f"reduce med {np.median((a[sp_, 18] - a[sp_, 17]) / 1e3):.2f} us")
     nt_ = np.maximum(a[:, 12], 1)
     print(f"   epilogue tiles med {np.median(a[:, 12]):.0f}; TMEM drain per tile med "
           f"{np.median(a[:, 13] / nt_) / 1e3:.2f} us, last tile med {np.median(a[:, 14]) / 1e3:.2f} us; "
