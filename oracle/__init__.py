@@ -21,6 +21,9 @@ Parity status per function:
                                                     S:316 flat segment, eps-direction invariant)
   laplacian_var / box_smooth / otsu / uncertainty   pinned (S:201-213 examples, brute-force Otsu
     (NEXT-2)                                        argmax, variance identities)
+  bf16_rne / gn_stats / gn_silu / resblock          pinned (torch RNE float->bfloat16 incl. ties,
+    (NEXT-3)                                        torch fp64 group_norm/silu/conv2d dense
+                                                    formulation, density 0, cache consistency)
 """
 import ctypes
 import os
@@ -91,6 +94,10 @@ def load():
             "oracle_otsu": [P, ctypes.c_long, P],
             "oracle_otsu_f64": [P, ctypes.c_long, P],
             "oracle_uncertainty": [P, I, I, I, I, I, P, P],
+            "oracle_gn_stats": [P, I, I, I, I, I, P, P],
+            "oracle_gn_silu": [P, I, I, I, I, I, P, P, P, P, D, P, P],
+            "oracle_resblock": [P, P, P, P, P, P, P, P, P, P, P, I, D, I, I, I, I, I, P, I,
+                                P, P, P, P, P, P, P, P, P, I],
         }
         for name, args in sig.items():
             fn = getattr(_lib, name)
@@ -100,6 +107,8 @@ def load():
         _lib.oracle_eq2.restype = D
         _lib.oracle_select_k.argtypes = [P, D]
         _lib.oracle_select_k.restype = ctypes.c_int32
+        _lib.oracle_bf16_rne.argtypes = [D]
+        _lib.oracle_bf16_rne.restype = ctypes.c_uint16
     return _lib
 
 
@@ -310,3 +319,58 @@ def uncertainty(rgb, window=7, smooth=5):
     tau = np.zeros(n, np.float32)
     _check(lib.oracle_uncertainty(_p(rgb), n, h, w, window, smooth, _p(U), _p(tau)), "uncertainty")
     return U, tau
+
+
+def bf16_rne(v):
+    """NEXT-3: bfloat16 bits of each double, round to nearest even (from fp64 directly)."""
+    lib = load()
+    v = np.asarray(v, np.float64)
+    return np.array([lib.oracle_bf16_rne(float(t)) for t in v.ravel()], np.uint16).reshape(v.shape)
+
+
+def gn_stats(x, groups):
+    """NEXT-3a: per (frame, group) mean and population variance over the full NHWC map."""
+    lib = load()
+    x = _c(x, np.float64)
+    n, h, w, c = x.shape
+    mean = np.zeros((n, groups)); var = np.zeros((n, groups))
+    _check(lib.oracle_gn_stats(_p(x), n, h, w, c, groups, _p(mean), _p(var)), "gn_stats")
+    return mean, var
+
+
+def gn_silu(x, groups, gamma, beta, eps, mean=None, var=None):
+    """NEXT-3b: (t, SiLU(t)) with t = GroupNorm(x) (statistics of x unless given)."""
+    lib = load()
+    x = _c(x, np.float64)
+    if mean is None:
+        mean, var = gn_stats(x, groups)
+    mean = _c(mean, np.float64); var = _c(var, np.float64)
+    gamma = _c(gamma, np.float32); beta = _c(beta, np.float32)
+    n, h, w, c = x.shape
+    t = np.zeros(x.shape); a = np.zeros(x.shape)
+    _check(lib.oracle_gn_silu(_p(x), n, h, w, c, groups, _p(mean), _p(var), _p(gamma), _p(beta),
+                              float(eps), _p(t), _p(a)), "gn_silu")
+    return t, a
+
+
+def resblock(x_bits, h_cache_bits, y_cache, w1_bits, b1, w2_bits, b2, g1, be1, g2, be2,
+             groups, eps, b, ids, n_threads=0):
+    """NEXT-3 sparse ResNet block (R-26, R-27).  Returns a dict of fp64 / bf16-bit arrays:
+    a1_pre, a1, h_pre, h_abs, h, a2_pre, a2, y, y_abs (see sphinx_oracle.c)."""
+    lib = load()
+    x = _c(x_bits, np.uint16); hc = _c(h_cache_bits, np.uint16); yc = _c(y_cache, np.float64)
+    w1 = _c(w1_bits, np.uint16); w2 = _c(w2_bits, np.uint16)
+    b1 = _c(b1, np.float32); b2 = _c(b2, np.float32)
+    g1 = _c(g1, np.float32); be1 = _c(be1, np.float32)
+    g2 = _c(g2, np.float32); be2 = _c(be2, np.float32)
+    ids = _c(ids, np.int32)
+    n, h, w, c = x.shape
+    o = {k: np.zeros(x.shape) for k in ("a1_pre", "h_pre", "h_abs", "a2_pre", "y", "y_abs")}
+    o.update({k: np.zeros(x.shape, np.uint16) for k in ("a1", "h", "a2")})
+    _check(lib.oracle_resblock(_p(x), _p(hc), _p(yc), _p(w1), _p(b1), _p(w2), _p(b2),
+                               _p(g1), _p(be1), _p(g2), _p(be2), int(groups), float(eps),
+                               n, h, w, c, b, _p(ids), len(ids),
+                               _p(o["a1_pre"]), _p(o["a1"]), _p(o["h_pre"]), _p(o["h_abs"]),
+                               _p(o["h"]), _p(o["a2_pre"]), _p(o["a2"]), _p(o["y"]),
+                               _p(o["y_abs"]), n_threads), "resblock")
+    return o

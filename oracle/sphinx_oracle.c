@@ -552,3 +552,170 @@ int oracle_uncertainty(const float* rgb, int n, int h, int w, int window, int sm
   free(B);
   return rc;
 }
+
+/* ------------------------------------------------------------- NEXT-3 ---- */
+
+/* Round a double to the nearest bfloat16 (8 significant bits), ties to even, directly
+ * from the fp64 value (no intermediate fp32 rounding).  Overflow -> +-inf; NaN -> qNaN. */
+uint16_t oracle_bf16_rne(double v) {
+  if (isnan(v)) return 0x7fc0;
+  double a = fabs(v);
+  double r;
+  if (a == 0.0) {
+    r = 0.0;
+  } else {
+    int e = ilogb(a);            /* a in [2^e, 2^(e+1)) */
+    if (e < -126) e = -126;      /* bf16 subnormals share the binary32 minimum exponent */
+    double ulp = ldexp(1.0, e - 7);
+    double q = a / ulp;          /* exact: power-of-two scaling */
+    double fl = floor(q);
+    double rem = q - fl;
+    if (rem > 0.5 || (rem == 0.5 && fmod(fl, 2.0) != 0.0)) fl += 1.0;
+    r = fl * ulp;
+    if (r > 3.3895313892515355e38) r = INFINITY;  /* above the largest bf16 */
+  }
+  float f = (float)(signbit(v) ? -r : r);  /* exact: r has <= 8 significant bits; keeps -0 */
+  uint32_t bits;
+  memcpy(&bits, &f, sizeof bits);
+  return (uint16_t)(bits >> 16);
+}
+
+/* GroupNorm statistics over the full current map (reading R-26): for frame i and group g
+ * (channels [g*c/G, (g+1)*c/G), consecutive as in torch.nn.GroupNorm), mean and population
+ * variance of the h*w*c/G values, two passes in fp64. */
+int oracle_gn_stats(const double* x, int n, int h, int w, int c, int groups, double* mean,
+                    double* var) {
+  if (!x || !mean || !var || n <= 0 || h <= 0 || w <= 0 || c <= 0 || groups <= 0 ||
+      c % groups != 0)
+    return BAD;
+  int cg = c / groups;
+  size_t plane = (size_t)h * w;
+  for (int i = 0; i < n; ++i)
+    for (int g = 0; g < groups; ++g) {
+      double s = 0.0;
+      for (size_t p = 0; p < plane; ++p)
+        for (int k = 0; k < cg; ++k) s += x[((size_t)i * plane + p) * c + g * cg + k];
+      double cnt = (double)plane * cg;
+      double m = s / cnt;
+      double ss = 0.0;
+      for (size_t p = 0; p < plane; ++p)
+        for (int k = 0; k < cg; ++k) {
+          double d = x[((size_t)i * plane + p) * c + g * cg + k] - m;
+          ss += d * d;
+        }
+      mean[i * groups + g] = m;
+      var[i * groups + g] = ss / cnt;
+    }
+  return 0;
+}
+
+/* GroupNorm + SiLU (the normalisation/activation in front of each conv of a UNet ResNet
+ * block; reading R-26): t = gamma[ch] (x - mean) / sqrt(var + eps) + beta[ch],
+ * a = SiLU(t) = t / (1 + exp(-t)).  Every pixel of the map.  t may be NULL. */
+int oracle_gn_silu(const double* x, int n, int h, int w, int c, int groups, const double* mean,
+                   const double* var, const float* gamma, const float* beta, double eps,
+                   double* t, double* a) {
+  if (!x || !mean || !var || !gamma || !beta || !a || n <= 0 || h <= 0 || w <= 0 || c <= 0 ||
+      groups <= 0 || c % groups != 0 || !(eps >= 0.0))
+    return BAD;
+  int cg = c / groups;
+  size_t plane = (size_t)h * w;
+  for (int i = 0; i < n; ++i)
+    for (size_t p = 0; p < plane; ++p)
+      for (int ch = 0; ch < c; ++ch) {
+        size_t o = ((size_t)i * plane + p) * c + ch;
+        int g = ch / cg;
+        double sd = sqrt(var[i * groups + g] + eps);
+        double tt = (double)gamma[ch] * (x[o] - mean[i * groups + g]) / sd + (double)beta[ch];
+        if (t) t[o] = tt;
+        a[o] = tt / (1.0 + exp(-tt));
+      }
+  return 0;
+}
+
+/* NEXT-3. Block-sparse UNet ResNet block with latent reuse ("ResNet layers ... can be
+ * safely applied only to frames selected for refinement"; "reuses cached latents from
+ * the last full denoising step for unrefined regions"; readings R-26, R-27):
+ *   a1 = bf16(SiLU(GN1(x)))                       GN statistics over the full current map x
+ *   h  = listed ? bf16(conv3x3(a1; w1) + b1) : h_cache
+ *   a2 = bf16(SiLU(GN2(h)))                       GN statistics over the full map h
+ *   y  = listed ? x + conv3x3(a2; w2) + b2 : y_cache       (identity skip, C_in = C_out)
+ * x, h_cache: bf16 bits NHWC [n][h][w][c]; y_cache: double.  w1, w2: bf16 bits [c][3][3][c];
+ * b1, b2, g1, be1, g2, be2: fp32 [c].  Outputs (every pixel, double unless noted):
+ * a1_pre / a2_pre = the SiLU values before bf16 rounding; a1, a2 = their bf16 bits;
+ * h_pre = listed ? conv1 value (before rounding) : decoded h_cache; h_out = bf16 bits of h;
+ * h_abs / y_abs = sum |w*a| (+|b|) at listed pixels (0 elsewhere); y.  Any output may be
+ * NULL except y. */
+int oracle_resblock(const uint16_t* x, const uint16_t* h_cache, const double* y_cache,
+                    const uint16_t* w1, const float* b1, const uint16_t* w2, const float* b2,
+                    const float* g1, const float* be1, const float* g2, const float* be2,
+                    int groups, double eps, int n, int h, int w, int c, int b,
+                    const int32_t* ids, int count, double* a1_pre, uint16_t* a1_out,
+                    double* h_pre, double* h_abs, uint16_t* h_out, double* a2_pre,
+                    uint16_t* a2_out, double* y, double* y_abs, int n_threads) {
+  if (!x || !h_cache || !y_cache || !w1 || !w2 || !g1 || !be1 || !g2 || !be2 || !y) return BAD;
+  if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || b <= 0 || groups <= 0 || c % groups != 0) return BAD;
+  if (count < 0 || (count > 0 && !ids)) return BAD;
+  int hb = (h + b - 1) / b, wb = (w + b - 1) / b;
+  for (int j = 0; j < count; ++j)
+    if (ids[j] < 0 || ids[j] >= n * hb * wb) return BAD;
+  size_t npx = (size_t)n * h * w, tot = npx * c;
+  /* listed[pixel]: the pixel's block is in the list (P:352 block granularity) */
+  uint8_t* listed = (uint8_t*)calloc(npx, 1);
+  double* xd = widen(x, tot);
+  double* m = (double*)malloc((size_t)n * groups * sizeof(double));
+  double* v = (double*)malloc((size_t)n * groups * sizeof(double));
+  double* act = (double*)malloc(tot * sizeof(double));
+  uint16_t* abits = (uint16_t*)malloc(tot * sizeof(uint16_t));
+  double* cv = (double*)malloc(tot * sizeof(double));
+  double* ca = (double*)malloc(tot * sizeof(double));
+  uint16_t* hb16 = (uint16_t*)malloc(tot * sizeof(uint16_t));
+  double* hd = (double*)malloc(tot * sizeof(double));
+  int rc = 0;
+  if (!listed || !xd || !m || !v || !act || !abits || !cv || !ca || !hb16 || !hd) { rc = -2; goto done; }
+  for (int j = 0; j < count; ++j) {
+    int id = ids[j];
+    int i = id / (hb * wb), by = (id / wb) % hb, bx = id % wb;
+    for (int yy = by * b; yy < by * b + b && yy < h; ++yy)
+      for (int xx = bx * b; xx < bx * b + b && xx < w; ++xx) listed[((size_t)i * h + yy) * w + xx] = 1;
+  }
+  /* 1. a1 = bf16(SiLU(GN1(x))) over the full map */
+  if ((rc = oracle_gn_stats(xd, n, h, w, c, groups, m, v)) != 0) goto done;
+  if ((rc = oracle_gn_silu(xd, n, h, w, c, groups, m, v, g1, be1, eps, NULL, act)) != 0) goto done;
+  for (size_t e = 0; e < tot; ++e) abits[e] = oracle_bf16_rne(act[e]);
+  if (a1_pre) memcpy(a1_pre, act, tot * sizeof(double));
+  if (a1_out) memcpy(a1_out, abits, tot * sizeof(uint16_t));
+  /* 2. h = listed ? bf16(conv1) : h_cache */
+  for (size_t e = 0; e < tot; ++e) { cv[e] = 0.0; ca[e] = 0.0; }
+  if ((rc = oracle_conv3x3_blocks(abits, w1, b1, n, h, w, c, c, b, ids, count, cv, ca, n_threads)) != 0)
+    goto done;
+  for (size_t p = 0; p < npx; ++p)
+    for (int ch = 0; ch < c; ++ch) {
+      size_t e = p * c + ch;
+      hb16[e] = listed[p] ? oracle_bf16_rne(cv[e]) : h_cache[e];
+      hd[e] = bf16_to_double(hb16[e]);
+      if (h_pre) h_pre[e] = listed[p] ? cv[e] : hd[e];
+      if (h_abs) h_abs[e] = listed[p] ? ca[e] : 0.0;
+    }
+  if (h_out) memcpy(h_out, hb16, tot * sizeof(uint16_t));
+  /* 3. a2 = bf16(SiLU(GN2(h))) over the full map */
+  if ((rc = oracle_gn_stats(hd, n, h, w, c, groups, m, v)) != 0) goto done;
+  if ((rc = oracle_gn_silu(hd, n, h, w, c, groups, m, v, g2, be2, eps, NULL, act)) != 0) goto done;
+  for (size_t e = 0; e < tot; ++e) abits[e] = oracle_bf16_rne(act[e]);
+  if (a2_pre) memcpy(a2_pre, act, tot * sizeof(double));
+  if (a2_out) memcpy(a2_out, abits, tot * sizeof(uint16_t));
+  /* 4. y = listed ? x + conv2 : y_cache  (identity skip) */
+  for (size_t e = 0; e < tot; ++e) { cv[e] = 0.0; ca[e] = 0.0; }
+  if ((rc = oracle_conv3x3_blocks(abits, w2, b2, n, h, w, c, c, b, ids, count, cv, ca, n_threads)) != 0)
+    goto done;
+  for (size_t p = 0; p < npx; ++p)
+    for (int ch = 0; ch < c; ++ch) {
+      size_t e = p * c + ch;
+      y[e] = listed[p] ? xd[e] + cv[e] : y_cache[e];
+      if (y_abs) y_abs[e] = listed[p] ? ca[e] + fabs(xd[e]) : 0.0;
+    }
+done:
+  free(listed); free(xd); free(m); free(v); free(act); free(abits); free(cv); free(ca);
+  free(hb16); free(hd);
+  return rc;
+}

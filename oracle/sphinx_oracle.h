@@ -140,6 +140,33 @@ int oracle_otsu_f64(const double* values, long count, float* tau);
 int oracle_uncertainty(const float* rgb, int n, int h, int w, int window, int smooth, double* U,
                        float* tau);
 
+/* NEXT-3 helpers.  Round a double to bfloat16 bits, nearest-even, directly from fp64. */
+uint16_t oracle_bf16_rne(double v);
+
+/* NEXT-3a. GroupNorm statistics over the full current map (reading R-26): per (frame i,
+ * group g) mean and population variance of the h*w*c/G values of channels
+ * [g*c/G, (g+1)*c/G), two passes in fp64.  mean, var: [n][groups]. */
+int oracle_gn_stats(const double* x, int n, int h, int w, int c, int groups, double* mean,
+                    double* var);
+
+/* NEXT-3b. t = gamma[ch] (x - mean)/sqrt(var + eps) + beta[ch]; a = SiLU(t) = t/(1+exp(-t)),
+ * every pixel (P:333 ResNet block normalisation/activation; R-26).  t may be NULL. */
+int oracle_gn_silu(const double* x, int n, int h, int w, int c, int groups, const double* mean,
+                   const double* var, const float* gamma, const float* beta, double eps,
+                   double* t, double* a);
+
+/* NEXT-3. Block-sparse ResNet block with latent reuse (R-26, R-27):
+ *   a1 = bf16(SiLU(GN1(x)));  h = listed ? bf16(conv(a1;w1)+b1) : h_cache;
+ *   a2 = bf16(SiLU(GN2(h)));  y = listed ? x + conv(a2;w2)+b2 : y_cache.
+ * GN statistics over the full current maps.  See sphinx_oracle.c for the outputs. */
+int oracle_resblock(const uint16_t* x, const uint16_t* h_cache, const double* y_cache,
+                    const uint16_t* w1, const float* b1, const uint16_t* w2, const float* b2,
+                    const float* g1, const float* be1, const float* g2, const float* be2,
+                    int groups, double eps, int n, int h, int w, int c, int b,
+                    const int32_t* ids, int count, double* a1_pre, uint16_t* a1_out,
+                    double* h_pre, double* h_abs, uint16_t* h_out, double* a2_pre,
+                    uint16_t* a2_out, double* y, double* y_abs, int n_threads);
+
 #ifdef __cplusplus
 }
 #endif

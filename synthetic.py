@@ -141,6 +141,27 @@ def bias_f32(cout, tag):
     return (rng("bias", tag, cout).standard_normal(cout, dtype=np.float32) * np.float32(0.01))
 
 
+def resblock_features_bf16(shape, tag):
+    """NEXT-3 ResNet-block input: per-channel offset U(-1,1) and scale U(0.5,2) on N(0,1)
+    (so the GroupNorm statistics are far from (0,1)), rounded to bf16 bits."""
+    g = rng("rbfeat", tag, shape)
+    c = shape[-1]
+    off = g.uniform(-1.0, 1.0, c).astype(np.float32)
+    sc = g.uniform(0.5, 2.0, c).astype(np.float32)
+    return to_bf16_bits(g.standard_normal(shape, dtype=np.float32) * sc + off)
+
+
+def gn_affine_f32(c, tag):
+    """GroupNorm affine parameters: gamma ~ 1 + 0.2 N(0,1), beta ~ 0.2 N(0,1), fp32 [c]."""
+    g = rng("gn", tag, c)
+    return ((1.0 + 0.2 * g.standard_normal(c)).astype(np.float32),
+            (0.2 * g.standard_normal(c)).astype(np.float32))
+
+
+GN_GROUPS = 32     # torch/SD UNet Normalize(): GroupNorm(32, C, eps=1e-6) (reading R-26)
+GN_EPS = 1e-6
+
+
 def latents_f32(shape, tag):
     return rng("lat", tag, shape).standard_normal(shape, dtype=np.float32)
 

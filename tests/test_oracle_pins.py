@@ -500,3 +500,109 @@ def test_uncertainty_blur_mask_properties():
     m = U[0] > tau[0]
     assert m[:, 40:].mean() >= 0.95 and m[:, :24].mean() <= 0.05
     assert set(np.unique(m)) <= {False, True}
+
+
+# ------------------------------------------------------- NEXT-3 sparse ResNet block
+
+def _listed_px(ids, n, h, w, b):
+    hb, wb = -(-h // b), -(-w // b)
+    m = np.zeros((n, h, w), bool)
+    for id_ in ids:
+        i, r = divmod(int(id_), hb * wb)
+        by, bx = divmod(r, wb)
+        m[i, by * b:(by + 1) * b, bx * b:(bx + 1) * b] = True
+    return m
+
+
+def test_bf16_rne_matches_torch_including_ties():
+    """oracle_bf16_rne == torch's float32 -> bfloat16 conversion (round to nearest even) on
+    fp32-representable doubles, including exact ties (low 16 bits 0x8000) and signed zero."""
+    torch = pytest.importorskip("torch")
+    rg = np.random.default_rng(11)
+    f = rg.standard_normal(20000).astype(np.float32) * np.float32(3.0)
+    bits = f.view(np.uint32)
+    ties = ((bits[:4000] & 0xFFFF0000) | 0x8000).view(np.float32)   # exact halfway cases
+    vals = np.concatenate([f, ties, np.float32([0.0, -0.0, 1e-30, -2.5e-39, 3.3e38])])
+    want = torch.from_numpy(vals).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    got = oracle.bf16_rne(vals.astype(np.float64))
+    assert np.array_equal(got, want)
+
+
+def test_gn_silu_matches_torch_group_norm():
+    """GroupNorm (consecutive channel groups, population variance, per-sample statistics)
+    + SiLU equals torch.nn.functional.group_norm / silu in fp64 on the NCHW view."""
+    torch = pytest.importorskip("torch")
+    n, h, w, c, G = 2, 9, 7, 40, 4
+    x = syn.bf16_bits_to_f32(syn.resblock_features_bf16((n, h, w, c), "pin-gn")).astype(np.float64)
+    g, be = syn.gn_affine_f32(c, "pin-gn")
+    t, a = oracle.gn_silu(x, G, g, be, 1e-6)
+    xt = torch.from_numpy(x).permute(0, 3, 1, 2)
+    ref = torch.nn.functional.group_norm(xt, G, torch.from_numpy(g.astype(np.float64)),
+                                         torch.from_numpy(be.astype(np.float64)), eps=1e-6)
+    assert np.max(np.abs(t - ref.permute(0, 2, 3, 1).numpy())) <= 1e-12
+    assert np.max(np.abs(a - torch.nn.functional.silu(ref).permute(0, 2, 3, 1).numpy())) <= 1e-12
+    m, v = oracle.gn_stats(x, G)
+    assert np.allclose(m[1, 2], x[1, :, :, 20:30].mean(), rtol=0, atol=1e-13)
+
+
+def _rb_inputs(n, h, w, c, tag):
+    x = syn.resblock_features_bf16((n, h, w, c), tag)
+    hc = syn.resblock_features_bf16((n, h, w, c), tag + "-hc")
+    yc = syn.bf16_bits_to_f32(syn.features_bf16((n, h, w, c), tag + "-yc")).astype(np.float64)
+    w1, w2 = syn.weights_bf16(c, c, tag + "-1"), syn.weights_bf16(c, c, tag + "-2")
+    b1, b2 = syn.bias_f32(c, tag + "-1"), syn.bias_f32(c, tag + "-2")
+    g1, be1 = syn.gn_affine_f32(c, tag + "-1")
+    g2, be2 = syn.gn_affine_f32(c, tag + "-2")
+    return x, hc, yc, w1, b1, w2, b2, g1, be1, g2, be2
+
+
+def test_resblock_matches_torch_dense_formulation():
+    """R-26/R-27 written as torch fp64 dense ops + where(): h = where(listed, conv2d(a1)+b1,
+    h_cache), GroupNorm of the FULL map h (fresh + cached), y = where(listed, x + conv2d(a2)
+    + b2, y_cache).  Each rounding point uses the oracle's a1/h/a2 bits (bf16_rne is pinned
+    above), each arithmetic stage is re-derived with library ops."""
+    torch = pytest.importorskip("torch")
+    F = torch.nn.functional
+    n, h, w, c, b, G = 2, 12, 10, 32, 4, 8
+    x, hc, yc, w1, b1, w2, b2, g1, be1, g2, be2 = _rb_inputs(n, h, w, c, "pin-rb")
+    hb, wb = 3, 3
+    ids = np.array([0, 1, 4, 8, 9, 12, 17])
+    o = oracle.resblock(x, hc, yc, w1, b1, w2, b2, g1, be1, g2, be2, G, 1e-6, b, ids)
+    L = _listed_px(ids, n, h, w, b)[..., None]
+    d = lambda bits: torch.from_numpy(syn.bf16_bits_to_f32(bits).astype(np.float64)).permute(0, 3, 1, 2)
+    nhwc = lambda t: t.permute(0, 2, 3, 1).numpy()
+    t64 = lambda a: torch.from_numpy(np.asarray(a, np.float64))
+    a1 = nhwc(F.silu(F.group_norm(d(x), G, t64(g1), t64(be1), eps=1e-6)))
+    assert np.max(np.abs(o["a1_pre"] - a1)) <= 1e-12
+    assert np.array_equal(o["a1"], oracle.bf16_rne(o["a1_pre"]))
+    c1 = nhwc(F.conv2d(d(o["a1"]), d(w1), t64(b1), padding=1))
+    assert np.max(np.abs(np.where(L, o["h_pre"], 0) - np.where(L, c1, 0))) <= 1e-12
+    assert np.array_equal(o["h"], np.where(L, oracle.bf16_rne(c1), hc))
+    a2 = nhwc(F.silu(F.group_norm(d(o["h"]), G, t64(g2), t64(be2), eps=1e-6)))
+    assert np.max(np.abs(o["a2_pre"] - a2)) <= 1e-12
+    c2 = nhwc(F.conv2d(d(o["a2"]), d(w2), t64(b2), padding=1))
+    xd = nhwc(d(x))
+    assert np.max(np.abs(o["y"] - np.where(L, xd + c2, yc))) <= 1e-12
+
+
+def test_resblock_density_0_and_full_cache_consistency():
+    """Density 0: y == y_cache and h == h_cache exactly.  Latent reuse: with caches
+    from the dense pass (every block listed) on the same x, ANY block list reproduces the
+    dense output bit for bit (the sparse block is exact, not an approximation, when the
+    cache is current)."""
+    n, h, w, c, b, G = 2, 16, 16, 16, 8, 4
+    x, hc, yc, w1, b1, w2, b2, g1, be1, g2, be2 = _rb_inputs(n, h, w, c, "pin-rb0")
+    args = (w1, b1, w2, b2, g1, be1, g2, be2, G, 1e-6, b)
+    o0 = oracle.resblock(x, hc, yc, *args, np.zeros(0, np.int32))
+    assert np.array_equal(o0["y"], yc) and np.array_equal(o0["h"], hc)
+    dense = oracle.resblock(x, hc, yc, *args, np.arange(n * 4))
+    for ids in ([0], [1, 2, 7], [3, 4, 5, 6]):
+        o = oracle.resblock(x, dense["h"], dense["y"], *args, np.array(ids))
+        assert np.array_equal(o["y"], dense["y"]) and np.array_equal(o["h"], dense["h"])
+    # and a stale cache is visible through the halo and the statistics: change the cached h
+    # of an unlisted block -> listed outputs change (GN2 over the full map, halo reads cache)
+    hc2 = dense["h"].copy()
+    hc2[0, 0:8, 8:16] = syn.resblock_features_bf16((8, 8, c), "pin-rb0-stale")
+    o = oracle.resblock(x, hc2, dense["y"], *args, np.array([0]))
+    assert not np.array_equal(o["y"][0, 0:8, 0:8], dense["y"][0, 0:8, 0:8])
+    assert np.array_equal(o["y"][1], dense["y"][1])   # frame 1: nothing listed
