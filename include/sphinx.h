@@ -12,6 +12,10 @@
  *   (3) sphinx_noise_inject    x_t = sqrt(abar) x0 + sqrt(1-abar) eps on listed blocks
  *   (4) sphinx_sparse_conv3x3  halo gather + 3x3 implicit GEMM (tcgen05/TMEM) on listed blocks
  *   (5) sphinx_scatter_cached  out = active ? computed : latent cache
+ * and the SURVEY §8(f) "next" rows built on them: sphinx_ddim_step (NEXT-1),
+ * sphinx_uncertainty_map (NEXT-2), and the block-sparse ResNet block (NEXT-3:
+ * sphinx_gn_block_stats, sphinx_gn_silu, sphinx_sparse_conv3x3_residual,
+ * sphinx_sparse_resblock).
  *
  * CONVENTIONS (all entry points)
  *  - Ownership: every array pointer is caller-owned memory.  "device" pointers must be
@@ -102,7 +106,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 1
+#define SPHINX_ABI_VERSION 2
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -264,6 +268,73 @@ SPHINX_API sphinx_status sphinx_uncertainty_map(const float* rgb, int32_t n, int
                                                 float* tau_u, void* workspace, size_t workspace_bytes,
                                                 sphinx_stream_t stream);
 SPHINX_API size_t sphinx_uncertainty_workspace_size(int32_t n);
+
+/* ---------------------------------------------------------------------------------
+ * NEXT-3. Block-sparse UNet ResNet block with latent reuse ("ResNet layers ...
+ * operate independently on each frame ... can be safely applied only to frames selected for
+ * refinement"; "reuses cached latents from the last full denoising step for unrefined
+ * regions"; readings R-26, R-27 in DESIGN.md):
+ *   a1 = bf16(SiLU(GN1(x)));   h = listed ? bf16(conv3x3(a1; w1) + b1) : h (cached)
+ *   a2 = bf16(SiLU(GN2(h)));   y = listed ? x + conv3x3(a2; w2) + b2 : y (cached)
+ * GroupNorm (torch.nn.GroupNorm semantics: `groups` consecutive-channel groups, population
+ * variance, per-channel affine) takes its statistics over the FULL current map (fresh values
+ * in listed blocks, cached values elsewhere).  They are maintained incrementally in a
+ * persistent per-block statistics buffer so a partial step reads active bytes only.
+ *
+ * Per-block statistics buffer: fp32 [N][Hb][Wb][groups][2] = (mean, M2) of the block's real
+ * pixels x the group's c/groups channels; sphinx_gn_stats_size(...) bytes, 8-byte aligned.
+ * Caller-owned and persistent: at a full step (every block listed, e.g. SELECT_ALL) every entry
+ * is written; a partial step rewrites only listed blocks, the others keep describing the
+ * cached content (which is what the full-map statistics need).
+ * ------------------------------------------------------------------------------- */
+SPHINX_API size_t sphinx_gn_stats_size(int32_t n, int32_t h, int32_t w, int32_t groups, int32_t block);
+
+/* Rewrites the statistics entries of the listed blocks of the bf16 NHWC map x [N][h][w][c]
+ * (fp32 shifted sums per channel, Chan combination per group).  c % 8 == 0, c <= 2048,
+ * c % groups == 0, groups <= 256 (else UNSUPPORTED / INVALID_ARGUMENT). */
+SPHINX_API sphinx_status sphinx_gn_block_stats(const void* x, int32_t n, int32_t h, int32_t w, int32_t c,
+                                               int32_t groups, int32_t block, const int32_t* block_ids,
+                                               const int32_t* count, int32_t capacity, float* stats,
+                                               sphinx_stream_t stream);
+
+/* a = bf16(SiLU(gamma[ch] (x - mean_g) / sqrt(var_g + eps) + beta[ch])), var = M2 / count,
+ * with (mean_g, var_g) of frame n combined from ALL Hb*Wb entries of `stats` (fp32), written
+ * for every pixel of every listed block AND its 1-pixel ring clipped to the image (exactly the
+ * pixels a 3x3 conv over the listed blocks reads); other pixels of `a` are untouched.
+ * x, a: bf16 NHWC [N][h][w][c] device, a != x.  gamma, beta: fp32 [c] device.  eps >= 0. */
+SPHINX_API sphinx_status sphinx_gn_silu(const void* x, const float* stats, const float* gamma,
+                                        const float* beta, float eps, int32_t n, int32_t h, int32_t w,
+                                        int32_t c, int32_t groups, int32_t block,
+                                        const int32_t* block_ids, const int32_t* count,
+                                        int32_t capacity, void* a, sphinx_stream_t stream);
+
+/* sphinx_sparse_conv3x3 with a bf16 NHWC residual [N][h][w][c_out] (16-byte aligned, != x)
+ * added in the epilogue: y = residual + bias + conv (the ResNet block's identity skip). */
+SPHINX_API sphinx_status sphinx_sparse_conv3x3_residual(
+    const void* x, const void* w, const float* bias, const void* residual, void* y,
+    sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, sphinx_stream_t stream);
+
+/* The whole block (6 launches, stream-ordered, graph capturable):
+ *   gn_block_stats(x) -> gn_silu(x) -> conv(w1,b1) into h -> gn_block_stats(h) -> gn_silu(h)
+ *   -> conv_residual(w2,b2, residual x) into y.
+ * x        bf16 NHWC [N][h][w][c]: the current full map (cached values in unlisted blocks).
+ * w1, w2   bf16 OHWI [c][3][3][c]; b1, b2 fp32 [c] or NULL; gn*_gamma/beta fp32 [c].
+ * h_buf    bf16 NHWC, persistent: holds the cached conv1 output; listed pixels are rewritten.
+ * x_stats, h_stats  persistent per-block statistics of x and h (see above); listed entries
+ *          are rewritten.  Initialise them (and h_buf, y) with a full step.
+ * y        NHWC bf16 or fp32, persistent: the block output; listed pixels rewritten.
+ * a_scratch bf16 NHWC [N][h][w][c] scratch (the normalised activations).
+ * workspace as for sphinx_sparse_conv3x3 (c_in = c_out = c).
+ * Buffers must be distinct (no aliasing among x, h_buf, y, a_scratch; x_stats != h_stats). */
+SPHINX_API sphinx_status sphinx_sparse_resblock(
+    const void* x, const void* w1, const float* b1, const void* w2, const float* b2,
+    const float* gn1_gamma, const float* gn1_beta, const float* gn2_gamma, const float* gn2_beta,
+    int32_t groups, float eps, void* h_buf, float* x_stats, float* h_stats, void* y,
+    sphinx_dtype y_dtype, void* a_scratch, int32_t n, int32_t h, int32_t w, int32_t c,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, sphinx_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,10 @@ Functions carry the C names:
     sphinx_noise_inject     step 3  (Alg1 lines 12, 19)
     sphinx_sparse_conv3x3   step 4
     sphinx_scatter_cached   step 5
+    sphinx_ddim_step        NEXT-1  (Alg1 line 18)
+    sphinx_uncertainty_map  NEXT-2  (Alg1 lines 7-8)
+    sphinx_gn_block_stats / sphinx_gn_silu / sphinx_sparse_conv3x3_residual /
+    sphinx_sparse_resblock  NEXT-3  (block-sparse ResNet block)
 """
 import ctypes
 import os
@@ -23,11 +27,13 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 1
+ABI_VERSION = 2
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
-           "sphinx_uncertainty_map", "sphinx_uncertainty_workspace_size")
+           "sphinx_uncertainty_map", "sphinx_uncertainty_workspace_size",
+           "sphinx_gn_stats_size", "sphinx_gn_block_stats", "sphinx_gn_silu",
+           "sphinx_sparse_conv3x3_residual", "sphinx_sparse_resblock")
 
 _lib = None
 
@@ -86,6 +92,12 @@ def load(path=SO_PATH):
         "sphinx_ddim_step": ([P, P, P, I, I, I, I, I, P, P, I, I, P, I, P], I),
         "sphinx_uncertainty_map": ([P, I, I, I, I, I, P, P, P, Z, P], I),
         "sphinx_uncertainty_workspace_size": ([I], Z),
+        "sphinx_gn_stats_size": ([I, I, I, I, I], Z),
+        "sphinx_gn_block_stats": ([P, I, I, I, I, I, I, P, P, I, P, P], I),
+        "sphinx_gn_silu": ([P, P, P, P, F, I, I, I, I, I, I, P, P, I, P, P], I),
+        "sphinx_sparse_conv3x3_residual": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_sparse_resblock": ([P, P, P, P, P, P, P, P, P, I, F, P, P, P, P, I, P,
+                                    I, I, I, I, I, P, P, I, P, Z, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -207,7 +219,7 @@ def conv_workspace(c_out, device, n=1, h=1, w=1, block=8):
 
 
 def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None, stream=None,
-                          workspace=None):
+                          workspace=None, residual=None):
     """Step 4.  x bf16 NHWC [N,H,W,Cin]; w bf16 [Cout,3,3,Cin]; bias fp32 [Cout] or None;
     y NHWC [N,H,W,Cout] bf16 or fp32 (only listed blocks are written).
     workspace: None = a cached zeroed split-K workspace for this device, False = no split-K,
@@ -226,6 +238,14 @@ def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None,
     if workspace is None:
         workspace = conv_workspace(cout, y.device, n, h, wd, block)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
+    if residual is not None:
+        _dev(residual, torch.bfloat16, "residual")
+        rc = load().sphinx_sparse_conv3x3_residual(
+            _ptr(x), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y),
+            F32 if y.dtype == torch.float32 else BF16, n, h, wd, cin, cout, int(block),
+            _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes, _stream(stream))
+        _chk("sphinx_sparse_conv3x3_residual", rc)
+        return
     rc = load().sphinx_sparse_conv3x3(_ptr(x), _ptr(w), _ptr(bias), _ptr(y),
                                       F32 if y.dtype == torch.float32 else BF16,
                                       n, h, wd, cin, cout, int(block), _ptr(block_ids), _ptr(count),
@@ -292,3 +312,74 @@ def sphinx_uncertainty_map(rgb, uncertainty, tau_u, window=7, smooth=5, workspac
     rc = load().sphinx_uncertainty_map(_ptr(rgb), n, h, w, int(window), int(smooth), _ptr(uncertainty),
                                        _ptr(tau_u), _ptr(workspace), workspace.numel(), _stream(stream))
     _chk("sphinx_uncertainty_map", rc)
+
+
+def gn_stats_buffer(n, h, w, groups, block, device):
+    """A per-block GroupNorm statistics buffer (fp32 [N,Hb,Wb,G,2]) for NEXT-3; memory only."""
+    import torch
+    hb, wb = -(-h // block), -(-w // block)
+    return torch.zeros((n, hb, wb, groups, 2), dtype=torch.float32, device=device)
+
+
+def sphinx_gn_block_stats(x, groups, block, block_ids, count, stats, capacity=None, stream=None):
+    """NEXT-3: rewrite the per-block (mean, M2) entries of the listed blocks of bf16 NHWC x."""
+    import torch
+    _dev(x, torch.bfloat16, "x")
+    _dev(stats, torch.float32, "stats")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, h, w, c = x.shape
+    if stats.numel() * 4 != load().sphinx_gn_stats_size(n, h, w, int(groups), int(block)):
+        raise ValueError("stats: expected fp32 [N,Hb,Wb,groups,2]")
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = load().sphinx_gn_block_stats(_ptr(x), n, h, w, c, int(groups), int(block), _ptr(block_ids),
+                                      _ptr(count), int(cap), _ptr(stats), _stream(stream))
+    _chk("sphinx_gn_block_stats", rc)
+
+
+def sphinx_gn_silu(x, stats, gamma, beta, eps, groups, block, block_ids, count, a, capacity=None,
+                   stream=None):
+    """NEXT-3: a = bf16(SiLU(GroupNorm(x))) on listed blocks + their 1-pixel ring."""
+    import torch
+    _dev(x, torch.bfloat16, "x")
+    _dev(a, torch.bfloat16, "a")
+    _dev(stats, torch.float32, "stats")
+    _dev(gamma, torch.float32, "gamma")
+    _dev(beta, torch.float32, "beta")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, h, w, c = x.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = load().sphinx_gn_silu(_ptr(x), _ptr(stats), _ptr(gamma), _ptr(beta), float(eps), n, h, w, c,
+                               int(groups), int(block), _ptr(block_ids), _ptr(count), int(cap), _ptr(a),
+                               _stream(stream))
+    _chk("sphinx_gn_silu", rc)
+
+
+def sphinx_sparse_resblock(x, w1, b1, w2, b2, gn1, gn2, groups, eps, h_buf, x_stats, h_stats, y,
+                           a_scratch, block, block_ids, count, capacity=None, workspace=None,
+                           stream=None):
+    """NEXT-3 block-sparse ResNet block (R-26, R-27).  gn1/gn2 = (gamma, beta)
+    fp32 [C]; h_buf bf16 / y bf16-or-fp32 / x_stats / h_stats persistent (see sphinx.h)."""
+    import torch
+    for t, nm in ((x, "x"), (w1, "w1"), (w2, "w2"), (h_buf, "h_buf"), (a_scratch, "a_scratch")):
+        _dev(t, torch.bfloat16, nm)
+    for t, nm in ((b1, "b1"), (b2, "b2"), (gn1[0], "gn1.gamma"), (gn1[1], "gn1.beta"),
+                  (gn2[0], "gn2.gamma"), (gn2[1], "gn2.beta"), (x_stats, "x_stats"),
+                  (h_stats, "h_stats")):
+        _dev(t, torch.float32, nm)
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    if y.dtype not in (torch.bfloat16, torch.float32) or not (y.is_cuda and y.is_contiguous()):
+        raise ValueError("y: contiguous CUDA bf16/fp32")
+    n, h, wd, c = x.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    if workspace is None:
+        workspace = conv_workspace(c, y.device, n, h, wd, block)
+    ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
+    rc = load().sphinx_sparse_resblock(
+        _ptr(x), _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), _ptr(gn1[0]), _ptr(gn1[1]), _ptr(gn2[0]),
+        _ptr(gn2[1]), int(groups), float(eps), _ptr(h_buf), _ptr(x_stats), _ptr(h_stats), _ptr(y),
+        F32 if y.dtype == torch.float32 else BF16, _ptr(a_scratch), n, h, wd, c, int(block),
+        _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes, _stream(stream))
+    _chk("sphinx_sparse_resblock", rc)

@@ -69,6 +69,7 @@ struct ConvParams {
   const int32_t* count;
   const float* bias;
   void* y;
+  const __nv_bfloat16* res;  // NEXT-3: bf16 NHWC residual added in the epilogue (identity skip), or NULL
   int y_f32;
   int h, w, cout, b, hb, wb;
   int kc;         // 64-channel chunks per tap
@@ -171,7 +172,25 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// 32 consecutive output channels [co, co+32) of one pixel: + bias, fp32 or bf16 store.
+// + residual[pix + co + i] for i < NV (bf16, same NHWC layout as y), 16-byte loads.
+template <int NV>
+__device__ __forceinline__ void add_residual(const ConvParams& p, size_t pix, int co, float* v) {
+  const __nv_bfloat16* rp = p.res + pix + co;
+#pragma unroll
+  for (int g = 0; g < NV; g += 8) {
+    if (co + g < p.cout) {
+      const uint4 r = __ldg(reinterpret_cast<const uint4*>(rp + g));
+      const uint32_t w4[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[g + 2 * k] += __uint_as_float(w4[k] << 16);
+        v[g + 2 * k + 1] += __uint_as_float(w4[k] & 0xffff0000u);
+      }
+    }
+  }
+}
+
+// 32 consecutive output channels [co, co+32) of one pixel: + bias (+ residual), fp32 or bf16 store.
 __device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix, int co, float (&v)[32],
                                                 const float* sb) {
   // sb: this chunk's 32 bias values in shared memory (zero-padded): broadcast LDS.128, no
@@ -184,6 +203,7 @@ __device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix,
     v[i + 2] += b4.z;
     v[i + 3] += b4.w;
   }
+  if (p.res) add_residual<32>(p, pix, co, v);
 #ifdef SPHINX_TRACE
   if (p.dbg & 1) {
     float acc = 0.f;
@@ -949,6 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
 #pragma unroll
               for (int i = 0; i < 8; ++i) v8[i] += sbt[c0s + c + i];
+              if (p.res) add_residual<8>(p, pix, co, v8);
               if (p.y_f32) {
                 float* yp = static_cast<float*>(p.y) + pix + co;
                 *reinterpret_cast<float4*>(yp) = make_float4(v8[0], v8[1], v8[2], v8[3]);
@@ -1171,14 +1192,13 @@ extern "C" size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, i
   return kCntBytes + plan_bytes(capacity) + (size_t)sms * slot_bytes(2, pick_bn(c_out));
 }
 
-extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, const float* bias,
-                                               void* y, sphinx_dtype y_dtype, int32_t n, int32_t h,
-                                               int32_t w_, int32_t c_in, int32_t c_out,
-                                               int32_t block, const int32_t* block_ids,
-                                               const int32_t* count, int32_t capacity,
-                                               void* workspace, size_t workspace_bytes,
-                                               sphinx_stream_t stream) {
+static sphinx_status conv_impl(const void* x, const void* w, const float* bias, const void* residual,
+                               void* y, sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_,
+                               int32_t c_in, int32_t c_out, int32_t block, const int32_t* block_ids,
+                               const int32_t* count, int32_t capacity, void* workspace,
+                               size_t workspace_bytes, sphinx_stream_t stream) {
   if (!x || !w || !y || !block_ids || !count) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (residual && (residual == x || !aligned16(residual))) return SPHINX_ERR_INVALID_ARGUMENT;
   if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u)) return SPHINX_ERR_INVALID_ARGUMENT;
   if (n <= 0 || h <= 0 || w_ <= 0 || c_in <= 0 || c_out <= 0 || block <= 0 || capacity < 0)
     return SPHINX_ERR_INVALID_ARGUMENT;
@@ -1236,6 +1256,7 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
   p.count = count;
   p.bias = bias;
   p.y = y;
+  p.res = static_cast<const __nv_bfloat16*>(residual);
   p.y_f32 = y_dtype == SPHINX_F32;
   p.h = h;
   p.w = w_;
@@ -1310,6 +1331,27 @@ extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
     case 64: return launch_cg<64>(cg, ta, tb, tc, p, grid, s);
     default: return launch_cg<32>(cg, ta, tb, tc, p, grid, s);
   }
+}
+
+extern "C" sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, const float* bias,
+                                               void* y, sphinx_dtype y_dtype, int32_t n, int32_t h,
+                                               int32_t w_, int32_t c_in, int32_t c_out,
+                                               int32_t block, const int32_t* block_ids,
+                                               const int32_t* count, int32_t capacity,
+                                               void* workspace, size_t workspace_bytes,
+                                               sphinx_stream_t stream) {
+  return conv_impl(x, w, bias, nullptr, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
+                   capacity, workspace, workspace_bytes, stream);
+}
+
+extern "C" sphinx_status sphinx_sparse_conv3x3_residual(
+    const void* x, const void* w, const float* bias, const void* residual, void* y,
+    sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, sphinx_stream_t stream) {
+  if (!residual) return SPHINX_ERR_INVALID_ARGUMENT;
+  return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
+                   capacity, workspace, workspace_bytes, stream);
 }
 
 #ifdef SPHINX_TRACE

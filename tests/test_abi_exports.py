@@ -50,3 +50,22 @@ def test_invalid_arguments_rejected_on_host():
     big = lib.sphinx_conv_workspace_size(168, 16, 16, 32, 32, 4)
     assert small > 4096 and big - small >= (168 - 1) * 16 * 4 - 256
     assert lib.sphinx_conv_workspace_size(0, 16, 16, 32, 32, 4) == 0
+
+
+def test_next3_host_validation():
+    """NEXT-3 entry points reject bad host-visible arguments before touching a GPU."""
+    lib = sp.load()
+    p, null = ctypes.c_void_p(1024), None
+    # c % groups != 0 -> invalid; c % 8 != 0 -> unsupported
+    assert lib.sphinx_gn_block_stats(p, 1, 16, 16, 40, 32, 8, p, p, 4, p, null) == sp.ERR_INVALID_ARGUMENT
+    assert lib.sphinx_gn_block_stats(p, 1, 16, 16, 36, 4, 8, p, p, 4, p, null) == sp.ERR_UNSUPPORTED
+    assert lib.sphinx_gn_silu(p, p, p, p, 1e-6, 1, 16, 16, 32, 8, 8, p, p, 4, p, null) == \
+        sp.ERR_INVALID_ARGUMENT  # a aliases x
+    assert lib.sphinx_gn_stats_size(2, 18, 18, 32, 8) == 2 * 9 * 32 * 8
+    assert lib.sphinx_sparse_conv3x3_residual(p, p, null, null, p, sp.F32, 1, 16, 16, 32, 32, 8, p, p,
+                                              4, null, 0, null) == sp.ERR_INVALID_ARGUMENT
+    q = ctypes.c_void_p(2048)
+    # h_buf aliases x
+    assert lib.sphinx_sparse_resblock(p, p, null, p, null, p, p, p, p, 32, 1e-6, p, q, ctypes.c_void_p(4096),
+                                      q, sp.BF16, ctypes.c_void_p(8192), 1, 16, 16, 64, 8, p, p, 4, null,
+                                      0, null) == sp.ERR_INVALID_ARGUMENT
