@@ -348,6 +348,54 @@ def memory_kernels(torch, st, req, reps=10):
     return out
 
 
+def resblock_levels(torch, st, req, reps=20):
+    """NEXT-3: the block-sparse ResNet block (GN+SiLU -> conv -> GN+SiLU -> conv + skip) at each
+    UNet level over the step's active list, after a full step (every block) filled the persistent
+    h / y / statistics buffers.  Graph-replay device time per block (L2-warm) and its parts."""
+    sp, d, dev = st.sp, st.d, st.dev
+    out = []
+    for l, (h, c) in enumerate(LEVELS):
+        n, hb = N_FRAMES, st.dims[l][1]
+        x = d[f"feat{l}"]
+        g1, be1 = (torch.from_numpy(a).to(dev) for a in syn.gn_affine_f32(c, f"gn{l}1"))
+        g2, be2 = (torch.from_numpy(a).to(dev) for a in syn.gn_affine_f32(c, f"gn{l}2"))
+        hbuf = d[f"cache{l}"].clone()
+        y = d[f"cache{l}"].clone()
+        a = torch.empty_like(x)
+        xs = sp.gn_stats_buffer(n, h, h, syn.GN_GROUPS, B, dev)
+        hs = sp.gn_stats_buffer(n, h, h, syn.GN_GROUPS, B, dev)
+        all_ids = torch.arange(n * hb * hb, dtype=torch.int32, device=dev)
+        all_cnt = torch.tensor([n * hb * hb], dtype=torch.int32, device=dev)
+        ids, cnt = st.ids[l], st.cnt[l]
+
+        def block(i=ids, k=cnt):
+            sp.sphinx_sparse_resblock(x, d[f"w{l}0"], d[f"b{l}0"], d[f"w{l}1"], d[f"b{l}1"], (g1, be1),
+                                      (g2, be2), syn.GN_GROUPS, syn.GN_EPS, hbuf, xs, hs, y, a, B, i, k)
+        block(all_ids, all_cnt)  # the full step: every block, fills h, y and both statistics
+        t_block = graph_time(torch, block, reps)
+        t_gn = graph_time(torch, lambda: (
+            sp.sphinx_gn_block_stats(x, syn.GN_GROUPS, B, ids, cnt, xs),
+            sp.sphinx_gn_silu(x, xs, g1, be1, syn.GN_EPS, syn.GN_GROUPS, B, ids, cnt, a)), reps)
+        t_conv = graph_time(torch, lambda: sp.sphinx_sparse_conv3x3(a, d[f"w{l}0"], d[f"b{l}0"], hbuf, B, ids, cnt),
+                            reps)
+        nb = int(cnt.item())
+        idn = ids[:nb].cpu().numpy() % (hb * hb)
+        by, bx = idn // hb, idn % hb
+        px = int((np.minimum(B, h - by * B) * np.minimum(B, h - bx * B)).sum())
+        ring = int(((np.minimum(by * B + B + 1, h) - np.maximum(by * B - 1, 0)) *
+                    (np.minimum(bx * B + B + 1, h) - np.maximum(bx * B - 1, 0))).sum())
+        flops = 2 * px * 2 * 9 * c * c
+        gn_bytes = px * c * 2 + ring * c * 4  # stats read + activation read/write (ring incl.)
+        out.append({"level": l, "shape": [n, h, h, c], "active_blocks": nb, "real_px": px,
+                    "block_ms": round(t_block, 5), "block_tflops": round(flops / (t_block * 1e-3) / 1e12, 2),
+                    "gn_silu_ms": round(t_gn, 5), "gn_silu_gbs": round(gn_bytes / (t_gn * 1e-3) / 1e9, 1),
+                    "conv_ms": round(t_conv, 5),
+                    "gn_share_of_block": round(2 * t_gn / t_block, 4)})
+    return {"levels": out, "timing": "CUDA-graph replay of 20 blocks, L2-warm; block = 6 launches "
+            "(gn_block_stats, gn_silu, conv, gn_block_stats, gn_silu, conv+residual)",
+            "block_tflops_note": "2 convs' algorithmic FLOPs (real active px) / whole-block time"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -463,6 +511,7 @@ def run_gpu(args):
     if rank == 0 and not args.no_sweep:
         sweep = density_sweep(torch, st.sp, dev)
     mem = memory_kernels(torch, st, req) if rank == 0 else None
+    rblk = resblock_levels(torch, st, req) if (rank == 0 and not args.no_resblock) else None
 
     if rank == 0:
         cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(req, bounded_s=args.cpu_seconds)
@@ -492,6 +541,7 @@ def run_gpu(args):
             "conv_levels": per_level,
             "conv_isolated_ms": iso,
             "memory_kernels": mem,
+            "resblock (NEXT-3)": rblk,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "density_sweep": sweep,
@@ -643,6 +693,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-resblock", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-flush", action="store_true", help="diagnostic: keep L2 warm between steps")

@@ -281,28 +281,31 @@ SPHINX_API size_t sphinx_uncertainty_workspace_size(int32_t n);
  * in listed blocks, cached values elsewhere).  They are maintained incrementally in a
  * persistent per-block statistics buffer so a partial step reads active bytes only.
  *
- * Per-block statistics buffer: fp32 [N][Hb][Wb][groups][2] = (mean, M2) of the block's real
- * pixels x the group's c/groups channels; sphinx_gn_stats_size(...) bytes, 8-byte aligned.
- * Caller-owned and persistent: at a full step (every block listed, e.g. SELECT_ALL) every entry
- * is written; a partial step rewrites only listed blocks, the others keep describing the
- * cached content (which is what the full-map statistics need).
+ * Statistics buffer (sphinx_gn_stats_size(...) bytes, 8-byte aligned, caller-owned):
+ *   block entries fp32 [N][Hb][Wb][groups][2] = (mean, M2) of the block's real pixels x the
+ *   group's c/groups channels, then frame entries fp32 [N][groups][2] = (mean, 1/sqrt(var+eps))
+ *   written by sphinx_gn_silu.  Persistent: at a full step (every block listed, e.g.
+ *   SELECT_ALL) every block entry is written; a partial step rewrites only listed blocks, the
+ *   others keep describing the cached content (which is what the full-map statistics need).
  * ------------------------------------------------------------------------------- */
 SPHINX_API size_t sphinx_gn_stats_size(int32_t n, int32_t h, int32_t w, int32_t groups, int32_t block);
 
 /* Rewrites the statistics entries of the listed blocks of the bf16 NHWC map x [N][h][w][c]
- * (fp32 shifted sums per channel, Chan combination per group).  c % 8 == 0, c <= 2048,
- * c % groups == 0, groups <= 256 (else UNSUPPORTED / INVALID_ARGUMENT). */
+ * (fp32 shifted sums per channel, Chan combination per group).  c % groups == 0 (else
+ * INVALID_ARGUMENT); c % 8 == 0 and lcm(c/groups, 8) <= 2048 (else UNSUPPORTED). */
 SPHINX_API sphinx_status sphinx_gn_block_stats(const void* x, int32_t n, int32_t h, int32_t w, int32_t c,
                                                int32_t groups, int32_t block, const int32_t* block_ids,
                                                const int32_t* count, int32_t capacity, float* stats,
                                                sphinx_stream_t stream);
 
 /* a = bf16(SiLU(gamma[ch] (x - mean_g) / sqrt(var_g + eps) + beta[ch])), var = M2 / count,
- * with (mean_g, var_g) of frame n combined from ALL Hb*Wb entries of `stats` (fp32), written
- * for every pixel of every listed block AND its 1-pixel ring clipped to the image (exactly the
- * pixels a 3x3 conv over the listed blocks reads); other pixels of `a` are untouched.
- * x, a: bf16 NHWC [N][h][w][c] device, a != x.  gamma, beta: fp32 [c] device.  eps >= 0. */
-SPHINX_API sphinx_status sphinx_gn_silu(const void* x, const float* stats, const float* gamma,
+ * with (mean_g, var_g) of every frame combined from ALL Hb*Wb block entries of `stats` (fp32;
+ * written to the buffer's frame entries), applied to every pixel of every listed block AND its
+ * 1-pixel ring clipped to the image (exactly the pixels a 3x3 conv over the listed blocks
+ * reads); other pixels of `a` are untouched.
+ * x, a: bf16 NHWC [N][h][w][c] device, a != x.  gamma, beta: fp32 [c] device, 16-byte aligned.
+ * eps >= 0. */
+SPHINX_API sphinx_status sphinx_gn_silu(const void* x, float* stats, const float* gamma,
                                         const float* beta, float eps, int32_t n, int32_t h, int32_t w,
                                         int32_t c, int32_t groups, int32_t block,
                                         const int32_t* block_ids, const int32_t* count,

@@ -315,10 +315,17 @@ def sphinx_uncertainty_map(rgb, uncertainty, tau_u, window=7, smooth=5, workspac
 
 
 def gn_stats_buffer(n, h, w, groups, block, device):
-    """A per-block GroupNorm statistics buffer (fp32 [N,Hb,Wb,G,2]) for NEXT-3; memory only."""
+    """A GroupNorm statistics buffer for NEXT-3 (flat fp32: block entries [N,Hb,Wb,G,2] then
+    frame entries [N,G,2]); memory only."""
     import torch
+    nbytes = int(load().sphinx_gn_stats_size(int(n), int(h), int(w), int(groups), int(block)))
+    return torch.zeros(nbytes // 4, dtype=torch.float32, device=device)
+
+
+def gn_block_entries(stats, n, h, w, groups, block):
+    """View of the per-block (mean, M2) entries of a statistics buffer: [N,Hb,Wb,G,2]."""
     hb, wb = -(-h // block), -(-w // block)
-    return torch.zeros((n, hb, wb, groups, 2), dtype=torch.float32, device=device)
+    return stats[: n * hb * wb * groups * 2].view(n, hb, wb, groups, 2)
 
 
 def sphinx_gn_block_stats(x, groups, block, block_ids, count, stats, capacity=None, stream=None):
@@ -330,7 +337,7 @@ def sphinx_gn_block_stats(x, groups, block, block_ids, count, stats, capacity=No
     _dev(count, torch.int32, "count")
     n, h, w, c = x.shape
     if stats.numel() * 4 != load().sphinx_gn_stats_size(n, h, w, int(groups), int(block)):
-        raise ValueError("stats: expected fp32 [N,Hb,Wb,groups,2]")
+        raise ValueError("stats: expected a gn_stats_buffer(...) of this geometry")
     cap = block_ids.numel() if capacity is None else capacity
     rc = load().sphinx_gn_block_stats(_ptr(x), n, h, w, c, int(groups), int(block), _ptr(block_ids),
                                       _ptr(count), int(cap), _ptr(stats), _stream(stream))

@@ -10,18 +10,18 @@
 // from all Hb*Wb entries of the frame (Chan's pairwise update, a few KB from L2).  Equal to the
 // full-map definition up to rounding.
 //
-//  gn_block_stats_kernel  one CTA per listed block: 16-byte loads (8 channels) per thread,
-//                         per-channel shifted sums (shift = the block's first pixel, so no
-//                         cancellation for |mean| >> std), per-channel (mean, M2), then
+// Stats buffer = [N][Hb][Wb][G] float2 block entries + [N][G] float2 frame entries (mean, rstd).
+// Work unit = (listed block, channel slice of whole groups); thread t owns one 16-byte vector
+// (8 channels) of the slice for the whole unit and walks pixel lanes, 4 loads in flight.
+//  gn_block_stats_kernel  per unit: per-channel shifted sums (shift = the block's first pixel,
+//                         so no cancellation for |mean| >> std) -> per-channel (mean, M2) ->
 //                         per-group Chan combination.  HBM-bound on the active bytes.
-//  gn_silu_kernel         contiguous chunk of the list per CTA (frames change rarely along the
-//                         ascending list): frame statistics -> per-channel (mean, gamma*rstd,
-//                         beta) in shared memory, then a = bf16(SiLU(gamma (x-mean) rstd +
-//                         beta)) for every pixel of the block AND its 1-pixel ring clipped to
-//                         the image: exactly the pixels a 3x3 conv over the listed blocks reads
-//                         (ring pixels of unlisted neighbours = normalised cached values with the
-//                         current statistics).  Two CTAs may write the same ring pixel: both
-//                         write identical bits (same inputs, same instruction sequence).
+//  gn_finalize_kernel     one warp per (frame, group): the frame's Hb*Wb entries -> (mean, rstd).
+//  gn_silu_kernel         per unit over the block AND its 1-pixel ring clipped to the image
+//                         (exactly the pixels a 3x3 conv over the listed blocks reads; ring pixels
+//                         of unlisted neighbours = normalised cached values with the current
+//                         statistics): a = bf16(SiLU((x - mean) gamma rstd + beta)).  Two units
+//                         may write the same ring pixel: identical bits (same inputs, same code).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -39,37 +39,61 @@ __device__ __forceinline__ void unpack8(const uint4 r, float (&f)[8]) {
   }
 }
 
+// Work unit = (listed block, channel slice).  A slice holds S channels, S | c and S a
+// multiple of lcm(c/G, 8), so it contains whole groups and whole 16-byte vectors; thread t
+// owns vector v = t % (S/8) of the slice for the whole unit and walks pixel lanes t / (S/8).
+struct GnGeom {
+  int h, w, c, G, b, hb, wb;
+  int S, V, R, nslice;  // slice channels, vectors per slice pixel, pixel lanes, slices per pixel
+};
+
 __global__ void __launch_bounds__(kGnThreads) gn_block_stats_kernel(
-    const __nv_bfloat16* __restrict__ x, int h, int w, int c, int G, int b, int hb, int wb,
-    const int32_t* __restrict__ ids, const int32_t* __restrict__ count, float2* stats) {
-  extern __shared__ float sm[];
-  const int V = c >> 3;               // 16-byte vectors per pixel
-  const int R = kGnThreads / V;       // pixel lanes
-  float* s1 = sm;                     // [R][c]
-  float* s2 = sm + R * c;             // [R][c]
-  float* cmean = sm + 2 * R * c;      // [c]
-  float* cm2 = cmean + c;             // [c]
+    const __nv_bfloat16* __restrict__ x, const GnGeom g, const int32_t* __restrict__ ids,
+    const int32_t* __restrict__ count, float2* stats) {
+  __shared__ float s1[2 * kGnThreads * 8];  // [R][S] shifted sums, then [R][S] squares
+  __shared__ float cmean[kGnThreads * 8], cm2[kGnThreads * 8];
   pdl_wait();
   pdl_trigger();
   const int cnt = *count;
-  const int t = threadIdx.x, v = t % V, r0 = t / V;
-  const int cg = c / G;
-  for (int j = blockIdx.x; j < cnt; j += gridDim.x) {
+  const int t = threadIdx.x, V = g.V, R = g.R, S = g.S;
+  const int v = t % V, r0 = t / V;
+  const int cg = g.c / g.G;
+  float* s2 = s1 + R * S;
+  const long long units = (long long)cnt * g.nslice;
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const int j = (int)(u / g.nslice), sl = (int)(u - (long long)j * g.nslice);
     const int id = __ldg(ids + j);
-    const int n = id / (hb * wb), rem = id - n * hb * wb;
-    const int by = rem / wb, bx = rem - by * wb;
-    const int rows = min(b, h - by * b), cols = min(b, w - bx * b), np = rows * cols;
-    const __nv_bfloat16* base = x + (((size_t)n * h + by * b) * w + bx * b) * c;
+    const int n = id / (g.hb * g.wb), rem = id - n * g.hb * g.wb;
+    const int by = rem / g.wb, bx = rem - by * g.wb;
+    const int rows = min(g.b, g.h - by * g.b), cols = min(g.b, g.w - bx * g.b), np = rows * cols;
+    const __nv_bfloat16* base = x + (((size_t)n * g.h + by * g.b) * g.w + bx * g.b) * g.c + sl * S;
     if (r0 < R) {
       float K[8], a1[8], a2[8];
       unpack8(__ldg(reinterpret_cast<const uint4*>(base) + v), K);
 #pragma unroll
       for (int i = 0; i < 8; ++i) a1[i] = a2[i] = 0.f;
-#pragma unroll 4
-      for (int p = r0; p < np; p += R) {
+      int p = r0;
+      // 4 independent 16-byte loads in flight per thread
+      for (; p + 3 * R < np; p += 4 * R) {
+        float f[4][8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int pp = p + q * R, py = pp / cols, px = pp - py * cols;
+          unpack8(__ldg(reinterpret_cast<const uint4*>(base + ((size_t)py * g.w + px) * g.c) + v), f[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float d = f[q][i] - K[i];
+            a1[i] += d;
+            a2[i] = fmaf(d, d, a2[i]);
+          }
+      }
+      for (; p < np; p += R) {
         const int py = p / cols, px = p - py * cols;
         float f[8];
-        unpack8(__ldg(reinterpret_cast<const uint4*>(base + ((size_t)py * w + px) * c) + v), f);
+        unpack8(__ldg(reinterpret_cast<const uint4*>(base + ((size_t)py * g.w + px) * g.c) + v), f);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float d = f[i] - K[i];
@@ -79,34 +103,34 @@ __global__ void __launch_bounds__(kGnThreads) gn_block_stats_kernel(
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        s1[r0 * c + v * 8 + i] = a1[i];
-        s2[r0 * c + v * 8 + i] = a2[i];
+        s1[r0 * S + v * 8 + i] = a1[i];
+        s2[r0 * S + v * 8 + i] = a2[i];
       }
     }
     __syncthreads();
     const float inv_np = 1.f / (float)np;
-    for (int ch = t; ch < c; ch += kGnThreads) {
-      float S1 = 0.f, S2 = 0.f;
+    for (int ch = t; ch < S; ch += kGnThreads) {
+      float A = 0.f, B2 = 0.f;
       for (int r = 0; r < R; ++r) {
-        S1 += s1[r * c + ch];
-        S2 += s2[r * c + ch];
+        A += s1[r * S + ch];
+        B2 += s2[r * S + ch];
       }
       const float K = __bfloat162float(base[ch]);
-      cmean[ch] = K + S1 * inv_np;
-      cm2[ch] = fmaxf(S2 - S1 * S1 * inv_np, 0.f);
+      cmean[ch] = K + A * inv_np;
+      cm2[ch] = fmaxf(B2 - A * A * inv_np, 0.f);
     }
     __syncthreads();
-    for (int g = t; g < G; g += kGnThreads) {
+    for (int q = t; q < S / cg; q += kGnThreads) {
       float m = 0.f;
-      for (int k = 0; k < cg; ++k) m += cmean[g * cg + k];
+      for (int k = 0; k < cg; ++k) m += cmean[q * cg + k];
       m /= (float)cg;
       float M2 = 0.f, dev = 0.f;
       for (int k = 0; k < cg; ++k) {
-        const float d = cmean[g * cg + k] - m;
-        M2 += cm2[g * cg + k];
+        const float d = cmean[q * cg + k] - m;
+        M2 += cm2[q * cg + k];
         dev = fmaf(d, d, dev);
       }
-      stats[(size_t)id * G + g] = make_float2(m, fmaf((float)np, dev, M2));
+      stats[(size_t)id * g.G + sl * (S / cg) + q] = make_float2(m, fmaf((float)np, dev, M2));
     }
     __syncthreads();
   }
@@ -114,113 +138,150 @@ __global__ void __launch_bounds__(kGnThreads) gn_block_stats_kernel(
 
 // Chan et al. pairwise update of (count, mean, M2).
 __device__ __forceinline__ void chan_merge(float& na, float& ma, float& qa, float nb, float mb, float qb) {
-  const float n = na + nb;
   if (nb == 0.f) return;
+  const float n = na + nb;
   const float d = mb - ma, f = nb / n;
   ma = fmaf(d, f, ma);
   qa = qa + qb + d * d * na * f;
   na = n;
 }
 
+// Frame statistics: one warp per (frame, group) combines the frame's Hb*Wb block entries
+// (lane-strided, then a fixed butterfly: deterministic, both partners hold identical bits) into
+// (mean, rstd) = (mean, 1/sqrt(M2/count + eps)) at fstats[n * G + g].
+__global__ void __launch_bounds__(kGnThreads) gn_finalize_kernel(const float2* __restrict__ stats,
+                                                                  float2* fstats, const GnGeom g,
+                                                                  int n_frames, float eps) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = (blockIdx.x * kGnThreads + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n_frames * g.G) return;
+  const int n = warp / g.G, gi = warp - n * g.G;
+  const int nblk = g.hb * g.wb, cg = g.c / g.G;
+  const int rb = g.h - (g.hb - 1) * g.b, cb = g.w - (g.wb - 1) * g.b;
+  float na = 0.f, ma = 0.f, qa = 0.f;
+  for (int i = lane; i < nblk; i += 32) {
+    const int iy = i / g.wb, ix = i - iy * g.wb;
+    const float npx = (float)((iy == g.hb - 1 ? rb : g.b) * (ix == g.wb - 1 ? cb : g.b) * cg);
+    const float2 st = __ldg(stats + ((size_t)n * nblk + i) * g.G + gi);
+    chan_merge(na, ma, qa, npx, st.x, st.y);
+  }
+  for (int o = 1; o < 32; o <<= 1) {
+    const float nb2 = __shfl_xor_sync(0xffffffffu, na, o);
+    const float mb2 = __shfl_xor_sync(0xffffffffu, ma, o);
+    const float qb2 = __shfl_xor_sync(0xffffffffu, qa, o);
+    if ((lane & o) == 0) {
+      chan_merge(na, ma, qa, nb2, mb2, qb2);
+    } else {
+      float nn = nb2, mm = mb2, qq = qb2;
+      chan_merge(nn, mm, qq, na, ma, qa);
+      na = nn; ma = mm; qa = qq;
+    }
+  }
+  if (lane == 0) fstats[warp] = make_float2(ma, 1.f / sqrtf(qa / na + eps));
+}
+
+// a = bf16(SiLU((x - mean_g) * gamma_c * rstd_g + beta_c)) over (listed block + 1-px ring,
+// channel slice) units; each thread's 8 channels' parameters live in registers for the unit.
 __global__ void __launch_bounds__(kGnThreads) gn_silu_kernel(
-    const __nv_bfloat16* __restrict__ x, const float2* __restrict__ stats,
-    const float* __restrict__ gamma, const float* __restrict__ beta, float eps, int h, int w,
-    int c, int G, int b, int hb, int wb, const int32_t* __restrict__ ids,
-    const int32_t* __restrict__ count, __nv_bfloat16* a) {
-  extern __shared__ float sm[];
-  float* s_mean = sm;          // [c] group mean per channel
-  float* s_scale = sm + c;     // [c] gamma * rstd
-  float* s_beta = sm + 2 * c;  // [c]
-  float* g_mean = sm + 3 * c;  // [G]
-  float* g_rstd = g_mean + G;  // [G]
+    const __nv_bfloat16* __restrict__ x, const float2* __restrict__ fstats,
+    const float* __restrict__ gamma, const float* __restrict__ beta, const GnGeom g,
+    const int32_t* __restrict__ ids, const int32_t* __restrict__ count, __nv_bfloat16* a) {
   pdl_wait();
   pdl_trigger();
   const int cnt = *count;
-  const int j0 = (int)((long long)blockIdx.x * cnt / gridDim.x);
-  const int j1 = (int)((long long)(blockIdx.x + 1) * cnt / gridDim.x);
-  const int t = threadIdx.x, V = c >> 3, cg = c / G;
-  // threads per group for the frame reduction: a power of two <= 32 dividing the warp
-  int tpg = 32;
-  while (tpg > 1 && tpg * G > kGnThreads) tpg >>= 1;
-  const int nblk = hb * wb;
-  const int rb = h - (hb - 1) * b, cb = w - (wb - 1) * b;  // rows / cols of edge blocks
-  int cur = -1;
-  for (int j = j0; j < j1; ++j) {
+  const int t = threadIdx.x, V = g.V, R = g.R, S = g.S;
+  const int v = t % V, r0 = t / V;
+  if (r0 >= R) return;
+  const int cg = g.c / g.G;
+  const long long units = (long long)cnt * g.nslice;
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const int j = (int)(u / g.nslice), sl = (int)(u - (long long)j * g.nslice);
     const int id = __ldg(ids + j);
-    const int n = id / nblk, rem = id - n * nblk;
-    const int by = rem / wb, bx = rem - by * wb;
-    if (n != cur) {
-      __syncthreads();  // previous frame's tables no longer read
-      for (int g0 = 0; g0 < G; g0 += kGnThreads / tpg) {
-        const int g = g0 + t / tpg, sub = t % tpg;
-        float na = 0.f, ma = 0.f, qa = 0.f;
-        if (g < G) {
-          for (int i = sub; i < nblk; i += tpg) {
-            const int iy = i / wb, ix = i - iy * wb;
-            const float npx = (float)((iy == hb - 1 ? rb : b) * (ix == wb - 1 ? cb : b) * cg);
-            const float2 st = __ldg(stats + ((size_t)n * nblk + i) * G + g);
-            chan_merge(na, ma, qa, npx, st.x, st.y);
-          }
-        }
-        // butterfly over the tpg lanes of the group (fixed order: deterministic)
-        for (int o = 1; o < tpg; o <<= 1) {
-          const float nb2 = __shfl_xor_sync(0xffffffffu, na, o);
-          const float mb2 = __shfl_xor_sync(0xffffffffu, ma, o);
-          const float qb2 = __shfl_xor_sync(0xffffffffu, qa, o);
-          // merge in a lane-independent order so both partners hold identical bits
-          if ((t & o) == 0) {
-            chan_merge(na, ma, qa, nb2, mb2, qb2);
-          } else {
-            float nn = nb2, mm = mb2, qq = qb2;
-            chan_merge(nn, mm, qq, na, ma, qa);
-            na = nn; ma = mm; qa = qq;
-          }
-        }
-        if (g < G && sub == 0) {
-          g_mean[g] = ma;
-          g_rstd[g] = 1.f / sqrtf(qa / na + eps);
-        }
+    const int n = id / (g.hb * g.wb), rem = id - n * g.hb * g.wb;
+    const int by = rem / g.wb, bx = rem - by * g.wb;
+    const int c0 = sl * S + v * 8;
+    float mu[8], sc[8], be[8];
+    {
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c0));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c0 + 4));
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + c0));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + c0 + 4));
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 fs = __ldg(fstats + (size_t)n * g.G + (c0 + i) / cg);
+        mu[i] = fs.x;
+        sc[i] = gg[i] * fs.y;
+        be[i] = bb[i];
       }
-      __syncthreads();
-      for (int ch = t; ch < c; ch += kGnThreads) {
-        const int g = ch / cg;
-        s_mean[ch] = g_mean[g];
-        s_scale[ch] = __ldg(gamma + ch) * g_rstd[g];
-        s_beta[ch] = __ldg(beta + ch);
-      }
-      __syncthreads();
-      cur = n;
     }
-    const int y0 = max(by * b - 1, 0), y1 = min(by * b + b + 1, h);
-    const int x0 = max(bx * b - 1, 0), x1 = min(bx * b + b + 1, w);
-    const int rw = x1 - x0, total = (y1 - y0) * rw * V;
-    for (int e = t; e < total; e += kGnThreads) {
-      const int p = e / V, vv = e - p * V;
-      const int yy = y0 + p / rw, xx = x0 + p % rw;
-      const size_t off = (((size_t)n * h + yy) * w + xx) * c + vv * 8;
+    const int y0 = max(by * g.b - 1, 0), y1 = min(by * g.b + g.b + 1, g.h);
+    const int x0 = max(bx * g.b - 1, 0), x1 = min(bx * g.b + g.b + 1, g.w);
+    const int rw = x1 - x0, np = (y1 - y0) * rw;
+    const size_t base = (((size_t)n * g.h + y0) * g.w + x0) * g.c + c0;
+    auto apply = [&](const uint4 r, size_t off) {
       float f[8];
-      unpack8(__ldg(reinterpret_cast<const uint4*>(x + off)), f);
+      unpack8(r, f);
       uint32_t o4[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         float r2[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int ch = vv * 8 + 2 * k + q;
-          const float tt = fmaf(f[2 * k + q] - s_mean[ch], s_scale[ch], s_beta[ch]);
+          const int i = 2 * k + q;
+          const float tt = fmaf(f[i] - mu[i], sc[i], be[i]);
           r2[q] = tt / (1.f + expf(-tt));
         }
         const __nv_bfloat162 pk = __floats2bfloat162_rn(r2[0], r2[1]);
         o4[k] = *reinterpret_cast<const uint32_t*>(&pk);
       }
       *reinterpret_cast<uint4*>(a + off) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    };
+    int p = r0;
+    for (; p + 3 * R < np; p += 4 * R) {
+      uint4 r[4];
+      size_t off[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pp = p + q * R, py = pp / rw, px = pp - py * rw;
+        off[q] = base + ((size_t)py * g.w + px) * g.c;
+        r[q] = __ldg(reinterpret_cast<const uint4*>(x + off[q]));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) apply(r[q], off[q]);
+    }
+    for (; p < np; p += R) {
+      const int py = p / rw, px = p - py * rw;
+      const size_t off = base + ((size_t)py * g.w + px) * g.c;
+      apply(__ldg(reinterpret_cast<const uint4*>(x + off)), off);
     }
   }
 }
 
-static int gn_grid(int capacity, int sms) {
-  const int cap = sms * 8;
-  return capacity < cap ? (capacity > 0 ? capacity : 1) : cap;
+static int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
+
+// Slice: the largest S | c, S a multiple of lcm(c/G, 8), with S/8 <= 64 vectors (>= 4 pixel
+// lanes per CTA); else the smallest such S (S/8 <= 256 guaranteed by the host checks).
+static GnGeom gn_geom(int h, int w, int c, int G, int b) {
+  GnGeom g;
+  g.h = h; g.w = w; g.c = c; g.G = G; g.b = b;
+  g.hb = cdiv(h, b); g.wb = cdiv(w, b);
+  const int cg = c / G, L = cg / gcd_i(cg, 8) * 8;
+  int best = 0;
+  for (int S = L; S <= c; S += L)
+    if (c % S == 0 && S / 8 <= 64) best = S;
+  g.S = best ? best : L;
+  g.V = g.S / 8;
+  g.R = kGnThreads / g.V;
+  g.nslice = c / g.S;
+  return g;
+}
+
+static int gn_grid(long long units, int sms) {
+  const long long cap = (long long)sms * 8;
+  return (int)(units < cap ? (units > 0 ? units : 1) : cap);
 }
 
 }  // namespace sphinx
@@ -235,15 +296,21 @@ static sphinx_status gn_check(const void* x, int32_t n, int32_t h, int32_t w, in
     return SPHINX_ERR_INVALID_ARGUMENT;
   if (c % groups) return SPHINX_ERR_INVALID_ARGUMENT;
   if ((int64_t)capacity > (int64_t)n * cdiv(h, block) * cdiv(w, block)) return SPHINX_ERR_INVALID_ARGUMENT;
-  if (c % 8 || c > 8 * kGnThreads || groups > kGnThreads || block > 64) return SPHINX_ERR_UNSUPPORTED;
+  if (c % 8 || block > 64) return SPHINX_ERR_UNSUPPORTED;
+  const int cg = c / groups;
+  if (cg / gcd_i(cg, 8) * 8 > 8 * kGnThreads) return SPHINX_ERR_UNSUPPORTED;  // slice > 256 vectors
   if (!aligned16(x)) return SPHINX_ERR_UNSUPPORTED;
   return SPHINX_OK;
+}
+
+static size_t gn_block_bytes(int32_t n, int32_t h, int32_t w, int32_t groups, int32_t block) {
+  return (size_t)n * cdiv(h, block) * cdiv(w, block) * groups * sizeof(float2);
 }
 
 extern "C" size_t sphinx_gn_stats_size(int32_t n, int32_t h, int32_t w, int32_t groups,
                                        int32_t block) {
   if (n <= 0 || h <= 0 || w <= 0 || groups <= 0 || block <= 0) return 0;
-  return (size_t)n * cdiv(h, block) * cdiv(w, block) * groups * sizeof(float2);
+  return gn_block_bytes(n, h, w, groups, block) + (size_t)n * groups * sizeof(float2);
 }
 
 extern "C" sphinx_status sphinx_gn_block_stats(const void* x, int32_t n, int32_t h, int32_t w,
@@ -257,18 +324,16 @@ extern "C" sphinx_status sphinx_gn_block_stats(const void* x, int32_t n, int32_t
   int sms = 0;
   if ((st = check_device(&sms)) != SPHINX_OK) return st;
   if (capacity == 0) return SPHINX_OK;
-  const int V = c / 8, R = kGnThreads / V;
-  const size_t smem = (size_t)(2 * R * c + 2 * c) * sizeof(float);
-  cudaError_t e = launch_k(gn_block_stats_kernel, dim3(gn_grid(capacity, sms)), dim3(kGnThreads), smem,
-                           reinterpret_cast<cudaStream_t>(stream),
-                           static_cast<const __nv_bfloat16*>(x), (int)h, (int)w, (int)c, (int)groups,
-                           (int)block, cdiv(h, block), cdiv(w, block), block_ids, count,
+  const GnGeom g = gn_geom(h, w, c, groups, block);
+  cudaError_t e = launch_k(gn_block_stats_kernel, dim3(gn_grid((long long)capacity * g.nslice, sms)),
+                           dim3(kGnThreads), 0, reinterpret_cast<cudaStream_t>(stream),
+                           static_cast<const __nv_bfloat16*>(x), g, block_ids, count,
                            reinterpret_cast<float2*>(stats));
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }
 
-extern "C" sphinx_status sphinx_gn_silu(const void* x, const float* stats, const float* gamma,
+extern "C" sphinx_status sphinx_gn_silu(const void* x, float* stats, const float* gamma,
                                         const float* beta, float eps, int32_t n, int32_t h,
                                         int32_t w, int32_t c, int32_t groups, int32_t block,
                                         const int32_t* block_ids, const int32_t* count,
@@ -276,17 +341,23 @@ extern "C" sphinx_status sphinx_gn_silu(const void* x, const float* stats, const
   sphinx_status st = gn_check(x, n, h, w, c, groups, block, block_ids, count, capacity);
   if (st != SPHINX_OK) return st;
   if (!stats || !gamma || !beta || !a || a == x || !(eps >= 0.f)) return SPHINX_ERR_INVALID_ARGUMENT;
-  if (!aligned16(a)) return SPHINX_ERR_UNSUPPORTED;
+  if (!aligned16(a) || !aligned16(gamma) || !aligned16(beta) ||
+      (reinterpret_cast<uintptr_t>(stats) & 7u))
+    return SPHINX_ERR_UNSUPPORTED;
   int sms = 0;
   if ((st = check_device(&sms)) != SPHINX_OK) return st;
   if (capacity == 0) return SPHINX_OK;
-  const size_t smem = (size_t)(3 * c + 2 * groups) * sizeof(float);
-  cudaError_t e = launch_k(gn_silu_kernel, dim3(gn_grid(capacity, sms)), dim3(kGnThreads), smem,
-                           reinterpret_cast<cudaStream_t>(stream),
-                           static_cast<const __nv_bfloat16*>(x), reinterpret_cast<const float2*>(stats),
-                           gamma, beta, eps, (int)h, (int)w, (int)c, (int)groups, (int)block,
-                           cdiv(h, block), cdiv(w, block), block_ids, count,
-                           static_cast<__nv_bfloat16*>(a));
+  const GnGeom g = gn_geom(h, w, c, groups, block);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const float2* blk = reinterpret_cast<const float2*>(stats);
+  float2* fst = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(stats) + gn_block_bytes(n, h, w, groups, block));
+  const int warps = n * groups;
+  cudaError_t e = launch_k(gn_finalize_kernel, dim3(cdiv(warps, kGnThreads / 32)), dim3(kGnThreads), 0, s,
+                           blk, fst, g, (int)n, eps);
+  if (e != cudaSuccess) return cuda_fail(e);
+  e = launch_k(gn_silu_kernel, dim3(gn_grid((long long)capacity * g.nslice, sms)), dim3(kGnThreads), 0, s,
+               static_cast<const __nv_bfloat16*>(x), static_cast<const float2*>(fst), gamma, beta, g,
+               block_ids, count, static_cast<__nv_bfloat16*>(a));
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }

@@ -61,7 +61,7 @@ def test_next3_host_validation():
     assert lib.sphinx_gn_block_stats(p, 1, 16, 16, 36, 4, 8, p, p, 4, p, null) == sp.ERR_UNSUPPORTED
     assert lib.sphinx_gn_silu(p, p, p, p, 1e-6, 1, 16, 16, 32, 8, 8, p, p, 4, p, null) == \
         sp.ERR_INVALID_ARGUMENT  # a aliases x
-    assert lib.sphinx_gn_stats_size(2, 18, 18, 32, 8) == 2 * 9 * 32 * 8
+    assert lib.sphinx_gn_stats_size(2, 18, 18, 32, 8) == 2 * 9 * 32 * 8 + 2 * 32 * 8
     assert lib.sphinx_sparse_conv3x3_residual(p, p, null, null, p, sp.F32, 1, 16, 16, 32, 32, 8, p, p,
                                               4, null, 0, null) == sp.ERR_INVALID_ARGUMENT
     q = ctypes.c_void_p(2048)

@@ -127,14 +127,14 @@ def test_gn_silu_vs_oracle_incremental_stats(sphinx, n, h, w, c, b, groups, dens
     stats = sphinx.gn_stats_buffer(n, h, w, groups, b, dev)
     all_ids, all_cnt = gpu_ids(sphinx, np.ones_like(mask))
     sphinx.sphinx_gn_block_stats(bf16(x_old), groups, b, all_ids, all_cnt, stats)
-    before = stats.cpu().numpy().copy()
+    before = sphinx.gn_block_entries(stats, n, h, w, groups, b).cpu().numpy().copy()
     ids, cnt = gpu_ids(sphinx, mask)
     xg = bf16(x_new)
     sphinx.sphinx_gn_block_stats(xg, groups, b, ids, cnt, stats)
     a = torch.full((n, h, w, c), 77.0, dtype=torch.bfloat16, device=dev)
     sphinx.sphinx_gn_silu(xg, stats, T(g1), T(be1), EPS, groups, b, ids, cnt, a)
     torch.cuda.synchronize()
-    after = stats.cpu().numpy()
+    after = sphinx.gn_block_entries(stats, n, h, w, groups, b).cpu().numpy()
     assert np.array_equal(after[mask == 0], before[mask == 0])   # unlisted entries untouched
     xd = dec(x_new)
     t, a_ref = oracle.gn_silu(xd, groups, g1, be1, EPS)
@@ -310,7 +310,7 @@ def test_resblock_vs_oracle(sphinx, n, h, w, c, b, groups, dens, pattern, shift)
     params = _params(c, tag, shift)
     rb = RB(sphinx, n, h, w, c, b, groups, h_cache, y_cache)
     _stats_init(sphinx, rb, x, h_cache, mask)
-    hs_before = rb.hs.cpu().numpy().copy()
+    hs_before = sphinx.gn_block_entries(rb.hs, n, h, w, groups, b).cpu().numpy().copy()
     ids, cnt = gpu_ids(sphinx, mask)
     rb.run(x, params, ids, cnt)
     torch.cuda.synchronize()
@@ -321,7 +321,8 @@ def test_resblock_vs_oracle(sphinx, n, h, w, c, b, groups, dens, pattern, shift)
     # unlisted pixels and statistics entries: untouched, bitwise
     assert np.array_equal(h_got[~L], h_cache[~L])
     assert np.array_equal(y_got[~L], y_cache[~L].astype(np.float32).astype(np.float64))
-    assert np.array_equal(rb.hs.cpu().numpy()[mask == 0], hs_before[mask == 0])
+    hs_after = sphinx.gn_block_entries(rb.hs, n, h, w, groups, b).cpu().numpy()
+    assert np.array_equal(hs_after[mask == 0], hs_before[mask == 0])
     # h on listed pixels: conv1 bound (shift: exact copy of a1 up to its rounding)
     h_tol = _h_tol(o, x, params, groups, shift)
     herr = np.abs(dec(h_got) - o["h_pre"])
