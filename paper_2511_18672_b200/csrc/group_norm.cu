@@ -45,9 +45,10 @@ __device__ __forceinline__ void unpack8(const uint4 r, float (&f)[8]) {
 struct GnGeom {
   int h, w, c, G, b, hb, wb;
   int S, V, R, nslice;  // slice channels, vectors per slice pixel, pixel lanes, slices per pixel
+  int rg, nrg;          // gn_silu: ring rows per unit, units per (block, slice)
 };
 
-__global__ void __launch_bounds__(kGnThreads) gn_block_stats_kernel(
+__global__ void __launch_bounds__(kGnThreads, 4) gn_block_stats_kernel(
     const __nv_bfloat16* __restrict__ x, const GnGeom g, const int32_t* __restrict__ ids,
     const int32_t* __restrict__ count, float2* stats) {
   __shared__ float s1[2 * kGnThreads * 8];  // [R][S] shifted sums, then [R][S] squares
@@ -72,33 +73,30 @@ __global__ void __launch_bounds__(kGnThreads) gn_block_stats_kernel(
       unpack8(__ldg(reinterpret_cast<const uint4*>(base) + v), K);
 #pragma unroll
       for (int i = 0; i < 8; ++i) a1[i] = a2[i] = 0.f;
-      int p = r0;
-      // 4 independent 16-byte loads in flight per thread
-      for (; p + 3 * R < np; p += 4 * R) {
-        float f[4][8];
+      const float inv_cols = 1.f / (float)cols;  // exact floor((pp + 0.5) / cols) for pp < 2^20
+      const uint32_t row_stride = (uint32_t)g.w * g.c;
+      // 4 independent (predicated) 16-byte loads in flight per thread
+      for (int p0 = r0; p0 < np; p0 += 4 * R) {
+        uint4 raw[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int pp = p + q * R, py = pp / cols, px = pp - py * cols;
-          unpack8(__ldg(reinterpret_cast<const uint4*>(base + ((size_t)py * g.w + px) * g.c) + v), f[q]);
+          const int pp = p0 + q * R;
+          const int py = __float2int_rz(((float)pp + 0.5f) * inv_cols), px = pp - py * cols;
+          if (pp < np)
+            raw[q] = __ldg(reinterpret_cast<const uint4*>(base + (uint32_t)py * row_stride + (uint32_t)px * g.c) + v);
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q) {
+          if (p0 + q * R < np) {
+            float f[8];
+            unpack8(raw[q], f);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float d = f[q][i] - K[i];
-            a1[i] += d;
-            a2[i] = fmaf(d, d, a2[i]);
+            for (int i = 0; i < 8; ++i) {
+              const float d = f[i] - K[i];
+              a1[i] += d;
+              a2[i] = fmaf(d, d, a2[i]);
+            }
           }
-      }
-      for (; p < np; p += R) {
-        const int py = p / cols, px = p - py * cols;
-        float f[8];
-        unpack8(__ldg(reinterpret_cast<const uint4*>(base + ((size_t)py * g.w + px) * g.c) + v), f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float d = f[i] - K[i];
-          a1[i] += d;
-          a2[i] = fmaf(d, d, a2[i]);
         }
       }
 #pragma unroll
@@ -182,8 +180,11 @@ __global__ void __launch_bounds__(kGnThreads) gn_finalize_kernel(const float2* _
 }
 
 // a = bf16(SiLU((x - mean_g) * gamma_c * rstd_g + beta_c)) over (listed block + 1-px ring,
-// channel slice) units; each thread's 8 channels' parameters live in registers for the unit.
-__global__ void __launch_bounds__(kGnThreads) gn_silu_kernel(
+// channel slice, group of ring rows) units: each thread's 8 channels' parameters are loaded
+// once per unit into registers, then up to 8 predicated 16-byte loads are in flight.
+// (Measured: a flat one-vector-per-thread variant is 1.4-2x slower here: per-element
+// parameter loads and empty CTAs past the device count.)
+__global__ void __launch_bounds__(kGnThreads, 2) gn_silu_kernel(
     const __nv_bfloat16* __restrict__ x, const float2* __restrict__ fstats,
     const float* __restrict__ gamma, const float* __restrict__ beta, const GnGeom g,
     const int32_t* __restrict__ ids, const int32_t* __restrict__ count, __nv_bfloat16* a) {
@@ -194,9 +195,11 @@ __global__ void __launch_bounds__(kGnThreads) gn_silu_kernel(
   const int v = t % V, r0 = t / V;
   if (r0 >= R) return;
   const int cg = g.c / g.G;
-  const long long units = (long long)cnt * g.nslice;
+  const int per_blk = g.nslice * g.nrg;
+  const long long units = (long long)cnt * per_blk;
   for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-    const int j = (int)(u / g.nslice), sl = (int)(u - (long long)j * g.nslice);
+    const int j = (int)(u / per_blk), r = (int)(u - (long long)j * per_blk);
+    const int sl = r / g.nrg, rgi = r - sl * g.nrg;
     const int id = __ldg(ids + j);
     const int n = id / (g.hb * g.wb), rem = id - n * g.hb * g.wb;
     const int by = rem / g.wb, bx = rem - by * g.wb;
@@ -209,53 +212,61 @@ __global__ void __launch_bounds__(kGnThreads) gn_silu_kernel(
       const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + c0 + 4));
       const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
       const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const int q0 = c0 / cg, rq = c0 - q0 * cg;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float2 fs = __ldg(fstats + (size_t)n * g.G + (c0 + i) / cg);
+        int gi = q0, rr = rq + i;
+        while (rr >= cg) {
+          rr -= cg;
+          ++gi;
+        }
+        const float2 fs = __ldg(fstats + (size_t)n * g.G + gi);
         mu[i] = fs.x;
         sc[i] = gg[i] * fs.y;
         be[i] = bb[i];
       }
     }
-    const int y0 = max(by * g.b - 1, 0), y1 = min(by * g.b + g.b + 1, g.h);
+    // this unit's ring rows: [by*b - 1 + rgi*rg, ... + rg) clipped to the image
+    const int ya = by * g.b - 1 + rgi * g.rg;
+    const int y0 = max(ya, 0), y1 = min(min(ya + g.rg, by * g.b + g.b + 1), g.h);
+    if (y0 >= y1) continue;
     const int x0 = max(bx * g.b - 1, 0), x1 = min(bx * g.b + g.b + 1, g.w);
     const int rw = x1 - x0, np = (y1 - y0) * rw;
-    const size_t base = (((size_t)n * g.h + y0) * g.w + x0) * g.c + c0;
-    auto apply = [&](const uint4 r, size_t off) {
-      float f[8];
-      unpack8(r, f);
-      uint32_t o4[4];
+    const __nv_bfloat16* xb = x + (((size_t)n * g.h + y0) * g.w + x0) * g.c + c0;
+    __nv_bfloat16* ab = a + (((size_t)n * g.h + y0) * g.w + x0) * g.c + c0;
+    const float inv_rw = 1.f / (float)rw;  // exact floor((pp + 0.5) / rw) for pp < 2^20
+    const uint32_t row_stride = (uint32_t)g.w * g.c;
+    for (int p0 = r0; p0 < np; p0 += 8 * R) {
+      uint4 raw[8];
+      uint32_t off[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float r2[2];
+      for (int q = 0; q < 8; ++q) {
+        const int pp = p0 + q * R;
+        const int py = __float2int_rz(((float)pp + 0.5f) * inv_rw), px = pp - py * rw;
+        off[q] = (uint32_t)py * row_stride + (uint32_t)px * g.c;
+        if (pp < np) raw[q] = __ldg(reinterpret_cast<const uint4*>(xb + off[q]));
+      }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int i = 2 * k + q;
-          const float tt = fmaf(f[i] - mu[i], sc[i], be[i]);
-          r2[q] = tt / (1.f + expf(-tt));
+      for (int q = 0; q < 8; ++q) {
+        if (p0 + q * R >= np) continue;
+        float f[8];
+        unpack8(raw[q], f);
+        uint32_t o4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float r2[2];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int i = 2 * k + h2;
+            const float tt = fmaf(f[i] - mu[i], sc[i], be[i]);
+            // SiLU with the SFU exponential: relative error ~1e-6 (inside the bar of R-27)
+            r2[h2] = __fdividef(tt, 1.f + __expf(-tt));
+          }
+          const __nv_bfloat162 pk = __floats2bfloat162_rn(r2[0], r2[1]);
+          o4[k] = *reinterpret_cast<const uint32_t*>(&pk);
         }
-        const __nv_bfloat162 pk = __floats2bfloat162_rn(r2[0], r2[1]);
-        o4[k] = *reinterpret_cast<const uint32_t*>(&pk);
+        *reinterpret_cast<uint4*>(ab + off[q]) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
       }
-      *reinterpret_cast<uint4*>(a + off) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
-    };
-    int p = r0;
-    for (; p + 3 * R < np; p += 4 * R) {
-      uint4 r[4];
-      size_t off[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int pp = p + q * R, py = pp / rw, px = pp - py * rw;
-        off[q] = base + ((size_t)py * g.w + px) * g.c;
-        r[q] = __ldg(reinterpret_cast<const uint4*>(x + off[q]));
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) apply(r[q], off[q]);
-    }
-    for (; p < np; p += R) {
-      const int py = p / rw, px = p - py * rw;
-      const size_t off = base + ((size_t)py * g.w + px) * g.c;
-      apply(__ldg(reinterpret_cast<const uint4*>(x + off)), off);
     }
   }
 }
@@ -276,6 +287,9 @@ static GnGeom gn_geom(int h, int w, int c, int G, int b) {
   g.V = g.S / 8;
   g.R = kGnThreads / g.V;
   g.nslice = c / g.S;
+  // ring rows per gn_silu unit: about 8 16-byte loads per thread in one batch
+  g.rg = max(1, min(b + 2, (8 * g.R) / (b + 2)));
+  g.nrg = cdiv(b + 2, g.rg);
   return g;
 }
 
@@ -355,7 +369,7 @@ extern "C" sphinx_status sphinx_gn_silu(const void* x, float* stats, const float
   cudaError_t e = launch_k(gn_finalize_kernel, dim3(cdiv(warps, kGnThreads / 32)), dim3(kGnThreads), 0, s,
                            blk, fst, g, (int)n, eps);
   if (e != cudaSuccess) return cuda_fail(e);
-  e = launch_k(gn_silu_kernel, dim3(gn_grid((long long)capacity * g.nslice, sms)), dim3(kGnThreads), 0, s,
+  e = launch_k(gn_silu_kernel, dim3(gn_grid((long long)capacity * g.nslice * g.nrg, sms)), dim3(kGnThreads), 0, s,
                static_cast<const __nv_bfloat16*>(x), static_cast<const float2*>(fst), gamma, beta, g,
                block_ids, count, static_cast<__nv_bfloat16*>(a));
   if (e != cudaSuccess) return cuda_fail(e);
