@@ -24,6 +24,10 @@ Parity status per function:
   bf16_rne / gn_stats / gn_silu / resblock          pinned (torch RNE float->bfloat16 incl. ties,
     (NEXT-3)                                        torch fp64 group_norm/silu/conv2d dense
                                                     formulation, density 0, cache consistency)
+  temporal_attn (NEXT-4)                            pinned (T=1 closed form o = v, torch fp64
+                                                    linear + scaled_dot_product_attention,
+                                                    frame-permutation equivariance, uniform keys,
+                                                    cache consistency, stale-cache locality)
 """
 import ctypes
 import os
@@ -98,6 +102,8 @@ def load():
             "oracle_gn_silu": [P, I, I, I, I, I, P, P, P, P, D, P, P],
             "oracle_resblock": [P, P, P, P, P, P, P, P, P, P, P, I, D, I, I, I, I, I, P, I,
                                 P, P, P, P, P, P, P, P, P, I],
+            "oracle_temporal_attn": [P, P, P, P, P, P, P, I, I, I, I, I, I, I, P, I,
+                                     P, P, P, P, P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(_lib, name)
@@ -373,4 +379,22 @@ def resblock(x_bits, h_cache_bits, y_cache, w1_bits, b1, w2_bits, b2, g1, be1, g
                                _p(o["a1_pre"]), _p(o["a1"]), _p(o["h_pre"]), _p(o["h_abs"]),
                                _p(o["h"]), _p(o["a2_pre"]), _p(o["a2"]), _p(o["y"]),
                                _p(o["y_abs"]), n_threads), "resblock")
+    return o
+
+
+def temporal_attn(x_bits, qkv_cache_bits, y_cache, wqkv_bits, bqkv, wo_bits, bo, heads, T, b, ids):
+    """NEXT-4 frame-sparse temporal attention with the K/V cache (R-28).  Returns a dict:
+    qkv_pre, qkv (bits), qkv_abs, o_pre, o (bits), y, y_abs (see sphinx_oracle.c)."""
+    lib = load()
+    x = _c(x_bits, np.uint16); qc = _c(qkv_cache_bits, np.uint16); yc = _c(y_cache, np.float64)
+    wq = _c(wqkv_bits, np.uint16); wo = _c(wo_bits, np.uint16)
+    bq = _c(bqkv, np.float32); bo = _c(bo, np.float32); ids = _c(ids, np.int32)
+    n, h, w, c = x.shape
+    o = {"qkv_pre": np.zeros((n, h, w, 3 * c)), "qkv": np.zeros((n, h, w, 3 * c), np.uint16),
+         "qkv_abs": np.zeros((n, h, w, 3 * c)), "o_pre": np.zeros(x.shape),
+         "o": np.zeros(x.shape, np.uint16), "y": np.zeros(x.shape), "y_abs": np.zeros(x.shape)}
+    _check(lib.oracle_temporal_attn(_p(x), _p(qc), _p(yc), _p(wq), _p(bq), _p(wo), _p(bo), n, h, w, c,
+                                    int(heads), int(T), int(b), _p(ids), len(ids), _p(o["qkv_pre"]),
+                                    _p(o["qkv"]), _p(o["qkv_abs"]), _p(o["o_pre"]), _p(o["o"]),
+                                    _p(o["y"]), _p(o["y_abs"])), "temporal_attn")
     return o

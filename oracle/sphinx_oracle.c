@@ -719,3 +719,129 @@ done:
   free(hb16); free(hd);
   return rc;
 }
+
+/* ------------------------------------------------------------- NEXT-4 ---- */
+
+/* NEXT-4. Frame-sparse temporal attention with the latent cache ("every T steps, the
+ * model performs a full denoising pass ... the intermediate latent representations from each
+ * temporal attention layer are cached.  In the subsequent (T-1) partial denoising steps,
+ * frames that are not actively refined simply retrieve and reuse these cached latents";
+ * reading R-28).  Per pixel p, the frames of a sequence (T consecutive frames) are the tokens:
+ *   qkv = listed ? bf16(Wqkv x + bqkv) : qkv_cache                   (K/V cache of every frame)
+ *   o[n,p] = softmax_m(q_n . k_m / sqrt(d)) v_m, m over n's sequence, per head of d = c/heads
+ *   y = listed ? x + Wo bf16(o) + bo : y_cache                       (identity residual)
+ * x: bf16 bits [n][h][w][c]; qkv_cache: bf16 bits [n][h][w][3c] (q | k | v, head-major);
+ * wqkv: bf16 bits [3c][c]; wo: bf16 bits [c][c]; bqkv [3c], bo [c] fp32 or NULL.
+ * Outputs (every pixel): qkv_pre (listed: fp64 projection, else decoded cache), qkv_out
+ * (bits), qkv_abs (sum |w x| + |b| at listed, else 0), o_pre / o_out (listed only, else 0),
+ * y, y_abs (|x| + |bo| + sum |wo o| at listed, else 0).  Outputs other than y may be NULL. */
+int oracle_temporal_attn(const uint16_t* x, const uint16_t* qkv_cache, const double* y_cache,
+                         const uint16_t* wqkv, const float* bqkv, const uint16_t* wo,
+                         const float* bo, int n, int h, int w, int c, int heads, int T, int b,
+                         const int32_t* ids, int count, double* qkv_pre, uint16_t* qkv_out,
+                         double* qkv_abs, double* o_pre, uint16_t* o_out, double* y, double* y_abs) {
+  if (!x || !qkv_cache || !y_cache || !wqkv || !wo || !y) return BAD;
+  if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || b <= 0 || heads <= 0 || c % heads != 0 || T <= 0 ||
+      n % T != 0)
+    return BAD;
+  if (count < 0 || (count > 0 && !ids)) return BAD;
+  int hb = (h + b - 1) / b, wb = (w + b - 1) / b;
+  for (int j = 0; j < count; ++j)
+    if (ids[j] < 0 || ids[j] >= n * hb * wb) return BAD;
+  int c3 = 3 * c, d = c / heads;
+  size_t npx = (size_t)n * h * w, plane = (size_t)h * w;
+  uint8_t* listed = (uint8_t*)calloc(npx, 1);
+  double* xd = widen(x, npx * c);
+  double* wq = widen(wqkv, (size_t)c3 * c);
+  double* wd = widen(wo, (size_t)c * c);
+  uint16_t* qb = (uint16_t*)malloc(npx * c3 * sizeof(uint16_t));
+  double* qv = (double*)malloc(npx * c3 * sizeof(double));
+  uint16_t* ob = (uint16_t*)calloc(npx * c, sizeof(uint16_t));
+  double* sc = (double*)malloc((size_t)T * sizeof(double));
+  int rc = 0;
+  if (!listed || !xd || !wq || !wd || !qb || !qv || !ob || !sc) { rc = -2; goto done4; }
+  for (int j = 0; j < count; ++j) {
+    int id = ids[j];
+    int i = id / (hb * wb), by = (id / wb) % hb, bx = id % wb;
+    for (int yy = by * b; yy < by * b + b && yy < h; ++yy)
+      for (int xx = bx * b; xx < bx * b + b && xx < w; ++xx) listed[((size_t)i * h + yy) * w + xx] = 1;
+  }
+  /* 1. projections of the listed (frame, pixel) tokens; cached K/V (and Q) elsewhere */
+  for (size_t p = 0; p < npx; ++p)
+    for (int j = 0; j < c3; ++j) {
+      size_t e = p * c3 + j;
+      if (listed[p]) {
+        double acc = bqkv ? (double)bqkv[j] : 0.0, aab = bqkv ? fabs((double)bqkv[j]) : 0.0;
+        for (int ci = 0; ci < c; ++ci) {
+          double pr = wq[(size_t)j * c + ci] * xd[p * c + ci];
+          acc += pr;
+          aab += fabs(pr);
+        }
+        if (qkv_pre) qkv_pre[e] = acc;
+        if (qkv_abs) qkv_abs[e] = aab;
+        qb[e] = oracle_bf16_rne(acc);
+      } else {
+        qb[e] = qkv_cache[e];
+        if (qkv_pre) qkv_pre[e] = bf16_to_double(qkv_cache[e]);
+        if (qkv_abs) qkv_abs[e] = 0.0;
+      }
+      qv[e] = bf16_to_double(qb[e]);
+    }
+  if (qkv_out) memcpy(qkv_out, qb, npx * c3 * sizeof(uint16_t));
+  /* 2. attention over the frames of the sequence at the same pixel, listed queries only */
+  double inv = 1.0 / sqrt((double)d);
+  for (int i = 0; i < n; ++i)
+    for (size_t p = 0; p < plane; ++p) {
+      size_t pi = (size_t)i * plane + p;
+      for (int hd = 0; hd < heads; ++hd)
+        for (int k = 0; k < d; ++k) {
+          size_t eo = pi * c + hd * d + k;
+          if (o_pre) o_pre[eo] = 0.0;
+        }
+      if (!listed[pi]) continue;
+      int s0 = (i / T) * T;
+      for (int hd = 0; hd < heads; ++hd) {
+        const double* q = qv + pi * c3 + hd * d;
+        double mx = -INFINITY;
+        for (int m = 0; m < T; ++m) {
+          const double* kk = qv + ((size_t)(s0 + m) * plane + p) * c3 + c + hd * d;
+          double s = 0.0;
+          for (int k = 0; k < d; ++k) s += q[k] * kk[k];
+          sc[m] = s * inv;
+          if (sc[m] > mx) mx = sc[m];
+        }
+        double den = 0.0;
+        for (int m = 0; m < T; ++m) { sc[m] = exp(sc[m] - mx); den += sc[m]; }
+        for (int k = 0; k < d; ++k) {
+          double o = 0.0;
+          for (int m = 0; m < T; ++m)
+            o += sc[m] / den * qv[((size_t)(s0 + m) * plane + p) * c3 + 2 * c + hd * d + k];
+          size_t eo = pi * c + hd * d + k;
+          if (o_pre) o_pre[eo] = o;
+          ob[eo] = oracle_bf16_rne(o);
+        }
+      }
+    }
+  if (o_out) memcpy(o_out, ob, npx * c * sizeof(uint16_t));
+  /* 3. output projection + identity residual on listed pixels, cache elsewhere */
+  for (size_t p = 0; p < npx; ++p)
+    for (int co = 0; co < c; ++co) {
+      size_t e = p * c + co;
+      if (!listed[p]) {
+        y[e] = y_cache[e];
+        if (y_abs) y_abs[e] = 0.0;
+        continue;
+      }
+      double acc = (bo ? (double)bo[co] : 0.0), aab = (bo ? fabs((double)bo[co]) : 0.0);
+      for (int ci = 0; ci < c; ++ci) {
+        double pr = wd[(size_t)co * c + ci] * bf16_to_double(ob[p * c + ci]);
+        acc += pr;
+        aab += fabs(pr);
+      }
+      y[e] = xd[e] + acc;
+      if (y_abs) y_abs[e] = aab + fabs(xd[e]);
+    }
+done4:
+  free(listed); free(xd); free(wq); free(wd); free(qb); free(qv); free(ob); free(sc);
+  return rc;
+}

@@ -167,6 +167,16 @@ int oracle_resblock(const uint16_t* x, const uint16_t* h_cache, const double* y_
                     double* h_pre, double* h_abs, uint16_t* h_out, double* a2_pre,
                     uint16_t* a2_out, double* y, double* y_abs, int n_threads);
 
+/* NEXT-4. Frame-sparse temporal attention with the latent (K/V) cache (R-28):
+ *   qkv = listed ? bf16(Wqkv x + bqkv) : qkv_cache;  per pixel and head, o[n] = softmax over
+ *   the T frames m of n's sequence of q_n.k_m/sqrt(d), times v_m;  y = listed ? x + Wo bf16(o)
+ *   + bo : y_cache.  See sphinx_oracle.c for the outputs. */
+int oracle_temporal_attn(const uint16_t* x, const uint16_t* qkv_cache, const double* y_cache,
+                         const uint16_t* wqkv, const float* bqkv, const uint16_t* wo,
+                         const float* bo, int n, int h, int w, int c, int heads, int T, int b,
+                         const int32_t* ids, int count, double* qkv_pre, uint16_t* qkv_out,
+                         double* qkv_abs, double* o_pre, uint16_t* o_out, double* y, double* y_abs);
+
 #ifdef __cplusplus
 }
 #endif

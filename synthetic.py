@@ -158,6 +158,13 @@ def gn_affine_f32(c, tag):
             (0.2 * g.standard_normal(c)).astype(np.float32))
 
 
+def linear_weights_bf16(cout, cin, tag, gain=1.0):
+    """Pointwise (1x1) projection W ~ N(0, gain^2/cin), [cout][cin] bf16 bits (NEXT-4 Wqkv, Wo)."""
+    w = rng("lin", tag, cout, cin).standard_normal((cout, cin), dtype=np.float32)
+    return to_bf16_bits(w * np.float32(gain / math.sqrt(cin)))
+
+
+ATTN_HEAD_DIM = 64  # SD/SVD attention head width (reading R-28)
 GN_GROUPS = 32     # torch/SD UNet Normalize(): GroupNorm(32, C, eps=1e-6) (reading R-26)
 GN_EPS = 1e-6
 

@@ -606,3 +606,77 @@ def test_resblock_density_0_and_full_cache_consistency():
     o = oracle.resblock(x, hc2, dense["y"], *args, np.array([0]))
     assert not np.array_equal(o["y"][0, 0:8, 0:8], dense["y"][0, 0:8, 0:8])
     assert np.array_equal(o["y"][1], dense["y"][1])   # frame 1: nothing listed
+
+
+# --------------------------------------------- NEXT-4 temporal attention + K/V cache
+
+def _ta_inputs(n, h, w, c, tag, gain=1.0):
+    x = syn.resblock_features_bf16((n, h, w, c), tag)
+    qc = syn.resblock_features_bf16((n, h, w, 3 * c), tag + "-qc")
+    yc = syn.bf16_bits_to_f32(syn.features_bf16((n, h, w, c), tag + "-yc")).astype(np.float64)
+    wq = syn.linear_weights_bf16(3 * c, c, tag + "-q", gain)
+    wo = syn.linear_weights_bf16(c, c, tag + "-o")
+    bq, bo = syn.bias_f32(3 * c, tag + "-q"), syn.bias_f32(c, tag + "-o")
+    return x, qc, yc, wq, bq, wo, bo
+
+
+def test_temporal_attn_single_frame_is_value():
+    """T = 1: the softmax over one key is exactly 1, so o = v of the same token (closed form)."""
+    n, h, w, c, b = 3, 8, 8, 128, 4
+    x, qc, yc, wq, bq, wo, bo = _ta_inputs(n, h, w, c, "pin-ta1")
+    o = oracle.temporal_attn(x, qc, yc, wq, bq, wo, bo, 2, 1, b, np.arange(n * 4))
+    v = syn.bf16_bits_to_f32(o["qkv"][..., 2 * c:]).astype(np.float64)
+    assert np.array_equal(o["o_pre"], v)
+
+
+def test_temporal_attn_matches_torch_dense():
+    """Every block listed: qkv = torch fp64 linear(x); o = torch fp64 scaled_dot_product_attention
+    over the frames of each sequence at each pixel (on the oracle's bf16 qkv, whose rounding is
+    pinned above); y = x + linear(o bits)."""
+    torch = pytest.importorskip("torch")
+    F = torch.nn.functional
+    n, h, w, c, b, heads, T = 4, 8, 6, 128, 4, 2, 2
+    x, qc, yc, wq, bq, wo, bo = _ta_inputs(n, h, w, c, "pin-ta2")
+    ids = np.arange(n * 2 * 2)
+    o = oracle.temporal_attn(x, qc, yc, wq, bq, wo, bo, heads, T, b, ids)
+    dec = lambda bits: torch.from_numpy(syn.bf16_bits_to_f32(bits).astype(np.float64))
+    t64 = lambda a: torch.from_numpy(np.asarray(a, np.float64))
+    q_ref = F.linear(dec(x), dec(wq), t64(bq)).numpy()
+    assert np.max(np.abs(o["qkv_pre"] - q_ref)) <= 1e-12
+    qkv = dec(o["qkv"]).reshape(n // T, T, h * w, 3, heads, c // heads)    # [s, t, p, qkv, hd, d]
+    qkv = qkv.permute(3, 0, 2, 4, 1, 5)                                      # [qkv, s, p, hd, t, d]
+    att = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2])            # [s, p, hd, t, d]
+    att = att.permute(0, 3, 1, 2, 4).reshape(n, h, w, c).numpy()
+    assert np.max(np.abs(o["o_pre"] - att)) <= 1e-12
+    y_ref = dec(x).numpy() + F.linear(dec(o["o"]), dec(wo), t64(bo)).numpy()
+    assert np.max(np.abs(o["y"] - y_ref)) <= 1e-12
+
+
+def test_temporal_attn_permutation_uniform_and_cache():
+    """Permuting the frames of a sequence permutes the outputs (no positional term); identical
+    keys give the mean of the values; caches from the dense pass make ANY list reproduce the
+    dense output bit for bit; a stale cached K/V of an unlisted frame changes listed outputs at
+    the same pixel only (the cache is read, per pixel)."""
+    n, h, w, c, b, heads, T = 3, 8, 8, 64, 4, 1, 3
+    x, qc, yc, wq, bq, wo, bo = _ta_inputs(n, h, w, c, "pin-ta3")
+    all_ids = np.arange(n * 4)
+    d0 = oracle.temporal_attn(x, qc, yc, wq, bq, wo, bo, heads, T, b, all_ids)
+    perm = [2, 0, 1]
+    dp = oracle.temporal_attn(x[perm], qc[perm], yc[perm], wq, bq, wo, bo, heads, T, b, all_ids)
+    assert np.array_equal(dp["y"], d0["y"][perm])
+    # uniform keys: Wk = 0 and bk = 0 -> every score 0 -> o = mean over frames of v
+    wq0 = wq.copy(); wq0[c:2 * c] = 0
+    bq0 = bq.copy(); bq0[c:2 * c] = 0
+    du = oracle.temporal_attn(x, qc, yc, wq0, bq0, wo, bo, heads, T, b, all_ids)
+    v = syn.bf16_bits_to_f32(du["qkv"][..., 2 * c:]).astype(np.float64)
+    assert np.allclose(du["o_pre"], np.broadcast_to(v.mean(axis=0), v.shape), rtol=0, atol=1e-12)
+    for ids in ([0], [1, 5, 6], [3, 4, 8, 11]):
+        o = oracle.temporal_attn(x, d0["qkv"], d0["y"], wq, bq, wo, bo, heads, T, b, np.array(ids))
+        assert np.array_equal(o["y"], d0["y"]) and np.array_equal(o["qkv"], d0["qkv"])
+    stale = d0["qkv"].copy()
+    stale[2, 0, 0, c:] = syn.resblock_features_bf16((2 * c,), "pin-ta3-stale")  # frame 2, pixel (0,0)
+    o = oracle.temporal_attn(x, stale, d0["y"], wq, bq, wo, bo, heads, T, b, np.array([0]))  # frame 0 blk 0
+    assert not np.array_equal(o["y"][0, 0, 0], d0["y"][0, 0, 0])
+    assert np.array_equal(o["y"][0, 1:4], d0["y"][0, 1:4]) and np.array_equal(o["y"][0, 0, 1:4], d0["y"][0, 0, 1:4])
+    o0 = oracle.temporal_attn(x, qc, yc, wq, bq, wo, bo, heads, T, b, np.zeros(0, np.int32))
+    assert np.array_equal(o0["y"], yc) and np.array_equal(o0["qkv"], qc)
