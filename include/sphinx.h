@@ -15,7 +15,8 @@
  * and the SURVEY §8(f) "next" rows built on them: sphinx_ddim_step (NEXT-1),
  * sphinx_uncertainty_map (NEXT-2), and the block-sparse ResNet block (NEXT-3:
  * sphinx_gn_block_stats, sphinx_gn_silu, sphinx_sparse_conv3x3_residual,
- * sphinx_sparse_resblock).
+ * sphinx_sparse_resblock), and the temporal-attention latent cache (NEXT-4:
+ * sphinx_sparse_pointwise, sphinx_temporal_attention, sphinx_temporal_block).
  *
  * CONVENTIONS (all entry points)
  *  - Ownership: every array pointer is caller-owned memory.  "device" pointers must be
@@ -106,7 +107,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 2
+#define SPHINX_ABI_VERSION 3
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -338,6 +339,62 @@ SPHINX_API sphinx_status sphinx_sparse_resblock(
     sphinx_dtype y_dtype, void* a_scratch, int32_t n, int32_t h, int32_t w, int32_t c,
     int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
     void* workspace, size_t workspace_bytes, sphinx_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
+ * NEXT-4. Temporal-attention latent cache ("Every T steps, the model performs a full
+ * denoising pass over all input and target frames, during which the intermediate latent
+ * representations from each temporal attention layer are cached.  In the subsequent (T-1)
+ * partial denoising steps, frames that are not actively refined simply retrieve and reuse these
+ * cached latents"; reading R-28).  Tokens of temporal attention are the frames of one sequence
+ * (frames_per_seq consecutive frames of the batch) at the same pixel.  The cache is the
+ * persistent q|k|v buffer: listed (frame, block) tokens are re-projected, every other token keeps
+ * the K/V of the last full step.
+ * ------------------------------------------------------------------------------- */
+
+/* Pointwise (1x1) projection on listed blocks, the tcgen05 kernel of sphinx_sparse_conv3x3 with
+ * one tap:  y[n,p,co] = (residual[n,p,co]) + bias[co] + sum_ci W[co][ci] x[n,p,ci]  for every
+ * real pixel of every listed block; other pixels untouched.  w: bf16 [c_out][c_in] (row-major =
+ * OHWI with 1x1 taps); residual: bf16 NHWC [N][h][w][c_out] or NULL (16-byte aligned, != x);
+ * other arguments, constraints and the workspace as for sphinx_sparse_conv3x3. */
+SPHINX_API sphinx_status sphinx_sparse_pointwise(
+    const void* x, const void* w, const float* bias, const void* residual, void* y,
+    sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, sphinx_stream_t stream);
+
+/* Attention of the listed tokens over the frames of their sequence:
+ *   o[n,p, head hd] = sum_m softmax_m(q[n,p,hd] . k[m,p,hd] / sqrt(64)) v[m,p,hd]
+ * m over the frames_per_seq frames of n's sequence, q|k|v read from qkv (listed tokens fresh,
+ * unlisted tokens cached), fp32 arithmetic, bf16 output written for listed pixels only.
+ * qkv  bf16 NHWC [N][h][w][3c] = q | k | v, each head-major (head hd = channels [64 hd, 64 hd+64)).
+ * o    bf16 NHWC [N][h][w][c].  c / heads must be 64; frames_per_seq <= 32 and divides N;
+ *      frames_per_seq * (6c + 4) bytes <= 227 KB (else UNSUPPORTED).
+ * workspace  sphinx_temporal_attention_workspace_size(...) bytes (4-byte aligned): the per
+ *      (sequence, block position) listed-frame bitmasks, rebuilt by every call. */
+SPHINX_API size_t sphinx_temporal_attention_workspace_size(int32_t n, int32_t h, int32_t w,
+                                                           int32_t frames_per_seq, int32_t block);
+SPHINX_API sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int32_t n, int32_t h,
+                                                   int32_t w, int32_t c, int32_t heads,
+                                                   int32_t frames_per_seq, int32_t block,
+                                                   const int32_t* block_ids, const int32_t* count,
+                                                   int32_t capacity, void* workspace,
+                                                   size_t workspace_bytes, sphinx_stream_t stream);
+
+/* The temporal block (3 launches + 1 plan kernel, graph capturable):
+ *   qkv_buf[listed] = bf16(Wqkv x + bqkv)       (sphinx_sparse_pointwise, c -> 3c)
+ *   o = attention(qkv_buf)                      (sphinx_temporal_attention)
+ *   y[listed] = x + Wo o + bo                   (sphinx_sparse_pointwise with residual x)
+ * x bf16 NHWC [N][h][w][c]; wqkv bf16 [3c][c]; wo bf16 [c][c]; bqkv [3c], bo [c] fp32 or NULL.
+ * qkv_buf bf16 [N][h][w][3c] and y (bf16/fp32 [N][h][w][c]) are persistent (initialise with a
+ * full step: every block listed); o_scratch bf16 [N][h][w][c].  workspace: a conv workspace for
+ * c_out = 3c (sphinx_conv_workspace_size); attn_workspace as above.  Buffers must not alias. */
+SPHINX_API sphinx_status sphinx_temporal_block(
+    const void* x, const void* wqkv, const float* bqkv, const void* wo, const float* bo,
+    int32_t heads, int32_t frames_per_seq, void* qkv_buf, void* o_scratch, void* y,
+    sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w, int32_t c, int32_t block,
+    const int32_t* block_ids, const int32_t* count, int32_t capacity, void* workspace,
+    size_t workspace_bytes, void* attn_workspace, size_t attn_workspace_bytes,
+    sphinx_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,8 @@ Functions carry the C names:
     sphinx_uncertainty_map  NEXT-2  (Alg1 lines 7-8)
     sphinx_gn_block_stats / sphinx_gn_silu / sphinx_sparse_conv3x3_residual /
     sphinx_sparse_resblock  NEXT-3  (block-sparse ResNet block)
+    sphinx_sparse_pointwise / sphinx_temporal_attention / sphinx_temporal_block
+                            NEXT-4  (temporal-attention latent cache)
 """
 import ctypes
 import os
@@ -27,13 +29,15 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 2
+ABI_VERSION = 3
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
            "sphinx_uncertainty_map", "sphinx_uncertainty_workspace_size",
            "sphinx_gn_stats_size", "sphinx_gn_block_stats", "sphinx_gn_silu",
-           "sphinx_sparse_conv3x3_residual", "sphinx_sparse_resblock")
+           "sphinx_sparse_conv3x3_residual", "sphinx_sparse_resblock",
+           "sphinx_sparse_pointwise", "sphinx_temporal_attention_workspace_size",
+           "sphinx_temporal_attention", "sphinx_temporal_block")
 
 _lib = None
 
@@ -98,6 +102,11 @@ def load(path=SO_PATH):
         "sphinx_sparse_conv3x3_residual": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_sparse_resblock": ([P, P, P, P, P, P, P, P, P, I, F, P, P, P, P, I, P,
                                     I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_sparse_pointwise": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_temporal_attention_workspace_size": ([I, I, I, I, I], Z),
+        "sphinx_temporal_attention": ([P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_temporal_block": ([P, P, P, P, P, I, I, P, P, P, I, I, I, I, I, I, P, P, I,
+                                   P, Z, P, Z, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -390,3 +399,87 @@ def sphinx_sparse_resblock(x, w1, b1, w2, b2, gn1, gn2, groups, eps, h_buf, x_st
         F32 if y.dtype == torch.float32 else BF16, _ptr(a_scratch), n, h, wd, c, int(block),
         _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes, _stream(stream))
     _chk("sphinx_sparse_resblock", rc)
+
+
+def attn_workspace(n, h, w, frames_per_seq, block, device):
+    """Workspace of sphinx_temporal_attention (listed-frame bitmasks), cached; memory only."""
+    key = ("attn", device, n, h, w, frames_per_seq, block)
+    ws = _ws_cache.get(key)
+    if ws is None:
+        import torch
+        nbytes = int(load().sphinx_temporal_attention_workspace_size(int(n), int(h), int(w),
+                                                                     int(frames_per_seq), int(block)))
+        ws = _ws_cache[key] = torch.zeros(max(nbytes, 4), dtype=torch.uint8, device=device)
+    return ws
+
+
+def sphinx_sparse_pointwise(x, w, bias, y, block, block_ids, count, residual=None, capacity=None,
+                            workspace=None, stream=None):
+    """NEXT-4 pointwise projection on listed blocks: y = (residual) + bias + W x.
+    x bf16 NHWC [N,H,W,Cin]; w bf16 [Cout, Cin]; y NHWC bf16/fp32 [N,H,W,Cout]."""
+    import torch
+    _dev(x, torch.bfloat16, "x")
+    _dev(w, torch.bfloat16, "w")
+    _dev(bias, torch.float32, "bias")
+    _dev(residual, torch.bfloat16, "residual")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    if y.dtype not in (torch.bfloat16, torch.float32) or not (y.is_cuda and y.is_contiguous()):
+        raise ValueError("y: contiguous CUDA bf16/fp32")
+    n, h, wd, cin = x.shape
+    cout = w.shape[0]
+    cap = block_ids.numel() if capacity is None else capacity
+    if workspace is None:
+        workspace = conv_workspace(cout, y.device, n, h, wd, block)
+    ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
+    rc = load().sphinx_sparse_pointwise(_ptr(x), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y),
+                                        F32 if y.dtype == torch.float32 else BF16, n, h, wd, cin, cout,
+                                        int(block), _ptr(block_ids), _ptr(count), int(cap), ws_ptr,
+                                        ws_bytes, _stream(stream))
+    _chk("sphinx_sparse_pointwise", rc)
+
+
+def sphinx_temporal_attention(qkv, o, heads, frames_per_seq, block, block_ids, count, capacity=None,
+                              workspace=None, stream=None):
+    """NEXT-4 attention of listed tokens over their sequence's frames (K/V cache in qkv)."""
+    import torch
+    _dev(qkv, torch.bfloat16, "qkv")
+    _dev(o, torch.bfloat16, "o")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, h, w, c = o.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    if workspace is None:
+        workspace = attn_workspace(n, h, w, frames_per_seq, block, o.device)
+    rc = load().sphinx_temporal_attention(_ptr(qkv), _ptr(o), n, h, w, c, int(heads), int(frames_per_seq),
+                                          int(block), _ptr(block_ids), _ptr(count), int(cap),
+                                          _ptr(workspace), workspace.numel(), _stream(stream))
+    _chk("sphinx_temporal_attention", rc)
+
+
+def sphinx_temporal_block(x, wqkv, bqkv, wo, bo, heads, frames_per_seq, qkv_buf, o_scratch, y, block,
+                          block_ids, count, capacity=None, workspace=None, attn_ws=None, stream=None):
+    """NEXT-4 temporal block (R-28): y[listed] = x + Wo attn(qkv) + bo with the
+    persistent q|k|v buffer as the latent cache of unlisted tokens."""
+    import torch
+    for t, nm in ((x, "x"), (wqkv, "wqkv"), (wo, "wo"), (qkv_buf, "qkv_buf"), (o_scratch, "o_scratch")):
+        _dev(t, torch.bfloat16, nm)
+    _dev(bqkv, torch.float32, "bqkv")
+    _dev(bo, torch.float32, "bo")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    if y.dtype not in (torch.bfloat16, torch.float32) or not (y.is_cuda and y.is_contiguous()):
+        raise ValueError("y: contiguous CUDA bf16/fp32")
+    n, h, wd, c = x.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    if workspace is None:
+        workspace = conv_workspace(3 * c, y.device, n, h, wd, block)
+    if attn_ws is None:
+        attn_ws = attn_workspace(n, h, wd, frames_per_seq, block, y.device)
+    ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
+    rc = load().sphinx_temporal_block(
+        _ptr(x), _ptr(wqkv), _ptr(bqkv), _ptr(wo), _ptr(bo), int(heads), int(frames_per_seq),
+        _ptr(qkv_buf), _ptr(o_scratch), _ptr(y), F32 if y.dtype == torch.float32 else BF16,
+        n, h, wd, c, int(block), _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes,
+        _ptr(attn_ws), attn_ws.numel(), _stream(stream))
+    _chk("sphinx_temporal_block", rc)

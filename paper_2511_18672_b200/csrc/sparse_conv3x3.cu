@@ -73,6 +73,7 @@ struct ConvParams {
   int y_f32;
   int h, w, cout, b, hb, wb;
   int kc;         // 64-channel chunks per tap
+  int taps;       // 9 = 3x3 conv; 1 = pointwise (1x1) projection (NEXT-4), per-tap path only
   int n_tiles_n;  // tiles along C_out
   int bpt;        // blocks per 128-row tile = 128 / b^2
   // split-K workspace (NULL = never split): per-(tile, split) fp32 partial tiles and one
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  (nR + p.bpt_r * CG - 1) / (p.bpt_r * CG)
                            : (count + bpt_pair - 1) / bpt_pair;
   const int tiles = m_tiles * p.n_tiles_n;
-  const int ksteps = 9 * p.kc;
+  const int ksteps = p.taps * p.kc;
   // halo mode splits K at 64-channel chunk boundaries (all 9 taps of a chunk stay together)
   // Full waves of tiles run unsplit; the last partial wave (rem tiles) is split nsplit ways
   // along K so that it fills one co-resident round (tail split-K).  Halo mode splits at
@@ -608,7 +609,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         int tap = ks0 / p.kc, kc = ks0 - (ks0 / p.kc) * p.kc;
         for (int ks = ks0; ks < ks1; ++ks) {
           {
-            const int dy = tap / 3, dx = tap - 3 * (tap / 3);
+            // 3x3: tap (dy, dx); pointwise: the block itself (centre tap)
+            const int dy = p.taps == 9 ? tap / 3 : 1, dx = p.taps == 9 ? tap - 3 * (tap / 3) : 1;
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* a_dst = sA + stage * kStageA;
             uint8_t* b_dst = sB + stage * Cfg::kStageB;
@@ -1196,7 +1198,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
                                void* y, sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_,
                                int32_t c_in, int32_t c_out, int32_t block, const int32_t* block_ids,
                                const int32_t* count, int32_t capacity, void* workspace,
-                               size_t workspace_bytes, sphinx_stream_t stream) {
+                               size_t workspace_bytes, sphinx_stream_t stream, int taps = 9) {
   if (!x || !w || !y || !block_ids || !count) return SPHINX_ERR_INVALID_ARGUMENT;
   if (residual && (residual == x || !aligned16(residual))) return SPHINX_ERR_INVALID_ARGUMENT;
   if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u)) return SPHINX_ERR_INVALID_ARGUMENT;
@@ -1219,7 +1221,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   int cg = 2;
   if (const char* env = getenv("SPHINX_CONV_CG")) cg = atoi(env) == 1 ? 1 : 2;
   // halo-staged A for 8x8 blocks unless overridden: each activation read once per chunk
-  int halo = block == 8 ? 1 : 0;
+  int halo = (block == 8 && taps == 9) ? 1 : 0;
   if (const char* env = getenv("SPHINX_CONV_HALO")) halo = halo && atoi(env) != 0;
   CUtensorMap ta, tb, tc;
   {
@@ -1242,8 +1244,8 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
   }
   {
-    const cuuint64_t dims[3] = {(cuuint64_t)c_in, 9, (cuuint64_t)c_out};
-    const cuuint64_t strides[2] = {(cuuint64_t)c_in * 2, (cuuint64_t)9 * c_in * 2};
+    const cuuint64_t dims[3] = {(cuuint64_t)c_in, (cuuint64_t)taps, (cuuint64_t)c_out};
+    const cuuint64_t strides[2] = {(cuuint64_t)c_in * 2, (cuuint64_t)taps * c_in * 2};
     const cuuint32_t box[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)(bn / cg)};
     const cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides,
@@ -1265,6 +1267,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.hb = hb;
   p.wb = wb;
   p.kc = cdiv(c_in, kBK);
+  p.taps = taps;
   p.n_tiles_n = cdiv(c_out, bn);
   p.bpt = kBM / (block * block);
   p.halo = halo;
@@ -1352,6 +1355,15 @@ extern "C" sphinx_status sphinx_sparse_conv3x3_residual(
   if (!residual) return SPHINX_ERR_INVALID_ARGUMENT;
   return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
                    capacity, workspace, workspace_bytes, stream);
+}
+
+extern "C" sphinx_status sphinx_sparse_pointwise(
+    const void* x, const void* w, const float* bias, const void* residual, void* y,
+    sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, sphinx_stream_t stream) {
+  return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
+                   capacity, workspace, workspace_bytes, stream, 1);
 }
 
 #ifdef SPHINX_TRACE

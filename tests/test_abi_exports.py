@@ -69,3 +69,16 @@ def test_next3_host_validation():
     assert lib.sphinx_sparse_resblock(p, p, null, p, null, p, p, p, p, 32, 1e-6, p, q, ctypes.c_void_p(4096),
                                       q, sp.BF16, ctypes.c_void_p(8192), 1, 16, 16, 64, 8, p, p, 4, null,
                                       0, null) == sp.ERR_INVALID_ARGUMENT
+
+
+def test_next4_host_validation():
+    lib = sp.load()
+    p, null = ctypes.c_void_p(1024), None
+    q = ctypes.c_void_p(4096)
+    # head dim must be 64 (c / heads), frames_per_seq must divide N
+    assert lib.sphinx_temporal_attention(p, q, 4, 8, 8, 128, 1, 2, 8, p, p, 4, p, 64, null) == sp.ERR_UNSUPPORTED
+    assert lib.sphinx_temporal_attention(p, q, 5, 8, 8, 128, 2, 2, 8, p, p, 5, p, 64, null) == \
+        sp.ERR_INVALID_ARGUMENT
+    assert lib.sphinx_temporal_attention_workspace_size(42, 72, 72, 21, 8) == 2 * 81 * 4
+    assert lib.sphinx_sparse_pointwise(p, p, null, null, p, sp.F32, 1, 16, 16, 12, 32, 8, p, p, 4, null, 0,
+                                       null) == sp.ERR_UNSUPPORTED

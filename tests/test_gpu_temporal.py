@@ -1,0 +1,249 @@
+"""GPU parity of NEXT-4, the temporal-attention latent cache (reading R-28), through
+the C ABI against the CPU oracle on the same seeded inputs.
+
+Bars (derived from the arithmetic):
+* Pointwise projection: the conv bar, |y - y_ref| <= 1e-3 sum|w x| + 1e-6 (+ the bf16 output
+  rounding 2^-8 |y_ref|).
+* Attention with scaled-identity projections (q = k = v = x/4, exact in bf16, so both sides
+  see the same tokens): fp32 scores/softmax/accumulation vs fp64, bound
+  d = 2e-5 * max_m |v_m| + 1e-6 per (token, head); the GPU's bf16 output must lie within half
+  an ulp + d of the oracle's unrounded value (it is the oracle's own rounding except within d
+  of a midpoint).  Then y = x + o exactly up to fp32 rounding.
+* Random projections: first-order chain from the projection bound through the scores
+  (|ds| <= sum |dq||k| + |q||dk| + |dq||dk|, scaled), the softmax (|dP| <= P (e^{2 max|ds|} - 1)),
+  the values and the output projection (1e-3 sum|Wo o| + |Wo| E_o).
+* Unlisted tokens of the q|k|v cache and of y: untouched, bitwise.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synthetic as syn
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+dev = "cuda"
+D = syn.ATTN_HEAD_DIM
+
+
+def T_(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(dev)
+
+
+def bf16(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(dev)
+
+
+def bits_of(t):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def dec(bits):
+    return syn.bf16_bits_to_f32(bits).astype(np.float64)
+
+
+def half_ulp(v):
+    _, e = np.frexp(np.abs(np.asarray(v, np.float64)))
+    return np.ldexp(1.0, e - 9)
+
+
+def gpu_ids(sp, mask):
+    n, hb, wb = mask.shape
+    ids = torch.full((n * hb * wb,), -7, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    sp.sphinx_compact_blocks(T_(mask.astype(np.uint8)), None, 0, 0, ids, cnt, shape=(n, hb, wb))
+    return ids, cnt
+
+
+def block_mask(n, h, w, b, density, pattern, tag):
+    hb, wb = -(-h // b), -(-w // b)
+    rg = syn.rng("ta-mask", tag)
+    return np.stack([syn.choose_cells(rg, hb, wb, round(density * hb * wb), pattern)
+                     for _ in range(n)]).astype(np.uint8)
+
+
+def listed_px(mask, h, w, b):
+    n = mask.shape[0]
+    m = np.zeros((n, h, w), bool)
+    for i, by, bx in zip(*np.nonzero(mask)):
+        m[i, by * b:by * b + b, bx * b:bx * b + b] = True
+    return m
+
+
+def identity_params(c):
+    """q = k = v = x/4 (exact in bf16), Wo = I, no biases: the tight configuration."""
+    eye = np.eye(c, dtype=np.float32)
+    wq = syn.to_bf16_bits(np.concatenate([eye * 0.25] * 3, axis=0))
+    return wq, None, syn.to_bf16_bits(eye), None
+
+
+def random_params(c, tag):
+    return (syn.linear_weights_bf16(3 * c, c, tag + "-q", 0.5), syn.bias_f32(3 * c, tag + "-q"),
+            syn.linear_weights_bf16(c, c, tag + "-o"), syn.bias_f32(c, tag + "-o"))
+
+
+class TB:
+    """GPU state of one temporal block: the persistent q|k|v cache and y."""
+
+    def __init__(self, sp, n, h, w, c, heads, T, b, qkv_cache, y_cache):
+        self.sp, self.heads, self.T, self.b = sp, heads, T, b
+        self.qkv = bf16(qkv_cache)
+        self.y = T_(y_cache.astype(np.float32))
+        self.o = torch.zeros((n, h, w, c), dtype=torch.bfloat16, device=dev)
+
+    def run(self, x_bits, params, ids, cnt):
+        wq, bq, wo, bo = params
+        self.sp.sphinx_temporal_block(bf16(x_bits), bf16(wq), None if bq is None else T_(bq), bf16(wo),
+                                      None if bo is None else T_(bo), self.heads, self.T, self.qkv, self.o,
+                                      self.y, self.b, ids, cnt)
+
+
+def attn_tol(o, heads, T, c, E_qkv=None):
+    """Per-element bound on |o_gpu - o_pre| for listed tokens (module docstring)."""
+    n, h, w, _ = o["o_pre"].shape
+    qkv = dec(o["qkv"]).reshape(n // T, T, h, w, 3, heads, D)
+    q, k, v = qkv[..., 0, :, :], qkv[..., 1, :, :], qkv[..., 2, :, :]     # [s, t, h, w, hd, d]
+    vmax = np.abs(v).max(axis=(1, 5))                                        # [s, h, w, hd]
+    fp = 2e-5 * vmax + 1e-6
+    if E_qkv is None:
+        E = np.broadcast_to(fp[:, None, :, :, :, None], (n // T, T, h, w, heads, D))
+        return E.reshape(n, h, w, c)
+    Ee = E_qkv.reshape(n // T, T, h, w, 3, heads, D)
+    dq, dk, dv = Ee[..., 0, :, :], Ee[..., 1, :, :], Ee[..., 2, :, :]
+    # |ds[t, m]| <= sum_d (|dq_t||k_m| + |q_t||dk_m| + |dq_t||dk_m|) / 8, max over m
+    aq, ak = np.abs(q), np.abs(k)
+    ds = (np.einsum("sthwed,smhwed->sthwem", dq, ak + dk) + np.einsum("sthwed,smhwed->sthwem", aq, dk)) / 8.0
+    dmax = ds.max(axis=-1)                                                   # [s, t, h, w, hd]
+    g = np.expm1(2.0 * dmax)
+    sv = np.abs(v).max(axis=1)                                               # [s, h, w, hd, d]
+    dvm = dv.max(axis=1)
+    E = g[..., None] * sv[:, None] + (1.0 + g[..., None]) * dvm[:, None] + fp[:, None, :, :, :, None]
+    return E.reshape(n, h, w, c)
+
+
+@pytest.mark.parametrize("n,h,c,b,dens,out", [(2, 16, 64, 4, 0.3, "f32"), (4, 24, 320, 8, 0.25, "bf16"),
+                                              (2, 18, 640, 8, 0.5, "f32"), (2, 18, 1280, 8, 0.5, "bf16"),
+                                              (3, 20, 128, 8, 0.6, "f32")])
+def test_pointwise_vs_oracle(sphinx, n, h, c, b, dens, out):
+    """The 1x1 (one-tap) mode of the tcgen05 conv kernel = the q|k|v projection of listed tokens."""
+    tag = f"pw{n}{h}{c}"
+    x = syn.resblock_features_bf16((n, h, h, c), tag)
+    wq, bq, wo, bo = random_params(c, tag)
+    mask = block_mask(n, h, h, b, dens, "scattered", tag)
+    ids, cnt = gpu_ids(sphinx, mask)
+    dt = torch.float32 if out == "f32" else torch.bfloat16
+    y = torch.full((n, h, h, 3 * c), -5.0, dtype=dt, device=dev)
+    sphinx.sphinx_sparse_pointwise(bf16(x), bf16(wq), T_(bq), y, b, ids, cnt)
+    torch.cuda.synchronize()
+    qc = np.zeros((n, h, h, 3 * c), np.uint16)
+    o = oracle.temporal_attn(x, qc, np.zeros((n, h, h, c)), wq, bq, wo, bo, c // D, 1, b, oracle.compact(mask))
+    L = listed_px(mask, h, h, b)
+    got = y.float().cpu().numpy().astype(np.float64)
+    tol = 1e-3 * o["qkv_abs"][L] + 1e-6
+    if out == "bf16":
+        tol = tol + 2.0 ** -8 * np.abs(o["qkv_pre"][L])
+    err = np.abs(got[L] - o["qkv_pre"][L])
+    assert np.all(err <= tol), f"max err/tol {np.max(err / tol)}"
+    assert np.all(got[~L] == -5.0)
+
+
+@pytest.mark.parametrize("n,h,w,c,T,b,dens,pattern,ident", [
+    (4, 8, 8, 64, 2, 4, 0.5, "scattered", True),
+    (21, 24, 24, 320, 21, 8, 0.25, "clustered", True),
+    (6, 18, 18, 640, 3, 8, 0.5, "scattered", True),
+    (4, 16, 16, 1280, 4, 8, 0.5, "checker", True),
+    (4, 8, 8, 64, 2, 4, 0.5, "scattered", False),
+    (21, 24, 24, 320, 21, 8, 0.25, "clustered", False),
+    (4, 18, 18, 1280, 4, 8, 0.5, "scattered", False),
+])
+def test_temporal_block_vs_oracle(sphinx, n, h, w, c, T, b, dens, pattern, ident):
+    tag = f"tb{n}{h}{c}{T}{ident}"
+    heads = c // D
+    x = syn.resblock_features_bf16((n, h, w, c), tag)
+    qkv_cache = syn.resblock_features_bf16((n, h, w, 3 * c), tag + "-qc")
+    y_cache = dec(syn.features_bf16((n, h, w, c), tag + "-yc"))
+    params = identity_params(c) if ident else random_params(c, tag)
+    mask = block_mask(n, h, w, b, dens, pattern, tag)
+    tb = TB(sphinx, n, h, w, c, heads, T, b, qkv_cache, y_cache)
+    ids, cnt = gpu_ids(sphinx, mask)
+    tb.run(x, params, ids, cnt)
+    torch.cuda.synchronize()
+    o = oracle.temporal_attn(x, qkv_cache, y_cache, *params, heads, T, b, oracle.compact(mask))
+    L = listed_px(mask, h, w, b)
+    qkv_got = bits_of(tb.qkv)
+    y_got = tb.y.cpu().numpy().astype(np.float64)
+    o_got = dec(bits_of(tb.o))
+    assert np.array_equal(qkv_got[~L], qkv_cache[~L])                      # the cache is untouched
+    assert np.array_equal(y_got[~L], y_cache[~L].astype(np.float32).astype(np.float64))
+    if ident:
+        assert np.array_equal(qkv_got[L], o["qkv"][L])                     # exact projections
+        E_o = attn_tol(o, heads, T, c)
+        tol_o = half_ulp(o["o_pre"]) + E_o
+        err = np.abs(o_got - o["o_pre"])
+        assert np.all(err[L] <= tol_o[L]), f"o max err/tol {np.max(err[L] / tol_o[L])}"
+        tol_y = 2 * half_ulp(o["o_pre"]) + E_o + 2.0 ** -23 * np.abs(o["y"]) + 1e-7
+    else:
+        E_qkv = 1e-3 * o["qkv_abs"] + 2 * half_ulp(o["qkv_pre"]) + 1e-6
+        E_qkv = np.where(L[..., None], E_qkv, 0.0)
+        E_o = attn_tol(o, heads, T, c, E_qkv)
+        tol_o = half_ulp(o["o_pre"]) + E_o
+        err = np.abs(o_got - o["o_pre"])
+        assert np.all(err[L] <= tol_o[L]), f"o max err/tol {np.max(err[L] / tol_o[L])}"
+        E_ob = 2 * half_ulp(o["o_pre"]) + E_o
+        wo_abs = np.abs(dec(params[2]))
+        tol_y = 1e-3 * o["y_abs"] + E_ob @ wo_abs.T + 2.0 ** -23 * np.abs(o["y"]) + 1e-6
+    err = np.abs(y_got - o["y"])
+    assert np.all(err[L] <= tol_y[L]), f"y max err/tol {np.max(err[L] / tol_y[L])}"
+
+
+def test_temporal_block_full_then_partial_steps(sphinx):
+    """Full step (every block: fills the q|k|v cache and y), then partial steps with a growing
+    active set and fresh x on listed blocks; each step equals the oracle run on its own caches
+    (identity projections: exact q|k|v, tight attention bound)."""
+    n, h, w, c, T, b = 6, 16, 16, 128, 3, 8
+    heads = c // D
+    params = identity_params(c)
+    x = syn.resblock_features_bf16((n, h, w, c), "tbloop-x0")
+    qc0 = syn.resblock_features_bf16((n, h, w, 3 * c), "tbloop-qc")
+    yc0 = dec(syn.features_bf16((n, h, w, c), "tbloop-yc"))
+    full = np.ones((n, 2, 2), np.uint8)
+    tb = TB(sphinx, n, h, w, c, heads, T, b, qc0, yc0)
+    ids, cnt = gpu_ids(sphinx, full)
+    tb.run(x, params, ids, cnt)
+    o = oracle.temporal_attn(x, qc0, yc0, *params, heads, T, b, oracle.compact(full))
+    rg = syn.rng("tbloop-masks")
+    mask = np.zeros((n, 2, 2), np.uint8)
+    for step in range(3):
+        mask |= (rg.random((n, 2, 2)) < 0.3).astype(np.uint8)
+        L = listed_px(mask, h, w, b)
+        x = x.copy()
+        x[L] = syn.resblock_features_bf16((n, h, w, c), f"tbloop-x{step + 1}")[L]
+        ids, cnt = gpu_ids(sphinx, mask)
+        tb.run(x, params, ids, cnt)
+        torch.cuda.synchronize()
+        o = oracle.temporal_attn(x, o["qkv"], o["y"], *params, heads, T, b, oracle.compact(mask))
+        assert np.array_equal(bits_of(tb.qkv), o["qkv"])                    # cache identical
+        E_o = attn_tol(o, heads, T, c)
+        y_got = tb.y.cpu().numpy().astype(np.float64)
+        tol = 2 * half_ulp(o["o_pre"]) + E_o + 2.0 ** -23 * np.abs(o["y"]) + 1e-7
+        err = np.abs(y_got - o["y"])
+        # earlier steps' bounded differences persist in unlisted y: check listed pixels
+        assert np.all(err[L] <= tol[L]), f"step {step}: max err/tol {np.max(err[L] / tol[L])}"
+
+
+def test_temporal_block_density_zero_and_validation(sphinx):
+    n, h, w, c, T, b = 2, 8, 8, 64, 2, 8
+    x = syn.resblock_features_bf16((n, h, w, c), "tb0")
+    qc = syn.resblock_features_bf16((n, h, w, 3 * c), "tb0-q")
+    yc = dec(syn.features_bf16((n, h, w, c), "tb0-y"))
+    tb = TB(sphinx, n, h, w, c, 1, T, b, qc, yc)
+    ids, cnt = gpu_ids(sphinx, np.zeros((n, 1, 1), np.uint8))
+    tb.run(x, identity_params(c), ids, cnt)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits_of(tb.qkv), qc)
+    assert np.array_equal(tb.y.cpu().numpy(), yc.astype(np.float32))
+    with pytest.raises(sphinx.SphinxError):   # head dim 32 is not supported
+        sphinx.sphinx_temporal_attention(tb.qkv, tb.o, 2, T, b, ids, cnt)
