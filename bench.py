@@ -396,6 +396,57 @@ def resblock_levels(torch, st, req, reps=20):
             "block_tflops_note": "2 convs' algorithmic FLOPs (real active px) / whole-block time"}
 
 
+def temporal_levels(torch, st, req, reps=20):
+    """NEXT-4: the temporal-attention block with the K/V latent cache at each UNet level over the
+    step's active list (T = 21 frames = one request), after a full step (every block) filled the
+    persistent q|k|v cache and y.  Graph-replay device time (L2-warm) and its parts."""
+    sp, d, dev = st.sp, st.d, st.dev
+    out = []
+    for l, (h, c) in enumerate(LEVELS):
+        n, hb = N_FRAMES, st.dims[l][1]
+        heads = c // syn.ATTN_HEAD_DIM
+        x = d[f"feat{l}"]
+        bf = st.bf
+        wq = bf(syn.linear_weights_bf16(3 * c, c, f"tq{l}", 0.5))
+        wo = bf(syn.linear_weights_bf16(c, c, f"to{l}"))
+        bq = torch.from_numpy(syn.bias_f32(3 * c, f"tq{l}")).to(dev)
+        bo = torch.from_numpy(syn.bias_f32(c, f"to{l}")).to(dev)
+        qkv = torch.zeros((n, h, h, 3 * c), dtype=torch.bfloat16, device=dev)
+        o = torch.zeros_like(x)
+        y = d[f"cache{l}"].clone()
+        all_ids = torch.arange(n * hb * hb, dtype=torch.int32, device=dev)
+        all_cnt = torch.tensor([n * hb * hb], dtype=torch.int32, device=dev)
+        ids, cnt = st.ids[l], st.cnt[l]
+
+        def block(i=ids, k=cnt):
+            sp.sphinx_temporal_block(x, wq, bq, wo, bo, heads, N_FRAMES, qkv, o, y, B, i, k)
+        block(all_ids, all_cnt)  # the full step: every token's q|k|v cached, y filled
+        t_block = graph_time(torch, block, reps)
+        t_qkv = graph_time(torch, lambda: sp.sphinx_sparse_pointwise(x, wq, bq, qkv, B, ids, cnt), reps)
+        t_att = graph_time(torch, lambda: sp.sphinx_temporal_attention(qkv, o, heads, N_FRAMES, B, ids, cnt), reps)
+        nb = int(cnt.item())
+        idn = ids[:nb].cpu().numpy()
+        pos = idn % (hb * hb)
+        by, bx = pos // hb, pos % hb
+        px = int((np.minimum(B, h - by * B) * np.minimum(B, h - bx * B)).sum())
+        upos = np.unique(pos)
+        upx = int((np.minimum(B, h - (upos // hb) * B) * np.minimum(B, h - (upos % hb) * B)).sum())
+        proj_flops = px * 2 * (3 * c * c + c * c)
+        attn_flops = px * 4 * N_FRAMES * c
+        staged = upx * N_FRAMES * 3 * c * 2
+        out.append({"level": l, "shape": [n, h, h, c], "heads": heads, "frames_per_seq": N_FRAMES,
+                    "active_blocks": nb, "real_px": px, "block_ms": round(t_block, 5),
+                    "block_tflops": round((proj_flops + attn_flops) / (t_block * 1e-3) / 1e12, 2),
+                    "qkv_proj_ms": round(t_qkv, 5),
+                    "qkv_proj_tflops": round(px * 2 * 3 * c * c / (t_qkv * 1e-3) / 1e12, 2),
+                    "attention_ms": round(t_att, 5),
+                    "attention_staged_gbs": round(staged / (t_att * 1e-3) / 1e9, 1)})
+    return {"levels": out, "timing": "CUDA-graph replay of 20 blocks, L2-warm; block = qkv pointwise "
+            "(tcgen05) + plan + attention + output pointwise with residual",
+            "flops_note": "projections 8 C^2 + attention 4 T C FLOP per listed token",
+            "attention_bytes_note": "staged token bytes: T x 3C x 2 B per pixel position with any listed frame"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -512,6 +563,7 @@ def run_gpu(args):
         sweep = density_sweep(torch, st.sp, dev)
     mem = memory_kernels(torch, st, req) if rank == 0 else None
     rblk = resblock_levels(torch, st, req) if (rank == 0 and not args.no_resblock) else None
+    tblk = temporal_levels(torch, st, req) if (rank == 0 and not args.no_resblock) else None
 
     if rank == 0:
         cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(req, bounded_s=args.cpu_seconds)
@@ -542,6 +594,7 @@ def run_gpu(args):
             "conv_isolated_ms": iso,
             "memory_kernels": mem,
             "resblock (NEXT-3)": rblk,
+            "temporal_attention (NEXT-4)": tblk,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "density_sweep": sweep,
