@@ -12,15 +12,17 @@
 //   ta_plan_kernel   one CTA: per (sequence, block position) a bitmask of listed frames
 //                    (atomicOr of bits: order-free, deterministic).
 //   ta_attn_kernel   unit = (sequence, block position, pixel) with a non-zero mask: the pixel's
-//                    T x 3C bf16 tokens are staged in shared memory by one thread with T bulk
-//                    async copies (cp.async.bulk + mbarrier), double-buffered so the next
-//                    pixel's tokens land while this one computes (row stride 6C+16 bytes, an odd
-//                    number of 16-byte units: the per-key 16-byte reads are conflict-free);
-//                    one warp per (listed frame, head): lane m < T computes the score q.k_m
-//                    (head dim 64, fp32), warp-shuffle softmax (SFU exponential), lane l then
-//                    accumulates output dims (2l, 2l+1) over the T values; bf16 store.
-// CUDA cores, not tensor cores: per (query, head) the work is T x 64 x 2 MACs against T x 256 B
-// of staged tokens — an L2/latency-bound gather-reduce, not a dense contraction.
+//                    q|k|v tokens of all T frames are staged in shared memory by T bulk async
+//                    copies (cp.async.bulk + mbarrier), double-buffered so the next pixel's
+//                    tokens land while this one computes; row stride 6C+16 bytes (an odd number
+//                    of 16-byte units: conflict-free ldmatrix rows).
+//                    One warp per (head, 16 listed queries): S = Q K^T with mma.sync m16n8k16
+//                    (bf16 in, fp32 accumulate), register softmax (quad shuffles, SFU exp), then
+//                    O = P V with P split into bf16 hi + lo parts (|P - hi - lo| <= 2^-17 P) and
+//                    V^T fragments from ldmatrix.trans; bf16 output of listed queries only.
+// Per (pixel, head) the contraction is tiny (<= 32 x 32 x 64): warp-level mma.sync is the right
+// tensor-core granularity (a CTA-wide tcgen05 tile would be >90% padding); the kernel is bound by
+// staging the T tokens of every pixel with a listed frame (HBM/L2), not by the math.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -46,6 +48,29 @@ __global__ void __launch_bounds__(1024) ta_plan_kernel(const int32_t* __restrict
   }
 }
 
+// ---- warp-level tensor-core helpers (mma.sync m16n8k16 bf16 -> fp32, ldmatrix)
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
 struct TaGeom {
   int h, w, c, heads, T, b, hb, wb, n_seq, nbuf;
   uint32_t rs;  // staged token row stride in bytes: 6c + 16 (an odd number of 16-byte units)
@@ -54,13 +79,13 @@ struct TaGeom {
 
 // Next unit (sequence, block position, pixel) at or after u, stepping by `step`, whose pixel is
 // inside the image and whose position has a listed frame; -1 if none.
-__device__ __forceinline__ long long ta_next(long long u, long long step, long long units,
+__device__ __forceinline__ int ta_next(int u, int step, int units,
                                              const uint32_t* __restrict__ posmask, const TaGeom& g,
                                              uint32_t& M, size_t& pix, int& s) {
   const int nblk = g.hb * g.wb, bb = g.b * g.b;
   for (; u < units; u += step) {
-    s = (int)(u / ((long long)nblk * bb));
-    const int r = (int)(u - (long long)s * nblk * bb);
+    s = u / (nblk * bb);
+    const int r = u - s * nblk * bb;
     const int pos = r / bb, px = r - pos * bb;
     M = __ldg(posmask + s * nblk + pos);
     if (M == 0u) continue;
@@ -77,9 +102,12 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
     const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* o, const uint32_t* __restrict__ posmask,
     const TaGeom g) {
   extern __shared__ __align__(128) uint8_t ta_sm[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ta_sm);
   uint8_t* rows = ta_sm + 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ta_sm);
+  // a 16-byte zero row at offset 64: ldmatrix rows of padded keys (>= T) point here
+  const uint32_t zero_row = smem_u32(ta_sm + 64);
+  if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(ta_sm + 64)[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -90,9 +118,11 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
   pdl_trigger();
   const int c = g.c, c3 = 3 * c, T = g.T;
   const size_t plane = (size_t)g.h * g.w;
-  const long long units = (long long)g.n_seq * g.hb * g.wb * g.b * g.b;
+  const int units = g.n_seq * g.hb * g.wb * g.b * g.b;
+  // one elected thread stages the pixel's T tokens (q|k|v rows, contiguous per frame) with T bulk
+  // async copies onto an mbarrier.  (Measured alternatives: k|v of all frames + q of listed frames
+  // only -- more, smaller copies -- and 16-byte cp.async by all threads were both 1.3x slower.)
   const uint32_t tok_bytes = (uint32_t)c3 * 2;
-  // one elected thread stages the pixel's T tokens with bulk async copies (one per frame)
   auto stage = [&](int buf, int s, size_t pix) {
     if (threadIdx.x == 0) {
       mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)T);
@@ -104,7 +134,7 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
   uint32_t M;
   size_t pix;
   int s;
-  long long u = ta_next(blockIdx.x, gridDim.x, units, posmask, g, M, pix, s);
+  int u = ta_next(blockIdx.x, gridDim.x, units, posmask, g, M, pix, s);
   if (u >= 0) stage(0, s, pix);
   uint32_t phase = 0u;  // bit k = parity of buffer k
   int buf = 0;
@@ -112,56 +142,126 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
     uint32_t Mn;
     size_t pixn;
     int sn;
-    const long long un = ta_next(u + gridDim.x, gridDim.x, units, posmask, g, Mn, pixn, sn);
+    const int un = ta_next(u + gridDim.x, gridDim.x, units, posmask, g, Mn, pixn, sn);
     if (un >= 0 && g.nbuf == 2) stage(buf ^ 1, sn, pixn);  // prefetch (that buffer is free)
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
     phase ^= 1u << buf;
-    const uint8_t* tk = rows + (size_t)buf * T * g.rs;
+    const uint32_t tk = smem_u32(rows + (size_t)buf * T * g.rs);
     const int nq = __popc(M);
-    for (int task = warp; task < nq * g.heads; task += kTaThreads / 32) {
-      const int qi = task / g.heads, hd = task - qi * g.heads;
-      uint32_t mm = M;
-      for (int k = 0; k < qi; ++k) mm &= mm - 1;
-      const int f = __ffs(mm) - 1;
-      float sc = -INFINITY;
-      if (lane < T) {
-        // 16-byte reads: the row stride is an odd number of 16-byte units, so the 8 lanes of each
-        // quarter-warp phase hit distinct bank quads (conflict-free); q is a broadcast
-        const uint4* q4 = reinterpret_cast<const uint4*>(tk + (size_t)f * g.rs + hd * kHeadDim * 2);
-        const uint4* k4 = reinterpret_cast<const uint4*>(tk + (size_t)lane * g.rs + (c + hd * kHeadDim) * 2);
-        float a0 = 0.f, a1 = 0.f;
+    const int mtiles = (nq + 15) >> 4;
+    const int gq = lane >> 2, tq = lane & 3;        // mma fragment row group / thread-in-group
+    const int mi = lane >> 3, ri = lane & 7;        // ldmatrix: matrix index / row within it
+    const int NT = (T + 7) >> 3;                    // key tiles of 8 (<= 4)
+    for (int task = warp; task < g.heads * mtiles; task += kTaThreads / 32) {
+      const int hd = task % g.heads, mt = task / g.heads;
+      // ---- S = Q K^T on the tensor cores (bf16 products exact, fp32 accumulation)
+      float S[4][4];
 #pragma unroll
-        for (int k = 0; k < kHeadDim / 8; ++k) {
-          const uint4 qa = q4[k], ka = k4[k];
-          const uint32_t qw[4] = {qa.x, qa.y, qa.z, qa.w}, kw[4] = {ka.x, ka.y, ka.z, ka.w};
+      for (int j = 0; j < 4; ++j) S[j][0] = S[j][1] = S[j][2] = S[j][3] = 0.f;
+      // this lane's ldmatrix row for the Q tile: query (mi & 1) * 8 + ri of the m-tile
+      const int qidx = mt * 16 + (mi & 1) * 8 + ri;
+      const int qf = __fns(M, 0, (qidx < nq ? qidx : 0) + 1);
+      const uint32_t qrow = tk + (uint32_t)qf * g.rs + (uint32_t)(hd * kHeadDim + (mi >> 1) * 8) * 2;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            a0 = fmaf(__uint_as_float(qw[i] << 16), __uint_as_float(kw[i] << 16), a0);
-            a1 = fmaf(__uint_as_float(qw[i] & 0xffff0000u), __uint_as_float(kw[i] & 0xffff0000u), a1);
-          }
+      for (int kk = 0; kk < kHeadDim / 16; ++kk) {
+        uint32_t a[4];
+        ldsm_x4(qrow + kk * 32, a);
+#pragma unroll
+        for (int j = 0; j < 4; j += 2) {
+          if (j >= NT) break;
+          // matrices: (keys 8j.., dims lo), (keys 8j.., dims hi), (keys 8j+8.., lo), (.., hi)
+          const int key = 8 * (j + (mi >> 1)) + ri;
+          const uint32_t addr = key < T ? tk + (uint32_t)key * g.rs + (uint32_t)(c + hd * kHeadDim + kk * 16 +
+                                                                               (mi & 1) * 8) * 2
+                                        : zero_row;
+          uint32_t bm[4];
+          ldsm_x4(addr, bm);
+          mma16816(S[j], a, bm[0], bm[1]);
+          if (j + 1 < NT) mma16816(S[j + 1], a, bm[2], bm[3]);
         }
-        sc = (a0 + a1) * g.scale;
       }
-      float mx = sc;
+      // ---- softmax over keys (row gq: S[j][0..1], row gq+8: S[j][2..3]); masked keys -> 0
+      float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
-      const float pr = lane < T ? __expf(sc - mx) : 0.f;
-      float den = pr;
+      for (int j = 0; j < 4; ++j) {
 #pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o2);
-      float o0 = 0.f, o1 = 0.f;
-      const uint32_t* vcol = reinterpret_cast<const uint32_t*>(tk + (2 * c + hd * kHeadDim) * 2) + lane;
-      const uint32_t rsw = g.rs / 4;
-      for (int m = 0; m < T; ++m) {
-        const float pm = __shfl_sync(0xffffffffu, pr, m);
-        const uint32_t vw = vcol[m * rsw];
-        o0 = fmaf(pm, __uint_as_float(vw << 16), o0);
-        o1 = fmaf(pm, __uint_as_float(vw & 0xffff0000u), o1);
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = j < NT && 8 * j + 2 * tq + e < T;
+          S[j][e] = ok ? S[j][e] * g.scale : -INFINITY;
+          S[j][2 + e] = ok ? S[j][2 + e] * g.scale : -INFINITY;
+          mx0 = fmaxf(mx0, S[j][e]);
+          mx1 = fmaxf(mx1, S[j][2 + e]);
+        }
       }
-      const float inv = 1.f / den;
-      const __nv_bfloat162 pk = __floats2bfloat162_rn(o0 * inv, o1 * inv);
-      *reinterpret_cast<__nv_bfloat162*>(o + (((size_t)s * T + f) * plane + pix) * c + hd * kHeadDim +
-                                         2 * lane) = pk;
+#pragma unroll
+      for (int o2 = 1; o2 < 4; o2 <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o2));
+      }
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          S[j][e] = __expf(S[j][e] - mx0);          // exp(-inf) = 0 for masked keys
+          S[j][2 + e] = __expf(S[j][2 + e] - mx1);
+          sum0 += S[j][e];
+          sum1 += S[j][2 + e];
+        }
+      }
+#pragma unroll
+      for (int o2 = 1; o2 < 4; o2 <<= 1) {
+        sum0 += __shfl_xor_sync(0xffffffffu, sum0, o2);
+        sum1 += __shfl_xor_sync(0xffffffffu, sum1, o2);
+      }
+      // ---- O = P V: P (fp32) split into bf16 hi + lo parts (P - hi - lo ~ 2^-17 P), V bf16 exact
+      float O[8][4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) O[j][0] = O[j][1] = O[j][2] = O[j][3] = 0.f;
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        if (16 * k2 >= T) break;
+        uint32_t ph[4], pl[4];
+        const int t0 = 2 * k2, t1 = 2 * k2 + 1;
+        const float p00 = S[t0][0], p01 = S[t0][1], p02 = S[t0][2], p03 = S[t0][3];
+        const float p10 = t1 < 4 ? S[t1][0] : 0.f, p11 = t1 < 4 ? S[t1][1] : 0.f;
+        const float p12 = t1 < 4 ? S[t1][2] : 0.f, p13 = t1 < 4 ? S[t1][3] : 0.f;
+        ph[0] = pack_bf16(p00, p01); ph[1] = pack_bf16(p02, p03);
+        ph[2] = pack_bf16(p10, p11); ph[3] = pack_bf16(p12, p13);
+        pl[0] = pack_bf16(p00 - bf16_lo(ph[0]), p01 - bf16_hi(ph[0]));
+        pl[1] = pack_bf16(p02 - bf16_lo(ph[1]), p03 - bf16_hi(ph[1]));
+        pl[2] = pack_bf16(p10 - bf16_lo(ph[2]), p11 - bf16_hi(ph[2]));
+        pl[3] = pack_bf16(p12 - bf16_lo(ph[3]), p13 - bf16_hi(ph[3]));
+        // V^T fragments via ldmatrix.trans: matrices (keys lo 8, dims lo), (keys hi 8, dims lo),
+        // (keys lo, dims hi), (keys hi, dims hi) of a 16-key x 16-dim slab
+        const int key = 16 * k2 + (mi & 1) * 8 + ri;
+#pragma unroll
+        for (int jn = 0; jn < 4; ++jn) {
+          const uint32_t addr = key < T ? tk + (uint32_t)key * g.rs +
+                                              (uint32_t)(2 * c + hd * kHeadDim + jn * 16 + (mi >> 1) * 8) * 2
+                                        : zero_row;
+          uint32_t bv[4];
+          ldsm_x4_t(addr, bv);
+          mma16816(O[2 * jn], ph, bv[0], bv[1]);
+          mma16816(O[2 * jn], pl, bv[0], bv[1]);
+          mma16816(O[2 * jn + 1], ph, bv[2], bv[3]);
+          mma16816(O[2 * jn + 1], pl, bv[2], bv[3]);
+        }
+      }
+      const float inv0 = 1.f / sum0, inv1 = 1.f / sum1;
+      const int q0 = mt * 16 + gq, q1 = q0 + 8;
+      if (q0 < nq) {
+        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q0 + 1)) * plane + pix) * c + hd * kHeadDim + 2 * tq;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][0] * inv0, O[j][1] * inv0);
+      }
+      if (q1 < nq) {
+        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q1 + 1)) * plane + pix) * c + hd * kHeadDim + 2 * tq;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][2] * inv1, O[j][3] * inv1);
+      }
     }
     __syncthreads();  // every warp is done with this buffer before it is staged again
     if (un >= 0 && g.nbuf == 1) stage(0, sn, pixn);
@@ -197,7 +297,8 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   if ((int64_t)capacity > (int64_t)n * cdiv(h, block) * cdiv(w, block)) return SPHINX_ERR_INVALID_ARGUMENT;
   if (workspace_bytes < sphinx_temporal_attention_workspace_size(n, h, w, T, block))
     return SPHINX_ERR_INVALID_ARGUMENT;
-  if (c / heads != kHeadDim || T > 32 || block > 64 || ta_smem(c, T, 1) > 227 * 1024)
+  if (c / heads != kHeadDim || T > 32 || block > 64 || ta_smem(c, T, 1) > 227 * 1024 ||
+      (long long)n * cdiv(h, block) * cdiv(w, block) * block * block >= (1ll << 31))
     return SPHINX_ERR_UNSUPPORTED;
   if (!aligned16(qkv) || !aligned16(o) || (reinterpret_cast<uintptr_t>(workspace) & 3u))
     return SPHINX_ERR_UNSUPPORTED;
