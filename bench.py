@@ -629,7 +629,9 @@ def run_e2e(torch, st, g, req, dev, args, flops):
                "feat2"]
     host = {k: torch.from_numpy(np.ascontiguousarray(req[k].view(np.int16) if req[k].dtype == np.uint16
                                                      else req[k])).pin_memory() for k in in_keys}
-    outs = [st.z[l] for l in range(3)] + [st.lat_out]
+    # the step's result is the refined latent (a6's output); the feature maps are intermediates of
+    # the UNet levels and stay on the device for the next layer
+    outs = [st.lat_out]
     out_host = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
     h2d = sum(h.numel() * h.element_size() for h in host.values())
     d2h = sum(o.numel() * o.element_size() for o in out_host)
@@ -658,8 +660,8 @@ def run_e2e(torch, st, g, req, dev, args, flops):
     ms = e0.elapsed_time(e1) / reps
     return {"value": round(flops / (ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "note": "conv weights resident on device (model state); per-step maps, features and latents "
-                    "H2D, refined feature maps + latent D2H"}
+            "note": "conv weights resident on device (model state); per-step opacity/uncertainty maps, "
+                    "level input features and latents H2D; the refined latent (the step's result) D2H"}
 
 
 # ----------------------------------------------------------------- CPU oracle arm

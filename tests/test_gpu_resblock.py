@@ -379,3 +379,27 @@ def test_resblock_full_step_then_partial_steps(sphinx):
         # caches carry the earlier steps' (bounded) differences: allow the full-step bound there
         err = np.abs(y_got - o["y"])
         assert np.all(err[L] <= 2 * tol[L]), f"step {step}: y max err/tol {np.max(err[L] / tol[L])}"
+
+
+def test_resblock_full_size_bench_config(sphinx):
+    """BASELINE configs[2] level-0 size in the bench's launch configuration: 21 frames x 72x72x320,
+    clustered ~25% of blocks, persistent buffers after a full step; shift weights (tight bound)."""
+    n, h, w, c, b, groups = 21, 72, 72, 320, 8, 32
+    shift = (2, 1)
+    x = syn.resblock_features_bf16((n, h, w, c), "rbfull")
+    h_cache = syn.resblock_features_bf16((n, h, w, c), "rbfull-hc")
+    y_cache = dec(syn.features_bf16((n, h, w, c), "rbfull-yc"))
+    mask = block_mask(n, h, w, b, 0.25, "clustered", "rbfull")
+    params = _params(c, "rbfull", shift)
+    rb = RB(sphinx, n, h, w, c, b, groups, h_cache, y_cache)
+    _stats_init(sphinx, rb, x, h_cache, mask)
+    ids, cnt = gpu_ids(sphinx, mask)
+    rb.run(x, params, ids, cnt)
+    torch.cuda.synchronize()
+    o = oracle.resblock(x, h_cache, y_cache, *params, groups, EPS, b, oracle.compact(mask))
+    L = listed_px(mask, h, w, b)
+    assert np.array_equal(bits_of(rb.h)[~L], h_cache[~L])
+    y_got = rb.y.cpu().numpy().astype(np.float64)
+    tol = _chain_tol(o, x, params, groups, shift)
+    err = np.abs(y_got - o["y"])
+    assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"

@@ -247,3 +247,26 @@ def test_temporal_block_density_zero_and_validation(sphinx):
     assert np.array_equal(tb.y.cpu().numpy(), yc.astype(np.float32))
     with pytest.raises(sphinx.SphinxError):   # head dim 32 is not supported
         sphinx.sphinx_temporal_attention(tb.qkv, tb.o, 2, T, b, ids, cnt)
+
+
+def test_temporal_block_full_size_bench_config(sphinx):
+    """BASELINE configs[2] level-0 size in the bench's launch configuration: one 21-frame
+    request at 72x72x320 (5 heads), clustered ~25% of blocks, identity projections (tight)."""
+    n, h, w, c, T, b = 21, 72, 72, 320, 21, 8
+    heads = c // D
+    x = syn.resblock_features_bf16((n, h, w, c), "tbfull")
+    qkv_cache = syn.resblock_features_bf16((n, h, w, 3 * c), "tbfull-qc")
+    y_cache = dec(syn.features_bf16((n, h, w, c), "tbfull-yc"))
+    params = identity_params(c)
+    mask = block_mask(n, h, w, b, 0.25, "clustered", "tbfull")
+    tb = TB(sphinx, n, h, w, c, heads, T, b, qkv_cache, y_cache)
+    ids, cnt = gpu_ids(sphinx, mask)
+    tb.run(x, params, ids, cnt)
+    torch.cuda.synchronize()
+    o = oracle.temporal_attn(x, qkv_cache, y_cache, *params, heads, T, b, oracle.compact(mask))
+    L = listed_px(mask, h, w, b)
+    assert np.array_equal(bits_of(tb.qkv), o["qkv"])
+    E_o = attn_tol(o, heads, T, c)
+    tol = 2 * half_ulp(o["o_pre"]) + E_o + 2.0 ** -23 * np.abs(o["y"]) + 1e-7
+    err = np.abs(tb.y.cpu().numpy().astype(np.float64) - o["y"])
+    assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
