@@ -107,7 +107,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 3
+#define SPHINX_ABI_VERSION 4
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -320,7 +320,30 @@ SPHINX_API sphinx_status sphinx_sparse_conv3x3_residual(
     int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
     void* workspace, size_t workspace_bytes, sphinx_stream_t stream);
 
-/* The whole block (6 launches, stream-ordered, graph capturable):
+/* Fused-conv table: combines the frame statistics from ALL block entries of `stats` (also written to
+ * its frame entries) into table fp32 [N][c][2] = (gamma[ch] rstd_g, beta[ch] - mean_g gamma[ch]
+ * rstd_g), so that SiLU(GN(x)) = SiLU(x * scale + shift).  table: device, 8-byte aligned. */
+SPHINX_API sphinx_status sphinx_gn_scale_shift(float* stats, const float* gamma, const float* beta,
+                                               float eps, int32_t n, int32_t h, int32_t w, int32_t c,
+                                               int32_t groups, int32_t block, float* table,
+                                               sphinx_stream_t stream);
+
+/* sphinx_sparse_conv3x3 of the activation a = SiLU(x * scale[n][ci] + shift[n][ci]) computed ON
+ * THE FLY from the raw map x: the halo tiles are normalised in shared memory between their TMA
+ * load and the MMA (out-of-image halo pixels stay zero: zero padding of a), so a never exists
+ * in HBM.  scale_shift: sphinx_gn_scale_shift's table.  Residual optional (as in _residual).
+ * Needs the halo-staged path: block == 8 (else UNSUPPORTED). */
+SPHINX_API sphinx_status sphinx_sparse_conv3x3_gn_silu(
+    const void* x, const float* scale_shift, const void* w, const float* bias, const void* residual,
+    void* y, sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity, void* workspace,
+    size_t workspace_bytes, sphinx_stream_t stream);
+
+/* The whole block (6 launches, stream-ordered, graph capturable).  With env SPHINX_RB_FUSED=1
+ * and block == 8:
+ *   gn_block_stats(x) -> gn_scale_shift(x) -> conv_gn_silu(x; w1,b1) into h -> gn_block_stats(h)
+ *   -> gn_scale_shift(h) -> conv_gn_silu(h; w2,b2, residual x) into y   (GN+SiLU fused into the
+ *   convs; a_scratch holds the scale/shift table).  Default (measured faster, DESIGN 6.8):
  *   gn_block_stats(x) -> gn_silu(x) -> conv(w1,b1) into h -> gn_block_stats(h) -> gn_silu(h)
  *   -> conv_residual(w2,b2, residual x) into y.
  * x        bf16 NHWC [N][h][w][c]: the current full map (cached values in unlisted blocks).

@@ -29,7 +29,7 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 3
+ABI_VERSION = 4
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
@@ -37,7 +37,8 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_gn_stats_size", "sphinx_gn_block_stats", "sphinx_gn_silu",
            "sphinx_sparse_conv3x3_residual", "sphinx_sparse_resblock",
            "sphinx_sparse_pointwise", "sphinx_temporal_attention_workspace_size",
-           "sphinx_temporal_attention", "sphinx_temporal_block")
+           "sphinx_temporal_attention", "sphinx_temporal_block", "sphinx_gn_scale_shift",
+           "sphinx_sparse_conv3x3_gn_silu")
 
 _lib = None
 
@@ -103,6 +104,8 @@ def load(path=SO_PATH):
         "sphinx_sparse_resblock": ([P, P, P, P, P, P, P, P, P, I, F, P, P, P, P, I, P,
                                     I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_sparse_pointwise": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_gn_scale_shift": ([P, P, P, F, I, I, I, I, I, I, P, P], I),
+        "sphinx_sparse_conv3x3_gn_silu": ([P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_temporal_attention_workspace_size": ([I, I, I, I, I], Z),
         "sphinx_temporal_attention": ([P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_temporal_block": ([P, P, P, P, P, I, I, P, P, P, I, I, I, I, I, I, P, P, I,
@@ -483,3 +486,38 @@ def sphinx_temporal_block(x, wqkv, bqkv, wo, bo, heads, frames_per_seq, qkv_buf,
         n, h, wd, c, int(block), _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes,
         _ptr(attn_ws), attn_ws.numel(), _stream(stream))
     _chk("sphinx_temporal_block", rc)
+
+
+def sphinx_gn_scale_shift(stats, gamma, beta, eps, n, h, w, c, groups, block, table, stream=None):
+    """NEXT-3 fused-conv table [N,C,2] = (gamma*rstd, beta - mean*gamma*rstd) from the statistics."""
+    import torch
+    for t, nm in ((stats, "stats"), (gamma, "gamma"), (beta, "beta"), (table, "table")):
+        _dev(t, torch.float32, nm)
+    rc = load().sphinx_gn_scale_shift(_ptr(stats), _ptr(gamma), _ptr(beta), float(eps), int(n), int(h), int(w),
+                                      int(c), int(groups), int(block), _ptr(table), _stream(stream))
+    _chk("sphinx_gn_scale_shift", rc)
+
+
+def sphinx_sparse_conv3x3_gn_silu(x, scale_shift, w, bias, y, block, block_ids, count, residual=None,
+                                  capacity=None, workspace=None, stream=None):
+    """NEXT-3: conv3x3 of SiLU(x*scale+shift) with the normalisation fused into the conv's halo
+    path (x raw bf16 NHWC; scale_shift fp32 [N,Cin,2])."""
+    import torch
+    _dev(x, torch.bfloat16, "x")
+    _dev(w, torch.bfloat16, "w")
+    _dev(scale_shift, torch.float32, "scale_shift")
+    _dev(bias, torch.float32, "bias")
+    _dev(residual, torch.bfloat16, "residual")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, h, wd, cin = x.shape
+    cout = w.shape[0]
+    cap = block_ids.numel() if capacity is None else capacity
+    if workspace is None:
+        workspace = conv_workspace(cout, y.device, n, h, wd, block)
+    ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
+    rc = load().sphinx_sparse_conv3x3_gn_silu(
+        _ptr(x), _ptr(scale_shift), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y),
+        F32 if y.dtype == torch.float32 else BF16, n, h, wd, cin, cout, int(block), _ptr(block_ids),
+        _ptr(count), int(cap), ws_ptr, ws_bytes, _stream(stream))
+    _chk("sphinx_sparse_conv3x3_gn_silu", rc)

@@ -147,9 +147,14 @@ __device__ __forceinline__ void chan_merge(float& na, float& ma, float& qa, floa
 // Frame statistics: one warp per (frame, group) combines the frame's Hb*Wb block entries
 // (lane-strided, then a fixed butterfly: deterministic, both partners hold identical bits) into
 // (mean, rstd) = (mean, 1/sqrt(M2/count + eps)) at fstats[n * G + g].
+// With `tab` != NULL the warp also writes, for the group's channels, the fused-conv table
+// tab[n][ch] = (gamma*rstd, beta - mean*gamma*rstd), i.e. a = SiLU(x * scale + shift).
 __global__ void __launch_bounds__(kGnThreads) gn_finalize_kernel(const float2* __restrict__ stats,
                                                                   float2* fstats, const GnGeom g,
-                                                                  int n_frames, float eps) {
+                                                                  int n_frames, float eps,
+                                                                  const float* __restrict__ gamma,
+                                                                  const float* __restrict__ beta,
+                                                                  float2* tab) {
   pdl_wait();
   pdl_trigger();
   const int warp = (blockIdx.x * kGnThreads + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -176,7 +181,15 @@ __global__ void __launch_bounds__(kGnThreads) gn_finalize_kernel(const float2* _
       na = nn; ma = mm; qa = qq;
     }
   }
-  if (lane == 0) fstats[warp] = make_float2(ma, 1.f / sqrtf(qa / na + eps));
+  const float rstd = 1.f / sqrtf(qa / na + eps);
+  if (lane == 0) fstats[warp] = make_float2(ma, rstd);
+  if (tab != nullptr) {
+    for (int k = lane; k < cg; k += 32) {
+      const int ch = gi * cg + k;
+      const float sc = __ldg(gamma + ch) * rstd;
+      tab[(size_t)n * g.c + ch] = make_float2(sc, fmaf(-ma, sc, __ldg(beta + ch)));
+    }
+  }
 }
 
 // a = bf16(SiLU((x - mean_g) * gamma_c * rstd_g + beta_c)) over (listed block + 1-px ring,
@@ -367,13 +380,43 @@ extern "C" sphinx_status sphinx_gn_silu(const void* x, float* stats, const float
   float2* fst = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(stats) + gn_block_bytes(n, h, w, groups, block));
   const int warps = n * groups;
   cudaError_t e = launch_k(gn_finalize_kernel, dim3(cdiv(warps, kGnThreads / 32)), dim3(kGnThreads), 0, s,
-                           blk, fst, g, (int)n, eps);
+                           blk, fst, g, (int)n, eps, static_cast<const float*>(nullptr),
+                           static_cast<const float*>(nullptr), static_cast<float2*>(nullptr));
   if (e != cudaSuccess) return cuda_fail(e);
   e = launch_k(gn_silu_kernel, dim3(gn_grid((long long)capacity * g.nslice * g.nrg, sms)), dim3(kGnThreads), 0, s,
                static_cast<const __nv_bfloat16*>(x), static_cast<const float2*>(fst), gamma, beta, g,
                block_ids, count, static_cast<__nv_bfloat16*>(a));
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
+}
+
+extern "C" sphinx_status sphinx_gn_scale_shift(float* stats, const float* gamma, const float* beta,
+                                               float eps, int32_t n, int32_t h, int32_t w, int32_t c,
+                                               int32_t groups, int32_t block, float* table,
+                                               sphinx_stream_t stream) {
+  if (!stats || !gamma || !beta || !table || !(eps >= 0.f) || n <= 0 || h <= 0 || w <= 0 || c <= 0 ||
+      groups <= 0 || block <= 0 || c % groups)
+    return SPHINX_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(stats) & 7u) || (reinterpret_cast<uintptr_t>(table) & 7u))
+    return SPHINX_ERR_INVALID_ARGUMENT;
+  int sms = 0;
+  sphinx_status st = check_device(&sms);
+  if (st != SPHINX_OK) return st;
+  const GnGeom g = gn_geom(h, w, c, groups, block);
+  float2* fst = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(stats) + gn_block_bytes(n, h, w, groups, block));
+  cudaError_t e = launch_k(gn_finalize_kernel, dim3(cdiv(n * groups, kGnThreads / 32)), dim3(kGnThreads), 0,
+                           reinterpret_cast<cudaStream_t>(stream), static_cast<const float2*>(
+                               reinterpret_cast<float2*>(stats)), fst, g, (int)n, eps, gamma, beta,
+                           reinterpret_cast<float2*>(table));
+  if (e != cudaSuccess) return cuda_fail(e);
+  return SPHINX_OK;
+}
+
+// The GN+SiLU-in-conv path is opt-in (SPHINX_RB_FUSED=1): measured slower than the separate
+// activation pass at every UNet level.  Read per call (tests toggle it).
+static bool rb_fused_enabled() {
+  const char* e = getenv("SPHINX_RB_FUSED");
+  return e && atoi(e) != 0;
 }
 
 extern "C" sphinx_status sphinx_sparse_resblock(
@@ -388,6 +431,30 @@ extern "C" sphinx_status sphinx_sparse_resblock(
       x_stats == h_stats)
     return SPHINX_ERR_INVALID_ARGUMENT;
   sphinx_status st;
+  if (block == 8 && c % 8 == 0 && rb_fused_enabled()) {
+    // Fused path (opt-in): GN+SiLU is applied inside the conv (transform warps between the halo
+    // TMA and the MMA), so the activation never round-trips through HBM; a_scratch holds the
+    // per-(frame, channel) (scale, shift) table ([N][c] float2 <= N*h*w*c*2 bytes).
+    float* tab = static_cast<float*>(a_scratch);
+    if ((st = sphinx_gn_block_stats(x, n, h, w, c, groups, block, block_ids, count, capacity, x_stats,
+                                    stream)) != SPHINX_OK)
+      return st;
+    if ((st = sphinx_gn_scale_shift(x_stats, gn1_gamma, gn1_beta, eps, n, h, w, c, groups, block, tab,
+                                    stream)) != SPHINX_OK)
+      return st;
+    if ((st = sphinx_sparse_conv3x3_gn_silu(x, tab, w1, b1, nullptr, h_buf, SPHINX_BF16, n, h, w, c, c,
+                                            block, block_ids, count, capacity, workspace, workspace_bytes,
+                                            stream)) != SPHINX_OK)
+      return st;
+    if ((st = sphinx_gn_block_stats(h_buf, n, h, w, c, groups, block, block_ids, count, capacity, h_stats,
+                                    stream)) != SPHINX_OK)
+      return st;
+    if ((st = sphinx_gn_scale_shift(h_stats, gn2_gamma, gn2_beta, eps, n, h, w, c, groups, block, tab,
+                                    stream)) != SPHINX_OK)
+      return st;
+    return sphinx_sparse_conv3x3_gn_silu(h_buf, tab, w2, b2, x, y, y_dtype, n, h, w, c, c, block, block_ids,
+                                         count, capacity, workspace, workspace_bytes, stream);
+  }
   // (1) statistics of x on the listed blocks; (2) a = SiLU(GN1(x)) on listed blocks + ring
   if ((st = sphinx_gn_block_stats(x, n, h, w, c, groups, block, block_ids, count, capacity, x_stats,
                                   stream)) != SPHINX_OK)

@@ -40,6 +40,9 @@ constexpr int kBK = 64;           // channels per K chunk: 128 B rows, SWIZZLE_1
 constexpr int kStageA = kBM * kBK * 2;  // 16 KB
 constexpr int kThreads = 224;
 constexpr int kAWarp = 6;  // halo mode: the halo (A) producer warp when the producers are split
+constexpr int kXWarp = 7;   // NORM (fused GroupNorm+SiLU) kernels: first transform warp
+constexpr int kXThreads = 256;  // transform threads (8 warps)
+constexpr int kThreadsNorm = kThreads + kXThreads;
 
 #ifdef SPHINX_TRACE
 // Dev-only timeline trace (libsphinx_trace.so): globaltimer stamps per CTA of one launch.
@@ -70,6 +73,9 @@ struct ConvParams {
   const float* bias;
   void* y;
   const __nv_bfloat16* res;  // NEXT-3: bf16 NHWC residual added in the epilogue (identity skip), or NULL
+  const float2* norm_tab;    // NEXT-3 fused GN+SiLU: [N][c_in] (scale, shift), a = SiLU(x*scale+shift)
+  int cin;
+  int xform_dbg;             // dev A/B knob (SPHINX_XFORM_DBG): 1 = skip the transform math
   int y_f32;
   int h, w, cout, b, hb, wb;
   int kc;         // 64-channel chunks per tap
@@ -127,13 +133,14 @@ __device__ __forceinline__ int choose_split(int tiles, int n_clusters, int kstep
 // (dy,dx) is the start shift dy*bpt*1280 + dx*128.  Valid because the SW128 XOR phase is
 // derived from absolute smem address bits (measured: base-offset field 0), exactly as TMA
 // writes it.  Plus a B ring of kBNum (tap, chunk) weight tiles.
-template <int BN, int CG, bool HALO, bool EDGE = false>
+template <int BN, int CG, bool HALO, bool EDGE = false, bool NORM = false>
 struct ConvCfg {
   static constexpr int kBNc = BN / CG;  // B rows (output channels) held by this CTA
   static constexpr int kStageB = kBNc * kBK * 2;
   static constexpr int kStageBytes = kStageA + kStageB;
   // barriers + split-K pixel table + per-accumulator bias slices (2 x 256 fp32)
-  static constexpr int kBarBytes = 512 + kBM * 8 + 2 * 256 * 4;
+  // NORM: + the per-chunk (scale, shift) table [8 blocks][8 groups][20 floats] + halo row info
+  static constexpr int kBarBytes = 512 + kBM * 8 + 2 * 256 * 4 + (NORM ? 8 * 8 * 20 * 4 + 512 : 0);
   static constexpr int kMaxSmem = 232448;          // 227 KB opt-in per CTA
   static constexpr int kAvail = kMaxSmem - 1024 - kBarBytes;
   // per-tap mode
@@ -156,7 +163,7 @@ struct ConvCfg {
                                         : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kSmem = 1024 + kRingBytes + kBarBytes;
   static_assert(HALO ? kBNum >= 3 : kStages >= 3, "pipeline too shallow");
-  static_assert((2 * kNumBars + 6) * 8 + 8 <= 512, "barrier area");
+  static_assert((2 * kNumBars + 5 + 3) * 8 <= 512, "barrier area");
   // stream-K owner staging: 2 buffers x kMaxParts parts x (32 cols x 128 rows fp32)
   static constexpr int kMaxParts = (kRingBytes / (2 * 32 * kBM * 4)) < 6 ? (kRingBytes / (2 * 32 * kBM * 4)) : 6;
   static_assert(kRingBytes >= (kBM + 16) * BN * 4, "split-K staging must fit the ring");
@@ -167,6 +174,47 @@ __device__ __forceinline__ void decode_block(int id, int hb, int wb, int& n, int
   const int r = id - n * hb * wb;
   by = r / wb;
   bx = r - by * wb;
+}
+
+// NORM hand-off: transform threads publish their generic-proxy smem writes to the tensor core
+// (async proxy) and to the leader CTA's MMA thread (cluster scope).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Explicit shared-space accesses for the transform warps (pointers derived from the aligned
+// dynamic-smem base otherwise compile to generic LD.E/ST.E).
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void sts64f(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -340,12 +388,13 @@ __device__ __forceinline__ HaloTile halo_tile(int mt, int rank, int nF, int nB, 
 //   (rank 0) waits for both halves on its full barrier and issues the MMAs; commits are
 //   multicast to both CTAs' barriers; each CTA's epilogue drains its own TMEM lanes and
 //   arrives on the leader's accumulator-empty barrier.  B traffic per SM halves.
-template <int BN, int CG, int BLK, bool HALO, bool EDGE>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int CG, int BLK, bool HALO, bool EDGE, bool NORM>
+__global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
     sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
-  using Cfg = ConvCfg<BN, CG, HALO, EDGE>;
+  using Cfg = ConvCfg<BN, CG, HALO, EDGE, NORM>;
+  static_assert(!NORM || HALO, "the fused GN+SiLU transform works on halo slots");
   static_assert(!EDGE || HALO, "edge packing is a halo-mode feature");
   static_assert(!HALO || BLK == 8, "halo staging needs 8x8 blocks");
   constexpr int S = Cfg::kStages;
@@ -363,6 +412,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* red_bar = tempty + 2;  // [2] split-K / stream-K partial staging barriers
   // bias of the tile held in accumulator a: s_bias[a * 256 + column] (0 beyond cout / no bias)
   float* s_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512 + kBM * 8);
+  // NORM: per-chunk (scale, shift) of the tile's blocks [8 blocks][64 channels], then the
+  // per-slot "halo landed" barriers (the A slots' full barriers become "transformed")
+  // table row (block i, 8-channel group j) at s_tab + (i * 8 + j) * 20 floats: the 80-byte stride
+  // puts the 8 groups a warp reads on disjoint bank quads (a 64-byte stride was 4-way conflicted)
+  float* s_tab = s_bias + 2 * 256;
+  uint8_t* s_rowinfo = reinterpret_cast<uint8_t*>(s_tab + 8 * 8 * 20);  // [<= 320 halo rows]: block or 255
+  uint64_t* landed = tempty + 5;  // after tmem_slot (tempty + 4)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef SPHINX_TRACE
@@ -376,9 +432,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmB);
     if constexpr (EDGE) tma_prefetch(&tmC);
     for (int s = 0; s < NB; ++s) {
-      mbar_init(&full[s], 1);
+      // NORM: an A slot is ready when BOTH CTAs' transform warps have arrived
+      mbar_init(&full[s], (NORM && s < Cfg::kANum) ? CG : 1);
       mbar_init(&empty[s], 1);
     }
+    if constexpr (NORM)
+      for (int s = 0; s < Cfg::kANum; ++s) mbar_init(&landed[s], 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);
@@ -519,7 +578,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* a_dst = sA + stage * Cfg::kASlot;
             uint32_t bar;
-            if constexpr (CG == 1) {
+            if constexpr (NORM) {
+              // raw halos land on this CTA's own barrier; the transform warps hand the slot on
+              mbar_arrive_expect_tx(&landed[stage], a_bytes);
+              bar = smem_u32(&landed[stage]);
+            } else if constexpr (CG == 1) {
               mbar_arrive_expect_tx(&full[stage], a_bytes);
               bar = smem_u32(&full[stage]);
             } else {
@@ -533,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* dst = a_dst + (l * g.bpt + i) * Cfg::kHaloRow;
                 const CUtensorMap* tm = g.tr ? &tmC : &tmA;
                 const int xx = g.tr ? cx[i] + l : cx[i], yy = g.tr ? cy[i] : cy[i] + l;
-                if constexpr (CG == 1) tma_load_4d_bar(tm, bar, dst, ca.kc * kBK, xx, yy, cn[i], pol_a);
+                if constexpr (CG == 1 || NORM) tma_load_4d_bar(tm, bar, dst, ca.kc * kBK, xx, yy, cn[i], pol_a);
                 else tma_load_4d_cg2(tm, bar, dst, ca.kc * kBK, xx, yy, cn[i], pol_a);
               }
             }
@@ -670,7 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
           for (int kc = kc0; kc < kc1; ++kc) {
-            mbar_wait(&full[stage], phase);
+            if constexpr (NORM) mbar_wait_acq_cluster(&full[stage], phase);
+            else mbar_wait(&full[stage], phase);
             tc_fence_after();
 #ifdef SPHINX_TRACE
             if (first) CONV_TRACE(10, gtimer());
@@ -1006,6 +1070,101 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if constexpr (NORM) {
+    if (warp >= kXWarp) {
+      // ============ fused GroupNorm + SiLU (NEXT-3): transform warps 7..14, both CTAs ============
+      // Each raw halo slot lands on this CTA's `landed` barrier; the kXThreads transform threads apply
+      // a = SiLU(x * scale + shift) in place (scale/shift per (frame, channel) from p.norm_tab),
+      // leaving out-of-image halo pixels at zero (the conv's zero padding is in the activation
+      // domain), fence the generic-proxy writes for the tensor core, and arrive on the leader's
+      // A-slot barrier (count = CTAs per pair).  Thread xt always touches the physical 16-byte
+      // unit xt & 7 of rows kXThreads/8 apart, so its SW128 phase -- and hence its logical 8-channel group
+      // -- is fixed (rows kXThreads/8 apart, a multiple of 8).
+      const int xt = threadIdx.x - kXWarp * 32;
+      const int u16 = xt & 7;
+      const int jl = u16 ^ ((xt >> 3) & 7);
+      int stage = 0;
+      uint32_t phase = 0;
+      SegIter it = it0;
+      Seg sg;
+      long long a_seg = -1;
+      HaloTile g{};
+      int rows = 0;
+      for (; it.get(sg); it.next(sg)) {
+        if (it.x != a_seg) {
+          // new tile: per halo row (= one pixel of one block's halo line) the block index, or 255
+          // if the pixel lies outside the image (its zero fill must stay zero); chunk-invariant
+          a_seg = it.x;
+          g = halo_tile<CG>(sg.t / p.n_tiles_n, rank, nF, nB, list, nR, p);
+          rows = g.lines * g.bpt * 10;
+          for (int row = xt; row < rows; row += kXThreads) {
+            const int lb = row / 10, px = row - lb * 10;
+            const int l = lb / g.bpt, i = lb - l * g.bpt;
+            int n = 0, by = 0, bx = 0;
+            decode_block(__ldg(g.list + min(g.j0 + i, g.nblk - 1)), p.hb, p.wb, n, by, bx);
+            const int y0 = by * BLK - 1, x0 = bx * BLK - 1;
+            const int yy = g.tr ? y0 + px : y0 + l, xx = g.tr ? x0 + l : x0 + px;
+            sts_u8(smem_u32(s_rowinfo) + row, (yy < 0 || yy >= p.h || xx < 0 || xx >= p.w) ? 255u : (uint32_t)i);
+          }
+        }
+        for (int kc = sg.k0; kc < sg.k1; ++kc) {
+          // this chunk's (scale, shift) for the tile's blocks x 64 channels
+          for (int idx = xt; idx < g.bpt * 64; idx += kXThreads) {
+            const int i = idx >> 6, ch = kc * kBK + (idx & 63);
+            int n = 0, by = 0, bx = 0;
+            decode_block(__ldg(g.list + min(g.j0 + i, g.nblk - 1)), p.hb, p.wb, n, by, bx);
+            const float2 v2 = ch < p.cin ? __ldg(p.norm_tab + (size_t)n * p.cin + ch) : make_float2(0.f, 0.f);
+            sts64f(smem_u32(s_tab + (i * 8 + ((idx & 63) >> 3)) * 20 + (idx & 7) * 2), v2.x, v2.y);
+          }
+          mbar_wait(&landed[stage], phase);
+          named_bar_sync(2, kXThreads);
+          const uint32_t slot = smem_u32(sA + stage * Cfg::kASlot + u16 * 16);
+          const uint32_t rinfo = smem_u32(s_rowinfo), tab0 = smem_u32(s_tab);
+          // 4 rows per iteration (rows kXThreads/8 apart keep this thread's SW128 phase):
+          // independent LDS / SFU chains in flight
+          constexpr int kRS = kXThreads / 8;
+          for (int r0 = xt >> 3; r0 < (p.xform_dbg ? 0 : rows); r0 += 4 * kRS) {
+            uint4 v[4];
+            int bi[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int row = r0 + kRS * q;
+              bi[q] = row < rows ? (int)lds_u8(rinfo + row) : 255;
+              if (bi[q] != 255) v[q] = lds128(slot + row * 128);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (bi[q] == 255) continue;
+              const uint32_t w4[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+              const uint32_t tb = tab0 + (uint32_t)((bi[q] * 8 + jl) * 20) * 4;
+              uint32_t o4[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint4 tu = lds128(tb + k * 16);  // (scale, shift) of channels 2k, 2k+1
+                const float4 t = make_float4(__uint_as_float(tu.x), __uint_as_float(tu.y),
+                                             __uint_as_float(tu.z), __uint_as_float(tu.w));
+                const float a0 = fmaf(__uint_as_float(w4[k] << 16), t.x, t.y);
+                const float a1 = fmaf(__uint_as_float(w4[k] & 0xffff0000u), t.z, t.w);
+                const __nv_bfloat162 pk = __floats2bfloat162_rn(__fdividef(a0, 1.f + __expf(-a0)),
+                                                                __fdividef(a1, 1.f + __expf(-a1)));
+                o4[k] = *reinterpret_cast<const uint32_t*>(&pk);
+              }
+              sts128(slot + (r0 + kRS * q) * 128, make_uint4(o4[0], o4[1], o4[2], o4[3]));
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(2, kXThreads);
+          if (xt == 0) {
+            if constexpr (CG == 1) mbar_arrive(&full[stage]);
+            else mbar_arrive_release_cluster(leader_addr(&full[stage]));
+          }
+          if (++stage == Cfg::kANum) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
   }
 #ifdef SPHINX_TRACE
   if (warp == 2 && lane == 0) CONV_TRACE(4, gtimer());
@@ -1108,11 +1267,11 @@ static PFN_encodeTiled_t get_encode_tiled() {
   return fn;
 }
 
-template <int BN, int CG, int BLK, bool HALO, bool EDGE = false>
+template <int BN, int CG, int BLK, bool HALO, bool EDGE = false, bool NORM = false>
 static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                                const ConvParams& p, int grid, cudaStream_t s) {
-  using Cfg = ConvCfg<BN, CG, HALO, EDGE>;
-  auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK, HALO, EDGE>;
+  using Cfg = ConvCfg<BN, CG, HALO, EDGE, NORM>;
+  auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK, HALO, EDGE, NORM>;
   static bool attr_set = false;  // per process; the attribute is per function
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
@@ -1121,7 +1280,7 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(NORM ? kThreadsNorm : kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -1141,6 +1300,10 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
 template <int BN>
 static sphinx_status launch_cg(int cg, const CUtensorMap& ta, const CUtensorMap& tb,
                                const CUtensorMap& tc, const ConvParams& p, int grid, cudaStream_t s) {
+  if (p.norm_tab) {  // fused GN+SiLU (halo mode, CTA pair; checked by the caller)
+    return p.plan_ids ? launch_bn<BN, 2, 8, true, true, true>(ta, tb, tc, p, grid, s)
+                      : launch_bn<BN, 2, 8, true, false, true>(ta, tb, tc, p, grid, s);
+  }
   if (p.b == 8 && p.halo && p.plan_ids)
     return cg == 2 ? launch_bn<BN, 2, 8, true, true>(ta, tb, tc, p, grid, s)
                    : launch_bn<BN, 1, 8, true, true>(ta, tb, tc, p, grid, s);
@@ -1198,7 +1361,8 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
                                void* y, sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_,
                                int32_t c_in, int32_t c_out, int32_t block, const int32_t* block_ids,
                                const int32_t* count, int32_t capacity, void* workspace,
-                               size_t workspace_bytes, sphinx_stream_t stream, int taps = 9) {
+                               size_t workspace_bytes, sphinx_stream_t stream, int taps = 9,
+                               const float2* norm_tab = nullptr) {
   if (!x || !w || !y || !block_ids || !count) return SPHINX_ERR_INVALID_ARGUMENT;
   if (residual && (residual == x || !aligned16(residual))) return SPHINX_ERR_INVALID_ARGUMENT;
   if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u)) return SPHINX_ERR_INVALID_ARGUMENT;
@@ -1223,6 +1387,10 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   // halo-staged A for 8x8 blocks unless overridden: each activation read once per chunk
   int halo = (block == 8 && taps == 9) ? 1 : 0;
   if (const char* env = getenv("SPHINX_CONV_HALO")) halo = halo && atoi(env) != 0;
+  if (norm_tab) {
+    if (!halo) return SPHINX_ERR_UNSUPPORTED;  // the transform works on halo slots (b = 8, 3x3)
+    cg = 2;
+  }
   CUtensorMap ta, tb, tc;
   {
     const cuuint64_t dims[4] = {(cuuint64_t)c_in, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
@@ -1259,6 +1427,10 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.bias = bias;
   p.y = y;
   p.res = static_cast<const __nv_bfloat16*>(residual);
+  p.norm_tab = norm_tab;
+  p.cin = c_in;
+  p.xform_dbg = 0;
+  if (const char* env = getenv("SPHINX_XFORM_DBG")) p.xform_dbg = atoi(env);
   p.y_f32 = y_dtype == SPHINX_F32;
   p.h = h;
   p.w = w_;
@@ -1364,6 +1536,17 @@ extern "C" sphinx_status sphinx_sparse_pointwise(
     void* workspace, size_t workspace_bytes, sphinx_stream_t stream) {
   return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
                    capacity, workspace, workspace_bytes, stream, 1);
+}
+
+extern "C" sphinx_status sphinx_sparse_conv3x3_gn_silu(
+    const void* x, const float* scale_shift, const void* w, const float* bias, const void* residual,
+    void* y, sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity, void* workspace,
+    size_t workspace_bytes, sphinx_stream_t stream) {
+  if (!scale_shift || (reinterpret_cast<uintptr_t>(scale_shift) & 7u)) return SPHINX_ERR_INVALID_ARGUMENT;
+  return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
+                   capacity, workspace, workspace_bytes, stream, 9,
+                   reinterpret_cast<const float2*>(scale_shift));
 }
 
 #ifdef SPHINX_TRACE

@@ -291,6 +291,14 @@ def _chain_tol(o, x_bits, params, groups, shift):
     return 1e-3 * o["y_abs"] + prop + 2.0 ** -23 * np.abs(o["y"]) + 1e-6
 
 
+@pytest.fixture(params=["fused", "unfused"])
+def rb_path(request, monkeypatch):
+    """The block with GN+SiLU fused into the conv's halo path (SPHINX_RB_FUSED=1, 8x8 blocks) and
+    with the separate gn_silu activation pass (the default)."""
+    monkeypatch.setenv("SPHINX_RB_FUSED", "1" if request.param == "fused" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("n,h,w,c,b,groups,dens,pattern,shift", [
     (2, 16, 16, 32, 4, 8, 0.3, "scattered", (2, 2)),
     (2, 20, 13, 64, 8, 16, 0.5, "scattered", (0, 1)),
@@ -301,7 +309,7 @@ def _chain_tol(o, x_bits, params, groups, shift):
     (2, 72, 72, 320, 8, 32, 0.25, "clustered", None),
     (2, 18, 18, 1280, 8, 32, 0.5, "scattered", None),
 ])
-def test_resblock_vs_oracle(sphinx, n, h, w, c, b, groups, dens, pattern, shift):
+def test_resblock_vs_oracle(sphinx, rb_path, n, h, w, c, b, groups, dens, pattern, shift):
     tag = f"rb{n}{h}{w}{c}{shift}"
     x = syn.resblock_features_bf16((n, h, w, c), tag)
     h_cache = syn.resblock_features_bf16((n, h, w, c), tag + "-hc")
@@ -332,7 +340,7 @@ def test_resblock_vs_oracle(sphinx, n, h, w, c, b, groups, dens, pattern, shift)
     assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
 
 
-def test_resblock_density_zero(sphinx):
+def test_resblock_density_zero(sphinx, rb_path):
     n, h, w, c, b = 1, 16, 16, 64, 8
     x = syn.resblock_features_bf16((n, h, w, c), "rb0")
     hc = syn.resblock_features_bf16((n, h, w, c), "rb0-h")
@@ -346,7 +354,7 @@ def test_resblock_density_zero(sphinx):
     assert np.array_equal(rb.y.cpu().numpy(), yc.astype(np.float32))
 
 
-def test_resblock_full_step_then_partial_steps(sphinx):
+def test_resblock_full_step_then_partial_steps(sphinx, rb_path):
     """The serving loop (R-17): a full step (every block) fills h, y and both
     statistics buffers; partial steps with a growing active set (A_u monotone) and
     fresh x on listed blocks rewrite listed data only.  Each partial step equals the oracle
