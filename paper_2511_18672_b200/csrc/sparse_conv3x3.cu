@@ -1386,7 +1386,16 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   if (const char* env = getenv("SPHINX_CONV_CG")) cg = atoi(env) == 1 ? 1 : 2;
   // halo-staged A for 8x8 blocks unless overridden: each activation read once per chunk
   int halo = (block == 8 && taps == 9) ? 1 : 0;
-  if (const char* env = getenv("SPHINX_CONV_HALO")) halo = halo && atoi(env) != 0;
+  if (const char* env = getenv("SPHINX_CONV_HALO")) {
+    halo = halo && atoi(env) != 0;  // 1 = force halo staging, 0 = force per-tap
+  } else if (halo && !norm_tab) {
+    // At most one wave of tiles even if every capacity block is listed (e.g. a single frame):
+    // the problem is latency-bound, and the per-tap path's split-K over (tap, chunk) K-steps
+    // (halo mode splits only at 64-channel chunks) fills more of the GPU.  Measured on one
+    // 72x72x320 frame: 9.5 vs 12.6 us at 5% density, 15.5 vs 17.8 us dense.
+    const long long max_tiles = (long long)cdiv(capacity, (kBM / (block * block)) * 2) * cdiv(c_out, pick_bn(c_out));
+    if (max_tiles <= sms / 2) halo = 0;
+  }
   if (norm_tab) {
     if (!halo) return SPHINX_ERR_UNSUPPORTED;  // the transform works on halo slots (b = 8, 3x3)
     cg = 2;
