@@ -82,3 +82,21 @@ def test_next4_host_validation():
     assert lib.sphinx_temporal_attention_workspace_size(42, 72, 72, 21, 8) == 2 * 81 * 4
     assert lib.sphinx_sparse_pointwise(p, p, null, null, p, sp.F32, 1, 16, 16, 12, 32, 8, p, p, 4, null, 0,
                                        null) == sp.ERR_UNSUPPORTED
+
+
+def test_sass_uses_tcgen05_tma_and_mma():
+    """The built library is sm_100a code whose conv kernels issue tcgen05 MMAs (UTCHMMA, incl.
+    the CTA-pair form), TMA tensor loads (UTMALDG) and bulk copies (UBLKCP), read TMEM with
+    LDTM, and whose temporal attention uses warp-level tensor cores (HMMA bf16)."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    so = os.path.join(ROOT, "paper_2511_18672_b200", "libsphinx.so")
+    elf = subprocess.run([tool, "-lelf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in elf
+    sass = subprocess.run([tool, "-sass", so], capture_output=True, text=True).stdout
+    for mnemonic in ("UTCHMMA.2CTA", "UTCHMMA", "UTMALDG.4D", "UTMALDG.3D.2CTA", "UBLKCP", "LDTM",
+                     "HMMA.16816.F32.BF16"):
+        assert mnemonic in sass, mnemonic
