@@ -129,7 +129,9 @@ class GpuStep:
         self.z = [self.d[f"cache{l}"].clone() for l in range(3)]
         self.lat_out = torch.empty_like(self.d["x0"])
         self.logics = [sp.make_klogic(syn.SPEC_KLOGIC["thr"], syn.SPEC_KLOGIC["steps"])]
-        self.launches_per_step = 2 + 4 + 2 + 3 * CONVS_PER_LEVEL + 1
+        # block_mask (2) + batched compaction (1) + noise (2) + convs + edge plans (levels 1, 2:
+        # once per level) + scatter (1)
+        self.launches_per_step = 2 + 1 + 2 + 3 * CONVS_PER_LEVEL + 2 + 1
         self.conv_events = None
 
     def run(self, conv_events=None):
@@ -137,10 +139,12 @@ class GpuStep:
         start = dict(q_reg=d["q"], c0=d["c0"], c1=d["c1"], t=d["t"], gamma=GAMMA, logics=self.logics,
                      logic_id=d["lid"])
         sp.sphinx_block_mask(d["O"], d["U"], d["tau_u"], 0.5, F, B, self.masks, self.counts, start, self.k)
-        for l in range(3):
-            sp.sphinx_compact_blocks(self.masks[l], self.k, U_STEP, sp.SELECT_ACTIVE, self.ids[l], self.cnt[l])
-        sp.sphinx_compact_blocks(None, self.k, U_STEP, sp.SELECT_INACTIVE_FRAMES, self.ids_in, self.cnt_in,
-                                 shape=tuple(self.masks[0].shape))
+        # the three levels' ACTIVE lists and the INACTIVE_FRAMES list: one launch, one CTA per list
+        sp.sphinx_compact_blocks_batch(
+            [dict(block_mask=self.masks[l], start_step=self.k, step_u=U_STEP, select=sp.SELECT_ACTIVE,
+                  block_ids=self.ids[l], count=self.cnt[l]) for l in range(3)] +
+            [dict(block_mask=None, start_step=self.k, step_u=U_STEP, select=sp.SELECT_INACTIVE_FRAMES,
+                  block_ids=self.ids_in, count=self.cnt_in, shape=tuple(self.masks[0].shape))])
         # Alg1 line 12: active latent blocks noised to their start step k; line 19: inactive
         # frames resampled to u+1 from the clean latent
         sp.sphinx_noise_inject(d["x0"], d["eps"], self.zt, B, self.ids[0], self.cnt[0], self.k, d["abar"])
@@ -151,7 +155,9 @@ class GpuStep:
                 dst = self.y[l] if j % 2 == 0 else self.z[l]
                 if conv_events is not None:
                     conv_events[l][j][0].record()
-                sp.sphinx_sparse_conv3x3(src, d[f"w{l}{j}"], d[f"b{l}{j}"], dst, B, self.ids[l], self.cnt[l])
+                # the second conv of a level uses the same list and workspace: reuse its edge plan
+                sp.sphinx_sparse_conv3x3(src, d[f"w{l}{j}"], d[f"b{l}{j}"], dst, B, self.ids[l], self.cnt[l],
+                                         reuse_plan=j > 0)
                 if conv_events is not None:
                     conv_events[l][j][1].record()
                 src = dst

@@ -107,7 +107,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 4
+#define SPHINX_ABI_VERSION 5
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -158,6 +158,22 @@ SPHINX_API sphinx_status sphinx_block_mask(const float* opacity, const float* un
 SPHINX_API sphinx_status sphinx_compact_blocks(const uint8_t* block_mask, int32_t n, int32_t hb, int32_t wb,
                                     const int32_t* start_step, int32_t step_u, sphinx_select select,
                                     int32_t* block_ids, int32_t* count, sphinx_stream_t stream);
+
+/* Several compactions in ONE launch (one CTA per job; each job exactly as
+ * sphinx_compact_blocks with the same arguments): e.g. the ACTIVE lists of every UNet level and
+ * the INACTIVE_FRAMES list of one step.  jobs: host array, copied into the launch. */
+#define SPHINX_MAX_COMPACT_JOBS 8
+typedef struct {
+  const uint8_t* block_mask;  /* device u8 [n][hb][wb] (may be NULL for INACTIVE_FRAMES / ALL) */
+  int32_t n, hb, wb;
+  const int32_t* start_step;  /* device [n] or NULL */
+  int32_t step_u;
+  sphinx_select select;
+  int32_t* block_ids;         /* device out, capacity n*hb*wb */
+  int32_t* count;             /* device out */
+} sphinx_compact_job;
+SPHINX_API sphinx_status sphinx_compact_blocks_batch(const sphinx_compact_job* jobs, int32_t n_jobs,
+                                                     sphinx_stream_t stream);
 
 /* ---------------------------------------------------------------------------------
  * (3) Forward noise on listed blocks (Alg1 line 12 add_noise(Z0, k_min); line 19
@@ -210,6 +226,18 @@ SPHINX_API sphinx_status sphinx_sparse_conv3x3(const void* x, const void* w, con
                                     sphinx_stream_t stream);
 SPHINX_API size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
                                   int32_t block);
+
+/* sphinx_sparse_conv3x3 with an optional residual (as in _residual, NULL = none) and flags:
+ * SPHINX_CONV_REUSE_PLAN  the workspace already holds the edge-class plan of THIS list (the
+ *                         caller's previous conv on this stream used the same block_ids, count and
+ *                         workspace, e.g. the second conv of a ResNet block): skip recomputing it.
+ *                         Undefined results if the list changed in between. */
+#define SPHINX_CONV_REUSE_PLAN 1
+SPHINX_API sphinx_status sphinx_sparse_conv3x3_ex(
+    const void* x, const void* w, const float* bias, const void* residual, void* y,
+    sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, int32_t flags, sphinx_stream_t stream);
 
 /* ---------------------------------------------------------------------------------
  * (5) Cached scatter ("reuses cached latents from the last full denoising step for

@@ -29,7 +29,7 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 4
+ABI_VERSION = 5
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
@@ -38,7 +38,7 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_sparse_conv3x3_residual", "sphinx_sparse_resblock",
            "sphinx_sparse_pointwise", "sphinx_temporal_attention_workspace_size",
            "sphinx_temporal_attention", "sphinx_temporal_block", "sphinx_gn_scale_shift",
-           "sphinx_sparse_conv3x3_gn_silu")
+           "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex")
 
 _lib = None
 
@@ -56,6 +56,17 @@ class KLogic(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int32), ("thr", ctypes.c_double * 16),
                 ("step", ctypes.c_int32 * 16), ("fallback_k", ctypes.c_int32),
                 ("k_max", ctypes.c_int32)]
+
+
+class CompactJob(ctypes.Structure):
+    """sphinx_compact_job (one list of a batched compaction)."""
+    _fields_ = [("block_mask", ctypes.c_void_p), ("n", ctypes.c_int32), ("hb", ctypes.c_int32),
+                ("wb", ctypes.c_int32), ("start_step", ctypes.c_void_p), ("step_u", ctypes.c_int32),
+                ("select", ctypes.c_int32), ("block_ids", ctypes.c_void_p), ("count", ctypes.c_void_p)]
+
+
+MAX_COMPACT_JOBS = 8
+CONV_REUSE_PLAN = 1
 
 
 class StartArgs(ctypes.Structure):
@@ -105,6 +116,8 @@ def load(path=SO_PATH):
                                     I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_sparse_pointwise": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_gn_scale_shift": ([P, P, P, F, I, I, I, I, I, I, P, P], I),
+        "sphinx_compact_blocks_batch": ([P, I, P], I),
+        "sphinx_sparse_conv3x3_ex": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, I, P], I),
         "sphinx_sparse_conv3x3_gn_silu": ([P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_temporal_attention_workspace_size": ([I, I, I, I, I], Z),
         "sphinx_temporal_attention": ([P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
@@ -197,6 +210,28 @@ def sphinx_compact_blocks(block_mask, start_step, step_u, select, block_ids, cou
     _chk("sphinx_compact_blocks", rc)
 
 
+def sphinx_compact_blocks_batch(jobs, stream=None):
+    """Several compactions in one launch.  jobs: list of dicts with the arguments of
+    sphinx_compact_blocks (block_mask, start_step, step_u, select, block_ids, count, shape)."""
+    import torch
+    if not 0 < len(jobs) <= MAX_COMPACT_JOBS:
+        raise ValueError("1..8 jobs")
+    arr = (CompactJob * len(jobs))()
+    for i, jb in enumerate(jobs):
+        m = jb.get("block_mask")
+        _dev(m, torch.uint8, "block_mask")
+        _dev(jb.get("start_step"), torch.int32, "start_step")
+        _dev(jb["block_ids"], torch.int32, "block_ids")
+        _dev(jb["count"], torch.int32, "count")
+        n, hb, wb = m.shape if m is not None else jb["shape"]
+        arr[i] = CompactJob(None if m is None else m.data_ptr(), n, hb, wb,
+                            None if jb.get("start_step") is None else jb["start_step"].data_ptr(),
+                            int(jb.get("step_u", 0)), int(jb["select"]), jb["block_ids"].data_ptr(),
+                            jb["count"].data_ptr())
+    rc = load().sphinx_compact_blocks_batch(ctypes.cast(arr, ctypes.c_void_p), len(jobs), _stream(stream))
+    _chk("sphinx_compact_blocks_batch", rc)
+
+
 def sphinx_noise_inject(x0, eps, x_t, block, block_ids, count, step, abar, capacity=None,
                         stream=None):
     """Step 3.  x0/eps/x_t NHWC fp32 [N,H,W,C]; step int32 [N]; abar fp32 [S+1]."""
@@ -231,7 +266,7 @@ def conv_workspace(c_out, device, n=1, h=1, w=1, block=8):
 
 
 def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None, stream=None,
-                          workspace=None, residual=None):
+                          workspace=None, residual=None, reuse_plan=False):
     """Step 4.  x bf16 NHWC [N,H,W,Cin]; w bf16 [Cout,3,3,Cin]; bias fp32 [Cout] or None;
     y NHWC [N,H,W,Cout] bf16 or fp32 (only listed blocks are written).
     workspace: None = a cached zeroed split-K workspace for this device, False = no split-K,
@@ -250,6 +285,14 @@ def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None,
     if workspace is None:
         workspace = conv_workspace(cout, y.device, n, h, wd, block)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
+    if reuse_plan:
+        _dev(residual, torch.bfloat16, "residual")
+        rc = load().sphinx_sparse_conv3x3_ex(
+            _ptr(x), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y), F32 if y.dtype == torch.float32 else BF16,
+            n, h, wd, cin, cout, int(block), _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes,
+            CONV_REUSE_PLAN, _stream(stream))
+        _chk("sphinx_sparse_conv3x3_ex", rc)
+        return
     if residual is not None:
         _dev(residual, torch.bfloat16, "residual")
         rc = load().sphinx_sparse_conv3x3_residual(

@@ -10,13 +10,9 @@
 
 namespace sphinx {
 
-__global__ void __launch_bounds__(1024) compact_kernel(const uint8_t* __restrict__ mask, int n,
-                                                       int per_frame, const int32_t* __restrict__ k,
-                                                       int u, int select,
-                                                       int32_t* __restrict__ ids,
-                                                       int32_t* __restrict__ count) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void compact_list(const uint8_t* __restrict__ mask, int n, int per_frame,
+                                             const int32_t* __restrict__ k, int u, int select,
+                                             int32_t* __restrict__ ids, int32_t* __restrict__ count) {
   __shared__ int warp_off[32];
   __shared__ int round_total;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -59,6 +55,30 @@ __global__ void __launch_bounds__(1024) compact_kernel(const uint8_t* __restrict
   if (threadIdx.x == 0) *count = base;
 }
 
+__global__ void __launch_bounds__(1024) compact_kernel(const uint8_t* __restrict__ mask, int n,
+                                                       int per_frame, const int32_t* __restrict__ k,
+                                                       int u, int select,
+                                                       int32_t* __restrict__ ids,
+                                                       int32_t* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
+  compact_list(mask, n, per_frame, k, u, select, ids, count);
+}
+
+struct CompactJobs {
+  sphinx_compact_job j[SPHINX_MAX_COMPACT_JOBS];
+};
+
+// Several independent lists (e.g. the UNet levels and the inactive-frame list of one step) in
+// ONE launch: CTA b compacts job b (each list is still one CTA, order = flat id).
+__global__ void __launch_bounds__(1024) compact_batch_kernel(const __grid_constant__ CompactJobs jobs) {
+  pdl_wait();
+  pdl_trigger();
+  const sphinx_compact_job& jb = jobs.j[blockIdx.x];
+  compact_list(jb.block_mask, jb.n, jb.hb * jb.wb, jb.start_step, jb.step_u, (int)jb.select, jb.block_ids,
+               jb.count);
+}
+
 }  // namespace sphinx
 
 using namespace sphinx;
@@ -80,6 +100,29 @@ extern "C" sphinx_status sphinx_compact_blocks(const uint8_t* block_mask, int32_
   cudaError_t e = launch_k(compact_kernel, dim3(1), dim3(1024), 0,
                            reinterpret_cast<cudaStream_t>(stream), block_mask, (int)n, (int)(hb * wb),
                            start_step, (int)step_u, (int)select, block_ids, count);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return SPHINX_OK;
+}
+
+extern "C" sphinx_status sphinx_compact_blocks_batch(const sphinx_compact_job* jobs, int32_t n_jobs,
+                                                     sphinx_stream_t stream) {
+  if (!jobs || n_jobs <= 0 || n_jobs > SPHINX_MAX_COMPACT_JOBS) return SPHINX_ERR_INVALID_ARGUMENT;
+  CompactJobs cj;
+  for (int i = 0; i < n_jobs; ++i) {
+    const sphinx_compact_job& jb = jobs[i];
+    if (!jb.block_ids || !jb.count || jb.n <= 0 || jb.hb <= 0 || jb.wb <= 0) return SPHINX_ERR_INVALID_ARGUMENT;
+    if (jb.select != SPHINX_SELECT_ACTIVE && jb.select != SPHINX_SELECT_INACTIVE_FRAMES &&
+        jb.select != SPHINX_SELECT_ALL)
+      return SPHINX_ERR_INVALID_ARGUMENT;
+    if (jb.select == SPHINX_SELECT_ACTIVE && !jb.block_mask) return SPHINX_ERR_INVALID_ARGUMENT;
+    if (jb.select == SPHINX_SELECT_INACTIVE_FRAMES && !jb.start_step) return SPHINX_ERR_INVALID_ARGUMENT;
+    if ((int64_t)jb.n * jb.hb * jb.wb > (int64_t)1 << 30) return SPHINX_ERR_UNSUPPORTED;
+    cj.j[i] = jb;
+  }
+  sphinx_status st = check_device();
+  if (st != SPHINX_OK) return st;
+  cudaError_t e = launch_k(compact_batch_kernel, dim3(n_jobs), dim3(1024), 0,
+                           reinterpret_cast<cudaStream_t>(stream), cj);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }

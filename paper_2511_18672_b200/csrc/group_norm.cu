@@ -474,8 +474,9 @@ extern "C" sphinx_status sphinx_sparse_resblock(
   if ((st = sphinx_gn_silu(h_buf, h_stats, gn2_gamma, gn2_beta, eps, n, h, w, c, groups, block,
                            block_ids, count, capacity, a_scratch, stream)) != SPHINX_OK)
     return st;
-  // (6) y = x + conv2(a) + b2 on listed pixels (identity skip fused in the epilogue)
-  return sphinx_sparse_conv3x3_residual(a_scratch, w2, b2, x, y, y_dtype, n, h, w, c, c, block,
-                                        block_ids, count, capacity, workspace, workspace_bytes,
-                                        stream);
+  // (6) y = x + conv2(a) + b2 on listed pixels (identity skip fused in the epilogue); same list
+  // and workspace as conv1, so its edge plan is reused
+  return sphinx_sparse_conv3x3_ex(a_scratch, w2, b2, x, y, y_dtype, n, h, w, c, c, block, block_ids,
+                                  count, capacity, workspace, workspace_bytes, SPHINX_CONV_REUSE_PLAN,
+                                  stream);
 }

@@ -1362,7 +1362,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
                                int32_t c_in, int32_t c_out, int32_t block, const int32_t* block_ids,
                                const int32_t* count, int32_t capacity, void* workspace,
                                size_t workspace_bytes, sphinx_stream_t stream, int taps = 9,
-                               const float2* norm_tab = nullptr) {
+                               const float2* norm_tab = nullptr, int flags = 0) {
   if (!x || !w || !y || !block_ids || !count) return SPHINX_ERR_INVALID_ARGUMENT;
   if (residual && (residual == x || !aligned16(residual))) return SPHINX_ERR_INVALID_ARGUMENT;
   if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 255u)) return SPHINX_ERR_INVALID_ARGUMENT;
@@ -1502,7 +1502,9 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   const long long want = p.ws_part ? max_tiles * 16 : max_tiles;  // split-K may multiply units
   const int grid = cg * (int)(want < max_clusters ? want : max_clusters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (p.plan_ids) {
+  // SPHINX_CONV_REUSE_PLAN: the workspace already holds the edge plan of this very list (the
+  // caller's previous conv on this stream used the same list and workspace): skip the plan launch
+  if (p.plan_ids && !(flags & SPHINX_CONV_REUSE_PLAN)) {
     cudaError_t e = launch_k(conv_plan_kernel, dim3(1), dim3(1024), 0, s, block_ids, count, hb, wb,
                              (int)(p.rb != 0), (int)(p.cr != 0), const_cast<int32_t*>(p.plan_ids),
                              const_cast<int32_t*>(p.plan_meta));
@@ -1545,6 +1547,16 @@ extern "C" sphinx_status sphinx_sparse_pointwise(
     void* workspace, size_t workspace_bytes, sphinx_stream_t stream) {
   return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
                    capacity, workspace, workspace_bytes, stream, 1);
+}
+
+extern "C" sphinx_status sphinx_sparse_conv3x3_ex(
+    const void* x, const void* w, const float* bias, const void* residual, void* y,
+    sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, int32_t flags, sphinx_stream_t stream) {
+  if (flags & ~SPHINX_CONV_REUSE_PLAN) return SPHINX_ERR_INVALID_ARGUMENT;
+  return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
+                   capacity, workspace, workspace_bytes, stream, 9, nullptr, (int)flags);
 }
 
 extern "C" sphinx_status sphinx_sparse_conv3x3_gn_silu(

@@ -430,3 +430,39 @@ def test_uncertainty_map_degenerate_and_semantics(sphinx):
     masks, counts, _ = gpu_block_mask(sphinx, O, U.cpu().numpy(), tau.cpu().numpy(), 0.5, 1, 8, 1)
     want, _ = oracle.block_mask(O, U.cpu().numpy(), tau.cpu().numpy(), 0.5, 1, 8, 1)
     assert np.array_equal(masks[0], want[0])
+
+
+def test_compact_batch_equals_single_calls(sphinx):
+    """sphinx_compact_blocks_batch (one launch, one CTA per list) = the single calls, bit for bit."""
+    rg = np.random.default_rng(5)
+    jobs, want = [], []
+    for (n, hb, wb, sel) in [(21, 9, 9, 0), (21, 5, 5, 0), (21, 3, 3, 0), (21, 9, 9, 1), (3, 4, 7, 2)]:
+        m = (rg.random((n, hb, wb)) < 0.3).astype(np.uint8)
+        k = rg.integers(-1, 45, n).astype(np.int32)
+        ids = torch.full((n * hb * wb,), -3, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        jobs.append(dict(block_mask=T(m), start_step=T(k, torch.int32), step_u=25, select=sel, block_ids=ids,
+                         count=cnt))
+        want.append(oracle.compact(m, k, 25, sel))
+    sphinx.sphinx_compact_blocks_batch(jobs)
+    torch.cuda.synchronize()
+    for jb, w in zip(jobs, want):
+        c = int(jb["count"].item())
+        assert np.array_equal(jb["block_ids"][:c].cpu().numpy(), w)
+
+
+def test_conv_reuse_plan(sphinx):
+    """SPHINX_CONV_REUSE_PLAN: a second conv over the same list/workspace (edge-class maps) that
+    skips the plan launch gives bit-identical output to a conv that recomputes it."""
+    n, h, c, b = 3, 36, 64, 8
+    x = bf16(syn.features_bf16((n, h, h, c), "reuse"))
+    w = bf16(syn.weights_bf16(c, c, "reuse"))
+    m = (np.random.default_rng(2).random((n, 5, 5)) < 0.5).astype(np.uint8)
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, None, 0)
+    ws = torch.zeros(sphinx.load().sphinx_conv_workspace_size(n, h, h, c, c, b), dtype=torch.uint8, device=dev)
+    y0 = torch.zeros((n, h, h, c), device=dev)
+    y1 = torch.zeros((n, h, h, c), device=dev)
+    sphinx.sphinx_sparse_conv3x3(x, w, None, y0, b, g_ids, g_cnt, workspace=ws)
+    sphinx.sphinx_sparse_conv3x3(x, w, None, y1, b, g_ids, g_cnt, workspace=ws, reuse_plan=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(y0.cpu().numpy().view(np.uint32), y1.cpu().numpy().view(np.uint32))
