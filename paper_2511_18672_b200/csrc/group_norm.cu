@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kGnThreads) gn_finalize_kernel(const float2* _
 // once per unit into registers, then up to 8 predicated 16-byte loads are in flight.
 // (Measured: a flat one-vector-per-thread variant is 1.4-2x slower here: per-element
 // parameter loads and empty CTAs past the device count.)
-__global__ void __launch_bounds__(kGnThreads, 2) gn_silu_kernel(
+__global__ void __launch_bounds__(kGnThreads, 4) gn_silu_kernel(
     const __nv_bfloat16* __restrict__ x, const float2* __restrict__ fstats,
     const float* __restrict__ gamma, const float* __restrict__ beta, const GnGeom g,
     const int32_t* __restrict__ ids, const int32_t* __restrict__ count, __nv_bfloat16* a) {
@@ -249,18 +249,18 @@ __global__ void __launch_bounds__(kGnThreads, 2) gn_silu_kernel(
     __nv_bfloat16* ab = a + (((size_t)n * g.h + y0) * g.w + x0) * g.c + c0;
     const float inv_rw = 1.f / (float)rw;  // exact floor((pp + 0.5) / rw) for pp < 2^20
     const uint32_t row_stride = (uint32_t)g.w * g.c;
-    for (int p0 = r0; p0 < np; p0 += 8 * R) {
-      uint4 raw[8];
-      uint32_t off[8];
+    for (int p0 = r0; p0 < np; p0 += 4 * R) {
+      uint4 raw[4];
+      uint32_t off[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < 4; ++q) {
         const int pp = p0 + q * R;
         const int py = __float2int_rz(((float)pp + 0.5f) * inv_rw), px = pp - py * rw;
         off[q] = (uint32_t)py * row_stride + (uint32_t)px * g.c;
         if (pp < np) raw[q] = __ldg(reinterpret_cast<const uint4*>(xb + off[q]));
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < 4; ++q) {
         if (p0 + q * R >= np) continue;
         float f[8];
         unpack8(raw[q], f);
@@ -301,7 +301,7 @@ static GnGeom gn_geom(int h, int w, int c, int G, int b) {
   g.R = kGnThreads / g.V;
   g.nslice = c / g.S;
   // ring rows per gn_silu unit: about 8 16-byte loads per thread in one batch
-  g.rg = max(1, min(b + 2, (8 * g.R) / (b + 2)));
+  g.rg = max(1, min(b + 2, (4 * g.R) / (b + 2)));
   g.nrg = cdiv(b + 2, g.rg);
   return g;
 }
