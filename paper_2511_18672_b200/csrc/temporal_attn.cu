@@ -119,16 +119,19 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
   const int c = g.c, c3 = 3 * c, T = g.T;
   const size_t plane = (size_t)g.h * g.w;
   const int units = g.n_seq * g.hb * g.wb * g.b * g.b;
-  // one elected thread stages the pixel's T tokens (q|k|v rows, contiguous per frame) with T bulk
-  // async copies onto an mbarrier.  (Measured alternatives: k|v of all frames + q of listed frames
-  // only -- more, smaller copies -- and 16-byte cp.async by all threads were both 1.3x slower.)
+  // warp 0 stages the pixel's T tokens (q|k|v rows, contiguous per frame) with T bulk async copies
+  // onto an mbarrier, lane m issuing frame m's copy (one issuing thread was TMA-op-rate bound:
+  // ~T ops back to back per pixel).  Lane 0 posts the expected bytes before any copy is issued.
+  // (Measured alternatives: k|v of all frames + q of listed frames only -- more, smaller copies
+  // -- and 16-byte cp.async by all threads were both 1.3x slower.)
   const uint32_t tok_bytes = (uint32_t)c3 * 2;
   auto stage = [&](int buf, int s, size_t pix) {
-    if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)T);
-      uint8_t* dst = rows + (size_t)buf * T * g.rs;
-      for (int m = 0; m < T; ++m)
-        bulk_g2s(dst + (size_t)m * g.rs, qkv + (((size_t)s * T + m) * plane + pix) * c3, tok_bytes, &bars[buf]);
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)T);
+      __syncwarp();
+      if (lane < T)
+        bulk_g2s(rows + (size_t)buf * T * g.rs + (size_t)lane * g.rs,
+                 qkv + (((size_t)s * T + lane) * plane + pix) * c3, tok_bytes, &bars[buf]);
     }
   };
   uint32_t M;
