@@ -281,6 +281,48 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0
     return out
 
 
+def dense_step(torch, st, flush, reps):
+    """configs[4]'s comparison: the same step done densely -- the six convs over every pixel
+    (cuDNN via torch conv2d, channels_last bf16, fp32 accumulate) plus dense noise on the whole
+    latent -- as a CUDA graph, same cold-L2 protocol as the sparse step."""
+    d = st.d
+    xs = [d[f"feat{l}"].permute(0, 3, 1, 2) for l in range(3)]
+    ws = [[d[f"w{l}{j}"].permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
+           for j in range(CONVS_PER_LEVEL)] for l in range(3)]
+    bs = [[d[f"b{l}{j}"].to(torch.bfloat16) for j in range(CONVS_PER_LEVEL)] for l in range(3)]
+    ab = d["abar"][U_STEP]
+    a, sgm = ab.sqrt(), (1 - ab).sqrt()
+
+    def run():
+        zt = a * d["x0"] + sgm * d["eps"]
+        outs = [zt]
+        for l in range(3):
+            src = xs[l]
+            for j in range(CONVS_PER_LEVEL):
+                src = torch.nn.functional.conv2d(src, ws[l][j], bs[l][j], padding=1)
+            outs.append(src)
+        return outs
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run()
+    ts = []
+    for _ in range(max(reps, 3)):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.mean(ts)
+    dense_flops = sum(N_FRAMES * h * h * 2 * 9 * c * c * CONVS_PER_LEVEL for (h, c) in LEVELS)
+    return {"ms": round(ms, 5), "dense_tflops": round(dense_flops / (ms * 1e-3) / 1e12, 1),
+            "what": "6 dense convs (cuDNN, channels_last bf16) + dense noise, CUDA graph, L2 flushed"}
+
+
 def capture_step(torch, st, with_conv_events):
     """Captures one step into a CUDA graph (launch-bound chain of ~15 kernels).  Conv launches
     are bracketed by external event-record nodes so their device time is measured inside the
@@ -563,6 +605,7 @@ def run_gpu(args):
         d = st.d
         iso.append(round(graph_time(torch, lambda: st.sp.sphinx_sparse_conv3x3(
             d[f"feat{l}"], d[f"w{l}0"], d[f"b{l}0"], st.y[l], B, st.ids[l], st.cnt[l])), 5))
+    dense = dense_step(torch, st, flush, reps) if rank == 0 else None
     e2e = None if args.no_e2e else run_e2e(torch, st, g, req, dev, args, flops)
     sweep = None
     if rank == 0 and not args.no_sweep:
@@ -598,6 +641,7 @@ def run_gpu(args):
                          "conv_share_of_step": round(conv_total_ms / ms_all, 4)},
             "conv_levels": per_level,
             "conv_isolated_ms": iso,
+            "dense_step": (dict(dense, speedup_of_step=round(dense["ms"] / ms_all, 3)) if dense else None),
             "memory_kernels": mem,
             "resblock (NEXT-3)": rblk,
             "temporal_attention (NEXT-4)": tblk,
