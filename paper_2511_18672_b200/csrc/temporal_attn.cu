@@ -73,26 +73,29 @@ __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w 
 
 struct TaGeom {
   int h, w, c, heads, T, b, hb, wb, n_seq, nbuf;
-  uint32_t rs;  // staged token row stride in bytes: 6c + 16 (an odd number of 16-byte units)
+  int ppu;      // pixels per unit: 2 = two x-adjacent pixels share one bulk copy per frame
+  uint32_t rs;  // staged frame row stride in bytes: ppu*6c + 16 (an odd number of 16-byte units)
   float scale;
 };
 
-// Next unit (sequence, block position, pixel) at or after u, stepping by `step`, whose pixel is
-// inside the image and whose position has a listed frame; -1 if none.
+// Next unit (sequence, block position, group of ppu x-adjacent pixels) at or after u, stepping
+// by `step`, whose first pixel is inside the image and whose position has a listed frame; -1 if
+// none.  npx = pixels of the group inside the image.
 __device__ __forceinline__ int ta_next(int u, int step, int units,
-                                             const uint32_t* __restrict__ posmask, const TaGeom& g,
-                                             uint32_t& M, size_t& pix, int& s) {
-  const int nblk = g.hb * g.wb, bb = g.b * g.b;
+                                       const uint32_t* __restrict__ posmask, const TaGeom& g,
+                                       uint32_t& M, size_t& pix, int& s, int& npx) {
+  const int nblk = g.hb * g.wb, bbu = g.b * g.b / g.ppu;
   for (; u < units; u += step) {
-    s = u / (nblk * bb);
-    const int r = u - s * nblk * bb;
-    const int pos = r / bb, px = r - pos * bb;
+    s = u / (nblk * bbu);
+    const int r = u - s * nblk * bbu;
+    const int pos = r / bbu, px = (r - pos * bbu) * g.ppu;
     M = __ldg(posmask + s * nblk + pos);
     if (M == 0u) continue;
     const int by = pos / g.wb, bx = pos - by * g.wb;
     const int yy = by * g.b + px / g.b, xx = bx * g.b + px % g.b;
     if (yy >= g.h || xx >= g.w) continue;
     pix = (size_t)yy * g.w + xx;
+    npx = (g.ppu == 2 && xx + 1 < g.w) ? 2 : 1;
     return u;
   }
   return -1;
@@ -118,44 +121,47 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
   pdl_trigger();
   const int c = g.c, c3 = 3 * c, T = g.T;
   const size_t plane = (size_t)g.h * g.w;
-  const int units = g.n_seq * g.hb * g.wb * g.b * g.b;
+  const int units = g.n_seq * g.hb * g.wb * g.b * g.b / g.ppu;
   // warp 0 stages the pixel's T tokens (q|k|v rows, contiguous per frame) with T bulk async copies
   // onto an mbarrier, lane m issuing frame m's copy (one issuing thread was TMA-op-rate bound:
   // ~T ops back to back per pixel).  Lane 0 posts the expected bytes before any copy is issued.
   // (Measured alternatives: k|v of all frames + q of listed frames only -- more, smaller copies
   // -- and 16-byte cp.async by all threads were both 1.3x slower.)
   const uint32_t tok_bytes = (uint32_t)c3 * 2;
-  auto stage = [&](int buf, int s, size_t pix) {
+  auto stage = [&](int buf, int s, size_t pix, int npx) {
     if (warp == 0) {
-      if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)T);
+      if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)(T * npx));
       __syncwarp();
       if (lane < T)
         bulk_g2s(rows + (size_t)buf * T * g.rs + (size_t)lane * g.rs,
-                 qkv + (((size_t)s * T + lane) * plane + pix) * c3, tok_bytes, &bars[buf]);
+                 qkv + (((size_t)s * T + lane) * plane + pix) * c3, tok_bytes * (uint32_t)npx, &bars[buf]);
     }
   };
   uint32_t M;
   size_t pix;
-  int s;
-  int u = ta_next(blockIdx.x, gridDim.x, units, posmask, g, M, pix, s);
-  if (u >= 0) stage(0, s, pix);
+  int s, npx;
+  int u = ta_next(blockIdx.x, gridDim.x, units, posmask, g, M, pix, s, npx);
+  if (u >= 0) stage(0, s, pix, npx);
   uint32_t phase = 0u;  // bit k = parity of buffer k
   int buf = 0;
   while (u >= 0) {
     uint32_t Mn;
     size_t pixn;
-    int sn;
-    const int un = ta_next(u + gridDim.x, gridDim.x, units, posmask, g, Mn, pixn, sn);
-    if (un >= 0 && g.nbuf == 2) stage(buf ^ 1, sn, pixn);  // prefetch (that buffer is free)
+    int sn, npxn;
+    const int un = ta_next(u + gridDim.x, gridDim.x, units, posmask, g, Mn, pixn, sn, npxn);
+    if (un >= 0 && g.nbuf == 2) stage(buf ^ 1, sn, pixn, npxn);  // prefetch (that buffer is free)
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
     phase ^= 1u << buf;
-    const uint32_t tk = smem_u32(rows + (size_t)buf * T * g.rs);
+    const uint32_t tk0 = smem_u32(rows + (size_t)buf * T * g.rs);
     const int nq = __popc(M);
     const int mtiles = (nq + 15) >> 4;
     const int gq = lane >> 2, tq = lane & 3;        // mma fragment row group / thread-in-group
     const int mi = lane >> 3, ri = lane & 7;        // ldmatrix: matrix index / row within it
     const int NT = (T + 7) >> 3;                    // key tiles of 8 (<= 4)
-    for (int task = warp; task < g.heads * mtiles; task += kTaThreads / 32) {
+    const int ntask = g.heads * mtiles;
+    for (int task2 = warp; task2 < npx * ntask; task2 += kTaThreads / 32) {
+      const int pp = task2 / ntask, task = task2 - pp * ntask;  // pixel of the group, (head, m-tile)
+      const uint32_t tk = tk0 + (uint32_t)(pp * 6 * c);
       const int hd = task % g.heads, mt = task / g.heads;
       // ---- S = Q K^T on the tensor cores (bf16 products exact, fp32 accumulation)
       float S[4][4];
@@ -254,27 +260,27 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
       const float inv0 = 1.f / sum0, inv1 = 1.f / sum1;
       const int q0 = mt * 16 + gq, q1 = q0 + 8;
       if (q0 < nq) {
-        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q0 + 1)) * plane + pix) * c + hd * kHeadDim + 2 * tq;
+        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q0 + 1)) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][0] * inv0, O[j][1] * inv0);
       }
       if (q1 < nq) {
-        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q1 + 1)) * plane + pix) * c + hd * kHeadDim + 2 * tq;
+        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q1 + 1)) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][2] * inv1, O[j][3] * inv1);
       }
     }
     __syncthreads();  // every warp is done with this buffer before it is staged again
-    if (un >= 0 && g.nbuf == 1) stage(0, sn, pixn);
+    if (un >= 0 && g.nbuf == 1) stage(0, sn, pixn, npxn);
     if (g.nbuf == 2) buf ^= 1;
-    u = un; M = Mn; pix = pixn; s = sn;
+    u = un; M = Mn; pix = pixn; s = sn; npx = npxn;
   }
 }
 
-static size_t ta_row(int c) { return (size_t)6 * c + 16; }
-static size_t ta_smem(int c, int T, int nbuf) { return 128 + (size_t)nbuf * T * ta_row(c); }
+static size_t ta_row(int c, int ppu = 1) { return (size_t)ppu * 6 * c + 16; }
+static size_t ta_smem(int c, int T, int nbuf, int ppu = 1) { return 128 + (size_t)nbuf * T * ta_row(c, ppu); }
 
 }  // namespace sphinx
 
@@ -318,14 +324,19 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   TaGeom g;
   g.h = h; g.w = w; g.c = c; g.heads = heads; g.T = T; g.b = block; g.hb = hb; g.wb = wb;
   g.n_seq = n_seq;
-  g.rs = (uint32_t)ta_row(c);
   g.scale = 1.f / sqrtf((float)kHeadDim);
-  // double-buffer the staged tokens (prefetch the next pixel during this one) when two fit
+  // One pixel per unit, double-buffered when two buffers fit (prefetch the next unit during this
+  // one).  SPHINX_TA_PPU=2 stages two x-adjacent pixels per unit with one bulk copy per frame:
+  // measured slower at level 0 (90 vs 65 us: the larger buffers halve the resident CTAs).
+  g.ppu = 1;
   g.nbuf = ta_smem(c, T, 2) <= 200 * 1024 ? 2 : 1;
-  const size_t smem = ta_smem(c, T, g.nbuf);
+  if (const char* env = getenv("SPHINX_TA_PPU"))
+    if (atoi(env) == 2 && block % 2 == 0 && ta_smem(c, T, g.nbuf, 2) <= 227 * 1024) g.ppu = 2;
+  g.rs = (uint32_t)ta_row(c, g.ppu);
+  const size_t smem = ta_smem(c, T, g.nbuf, g.ppu);
   e = cudaFuncSetAttribute(ta_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return cuda_fail(e);
-  const long long units = (long long)n_seq * hb * wb * block * block;
+  const long long units = (long long)n_seq * hb * wb * block * block / g.ppu;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
   per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
   const long long cap = (long long)sms * per_sm;

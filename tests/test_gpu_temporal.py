@@ -270,3 +270,25 @@ def test_temporal_block_full_size_bench_config(sphinx):
     tol = 2 * half_ulp(o["o_pre"]) + E_o + 2.0 ** -23 * np.abs(o["y"]) + 1e-7
     err = np.abs(tb.y.cpu().numpy().astype(np.float64) - o["y"])
     assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
+
+
+def test_temporal_block_two_pixel_units(sphinx, monkeypatch):
+    """The SPHINX_TA_PPU=2 staging variant (two x-adjacent pixels per bulk copy) on an odd-width
+    map (ragged last pair) equals the oracle like the default path."""
+    monkeypatch.setenv("SPHINX_TA_PPU", "2")
+    n, h, w, c, T, b = 4, 16, 13, 64, 2, 8
+    x = syn.resblock_features_bf16((n, h, w, c), "tbppu")
+    qkv_cache = syn.resblock_features_bf16((n, h, w, 3 * c), "tbppu-qc")
+    y_cache = dec(syn.features_bf16((n, h, w, c), "tbppu-yc"))
+    params = identity_params(c)
+    mask = block_mask(n, h, w, b, 0.6, "scattered", "tbppu")
+    tb = TB(sphinx, n, h, w, c, 1, T, b, qkv_cache, y_cache)
+    ids, cnt = gpu_ids(sphinx, mask)
+    tb.run(x, params, ids, cnt)
+    torch.cuda.synchronize()
+    o = oracle.temporal_attn(x, qkv_cache, y_cache, *params, 1, T, b, oracle.compact(mask))
+    L = listed_px(mask, h, w, b)
+    E_o = attn_tol(o, 1, T, c)
+    tol = 2 * half_ulp(o["o_pre"]) + E_o + 2.0 ** -23 * np.abs(o["y"]) + 1e-7
+    err = np.abs(tb.y.cpu().numpy().astype(np.float64) - o["y"])
+    assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
