@@ -325,11 +325,14 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   g.h = h; g.w = w; g.c = c; g.heads = heads; g.T = T; g.b = block; g.hb = hb; g.wb = wb;
   g.n_seq = n_seq;
   g.scale = 1.f / sqrtf((float)kHeadDim);
-  // One pixel per unit, double-buffered when two buffers fit (prefetch the next unit during this
-  // one).  SPHINX_TA_PPU=2 stages two x-adjacent pixels per unit with one bulk copy per frame:
+  // One pixel per unit, double-buffered (prefetch the next unit during this one) when that still
+  // leaves two resident CTAs per SM; otherwise two single-buffered CTAs are faster (measured:
+  // level 0 66 us double-buffered vs 84 single; level 1 56 double (1 CTA/SM) vs 42 single (2)).
+  // SPHINX_TA_PPU=2 stages two x-adjacent pixels per unit with one bulk copy per frame:
   // measured slower at level 0 (90 vs 65 us: the larger buffers halve the resident CTAs).
   g.ppu = 1;
-  g.nbuf = ta_smem(c, T, 2) <= 200 * 1024 ? 2 : 1;
+  g.nbuf = ta_smem(c, T, 2) <= 113 * 1024 ? 2 : 1;
+  if (const char* env = getenv("SPHINX_TA_NBUF")) g.nbuf = atoi(env) == 1 ? 1 : g.nbuf;
   if (const char* env = getenv("SPHINX_TA_PPU"))
     if (atoi(env) == 2 && block % 2 == 0 && ta_smem(c, T, g.nbuf, 2) <= 227 * 1024) g.ppu = 2;
   g.rs = (uint32_t)ta_row(c, g.ppu);
