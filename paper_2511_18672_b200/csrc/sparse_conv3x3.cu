@@ -43,6 +43,9 @@ constexpr int kAWarp = 6;  // halo mode: the halo (A) producer warp when the pro
 constexpr int kXWarp = 7;   // NORM (fused GroupNorm+SiLU) kernels: first transform warp
 constexpr int kXThreads = 256;  // transform threads (8 warps)
 constexpr int kThreadsNorm = kThreads + kXThreads;
+// non-NORM kernels: 4 more epilogue warps (7..10) split the accumulator columns with warps 2..5
+// (same TMEM lane quarters, warp & 3), halving the TMEM drain and the split-K park / reduce
+constexpr int kThreadsEpi8 = kThreads + 128;
 
 #ifdef SPHINX_TRACE
 // Dev-only timeline trace (libsphinx_trace.so): globaltimer stamps per CTA of one launch.
@@ -389,7 +392,7 @@ __device__ __forceinline__ HaloTile halo_tile(int mt, int rank, int nF, int nB, 
 //   multicast to both CTAs' barriers; each CTA's epilogue drains its own TMEM lanes and
 //   arrives on the leader's accumulator-empty barrier.  B traffic per SM halves.
 template <int BN, int CG, int BLK, bool HALO, bool EDGE, bool NORM>
-__global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
+__global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
     sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
       for (int s = 0; s < Cfg::kANum; ++s) mbar_init(&landed[s], 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * CG);
+      mbar_init(&tempty[a], (NORM ? 4 : 8) * CG);
     }
     mbar_init(&red_bar[0], 1);
     mbar_init(&red_bar[1], 1);
@@ -820,10 +823,13 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
         }
       }
     }
-  } else if (warp < kAWarp) {
-    // ===================== epilogue (warps 2..5, both CTAs) =====================
+  } else if (warp < kAWarp || (!NORM && warp >= kXWarp)) {
+    // ============ epilogue (warps 2..5, and 7..10 for non-NORM kernels; both CTAs) ============
+    constexpr int kEpiW = NORM ? 4 : 8, kEpiT = kEpiW * 32, kHalves = kEpiW / 4;
+    const int half = warp >= kXWarp ? 1 : 0;  // which half of the 32-column chunks this warp drains
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
+    const int erow = half * kBM + row;  // epilogue thread index
     int acc = 0;
     uint32_t acc_phase = 0;
     SegIter it = it0;
@@ -873,8 +879,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
         // the previous tile's barrier below)
         float* sb = s_bias + acc * 256;
         const int nb = p.bias ? min(BN, p.cout - nt * BN) : 0;
-        for (int c = row; c < BN; c += kBM) sb[c] = c < nb ? __ldg(p.bias + nt * BN + c) : 0.f;
-        named_bar_sync(1, 128);
+        for (int c = erow; c < BN; c += kEpiT) sb[c] = c < nb ? __ldg(p.bias + nt * BN + c) : 0.f;
+        named_bar_sync(1, kEpiT);
       }
       const float* sbt = s_bias + acc * 256;
       mbar_wait(&tfull[acc], acc_phase);
@@ -886,6 +892,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
       }
 #endif
       if (sg.role == kOwner) {
+       if (half == 0) {  // the owner reduction runs on warps 2..5 (barrier 3, 128 threads)
         // ---- stream-K owner: wait for the parts of tile t, then add them chunk by chunk
         const int c_last = sk_cluster_of((long long)(t + 1) * p.kc - 1, Wk, n_clusters);
         const int n_parts = c_last - cluster_id;
@@ -898,7 +905,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
           } while (seen < n_parts);
           fence_proxy_async_global();
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(3, 128);
         float* stage_buf = reinterpret_cast<float*>(sA);  // the operand ring is idle now
         const uint32_t chunk_bytes = 32u * kBM * 4u;          // 32 columns x 128 rows, fp32
         auto stage_chunk = [&](int c0, int buf) {             // issued by row 0 only
@@ -928,12 +935,13 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
             for (int i = 0; i < 32; ++i) v[i] += src[i * kBM];  // lanes = consecutive rows
           }
           if (valid) store_row_chunk(p, pix, nt * BN + c0, v, sbt + c0);
-          named_bar_sync(1, 128);  // every thread done with buf before it is refilled
+          named_bar_sync(3, 128);  // every thread done with buf before it is refilled
         }
         if (row == 0) cnt[0] = 0;  // leave the counter zeroed for the next launch
+       }
       } else {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = half * 32; c0 < BN; c0 += 32 * kHalves) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
           tc_wait_ld();
@@ -972,8 +980,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
       if (sg.role == kPart) {
         // publish this part to the tile's owner (never waits)
         __threadfence();
-        named_bar_sync(1, 128);
-        if (row == 0) {
+        named_bar_sync(1, kEpiT);
+        if (erow == 0) {
           const int owner = sk_cluster_of((long long)t * p.kc, Wk, n_clusters);
           atomicAdd(p.ws_cnt + (owner * CG + rank) * 2, 1);
         }
@@ -983,15 +991,15 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
         // then each reduces a 1/nsplit slice of the rows, summing partials in split order
         // (deterministic), with coalesced float4 loads across the epilogue threads.
         __threadfence();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiT);
 #ifdef SPHINX_TRACE
-        if (row == 0) {
+        if (erow == 0) {
           CONV_TRACE(16, gtimer());
           CONV_TRACE(19, (unsigned long long)ns);
         }
 #endif
         int* arrive = p.ws_cnt + (U.slot * CG + rank) * 2;
-        if (row == 0) {
+        if (erow == 0) {
           atomicAdd(arrive, 1);
           int seen;
           do {
@@ -999,9 +1007,9 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
             if (seen < ns) __nanosleep(64);
           } while (seen < ns);
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiT);
 #ifdef SPHINX_TRACE
-        if (row == 0) CONV_TRACE(17, gtimer());
+        if (erow == 0) CONV_TRACE(17, gtimer());
 #endif
         // this unit reduces output columns [c0s, c1s) (multiples of 8) of all 128 rows: from every
         // part that column range is one contiguous column-major block -> one bulk copy each
@@ -1012,7 +1020,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
         const size_t split_stride = (size_t)CG * kBM * BN;
         float* stage_buf = reinterpret_cast<float*>(sA);  // the operand ring is idle now
         if ((size_t)ns * slice_bytes > (size_t)Cfg::kRingBytes) __trap();  // never at BN <= 256
-        if (row == 0 && ncol > 0) {
+        if (erow == 0 && ncol > 0) {
           fence_proxy_async_global();
           mbar_arrive_expect_tx(red_bar, slice_bytes * (uint32_t)ns);
           for (int s2 = 0; s2 < ns; ++s2)
@@ -1022,7 +1030,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
           mbar_wait(red_bar, 0);
           if (valid) {
             // thread = row (its own pixel); partials summed in split order (deterministic)
-            for (int c = 0; c < ncol; c += 8) {
+            for (int c = half * 8; c < ncol; c += 8 * kHalves) {
               const int co = nt * BN + c0s + c;
               if (co >= p.cout) break;
               float v8[8];
@@ -1056,11 +1064,11 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreads, 1)
           }
         }
         // departure: the last unit to leave re-zeroes both counters for the next launch
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiT);
 #ifdef SPHINX_TRACE
-        if (row == 0) CONV_TRACE(18, gtimer());
+        if (erow == 0) CONV_TRACE(18, gtimer());
 #endif
-        if (row == 0) {
+        if (erow == 0) {
           const int old = atomicAdd(arrive + 1, 1);
           if (old == ns - 1) {
             arrive[0] = 0;
@@ -1280,7 +1288,7 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NORM ? kThreadsNorm : kThreads);
+  cfg.blockDim = dim3(NORM ? kThreadsNorm : kThreadsEpi8);
   cfg.dynamicSmemBytes = Cfg::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
