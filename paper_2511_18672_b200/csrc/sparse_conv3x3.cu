@@ -18,13 +18,17 @@
 //    stage (empty barrier) and, after the last K step, hands the accumulator to the
 //    epilogue.  Two TMEM accumulators (2*BN columns) let the epilogue of tile i
 //    overlap the main loop of tile i+1.
-//  - Epilogue: 4 warps tcgen05.ld their 32 TMEM lanes (= 32 pixels), add bias, and
-//    store straight into the full-resolution NHWC output at each pixel's own
-//    position (the scatter of computed blocks is fused; unlisted pixels untouched).
+//  - Epilogue: 8 warps (two per TMEM lane quarter, alternate 32-column chunks) tcgen05.ld
+//    their 32 TMEM lanes (= 32 pixels), add bias (+ residual), and store straight into the
+//    full-resolution NHWC output at each pixel's own position (the scatter of computed
+//    blocks is fused; unlisted pixels untouched).
 //  - Persistent CTAs (grid = #SMs) walk the tile list in a static stride; the tile
 //    count comes from the device-side block count, so no host synchronisation.
-//  Warp roles (192 threads): w0 TMA producer, w1 TMEM allocator + MMA issuer,
-//  w2..w5 epilogue.
+//  Warp roles (352 threads): w0 weight (B) TMA producer, w6 halo (A) TMA producer (halo
+//  mode), w1 TMEM allocator + MMA issuer, w2..w5 + w7..w10 epilogue.  The fused-GN variant
+//  (NORM) keeps w2..w5 as epilogue and uses w7..w14 as GroupNorm+SiLU transform warps.
+//  (The per-tap / halo / split-K / stream-K / edge-class details are documented inline and in
+//  DESIGN.md section 6.4.)
 #include <cuda.h>
 #include <cuda_bf16.h>
 
