@@ -34,9 +34,14 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 //   ~ 2^-23 E[L^2]; for images in [0,1] the Laplacian of a window with small variance but a
 //   large mean (constant curvature) is itself small, so after min-max normalisation the error
 //   stays ~1e-6 (parity tolerance 1e-4 vs the fp64 two-pass oracle, tests/test_gpu_parity).
+// RV, RS > 0: compile-time radii (the SPEC defaults 3 / 2): the window loops unroll and taps away
+// from the image border skip the clamp (measured ncu: the generic version was issue-bound at 88%
+// SM throughput on index arithmetic).  RV = RS = 0: runtime radii.
+template <int RV, int RS>
 __global__ void __launch_bounds__(256) lapvar_smooth_kernel(const float* __restrict__ rgb, int h, int w,
-                                                            int rv, int rs, float* __restrict__ S_out,
+                                                            int rv_rt, int rs_rt, float* __restrict__ S_out,
                                                             int* __restrict__ minmax) {
+  const int rv = RV > 0 ? RV : rv_rt, rs = RS > 0 ? RS : rs_rt;
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -59,14 +64,33 @@ __global__ void __launch_bounds__(256) lapvar_smooth_kernel(const float* __restr
   const size_t plane = (size_t)h * w;
   const float* img = rgb + (size_t)n * plane * 3;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int a = wid; a < YH; a += nw)
-    for (int c = lane; c < YW; c += 32) {
-      const float* px = img + ((size_t)(yy0 + a) * w + (yx0 + c)) * 3;
-      Ys[a * YW + c] = 0.299f * __ldg(px) + 0.587f * __ldg(px + 1) + 0.114f * __ldg(px + 2);
+  // luminance of the tile + halo: 8 pixels (24 independent loads) in flight per thread (one
+  // pixel per iteration left each warp ~11 serial load latencies: ncu's top stall)
+  {
+    const int ny = YH * YW;
+    for (int e0 = threadIdx.x; e0 < ny; e0 += 8 * 256) {
+      float v[8][3];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = e0 + k * 256;
+        if (e < ny) {
+          const int a = e / YW, c = e - a * YW;
+          const float* px = img + ((size_t)(yy0 + a) * w + (yx0 + c)) * 3;
+          v[k][0] = __ldg(px);
+          v[k][1] = __ldg(px + 1);
+          v[k][2] = __ldg(px + 2);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = e0 + k * 256;
+        if (e < ny) Ys[e] = 0.299f * v[k][0] + 0.587f * v[k][1] + 0.114f * v[k][2];
+      }
     }
+  }
   __syncthreads();
-  for (int a = wid; a < LH; a += nw)
-   for (int c = lane; c < LW; c += 32) {
+  for (int e = threadIdx.x; e < LH * LW; e += blockDim.x) {
+   const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)LW)), c = e - a * LW;
     const int i = a * LW + c;
     const int py = ly0 + a, px = lx0 + c;  // in-image position; neighbours clamped to the image
     const int cy = py - yy0, cx = px - yx0;
@@ -75,48 +99,103 @@ __global__ void __launch_bounds__(256) lapvar_smooth_kernel(const float* __restr
     Ls[i] = Ys[uy * YW + cx] + Ys[dy * YW + cx] + Ys[cy * YW + lx] + Ys[cy * YW + rx] - 4.0f * Ys[cy * YW + cx];
    }
   __syncthreads();
-  for (int a = wid; a < LH; a += nw)  // horizontal window sums of L and L^2
-    for (int c = lane; c < VW; c += 32) {
+  for (int e = threadIdx.x; e < LH * VW; e += blockDim.x) {  // horizontal window sums of L and L^2
+    const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)VW)), c = e - a * VW;
       const int px = vx0 + c;
       float s1 = 0.0f, s2 = 0.0f;
-      for (int d = -rv; d <= rv; ++d) {
-        const float l = Ls[a * LW + min(max(px + d, 0), w - 1) - lx0];
-        s1 += l;
-        s2 = fmaf(l, l, s2);
+      if (px - rv >= 0 && px + rv < w) {
+        const float* lr = Ls + a * LW + (px - lx0);
+        if constexpr (RV > 0) {
+#pragma unroll
+          for (int d = -RV; d <= RV; ++d) {
+            const float l = lr[d];
+            s1 += l;
+            s2 = fmaf(l, l, s2);
+          }
+        } else {
+          for (int d = -rv; d <= rv; ++d) {
+            const float l = lr[d];
+            s1 += l;
+            s2 = fmaf(l, l, s2);
+          }
+        }
+      } else {
+        for (int d = -rv; d <= rv; ++d) {
+          const float l = Ls[a * LW + min(max(px + d, 0), w - 1) - lx0];
+          s1 += l;
+          s2 = fmaf(l, l, s2);
+        }
       }
       R1[a * VW + c] = s1;
       R2[a * VW + c] = s2;
     }
   __syncthreads();
   const float inv_cnt = 1.0f / (float)((2 * rv + 1) * (2 * rv + 1));
-  for (int a = wid; a < VH; a += nw)  // vertical window sums -> variance
-    for (int c = lane; c < VW; c += 32) {
+  for (int e = threadIdx.x; e < VH * VW; e += blockDim.x) {  // vertical window sums -> variance
+    const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)VW)), c = e - a * VW;
       const int py = vy0 + a;
       float s1 = 0.0f, s2 = 0.0f;
-      for (int d = -rv; d <= rv; ++d) {
-        const int r = min(max(py + d, 0), h - 1) - ly0;
-        s1 += R1[r * VW + c];
-        s2 += R2[r * VW + c];
+      if (py - rv >= 0 && py + rv < h) {
+        const float* r1 = R1 + (py - ly0) * VW + c;
+        const float* r2 = R2 + (py - ly0) * VW + c;
+        if constexpr (RV > 0) {
+#pragma unroll
+          for (int d = -RV; d <= RV; ++d) {
+            s1 += r1[d * VW];
+            s2 += r2[d * VW];
+          }
+        } else {
+          for (int d = -rv; d <= rv; ++d) {
+            s1 += r1[d * VW];
+            s2 += r2[d * VW];
+          }
+        }
+      } else {
+        for (int d = -rv; d <= rv; ++d) {
+          const int r = min(max(py + d, 0), h - 1) - ly0;
+          s1 += R1[r * VW + c];
+          s2 += R2[r * VW + c];
+        }
       }
       const float m = s1 * inv_cnt;
       Vs[a * VW + c] = fmaxf(fmaf(-m, m, s2 * inv_cnt), 0.0f);
     }
   __syncthreads();
-  for (int a = wid; a < VH; a += nw)  // box: horizontal sums of V
-    for (int c = lane; c < SW; c += 32) {
+  for (int e = threadIdx.x; e < VH * SW; e += blockDim.x) {  // box: horizontal sums of V
+    const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)SW)), c = e - a * SW;
       const int px = sx0 + c;
       float s1 = 0.0f;
-      for (int d = -rs; d <= rs; ++d) s1 += Vs[a * VW + min(max(px + d, 0), w - 1) - vx0];
+      if (px - rs >= 0 && px + rs < w) {
+        const float* vr = Vs + a * VW + (px - vx0);
+        if constexpr (RS > 0) {
+#pragma unroll
+          for (int d = -RS; d <= RS; ++d) s1 += vr[d];
+        } else {
+          for (int d = -rs; d <= rs; ++d) s1 += vr[d];
+        }
+      } else {
+        for (int d = -rs; d <= rs; ++d) s1 += Vs[a * VW + min(max(px + d, 0), w - 1) - vx0];
+      }
       Ts[a * SW + c] = s1;
     }
   __syncthreads();
   const float inv_box = 1.0f / (float)((2 * rs + 1) * (2 * rs + 1));
   float lo = 3.0e38f, hi = 0.0f;
-  for (int a = wid; a < SH; a += nw)  // box: vertical sums -> S
-   for (int c = lane; c < SW; c += 32) {
+  for (int e = threadIdx.x; e < SH * SW; e += blockDim.x) {  // box: vertical sums -> S
+   const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)SW)), c = e - a * SW;
     const int py = sy0 + a;
     float s1 = 0.0f;
-    for (int d = -rs; d <= rs; ++d) s1 += Ts[(min(max(py + d, 0), h - 1) - vy0) * SW + c];
+    if (py - rs >= 0 && py + rs < h) {
+      const float* tr = Ts + (py - vy0) * SW + c;
+      if constexpr (RS > 0) {
+#pragma unroll
+        for (int d = -RS; d <= RS; ++d) s1 += tr[d * SW];
+      } else {
+        for (int d = -rs; d <= rs; ++d) s1 += tr[d * SW];
+      }
+    } else {
+      for (int d = -rs; d <= rs; ++d) s1 += Ts[(min(max(py + d, 0), h - 1) - vy0) * SW + c];
+    }
     const float sv = s1 * inv_box;
     S_out[(size_t)n * plane + (size_t)py * w + sx0 + c] = sv;
     lo = fminf(lo, sv);
@@ -248,12 +327,15 @@ extern "C" sphinx_status sphinx_uncertainty_map(const float* rgb, int32_t n, int
                       (size_t)(NY * NY + NL * NL + NV * NV + NV * kUT) * sizeof(float);
   static bool attr_set = false;
   if (!attr_set) {
-    e = cudaFuncSetAttribute(lapvar_smooth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    e = cudaFuncSetAttribute(lapvar_smooth_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lapvar_smooth_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return cuda_fail(e);
     attr_set = true;
   }
-  e = launch_k(lapvar_smooth_kernel, dim3(cdiv(w, kUT), cdiv(h, kUT), n), dim3(256), smem, s, rgb,
-               (int)h, (int)w, rv, rs, uncertainty, minmax);
+  e = launch_k((rv == 3 && rs == 2) ? lapvar_smooth_kernel<3, 2> : lapvar_smooth_kernel<0, 0>,
+               dim3(cdiv(w, kUT), cdiv(h, kUT), n), dim3(256), smem, s, rgb, (int)h, (int)w, rv, rs,
+               uncertainty, minmax);
   if (e != cudaSuccess) return cuda_fail(e);
   const int plane = h * w;
   e = launch_k(normalize_hist_kernel, dim3(cdiv(plane, 256 * 8), n), dim3(256), 0, s, uncertainty, plane,
