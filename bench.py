@@ -596,7 +596,7 @@ def run_gpu(args):
     dom_flops = dom["real_px"] * 2 * 9 * LEVELS[dom["level"]][1] ** 2
     achieved = dom_flops / (dom["conv_ms"] * 1e-3) / 1e12
     all_conv_tflops = flops / (conv_total_ms * 1e-3) / 1e12
-    bn_sig = {0: "<160, 2, 8, 1, 0>", 1: "<160, 2, 8, 1, 1>", 2: "<256, 2, 8, 1, 1>"}[dom["level"]]
+    bn_sig = {0: "<160, 2, 8, 1, 0, 0>", 1: "<160, 2, 8, 1, 1, 0>", 2: "<256, 2, 8, 1, 1, 0>"}[dom["level"]]
     traffic, traffic_src = ncu_traffic(bn_sig)
 
     # the same conv calls timed in isolation (graph of 20 back-to-back launches, L2-warm)
