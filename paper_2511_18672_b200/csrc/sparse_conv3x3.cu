@@ -50,6 +50,7 @@ constexpr int kThreadsNorm = kThreads + kXThreads;
 // non-NORM kernels: 4 more epilogue warps (7..10) split the accumulator columns with warps 2..5
 // (same TMEM lane quarters, warp & 3), halving the TMEM drain and the split-K park / reduce
 constexpr int kThreadsEpi8 = kThreads + 128;
+constexpr bool kRaggedDefault = false;  // SPHINX_CONV_RAGGED overrides (A/B)
 
 #ifdef SPHINX_TRACE
 // Dev-only timeline trace (libsphinx_trace.so): globaltimer stamps per CTA of one launch.
@@ -88,6 +89,7 @@ struct ConvParams {
   int kc;         // 64-channel chunks per tap
   int taps;       // 9 = 3x3 conv; 1 = pointwise (1x1) projection (NEXT-4), per-tap path only
   int n_tiles_n;  // tiles along C_out
+  int n_last;     // width of the last C_out tile (== BN unless ragged: e.g. 320 = 256 + 64)
   int bpt;        // blocks per 128-row tile = 128 / b^2
   // split-K workspace (NULL = never split): per-(tile, split) fp32 partial tiles and one
   // arrival counter per (tile, CTA of the pair); counters are zero between launches.
@@ -399,7 +401,8 @@ template <int BN, int CG, int BLK, bool HALO, bool EDGE, bool NORM>
 __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
     sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
-                             const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+                             const __grid_constant__ CUtensorMap tmC,
+                             const __grid_constant__ CUtensorMap tmB2, const ConvParams p) {
   using Cfg = ConvCfg<BN, CG, HALO, EDGE, NORM>;
   static_assert(!NORM || HALO, "the fused GN+SiLU transform works on halo slots");
   static_assert(!EDGE || HALO, "edge packing is a halo-mode feature");
@@ -551,6 +554,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         long long a_seg = -1;  // segment whose blocks are decoded in cx/cy/cn
         long long b_seg = -1;
         int b_n0 = 0;
+        uint32_t b_bytes = Cfg::kStageB;  // this CTA's bytes per (tap, chunk) weight tile
+        const CUtensorMap* b_tm = &tmB;
         HaloTile g{};
         int cx[8], cy[8], cn[8];
         int ahead = 0;  // chunks the A cursor is ahead of the B cursor
@@ -625,7 +630,12 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
           {
             if (cb.it.x != b_seg) {
               b_seg = cb.it.x;
-              b_n0 = (cb.g.t - (cb.g.t / p.n_tiles_n) * p.n_tiles_n) * BN + rank * Cfg::kBNc;
+              const int ntb = cb.g.t - (cb.g.t / p.n_tiles_n) * p.n_tiles_n;
+              // ragged last C_out tile: narrower weight box (second tensor map), fewer bytes
+              const bool nar = ntb == p.n_tiles_n - 1 && p.n_last < BN;
+              b_n0 = ntb * BN + rank * (nar ? p.n_last / CG : Cfg::kBNc);
+              b_bytes = nar ? (uint32_t)(p.n_last / CG) * kBK * 2 : (uint32_t)Cfg::kStageB;
+              b_tm = nar ? &tmB2 : &tmB;
             }
             const int n0 = b_n0;
             for (int tap = 0; tap < 9; ++tap) {
@@ -633,11 +643,11 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
               mbar_wait(&empty[Cfg::kANum + bs], bph ^ 1);
               uint8_t* b_dst = sB + bs * Cfg::kStageB;
               if constexpr (CG == 1) {
-                mbar_arrive_expect_tx(bf, (uint32_t)Cfg::kStageB);
-                tma_load_3d(&tmB, bf, b_dst, cb.kc * kBK, tap, n0, pol_b);
+                mbar_arrive_expect_tx(bf, b_bytes);
+                tma_load_3d(b_tm, bf, b_dst, cb.kc * kBK, tap, n0, pol_b);
               } else {
-                if (rank == 0) mbar_arrive_expect_tx(bf, (uint32_t)(2 * Cfg::kStageB));
-                tma_load_3d_cg2(&tmB, leader_addr(bf), b_dst, cb.kc * kBK, tap, n0, pol_b);
+                if (rank == 0) mbar_arrive_expect_tx(bf, 2 * b_bytes);
+                tma_load_3d_cg2(b_tm, leader_addr(bf), b_dst, cb.kc * kBK, tap, n0, pol_b);
               }
 #ifdef SPHINX_TRACE
               if (!tr_b) {
@@ -675,7 +685,11 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
           cy[i] = by * BLK - 1;
           cx[i] = bx * BLK - 1;
         }
-        const int n0 = nt * BN + rank * Cfg::kBNc;
+        const bool nar = nt == p.n_tiles_n - 1 && p.n_last < BN;
+        const int n0 = nt * BN + rank * (nar ? p.n_last / CG : Cfg::kBNc);
+        const uint32_t stage_bytes = (uint32_t)kStageA + (nar ? (uint32_t)(p.n_last / CG) * kBK * 2
+                                                              : (uint32_t)Cfg::kStageB);
+        const CUtensorMap* b_tm = nar ? &tmB2 : &tmB;
         int tap = ks0 / p.kc, kc = ks0 - (ks0 / p.kc) * p.kc;
         for (int ks = ks0; ks < ks1; ++ks) {
           {
@@ -685,20 +699,20 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
             uint8_t* a_dst = sA + stage * kStageA;
             uint8_t* b_dst = sB + stage * Cfg::kStageB;
             if constexpr (CG == 1) {
-              mbar_arrive_expect_tx(&full[stage], (uint32_t)Cfg::kStageBytes);
+              mbar_arrive_expect_tx(&full[stage], stage_bytes);
 #pragma unroll
               for (int i = 0; i < BPT; ++i)
                 tma_load_4d(&tmA, &full[stage], a_dst + i * bb * 128, kc * kBK, cx[i] + dx,
                             cy[i] + dy, cn[i], pol_a);
-              tma_load_3d(&tmB, &full[stage], b_dst, kc * kBK, tap, n0, pol_b);
+              tma_load_3d(b_tm, &full[stage], b_dst, kc * kBK, tap, n0, pol_b);
             } else {
-              if (rank == 0) mbar_arrive_expect_tx(&full[stage], (uint32_t)(2 * Cfg::kStageBytes));
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
               const uint32_t bar = leader_addr(&full[stage]);
 #pragma unroll
               for (int i = 0; i < BPT; ++i)
                 tma_load_4d_cg2(&tmA, bar, a_dst + i * bb * 128, kc * kBK, cx[i] + dx, cy[i] + dy,
                                 cn[i], pol_a);
-              tma_load_3d_cg2(&tmB, bar, b_dst, kc * kBK, tap, n0, pol_b);
+              tma_load_3d_cg2(b_tm, bar, b_dst, kc * kBK, tap, n0, pol_b);
             }
             if (++stage == S) {
               stage = 0;
@@ -736,6 +750,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
 #endif
           const HaloTile g = halo_tile<CG>(sg.t / p.n_tiles_n, 0, nF, nB, list, nR, p);
           const uint32_t line_stride = (uint32_t)(g.bpt * Cfg::kHaloRow);
+          const bool nar = sg.t % p.n_tiles_n == p.n_tiles_n - 1 && p.n_last < BN;
+          const uint32_t idesc_t = nar ? idesc_bf16_f32(kBM * CG, p.n_last) : idesc;
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -768,8 +784,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
                 const uint64_t ad = umma_desc_sw128(a_start + k * 32, Cfg::kHaloRow, p.desc_bo);
                 const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 1024);
                 const uint32_t accum = (kc != kc0 || tap != 0 || k != 0) ? 1u : 0u;
-                if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc, accum);
-                else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc, accum);
+                if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc_t, accum);
+                else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc_t, accum);
               }
               if constexpr (CG == 1) tc_commit(&empty[Cfg::kANum + bs]);
               else tc_commit_cg2_mc(&empty[Cfg::kANum + bs]);
@@ -798,6 +814,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
       for (int u = cluster_id; u < total; u += n_clusters) {
         const Unit U = decode_unit(u, n_full, nsplit);
         const int ks0 = U.sk * ksteps / U.ns, ks1 = (U.sk + 1) * ksteps / U.ns;
+        const bool nar = U.t % p.n_tiles_n == p.n_tiles_n - 1 && p.n_last < BN;
+        const uint32_t idesc_t = nar ? idesc_bf16_f32(kBM * CG, p.n_last) : idesc;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -811,8 +829,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
             const uint64_t ad = umma_desc_sw128(a_addr + k * 32, 1024);
             const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 1024);
             const uint32_t accum = (ks != ks0 || k != 0) ? 1u : 0u;
-            if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc, accum);
-            else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc, accum);
+            if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc_t, accum);
+            else tc_mma_bf16_cg2(d_tmem, ad, bd, idesc_t, accum);
           }
           if constexpr (CG == 1) tc_commit(&empty[stage]); else tc_commit_cg2_mc(&empty[stage]);
           if (++stage == S) {
@@ -945,7 +963,10 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
        }
       } else {
 #pragma unroll 1
-        for (int c0 = half * 32; c0 < BN; c0 += 32 * kHalves) {
+        // a ragged last C_out tile only has p.n_last valid accumulator columns (the rest are
+        // beyond C_out: never stored, so they need not be drained or parked either)
+        const int width = (nt == p.n_tiles_n - 1 && p.n_last < BN) ? p.n_last : BN;
+        for (int c0 = half * 32; c0 < width; c0 += 32 * kHalves) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
           tc_wait_ld();
@@ -1281,7 +1302,7 @@ static PFN_encodeTiled_t get_encode_tiled() {
 
 template <int BN, int CG, int BLK, bool HALO, bool EDGE = false, bool NORM = false>
 static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                               const ConvParams& p, int grid, cudaStream_t s) {
+                               const CUtensorMap& tb2, const ConvParams& p, int grid, cudaStream_t s) {
   using Cfg = ConvCfg<BN, CG, HALO, EDGE, NORM>;
   auto kern = sparse_conv3x3_tc_kernel<BN, CG, BLK, HALO, EDGE, NORM>;
   static bool attr_set = false;  // per process; the attribute is per function
@@ -1304,33 +1325,44 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tb2, p);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }
 
 template <int BN>
 static sphinx_status launch_cg(int cg, const CUtensorMap& ta, const CUtensorMap& tb,
-                               const CUtensorMap& tc, const ConvParams& p, int grid, cudaStream_t s) {
+                               const CUtensorMap& tc, const CUtensorMap& tb2, const ConvParams& p, int grid,
+                               cudaStream_t s) {
   if (p.norm_tab) {  // fused GN+SiLU (halo mode, CTA pair; checked by the caller)
-    return p.plan_ids ? launch_bn<BN, 2, 8, true, true, true>(ta, tb, tc, p, grid, s)
-                      : launch_bn<BN, 2, 8, true, false, true>(ta, tb, tc, p, grid, s);
+    return p.plan_ids ? launch_bn<BN, 2, 8, true, true, true>(ta, tb, tc, tb2, p, grid, s)
+                      : launch_bn<BN, 2, 8, true, false, true>(ta, tb, tc, tb2, p, grid, s);
   }
   if (p.b == 8 && p.halo && p.plan_ids)
-    return cg == 2 ? launch_bn<BN, 2, 8, true, true>(ta, tb, tc, p, grid, s)
-                   : launch_bn<BN, 1, 8, true, true>(ta, tb, tc, p, grid, s);
+    return cg == 2 ? launch_bn<BN, 2, 8, true, true>(ta, tb, tc, tb2, p, grid, s)
+                   : launch_bn<BN, 1, 8, true, true>(ta, tb, tc, tb2, p, grid, s);
   if (p.b == 8 && p.halo)
-    return cg == 2 ? launch_bn<BN, 2, 8, true>(ta, tb, tc, p, grid, s)
-                   : launch_bn<BN, 1, 8, true>(ta, tb, tc, p, grid, s);
+    return cg == 2 ? launch_bn<BN, 2, 8, true>(ta, tb, tc, tb2, p, grid, s)
+                   : launch_bn<BN, 1, 8, true>(ta, tb, tc, tb2, p, grid, s);
   if (p.b == 8)
-    return cg == 2 ? launch_bn<BN, 2, 8, false>(ta, tb, tc, p, grid, s)
-                   : launch_bn<BN, 1, 8, false>(ta, tb, tc, p, grid, s);
-  return cg == 2 ? launch_bn<BN, 2, 4, false>(ta, tb, tc, p, grid, s)
-                 : launch_bn<BN, 1, 4, false>(ta, tb, tc, p, grid, s);
+    return cg == 2 ? launch_bn<BN, 2, 8, false>(ta, tb, tc, tb2, p, grid, s)
+                   : launch_bn<BN, 1, 8, false>(ta, tb, tc, tb2, p, grid, s);
+  return cg == 2 ? launch_bn<BN, 2, 4, false>(ta, tb, tc, tb2, p, grid, s)
+                 : launch_bn<BN, 1, 4, false>(ta, tb, tc, tb2, p, grid, s);
+}
+
+// Ragged 256-wide C_out tiling (e.g. 320 = 256 + 64, 640 = 2 x 256 + 128) instead of equal
+// 160-wide tiles: the widest MMA reads the A operand once per 256 output columns.
+static bool ragged_ok(int cout) {
+  const char* env = getenv("SPHINX_CONV_RAGGED");
+  const bool on = env ? atoi(env) != 0 : kRaggedDefault;
+  const int last = cout % 256;
+  return on && cout > 256 && last != 0 && last % 32 == 0;
 }
 
 // Widest tile that minimises padded output columns (ties -> wider).
 static int pick_bn(int cout) {
+  if (ragged_ok(cout)) return 256;
   const int cands[] = {256, 160, 128, 64, 32};
   int best = 32, best_pad = 1 << 30;
   for (int bn : cands) {
@@ -1412,7 +1444,9 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     if (!halo) return SPHINX_ERR_UNSUPPORTED;  // the transform works on halo slots (b = 8, 3x3)
     cg = 2;
   }
-  CUtensorMap ta, tb, tc;
+  CUtensorMap ta, tb, tc, tb2;
+  // ragged C_out tiling: the last tile is n_last wide (its own weight tensor map)
+  const int n_last = c_out - (cdiv(c_out, bn) - 1) * bn;
   {
     const cuuint64_t dims[4] = {(cuuint64_t)c_in, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
     const cuuint64_t strides[3] = {(cuuint64_t)c_in * 2, (cuuint64_t)w_ * c_in * 2,
@@ -1441,6 +1475,12 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
+    const bool ragged = n_last < bn && ragged_ok(c_out);
+    const cuuint32_t box2[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)((ragged ? n_last : bn) / cg)};
+    r = enc(&tb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides, box2, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
   }
   ConvParams p;
   p.ids = block_ids;
@@ -1462,6 +1502,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.kc = cdiv(c_in, kBK);
   p.taps = taps;
   p.n_tiles_n = cdiv(c_out, bn);
+  p.n_last = (n_last < bn && ragged_ok(c_out)) ? n_last : bn;
   p.bpt = kBM / (block * block);
   p.halo = halo;
   p.a_ahead = 2;
@@ -1523,11 +1564,11 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     if (e != cudaSuccess) return cuda_fail(e);
   }
   switch (bn) {
-    case 256: return launch_cg<256>(cg, ta, tb, tc, p, grid, s);
-    case 160: return launch_cg<160>(cg, ta, tb, tc, p, grid, s);
-    case 128: return launch_cg<128>(cg, ta, tb, tc, p, grid, s);
-    case 64: return launch_cg<64>(cg, ta, tb, tc, p, grid, s);
-    default: return launch_cg<32>(cg, ta, tb, tc, p, grid, s);
+    case 256: return launch_cg<256>(cg, ta, tb, tc, tb2, p, grid, s);
+    case 160: return launch_cg<160>(cg, ta, tb, tc, tb2, p, grid, s);
+    case 128: return launch_cg<128>(cg, ta, tb, tc, tb2, p, grid, s);
+    case 64: return launch_cg<64>(cg, ta, tb, tc, tb2, p, grid, s);
+    default: return launch_cg<32>(cg, ta, tb, tc, tb2, p, grid, s);
   }
 }
 

@@ -466,3 +466,12 @@ def test_conv_reuse_plan(sphinx):
     sphinx.sphinx_sparse_conv3x3(x, w, None, y1, b, g_ids, g_cnt, workspace=ws, reuse_plan=True)
     torch.cuda.synchronize()
     assert np.array_equal(y0.cpu().numpy().view(np.uint32), y1.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("h,c,dens", [(72, 320, 0.25), (36, 640, 0.4), (20, 96 * 4, 0.6)])
+def test_conv_ragged_cout_tiles(sphinx, monkeypatch, h, c, dens):
+    """SPHINX_CONV_RAGGED=1: 256-wide C_out tiles with a narrower last tile (320 = 256 + 64,
+    640 = 2x256 + 128, 384 = 256 + 128) -- a measured-slower option kept under test."""
+    monkeypatch.setenv("SPHINX_CONV_RAGGED", "1")
+    for dt in (torch.float32, torch.bfloat16):
+        _conv_check(sphinx, 2, h, h, c, c, 8, dens, "scattered", f"ragged{h}{c}", out_dtype=dt)
