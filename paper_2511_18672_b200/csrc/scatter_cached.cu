@@ -10,26 +10,44 @@
 
 namespace sphinx {
 
-// One thread per 16-byte word of the map; consecutive threads cover consecutive words of a
-// pixel row, so each warp's accesses are coalesced whatever C is (4 fp32 latent channels or
-// 640 bf16 feature channels).
+// One CTA row (blockIdx.y) per pixel row of one frame, threads over the row's 16-byte words (4
+// per thread in flight): consecutive threads cover consecutive words, so each warp's accesses
+// are coalesced whatever C is (4 fp32 latent channels or 640 bf16 feature channels), and the
+// frame / block-row lookups are per CTA (the flat-index version spent its issue slots on 64-bit
+// divisions: 57% of HBM).
 __global__ void __launch_bounds__(256) scatter_full_kernel(
     const int4* src, const int4* __restrict__ cache, int4* out, int h, int w, int px_vec, int b,
     int hb, int wb, const uint8_t* __restrict__ mask, const int32_t* __restrict__ k, int u,
-    int in_place, long long total) {
+    int in_place, int rows) {
   pdl_wait();
   pdl_trigger();
   const int row_vec = w * px_vec;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long row = e / row_vec;  // = n * h + y
-    const int xv = (int)(e - row * row_vec);
-    const int n = (int)(row / h), y = (int)(row - (long long)n * h);
-    const int x = xv / px_vec;
+  const float inv_pv = 1.0f / (float)px_vec;  // exact floor((xv + 0.5) / px_vec) for xv < 2^20
+  for (int row = blockIdx.y; row < rows; row += gridDim.y) {
+    const int n = row / h, y = row - n * h;
     const int kf = k ? __ldg(k + n) : 0;
-    const bool act = (!k || (kf >= 0 && kf <= u)) && mask[((size_t)n * hb + y / b) * wb + x / b];
-    if (in_place && act) continue;
-    out[e] = act ? src[e] : __ldg(cache + e);
+    const bool frame_ok = !k || (kf >= 0 && kf <= u);
+    const uint8_t* mrow = mask + ((size_t)n * hb + y / b) * wb;
+    const size_t base = (size_t)row * row_vec;
+    for (int x0 = blockIdx.x * blockDim.x * 4 + threadIdx.x; x0 < row_vec; x0 += gridDim.x * blockDim.x * 4) {
+      int4 v[4];
+      bool act[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int xv = x0 + q * blockDim.x;
+        act[q] = false;
+        if (xv < row_vec) {
+          const int x = __float2int_rz(((float)xv + 0.5f) * inv_pv);
+          act[q] = frame_ok && mrow[x / b];
+          if (!(in_place && act[q])) v[q] = act[q] ? src[base + xv] : __ldg(cache + base + xv);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int xv = x0 + q * blockDim.x;
+        if (xv < row_vec && !(in_place && act[q])) out[base + xv] = v[q];
+      }
+    }
   }
 }
 
@@ -98,13 +116,14 @@ extern "C" sphinx_status sphinx_scatter_cached(const void* src, sphinx_src_layou
   if (src_layout == SPHINX_SRC_FULL) {
     int sms = 148;
     check_device(&sms);
-    const long long total = (long long)n * h * w * px_vec;
-    long long blocks = (total + 255) / 256;
-    if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
-    cudaError_t e = launch_k(scatter_full_kernel, dim3((unsigned)blocks), dim3(256), 0, s,
+    if ((long long)w * px_vec >= (1 << 20)) return SPHINX_ERR_UNSUPPORTED;  // row index math
+    const int rows = n * h, row_vec = w * px_vec;
+    const int gx = cdiv(row_vec, 256 * 4);
+    const int gy = rows < 65535 ? rows : 65535;
+    cudaError_t e = launch_k(scatter_full_kernel, dim3(gx, gy), dim3(256), 0, s,
                              static_cast<const int4*>(src), static_cast<const int4*>(cache),
                              static_cast<int4*>(out), (int)h, (int)w, px_vec, (int)b, hb, wb,
-                             block_mask, start_step, (int)step_u, out == src ? 1 : 0, total);
+                             block_mask, start_step, (int)step_u, out == src ? 1 : 0, rows);
     if (e != cudaSuccess) return cuda_fail(e);
   } else {
     cudaError_t e = launch_k(scatter_compact_kernel, dim3(grid), dim3(256), 0, s,
