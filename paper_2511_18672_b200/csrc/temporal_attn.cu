@@ -74,6 +74,7 @@ __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w 
 struct TaGeom {
   int h, w, c, heads, T, b, hb, wb, n_seq, nbuf;
   int ppu;      // pixels per unit: 2 = two x-adjacent pixels share one bulk copy per frame
+  int kv_only;  // stage k|v of every frame + q of listed frames only (one-pixel units)
   uint32_t rs;  // staged frame row stride in bytes: ppu*6c + 16 (an odd number of 16-byte units)
   float scale;
 };
@@ -128,20 +129,37 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
   // (Measured alternatives: k|v of all frames + q of listed frames only -- more, smaller copies
   // -- and 16-byte cp.async by all threads were both 1.3x slower.)
   const uint32_t tok_bytes = (uint32_t)c3 * 2;
-  auto stage = [&](int buf, int s, size_t pix, int npx) {
+  const bool kv_only = g.kv_only && g.ppu == 1;
+  auto stage = [&](int buf, int s, size_t pix, int npx, uint32_t Mq) {
     if (warp == 0) {
-      if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)(T * npx));
-      __syncwarp();
-      if (lane < T)
-        bulk_g2s(rows + (size_t)buf * T * g.rs + (size_t)lane * g.rs,
-                 qkv + (((size_t)s * T + lane) * plane + pix) * c3, tok_bytes * (uint32_t)npx, &bars[buf]);
+      uint8_t* dst0 = rows + (size_t)buf * T * g.rs;
+      if (!kv_only) {
+        if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)(T * npx));
+        __syncwarp();
+        if (lane < T)
+          bulk_g2s(dst0 + (size_t)lane * g.rs, qkv + (((size_t)s * T + lane) * plane + pix) * c3,
+                   tok_bytes * (uint32_t)npx, &bars[buf]);
+      } else {
+        // k|v of every frame (the cache of unlisted ones) + q of the listed frames only: a third
+        // fewer bytes; op i < T is frame i's k|v, op T + j the j-th listed frame's q
+        const uint32_t kvb = (uint32_t)c * 4, qb = (uint32_t)c * 2;
+        const int nq = __popc(Mq);
+        if (lane == 0) mbar_arrive_expect_tx(&bars[buf], kvb * (uint32_t)T + qb * (uint32_t)nq);
+        __syncwarp();
+        for (int i = lane; i < T + nq; i += 32) {
+          const int m = i < T ? i : __fns(Mq, 0, i - T + 1);
+          const __nv_bfloat16* src = qkv + (((size_t)s * T + m) * plane + pix) * c3;
+          if (i < T) bulk_g2s(dst0 + (size_t)m * g.rs + qb, src + c, kvb, &bars[buf]);
+          else bulk_g2s(dst0 + (size_t)m * g.rs, src, qb, &bars[buf]);
+        }
+      }
     }
   };
   uint32_t M;
   size_t pix;
   int s, npx;
   int u = ta_next(blockIdx.x, gridDim.x, units, posmask, g, M, pix, s, npx);
-  if (u >= 0) stage(0, s, pix, npx);
+  if (u >= 0) stage(0, s, pix, npx, M);
   uint32_t phase = 0u;  // bit k = parity of buffer k
   int buf = 0;
   while (u >= 0) {
@@ -149,7 +167,7 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
     size_t pixn;
     int sn, npxn;
     const int un = ta_next(u + gridDim.x, gridDim.x, units, posmask, g, Mn, pixn, sn, npxn);
-    if (un >= 0 && g.nbuf == 2) stage(buf ^ 1, sn, pixn, npxn);  // prefetch (that buffer is free)
+    if (un >= 0 && g.nbuf == 2) stage(buf ^ 1, sn, pixn, npxn, Mn);  // prefetch (that buffer is free)
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
     phase ^= 1u << buf;
     const uint32_t tk0 = smem_u32(rows + (size_t)buf * T * g.rs);
@@ -273,7 +291,7 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
       }
     }
     __syncthreads();  // every warp is done with this buffer before it is staged again
-    if (un >= 0 && g.nbuf == 1) stage(0, sn, pixn, npxn);
+    if (un >= 0 && g.nbuf == 1) stage(0, sn, pixn, npxn, Mn);
     if (g.nbuf == 2) buf ^= 1;
     u = un; M = Mn; pix = pixn; s = sn; npx = npxn;
   }
@@ -335,6 +353,8 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   if (const char* env = getenv("SPHINX_TA_NBUF")) g.nbuf = atoi(env) == 1 ? 1 : g.nbuf;
   if (const char* env = getenv("SPHINX_TA_PPU"))
     if (atoi(env) == 2 && block % 2 == 0 && ta_smem(c, T, g.nbuf, 2) <= 227 * 1024) g.ppu = 2;
+  g.kv_only = 0;
+  if (const char* env = getenv("SPHINX_TA_KVONLY")) g.kv_only = atoi(env) != 0;
   g.rs = (uint32_t)ta_row(c, g.ppu);
   const size_t smem = ta_smem(c, T, g.nbuf, g.ppu);
   e = cudaFuncSetAttribute(ta_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
