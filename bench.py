@@ -242,9 +242,9 @@ def graph_time(torch, fn, reps=20):
     return e0.elapsed_time(e1) / reps
 
 
-def density_sweep(torch, sp, dev, frames_list=(1, 21), dens=(0.05, 0.10, 0.25, 0.50, 0.75, 1.0)):
-    """configs[1]: 72x72x320, block 8, density sweep 5-100% (1 frame, and the 21-frame batched
-    variant): own sparse conv vs own dense launch (all blocks listed) vs cuDNN dense
+def density_sweep(torch, sp, dev, frames_list=(1, 21, 168), dens=(0.05, 0.10, 0.25, 0.50, 0.75, 1.0)):
+    """configs[1]: 72x72x320, block 8, density sweep 5-100% (1 frame, and the 21-frame and
+    168-frame = configs[3]-sized batched variants): own sparse conv vs own dense launch (all blocks listed) vs cuDNN dense
     (torch conv2d, channels_last bf16, fp32 accumulate).  Graph-replay device time, L2-warm."""
     h, c = 72, 320
     hb = 9
