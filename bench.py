@@ -157,7 +157,7 @@ class GpuStep:
                     conv_events[l][j][0].record()
                 # the second conv of a level uses the same list and workspace: reuse its edge plan
                 sp.sphinx_sparse_conv3x3(src, d[f"w{l}{j}"], d[f"b{l}{j}"], dst, B, self.ids[l], self.cnt[l],
-                                         reuse_plan=j > 0)
+                                         reuse_plan=j > 0, list_ready=True)
                 if conv_events is not None:
                     conv_events[l][j][1].record()
                 src = dst

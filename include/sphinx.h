@@ -231,8 +231,15 @@ SPHINX_API size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, i
  * SPHINX_CONV_REUSE_PLAN  the workspace already holds the edge-class plan of THIS list (the
  *                         caller's previous conv on this stream used the same block_ids, count and
  *                         workspace, e.g. the second conv of a ResNet block): skip recomputing it.
- *                         Undefined results if the list changed in between. */
+ *                         Undefined results if the list changed in between.
+ * SPHINX_CONV_LIST_READY  block_ids / count (and a reused plan) were written by a kernel that ran
+ *                         BEFORE the immediately preceding kernel on this stream (e.g. compaction
+ *                         earlier in the step): the conv reads them and starts its weight loads
+ *                         before waiting for the preceding kernel (programmatic dependent launch);
+ *                         its activation loads and stores still wait.  Ignored when the call
+ *                         launches its own edge plan. */
 #define SPHINX_CONV_REUSE_PLAN 1
+#define SPHINX_CONV_LIST_READY 2
 SPHINX_API sphinx_status sphinx_sparse_conv3x3_ex(
     const void* x, const void* w, const float* bias, const void* residual, void* y,
     sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,

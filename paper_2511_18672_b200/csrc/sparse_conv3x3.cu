@@ -106,6 +106,9 @@ struct ConvParams {
   int bpt_b, bpt_r;          // blocks per CTA tile of the two edge classes
   uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
   int trace;         // SPHINX_TRACE builds: record this launch's timeline
+  int early_list;    // ids/count/plan were written before the immediately preceding kernel: read
+                     // them (and start the weight loads) before griddepcontrol.wait; only the
+                     // halo producer and the epilogue wait for the predecessor
   int dbg;           // SPHINX_TRACE builds: 1 = skip epilogue global stores, 2 = skip bias
   int a_warp;        // halo mode: 1 = halos issued by their own producer warp
   int a_ahead;       // halo chunks the A cursor may run ahead of the B cursor (1..kANum-1)
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();  // ids, count, plan and x are produced upstream
+  if (!p.early_list) pdl_wait();  // ids, count, plan and x are produced upstream
   pdl_trigger();
 #ifdef SPHINX_TRACE
   if (threadIdx.x == 0) CONV_TRACE(1, gtimer());
@@ -516,6 +519,9 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
   if (threadIdx.x == 0) CONV_TRACE(15, gtimer());
 #endif
   if (warp == 0 || (HALO && warp == kAWarp)) {
+    // early_list: the halo (A) producer -- also warp 0 when it issues A (per-tap path, or halo
+    // mode without split producers) -- waits for the predecessor; the weight-only producer not
+    if (p.early_list && (warp == kAWarp || !HALO || p.a_warp == 0)) pdl_wait();
     // ===================== TMA producers (both CTAs) =====================
     // halo mode: warp 0 issues the weight (B) tiles and warp kAWarp the halos (A), so the two
     // streams of TMA issues overlap (a single issuing thread caps the per-SM TMA op rate)
@@ -846,6 +852,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
       }
     }
   } else if (warp < kAWarp || (!NORM && warp >= kXWarp)) {
+    if (p.early_list) pdl_wait();  // stores / residual reads after the predecessor completes
     // ============ epilogue (warps 2..5, and 7..10 for non-NORM kernels; both CTAs) ============
     constexpr int kEpiW = NORM ? 4 : 8, kEpiT = kEpiW * 32, kHalves = kEpiW / 4;
     const int half = warp >= kXWarp ? 1 : 0;  // which half of the 32-column chunks this warp drains
@@ -1508,6 +1515,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.a_ahead = 2;
   p.a_warp = 1;
   p.trace = 0;
+  p.early_list = 0;
   p.dbg = 0;
 #ifdef SPHINX_TRACE
   if (const char* env = getenv("SPHINX_DBG")) p.dbg = atoi(env);
@@ -1555,6 +1563,12 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   const long long want = p.ws_part ? max_tiles * 16 : max_tiles;  // split-K may multiply units
   const int grid = cg * (int)(want < max_clusters ? want : max_clusters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // SPHINX_CONV_LIST_READY: ids/count (and a reused plan) predate the preceding kernel; not when
+  // this call launches the plan kernel (its output becomes the immediate predecessor's) or for
+  // the fused-GN variant (its table comes from the preceding kernel)
+  p.early_list = (flags & SPHINX_CONV_LIST_READY) && !norm_tab &&
+                 !(p.plan_ids && !(flags & SPHINX_CONV_REUSE_PLAN)) ? 1 : 0;
+  if (const char* env = getenv("SPHINX_CONV_EARLY")) p.early_list = p.early_list && atoi(env) != 0;
   // SPHINX_CONV_REUSE_PLAN: the workspace already holds the edge plan of this very list (the
   // caller's previous conv on this stream used the same list and workspace): skip the plan launch
   if (p.plan_ids && !(flags & SPHINX_CONV_REUSE_PLAN)) {
@@ -1607,7 +1621,7 @@ extern "C" sphinx_status sphinx_sparse_conv3x3_ex(
     sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
     int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
     void* workspace, size_t workspace_bytes, int32_t flags, sphinx_stream_t stream) {
-  if (flags & ~SPHINX_CONV_REUSE_PLAN) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (flags & ~(SPHINX_CONV_REUSE_PLAN | SPHINX_CONV_LIST_READY)) return SPHINX_ERR_INVALID_ARGUMENT;
   return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
                    capacity, workspace, workspace_bytes, stream, 9, nullptr, (int)flags);
 }
