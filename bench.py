@@ -145,6 +145,11 @@ class GpuStep:
                   block_ids=self.ids[l], count=self.cnt[l]) for l in range(3)] +
             [dict(block_mask=None, start_step=self.k, step_u=U_STEP, select=sp.SELECT_INACTIVE_FRAMES,
                   block_ids=self.ids_in, count=self.cnt_in, shape=tuple(self.masks[0].shape))])
+        # the edge-class plans of the ragged levels (36x36, 18x18) right after compaction, so every
+        # conv of the step reuses its level's plan and may start before its predecessor ends
+        for l in (1, 2):
+            h, c = LEVELS[l]
+            sp.sphinx_conv_edge_plan(self.ids[l], self.cnt[l], N_FRAMES, h, h, B, c)
         # Alg1 line 12: active latent blocks noised to their start step k; line 19: inactive
         # frames resampled to u+1 from the clean latent
         sp.sphinx_noise_inject(d["x0"], d["eps"], self.zt, B, self.ids[0], self.cnt[0], self.k, d["abar"])
@@ -155,9 +160,9 @@ class GpuStep:
                 dst = self.y[l] if j % 2 == 0 else self.z[l]
                 if conv_events is not None:
                     conv_events[l][j][0].record()
-                # the second conv of a level uses the same list and workspace: reuse its edge plan
+                # every conv of a level uses the list's plan computed above (same workspace)
                 sp.sphinx_sparse_conv3x3(src, d[f"w{l}{j}"], d[f"b{l}{j}"], dst, B, self.ids[l], self.cnt[l],
-                                         reuse_plan=j > 0, list_ready=True)
+                                         reuse_plan=True, list_ready=True)
                 if conv_events is not None:
                     conv_events[l][j][1].record()
                 src = dst

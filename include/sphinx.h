@@ -107,7 +107,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 5
+#define SPHINX_ABI_VERSION 6
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -240,6 +240,15 @@ SPHINX_API size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, i
  *                         launches its own edge plan. */
 #define SPHINX_CONV_REUSE_PLAN 1
 #define SPHINX_CONV_LIST_READY 2
+
+/* Computes the edge-class plan of a list into a conv workspace (what a conv call without
+ * SPHINX_CONV_REUSE_PLAN does first), so that it can run early in a step and every conv over the
+ * list passes SPHINX_CONV_REUSE_PLAN (| SPHINX_CONV_LIST_READY).  A no-op for maps without partial
+ * edge blocks or block != 8. */
+SPHINX_API sphinx_status sphinx_conv_edge_plan(const int32_t* block_ids, const int32_t* count, int32_t n,
+                                               int32_t h, int32_t w_, int32_t block, int32_t capacity,
+                                               void* workspace, size_t workspace_bytes,
+                                               sphinx_stream_t stream);
 SPHINX_API sphinx_status sphinx_sparse_conv3x3_ex(
     const void* x, const void* w, const float* bias, const void* residual, void* y,
     sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,

@@ -29,7 +29,7 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 5
+ABI_VERSION = 6
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
@@ -38,7 +38,8 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_sparse_conv3x3_residual", "sphinx_sparse_resblock",
            "sphinx_sparse_pointwise", "sphinx_temporal_attention_workspace_size",
            "sphinx_temporal_attention", "sphinx_temporal_block", "sphinx_gn_scale_shift",
-           "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex")
+           "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex",
+           "sphinx_conv_edge_plan")
 
 _lib = None
 
@@ -118,6 +119,7 @@ def load(path=SO_PATH):
         "sphinx_sparse_pointwise": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_gn_scale_shift": ([P, P, P, F, I, I, I, I, I, I, P, P], I),
         "sphinx_compact_blocks_batch": ([P, I, P], I),
+        "sphinx_conv_edge_plan": ([P, P, I, I, I, I, I, P, Z, P], I),
         "sphinx_sparse_conv3x3_ex": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, I, P], I),
         "sphinx_sparse_conv3x3_gn_silu": ([P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_temporal_attention_workspace_size": ([I, I, I, I, I], Z),
@@ -308,6 +310,21 @@ def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None,
                                       n, h, wd, cin, cout, int(block), _ptr(block_ids), _ptr(count),
                                       int(cap), ws_ptr, ws_bytes, _stream(stream))
     _chk("sphinx_sparse_conv3x3", rc)
+
+
+def sphinx_conv_edge_plan(block_ids, count, n, h, w, block, c_out, capacity=None, workspace=None,
+                          stream=None):
+    """Edge-class plan of a list into the (cached) conv workspace of this geometry, so the convs
+    over the list can pass reuse_plan=True (and list_ready=True)."""
+    import torch
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    cap = block_ids.numel() if capacity is None else capacity
+    if workspace is None:
+        workspace = conv_workspace(c_out, block_ids.device, n, h, w, block)
+    rc = load().sphinx_conv_edge_plan(_ptr(block_ids), _ptr(count), int(n), int(h), int(w), int(block), int(cap),
+                                      _ptr(workspace), workspace.numel(), _stream(stream))
+    _chk("sphinx_conv_edge_plan", rc)
 
 
 def sphinx_scatter_cached(src, cache, out, block, block_mask=None, start_step=None, step_u=0,

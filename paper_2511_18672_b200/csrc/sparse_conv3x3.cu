@@ -1616,6 +1616,29 @@ extern "C" sphinx_status sphinx_sparse_pointwise(
                    capacity, workspace, workspace_bytes, stream, 1);
 }
 
+extern "C" sphinx_status sphinx_conv_edge_plan(const int32_t* block_ids, const int32_t* count, int32_t n,
+                                               int32_t h, int32_t w_, int32_t block, int32_t capacity,
+                                               void* workspace, size_t workspace_bytes,
+                                               sphinx_stream_t stream) {
+  if (!block_ids || !count || !workspace || n <= 0 || h <= 0 || w_ <= 0 || capacity < 0)
+    return SPHINX_ERR_INVALID_ARGUMENT;
+  if (reinterpret_cast<uintptr_t>(workspace) & 255u) return SPHINX_ERR_INVALID_ARGUMENT;
+  const int hb = cdiv(h, block), wb = cdiv(w_, block);
+  if ((int64_t)capacity > (int64_t)n * hb * wb) return SPHINX_ERR_INVALID_ARGUMENT;
+  // only the halo path (8x8 blocks) on maps with partial edge blocks uses a plan
+  if (block != 8 || (h % 8 == 0 && w_ % 8 == 0)) return SPHINX_OK;
+  if (workspace_bytes < kCntBytes + plan_bytes(capacity)) return SPHINX_ERR_INVALID_ARGUMENT;
+  sphinx_status st = check_device();
+  if (st != SPHINX_OK) return st;
+  uint8_t* ws8 = static_cast<uint8_t*>(workspace);
+  cudaError_t e = launch_k(conv_plan_kernel, dim3(1), dim3(1024), 0, reinterpret_cast<cudaStream_t>(stream),
+                           block_ids, count, hb, wb, (int)(h % 8 != 0), (int)(w_ % 8 != 0),
+                           reinterpret_cast<int32_t*>(ws8 + kCntBytes + 256),
+                           reinterpret_cast<int32_t*>(ws8 + kCntBytes));
+  if (e != cudaSuccess) return cuda_fail(e);
+  return SPHINX_OK;
+}
+
 extern "C" sphinx_status sphinx_sparse_conv3x3_ex(
     const void* x, const void* w, const float* bias, const void* residual, void* y,
     sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
