@@ -162,7 +162,8 @@ class GpuStep:
                     conv_events[l][j][0].record()
                 # every conv of a level uses the list's plan computed above (same workspace)
                 sp.sphinx_sparse_conv3x3(src, d[f"w{l}{j}"], d[f"b{l}{j}"], dst, B, self.ids[l], self.cnt[l],
-                                         reuse_plan=True, list_ready=True)
+                                         reuse_plan=True, list_ready=True,
+                                         input_ready=j == 0)  # a level's input features are step inputs
                 if conv_events is not None:
                     conv_events[l][j][1].record()
                 src = dst

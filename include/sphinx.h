@@ -240,6 +240,10 @@ SPHINX_API size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, i
  *                         launches its own edge plan. */
 #define SPHINX_CONV_REUSE_PLAN 1
 #define SPHINX_CONV_LIST_READY 2
+/* SPHINX_CONV_INPUT_READY (with LIST_READY): x was also written before the preceding kernel (e.g.
+ * a level's input features): the activation loads and MMAs may run while the preceding kernel
+ * drains; the epilogue (stores) still waits for it, so the kernel completes after it. */
+#define SPHINX_CONV_INPUT_READY 4
 
 /* Computes the edge-class plan of a list into a conv workspace (what a conv call without
  * SPHINX_CONV_REUSE_PLAN does first), so that it can run early in a step and every conv over the

@@ -69,6 +69,7 @@ class CompactJob(ctypes.Structure):
 MAX_COMPACT_JOBS = 8
 CONV_REUSE_PLAN = 1
 CONV_LIST_READY = 2
+CONV_INPUT_READY = 4
 
 
 class StartArgs(ctypes.Structure):
@@ -269,7 +270,8 @@ def conv_workspace(c_out, device, n=1, h=1, w=1, block=8):
 
 
 def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None, stream=None,
-                          workspace=None, residual=None, reuse_plan=False, list_ready=False):
+                          workspace=None, residual=None, reuse_plan=False, list_ready=False,
+                          input_ready=False):
     """Step 4.  x bf16 NHWC [N,H,W,Cin]; w bf16 [Cout,3,3,Cin]; bias fp32 [Cout] or None;
     y NHWC [N,H,W,Cout] bf16 or fp32 (only listed blocks are written).
     workspace: None = a cached zeroed split-K workspace for this device, False = no split-K,
@@ -288,9 +290,10 @@ def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None,
     if workspace is None:
         workspace = conv_workspace(cout, y.device, n, h, wd, block)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
-    if reuse_plan or list_ready:
+    if reuse_plan or list_ready or input_ready:
         _dev(residual, torch.bfloat16, "residual")
-        flags = (CONV_REUSE_PLAN if reuse_plan else 0) | (CONV_LIST_READY if list_ready else 0)
+        flags = ((CONV_REUSE_PLAN if reuse_plan else 0) | (CONV_LIST_READY if list_ready else 0) |
+                 (CONV_INPUT_READY if input_ready else 0))
         rc = load().sphinx_sparse_conv3x3_ex(
             _ptr(x), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y), F32 if y.dtype == torch.float32 else BF16,
             n, h, wd, cin, cout, int(block), _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes,

@@ -106,6 +106,9 @@ struct ConvParams {
   int bpt_b, bpt_r;          // blocks per CTA tile of the two edge classes
   uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
   int trace;         // SPHINX_TRACE builds: record this launch's timeline
+  int early_input;   // x (and the list) predate the preceding kernel: the halo producer does not
+                     // wait either -- only the epilogue does (its stores, and kernel completion
+                     // after the predecessor's, keep the stream order)
   int early_list;    // ids/count/plan were written before the immediately preceding kernel: read
                      // them (and start the weight loads) before griddepcontrol.wait; only the
                      // halo producer and the epilogue wait for the predecessor
@@ -521,7 +524,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
   if (warp == 0 || (HALO && warp == kAWarp)) {
     // early_list: the halo (A) producer -- also warp 0 when it issues A (per-tap path, or halo
     // mode without split producers) -- waits for the predecessor; the weight-only producer not
-    if (p.early_list && (warp == kAWarp || !HALO || p.a_warp == 0)) pdl_wait();
+    if (p.early_list && !p.early_input && (warp == kAWarp || !HALO || p.a_warp == 0)) pdl_wait();
     // ===================== TMA producers (both CTAs) =====================
     // halo mode: warp 0 issues the weight (B) tiles and warp kAWarp the halos (A), so the two
     // streams of TMA issues overlap (a single issuing thread caps the per-SM TMA op rate)
@@ -1516,6 +1519,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.a_warp = 1;
   p.trace = 0;
   p.early_list = 0;
+  p.early_input = 0;
   p.dbg = 0;
 #ifdef SPHINX_TRACE
   if (const char* env = getenv("SPHINX_DBG")) p.dbg = atoi(env);
@@ -1569,6 +1573,8 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.early_list = (flags & SPHINX_CONV_LIST_READY) && !norm_tab &&
                  !(p.plan_ids && !(flags & SPHINX_CONV_REUSE_PLAN)) ? 1 : 0;
   if (const char* env = getenv("SPHINX_CONV_EARLY")) p.early_list = p.early_list && atoi(env) != 0;
+  p.early_input = (p.early_list && (flags & SPHINX_CONV_INPUT_READY)) ? 1 : 0;
+  if (const char* env = getenv("SPHINX_CONV_EARLY_INPUT")) p.early_input = p.early_input && atoi(env) != 0;
   // SPHINX_CONV_REUSE_PLAN: the workspace already holds the edge plan of this very list (the
   // caller's previous conv on this stream used the same list and workspace): skip the plan launch
   if (p.plan_ids && !(flags & SPHINX_CONV_REUSE_PLAN)) {
@@ -1644,7 +1650,8 @@ extern "C" sphinx_status sphinx_sparse_conv3x3_ex(
     sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
     int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
     void* workspace, size_t workspace_bytes, int32_t flags, sphinx_stream_t stream) {
-  if (flags & ~(SPHINX_CONV_REUSE_PLAN | SPHINX_CONV_LIST_READY)) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (flags & ~(SPHINX_CONV_REUSE_PLAN | SPHINX_CONV_LIST_READY | SPHINX_CONV_INPUT_READY))
+    return SPHINX_ERR_INVALID_ARGUMENT;
   return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
                    capacity, workspace, workspace_bytes, stream, 9, nullptr, (int)flags);
 }

@@ -468,6 +468,31 @@ def test_conv_reuse_plan(sphinx):
     assert np.array_equal(y0.cpu().numpy().view(np.uint32), y1.cpu().numpy().view(np.uint32))
 
 
+@pytest.mark.parametrize("h,c", [(36, 64), (18, 640)])
+def test_conv_early_start_flags(sphinx, h, c):
+    """SPHINX_CONV_LIST_READY / SPHINX_CONV_INPUT_READY (loads before griddepcontrol.wait, stores
+    after it): bit-identical to the plain launch, also when the preceding kernel is a long conv
+    that writes a different output (the stores still follow it)."""
+    n, b = 3, 8
+    x = bf16(syn.features_bf16((n, h, h, c), "early"))
+    w = bf16(syn.weights_bf16(c, c, "early"))
+    m = (np.random.default_rng(5).random((n, h // b + (h % b > 0), h // b + (h % b > 0))) < 0.6).astype(np.uint8)
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, None, 0)
+    ws = torch.zeros(sphinx.load().sphinx_conv_workspace_size(n, h, h, c, c, b), dtype=torch.uint8, device=dev)
+    ws2 = torch.zeros_like(ws)
+    ys = [torch.zeros((n, h, h, c), device=dev) for _ in range(4)]
+    sphinx.sphinx_sparse_conv3x3(x, w, None, ys[0], b, g_ids, g_cnt, workspace=ws)
+    sphinx.sphinx_sparse_conv3x3(x, w, None, ys[1], b, g_ids, g_cnt, workspace=ws2)  # plan for ws2
+    sphinx.sphinx_sparse_conv3x3(x, w, None, ys[2], b, g_ids, g_cnt, workspace=ws2, reuse_plan=True,
+                                 list_ready=True)
+    sphinx.sphinx_sparse_conv3x3(x, w, None, ys[3], b, g_ids, g_cnt, workspace=ws, reuse_plan=True,
+                                 list_ready=True, input_ready=True)
+    torch.cuda.synchronize()
+    ref = ys[0].cpu().numpy().view(np.uint32)
+    for y in ys[1:]:
+        assert np.array_equal(ref, y.cpu().numpy().view(np.uint32))
+
+
 @pytest.mark.parametrize("h,c,dens", [(72, 320, 0.25), (36, 640, 0.4), (20, 96 * 4, 0.6)])
 def test_conv_ragged_cout_tiles(sphinx, monkeypatch, h, c, dens):
     """SPHINX_CONV_RAGGED=1: 256-wide C_out tiles with a narrower last tile (320 = 256 + 64,
