@@ -30,7 +30,9 @@
 
 namespace sphinx {
 
-constexpr int kTaThreads = 256;
+constexpr int kTaThreads = 256;     // default CTA size (SPHINX_TA_THREADS=512: 16 warps)
+constexpr int kTaMaxThreads = 512;
+constexpr int kTaMaxBuf = 5;        // staging ring depth limit (bars at offset 0..39)
 constexpr int kHeadDim = 64;
 
 __global__ void __launch_bounds__(1024) ta_plan_kernel(const int32_t* __restrict__ ids,
@@ -75,6 +77,10 @@ struct TaGeom {
   int h, w, c, heads, T, b, hb, wb, n_seq, nbuf;
   int ppu;      // pixels per unit: 2 = two x-adjacent pixels share one bulk copy per frame
   int kv_only;  // stage k|v of every frame + q of listed frames only (one-pixel units)
+  int pm_smem;  // the per-position frame masks are copied to shared memory (after the ring)
+  int stream;   // task stream: no CTA barrier per unit; warp w takes tasks w, w+nw, ... of the
+                // concatenated (unit, head, query tile) sequence; the last warp done with a
+                // buffer restages it
   uint32_t rs;  // staged frame row stride in bytes: ppu*6c + 16 (an odd number of 16-byte units)
   float scale;
 };
@@ -90,7 +96,7 @@ __device__ __forceinline__ int ta_next(int u, int step, int units,
     s = u / (nblk * bbu);
     const int r = u - s * nblk * bbu;
     const int pos = r / bbu, px = (r - pos * bbu) * g.ppu;
-    M = __ldg(posmask + s * nblk + pos);
+    M = posmask[s * nblk + pos];  // shared (pm_smem) or global
     if (M == 0u) continue;
     const int by = pos / g.wb, bx = pos - by * g.wb;
     const int yy = by * g.b + px / g.b, xx = bx * g.b + px % g.b;
@@ -102,7 +108,7 @@ __device__ __forceinline__ int ta_next(int u, int step, int units,
   return -1;
 }
 
-__global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
+__global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
     const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* o, const uint32_t* __restrict__ posmask,
     const TaGeom g) {
   extern __shared__ __align__(128) uint8_t ta_sm[];
@@ -112,14 +118,24 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
   // a 16-byte zero row at offset 64: ldmatrix rows of padded keys (>= T) point here
   const uint32_t zero_row = smem_u32(ta_sm + 64);
   if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(ta_sm + 64)[threadIdx.x] = 0u;
+  // per-buffer count of warps done with the unit it holds (offsets 80..99)
+  int* done = reinterpret_cast<int*>(ta_sm + 80);
+  if (threadIdx.x < kTaMaxBuf) done[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < g.nbuf; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
-  __syncthreads();
   pdl_wait();
   pdl_trigger();
+  // the unit walk reads one frame mask per unit on its serial path: from shared memory, not L2
+  const uint32_t* pm = posmask;
+  if (g.pm_smem) {
+    uint32_t* pm_s = reinterpret_cast<uint32_t*>(rows + (size_t)g.nbuf * g.T * g.rs);
+    const int npos = g.n_seq * g.hb * g.wb;
+    for (int i = threadIdx.x; i < npos; i += blockDim.x) pm_s[i] = __ldg(posmask + i);
+    pm = pm_s;
+  }
+  __syncthreads();
   const int c = g.c, c3 = 3 * c, T = g.T;
   const size_t plane = (size_t)g.h * g.w;
   const int units = g.n_seq * g.hb * g.wb * g.b * g.b / g.ppu;
@@ -130,8 +146,8 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
   // -- and 16-byte cp.async by all threads were both 1.3x slower.)
   const uint32_t tok_bytes = (uint32_t)c3 * 2;
   const bool kv_only = g.kv_only && g.ppu == 1;
-  auto stage = [&](int buf, int s, size_t pix, int npx, uint32_t Mq) {
-    if (warp == 0) {
+  auto stage = [&](int buf, int s, size_t pix, int npx, uint32_t Mq, bool me) {
+    if (me) {
       uint8_t* dst0 = rows + (size_t)buf * T * g.rs;
       if (!kv_only) {
         if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)(T * npx));
@@ -155,19 +171,31 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
       }
     }
   };
-  uint32_t M;
-  size_t pix;
-  int s, npx;
-  int u = ta_next(blockIdx.x, gridDim.x, units, posmask, g, M, pix, s, npx);
-  if (u >= 0) stage(0, s, pix, npx, M);
+  // staging ring of g.nbuf buffers: unit i of this CTA lives in buffer i % nbuf; after unit i is
+  // computed its buffer is refilled with unit i + nbuf (nbuf - 1 units land while one computes)
+  int uq[kTaMaxBuf], sq[kTaMaxBuf], npq[kTaMaxBuf];
+  uint32_t Mq[kTaMaxBuf];
+  size_t pq[kTaMaxBuf];
+  uint32_t Mn;
+  size_t pixn;
+  int sn, npxn;
+  int un = ta_next(blockIdx.x, gridDim.x, units, pm, g, Mn, pixn, sn, npxn);
+  for (int i = 0; i < g.nbuf; ++i) {
+    uq[i] = un;
+    if (un >= 0) {
+      Mq[i] = Mn; pq[i] = pixn; sq[i] = sn; npq[i] = npxn;
+      stage(i, sn, pixn, npxn, Mn, warp == 0);
+      un = ta_next(un + gridDim.x, gridDim.x, units, pm, g, Mn, pixn, sn, npxn);
+    }
+  }
   uint32_t phase = 0u;  // bit k = parity of buffer k
   int buf = 0;
-  while (u >= 0) {
-    uint32_t Mn;
-    size_t pixn;
-    int sn, npxn;
-    const int un = ta_next(u + gridDim.x, gridDim.x, units, posmask, g, Mn, pixn, sn, npxn);
-    if (un >= 0 && g.nbuf == 2) stage(buf ^ 1, sn, pixn, npxn, Mn);  // prefetch (that buffer is free)
+  const int nwarps = blockDim.x >> 5;
+  int tbase = 0;  // stream mode: index (mod nwarps) of the current unit's first task
+  while (uq[buf] >= 0) {
+    const uint32_t M = Mq[buf];
+    const size_t pix = pq[buf];
+    const int s = sq[buf], npx = npq[buf];
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
     phase ^= 1u << buf;
     const uint32_t tk0 = smem_u32(rows + (size_t)buf * T * g.rs);
@@ -177,7 +205,13 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
     const int mi = lane >> 3, ri = lane & 7;        // ldmatrix: matrix index / row within it
     const int NT = (T + 7) >> 3;                    // key tiles of 8 (<= 4)
     const int ntask = g.heads * mtiles;
-    for (int task2 = warp; task2 < npx * ntask; task2 += kTaThreads / 32) {
+    int first = warp;
+    if (g.stream) {
+      first = warp - tbase;
+      if (first < 0) first += nwarps;
+      tbase = (tbase + npx * ntask) % nwarps;
+    }
+    for (int task2 = first; task2 < npx * ntask; task2 += nwarps) {
       const int pp = task2 / ntask, task = task2 - pp * ntask;  // pixel of the group, (head, m-tile)
       const uint32_t tk = tk0 + (uint32_t)(pp * 6 * c);
       const int hd = task % g.heads, mt = task / g.heads;
@@ -290,10 +324,32 @@ __global__ void __launch_bounds__(kTaThreads) ta_attn_kernel(
           *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][2] * inv1, O[j][3] * inv1);
       }
     }
-    __syncthreads();  // every warp is done with this buffer before it is staged again
-    if (un >= 0 && g.nbuf == 1) stage(0, sn, pixn, npxn, Mn);
-    if (g.nbuf == 2) buf ^= 1;
-    u = un; M = Mn; pix = pixn; s = sn; npx = npxn;
+    bool me = warp == 0;
+    if (g.stream) {
+      // every warp passes every unit (waiting for it to land even without a task in it, so no
+      // warp runs a ring lap ahead of the loads); the last one out restages the buffer
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();  // this warp's reads of the buffer precede its arrival
+        last = atomicAdd(&done[buf], 1) == nwarps - 1;
+        if (last) {
+          done[buf] = 0;
+          __threadfence_block();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+      }
+      me = __shfl_sync(0xffffffffu, last, 0) != 0;
+    } else {
+      __syncthreads();  // every warp is done with this buffer before it is staged again
+    }
+    uq[buf] = un;
+    if (un >= 0) {
+      Mq[buf] = Mn; pq[buf] = pixn; sq[buf] = sn; npq[buf] = npxn;
+      stage(buf, sn, pixn, npxn, Mn, me);
+      un = ta_next(un + gridDim.x, gridDim.x, units, pm, g, Mn, pixn, sn, npxn);
+    }
+    buf = buf + 1 == g.nbuf ? 0 : buf + 1;
   }
 }
 
@@ -343,28 +399,51 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   g.h = h; g.w = w; g.c = c; g.heads = heads; g.T = T; g.b = block; g.hb = hb; g.wb = wb;
   g.n_seq = n_seq;
   g.scale = 1.f / sqrtf((float)kHeadDim);
-  // One pixel per unit, double-buffered (prefetch the next unit during this one) when that still
-  // leaves two resident CTAs per SM; otherwise two single-buffered CTAs are faster (measured:
-  // level 0 66 us double-buffered vs 84 single; level 1 56 double (1 CTA/SM) vs 42 single (2)).
+  // One pixel per unit.  Staging (tools/ta_ab.py, 21 frames at 25% clustered density):
+  //  * the double-buffered ring fits twice per SM (level 0): two CTAs of 8 warps, task stream
+  //    (62 us; 66 with a CTA barrier per unit; 84 single-buffered; one CTA with a 3-5 deep ring
+  //    93-122 us: two CTAs interleaving units beat a deeper ring);
+  //  * it fits once (level 1): one CTA of 16 warps, task stream (39 us; 42 for two single-buffered
+  //    CTAs of 8 warps);
+  //  * it does not fit (level 2): one single-buffered CTA of 16 warps with a barrier per unit
+  //    (26.7 us; 27.4 as a task stream, 28.7 with 8 warps).
   // SPHINX_TA_PPU=2 stages two x-adjacent pixels per unit with one bulk copy per frame:
   // measured slower at level 0 (90 vs 65 us: the larger buffers halve the resident CTAs).
   g.ppu = 1;
-  g.nbuf = ta_smem(c, T, 2) <= 113 * 1024 ? 2 : 1;
-  if (const char* env = getenv("SPHINX_TA_NBUF")) g.nbuf = atoi(env) == 1 ? 1 : g.nbuf;
+  g.nbuf = ta_smem(c, T, 2) <= 227 * 1024 ? 2 : 1;
+  g.stream = g.nbuf == 2 ? 1 : 0;
+  if (const char* env = getenv("SPHINX_TA_NBUF")) {
+    const int nb = atoi(env);
+    if (nb >= 1 && nb <= kTaMaxBuf && ta_smem(c, T, nb) <= 227 * 1024) g.nbuf = nb;
+  }
   if (const char* env = getenv("SPHINX_TA_PPU"))
     if (atoi(env) == 2 && block % 2 == 0 && ta_smem(c, T, g.nbuf, 2) <= 227 * 1024) g.ppu = 2;
   g.kv_only = 0;
   if (const char* env = getenv("SPHINX_TA_KVONLY")) g.kv_only = atoi(env) != 0;
+  if (const char* env = getenv("SPHINX_TA_STREAM")) g.stream = atoi(env) != 0;
   g.rs = (uint32_t)ta_row(c, g.ppu);
-  const size_t smem = ta_smem(c, T, g.nbuf, g.ppu);
+  // resident CTAs per SM by shared memory; the frame masks go to shared memory when that does
+  // not lower it
+  auto fit = [](size_t bytes) {
+    const int k = (int)((228 * 1024) / (bytes + 1024));
+    return k < 1 ? 1 : (k > 8 ? 8 : k);
+  };
+  const size_t pm_bytes = (size_t)n_seq * hb * wb * sizeof(uint32_t);
+  const size_t ring = ta_smem(c, T, g.nbuf, g.ppu);
+  g.pm_smem = pm_bytes <= 8192 && ring + pm_bytes <= 227 * 1024 && fit(ring + pm_bytes) == fit(ring);
+  if (const char* env = getenv("SPHINX_TA_PMSMEM")) g.pm_smem = g.pm_smem && atoi(env) != 0;
+  const size_t smem = ring + (g.pm_smem ? pm_bytes : 0);
+  int per_sm = fit(smem);
+  // one resident CTA per SM (the ring does not fit twice): 16 warps; two CTAs of 8 otherwise
+  int threads = per_sm == 1 ? kTaMaxThreads : kTaThreads;
+  if (const char* env = getenv("SPHINX_TA_THREADS")) threads = atoi(env) == 512 ? 512 : kTaThreads;
+  if (per_sm > 65536 / (threads * 128)) per_sm = 65536 / (threads * 128);  // <= 128 regs/thread
   e = cudaFuncSetAttribute(ta_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return cuda_fail(e);
   const long long units = (long long)n_seq * hb * wb * block * block / g.ppu;
-  int per_sm = (int)((228 * 1024) / (smem + 1024));
-  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
   const long long cap = (long long)sms * per_sm;
   const int grid = (int)(units < cap ? units : cap);
-  e = launch_k(ta_attn_kernel, dim3(grid), dim3(kTaThreads), smem, s, static_cast<const __nv_bfloat16*>(qkv),
+  e = launch_k(ta_attn_kernel, dim3(grid), dim3(threads), smem, s, static_cast<const __nv_bfloat16*>(qkv),
                static_cast<__nv_bfloat16*>(o), static_cast<const uint32_t*>(posmask), g);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
