@@ -972,7 +972,6 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         if (row == 0) cnt[0] = 0;  // leave the counter zeroed for the next launch
        }
       } else {
-#pragma unroll 1
         // a ragged last C_out tile only has p.n_last valid accumulator columns (the rest are
         // beyond C_out: never stored, so they need not be drained or parked either)
         const int width = (nt == p.n_tiles_n - 1 && p.n_last < BN) ? p.n_last : BN;

@@ -62,7 +62,6 @@ __device__ __forceinline__ void lapvar_body(const float* __restrict__ rgb, int h
   float* Ts = Vs + VH * VW;                                 // [VH][SW] sum_dx V (box rows)
   const size_t plane = (size_t)h * w;
   const float* img = rgb + (size_t)n * plane * 3;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   // luminance of the tile + halo: 8 pixels (24 independent loads) in flight per thread (one
   // pixel per iteration left each warp ~11 serial load latencies: ncu's top stall)
   {

@@ -272,13 +272,17 @@ def test_temporal_block_full_size_bench_config(sphinx):
     assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
 
 
-@pytest.mark.parametrize("knob", ["SPHINX_TA_PPU=2", "SPHINX_TA_KVONLY=1"])
+@pytest.mark.parametrize("knob", ["SPHINX_TA_PPU=2", "SPHINX_TA_KVONLY=1", "SPHINX_TA_STREAM=0",
+                                  "SPHINX_TA_STREAM=1,SPHINX_TA_NBUF=1", "SPHINX_TA_NBUF=3",
+                                  "SPHINX_TA_NBUF=5,SPHINX_TA_THREADS=512", "SPHINX_TA_PMSMEM=0"])
 def test_temporal_block_staging_variants(sphinx, monkeypatch, knob):
     """The measured-slower staging variants kept as options -- two x-adjacent pixels per bulk copy
-    (on an odd-width map: ragged last pair), and k|v of all frames + q of listed frames only --
-    equal the oracle like the default path."""
-    k, v = knob.split("=")
-    monkeypatch.setenv(k, v)
+    (on an odd-width map: ragged last pair), k|v of all frames + q of listed frames only, the CTA
+    barrier per unit instead of the task stream, other ring depths / CTA sizes, frame masks read
+    from global memory -- equal the oracle like the default path."""
+    for kv in knob.split(","):
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
     n, h, w, c, T, b = 4, 16, 13, 64, 2, 8
     x = syn.resblock_features_bf16((n, h, w, c), "tbppu")
     qkv_cache = syn.resblock_features_bf16((n, h, w, 3 * c), "tbppu-qc")
