@@ -230,7 +230,7 @@ def summarize_clocks(lines):
 
 def graph_time(torch, fn, reps=20):
     """Device time per call: `reps` calls captured in one CUDA graph and replayed (no host
-    launch overhead in the measurement)."""
+    launch overhead in the measurement); median over 5 replays."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -239,13 +239,16 @@ def graph_time(torch, fn, reps=20):
         for _ in range(reps):
             fn()
     g.replay()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record()
-    g.replay()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    ts = []
+    for _ in range(5):  # median of 5 replays (one replay moved by up to +-25% run to run)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / reps)
+    return sorted(ts)[2]
 
 
 def density_sweep(torch, sp, dev, frames_list=(1, 21, 168), dens=(0.05, 0.10, 0.25, 0.50, 0.75, 1.0)):
