@@ -50,6 +50,10 @@ def test_invalid_arguments_rejected_on_host():
     big = lib.sphinx_conv_workspace_size(168, 16, 16, 32, 32, 4)
     assert small > 4096 and big - small >= (168 - 1) * 16 * 4 - 256
     assert lib.sphinx_conv_workspace_size(0, 16, 16, 32, 32, 4) == 0
+    # _ex: flags outside REUSE_PLAN | LIST_READY | INPUT_READY are rejected before any device query
+    assert (sp.CONV_REUSE_PLAN, sp.CONV_LIST_READY, sp.CONV_INPUT_READY) == (1, 2, 4)
+    assert lib.sphinx_sparse_conv3x3_ex(p, p, null, null, p, sp.BF16, 1, 16, 16, 32, 32, 4, p, p, 16, p,
+                                        1 << 20, 8, null) == sp.ERR_INVALID_ARGUMENT
 
 
 def test_next3_host_validation():
