@@ -13,9 +13,12 @@
 //                    (atomicOr of bits: order-free, deterministic).
 //   ta_attn_kernel   unit = (sequence, block position, pixel) with a non-zero mask: the pixel's
 //                    q|k|v tokens of all T frames are staged in shared memory by T bulk async
-//                    copies (cp.async.bulk + mbarrier), double-buffered so the next pixel's
-//                    tokens land while this one computes; row stride 6C+16 bytes (an odd number
-//                    of 16-byte units: conflict-free ldmatrix rows).
+//                    copies (cp.async.bulk + mbarrier) into a ring of nbuf buffers (the next
+//                    pixels' tokens land while this one computes); row stride 6C+16 bytes (an odd
+//                    number of 16-byte units: conflict-free ldmatrix rows).  With the ring
+//                    double-buffered the warps run a task stream: no CTA barrier per unit, warp w
+//                    takes tasks w, w+nw, ... of the concatenated (unit, head, query tile)
+//                    sequence and the last warp done with a buffer restages it.
 //                    One warp per (head, 16 listed queries): S = Q K^T with mma.sync m16n8k16
 //                    (bf16 in, fp32 accumulate), register softmax (quad shuffles, SFU exp), then
 //                    O = P V with P split into bf16 hi + lo parts (|P - hi - lo| <= 2^-17 P) and
