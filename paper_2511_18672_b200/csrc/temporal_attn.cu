@@ -207,6 +207,8 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
     const int gq = lane >> 2, tq = lane & 3;        // mma fragment row group / thread-in-group
     const int mi = lane >> 3, ri = lane & 7;        // ldmatrix: matrix index / row within it
     const int NT = (T + 7) >> 3;                    // key tiles of 8 (<= 4)
+    // frame of the lane-th listed query (one find-nth-set per lane per unit, shuffled below)
+    const int lfr = lane < nq ? __fns(M, 0, lane + 1) : 0;
     const int ntask = g.heads * mtiles;
     int first = warp;
     if (g.stream) {
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
       for (int j = 0; j < 4; ++j) S[j][0] = S[j][1] = S[j][2] = S[j][3] = 0.f;
       // this lane's ldmatrix row for the Q tile: query (mi & 1) * 8 + ri of the m-tile
       const int qidx = mt * 16 + (mi & 1) * 8 + ri;
-      const int qf = __fns(M, 0, (qidx < nq ? qidx : 0) + 1);
+      const int qf = __shfl_sync(0xffffffffu, lfr, qidx < nq ? qidx : 0);
       const uint32_t qrow = tk + (uint32_t)qf * g.rs + (uint32_t)(hd * kHeadDim + (mi >> 1) * 8) * 2;
 #pragma unroll
       for (int kk = 0; kk < kHeadDim / 16; ++kk) {
@@ -314,14 +316,15 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
       }
       const float inv0 = 1.f / sum0, inv1 = 1.f / sum1;
       const int q0 = mt * 16 + gq, q1 = q0 + 8;
+      const int f0 = __shfl_sync(0xffffffffu, lfr, q0 & 31), f1 = __shfl_sync(0xffffffffu, lfr, q1 & 31);
       if (q0 < nq) {
-        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q0 + 1)) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
+        __nv_bfloat16* dst = o + (((size_t)s * T + f0) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][0] * inv0, O[j][1] * inv0);
       }
       if (q1 < nq) {
-        __nv_bfloat16* dst = o + (((size_t)s * T + __fns(M, 0, q1 + 1)) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
+        __nv_bfloat16* dst = o + (((size_t)s * T + f1) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][2] * inv1, O[j][3] * inv1);

@@ -7,14 +7,16 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.append(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_18672_b200 as sp  # noqa: E402
 import synthetic as syn  # noqa: E402
 
 LEVELS = [(72, 320), (36, 640), (18, 1280)]
-VARIANTS = {0: [(None, None, None), (None, None, 0), (1, 256, 0)],
-            1: [(None, None, None), (None, None, 0), (1, 256, 0)],
-            2: [(None, None, None), (None, None, 1)]}
+VARIANTS = {0: [(None, None, None)], 1: [(None, None, None)], 2: [(None, None, None)]}
+if os.environ.get("TA_AB_ALL"):
+    VARIANTS = {0: [(None, None, None), (None, None, 0), (1, 256, 0)],
+                1: [(None, None, None), (None, None, 0), (1, 256, 0)],
+                2: [(None, None, None), (None, None, 1)]}
 dev = torch.device("cuda", 0)
 n, b, T = 21, 8, 21
 bf = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
