@@ -13,6 +13,9 @@ import synthetic as syn  # noqa: E402
 
 LEVELS = [(72, 320), (36, 640), (18, 1280)]
 VARIANTS = {0: [(None, None, None)], 1: [(None, None, None)], 2: [(None, None, None)]}
+if os.environ.get("TA_AB_PPU"):
+    VARIANTS = {0: [(None, None, None), ("ppu2", None, None), ("ppu2", 256, None), ("ppu2", None, 0)],
+                1: [(None, None, None)], 2: [(None, None, None)]}
 if os.environ.get("TA_AB_ALL"):
     VARIANTS = {0: [(None, None, None), (None, None, 0), (1, 256, 0)],
                 1: [(None, None, None), (None, None, 0), (1, 256, 0)],
@@ -36,6 +39,10 @@ for l, (h, c) in enumerate(LEVELS):
     ws = sp.attn_workspace(n, h, h, T, b, dev) if hasattr(sp, "attn_workspace") else None
     ref = None
     for nb, th, pm in VARIANTS[l]:
+        os.environ.pop("SPHINX_TA_PPU", None)
+        if nb == "ppu2":
+            os.environ["SPHINX_TA_PPU"] = "2"
+            nb = None
         for k, v in (("SPHINX_TA_NBUF", nb), ("SPHINX_TA_THREADS", th), ("SPHINX_TA_STREAM", pm)):
             if v is None:
                 os.environ.pop(k, None)
