@@ -12,8 +12,9 @@
 //   ta_plan_kernel   one CTA: per (sequence, block position) a bitmask of listed frames
 //                    (atomicOr of bits: order-free, deterministic).
 //   ta_attn_kernel   unit = (sequence, block position, pixel) with a non-zero mask: the pixel's
-//                    q|k|v tokens of all T frames are staged in shared memory by T bulk async
-//                    copies (cp.async.bulk + mbarrier) into a ring of nbuf buffers (the next
+//                    q|k|v tokens of all T frames are staged in shared memory -- one 4-D TMA
+//                    tensor copy (128-B swizzled rows) with the double-buffered ring, else T
+//                    bulk async copies (cp.async.bulk + mbarrier) -- into a ring of nbuf buffers (the next
 //                    pixels' tokens land while this one computes); row stride 6C+16 bytes (an odd
 //                    number of 16-byte units: conflict-free ldmatrix rows).  With the ring
 //                    double-buffered the warps run a task stream: no CTA barrier per unit, warp w
@@ -26,7 +27,10 @@
 // Per (pixel, head) the contraction is tiny (<= 32 x 32 x 64): warp-level mma.sync is the right
 // tensor-core granularity (a CTA-wide tcgen05 tile would be >90% padding); the kernel is bound by
 // staging the T tokens of every pixel with a listed frame (HBM/L2), not by the math.
+#include <cuda.h>
 #include <cuda_bf16.h>
+
+#include <cstring>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -80,6 +84,9 @@ struct TaGeom {
   int h, w, c, heads, T, b, hb, wb, n_seq, nbuf;
   int ppu;      // pixels per unit: 2 = two x-adjacent pixels share one bulk copy per frame
   int kv_only;  // stage k|v of every frame + q of listed frames only (one-pixel units)
+  int tmode;    // one TMA tensor copy per unit (4-D map: 64-element rows x 3C/64 x pixels x
+                // frames, 128-B swizzle); staged rows are then swizzled, stride 6C
+  uint32_t bstride;  // bytes per staging buffer
   int pm_smem;  // the per-position frame masks are copied to shared memory (after the ring)
   int stream;   // task stream: no CTA barrier per unit; warp w takes tasks w, w+nw, ... of the
                 // concatenated (unit, head, query tile) sequence; the last warp done with a
@@ -112,10 +119,14 @@ __device__ __forceinline__ int ta_next(int u, int step, int units,
 }
 
 __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
-    const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* o, const uint32_t* __restrict__ posmask,
-    const TaGeom g) {
+    const __grid_constant__ CUtensorMap tm, const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* o,
+    const uint32_t* __restrict__ posmask, const TaGeom g) {
   extern __shared__ __align__(128) uint8_t ta_sm[];
-  uint8_t* rows = ta_sm + 128;
+  // staging buffers start at the first 1024-byte boundary past the 128-byte header (the 128-B
+  // swizzle of tensor mode repeats every 1024 B of shared address space)
+  const uint32_t sm0 = smem_u32(ta_sm);
+  uint8_t* rows = ta_sm + (g.tmode ? (((sm0 + 128u + 1023u) & ~1023u) - sm0) : 128u);
+  auto swz = [&](uint32_t a) { return g.tmode ? (a ^ (((a >> 7) & 7u) << 4)) : a; };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ta_sm);
   // a 16-byte zero row at offset 64: ldmatrix rows of padded keys (>= T) point here
@@ -133,7 +144,7 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
   // the unit walk reads one frame mask per unit on its serial path: from shared memory, not L2
   const uint32_t* pm = posmask;
   if (g.pm_smem) {
-    uint32_t* pm_s = reinterpret_cast<uint32_t*>(rows + (size_t)g.nbuf * g.T * g.rs);
+    uint32_t* pm_s = reinterpret_cast<uint32_t*>(rows + (size_t)g.nbuf * g.bstride);
     const int npos = g.n_seq * g.hb * g.wb;
     for (int i = threadIdx.x; i < npos; i += blockDim.x) pm_s[i] = __ldg(posmask + i);
     pm = pm_s;
@@ -151,8 +162,13 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
   const bool kv_only = g.kv_only && g.ppu == 1;
   auto stage = [&](int buf, int s, size_t pix, int npx, uint32_t Mq, bool me) {
     if (me) {
-      uint8_t* dst0 = rows + (size_t)buf * T * g.rs;
-      if (!kv_only) {
+      uint8_t* dst0 = rows + (size_t)buf * g.bstride;
+      if (g.tmode) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)T);
+          tma_load_4d(&tm, &bars[buf], dst0, 0, 0, (int)pix, s * T, policy_evict_normal());
+        }
+      } else if (!kv_only) {
         if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)(T * npx));
         __syncwarp();
         if (lane < T)
@@ -201,7 +217,7 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
     const int s = sq[buf], npx = npq[buf];
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
     phase ^= 1u << buf;
-    const uint32_t tk0 = smem_u32(rows + (size_t)buf * T * g.rs);
+    const uint32_t tk0 = smem_u32(rows + (size_t)buf * g.bstride);
     const int nq = __popc(M);
     const int mtiles = (nq + 15) >> 4;
     const int gq = lane >> 2, tq = lane & 3;        // mma fragment row group / thread-in-group
@@ -231,14 +247,14 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
 #pragma unroll
       for (int kk = 0; kk < kHeadDim / 16; ++kk) {
         uint32_t a[4];
-        ldsm_x4(qrow + kk * 32, a);
+        ldsm_x4(swz(qrow + kk * 32), a);
 #pragma unroll
         for (int j = 0; j < 4; j += 2) {
           if (j >= NT) break;
           // matrices: (keys 8j.., dims lo), (keys 8j.., dims hi), (keys 8j+8.., lo), (.., hi)
           const int key = 8 * (j + (mi >> 1)) + ri;
-          const uint32_t addr = key < T ? tk + (uint32_t)key * g.rs + (uint32_t)(c + hd * kHeadDim + kk * 16 +
-                                                                               (mi & 1) * 8) * 2
+          const uint32_t addr = key < T ? swz(tk + (uint32_t)key * g.rs + (uint32_t)(c + hd * kHeadDim + kk * 16 +
+                                                                                   (mi & 1) * 8) * 2)
                                         : zero_row;
           uint32_t bm[4];
           ldsm_x4(addr, bm);
@@ -303,8 +319,8 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
         const int key = 16 * k2 + (mi & 1) * 8 + ri;
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) {
-          const uint32_t addr = key < T ? tk + (uint32_t)key * g.rs +
-                                              (uint32_t)(2 * c + hd * kHeadDim + jn * 16 + (mi >> 1) * 8) * 2
+          const uint32_t addr = key < T ? swz(tk + (uint32_t)key * g.rs +
+                                                  (uint32_t)(2 * c + hd * kHeadDim + jn * 16 + (mi >> 1) * 8) * 2)
                                         : zero_row;
           uint32_t bv[4];
           ldsm_x4_t(addr, bv);
@@ -361,6 +377,26 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
 
 static size_t ta_row(int c, int ppu = 1) { return (size_t)ppu * 6 * c + 16; }
 static size_t ta_smem(int c, int T, int nbuf, int ppu = 1) { return 128 + (size_t)nbuf * T * ta_row(c, ppu); }
+// tensor mode: 1024-aligned buffers of T unpadded 6C-byte rows (+1024 alignment slack)
+static size_t ta_tbuf(int c, int T) { return ((size_t)T * 6 * c + 1023) / 1024 * 1024; }
+static size_t ta_smem_t(int c, int T, int nbuf) { return 128 + 1024 + (size_t)nbuf * ta_tbuf(c, T); }
+
+typedef CUresult (*PFN_taEncodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                        const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                        const cuuint32_t*, CUtensorMapInterleave,
+                                        CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                        CUtensorMapFloatOOBfill);
+static PFN_taEncodeTiled_t ta_encode_tiled() {
+  static PFN_taEncodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_taEncodeTiled_t>(ptr);
+  }
+  return fn;
+}
 
 }  // namespace sphinx
 
@@ -428,6 +464,31 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   if (const char* env = getenv("SPHINX_TA_KVONLY")) g.kv_only = atoi(env) != 0;
   if (const char* env = getenv("SPHINX_TA_STREAM")) g.stream = atoi(env) != 0;
   g.rs = (uint32_t)ta_row(c, g.ppu);
+  g.bstride = (uint32_t)((size_t)T * g.rs);
+  // tensor mode: one 4-D TMA copy per unit instead of T bulk copies (the staging is bulk-op-rate
+  // bound).  Default with the double-buffered ring (levels 0/1: 65.5 -> 55.5 and 40.1 -> 35.5 us
+  // same-box); single-buffered (level 2) it measured slower (27.3 -> 29.7 us).
+  // SPHINX_TA_TMAP=0/1 overrides.
+  bool want_t = g.nbuf == 2;
+  if (const char* env = getenv("SPHINX_TA_TMAP")) want_t = atoi(env) != 0;
+  g.tmode = want_t && g.ppu == 1 && !g.kv_only && (3 * c) % 64 == 0 && 3 * c / 64 <= 256 &&
+            ta_smem_t(c, T, g.nbuf) <= 227 * 1024;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  if (g.tmode) {
+    g.rs = (uint32_t)(6 * c);
+    g.bstride = (uint32_t)ta_tbuf(c, T);
+    PFN_taEncodeTiled_t enc = ta_encode_tiled();
+    if (!enc) return SPHINX_ERR_CUDA;
+    const cuuint64_t dims[4] = {64, (cuuint64_t)(3 * c / 64), (cuuint64_t)h * w, (cuuint64_t)n};
+    const cuuint64_t strides[3] = {128, (cuuint64_t)(3 * c) * 2, (cuuint64_t)h * w * 3 * c * 2};
+    const cuuint32_t box[4] = {64, (cuuint32_t)(3 * c / 64), 1, (cuuint32_t)T};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(qkv), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return SPHINX_ERR_UNSUPPORTED;
+  }
   // resident CTAs per SM by shared memory; the frame masks go to shared memory when that does
   // not lower it
   auto fit = [](size_t bytes) {
@@ -435,7 +496,7 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
     return k < 1 ? 1 : (k > 8 ? 8 : k);
   };
   const size_t pm_bytes = (size_t)n_seq * hb * wb * sizeof(uint32_t);
-  const size_t ring = ta_smem(c, T, g.nbuf, g.ppu);
+  const size_t ring = g.tmode ? ta_smem_t(c, T, g.nbuf) : ta_smem(c, T, g.nbuf, g.ppu);
   g.pm_smem = pm_bytes <= 8192 && ring + pm_bytes <= 227 * 1024 && fit(ring + pm_bytes) == fit(ring);
   if (const char* env = getenv("SPHINX_TA_PMSMEM")) g.pm_smem = g.pm_smem && atoi(env) != 0;
   const size_t smem = ring + (g.pm_smem ? pm_bytes : 0);
@@ -449,7 +510,7 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   const long long units = (long long)n_seq * hb * wb * block * block / g.ppu;
   const long long cap = (long long)sms * per_sm;
   const int grid = (int)(units < cap ? units : cap);
-  e = launch_k(ta_attn_kernel, dim3(grid), dim3(threads), smem, s, static_cast<const __nv_bfloat16*>(qkv),
+  e = launch_k(ta_attn_kernel, dim3(grid), dim3(threads), smem, s, tm, static_cast<const __nv_bfloat16*>(qkv),
                static_cast<__nv_bfloat16*>(o), static_cast<const uint32_t*>(posmask), g);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;

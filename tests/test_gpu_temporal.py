@@ -274,12 +274,15 @@ def test_temporal_block_full_size_bench_config(sphinx):
 
 @pytest.mark.parametrize("knob", ["SPHINX_TA_PPU=2", "SPHINX_TA_KVONLY=1", "SPHINX_TA_STREAM=0",
                                   "SPHINX_TA_STREAM=1,SPHINX_TA_NBUF=1", "SPHINX_TA_NBUF=3",
-                                  "SPHINX_TA_NBUF=5,SPHINX_TA_THREADS=512", "SPHINX_TA_PMSMEM=0"])
+                                  "SPHINX_TA_NBUF=5,SPHINX_TA_THREADS=512", "SPHINX_TA_PMSMEM=0",
+                                  "SPHINX_TA_TMAP=0", "SPHINX_TA_TMAP=1,SPHINX_TA_NBUF=1",
+                                  "SPHINX_TA_TMAP=1,SPHINX_TA_NBUF=3"])
 def test_temporal_block_staging_variants(sphinx, monkeypatch, knob):
     """The measured-slower staging variants kept as options -- two x-adjacent pixels per bulk copy
     (on an odd-width map: ragged last pair), k|v of all frames + q of listed frames only, the CTA
     barrier per unit instead of the task stream, other ring depths / CTA sizes, frame masks read
-    from global memory -- equal the oracle like the default path."""
+    from global memory, T bulk copies instead of the one TMA tensor copy per unit (and the tensor
+    copy single-buffered / 3-deep) -- equal the oracle like the default path."""
     for kv in knob.split(","):
         k, v = kv.split("=")
         monkeypatch.setenv(k, v)

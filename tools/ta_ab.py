@@ -13,6 +13,9 @@ import synthetic as syn  # noqa: E402
 
 LEVELS = [(72, 320), (36, 640), (18, 1280)]
 VARIANTS = {0: [(None, None, None)], 1: [(None, None, None)], 2: [(None, None, None)]}
+if os.environ.get("TA_AB_TMAP"):
+    VARIANTS = {0: [(None, None, None), ("notmap", None, None)], 1: [(None, None, None), ("notmap", None, None)],
+                2: [(None, None, None), ("tmap", None, None)]}
 if os.environ.get("TA_AB_PPU"):
     VARIANTS = {0: [(None, None, None), ("ppu2", None, None), ("ppu2", 256, None), ("ppu2", None, 0)],
                 1: [(None, None, None)], 2: [(None, None, None)]}
@@ -40,6 +43,10 @@ for l, (h, c) in enumerate(LEVELS):
     ref = None
     for nb, th, pm in VARIANTS[l]:
         os.environ.pop("SPHINX_TA_PPU", None)
+        os.environ.pop("SPHINX_TA_TMAP", None)
+        if nb in ("tmap", "notmap"):
+            os.environ["SPHINX_TA_TMAP"] = "1" if nb == "tmap" else "0"
+            nb = None
         if nb == "ppu2":
             os.environ["SPHINX_TA_PPU"] = "2"
             nb = None
