@@ -441,8 +441,9 @@ SPHINX_API sphinx_status sphinx_sparse_pointwise(
  * o    bf16 NHWC [N][h][w][c].  qkv and o 16-byte aligned; c / heads must be 64;
  *      frames_per_seq <= 32 and divides N; 128 + frames_per_seq * (6c + 16) bytes <= 227 KB
  *      (else UNSUPPORTED).  A pixel's frames_per_seq tokens are staged in shared memory by one
- *      TMA tensor copy when two staging buffers fit, else by frames_per_seq bulk copies
- *      (identical results; SPHINX_ERR_UNSUPPORTED if the driver rejects the tensor map).
+ *      TMA tensor copy when two staging buffers fit (else per (pixel, group of heads) when
+ *      a group's buffers fit twice per SM, else by frames_per_seq bulk copies); identical
+ *      results; SPHINX_ERR_UNSUPPORTED if the driver rejects the tensor map.
  * workspace  sphinx_temporal_attention_workspace_size(...) bytes (4-byte aligned): the per
  *      (sequence, block position) listed-frame bitmasks, rebuilt by every call. */
 SPHINX_API size_t sphinx_temporal_attention_workspace_size(int32_t n, int32_t h, int32_t w,

@@ -13,7 +13,8 @@
 //                    (atomicOr of bits: order-free, deterministic).
 //   ta_attn_kernel   unit = (sequence, block position, pixel) with a non-zero mask: the pixel's
 //                    q|k|v tokens of all T frames are staged in shared memory -- one 4-D TMA
-//                    tensor copy (128-B swizzled rows) with the double-buffered ring, else T
+//                    tensor copy (128-B swizzled rows) with the double-buffered ring (on wide
+//                    levels a unit is a (pixel, head group) so that ring fits twice), else T
 //                    bulk async copies (cp.async.bulk + mbarrier) -- into a ring of nbuf buffers (the next
 //                    pixels' tokens land while this one computes); row stride 6C+16 bytes (an odd
 //                    number of 16-byte units: conflict-free ldmatrix rows).  With the ring
@@ -87,6 +88,7 @@ struct TaGeom {
   int tmode;    // one TMA tensor copy per unit (4-D map: 64-element rows x 3C/64 x pixels x
                 // frames, 128-B swizzle); staged rows are then swizzled, stride 6C
   uint32_t bstride;  // bytes per staging buffer
+  int ngrp, hpg;     // tensor mode: head groups per pixel (one unit each), heads per group
   int pm_smem;  // the per-position frame masks are copied to shared memory (after the ring)
   int stream;   // task stream: no CTA barrier per unit; warp w takes tasks w, w+nw, ... of the
                 // concatenated (unit, head, query tile) sequence; the last warp done with a
@@ -103,8 +105,9 @@ __device__ __forceinline__ int ta_next(int u, int step, int units,
                                        uint32_t& M, size_t& pix, int& s, int& npx) {
   const int nblk = g.hb * g.wb, bbu = g.b * g.b / g.ppu;
   for (; u < units; u += step) {
-    s = u / (nblk * bbu);
-    const int r = u - s * nblk * bbu;
+    const int u0 = u / g.ngrp;  // unit = (pixel unit, head group), group fastest
+    s = u0 / (nblk * bbu);
+    const int r = u0 - s * nblk * bbu;
     const int pos = r / bbu, px = (r - pos * bbu) * g.ppu;
     M = posmask[s * nblk + pos];  // shared (pm_smem) or global
     if (M == 0u) continue;
@@ -152,7 +155,8 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
   __syncthreads();
   const int c = g.c, c3 = 3 * c, T = g.T;
   const size_t plane = (size_t)g.h * g.w;
-  const int units = g.n_seq * g.hb * g.wb * g.b * g.b / g.ppu;
+  const int units = g.n_seq * g.hb * g.wb * g.b * g.b / g.ppu * g.ngrp;
+  const int cs = g.hpg * kHeadDim;  // channels of one staged q (k, v) part
   // warp 0 stages the pixel's T tokens (q|k|v rows, contiguous per frame) with T bulk async copies
   // onto an mbarrier, lane m issuing frame m's copy (one issuing thread was TMA-op-rate bound:
   // ~T ops back to back per pixel).  Lane 0 posts the expected bytes before any copy is issued.
@@ -160,13 +164,18 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
   // -- and 16-byte cp.async by all threads were both 1.3x slower.)
   const uint32_t tok_bytes = (uint32_t)c3 * 2;
   const bool kv_only = g.kv_only && g.ppu == 1;
-  auto stage = [&](int buf, int s, size_t pix, int npx, uint32_t Mq, bool me) {
+  auto stage = [&](int buf, int s, size_t pix, int npx, uint32_t Mq, bool me, int grp) {
     if (me) {
       uint8_t* dst0 = rows + (size_t)buf * g.bstride;
       if (g.tmode) {
         if (lane == 0) {
-          mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)T);
-          tma_load_4d(&tm, &bars[buf], dst0, 0, 0, (int)pix, s * T, policy_evict_normal());
+          mbar_arrive_expect_tx(&bars[buf], (uint32_t)(6 * cs) * (uint32_t)T);
+          asm volatile(
+              "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst0)),
+              "l"(reinterpret_cast<uint64_t>(&tm)), "r"(smem_u32(&bars[buf])), "r"(0), "r"(grp * g.hpg),
+              "r"(0), "r"((int)pix), "r"(s * T)
+              : "memory");
         }
       } else if (!kv_only) {
         if (lane == 0) mbar_arrive_expect_tx(&bars[buf], tok_bytes * (uint32_t)(T * npx));
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
     uq[i] = un;
     if (un >= 0) {
       Mq[i] = Mn; pq[i] = pixn; sq[i] = sn; npq[i] = npxn;
-      stage(i, sn, pixn, npxn, Mn, warp == 0);
+      stage(i, sn, pixn, npxn, Mn, warp == 0, un % g.ngrp);
       un = ta_next(un + gridDim.x, gridDim.x, units, pm, g, Mn, pixn, sn, npxn);
     }
   }
@@ -225,7 +234,8 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
     const int NT = (T + 7) >> 3;                    // key tiles of 8 (<= 4)
     // frame of the lane-th listed query (one find-nth-set per lane per unit, shuffled below)
     const int lfr = lane < nq ? __fns(M, 0, lane + 1) : 0;
-    const int ntask = g.heads * mtiles;
+    const int ntask = g.hpg * mtiles;
+    const int grp = uq[buf] % g.ngrp;
     int first = warp;
     if (g.stream) {
       first = warp - tbase;
@@ -234,8 +244,8 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
     }
     for (int task2 = first; task2 < npx * ntask; task2 += nwarps) {
       const int pp = task2 / ntask, task = task2 - pp * ntask;  // pixel of the group, (head, m-tile)
-      const uint32_t tk = tk0 + (uint32_t)(pp * 6 * c);
-      const int hd = task % g.heads, mt = task / g.heads;
+      const uint32_t tk = tk0 + (uint32_t)(pp * 6 * cs);
+      const int hd = task % g.hpg, mt = task / g.hpg;
       // ---- S = Q K^T on the tensor cores (bf16 products exact, fp32 accumulation)
       float S[4][4];
 #pragma unroll
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
           if (j >= NT) break;
           // matrices: (keys 8j.., dims lo), (keys 8j.., dims hi), (keys 8j+8.., lo), (.., hi)
           const int key = 8 * (j + (mi >> 1)) + ri;
-          const uint32_t addr = key < T ? swz(tk + (uint32_t)key * g.rs + (uint32_t)(c + hd * kHeadDim + kk * 16 +
+          const uint32_t addr = key < T ? swz(tk + (uint32_t)key * g.rs + (uint32_t)(cs + hd * kHeadDim + kk * 16 +
                                                                                    (mi & 1) * 8) * 2)
                                         : zero_row;
           uint32_t bm[4];
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) {
           const uint32_t addr = key < T ? swz(tk + (uint32_t)key * g.rs +
-                                                  (uint32_t)(2 * c + hd * kHeadDim + jn * 16 + (mi >> 1) * 8) * 2)
+                                                  (uint32_t)(2 * cs + hd * kHeadDim + jn * 16 + (mi >> 1) * 8) * 2)
                                         : zero_row;
           uint32_t bv[4];
           ldsm_x4_t(addr, bv);
@@ -334,13 +344,13 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
       const int q0 = mt * 16 + gq, q1 = q0 + 8;
       const int f0 = __shfl_sync(0xffffffffu, lfr, q0 & 31), f1 = __shfl_sync(0xffffffffu, lfr, q1 & 31);
       if (q0 < nq) {
-        __nv_bfloat16* dst = o + (((size_t)s * T + f0) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
+        __nv_bfloat16* dst = o + (((size_t)s * T + f0) * plane + pix + pp) * c + (grp * g.hpg + hd) * kHeadDim + 2 * tq;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][0] * inv0, O[j][1] * inv0);
       }
       if (q1 < nq) {
-        __nv_bfloat16* dst = o + (((size_t)s * T + f1) * plane + pix + pp) * c + hd * kHeadDim + 2 * tq;
+        __nv_bfloat16* dst = o + (((size_t)s * T + f1) * plane + pix + pp) * c + (grp * g.hpg + hd) * kHeadDim + 2 * tq;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<uint32_t*>(dst + 8 * j) = pack_bf16(O[j][2] * inv1, O[j][3] * inv1);
@@ -368,7 +378,7 @@ __global__ void __launch_bounds__(kTaMaxThreads) ta_attn_kernel(
     uq[buf] = un;
     if (un >= 0) {
       Mq[buf] = Mn; pq[buf] = pixn; sq[buf] = sn; npq[buf] = npxn;
-      stage(buf, sn, pixn, npxn, Mn, me);
+      stage(buf, sn, pixn, npxn, Mn, me, un % g.ngrp);
       un = ta_next(un + gridDim.x, gridDim.x, units, pm, g, Mn, pixn, sn, npxn);
     }
     buf = buf + 1 == g.nbuf ? 0 : buf + 1;
@@ -473,18 +483,48 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   if (const char* env = getenv("SPHINX_TA_TMAP")) want_t = atoi(env) != 0;
   g.tmode = want_t && g.ppu == 1 && !g.kv_only && (3 * c) % 64 == 0 && 3 * c / 64 <= 256 &&
             ta_smem_t(c, T, g.nbuf) <= 227 * 1024;
+  // head groups (SPHINX_TA_HGROUP=k heads per unit, tensor mode): a unit stages the q|k|v slices of
+  // k heads only, so wide levels get the small double-buffered ring of level 0
+  // Default: when even the double-buffered ring of all heads does not fit (level 2), the largest
+  // group whose ring fits twice per SM (same box, level 2: 27.9 -> 21.2 us with 5-head groups;
+  // 10-head groups 22.1, 4-head 24.4; level 1 unchanged within noise, so it keeps all heads).
+  g.hpg = heads;
+  g.ngrp = 1;
+  int want_k = 0;
+  if (g.nbuf == 1 && g.ppu == 1 && !g.kv_only)
+    for (int k = heads - 1; k >= 1; --k)
+      if (heads % k == 0 && ta_smem_t(k * kHeadDim, T, 2) <= 113 * 1024) {
+        want_k = k;
+        break;
+      }
+  if (const char* env = getenv("SPHINX_TA_HGROUP")) want_k = atoi(env);
+  {
+    const int k = want_k;
+    if (k >= 1 && k < heads && heads % k == 0 && g.ppu == 1 && !g.kv_only &&
+        (long long)n_seq * hb * wb * block * block * (heads / k) < (1ll << 31)) {
+      g.hpg = k;
+      g.ngrp = heads / k;
+      g.nbuf = ta_smem_t(k * kHeadDim, T, 2) <= 227 * 1024 ? 2 : 1;
+      g.stream = g.nbuf == 2 ? 1 : 0;
+      if (const char* e2 = getenv("SPHINX_TA_STREAM")) g.stream = atoi(e2) != 0;
+      g.tmode = 1;
+    }
+  }
+  const int cs = g.hpg * kHeadDim;
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   if (g.tmode) {
-    g.rs = (uint32_t)(6 * c);
-    g.bstride = (uint32_t)ta_tbuf(c, T);
+    g.rs = (uint32_t)(6 * cs);
+    g.bstride = (uint32_t)ta_tbuf(cs, T);
     PFN_taEncodeTiled_t enc = ta_encode_tiled();
     if (!enc) return SPHINX_ERR_CUDA;
-    const cuuint64_t dims[4] = {64, (cuuint64_t)(3 * c / 64), (cuuint64_t)h * w, (cuuint64_t)n};
-    const cuuint64_t strides[3] = {128, (cuuint64_t)(3 * c) * 2, (cuuint64_t)h * w * 3 * c * 2};
-    const cuuint32_t box[4] = {64, (cuuint32_t)(3 * c / 64), 1, (cuuint32_t)T};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(qkv), dims, strides, box, estr,
+    // 5-D: 64-element rows x C/64 x {q, k, v} x pixels x frames; box = one head group's rows
+    const cuuint64_t dims[5] = {64, (cuuint64_t)(c / 64), 3, (cuuint64_t)h * w, (cuuint64_t)n};
+    const cuuint64_t strides[4] = {128, (cuuint64_t)c * 2, (cuuint64_t)(3 * c) * 2,
+                                   (cuuint64_t)h * w * 3 * c * 2};
+    const cuuint32_t box[5] = {64, (cuuint32_t)g.hpg, 3, 1, (cuuint32_t)T};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(qkv), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return SPHINX_ERR_UNSUPPORTED;
@@ -496,7 +536,7 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
     return k < 1 ? 1 : (k > 8 ? 8 : k);
   };
   const size_t pm_bytes = (size_t)n_seq * hb * wb * sizeof(uint32_t);
-  const size_t ring = g.tmode ? ta_smem_t(c, T, g.nbuf) : ta_smem(c, T, g.nbuf, g.ppu);
+  const size_t ring = g.tmode ? ta_smem_t(cs, T, g.nbuf) : ta_smem(c, T, g.nbuf, g.ppu);
   g.pm_smem = pm_bytes <= 8192 && ring + pm_bytes <= 227 * 1024 && fit(ring + pm_bytes) == fit(ring);
   if (const char* env = getenv("SPHINX_TA_PMSMEM")) g.pm_smem = g.pm_smem && atoi(env) != 0;
   const size_t smem = ring + (g.pm_smem ? pm_bytes : 0);
@@ -507,7 +547,7 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   if (per_sm > 65536 / (threads * 128)) per_sm = 65536 / (threads * 128);  // <= 128 regs/thread
   e = cudaFuncSetAttribute(ta_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return cuda_fail(e);
-  const long long units = (long long)n_seq * hb * wb * block * block / g.ppu;
+  const long long units = (long long)n_seq * hb * wb * block * block / g.ppu * g.ngrp;
   const long long cap = (long long)sms * per_sm;
   const int grid = (int)(units < cap ? units : cap);
   e = launch_k(ta_attn_kernel, dim3(grid), dim3(threads), smem, s, tm, static_cast<const __nv_bfloat16*>(qkv),

@@ -302,3 +302,16 @@ def test_temporal_block_staging_variants(sphinx, monkeypatch, knob):
     tol = 2 * half_ulp(o["o_pre"]) + E_o + 2.0 ** -23 * np.abs(o["y"]) + 1e-7
     err = np.abs(tb.y.cpu().numpy().astype(np.float64) - o["y"])
     assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
+
+
+@pytest.mark.parametrize("k,case", [
+    (5, (6, 18, 18, 640, 3, 8, 0.5, "scattered", True)),
+    (5, (4, 18, 18, 1280, 4, 8, 0.5, "scattered", False)),
+    (10, (4, 16, 16, 1280, 4, 8, 0.5, "checker", True)),
+    (1, (4, 18, 18, 1280, 4, 8, 0.5, "scattered", False)),
+])
+def test_temporal_block_head_groups(sphinx, monkeypatch, k, case):
+    """SPHINX_TA_HGROUP=k: units of (pixel, k heads) staged by one 5-D tensor copy of the group's
+    q|k|v slices -- equal to the oracle like the default path."""
+    monkeypatch.setenv("SPHINX_TA_HGROUP", str(k))
+    test_temporal_block_vs_oracle(sphinx, *case)

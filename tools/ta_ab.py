@@ -16,6 +16,9 @@ VARIANTS = {0: [(None, None, None)], 1: [(None, None, None)], 2: [(None, None, N
 if os.environ.get("TA_AB_TMAP"):
     VARIANTS = {0: [(None, None, None), ("notmap", None, None)], 1: [(None, None, None), ("notmap", None, None)],
                 2: [(None, None, None), ("tmap", None, None)]}
+if os.environ.get("TA_AB_HG"):
+    VARIANTS = {0: [(None, None, None)], 1: [(None, None, None), ("hg5", None, None)],
+                2: [(None, None, None), ("hg0", None, None), ("hg10", None, None)]}
 if os.environ.get("TA_AB_PPU"):
     VARIANTS = {0: [(None, None, None), ("ppu2", None, None), ("ppu2", 256, None), ("ppu2", None, 0)],
                 1: [(None, None, None)], 2: [(None, None, None)]}
@@ -44,6 +47,10 @@ for l, (h, c) in enumerate(LEVELS):
     for nb, th, pm in VARIANTS[l]:
         os.environ.pop("SPHINX_TA_PPU", None)
         os.environ.pop("SPHINX_TA_TMAP", None)
+        os.environ.pop("SPHINX_TA_HGROUP", None)
+        if isinstance(nb, str) and nb.startswith("hg"):
+            os.environ["SPHINX_TA_HGROUP"] = nb[2:]
+            nb = None
         if nb in ("tmap", "notmap"):
             os.environ["SPHINX_TA_TMAP"] = "1" if nb == "tmap" else "0"
             nb = None
