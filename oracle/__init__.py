@@ -10,7 +10,9 @@ through ctypes.
 
 Parity status per function:
   pixel_mask / maxpool / tile_blocks / block_mask   pinned (TV-1..5, brute force)
-  eq2 / select_k / start_step                       pinned (S:125-127, S:143-145, TV-6..8);
+  eq2 / select_k / start_step                       pinned (TV-6..8; gamma=0.5
+                                                    is the correctly rounded sqrt, checked exactly
+                                                    with rationals; realized-ratio cut points);
                                                     the k-logic TABLE values are parity unpinned
                                                     (Fig. k_logic is an image)
   compact                                           pinned (popcount, brute-force order, identity)
@@ -111,6 +113,8 @@ def load():
             fn.restype = ctypes.c_int
         _lib.oracle_eq2.argtypes = [D, D, D, D]
         _lib.oracle_eq2.restype = D
+        _lib.oracle_eq2_batch.argtypes = [P, P, P, D, I, P]
+        _lib.oracle_eq2_batch.restype = None
         _lib.oracle_select_k.argtypes = [P, D]
         _lib.oracle_select_k.restype = ctypes.c_int32
         _lib.oracle_bf16_rne.argtypes = [D]
@@ -188,6 +192,13 @@ def block_mask(O, U, tau_u, tau_o, f, b, n_levels):
 
 def eq2(c0, c1, t, gamma):
     return load().oracle_eq2(c0, c1, t, gamma)
+
+
+def eq2_batch(c0, c1, t, gamma):
+    c0 = _c(c0, np.float64); c1 = _c(c1, np.float64); t = _c(t, np.float64)
+    out = np.empty(len(t), np.float64)
+    load().oracle_eq2_batch(_p(c0), _p(c1), _p(t), float(gamma), len(t), _p(out))
+    return out
 
 
 def select_k(logic, r):

@@ -121,13 +121,28 @@ int oracle_block_mask(const float* O, const float* U, const float* tau_u, float 
 
 /* ---------------------------------------------------------------- a2 ---- */
 
+/* x^gamma with the exact definitions where they exist (reading R-16): x^1 = x and
+ * x^(1/2) = sqrt(x), which C99 / IEEE 754 round correctly.  glibc pow(x, 0.5) is NOT
+ * correctly rounded (it differs from sqrt for ~1.4e5 fp32 inputs in [2^-20, 1]), so it
+ * is used only for the remaining gamma, where no exact reference exists. */
+static double eq2_pow(double x, double gamma) {
+  if (gamma == 1.0) return x;
+  if (gamma == 0.5) return sqrt(x);
+  return pow(x, gamma);
+}
+
 /* Eq. 2: Q* = c0 + (c1 - c0) f(t); f = t^gamma if c1 >= c0,
  * else 1 - (1 - t)^gamma.  Literal transcription (reading R-11). */
 double oracle_eq2(double c0, double c1, double t, double gamma) {
   double f;
-  if (c1 >= c0) f = pow(t, gamma);
-  else f = 1.0 - pow(1.0 - t, gamma);
+  if (c1 >= c0) f = eq2_pow(t, gamma);
+  else f = 1.0 - eq2_pow(1.0 - t, gamma);
   return c0 + (c1 - c0) * f;
+}
+
+void oracle_eq2_batch(const double* c0, const double* c1, const double* t, double gamma, int n,
+                      double* out) {
+  for (int i = 0; i < n; ++i) out[i] = oracle_eq2(c0[i], c1[i], t[i], gamma);
 }
 
 /* S:143 k = steps[i] for the largest i with thresholds[i] <= r (left-closed,

@@ -65,6 +65,9 @@ int oracle_start_step(const float* q, const float* c0, const float* c1, const fl
 
 /* Eq. 2 alone, for pins. */
 double oracle_eq2(double c0, double c1, double t, double gamma);
+/* oracle_eq2 over n frames (marshalling only: out[i] = oracle_eq2(c0[i], c1[i], t[i], gamma)). */
+void oracle_eq2_batch(const double* c0, const double* c1, const double* t, double gamma, int n,
+                      double* out);
 /* k-logic lookup alone. */
 int32_t oracle_select_k(const oracle_klogic* lg, double r);
 

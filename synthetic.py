@@ -209,3 +209,62 @@ def request_densities(n_frames=21, mean=0.25, lo=0.05, hi=0.60):
 
 
 SPEC_KLOGIC = dict(thr=[0.85, 0.92, 0.97], steps=[10, 25, 40], fallback_k=0, k_max=40)
+
+
+def exhaustive_block_patterns(grid=4, cell=4, tag="exhaustive"):
+    """Every one of the 2^(grid*grid) block patterns of a grid x grid block map (configs[0]
+    geometry: 16x16 pixels, f=1, b=4): frame p paints one flagged pixel U(0, 0.4999) at a
+    random spot of every block whose bit is set in p; everything else U(0.5, 1.0) (0.5 itself
+    is not flagged, R-8).  Returns (O [2^(g*g), g*cell, g*cell] fp32, pattern bool [n, g*g])."""
+    nb = grid * grid
+    n = 1 << nb
+    pat = ((np.arange(n)[:, None] >> np.arange(nb)[None, :]) & 1).astype(bool)
+    rg = rng("pin-exhaustive", grid, cell) if tag == "exhaustive" else rng(tag, grid, cell)
+    side = grid * cell
+    O = rg.uniform(0.5, 1.0, size=(n, side, side)).astype(np.float32)
+    oy = rg.integers(0, cell, size=(n, nb))
+    ox = rg.integers(0, cell, size=(n, nb))
+    fi, bi = np.nonzero(pat)
+    by, bx = bi // grid, bi % grid
+    O[fi, by * cell + oy[fi, bi], bx * cell + ox[fi, bi]] = rg.uniform(0, 0.4999, size=len(fi))
+    return O, pat
+
+
+def sparse_pixel_maps(n, hp, wp, cell_px, n_px, tag="sparse-px"):
+    """Opacity + uncertainty maps with UNIFORMLY RANDOM isolated flagged pixels (no cell
+    structure): per frame n_px opacity pixels drawn U(0, 0.5) and n_px uncertainty spikes, half
+    of each placed on a row AND/OR column adjacent to a multiple of cell_px (block-footprint
+    boundaries, where an off-by-one in the footprint arithmetic shows), plus per frame one
+    opacity pixel exactly at tau_o = 0.5 and one uncertainty pixel exactly at tau_u (equality:
+    not flagged, R-8) and one NaN pixel (flagged, R-9).  Background opacity U(0.5+, 1.0),
+    uncertainty U(0, 0.6), tau_u = 0.7.  Returns (O, U, tau_u)."""
+    rg = rng(tag, n, hp, wp, cell_px, n_px)
+    O = rg.uniform(0.5000001, 1.0, size=(n, hp, wp)).astype(np.float32)
+    U = rg.uniform(0.0, 0.6, size=(n, hp, wp)).astype(np.float32)
+    tau_u = np.full(n, 0.7, np.float32)
+
+    def coords(k):
+        y = rg.integers(0, hp, size=k)
+        x = rg.integers(0, wp, size=k)
+        half = k // 2
+        # boundary rows/cols: c*cell_px - 1 or c*cell_px (the last / first pixel of a footprint)
+        by = rg.integers(0, -(-hp // cell_px), size=half) * cell_px - rg.integers(0, 2, size=half)
+        bx = rg.integers(0, -(-wp // cell_px), size=half) * cell_px - rg.integers(0, 2, size=half)
+        which = rg.integers(0, 3, size=half)  # 0: row only, 1: column only, 2: both
+        y[:half] = np.where(which != 1, np.clip(by, 0, hp - 1), y[:half])
+        x[:half] = np.where(which != 0, np.clip(bx, 0, wp - 1), x[:half])
+        return y, x
+
+    for i in range(n):
+        y, x = coords(n_px)
+        O[i, y, x] = rg.uniform(0.0, 0.5, size=n_px).astype(np.float32)
+        y, x = coords(n_px)
+        U[i, y, x] = rg.uniform(0.71, 1.0, size=n_px).astype(np.float32)
+        y, x = coords(3)
+        O[i, y[0], x[0]] = np.float32(0.5)
+        U[i, y[1], x[1]] = tau_u[i]
+        if i % 2 == 0:
+            O[i, y[2], x[2]] = np.nan
+        else:
+            U[i, y[2], x[2]] = np.nan
+    return O, U, tau_u

@@ -101,6 +101,24 @@ def test_block_mask_exhaustive_config1_patterns():
     assert np.array_equal(counts[:, 0], pat.sum(1))
 
 
+def test_block_mask_sparse_pixels_brute_force():
+    """Isolated random pixels on footprint boundaries, equality and NaN pixels (R-8, R-9) at
+    576x576, f=8, b=8, L=3: every level equals a brute-force any() over the block's truncated
+    b*f*2^l footprint of the raw pixel flags."""
+    O, U, tau = syn.sparse_pixel_maps(6, 576, 576, 64, 9, tag="pin-sparse")
+    masks, counts = oracle.block_mask(O, U, tau, 0.5, 8, 8, 3)
+    flag = ~(O >= 0.5) | ~(U <= tau[:, None, None])
+    for l in range(3):
+        fp = 64 << l
+        nb = -(-576 // fp)
+        want = np.zeros((6, nb, nb), np.uint8)
+        for by in range(nb):
+            for bx in range(nb):
+                want[:, by, bx] = flag[:, by * fp:(by + 1) * fp, bx * fp:(bx + 1) * fp].any(axis=(1, 2))
+        assert np.array_equal(masks[l], want), l
+        assert np.array_equal(counts[:, l], want.reshape(6, -1).sum(1))
+
+
 def test_block_mask_pyramid_nesting_and_counts():
     """Coarser levels never drop a refined region (S:232 'every coarser level >=
     max-pool of the finer'): with b=8 and /2 per level, a level-l block covers the
@@ -139,6 +157,61 @@ def test_eq2_gamma1_is_linear_and_endpoints():
         for (c0, c1) in ((60.0, 70.0), (70.0, 60.0)):
             assert oracle.eq2(c0, c1, 0.0, g) == c0
             assert oracle.eq2(c0, c1, 1.0, g) == c1
+
+
+def _is_correctly_rounded_sqrt(f, x):
+    """Exact check from the definition: f is the double nearest to sqrt(x) iff x lies between
+    the squares of the midpoints to f's neighbours (rational arithmetic, no rounding)."""
+    from fractions import Fraction as Fr
+    if x == 0.0:
+        return f == 0.0
+    lo, hi = Fr(math.nextafter(f, -math.inf)), Fr(math.nextafter(f, math.inf))
+    F = Fr(f)
+    return ((lo + F) / 2) ** 2 <= Fr(x) <= ((F + hi) / 2) ** 2
+
+
+def test_eq2_gamma_half_is_correctly_rounded_sqrt():
+    """Eq. 2 at gamma = 0.5 is c0 + (c1-c0) sqrt(t).  Reading R-16: both sides use
+    the correctly rounded sqrt, so k is bit-exact.  (c0, c1) = (0, 1) exposes f(t) itself; it
+    must be the correctly rounded sqrt -- checked exactly with rationals on a sample, and bit
+    for bit against IEEE sqrt (numpy) over > 10^6 fp32 t in [0, 1] incl. 0x3d00e96f, where
+    glibc pow(t, 0.5) is one ulp off."""
+    bits = np.arange(0, 0x3F800001, 1009, dtype=np.uint32)
+    bits = np.concatenate([bits, np.uint32([0x3D00E96F, 0x3F800000, 0x00000001, 0x3E800000])])
+    t = bits.view(np.float32).astype(np.float64)
+    assert len(t) > 10 ** 6
+    f = oracle.eq2_batch(np.zeros_like(t), np.ones_like(t), t, 0.5)
+    assert np.array_equal(f.view(np.uint64), np.sqrt(t).view(np.uint64))
+    # c1 < c0 branch: f = 1 - (1-t)^0.5 with (c0, c1) = (1, 0): Q* = 1 - f
+    g = oracle.eq2_batch(np.ones_like(t), np.zeros_like(t), t, 0.5)
+    assert np.array_equal(g.view(np.uint64), (1.0 - (1.0 - np.sqrt(1.0 - t))).view(np.uint64))
+    rg = syn.rng("pin-sqrt")
+    for i in list(rg.integers(0, len(t), 3000)) + [len(t) - 4]:
+        assert _is_correctly_rounded_sqrt(float(f[i]), float(t[i])), float(t[i])
+    # gamma = 1 is t itself (not pow): bitwise
+    f1 = oracle.eq2_batch(np.zeros_like(t), np.ones_like(t), t, 1.0)
+    assert np.array_equal(f1, t)
+
+
+GOLD_EQ2R = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "eq2_realized_ratio.json")))
+
+
+@pytest.mark.parametrize("case", GOLD_EQ2R["cases"], ids=lambda c: f"{c['t_bits']}-{c['c0']}-{c['c1']}")
+def test_start_step_cut_point_at_realized_ratio(case):
+    """A k-logic cut point exactly at the realized ratio r (what a decile calibration emits,
+    S:149): thresholds are left-closed, so thr = r selects the step and
+    thr = next double above r does not.  One ulp of Q* flips k here."""
+    import struct
+    t = struct.unpack("<f", struct.pack("<I", int(case["t_bits"], 16)))[0]
+    qs = float.fromhex(case["qstar_hex"])
+    assert oracle.eq2(case["c0"], case["c1"], t, 0.5) == qs
+    r = float.fromhex(case["r_hex"])
+    for thr, want in (([r], 25), ([math.nextafter(r, math.inf)], 0), ([math.nextafter(r, -math.inf)], 25),
+                      ([r - 0.1, r, r + 0.1], 30)):
+        steps = [25] if len(thr) == 1 else [10, 30, 40]
+        lg = oracle.make_klogic(thr, steps, 0, 40)
+        k = oracle.start_step([np.float32(case["q"])], [case["c0"]], [case["c1"]], [np.float32(t)], 0.5, [lg])
+        assert k[0] == want, (thr, want)
 
 
 def test_select_k_spec_and_monotone():
