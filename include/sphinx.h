@@ -107,7 +107,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 6
+#define SPHINX_ABI_VERSION 7
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -244,6 +244,22 @@ SPHINX_API size_t sphinx_conv_workspace_size(int32_t n, int32_t h, int32_t w_, i
  * a level's input features): the activation loads and MMAs may run while the preceding kernel
  * drains; the epilogue (stores) still waits for it, so the kernel completes after it. */
 #define SPHINX_CONV_INPUT_READY 4
+/* PDL ordering: a LIST_READY conv signals its dependents only after its own epilogue has waited
+ * for its predecessor, so any chain of LIST_READY convs (e.g. edge_plan(L1) -> conv(L0) ->
+ * conv(L1, REUSE_PLAN | LIST_READY)) keeps "every kernel before the preceding one is complete"
+ * transitively. */
+
+/* Kernel-variant overrides (tests and tuning only; the default choice is the measured-fastest
+ * one).  Every variant computes the same result within the conv bar and is
+ * bit-reproducible on its own. */
+#define SPHINX_CONV_FORCE_CG1 (1 << 8)      /* 1-SM tcgen05 kernel (cta_group::1) */
+#define SPHINX_CONV_FORCE_HALO (1 << 9)     /* halo-staged A even when one wave fits (b = 8) */
+#define SPHINX_CONV_FORCE_PERTAP (1 << 10)  /* per-tap A windows instead of halo staging */
+#define SPHINX_CONV_NO_SPLIT (1 << 11)      /* never split K (one pass per tile) */
+#define SPHINX_CONV_NO_EDGE (1 << 12)       /* no edge-class packing of partial edge blocks */
+#define SPHINX_CONV_NO_STREAMK (1 << 13)    /* tail split-K only, never stream-K */
+#define SPHINX_CONV_FORCE_STREAMK (1 << 14) /* stream-K whenever the workspace allows it */
+#define SPHINX_CONV_VARIANT_MASK (0x7f << 8)
 
 /* Computes the edge-class plan of a list into a conv workspace (what a conv call without
  * SPHINX_CONV_REUSE_PLAN does first), so that it can run early in a step and every conv over the
@@ -410,6 +426,18 @@ SPHINX_API sphinx_status sphinx_sparse_resblock(
     sphinx_dtype y_dtype, void* a_scratch, int32_t n, int32_t h, int32_t w, int32_t c,
     int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
     void* workspace, size_t workspace_bytes, sphinx_stream_t stream);
+/* sphinx_sparse_resblock with flags.  SPHINX_RB_FUSED_GN: GN+SiLU applied inside each conv's halo
+ * path (sphinx_gn_scale_shift + sphinx_sparse_conv3x3_gn_silu; block must be 8, else
+ * SPHINX_ERR_UNSUPPORTED) instead of the separate activation pass -- same result within the
+ * NEXT-3 bar, measured slower; a_scratch then holds the [N][c] float2 table. */
+#define SPHINX_RB_FUSED_GN 1
+SPHINX_API sphinx_status sphinx_sparse_resblock_ex(
+    const void* x, const void* w1, const float* b1, const void* w2, const float* b2,
+    const float* gn1_gamma, const float* gn1_beta, const float* gn2_gamma, const float* gn2_beta,
+    int32_t groups, float eps, void* h_buf, float* x_stats, float* h_stats, void* y,
+    sphinx_dtype y_dtype, void* a_scratch, int32_t n, int32_t h, int32_t w, int32_t c,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, int32_t flags, sphinx_stream_t stream);
 
 /* ---------------------------------------------------------------------------------
  * NEXT-4. Temporal-attention latent cache ("Every T steps, the model performs a full
@@ -454,6 +482,17 @@ SPHINX_API sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
                                                    const int32_t* block_ids, const int32_t* count,
                                                    int32_t capacity, void* workspace,
                                                    size_t workspace_bytes, sphinx_stream_t stream);
+/* sphinx_temporal_attention with an explicit head grouping (tests and tuning): head_group = k > 0
+ * stages units of (pixel, k heads) with one 5-D tensor copy (k divides heads; k = heads: no
+ * grouping); 0 = the default choice (groups only when the all-heads ring does not fit twice per
+ * SM).  Same result for every k. */
+SPHINX_API sphinx_status sphinx_temporal_attention_ex(const void* qkv, void* o, int32_t n, int32_t h,
+                                                      int32_t w, int32_t c, int32_t heads,
+                                                      int32_t frames_per_seq, int32_t block,
+                                                      const int32_t* block_ids, const int32_t* count,
+                                                      int32_t capacity, void* workspace,
+                                                      size_t workspace_bytes, int32_t head_group,
+                                                      sphinx_stream_t stream);
 
 /* The temporal block (3 launches + 1 plan kernel, graph capturable):
  *   qkv_buf[listed] = bf16(Wqkv x + bqkv)       (sphinx_sparse_pointwise, c -> 3c)

@@ -29,7 +29,7 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 6
+ABI_VERSION = 7
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
@@ -39,6 +39,7 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_sparse_pointwise", "sphinx_temporal_attention_workspace_size",
            "sphinx_temporal_attention", "sphinx_temporal_block", "sphinx_gn_scale_shift",
            "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex",
+           "sphinx_sparse_resblock_ex", "sphinx_temporal_attention_ex",
            "sphinx_conv_edge_plan")
 
 _lib = None
@@ -70,6 +71,14 @@ MAX_COMPACT_JOBS = 8
 CONV_REUSE_PLAN = 1
 CONV_LIST_READY = 2
 CONV_INPUT_READY = 4
+RB_FUSED_GN = 1
+CONV_FORCE_CG1 = 1 << 8
+CONV_FORCE_HALO = 1 << 9
+CONV_FORCE_PERTAP = 1 << 10
+CONV_NO_SPLIT = 1 << 11
+CONV_NO_EDGE = 1 << 12
+CONV_NO_STREAMK = 1 << 13
+CONV_FORCE_STREAMK = 1 << 14
 
 
 class StartArgs(ctypes.Structure):
@@ -117,6 +126,8 @@ def load(path=SO_PATH):
         "sphinx_sparse_conv3x3_residual": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_sparse_resblock": ([P, P, P, P, P, P, P, P, P, I, F, P, P, P, P, I, P,
                                     I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_sparse_resblock_ex": ([P, P, P, P, P, P, P, P, P, I, F, P, P, P, P, I, P,
+                                       I, I, I, I, I, P, P, I, P, Z, I, P], I),
         "sphinx_sparse_pointwise": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_gn_scale_shift": ([P, P, P, F, I, I, I, I, I, I, P, P], I),
         "sphinx_compact_blocks_batch": ([P, I, P], I),
@@ -125,6 +136,7 @@ def load(path=SO_PATH):
         "sphinx_sparse_conv3x3_gn_silu": ([P, P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_temporal_attention_workspace_size": ([I, I, I, I, I], Z),
         "sphinx_temporal_attention": ([P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_temporal_attention_ex": ([P, P, I, I, I, I, I, I, I, P, P, I, P, Z, I, P], I),
         "sphinx_temporal_block": ([P, P, P, P, P, I, I, P, P, P, I, I, I, I, I, I, P, P, I,
                                    P, Z, P, Z, P], I),
     }
@@ -256,11 +268,19 @@ def sphinx_noise_inject(x0, eps, x_t, block, block_ids, count, step, abar, capac
 _ws_cache = {}
 
 
-def conv_workspace(c_out, device, n=1, h=1, w=1, block=8):
+def _stream_key(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def conv_workspace(c_out, device, n=1, h=1, w=1, block=8, stream=None):
     """Zero-initialised workspace (split-K counters + partial tiles, edge-class plan) for a conv
-    of this geometry on `device`, allocated once and cached (the kernel leaves its counters
-    zeroed).  Memory only: no computation happens here."""
-    key = (device, c_out, n, h, w, block)
+    of this geometry on `device` and STREAM (sphinx.h: one workspace per stream), allocated once
+    and cached (the kernel leaves its counters zeroed).  Memory only: no computation happens
+    here.  CUDA-graph users warm up on the capture stream (so the workspace exists before the
+    capture) or pass their own workspace."""
+    key = (device, c_out, n, h, w, block, _stream_key(stream))
     ws = _ws_cache.get(key)
     if ws is None:
         import torch
@@ -271,11 +291,12 @@ def conv_workspace(c_out, device, n=1, h=1, w=1, block=8):
 
 def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None, stream=None,
                           workspace=None, residual=None, reuse_plan=False, list_ready=False,
-                          input_ready=False):
+                          input_ready=False, variant=0):
     """Step 4.  x bf16 NHWC [N,H,W,Cin]; w bf16 [Cout,3,3,Cin]; bias fp32 [Cout] or None;
     y NHWC [N,H,W,Cout] bf16 or fp32 (only listed blocks are written).
-    workspace: None = a cached zeroed split-K workspace for this device, False = no split-K,
-    or a caller-owned zero-initialised uint8 CUDA tensor (one per stream)."""
+    workspace: None = a cached zeroed split-K workspace for this device and stream, False = no
+    split-K, or a caller-owned zero-initialised uint8 CUDA tensor (one per stream).
+    variant: CONV_FORCE_* / CONV_NO_* kernel-variant flags (tests and tuning; 0 = default)."""
     import torch
     _dev(x, torch.bfloat16, "x")
     _dev(w, torch.bfloat16, "w")
@@ -288,12 +309,12 @@ def sphinx_sparse_conv3x3(x, w, bias, y, block, block_ids, count, capacity=None,
     cout = w.shape[0]
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = conv_workspace(cout, y.device, n, h, wd, block)
+        workspace = conv_workspace(cout, y.device, n, h, wd, block, stream)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
-    if reuse_plan or list_ready or input_ready:
+    if reuse_plan or list_ready or input_ready or variant:
         _dev(residual, torch.bfloat16, "residual")
         flags = ((CONV_REUSE_PLAN if reuse_plan else 0) | (CONV_LIST_READY if list_ready else 0) |
-                 (CONV_INPUT_READY if input_ready else 0))
+                 (CONV_INPUT_READY if input_ready else 0) | int(variant))
         rc = load().sphinx_sparse_conv3x3_ex(
             _ptr(x), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y), F32 if y.dtype == torch.float32 else BF16,
             n, h, wd, cin, cout, int(block), _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes,
@@ -324,7 +345,7 @@ def sphinx_conv_edge_plan(block_ids, count, n, h, w, block, c_out, capacity=None
     _dev(count, torch.int32, "count")
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = conv_workspace(c_out, block_ids.device, n, h, w, block)
+        workspace = conv_workspace(c_out, block_ids.device, n, h, w, block, stream)
     rc = load().sphinx_conv_edge_plan(_ptr(block_ids), _ptr(count), int(n), int(h), int(w), int(block), int(cap),
                                       _ptr(workspace), workspace.numel(), _stream(stream))
     _chk("sphinx_conv_edge_plan", rc)
@@ -381,7 +402,7 @@ def sphinx_uncertainty_map(rgb, uncertainty, tau_u, window=7, smooth=5, workspac
     if c != 3:
         raise ValueError("rgb: [N,H,W,3]")
     if workspace is None:
-        key = ("unc", rgb.device, n)
+        key = ("unc", rgb.device, n, _stream_key(stream))
         workspace = _ws_cache.get(key)
         if workspace is None:
             nbytes = int(load().sphinx_uncertainty_workspace_size(int(n)))
@@ -442,7 +463,7 @@ def sphinx_gn_silu(x, stats, gamma, beta, eps, groups, block, block_ids, count, 
 
 def sphinx_sparse_resblock(x, w1, b1, w2, b2, gn1, gn2, groups, eps, h_buf, x_stats, h_stats, y,
                            a_scratch, block, block_ids, count, capacity=None, workspace=None,
-                           stream=None):
+                           stream=None, fused=False):
     """NEXT-3 block-sparse ResNet block (R-26, R-27).  gn1/gn2 = (gamma, beta)
     fp32 [C]; h_buf bf16 / y bf16-or-fp32 / x_stats / h_stats persistent (see sphinx.h)."""
     import torch
@@ -459,19 +480,21 @@ def sphinx_sparse_resblock(x, w1, b1, w2, b2, gn1, gn2, groups, eps, h_buf, x_st
     n, h, wd, c = x.shape
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = conv_workspace(c, y.device, n, h, wd, block)
+        workspace = conv_workspace(c, y.device, n, h, wd, block, stream)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
-    rc = load().sphinx_sparse_resblock(
+    rc = load().sphinx_sparse_resblock_ex(
         _ptr(x), _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), _ptr(gn1[0]), _ptr(gn1[1]), _ptr(gn2[0]),
         _ptr(gn2[1]), int(groups), float(eps), _ptr(h_buf), _ptr(x_stats), _ptr(h_stats), _ptr(y),
         F32 if y.dtype == torch.float32 else BF16, _ptr(a_scratch), n, h, wd, c, int(block),
-        _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes, _stream(stream))
-    _chk("sphinx_sparse_resblock", rc)
+        _ptr(block_ids), _ptr(count), int(cap), ws_ptr, ws_bytes, RB_FUSED_GN if fused else 0,
+        _stream(stream))
+    _chk("sphinx_sparse_resblock_ex", rc)
 
 
-def attn_workspace(n, h, w, frames_per_seq, block, device):
-    """Workspace of sphinx_temporal_attention (listed-frame bitmasks), cached; memory only."""
-    key = ("attn", device, n, h, w, frames_per_seq, block)
+def attn_workspace(n, h, w, frames_per_seq, block, device, stream=None):
+    """Workspace of sphinx_temporal_attention (listed-frame bitmasks), cached per stream; memory
+    only."""
+    key = ("attn", device, n, h, w, frames_per_seq, block, _stream_key(stream))
     ws = _ws_cache.get(key)
     if ws is None:
         import torch
@@ -498,7 +521,7 @@ def sphinx_sparse_pointwise(x, w, bias, y, block, block_ids, count, residual=Non
     cout = w.shape[0]
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = conv_workspace(cout, y.device, n, h, wd, block)
+        workspace = conv_workspace(cout, y.device, n, h, wd, block, stream)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
     rc = load().sphinx_sparse_pointwise(_ptr(x), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y),
                                         F32 if y.dtype == torch.float32 else BF16, n, h, wd, cin, cout,
@@ -508,8 +531,9 @@ def sphinx_sparse_pointwise(x, w, bias, y, block, block_ids, count, residual=Non
 
 
 def sphinx_temporal_attention(qkv, o, heads, frames_per_seq, block, block_ids, count, capacity=None,
-                              workspace=None, stream=None):
-    """NEXT-4 attention of listed tokens over their sequence's frames (K/V cache in qkv)."""
+                              workspace=None, stream=None, head_group=0):
+    """NEXT-4 attention of listed tokens over their sequence's frames (K/V cache in qkv).
+    head_group: k > 0 stages (pixel, k heads) units (tests); 0 = the library's choice."""
     import torch
     _dev(qkv, torch.bfloat16, "qkv")
     _dev(o, torch.bfloat16, "o")
@@ -518,11 +542,12 @@ def sphinx_temporal_attention(qkv, o, heads, frames_per_seq, block, block_ids, c
     n, h, w, c = o.shape
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = attn_workspace(n, h, w, frames_per_seq, block, o.device)
-    rc = load().sphinx_temporal_attention(_ptr(qkv), _ptr(o), n, h, w, c, int(heads), int(frames_per_seq),
-                                          int(block), _ptr(block_ids), _ptr(count), int(cap),
-                                          _ptr(workspace), workspace.numel(), _stream(stream))
-    _chk("sphinx_temporal_attention", rc)
+        workspace = attn_workspace(n, h, w, frames_per_seq, block, o.device, stream)
+    rc = load().sphinx_temporal_attention_ex(_ptr(qkv), _ptr(o), n, h, w, c, int(heads),
+                                             int(frames_per_seq), int(block), _ptr(block_ids), _ptr(count),
+                                             int(cap), _ptr(workspace), workspace.numel(), int(head_group),
+                                             _stream(stream))
+    _chk("sphinx_temporal_attention_ex", rc)
 
 
 def sphinx_temporal_block(x, wqkv, bqkv, wo, bo, heads, frames_per_seq, qkv_buf, o_scratch, y, block,
@@ -541,9 +566,9 @@ def sphinx_temporal_block(x, wqkv, bqkv, wo, bo, heads, frames_per_seq, qkv_buf,
     n, h, wd, c = x.shape
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = conv_workspace(3 * c, y.device, n, h, wd, block)
+        workspace = conv_workspace(3 * c, y.device, n, h, wd, block, stream)
     if attn_ws is None:
-        attn_ws = attn_workspace(n, h, wd, frames_per_seq, block, y.device)
+        attn_ws = attn_workspace(n, h, wd, frames_per_seq, block, y.device, stream)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
     rc = load().sphinx_temporal_block(
         _ptr(x), _ptr(wqkv), _ptr(bqkv), _ptr(wo), _ptr(bo), int(heads), int(frames_per_seq),
@@ -579,7 +604,7 @@ def sphinx_sparse_conv3x3_gn_silu(x, scale_shift, w, bias, y, block, block_ids, 
     cout = w.shape[0]
     cap = block_ids.numel() if capacity is None else capacity
     if workspace is None:
-        workspace = conv_workspace(cout, y.device, n, h, wd, block)
+        workspace = conv_workspace(cout, y.device, n, h, wd, block, stream)
     ws_ptr, ws_bytes = (None, 0) if workspace is False else (_ptr(workspace), workspace.numel())
     rc = load().sphinx_sparse_conv3x3_gn_silu(
         _ptr(x), _ptr(scale_shift), _ptr(w), _ptr(bias), _ptr(residual), _ptr(y),

@@ -29,13 +29,15 @@ def _stale():
 
 
 def build(force=False, verbose=False, trace=False):
-    """trace=True builds the dev-only timeline variant libsphinx_trace.so (-DSPHINX_TRACE)."""
+    """trace=True builds the dev-only variant libsphinx_trace.so (-DSPHINX_TRACE timelines and the
+    -DSPHINX_DEV_KNOBS A/B environment knobs); the release libsphinx.so reads no environment
+    variable except SPHINX_PDL."""
     so = SO.replace("libsphinx.so", "libsphinx_trace.so") if trace else SO
     if not trace and not force and not _stale():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
-        (["-DSPHINX_TRACE"] if trace else []) + \
+        (["-DSPHINX_TRACE", "-DSPHINX_DEV_KNOBS"] if trace else []) + \
         ["-I", os.path.join(ROOT, "include"), "-o", so + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
     subprocess.check_call(cmd)
     os.replace(so + ".tmp", so)

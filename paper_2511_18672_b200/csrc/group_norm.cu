@@ -412,27 +412,21 @@ extern "C" sphinx_status sphinx_gn_scale_shift(float* stats, const float* gamma,
   return SPHINX_OK;
 }
 
-// The GN+SiLU-in-conv path is opt-in (SPHINX_RB_FUSED=1): measured slower than the separate
-// activation pass at every UNet level.  Read per call (tests toggle it).
-static bool rb_fused_enabled() {
-  const char* e = getenv("SPHINX_RB_FUSED");
-  return e && atoi(e) != 0;
-}
-
-extern "C" sphinx_status sphinx_sparse_resblock(
+static sphinx_status resblock_impl(
     const void* x, const void* w1, const float* b1, const void* w2, const float* b2,
     const float* gn1_gamma, const float* gn1_beta, const float* gn2_gamma, const float* gn2_beta,
     int32_t groups, float eps, void* h_buf, float* x_stats, float* h_stats, void* y,
     sphinx_dtype y_dtype, void* a_scratch, int32_t n, int32_t h, int32_t w, int32_t c,
     int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
-    void* workspace, size_t workspace_bytes, sphinx_stream_t stream) {
+    void* workspace, size_t workspace_bytes, bool fused, sphinx_stream_t stream) {
   if (!h_buf || !y || !a_scratch || !x_stats || !h_stats) return SPHINX_ERR_INVALID_ARGUMENT;
   if (h_buf == x || y == x || y == h_buf || a_scratch == x || a_scratch == h_buf || a_scratch == y ||
       x_stats == h_stats)
     return SPHINX_ERR_INVALID_ARGUMENT;
   sphinx_status st;
-  if (block == 8 && c % 8 == 0 && rb_fused_enabled()) {
-    // Fused path (opt-in): GN+SiLU is applied inside the conv (transform warps between the halo
+  if (fused) {
+    if (block != 8 || c % 8) return SPHINX_ERR_UNSUPPORTED;
+    // Fused path (opt-in, measured slower than the separate pass: DESIGN.md 6.8): GN+SiLU is applied inside the conv (transform warps between the halo
     // TMA and the MMA), so the activation never round-trips through HBM; a_scratch holds the
     // per-(frame, channel) (scale, shift) table ([N][c] float2 <= N*h*w*c*2 bytes).
     float* tab = static_cast<float*>(a_scratch);
@@ -479,4 +473,29 @@ extern "C" sphinx_status sphinx_sparse_resblock(
   return sphinx_sparse_conv3x3_ex(a_scratch, w2, b2, x, y, y_dtype, n, h, w, c, c, block, block_ids,
                                   count, capacity, workspace, workspace_bytes, SPHINX_CONV_REUSE_PLAN,
                                   stream);
+}
+
+extern "C" sphinx_status sphinx_sparse_resblock(
+    const void* x, const void* w1, const float* b1, const void* w2, const float* b2,
+    const float* gn1_gamma, const float* gn1_beta, const float* gn2_gamma, const float* gn2_beta,
+    int32_t groups, float eps, void* h_buf, float* x_stats, float* h_stats, void* y,
+    sphinx_dtype y_dtype, void* a_scratch, int32_t n, int32_t h, int32_t w, int32_t c,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, sphinx_stream_t stream) {
+  return resblock_impl(x, w1, b1, w2, b2, gn1_gamma, gn1_beta, gn2_gamma, gn2_beta, groups, eps, h_buf,
+                       x_stats, h_stats, y, y_dtype, a_scratch, n, h, w, c, block, block_ids, count,
+                       capacity, workspace, workspace_bytes, false, stream);
+}
+
+extern "C" sphinx_status sphinx_sparse_resblock_ex(
+    const void* x, const void* w1, const float* b1, const void* w2, const float* b2,
+    const float* gn1_gamma, const float* gn1_beta, const float* gn2_gamma, const float* gn2_beta,
+    int32_t groups, float eps, void* h_buf, float* x_stats, float* h_stats, void* y,
+    sphinx_dtype y_dtype, void* a_scratch, int32_t n, int32_t h, int32_t w, int32_t c,
+    int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
+    void* workspace, size_t workspace_bytes, int32_t flags, sphinx_stream_t stream) {
+  if (flags & ~SPHINX_RB_FUSED_GN) return SPHINX_ERR_INVALID_ARGUMENT;
+  return resblock_impl(x, w1, b1, w2, b2, gn1_gamma, gn1_beta, gn2_gamma, gn2_beta, groups, eps, h_buf,
+                       x_stats, h_stats, y, y_dtype, a_scratch, n, h, w, c, block, block_ids, count,
+                       capacity, workspace, workspace_bytes, (flags & SPHINX_RB_FUSED_GN) != 0, stream);
 }

@@ -50,7 +50,6 @@ constexpr int kThreadsNorm = kThreads + kXThreads;
 // non-NORM kernels: 4 more epilogue warps (7..10) split the accumulator columns with warps 2..5
 // (same TMEM lane quarters, warp & 3), halving the TMEM drain and the split-K park / reduce
 constexpr int kThreadsEpi8 = kThreads + 128;
-constexpr bool kRaggedDefault = false;  // SPHINX_CONV_RAGGED overrides (A/B)
 
 #ifdef SPHINX_TRACE
 // Dev-only timeline trace (libsphinx_trace.so): globaltimer stamps per CTA of one launch.
@@ -83,13 +82,12 @@ struct ConvParams {
   const __nv_bfloat16* res;  // NEXT-3: bf16 NHWC residual added in the epilogue (identity skip), or NULL
   const float2* norm_tab;    // NEXT-3 fused GN+SiLU: [N][c_in] (scale, shift), a = SiLU(x*scale+shift)
   int cin;
-  int xform_dbg;             // dev A/B knob (SPHINX_XFORM_DBG): 1 = skip the transform math
   int y_f32;
   int h, w, cout, b, hb, wb;
   int kc;         // 64-channel chunks per tap
   int taps;       // 9 = 3x3 conv; 1 = pointwise (1x1) projection (NEXT-4), per-tap path only
   int n_tiles_n;  // tiles along C_out
-  int n_last;     // width of the last C_out tile (== BN unless ragged: e.g. 320 = 256 + 64)
+  int n_last;     // width of the last C_out tile (== BN: C_out is tiled in equal widths)
   int bpt;        // blocks per 128-row tile = 128 / b^2
   // split-K workspace (NULL = never split): per-(tile, split) fp32 partial tiles and one
   // arrival counter per (tile, CTA of the pair); counters are zero between launches.
@@ -104,7 +102,6 @@ struct ConvParams {
   const int32_t* plan_meta;  // [3] = {n_full, n_bottom, n_right}
   int rb, cr;                // valid rows of bottom-edge blocks, valid cols of right-edge blocks
   int bpt_b, bpt_r;          // blocks per CTA tile of the two edge classes
-  uint32_t desc_bo;  // UMMA descriptor base-offset encoding for shifted halo windows
   int trace;         // SPHINX_TRACE builds: record this launch's timeline
   int early_input;   // x (and the list) predate the preceding kernel: the halo producer does not
                      // wait either -- only the epilogue does (its stores, and kernel completion
@@ -113,8 +110,6 @@ struct ConvParams {
                      // them (and start the weight loads) before griddepcontrol.wait; only the
                      // halo producer and the epilogue wait for the predecessor
   int dbg;           // SPHINX_TRACE builds: 1 = skip epilogue global stores, 2 = skip bias
-  int a_warp;        // halo mode: 1 = halos issued by their own producer warp
-  int a_ahead;       // halo chunks the A cursor may run ahead of the B cursor (1..kANum-1)
   int allow_streamk; // halo mode may use stream-K when it shortens the makespan
 };
 
@@ -470,8 +465,13 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (!p.early_list) pdl_wait();  // ids, count, plan and x are produced upstream
-  pdl_trigger();
+  if (!p.early_list) {
+    pdl_wait();  // ids, count, plan and x are produced upstream
+    pdl_trigger();
+  }
+  // early_list: the trigger follows the epilogue warps' griddepcontrol.wait (below), so a
+  // dependent launched early has every kernel before this one complete -- its own early reads
+  // of a list written two or more kernels back are then ordered transitively.
 #ifdef SPHINX_TRACE
   if (threadIdx.x == 0) CONV_TRACE(1, gtimer());
 #endif
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
   if (warp == 0 || (HALO && warp == kAWarp)) {
     // early_list: the halo (A) producer -- also warp 0 when it issues A (per-tap path, or halo
     // mode without split producers) -- waits for the predecessor; the weight-only producer not
-    if (p.early_list && !p.early_input && (warp == kAWarp || !HALO || p.a_warp == 0)) pdl_wait();
+    if (p.early_list && !p.early_input && (warp == kAWarp || !HALO)) pdl_wait();
     // ===================== TMA producers (both CTAs) =====================
     // halo mode: warp 0 issues the weight (B) tiles and warp kAWarp the halos (A), so the two
     // streams of TMA issues overlap (a single issuing thread caps the per-SM TMA op rate)
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         Cur ca, cb;
         cur_init(ca);
         cur_init(cb);
-        const int kAhead = p.a_ahead < Cfg::kANum - 1 ? p.a_ahead : Cfg::kANum - 1;
+        constexpr int kAhead = 2 < Cfg::kANum - 1 ? 2 : Cfg::kANum - 1;
         long long a_seg = -1;  // segment whose blocks are decoded in cx/cy/cn
         long long b_seg = -1;
         int b_n0 = 0;
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
 #ifdef SPHINX_TRACE
         bool tr_a = false, tr_b = false;
 #endif
-        const bool split = p.a_warp != 0;
+        constexpr bool split = true;
         const bool doA = split ? warp == kAWarp : warp == 0;
         const bool doB = warp == 0;
         while (doB ? cb.ok : ca.ok) {
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
               const uint32_t b_addr = smem_u32(sB + bs * Cfg::kStageB);
 #pragma unroll
               for (int k = 0; k < kBK / 16; ++k) {
-                const uint64_t ad = umma_desc_sw128(a_start + k * 32, Cfg::kHaloRow, p.desc_bo);
+                const uint64_t ad = umma_desc_sw128(a_start + k * 32, Cfg::kHaloRow, 0u);
                 const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 1024);
                 const uint32_t accum = (kc != kc0 || tap != 0 || k != 0) ? 1u : 0u;
                 if constexpr (CG == 1) tc_mma_bf16(d_tmem, ad, bd, idesc_t, accum);
@@ -855,7 +855,10 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
       }
     }
   } else if (warp < kAWarp || (!NORM && warp >= kXWarp)) {
-    if (p.early_list) pdl_wait();  // stores / residual reads after the predecessor completes
+    if (p.early_list) {
+      pdl_wait();  // stores / residual reads after the predecessor completes
+      pdl_trigger();
+    }
     // ============ epilogue (warps 2..5, and 7..10 for non-NORM kernels; both CTAs) ============
     constexpr int kEpiW = NORM ? 4 : 8, kEpiT = kEpiW * 32, kHalves = kEpiW / 4;
     const int half = warp >= kXWarp ? 1 : 0;  // which half of the 32-column chunks this warp drains
@@ -1165,7 +1168,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
           // 4 rows per iteration (rows kXThreads/8 apart keep this thread's SW128 phase):
           // independent LDS / SFU chains in flight
           constexpr int kRS = kXThreads / 8;
-          for (int r0 = xt >> 3; r0 < (p.xform_dbg ? 0 : rows); r0 += 4 * kRS) {
+          for (int r0 = xt >> 3; r0 < rows; r0 += 4 * kRS) {
             uint4 v[4];
             int bi[4];
 #pragma unroll
@@ -1360,18 +1363,9 @@ static sphinx_status launch_cg(int cg, const CUtensorMap& ta, const CUtensorMap&
                  : launch_bn<BN, 1, 4, false>(ta, tb, tc, tb2, p, grid, s);
 }
 
-// Ragged 256-wide C_out tiling (e.g. 320 = 256 + 64, 640 = 2 x 256 + 128) instead of equal
-// 160-wide tiles: the widest MMA reads the A operand once per 256 output columns.
-static bool ragged_ok(int cout) {
-  const char* env = getenv("SPHINX_CONV_RAGGED");
-  const bool on = env ? atoi(env) != 0 : kRaggedDefault;
-  const int last = cout % 256;
-  return on && cout > 256 && last != 0 && last % 32 == 0;
-}
-
-// Widest tile that minimises padded output columns (ties -> wider).
+// Widest tile that minimises padded output columns (ties -> wider).  (Ragged 256-wide tiles
+// with a narrow last tile, e.g. 320 = 256 + 64, measured slower: DESIGN.md §6.4.)
 static int pick_bn(int cout) {
-  if (ragged_ok(cout)) return 256;
   const int cands[] = {256, 160, 128, 64, 32};
   int best = 32, best_pad = 1 << 30;
   for (int bn : cands) {
@@ -1434,13 +1428,14 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   if (!enc) return cuda_fail(cudaErrorNotSupported);
 
   const int bn = pick_bn(c_out);
-  // CTA-pair (cta_group::2) unless overridden: halves the weight traffic per SM
-  int cg = 2;
-  if (const char* env = getenv("SPHINX_CONV_CG")) cg = atoi(env) == 1 ? 1 : 2;
-  // halo-staged A for 8x8 blocks unless overridden: each activation read once per chunk
+  // CTA-pair (cta_group::2) unless the caller forces the 1-SM kernel: halves the weight traffic
+  // per SM
+  int cg = (flags & SPHINX_CONV_FORCE_CG1) ? 1 : 2;
+  // halo-staged A for 8x8 blocks unless the caller forces a path: each activation read once per
+  // chunk
   int halo = (block == 8 && taps == 9) ? 1 : 0;
-  if (const char* env = getenv("SPHINX_CONV_HALO")) {
-    halo = halo && atoi(env) != 0;  // 1 = force halo staging, 0 = force per-tap
+  if (flags & (SPHINX_CONV_FORCE_HALO | SPHINX_CONV_FORCE_PERTAP)) {
+    halo = halo && !(flags & SPHINX_CONV_FORCE_PERTAP);
   } else if (halo && !norm_tab) {
     // At most one wave of tiles even if every capacity block is listed (e.g. a single frame):
     // the problem is latency-bound, and the per-tap path's split-K over (tap, chunk) K-steps
@@ -1454,8 +1449,6 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     cg = 2;
   }
   CUtensorMap ta, tb, tc, tb2;
-  // ragged C_out tiling: the last tile is n_last wide (its own weight tensor map)
-  const int n_last = c_out - (cdiv(c_out, bn) - 1) * bn;
   {
     const cuuint64_t dims[4] = {(cuuint64_t)c_in, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
     const cuuint64_t strides[3] = {(cuuint64_t)c_in * 2, (cuuint64_t)w_ * c_in * 2,
@@ -1484,8 +1477,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
-    const bool ragged = n_last < bn && ragged_ok(c_out);
-    const cuuint32_t box2[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)((ragged ? n_last : bn) / cg)};
+    const cuuint32_t box2[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)(bn / cg)};
     r = enc(&tb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides, box2, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1499,8 +1491,6 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.res = static_cast<const __nv_bfloat16*>(residual);
   p.norm_tab = norm_tab;
   p.cin = c_in;
-  p.xform_dbg = 0;
-  if (const char* env = getenv("SPHINX_XFORM_DBG")) p.xform_dbg = atoi(env);
   p.y_f32 = y_dtype == SPHINX_F32;
   p.h = h;
   p.w = w_;
@@ -1511,11 +1501,9 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.kc = cdiv(c_in, kBK);
   p.taps = taps;
   p.n_tiles_n = cdiv(c_out, bn);
-  p.n_last = (n_last < bn && ragged_ok(c_out)) ? n_last : bn;
+  p.n_last = bn;
   p.bpt = kBM / (block * block);
   p.halo = halo;
-  p.a_ahead = 2;
-  p.a_warp = 1;
   p.trace = 0;
   p.early_list = 0;
   p.early_input = 0;
@@ -1529,12 +1517,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     ++launch_no;
   }
 #endif
-  if (const char* env = getenv("SPHINX_A_WARP")) p.a_warp = atoi(env);
-  p.allow_streamk = 1;
-  if (const char* env = getenv("SPHINX_CONV_STREAMK")) p.allow_streamk = atoi(env);  // 2 = force
-  if (const char* env = getenv("SPHINX_A_AHEAD")) p.a_ahead = atoi(env) < 1 ? 1 : (atoi(env) > 2 ? 2 : atoi(env));
-  p.desc_bo = 0;  // measured: the SW128 phase comes from absolute smem address bits
-  if (const char* env = getenv("SPHINX_DESC_BO")) p.desc_bo = (uint32_t)atoi(env);
+  p.allow_streamk = (flags & SPHINX_CONV_FORCE_STREAMK) ? 2 : (flags & SPHINX_CONV_NO_STREAMK) ? 0 : 1;
   p.ws_part = nullptr;
   p.ws_cnt = nullptr;
   p.ws_slots = 0;
@@ -1546,9 +1529,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.bpt_b = p.rb ? (16 / p.rb < 8 ? 16 / p.rb : 8) : 8;
   p.bpt_r = p.cr ? (16 / p.cr < 8 ? 16 / p.cr : 8) : 8;
   const size_t pl_bytes = plan_bytes(capacity);
-  bool allow_split = true, allow_edge = true;
-  if (const char* env = getenv("SPHINX_CONV_SPLIT")) allow_split = atoi(env) != 0;
-  if (const char* env = getenv("SPHINX_CONV_EDGE")) allow_edge = atoi(env) != 0;
+  const bool allow_split = !(flags & SPHINX_CONV_NO_SPLIT), allow_edge = !(flags & SPHINX_CONV_NO_EDGE);
   const bool ws_ok = workspace && workspace_bytes >= kCntBytes + pl_bytes;
   uint8_t* ws8 = static_cast<uint8_t*>(workspace);
   if (ws_ok && allow_edge && halo && (p.rb || p.cr)) {
@@ -1571,9 +1552,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   // the fused-GN variant (its table comes from the preceding kernel)
   p.early_list = (flags & SPHINX_CONV_LIST_READY) && !norm_tab &&
                  !(p.plan_ids && !(flags & SPHINX_CONV_REUSE_PLAN)) ? 1 : 0;
-  if (const char* env = getenv("SPHINX_CONV_EARLY")) p.early_list = p.early_list && atoi(env) != 0;
   p.early_input = (p.early_list && (flags & SPHINX_CONV_INPUT_READY)) ? 1 : 0;
-  if (const char* env = getenv("SPHINX_CONV_EARLY_INPUT")) p.early_input = p.early_input && atoi(env) != 0;
   // SPHINX_CONV_REUSE_PLAN: the workspace already holds the edge plan of this very list (the
   // caller's previous conv on this stream used the same list and workspace): skip the plan launch
   if (p.plan_ids && !(flags & SPHINX_CONV_REUSE_PLAN)) {
@@ -1649,7 +1628,8 @@ extern "C" sphinx_status sphinx_sparse_conv3x3_ex(
     sphinx_dtype y_dtype, int32_t n, int32_t h, int32_t w_, int32_t c_in, int32_t c_out,
     int32_t block, const int32_t* block_ids, const int32_t* count, int32_t capacity,
     void* workspace, size_t workspace_bytes, int32_t flags, sphinx_stream_t stream) {
-  if (flags & ~(SPHINX_CONV_REUSE_PLAN | SPHINX_CONV_LIST_READY | SPHINX_CONV_INPUT_READY))
+  if (flags & ~(SPHINX_CONV_REUSE_PLAN | SPHINX_CONV_LIST_READY | SPHINX_CONV_INPUT_READY |
+                SPHINX_CONV_VARIANT_MASK))
     return SPHINX_ERR_INVALID_ARGUMENT;
   return conv_impl(x, w, bias, residual, y, y_dtype, n, h, w_, c_in, c_out, block, block_ids, count,
                    capacity, workspace, workspace_bytes, stream, 9, nullptr, (int)flags);

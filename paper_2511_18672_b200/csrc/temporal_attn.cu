@@ -418,12 +418,12 @@ extern "C" size_t sphinx_temporal_attention_workspace_size(int32_t n, int32_t h,
   return (size_t)(n / frames_per_seq) * cdiv(h, block) * cdiv(w, block) * sizeof(uint32_t);
 }
 
-extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int32_t n, int32_t h,
-                                                   int32_t w, int32_t c, int32_t heads,
-                                                   int32_t frames_per_seq, int32_t block,
-                                                   const int32_t* block_ids, const int32_t* count,
-                                                   int32_t capacity, void* workspace,
-                                                   size_t workspace_bytes, sphinx_stream_t stream) {
+static sphinx_status temporal_attention_impl(const void* qkv, void* o, int32_t n, int32_t h, int32_t w,
+                                             int32_t c, int32_t heads, int32_t frames_per_seq,
+                                             int32_t block, const int32_t* block_ids,
+                                             const int32_t* count, int32_t capacity, void* workspace,
+                                             size_t workspace_bytes, int32_t head_group,
+                                             sphinx_stream_t stream) {
   if (!qkv || !o || !block_ids || !count || !workspace || qkv == o) return SPHINX_ERR_INVALID_ARGUMENT;
   if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || heads <= 0 || block <= 0 || capacity < 0 ||
       frames_per_seq <= 0 || n % frames_per_seq || c % heads)
@@ -464,6 +464,7 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   g.ppu = 1;
   g.nbuf = ta_smem(c, T, 2) <= 227 * 1024 ? 2 : 1;
   g.stream = g.nbuf == 2 ? 1 : 0;
+#ifdef SPHINX_DEV_KNOBS  // measured-slower staging variants: dev builds only
   if (const char* env = getenv("SPHINX_TA_NBUF")) {
     const int nb = atoi(env);
     if (nb >= 1 && nb <= kTaMaxBuf && ta_smem(c, T, nb) <= 227 * 1024) g.nbuf = nb;
@@ -473,6 +474,9 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   g.kv_only = 0;
   if (const char* env = getenv("SPHINX_TA_KVONLY")) g.kv_only = atoi(env) != 0;
   if (const char* env = getenv("SPHINX_TA_STREAM")) g.stream = atoi(env) != 0;
+#else
+  g.kv_only = 0;
+#endif
   g.rs = (uint32_t)ta_row(c, g.ppu);
   g.bstride = (uint32_t)((size_t)T * g.rs);
   // tensor mode: one 4-D TMA copy per unit instead of T bulk copies (the staging is bulk-op-rate
@@ -480,7 +484,9 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   // same-box); single-buffered (level 2) it measured slower (27.3 -> 29.7 us).
   // SPHINX_TA_TMAP=0/1 overrides.
   bool want_t = g.nbuf == 2;
+#ifdef SPHINX_DEV_KNOBS
   if (const char* env = getenv("SPHINX_TA_TMAP")) want_t = atoi(env) != 0;
+#endif
   g.tmode = want_t && g.ppu == 1 && !g.kv_only && (3 * c) % 64 == 0 && 3 * c / 64 <= 256 &&
             ta_smem_t(c, T, g.nbuf) <= 227 * 1024;
   // head groups (SPHINX_TA_HGROUP=k heads per unit, tensor mode): a unit stages the q|k|v slices of
@@ -497,7 +503,7 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
         want_k = k;
         break;
       }
-  if (const char* env = getenv("SPHINX_TA_HGROUP")) want_k = atoi(env);
+  if (head_group > 0) want_k = head_group;  // caller override (tests); heads = no grouping
   {
     const int k = want_k;
     if (k >= 1 && k < heads && heads % k == 0 && g.ppu == 1 && !g.kv_only &&
@@ -506,7 +512,6 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
       g.ngrp = heads / k;
       g.nbuf = ta_smem_t(k * kHeadDim, T, 2) <= 227 * 1024 ? 2 : 1;
       g.stream = g.nbuf == 2 ? 1 : 0;
-      if (const char* e2 = getenv("SPHINX_TA_STREAM")) g.stream = atoi(e2) != 0;
       g.tmode = 1;
     }
   }
@@ -538,12 +543,16 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
   const size_t pm_bytes = (size_t)n_seq * hb * wb * sizeof(uint32_t);
   const size_t ring = g.tmode ? ta_smem_t(cs, T, g.nbuf) : ta_smem(c, T, g.nbuf, g.ppu);
   g.pm_smem = pm_bytes <= 8192 && ring + pm_bytes <= 227 * 1024 && fit(ring + pm_bytes) == fit(ring);
+#ifdef SPHINX_DEV_KNOBS
   if (const char* env = getenv("SPHINX_TA_PMSMEM")) g.pm_smem = g.pm_smem && atoi(env) != 0;
+#endif
   const size_t smem = ring + (g.pm_smem ? pm_bytes : 0);
   int per_sm = fit(smem);
   // one resident CTA per SM (the ring does not fit twice): 16 warps; two CTAs of 8 otherwise
   int threads = per_sm == 1 ? kTaMaxThreads : kTaThreads;
+#ifdef SPHINX_DEV_KNOBS
   if (const char* env = getenv("SPHINX_TA_THREADS")) threads = atoi(env) == 512 ? 512 : kTaThreads;
+#endif
   if (per_sm > 65536 / (threads * 128)) per_sm = 65536 / (threads * 128);  // <= 128 regs/thread
   e = cudaFuncSetAttribute(ta_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -554,6 +563,28 @@ extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int
                static_cast<__nv_bfloat16*>(o), static_cast<const uint32_t*>(posmask), g);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
+}
+
+extern "C" sphinx_status sphinx_temporal_attention(const void* qkv, void* o, int32_t n, int32_t h,
+                                                   int32_t w, int32_t c, int32_t heads,
+                                                   int32_t frames_per_seq, int32_t block,
+                                                   const int32_t* block_ids, const int32_t* count,
+                                                   int32_t capacity, void* workspace,
+                                                   size_t workspace_bytes, sphinx_stream_t stream) {
+  return temporal_attention_impl(qkv, o, n, h, w, c, heads, frames_per_seq, block, block_ids, count,
+                                 capacity, workspace, workspace_bytes, 0, stream);
+}
+
+extern "C" sphinx_status sphinx_temporal_attention_ex(const void* qkv, void* o, int32_t n, int32_t h,
+                                                      int32_t w, int32_t c, int32_t heads,
+                                                      int32_t frames_per_seq, int32_t block,
+                                                      const int32_t* block_ids, const int32_t* count,
+                                                      int32_t capacity, void* workspace,
+                                                      size_t workspace_bytes, int32_t head_group,
+                                                      sphinx_stream_t stream) {
+  if (head_group < 0 || (head_group > 0 && (heads % head_group))) return SPHINX_ERR_INVALID_ARGUMENT;
+  return temporal_attention_impl(qkv, o, n, h, w, c, heads, frames_per_seq, block, block_ids, count,
+                                 capacity, workspace, workspace_bytes, head_group, stream);
 }
 
 extern "C" sphinx_status sphinx_temporal_block(

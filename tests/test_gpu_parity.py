@@ -267,16 +267,21 @@ def test_noise_vs_oracle(sphinx, shape, b):
                         (1, 1, 1, 1, 2)],
                 ids=["cta1", "pair", "cta1-splitk", "pair-splitk", "pair-splitk-noedge", "pair-pertap",
                      "pair-pertap-splitk", "pair-streamk", "cta1-streamk"])
-def conv_cg(request, monkeypatch):
+def conv_cg(request, monkeypatch, sphinx):
     """Runs a conv test with the 1-SM (cta_group::1) and the CTA-pair (cta_group::2) kernels,
     without and with device-chosen split-K, with halo-staged (b=8 default, with and without
-    edge-class packing) and per-tap A, and with stream-K forced where feasible."""
+    edge-class packing) and per-tap A, and with stream-K forced where feasible -- the variant
+    flags of sphinx_sparse_conv3x3_ex (sphinx.h), passed explicitly on every conv call."""
     cg, split, halo, edge, streamk = request.param
-    monkeypatch.setenv("SPHINX_CONV_STREAMK", str(streamk))
-    monkeypatch.setenv("SPHINX_CONV_CG", str(cg))
-    monkeypatch.setenv("SPHINX_CONV_SPLIT", str(split))
-    monkeypatch.setenv("SPHINX_CONV_HALO", str(halo))
-    monkeypatch.setenv("SPHINX_CONV_EDGE", str(edge))
+    flags = ((sphinx.CONV_FORCE_CG1 if cg == 1 else 0) | (0 if split else sphinx.CONV_NO_SPLIT) |
+             (sphinx.CONV_FORCE_HALO if halo else sphinx.CONV_FORCE_PERTAP) |
+             (0 if edge else sphinx.CONV_NO_EDGE) |
+             {0: sphinx.CONV_NO_STREAMK, 1: 0, 2: sphinx.CONV_FORCE_STREAMK}[streamk])
+    plain = sphinx.sphinx_sparse_conv3x3
+
+    def with_variant(*a, **k):
+        return plain(*a, variant=flags | k.pop("variant", 0), **k)
+    monkeypatch.setattr(sphinx, "sphinx_sparse_conv3x3", with_variant)
     return request.param
 
 
@@ -370,10 +375,10 @@ def test_conv_deterministic_and_split_consistent(sphinx, monkeypatch):
     m = np.zeros((n, 3, 3), np.uint8); m[0, 0, :] = 1; m[0, 2, 2] = 1
     g_ids, g_cnt, _ = gpu_compact(sphinx, m, None, 0)
     outs = []
-    for split in ("1", "1", "0"):
-        monkeypatch.setenv("SPHINX_CONV_SPLIT", split)
+    for split in (True, True, False):
         y = torch.zeros((n, h, h, c), dtype=torch.float32, device=dev)
-        sphinx.sphinx_sparse_conv3x3(x, w, None, y, b, g_ids, g_cnt)
+        sphinx.sphinx_sparse_conv3x3(x, w, None, y, b, g_ids, g_cnt,
+                                     variant=0 if split else sphinx.CONV_NO_SPLIT)
         outs.append(y.cpu().numpy())
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
     xb = x.view(torch.int16).cpu().numpy().view(np.uint16)
@@ -589,10 +594,35 @@ def test_conv_early_start_flags(sphinx, h, c):
         assert np.array_equal(ref, y.cpu().numpy().view(np.uint32))
 
 
-@pytest.mark.parametrize("h,c,dens", [(72, 320, 0.25), (36, 640, 0.4), (20, 96 * 4, 0.6)])
-def test_conv_ragged_cout_tiles(sphinx, monkeypatch, h, c, dens):
-    """SPHINX_CONV_RAGGED=1: 256-wide C_out tiles with a narrower last tile (320 = 256 + 64,
-    640 = 2x256 + 128, 384 = 256 + 128) -- a measured-slower option kept under test."""
-    monkeypatch.setenv("SPHINX_CONV_RAGGED", "1")
-    for dt in (torch.float32, torch.bfloat16):
-        _conv_check(sphinx, 2, h, h, c, c, 8, dens, "scattered", f"ragged{h}{c}", out_dtype=dt)
+def test_conv_back_to_back_list_ready(sphinx):
+    """edge_plan(level 1) -> conv(level 0, LIST_READY) -> conv(level 1, LIST_READY |
+    REUSE_PLAN), the call order the contract allows.  The level-1 conv reads its plan (written two
+    kernels back) before its own griddepcontrol.wait; the level-0 conv only signals its dependents
+    after its epilogue waited, so the plan is complete.  Repeated with fresh lists each round so a
+    stale plan would show; results bit-identical to plain launches."""
+    rg = np.random.default_rng(11)
+    n = 4
+    x0 = bf16(syn.features_bf16((n, 72, 72, 320), "b2b0"))
+    w0 = bf16(syn.weights_bf16(320, 320, "b2b0"))
+    x1 = bf16(syn.features_bf16((n, 36, 36, 640), "b2b1"))
+    w1 = bf16(syn.weights_bf16(640, 640, "b2b1"))
+    ws0 = torch.zeros(sphinx.load().sphinx_conv_workspace_size(n, 72, 72, 320, 320, 8), dtype=torch.uint8,
+                      device=dev)
+    ws1 = torch.zeros(sphinx.load().sphinx_conv_workspace_size(n, 36, 36, 640, 640, 8), dtype=torch.uint8,
+                      device=dev)
+    for rnd in range(4):
+        m0 = (rg.random((n, 9, 9)) < 0.3 + 0.1 * rnd).astype(np.uint8)
+        m1 = (rg.random((n, 5, 5)) < 0.7 - 0.1 * rnd).astype(np.uint8)
+        i0, c0, _ = gpu_compact(sphinx, m0, None, 0)
+        i1, c1, _ = gpu_compact(sphinx, m1, None, 0)
+        ya = [torch.zeros((n, 72, 72, 320), device=dev), torch.zeros((n, 36, 36, 640), device=dev)]
+        yb = [torch.zeros_like(ya[0]), torch.zeros_like(ya[1])]
+        sphinx.sphinx_sparse_conv3x3(x0, w0, None, ya[0], 8, i0, c0, workspace=False)
+        sphinx.sphinx_sparse_conv3x3(x1, w1, None, ya[1], 8, i1, c1, workspace=False)
+        sphinx.sphinx_conv_edge_plan(i1, c1, n, 36, 36, 8, 640, workspace=ws1)
+        sphinx.sphinx_sparse_conv3x3(x0, w0, None, yb[0], 8, i0, c0, workspace=ws0, list_ready=True)
+        sphinx.sphinx_sparse_conv3x3(x1, w1, None, yb[1], 8, i1, c1, workspace=ws1, reuse_plan=True,
+                                     list_ready=True)
+        torch.cuda.synchronize()
+        for a, b in zip(ya, yb):
+            assert np.array_equal(a.cpu().numpy(), b.cpu().numpy()), rnd

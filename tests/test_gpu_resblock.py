@@ -292,10 +292,16 @@ def _chain_tol(o, x_bits, params, groups, shift):
 
 
 @pytest.fixture(params=["fused", "unfused"])
-def rb_path(request, monkeypatch):
-    """The block with GN+SiLU fused into the conv's halo path (SPHINX_RB_FUSED=1, 8x8 blocks) and
+def rb_path(request, monkeypatch, sphinx):
+    """The block with GN+SiLU fused into the conv's halo path (SPHINX_RB_FUSED_GN, 8x8 blocks) and
     with the separate gn_silu activation pass (the default)."""
-    monkeypatch.setenv("SPHINX_RB_FUSED", "1" if request.param == "fused" else "0")
+    if request.param == "fused":
+        plain = sphinx.sphinx_sparse_resblock
+
+        def fused(*a, **k):
+            bl = a[14] if len(a) > 14 else k["block"]
+            return plain(*a, fused=bl == 8, **k)
+        monkeypatch.setattr(sphinx, "sphinx_sparse_resblock", fused)
     return request.param
 
 

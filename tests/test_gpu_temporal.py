@@ -94,8 +94,18 @@ class TB:
         self.y = T_(y_cache.astype(np.float32))
         self.o = torch.zeros((n, h, w, c), dtype=torch.bfloat16, device=dev)
 
+    head_group = 0  # > 0: compose the block from its public calls with this head grouping
+
     def run(self, x_bits, params, ids, cnt):
         wq, bq, wo, bo = params
+        if self.head_group:
+            x = bf16(x_bits)
+            self.sp.sphinx_sparse_pointwise(x, bf16(wq), None if bq is None else T_(bq), self.qkv, self.b, ids, cnt)
+            self.sp.sphinx_temporal_attention(self.qkv, self.o, self.heads, self.T, self.b, ids, cnt,
+                                              head_group=self.head_group)
+            self.sp.sphinx_sparse_pointwise(self.o, bf16(wo), None if bo is None else T_(bo), self.y, self.b, ids,
+                                            cnt, residual=x)
+            return
         self.sp.sphinx_temporal_block(bf16(x_bits), bf16(wq), None if bq is None else T_(bq), bf16(wo),
                                       None if bo is None else T_(bo), self.heads, self.T, self.qkv, self.o,
                                       self.y, self.b, ids, cnt)
@@ -272,38 +282,6 @@ def test_temporal_block_full_size_bench_config(sphinx):
     assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
 
 
-@pytest.mark.parametrize("knob", ["SPHINX_TA_PPU=2", "SPHINX_TA_KVONLY=1", "SPHINX_TA_STREAM=0",
-                                  "SPHINX_TA_STREAM=1,SPHINX_TA_NBUF=1", "SPHINX_TA_NBUF=3",
-                                  "SPHINX_TA_NBUF=5,SPHINX_TA_THREADS=512", "SPHINX_TA_PMSMEM=0",
-                                  "SPHINX_TA_TMAP=0", "SPHINX_TA_TMAP=1,SPHINX_TA_NBUF=1",
-                                  "SPHINX_TA_TMAP=1,SPHINX_TA_NBUF=3"])
-def test_temporal_block_staging_variants(sphinx, monkeypatch, knob):
-    """The measured-slower staging variants kept as options -- two x-adjacent pixels per bulk copy
-    (on an odd-width map: ragged last pair), k|v of all frames + q of listed frames only, the CTA
-    barrier per unit instead of the task stream, other ring depths / CTA sizes, frame masks read
-    from global memory, T bulk copies instead of the one TMA tensor copy per unit (and the tensor
-    copy single-buffered / 3-deep) -- equal the oracle like the default path."""
-    for kv in knob.split(","):
-        k, v = kv.split("=")
-        monkeypatch.setenv(k, v)
-    n, h, w, c, T, b = 4, 16, 13, 64, 2, 8
-    x = syn.resblock_features_bf16((n, h, w, c), "tbppu")
-    qkv_cache = syn.resblock_features_bf16((n, h, w, 3 * c), "tbppu-qc")
-    y_cache = dec(syn.features_bf16((n, h, w, c), "tbppu-yc"))
-    params = identity_params(c)
-    mask = block_mask(n, h, w, b, 0.6, "scattered", "tbppu")
-    tb = TB(sphinx, n, h, w, c, 1, T, b, qkv_cache, y_cache)
-    ids, cnt = gpu_ids(sphinx, mask)
-    tb.run(x, params, ids, cnt)
-    torch.cuda.synchronize()
-    o = oracle.temporal_attn(x, qkv_cache, y_cache, *params, 1, T, b, oracle.compact(mask))
-    L = listed_px(mask, h, w, b)
-    E_o = attn_tol(o, 1, T, c)
-    tol = 2 * half_ulp(o["o_pre"]) + E_o + 2.0 ** -23 * np.abs(o["y"]) + 1e-7
-    err = np.abs(tb.y.cpu().numpy().astype(np.float64) - o["y"])
-    assert np.all(err[L] <= tol[L]), f"y max err/tol {np.max(err[L] / tol[L])}"
-
-
 @pytest.mark.parametrize("k,case", [
     (5, (6, 18, 18, 640, 3, 8, 0.5, "scattered", True)),
     (5, (4, 18, 18, 1280, 4, 8, 0.5, "scattered", False)),
@@ -311,7 +289,9 @@ def test_temporal_block_staging_variants(sphinx, monkeypatch, knob):
     (1, (4, 18, 18, 1280, 4, 8, 0.5, "scattered", False)),
 ])
 def test_temporal_block_head_groups(sphinx, monkeypatch, k, case):
-    """SPHINX_TA_HGROUP=k: units of (pixel, k heads) staged by one 5-D tensor copy of the group's
-    q|k|v slices -- equal to the oracle like the default path."""
-    monkeypatch.setenv("SPHINX_TA_HGROUP", str(k))
+    """head_group = k (sphinx_temporal_attention_ex): units of (pixel, k heads) staged by one 5-D
+    tensor copy of the group's q|k|v slices -- equal to the oracle like the default path.  The
+    block runs as its three public calls (q|k|v pointwise, attention with the override, output
+    pointwise + residual), the sequence sphinx_temporal_block launches."""
+    monkeypatch.setattr(TB, "head_group", k)
     test_temporal_block_vs_oracle(sphinx, *case)
