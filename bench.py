@@ -1,24 +1,33 @@
 """Benchmark of the Sphinx selective-refinement hot path on B200 (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-sweep]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload configs3|configs2|configs4] [--no-extras] ...
 
-A STEP is one pass of the whole hot path over one 21-frame
-request (BASELINE configs[2]): block masks + start steps from the 576x576 opacity and
-uncertainty maps -> compaction at 3 UNet levels (+ the inactive-frame list) -> noise
-injection on the active latent blocks (start step k) and resampling of inactive frames
-(u+1) -> per level two block-sparse 3x3 convs C->C in persistent-buffer mode
-(72x72x320, 36x36x640, 18x18x1280) -> cached scatter of the last conv output into the
-full-resolution map.  value = effective conv TFLOP/s over the step: algorithmic FLOPs
-(2*9*Cin*Cout per REAL active output pixel) / device step time.
+A STEP is one pass of the whole hot path over one batch of requests
+(paper_2511_18672_b200.step.RefinementStep): block masks + start steps from the 576x576
+opacity and uncertainty maps -> compaction at 3 UNet levels (+ the inactive-frame list) ->
+noise injection on the active latent blocks (start step k) and resampling of inactive frames
+(u+1) -> per level two block-sparse 3x3 convs C->C in persistent-buffer mode (72x72x320,
+36x36x640, 18x18x1280) -> cached scatter of the latent.  value = effective conv TFLOP/s of the
+whole job: algorithmic FLOPs (2*9*Cin*Cout per REAL active output pixel, every frame of the
+batch) / device step time (max over ranks).
 
-Multi-GPU (torchrun): weak scaling, every rank runs its own request (independent seed);
-no collective on the data path, the timing max is taken over ranks.
---impl reference times the CPU oracle (oracle/) on a bounded sample of the same step.
+Default workload = BASELINE configs[3]: 8 requests x 21 frames with request densities
+[5,10,25,50,75,25,10,5]%, sharded across the N ranks by active-block cost (LPT) with NCCL
+only for the mask/start-step all-gather and the owner gather of refined blocks;
+total work is fixed, so scaling is "strong".  At N = 1 the line also carries configs[2]
+(one request, round 1's headline workload), configs[4] (25% per request vs the same step
+done densely with cuDNN), the configs[1] density sweep, the HBM-bound kernels, the NEXT rows,
+the e2e serving loop and the CPU oracle baseline.
+
+Launch: with --gpus N > 1 and no WORLD_SIZE in the environment, the script re-executes itself
+under torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous).
+--impl reference times the CPU oracle (oracle/) on a bounded sample of the same workload.
 """
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,11 +41,39 @@ sys.path.insert(0, ROOT)
 
 import synthetic as syn  # noqa: E402
 
-LEVELS = [(72, 320), (36, 640), (18, 1280)]  # BASELINE configs[2]
-N_FRAMES, HP, F, B, S, U_STEP, GAMMA = 21, 576, 8, 8, 50, 25, 0.5
-MEAN_DENSITY = 0.25
+METRIC = "block-sparse conv effective TFLOP/s & speedup vs dense at 10/25/50% density"
+LEVELS = syn.UNET_LEVELS
 CONVS_PER_LEVEL = 2
+HP, F, B, U_STEP, GAMMA, FPR = 576, 8, 8, 25, 0.5, 21
 
+WORKLOADS = {
+    "configs3": dict(means=syn.CONFIG3_REQUEST_DENSITIES, tag="c3",
+                     desc="configs[3]: 8 requests x 21 frames (168), request densities [5,10,25,50,75,25,10,5]% "
+                          "(per-frame U-shape within each request), 3 UNet levels (72x72x320, 36x36x640, "
+                          "18x18x1280), per-frame adaptive start steps, u=25; frames sharded across ranks by "
+                          "active-block cost (LPT), refined blocks gathered to each request's owner"),
+    "configs2": dict(means=(0.25,), tag="r0",
+                     desc="configs[2]: 21-frame request, 3 UNet levels (72x72x320, 36x36x640, 18x18x1280), "
+                          "per-frame adaptive start steps, mean level-0 density 25%"),
+    "configs4": dict(means=(0.25,) * 8, tag="c4",
+                     desc="configs[4]: full refinement step, 8 requests x 21 frames at 25% mean level-0 density "
+                          "each, vs the same step done densely"),
+}
+
+
+def step_config(means):
+    from paper_2511_18672_b200.step import StepConfig
+    return StepConfig(hp=HP, f=F, b=B, levels=LEVELS, convs_per_level=CONVS_PER_LEVEL, frames_per_request=FPR,
+                      n_requests=len(means), u=U_STEP, gamma=GAMMA)
+
+
+def make_batch(name):
+    w = WORKLOADS[name]
+    return syn.make_batch(w["means"], tag=w["tag"], hp=HP, f=F, b=B, levels=LEVELS,
+                          convs_per_level=CONVS_PER_LEVEL, frames_per_request=FPR)
+
+
+# ----------------------------------------------------------------- measurement helpers
 
 def ncu_traffic(kernel_sig):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes) of the conv launches whose
@@ -72,121 +109,6 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-# ----------------------------------------------------------------- workload (host)
-
-def make_request(seed_tag):
-    """Host arrays of one 21-frame request (DESIGN.md §5 input recipe)."""
-    dens = syn.request_densities(N_FRAMES, MEAN_DENSITY)
-    O, cells = syn.opacity_maps(N_FRAMES, HP, HP, B * F, dens, "clustered", tag=f"O{seed_tag}")
-    U, tau_u = syn.uncertainty_maps(N_FRAMES, HP, HP, B * F, cells, tag=f"U{seed_tag}")
-    q, c0, c1, t = syn.request_scores(N_FRAMES, tag=f"q{seed_tag}")
-    # frames 0 and N-1 are the conditioning inputs (P:447): logic_id -1 excludes them (R-14)
-    lid = np.zeros(N_FRAMES, np.int32)
-    lid[0] = lid[-1] = -1
-    req = dict(O=O, U=U, tau_u=tau_u, q=q, c0=c0, c1=c1, t=t, lid=lid, abar=syn.abar_cosine(S))
-    h0 = HP // F
-    req["x0"] = syn.latents_f32((N_FRAMES, h0, h0, 4), f"x0{seed_tag}")
-    req["eps"] = syn.latents_f32((N_FRAMES, h0, h0, 4), f"eps{seed_tag}")
-    req["lat_cache"] = syn.latents_f32((N_FRAMES, h0, h0, 4), f"lc{seed_tag}")
-    for l, (h, c) in enumerate(LEVELS):
-        req[f"feat{l}"] = syn.features_bf16((N_FRAMES, h, h, c), f"x{l}{seed_tag}")
-        req[f"cache{l}"] = syn.features_bf16((N_FRAMES, h, h, c), f"c{l}{seed_tag}")
-        for j in range(CONVS_PER_LEVEL):
-            req[f"w{l}{j}"] = syn.weights_bf16(c, c, f"w{l}{j}")
-            req[f"b{l}{j}"] = syn.bias_f32(c, f"b{l}{j}")
-    return req
-
-
-# ----------------------------------------------------------------- GPU arm
-
-class GpuStep:
-    """Device buffers + the step as a sequence of C-ABI calls."""
-
-    def __init__(self, req, dev):
-        import torch
-        import paper_2511_18672_b200 as sp
-        self.sp, self.torch, self.dev = sp, torch, dev
-        sp.load()
-        self.req = req
-        g = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-        self.bf = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
-        self.d = {k: (self.bf(v) if v.dtype == np.uint16 else g(v)) for k, v in req.items()}
-        n = N_FRAMES
-        h0 = HP // F
-        self.dims = [(h0 >> l, -(-(h0 >> l) // B)) for l in range(3)]
-        self.masks = [torch.empty((n, hb, hb), dtype=torch.uint8, device=dev) for (_, hb) in self.dims]
-        self.counts = torch.empty((n, 3), dtype=torch.int32, device=dev)
-        self.k = torch.empty((n,), dtype=torch.int32, device=dev)
-        self.ids = [torch.empty((n * hb * hb,), dtype=torch.int32, device=dev) for (_, hb) in self.dims]
-        self.cnt = [torch.empty((1,), dtype=torch.int32, device=dev) for _ in range(3)]
-        self.ids_in = torch.empty((n * self.dims[0][1] ** 2,), dtype=torch.int32, device=dev)
-        self.cnt_in = torch.empty((1,), dtype=torch.int32, device=dev)
-        self.step_u1 = torch.full((n,), U_STEP + 1, dtype=torch.int32, device=dev)
-        self.zt = torch.empty_like(self.d["x0"])
-        # persistent buffers (R-17): pre-filled with the cache once (the full step's job), the
-        # conv epilogue then writes only active blocks, i.e. the feature-level scatter is fused
-        self.y = [self.d[f"cache{l}"].clone() for l in range(3)]
-        self.z = [self.d[f"cache{l}"].clone() for l in range(3)]
-        self.lat_out = torch.empty_like(self.d["x0"])
-        self.logics = [sp.make_klogic(syn.SPEC_KLOGIC["thr"], syn.SPEC_KLOGIC["steps"])]
-        # block_mask (2) + batched compaction (1) + noise (2) + convs + edge plans (levels 1, 2:
-        # once per level) + scatter (1)
-        self.launches_per_step = 2 + 1 + 2 + 3 * CONVS_PER_LEVEL + 2 + 1
-        self.conv_events = None
-
-    def run(self, conv_events=None):
-        sp, d = self.sp, self.d
-        start = dict(q_reg=d["q"], c0=d["c0"], c1=d["c1"], t=d["t"], gamma=GAMMA, logics=self.logics,
-                     logic_id=d["lid"])
-        sp.sphinx_block_mask(d["O"], d["U"], d["tau_u"], 0.5, F, B, self.masks, self.counts, start, self.k)
-        # the three levels' ACTIVE lists and the INACTIVE_FRAMES list: one launch, one CTA per list
-        sp.sphinx_compact_blocks_batch(
-            [dict(block_mask=self.masks[l], start_step=self.k, step_u=U_STEP, select=sp.SELECT_ACTIVE,
-                  block_ids=self.ids[l], count=self.cnt[l]) for l in range(3)] +
-            [dict(block_mask=None, start_step=self.k, step_u=U_STEP, select=sp.SELECT_INACTIVE_FRAMES,
-                  block_ids=self.ids_in, count=self.cnt_in, shape=tuple(self.masks[0].shape))])
-        # the edge-class plans of the ragged levels (36x36, 18x18) right after compaction, so every
-        # conv of the step reuses its level's plan and may start before its predecessor ends
-        for l in (1, 2):
-            h, c = LEVELS[l]
-            sp.sphinx_conv_edge_plan(self.ids[l], self.cnt[l], N_FRAMES, h, h, B, c)
-        # Alg1 line 12: active latent blocks noised to their start step k; line 19: inactive
-        # frames resampled to u+1 from the clean latent
-        sp.sphinx_noise_inject(d["x0"], d["eps"], self.zt, B, self.ids[0], self.cnt[0], self.k, d["abar"])
-        sp.sphinx_noise_inject(d["x0"], d["eps"], self.zt, B, self.ids_in, self.cnt_in, self.step_u1, d["abar"])
-        for l in range(3):
-            src = d[f"feat{l}"]
-            for j in range(CONVS_PER_LEVEL):
-                dst = self.y[l] if j % 2 == 0 else self.z[l]
-                if conv_events is not None:
-                    conv_events[l][j][0].record()
-                # every conv of a level uses the list's plan computed above (same workspace)
-                sp.sphinx_sparse_conv3x3(src, d[f"w{l}{j}"], d[f"b{l}{j}"], dst, B, self.ids[l], self.cnt[l],
-                                         reuse_plan=True, list_ready=True,
-                                         input_ready=j == 0)  # a level's input features are step inputs
-                if conv_events is not None:
-                    conv_events[l][j][1].record()
-                src = dst
-        # step 5 at latent resolution: refined latent blocks from this step, the latent cache of
-        # the last full step everywhere else (P:352 spatial latent reuse)
-        sp.sphinx_scatter_cached(self.zt, d["lat_cache"], self.lat_out, B, block_mask=self.masks[0],
-                                 start_step=self.k, step_u=U_STEP)
-
-    def active_stats(self):
-        """Algorithmic FLOPs of the step's convs: real active pixels x 2*9*Cin*Cout."""
-        flops, px_l, blocks = 0, [], []
-        for l, (h, c) in enumerate(LEVELS):
-            ids = self.ids[l][: int(self.cnt[l].item())].cpu().numpy()
-            hb = self.dims[l][1]
-            r = ids % (hb * hb)
-            by, bx = r // hb, r % hb
-            px = int((np.minimum(B, h - by * B) * np.minimum(B, h - bx * B)).sum())
-            px_l.append(px)
-            blocks.append(len(ids))
-            flops += CONVS_PER_LEVEL * px * 2 * 9 * c * c
-        return flops, px_l, blocks
-
-
 def sample_clocks(stop, out, gpu_index):
     cmd = ["nvidia-smi", "-i", str(gpu_index),
            "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
@@ -197,6 +119,7 @@ def sample_clocks(stop, out, gpu_index):
         p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
     except FileNotFoundError:
         return
+
     def reader():
         for line in p.stdout:
             out.append(line.strip())
@@ -230,18 +153,22 @@ def summarize_clocks(lines):
 
 def graph_time(torch, fn, reps=20):
     """Device time per call: `reps` calls captured in one CUDA graph and replayed (no host
-    launch overhead in the measurement); median over 5 replays."""
-    for _ in range(3):
-        fn()
+    launch overhead in the measurement); median over 5 replays.  Warm-up runs on the capture
+    stream, so per-stream workspaces exist before the capture."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    with torch.cuda.graph(g, stream=s):
         for _ in range(reps):
             fn()
     g.replay()
     torch.cuda.synchronize()
     ts = []
-    for _ in range(5):  # median of 5 replays (one replay moved by up to +-25% run to run)
+    for _ in range(5):  # median of 5 replays
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         g.replay()
@@ -251,10 +178,62 @@ def graph_time(torch, fn, reps=20):
     return sorted(ts)[2]
 
 
+def capture_step(torch, st, with_conv_events):
+    """Captures one single-rank step into a CUDA graph (a PDL chain of ~15 kernels).  Conv
+    launches are bracketed by external event-record nodes so their device time is measured
+    inside the replayed graph."""
+    conv_ev = None
+    L = st.cfg.L
+    if with_conv_events:
+        conv_ev = [[[torch.cuda.Event(enable_timing=True, external=True),
+                     torch.cuda.Event(enable_timing=True, external=True)]
+                    for _ in range(CONVS_PER_LEVEL)] for _ in range(L)]
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            st.run()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=side):
+        st.run(conv_ev)
+    torch.cuda.synchronize()
+    return g, conv_ev
+
+
+def timed_steps(torch, run_step, reps, flush, args, world, conv_events=None, conv_ms=None):
+    """K steps, each bracketed by CUDA events on the launching stream, the L2 flushed between
+    steps (256 MB write, outside the timed window), barrier + synchronize on both sides."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run_step()
+        e1.record()
+        if not args.no_flush:
+            flush.fill_(1.0)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        if conv_events is not None:
+            for l in range(len(conv_events)):
+                for j in range(CONVS_PER_LEVEL):
+                    conv_ms[l][j].append(conv_events[l][j][0].elapsed_time(conv_events[l][j][1]))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    return ms
+
+
 def density_sweep(torch, sp, dev, frames_list=(1, 21, 168), dens=(0.05, 0.10, 0.25, 0.50, 0.75, 1.0)):
     """configs[1]: 72x72x320, block 8, density sweep 5-100% (1 frame, and the 21-frame and
-    168-frame = configs[3]-sized batched variants): own sparse conv vs own dense launch (all blocks listed) vs cuDNN dense
-    (torch conv2d, channels_last bf16, fp32 accumulate).  Graph-replay device time, L2-warm."""
+    168-frame = configs[3]-sized batched variants): own sparse conv vs own dense launch (all
+    blocks listed) vs cuDNN dense (torch conv2d, channels_last bf16, fp32 accumulate).  Graph-
+    replay device time, L2-warm."""
     h, c = 72, 320
     hb = 9
     out = []
@@ -265,7 +244,7 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21, 168), dens=(0.05, 0.10, 0.
         xn = x.permute(0, 3, 1, 2)
         wn = w.permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
         t_cudnn = graph_time(torch, lambda: torch.nn.functional.conv2d(xn, wn, padding=1))
-        sp.conv_workspace(c, dev, nf, h, h, B)
+        ws = torch.zeros(int(sp.load().sphinx_conv_workspace_size(nf, h, h, c, c, B)), dtype=torch.uint8, device=dev)
         rows = []
         for d in list(dens):
             rg = syn.rng("sweep-mask", nf, d)
@@ -273,7 +252,7 @@ def density_sweep(torch, sp, dev, frames_list=(1, 21, 168), dens=(0.05, 0.10, 0.
             ids_np = np.flatnonzero(m.ravel()).astype(np.int32)
             ids = torch.from_numpy(ids_np).to(dev)
             cnt = torch.tensor([len(ids_np)], dtype=torch.int32, device=dev)
-            t = graph_time(torch, lambda: sp.sphinx_sparse_conv3x3(x, w, None, y, B, ids, cnt))
+            t = graph_time(torch, lambda: sp.sphinx_sparse_conv3x3(x, w, None, y, B, ids, cnt, workspace=ws))
             flops = len(ids_np) * 64 * 2 * 9 * c * c
             rows.append({"density": round(len(ids_np) / (nf * 81), 4), "active_blocks": int(len(ids_np)),
                          "sparse_ms": round(t, 5), "eff_tflops": round(flops / t / 1e9, 2)})
@@ -294,18 +273,18 @@ def dense_step(torch, st, flush, reps):
     """configs[4]'s comparison: the same step done densely -- the six convs over every pixel
     (cuDNN via torch conv2d, channels_last bf16, fp32 accumulate) plus dense noise on the whole
     latent -- as a CUDA graph, same cold-L2 protocol as the sparse step."""
-    d = st.d
-    xs = [d[f"feat{l}"].permute(0, 3, 1, 2) for l in range(3)]
+    d, cfg = st.d, st.cfg
+    xs = [d[f"feat{l}"].permute(0, 3, 1, 2) for l in range(cfg.L)]
     ws = [[d[f"w{l}{j}"].permute(0, 3, 1, 2).contiguous(memory_format=torch.channels_last)
-           for j in range(CONVS_PER_LEVEL)] for l in range(3)]
-    bs = [[d[f"b{l}{j}"].to(torch.bfloat16) for j in range(CONVS_PER_LEVEL)] for l in range(3)]
-    ab = d["abar"][U_STEP]
+           for j in range(CONVS_PER_LEVEL)] for l in range(cfg.L)]
+    bs = [[d[f"b{l}{j}"].to(torch.bfloat16) for j in range(CONVS_PER_LEVEL)] for l in range(cfg.L)]
+    ab = d["abar"][cfg.u]
     a, sgm = ab.sqrt(), (1 - ab).sqrt()
 
     def run():
         zt = a * d["x0"] + sgm * d["eps"]
         outs = [zt]
-        for l in range(3):
+        for l in range(cfg.L):
             src = xs[l]
             for j in range(CONVS_PER_LEVEL):
                 src = torch.nn.functional.conv2d(src, ws[l][j], bs[l][j], padding=1)
@@ -327,39 +306,16 @@ def dense_step(torch, st, flush, reps):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = statistics.mean(ts)
-    dense_flops = sum(N_FRAMES * h * h * 2 * 9 * c * c * CONVS_PER_LEVEL for (h, c) in LEVELS)
+    dense_flops = sum(cfg.n_frames * h * h * 2 * 9 * c * c * CONVS_PER_LEVEL for (h, c) in cfg.levels)
     return {"ms": round(ms, 5), "dense_tflops": round(dense_flops / (ms * 1e-3) / 1e12, 1),
             "what": "6 dense convs (cuDNN, channels_last bf16) + dense noise, CUDA graph, L2 flushed"}
 
 
-def capture_step(torch, st, with_conv_events):
-    """Captures one step into a CUDA graph (launch-bound chain of ~15 kernels).  Conv launches
-    are bracketed by external event-record nodes so their device time is measured inside the
-    replayed graph."""
-    conv_ev = None
-    if with_conv_events:
-        conv_ev = [[[torch.cuda.Event(enable_timing=True, external=True),
-                     torch.cuda.Event(enable_timing=True, external=True)]
-                    for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
-    g = torch.cuda.CUDAGraph()
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        for _ in range(2):
-            st.run()
-    torch.cuda.current_stream().wait_stream(side)
-    torch.cuda.synchronize()
-    with torch.cuda.graph(g):
-        st.run(conv_ev)
-    torch.cuda.synchronize()
-    return g, conv_ev
-
-
-def memory_kernels(torch, st, req, reps=10):
+def memory_kernels(torch, st, reps=10):
     """HBM-bound / latency-bound kernels timed one launch at a time after an L2 flush (cold),
     CUDA events on the launching stream; algorithmic bytes / time vs the measured HBM peak.
     Includes the NEXT rows (DDIM update, uncertainty producer) measured beside the step."""
-    sp, d, dev = st.sp, st.d, st.dev
+    sp, d, dev, cfg = st.ops, st.d, st.dev, st.cfg
     hbm = peaks()[0]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -377,93 +333,99 @@ def memory_kernels(torch, st, req, reps=10):
         return statistics.median(ts)
 
     out = {}
+
     def row(name, ms, nbytes, note):
         out[name] = {"ms": round(ms, 5), "algorithmic_bytes": int(nbytes),
-                     "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1), "hbm_frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4),
-                     "bytes": note}
-    n, hp = N_FRAMES, HP
-    start = dict(q_reg=d["q"], c0=d["c0"], c1=d["c1"], t=d["t"], gamma=GAMMA, logics=st.logics, logic_id=d["lid"])
-    ms = timed(lambda: sp.sphinx_block_mask(d["O"], d["U"], d["tau_u"], 0.5, F, B, st.masks, st.counts, start, st.k))
+                     "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
+                     "hbm_frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": note}
+    n, hp = cfg.n_frames, cfg.hp
+    ms = timed(lambda: sp.sphinx_block_mask(d["O"], d["U"], d["tau_u"], cfg.tau_o, cfg.f, cfg.b, st.masks,
+                                            st.counts, st._start_args(), st.k))
     row("block_mask", ms, n * hp * hp * 8, "two fp32 maps read (8 B/px)")
     cnt = int(st.cnt[0].item())
-    ms = timed(lambda: sp.sphinx_compact_blocks(st.masks[0], st.k, U_STEP, sp.SELECT_ACTIVE, st.ids[0], st.cnt[0]))
-    out["compact_blocks"] = {"ms": round(ms, 5), "entries": n * 81, "bound": "latency (one CTA)"}
-    ms = timed(lambda: sp.sphinx_noise_inject(d["x0"], d["eps"], st.zt, B, st.ids[0], st.cnt[0], st.k, d["abar"]))
-    row("noise_inject", ms, cnt * 64 * 4 * 12, "12 B per active latent element (x0, eps in; x_t out)")
+    ms = timed(lambda: sp.sphinx_compact_blocks(st.masks[0], st.k, cfg.u, sp.SELECT_ACTIVE, st.ids[0], st.cnt[0]))
+    out["compact_blocks"] = {"ms": round(ms, 5), "entries": n * cfg.hb[0] ** 2, "bound": "latency (one CTA)"}
+    ms = timed(lambda: sp.sphinx_noise_inject(d["x0"], d["eps"], st.zt, cfg.b, st.ids[0], st.cnt[0], st.k,
+                                              d["abar"]))
+    row("noise_inject", ms, cnt * 64 * cfg.c_lat * 12, "12 B per active latent element (x0, eps in; x_t out)")
     out0 = torch.empty_like(d["cache0"])
-    ms = timed(lambda: sp.sphinx_scatter_cached(st.z[0], d["cache0"], out0, B, block_mask=st.masks[0],
-                                                start_step=st.k, step_u=U_STEP))
-    row("scatter_cached_level0_features", ms, 2 * out0.numel() * 2, "2 x map bytes (21x72x72x320 bf16)")
+    ms = timed(lambda: sp.sphinx_scatter_cached(st.z[0], d["cache0"], out0, cfg.b, block_mask=st.masks[0],
+                                                start_step=st.k, step_u=cfg.u))
+    row("scatter_cached_level0_features", ms, 2 * out0.numel() * 2, f"2 x map bytes ({n}x72x72x320 bf16)")
+    pay = torch.empty((max(cnt, 1), cfg.b, cfg.b, 320), dtype=torch.bfloat16, device=dev)
+    ms = timed(lambda: sp.sphinx_gather_blocks(st.z[0], pay, cfg.b, st.ids[0], st.cnt[0]))
+    row("gather_blocks_level0 (data plane pack)", ms, 2 * cnt * 64 * 320 * 2, "2 x listed block bytes")
     zo = torch.empty_like(st.zt)
-    ms = timed(lambda: sp.sphinx_ddim_step(st.zt, d["x0"], zo, B, st.ids[0], st.cnt[0], U_STEP, req["abar"]))
-    row("ddim_step (NEXT-1)", ms, cnt * 64 * 4 * 12, "12 B per active latent element (z, x0_hat in; z' out)")
-    rgb = torch.rand((n, hp, hp, 3), device=dev, dtype=torch.float32)
-    U = torch.empty((n, hp, hp), device=dev, dtype=torch.float32)
-    tau = torch.empty((n,), device=dev, dtype=torch.float32)
+    ms = timed(lambda: sp.sphinx_ddim_step(st.zt, d["x0"], zo, cfg.b, st.ids[0], st.cnt[0], cfg.u,
+                                           d["abar"].cpu().numpy()))
+    row("ddim_step (NEXT-1)", ms, cnt * 64 * cfg.c_lat * 12, "12 B per active latent element (z, x0_hat in; z' out)")
+    nu = min(n, 21)
+    rgb = torch.rand((nu, hp, hp, 3), device=dev, dtype=torch.float32)
+    U = torch.empty((nu, hp, hp), device=dev, dtype=torch.float32)
+    tau = torch.empty((nu,), device=dev, dtype=torch.float32)
     ms = timed(lambda: sp.sphinx_uncertainty_map(rgb, U, tau))
-    row("uncertainty_map (NEXT-2)", ms, n * hp * hp * 16, "rgb read 12 B/px + U write 4 B/px (algorithmic)")
+    row("uncertainty_map (NEXT-2, 21 frames)", ms, nu * hp * hp * 16, "rgb read 12 B/px + U write 4 B/px")
     return out
 
 
-def resblock_levels(torch, st, req, reps=20):
+def resblock_levels(torch, st, reps=20):
     """NEXT-3: the block-sparse ResNet block (GN+SiLU -> conv -> GN+SiLU -> conv + skip) at each
     UNet level over the step's active list, after a full step (every block) filled the persistent
     h / y / statistics buffers.  Graph-replay device time per block (L2-warm) and its parts."""
-    sp, d, dev = st.sp, st.d, st.dev
+    sp, d, dev, cfg = st.ops, st.d, st.dev, st.cfg
     out = []
-    for l, (h, c) in enumerate(LEVELS):
-        n, hb = N_FRAMES, st.dims[l][1]
+    for l, (h, c) in enumerate(cfg.levels):
+        n, hb = cfg.n_frames, cfg.hb[l]
         x = d[f"feat{l}"]
         g1, be1 = (torch.from_numpy(a).to(dev) for a in syn.gn_affine_f32(c, f"gn{l}1"))
         g2, be2 = (torch.from_numpy(a).to(dev) for a in syn.gn_affine_f32(c, f"gn{l}2"))
         hbuf = d[f"cache{l}"].clone()
         y = d[f"cache{l}"].clone()
         a = torch.empty_like(x)
-        xs = sp.gn_stats_buffer(n, h, h, syn.GN_GROUPS, B, dev)
-        hs = sp.gn_stats_buffer(n, h, h, syn.GN_GROUPS, B, dev)
+        xs = sp.gn_stats_buffer(n, h, h, syn.GN_GROUPS, cfg.b, dev)
+        hs = sp.gn_stats_buffer(n, h, h, syn.GN_GROUPS, cfg.b, dev)
         all_ids = torch.arange(n * hb * hb, dtype=torch.int32, device=dev)
         all_cnt = torch.tensor([n * hb * hb], dtype=torch.int32, device=dev)
         ids, cnt = st.ids[l], st.cnt[l]
 
         def block(i=ids, k=cnt):
             sp.sphinx_sparse_resblock(x, d[f"w{l}0"], d[f"b{l}0"], d[f"w{l}1"], d[f"b{l}1"], (g1, be1),
-                                      (g2, be2), syn.GN_GROUPS, syn.GN_EPS, hbuf, xs, hs, y, a, B, i, k)
+                                      (g2, be2), syn.GN_GROUPS, syn.GN_EPS, hbuf, xs, hs, y, a, cfg.b, i, k)
         block(all_ids, all_cnt)  # the full step: every block, fills h, y and both statistics
         t_block = graph_time(torch, block, reps)
         t_gn = graph_time(torch, lambda: (
-            sp.sphinx_gn_block_stats(x, syn.GN_GROUPS, B, ids, cnt, xs),
-            sp.sphinx_gn_silu(x, xs, g1, be1, syn.GN_EPS, syn.GN_GROUPS, B, ids, cnt, a)), reps)
-        t_conv = graph_time(torch, lambda: sp.sphinx_sparse_conv3x3(a, d[f"w{l}0"], d[f"b{l}0"], hbuf, B, ids, cnt),
-                            reps)
+            sp.sphinx_gn_block_stats(x, syn.GN_GROUPS, cfg.b, ids, cnt, xs),
+            sp.sphinx_gn_silu(x, xs, g1, be1, syn.GN_EPS, syn.GN_GROUPS, cfg.b, ids, cnt, a)), reps)
+        t_conv = graph_time(torch, lambda: sp.sphinx_sparse_conv3x3(a, d[f"w{l}0"], d[f"b{l}0"], hbuf, cfg.b,
+                                                                    ids, cnt), reps)
         nb = int(cnt.item())
         idn = ids[:nb].cpu().numpy() % (hb * hb)
         by, bx = idn // hb, idn % hb
-        px = int((np.minimum(B, h - by * B) * np.minimum(B, h - bx * B)).sum())
-        ring = int(((np.minimum(by * B + B + 1, h) - np.maximum(by * B - 1, 0)) *
-                    (np.minimum(bx * B + B + 1, h) - np.maximum(bx * B - 1, 0))).sum())
+        px = int((np.minimum(cfg.b, h - by * cfg.b) * np.minimum(cfg.b, h - bx * cfg.b)).sum())
+        ring = int(((np.minimum(by * cfg.b + cfg.b + 1, h) - np.maximum(by * cfg.b - 1, 0)) *
+                    (np.minimum(bx * cfg.b + cfg.b + 1, h) - np.maximum(bx * cfg.b - 1, 0))).sum())
         flops = 2 * px * 2 * 9 * c * c
         gn_bytes = px * c * 2 + ring * c * 4  # stats read + activation read/write (ring incl.)
         out.append({"level": l, "shape": [n, h, h, c], "active_blocks": nb, "real_px": px,
                     "block_ms": round(t_block, 5), "block_tflops": round(flops / (t_block * 1e-3) / 1e12, 2),
                     "gn_silu_ms": round(t_gn, 5), "gn_silu_gbs": round(gn_bytes / (t_gn * 1e-3) / 1e9, 1),
-                    "conv_ms": round(t_conv, 5),
-                    "gn_share_of_block": round(2 * t_gn / t_block, 4)})
+                    "conv_ms": round(t_conv, 5), "gn_share_of_block": round(2 * t_gn / t_block, 4)})
     return {"levels": out, "timing": "CUDA-graph replay of 20 blocks, L2-warm; block = 6 launches "
             "(gn_block_stats, gn_silu, conv, gn_block_stats, gn_silu, conv+residual)",
             "block_tflops_note": "2 convs' algorithmic FLOPs (real active px) / whole-block time"}
 
 
-def temporal_levels(torch, st, req, reps=20):
+def temporal_levels(torch, st, reps=20):
     """NEXT-4: the temporal-attention block with the K/V latent cache at each UNet level over the
     step's active list (T = 21 frames = one request), after a full step (every block) filled the
     persistent q|k|v cache and y.  Graph-replay device time (L2-warm) and its parts."""
-    sp, d, dev = st.sp, st.d, st.dev
+    sp, d, dev, cfg = st.ops, st.d, st.dev, st.cfg
     out = []
-    for l, (h, c) in enumerate(LEVELS):
-        n, hb = N_FRAMES, st.dims[l][1]
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
+    for l, (h, c) in enumerate(cfg.levels):
+        n, hb = cfg.n_frames, cfg.hb[l]
         heads = c // syn.ATTN_HEAD_DIM
         x = d[f"feat{l}"]
-        bf = st.bf
         wq = bf(syn.linear_weights_bf16(3 * c, c, f"tq{l}", 0.5))
         wo = bf(syn.linear_weights_bf16(c, c, f"to{l}"))
         bq = torch.from_numpy(syn.bias_f32(3 * c, f"tq{l}")).to(dev)
@@ -476,22 +438,25 @@ def temporal_levels(torch, st, req, reps=20):
         ids, cnt = st.ids[l], st.cnt[l]
 
         def block(i=ids, k=cnt):
-            sp.sphinx_temporal_block(x, wq, bq, wo, bo, heads, N_FRAMES, qkv, o, y, B, i, k)
+            sp.sphinx_temporal_block(x, wq, bq, wo, bo, heads, cfg.frames_per_request, qkv, o, y, cfg.b, i, k)
         block(all_ids, all_cnt)  # the full step: every token's q|k|v cached, y filled
         t_block = graph_time(torch, block, reps)
-        t_qkv = graph_time(torch, lambda: sp.sphinx_sparse_pointwise(x, wq, bq, qkv, B, ids, cnt), reps)
-        t_att = graph_time(torch, lambda: sp.sphinx_temporal_attention(qkv, o, heads, N_FRAMES, B, ids, cnt), reps)
+        t_qkv = graph_time(torch, lambda: sp.sphinx_sparse_pointwise(x, wq, bq, qkv, cfg.b, ids, cnt), reps)
+        t_att = graph_time(torch, lambda: sp.sphinx_temporal_attention(qkv, o, heads, cfg.frames_per_request, cfg.b,
+                                                                       ids, cnt), reps)
         nb = int(cnt.item())
         idn = ids[:nb].cpu().numpy()
         pos = idn % (hb * hb)
         by, bx = pos // hb, pos % hb
-        px = int((np.minimum(B, h - by * B) * np.minimum(B, h - bx * B)).sum())
-        upos = np.unique(pos)
-        upx = int((np.minimum(B, h - (upos // hb) * B) * np.minimum(B, h - (upos % hb) * B)).sum())
+        px = int((np.minimum(cfg.b, h - by * cfg.b) * np.minimum(cfg.b, h - bx * cfg.b)).sum())
+        seq_pos = np.unique((idn // (hb * hb)) // cfg.frames_per_request * (hb * hb) + pos)
+        sp_pos = seq_pos % (hb * hb)
+        upx = int((np.minimum(cfg.b, h - (sp_pos // hb) * cfg.b) * np.minimum(cfg.b, h - (sp_pos % hb) * cfg.b)).sum())
+        T = cfg.frames_per_request
         proj_flops = px * 2 * (3 * c * c + c * c)
-        attn_flops = px * 4 * N_FRAMES * c
-        staged = upx * N_FRAMES * 3 * c * 2
-        out.append({"level": l, "shape": [n, h, h, c], "heads": heads, "frames_per_seq": N_FRAMES,
+        attn_flops = px * 4 * T * c
+        staged = upx * T * 3 * c * 2
+        out.append({"level": l, "shape": [n, h, h, c], "heads": heads, "frames_per_seq": T,
                     "active_blocks": nb, "real_px": px, "block_ms": round(t_block, 5),
                     "block_tflops": round((proj_flops + attn_flops) / (t_block * 1e-3) / 1e12, 2),
                     "qkv_proj_ms": round(t_qkv, 5),
@@ -501,210 +466,285 @@ def temporal_levels(torch, st, req, reps=20):
     return {"levels": out, "timing": "CUDA-graph replay of 20 blocks, L2-warm; block = qkv pointwise "
             "(tcgen05) + plan + attention + output pointwise with residual",
             "flops_note": "projections 8 C^2 + attention 4 T C FLOP per listed token",
-            "attention_bytes_note": "staged token bytes: T x 3C x 2 B per pixel position with any listed frame"}
+            "attention_bytes_note": "staged token bytes: T x 3C x 2 B per (sequence, pixel) with any listed frame"}
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms_all):
+    cfg = st.cfg
+    per_level = []
+    for l, (h, c) in enumerate(cfg.levels):
+        t_l = statistics.mean([statistics.mean(conv_ms[l][j]) for j in range(CONVS_PER_LEVEL)])
+        f_l = px_l[l] * 2 * 9 * c * c
+        per_level.append({"level": l, "shape": [cfg.n_frames, h, h, c], "active_blocks": blocks_l[l],
+                          "real_px": px_l[l], "density": round(blocks_l[l] / (cfg.n_frames * cfg.hb[l] ** 2), 4),
+                          "conv_ms": round(t_l, 5),
+                          "conv_ms_each": [round(statistics.mean(conv_ms[l][j]), 5) for j in range(CONVS_PER_LEVEL)],
+                          "tflops": round(f_l / (t_l * 1e-3) / 1e12, 2),
+                          "frac_burst": round(f_l / (t_l * 1e-3) / 1e12 / tc_peak, 4)})
+    conv_total_ms = sum(p["conv_ms"] for p in per_level) * CONVS_PER_LEVEL
+    dom = max(per_level, key=lambda p: p["conv_ms"])
+    dom_flops = dom["real_px"] * 2 * 9 * cfg.levels[dom["level"]][1] ** 2
+    achieved = dom_flops / (dom["conv_ms"] * 1e-3) / 1e12
+    bn = 256 if cfg.levels[dom["level"]][1] % 256 == 0 and cfg.levels[dom["level"]][1] > 640 else 160
+    edge = 1 if cfg.levels[dom["level"]][0] % cfg.b else 0
+    sig = f"<{bn}, 2, 8, 1, {edge}, 0>"
+    traffic, traffic_src = ncu_traffic(sig)
+    flops = sum(p["real_px"] * 2 * 9 * c * c for p, (_, c) in zip(per_level, cfg.levels)) * CONVS_PER_LEVEL
+    roof = {"bound": "tensor", "kernel": "sparse_conv3x3_tc_kernel%s (level %d)" % (sig, dom["level"]),
+            "achieved": round(achieved, 2), "peak": tc_peak, "unit": "TFLOP/s",
+            "frac": round(achieved / tc_peak, 4), "peak_kind": "measured bf16 burst (MEASURED_PEAKS.json)",
+            "frac_sustained": round(achieved / tc_sust, 4) if tc_sust else None,
+            "traffic": traffic, "traffic_unit": "bytes per launch (dram read+write)", "traffic_source": traffic_src,
+            "all_convs_tflops": round(flops / (conv_total_ms * 1e-3) / 1e12, 2),
+            "conv_share_of_step": round(conv_total_ms / ms_all, 4)}
+    return per_level, roof
+
+
+def single_rank_workload(torch, sp, name, dev, flush, args, tc_peak, tc_sust, with_dense=False):
+    """A secondary workload at N = 1 (configs[2] or configs[4]): graph-replayed step, cold L2."""
+    from paper_2511_18672_b200.step import RefinementStep
+    cfg = step_config(WORKLOADS[name]["means"])
+    st = RefinementStep(cfg, make_batch(name), dev, sp)
+    g, _ = capture_step(torch, st, False)
+    g_ev, conv_ev = capture_step(torch, st, True)
+    for _ in range(3):
+        g.replay()
+    reps = max(3, min(args.steps, 10))
+    ms = timed_steps(torch, g.replay, reps, flush, args, 1)
+    conv_ms = [[[] for _ in range(CONVS_PER_LEVEL)] for _ in range(cfg.L)]
+    timed_steps(torch, g_ev.replay, reps, flush, args, 1, conv_ev, conv_ms)
+    flops, px_l, blocks_l = st.active_stats()
+    step_ms = statistics.mean(ms)
+    per_level, roof = conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, step_ms)
+    out = {"workload": WORKLOADS[name]["desc"], "frames": cfg.n_frames, "ms_per_step": round(step_ms, 5),
+           "value_tflops": round(flops / (step_ms * 1e-3) / 1e12, 3), "conv_levels": per_level,
+           "roofline": roof}
+    if with_dense:
+        dense = dense_step(torch, st, flush, reps)
+        out["dense_step"] = dict(dense, speedup_of_step=round(dense["ms"] / step_ms, 3))
+    del st, g, g_ev
+    torch.cuda.empty_cache()
+    return out
+
+
+def warm_cold_conv(torch, st, flush, reps=10):
+    """One conv per level on the step's lists, timed alone: warm (back-to-back graph replays,
+    weights and features L2-resident) vs cold (256 MB L2 flush before each launch)."""
+    out = []
+    d, cfg, sp = st.d, st.cfg, st.ops
+    for l, (h, c) in enumerate(cfg.levels):
+        def fn():
+            sp.sphinx_sparse_conv3x3(d[f"feat{l}"], d[f"w{l}0"], d[f"b{l}0"], st.y[l], cfg.b, st.ids[l], st.cnt[l],
+                                     workspace=st.ws[l], reuse_plan=False)
+        warm = graph_time(torch, fn)
+        ts = []
+        for i in range(reps + 2):
+            flush.fill_(0.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(e0.elapsed_time(e1))
+        out.append({"level": l, "warm_ms": round(warm, 5), "cold_ms": round(statistics.median(ts), 5)})
+    return out
+
+
+def nccl_summary():
+    """What NCCL's INIT log (NCCL_DEBUG=INFO -> NCCL_DEBUG_FILE) says on this rank."""
+    import glob
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    if not path:
+        return None
+    files = sorted(glob.glob(path.replace("%h", "*").replace("%p", str(os.getpid()))))
+    lines = []
+    for f in files:
+        try:
+            lines += open(f).read().splitlines()
+        except OSError:
+            pass
+    pick = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines
+            if "NCCL INFO" in ln and any(k in ln for k in ("NCCL version", "nRanks", "NVLS", "P2P", "Channel 00", "CollNet"))]
+    return {"lines": pick[:12], "nvls": any("NVLS" in ln and "enabled" in ln.lower() for ln in lines),
+            "log": path}
 
 
 def run_gpu(args):
     import torch
     import torch.distributed as dist
+    import paper_2511_18672_b200 as sp
+    from paper_2511_18672_b200 import dist as sdist
+    from paper_2511_18672_b200.step import RefinementStep
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    req = make_request(f"r{rank}")
-    st = GpuStep(req, dev)
-    torch.cuda.synchronize()
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    sp.load()
     hbm, tc_peak, tc_sust, peak_kind = peaks()
-
+    name = args.workload
+    cfg = step_config(WORKLOADS[name]["means"])
+    batch = make_batch(name)
+    st = RefinementStep(cfg, batch, dev, sp, group=group, rank=rank, world=world)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
-    # The step is timed on an event-free graph (event nodes would break the PDL chain between
-    # kernels); a second graph with external event nodes around each conv gives the per-conv
-    # device times used for the roofline.
-    g, _ = capture_step(torch, st, with_conv_events=False)
-    try:
+    L = cfg.L
+    if world == 1:
+        # the step is timed on an event-free graph (event nodes would break the PDL chain between
+        # kernels); a second graph with external event nodes around each conv gives per-conv times
+        g, _ = capture_step(torch, st, with_conv_events=False)
         g_ev, conv_ev = capture_step(torch, st, with_conv_events=True)
-        graph_note = ("CUDA graph replay (event-free graph for the step; conv launches timed by "
-                      "captured external events in a second graph)")
-    except Exception as e:  # event nodes unsupported: time the convs outside the graph
-        g_ev, conv_ev = None, None
-        graph_note = f"CUDA graph replay; conv events unsupported in capture ({type(e).__name__})"
+        run_step, run_ev = g.replay, g_ev.replay
+        timing_note = ("CUDA graph replay (event-free graph for the step; conv launches timed by captured external "
+                       "events in a second graph)")
+    else:
+        conv_ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+                    for _ in range(CONVS_PER_LEVEL)] for _ in range(L)]
+        run_step, run_ev = st.run, (lambda: st.run(conv_ev))
+        timing_note = ("eager launches (the host LPT plan between the mask all-gather and the compaction makes "
+                       "one D2H sync per step); per-conv CUDA events on the compute stream")
     for _ in range(max(args.warmup, 3)):
-        g.replay()
+        run_step()
         flush.fill_(1.0)
     torch.cuda.synchronize()
     flops, px_l, blocks_l = st.active_stats()
-    step_ms, conv_ms = [], [[[] for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
     stop = threading.Event()
     clk_lines = []
     th = threading.Thread(target=sample_clocks, args=(stop, clk_lines, local), daemon=True)
     th.start()
     time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     reps = max(1, args.steps)
-    for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g.replay()
-        e1.record()
-        if not args.no_flush:
-            flush.fill_(1.0)  # L2 flush between timed steps (outside the e0..e1 window)
-        torch.cuda.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    # per-conv device times (same cold-L2 protocol), then a sustained stretch for the clocks
-    for _ in range(reps):
-        if g_ev is not None:
-            g_ev.replay()
-            torch.cuda.synchronize()
-            for l in range(3):
-                for j in range(CONVS_PER_LEVEL):
-                    conv_ms[l][j].append(conv_ev[l][j][0].elapsed_time(conv_ev[l][j][1]))
-        if not args.no_flush:
-            flush.fill_(1.0)
+    t_wall0 = time.time()
+    step_ms = timed_steps(torch, run_step, reps, flush, args, world)
+    wall_s = time.time() - t_wall0
+    conv_ms = [[[] for _ in range(CONVS_PER_LEVEL)] for _ in range(L)]
+    timed_steps(torch, run_ev, reps, flush, args, world, conv_ev, conv_ms)
     t_end = time.time() + 1.0
-    while time.time() < t_end:
-        g.replay()
+    while time.time() < t_end:  # a sustained stretch for the clock samples
+        run_step()
         torch.cuda.synchronize()
     stop.set()
     th.join(timeout=3)
-    if g_ev is None:  # eager fallback for per-conv timing
-        ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-               for _ in range(CONVS_PER_LEVEL)] for _ in range(3)]
-        for _ in range(reps):
-            st.run(ev)
-            torch.cuda.synchronize()
-            for l in range(3):
-                for j in range(CONVS_PER_LEVEL):
-                    conv_ms[l][j].append(ev[l][j][0].elapsed_time(ev[l][j][1]))
     ms = statistics.mean(step_ms)
-    if world > 1:  # whole-job throughput: sum of the work / max over ranks of the step time
-        from paper_2511_18672_b200 import dist as sdist
-        ms_all, flops_all = sdist.reduce_step(ms, flops, device=dev)
+    multi = None
+    if world > 1:
+        # whole-job throughput: the batch's work / max over ranks of the step time
+        ms_all, _ = sdist.reduce_step(ms, 0.0, device=dev)
+        ms_min = -sdist.reduce_step(-ms, 0.0, device=dev)[0]
+        sent = torch.tensor([float(st.bytes_sent)], dtype=torch.float64, device=dev)
+        dist.all_reduce(sent)
+        p = st.plan
+        multi = {"ranks": world, "partition": "LPT over frames by executed MMA work (sum_l count*C_l^2) at u",
+                 "plan_imbalance_max_over_mean": round(p["imbalance"], 4),
+                 "step_ms_max": round(ms_all, 5), "step_ms_min": round(ms_min, 5),
+                 "bytes_moved_per_step": int(sent.item()),
+                 "owner": "request j -> rank j*N//R", "nccl": nccl_summary() if rank == 0 else None}
     else:
-        ms_all, flops_all = ms, float(flops)
-    value = flops_all / (ms_all * 1e-3) / 1e12
+        ms_all = ms
+    value = flops / (ms_all * 1e-3) / 1e12
+    per_level, roof = conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms)
 
-    per_level = []
-    for l, (h, c) in enumerate(LEVELS):
-        t_l = statistics.mean([statistics.mean(conv_ms[l][j]) for j in range(CONVS_PER_LEVEL)])
-        f_l = px_l[l] * 2 * 9 * c * c
-        per_level.append({"level": l, "shape": [N_FRAMES, h, h, c], "active_blocks": blocks_l[l],
-                          "real_px": px_l[l], "conv_ms": round(t_l, 5),
-                          "conv_ms_each": [round(statistics.mean(conv_ms[l][j]), 5) for j in range(CONVS_PER_LEVEL)],
-                          "tflops": round(f_l / (t_l * 1e-3) / 1e12, 2)})
-    conv_total_ms = sum(p["conv_ms"] for p in per_level) * CONVS_PER_LEVEL
-    # dominant kernel = the conv launch family with the largest share of the step
-    dom = max(per_level, key=lambda p: p["conv_ms"])
-    dom_flops = dom["real_px"] * 2 * 9 * LEVELS[dom["level"]][1] ** 2
-    achieved = dom_flops / (dom["conv_ms"] * 1e-3) / 1e12
-    all_conv_tflops = flops / (conv_total_ms * 1e-3) / 1e12
-    bn_sig = {0: "<160, 2, 8, 1, 0, 0>", 1: "<160, 2, 8, 1, 1, 0>", 2: "<256, 2, 8, 1, 1, 0>"}[dom["level"]]
-    traffic, traffic_src = ncu_traffic(bn_sig)
-
-    # the same conv calls timed in isolation (graph of 20 back-to-back launches, L2-warm)
-    iso = []
-    for l in range(3):
-        d = st.d
-        iso.append(round(graph_time(torch, lambda: st.sp.sphinx_sparse_conv3x3(
-            d[f"feat{l}"], d[f"w{l}0"], d[f"b{l}0"], st.y[l], B, st.ids[l], st.cnt[l])), 5))
-    dense = dense_step(torch, st, flush, reps) if rank == 0 else None
-    e2e = None if args.no_e2e else run_e2e(torch, st, g, req, dev, args, flops)
-    sweep = None
-    if rank == 0 and not args.no_sweep:
-        sweep = density_sweep(torch, st.sp, dev)
-    mem = memory_kernels(torch, st, req) if rank == 0 else None
-    rblk = resblock_levels(torch, st, req) if (rank == 0 and not args.no_resblock) else None
-    tblk = temporal_levels(torch, st, req) if (rank == 0 and not args.no_resblock) else None
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras["conv_warm_cold"] = warm_cold_conv(torch, st, flush)
+        extras["e2e"] = run_e2e(torch, st, g, batch, dev, args, flops)
+        extras["memory_kernels"] = memory_kernels(torch, st)
+        extras["configs2"] = single_rank_workload(torch, sp, "configs2", dev, flush, args, tc_peak, tc_sust)
+        del g, g_ev
+        torch.cuda.empty_cache()
+        extras["configs4"] = single_rank_workload(torch, sp, "configs4", dev, flush, args, tc_peak, tc_sust,
+                                                  with_dense=True)
+        if not args.no_resblock:
+            st2 = RefinementStep(step_config(WORKLOADS["configs2"]["means"]), make_batch("configs2"), dev, sp)
+            st2.run()
+            torch.cuda.synchronize()
+            extras["resblock (NEXT-3)"] = resblock_levels(torch, st2)
+            extras["temporal_attention (NEXT-4)"] = temporal_levels(torch, st2)
+            del st2
+        if not args.no_sweep:
+            extras["density_sweep"] = density_sweep(torch, sp, dev)
 
     if rank == 0:
-        cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(req, bounded_s=args.cpu_seconds)
+        cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(batch, cfg, bounded_s=args.cpu_seconds)
         line = {
-            "metric": "block-sparse conv effective TFLOP/s & speedup vs dense at 10/25/50% density",
-            "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": reps,
+            "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": reps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_all, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "configs[2]: 21-frame request, 3 UNet levels (72x72x320, 36x36x640, "
-                                   "18x18x1280), per-frame adaptive start steps, mean level-0 density 25%; "
-                                   "one request per rank at N>1 (weak scaling)",
-                       "frames_per_rank": N_FRAMES, "image": [HP, HP], "block": B, "u": U_STEP,
-                       "convs_per_level": CONVS_PER_LEVEL, "active_blocks_per_level": blocks_l,
-                       "density_per_level": [round(blocks_l[l] / (N_FRAMES * st.dims[l][1] ** 2), 4)
-                                             for l in range(3)],
+            "scaling": "strong" if name != "configs2" else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": WORKLOADS[name]["desc"], "frames": cfg.n_frames, "requests": cfg.n_requests,
+                       "image": [HP, HP], "block": B, "u": U_STEP, "convs_per_level": CONVS_PER_LEVEL,
+                       "active_blocks_per_level": blocks_l,
+                       "density_per_level": [round(blocks_l[l] / (cfg.n_frames * cfg.hb[l] ** 2), 4) for l in range(L)],
                        "l2": ("NOT flushed (diagnostic --no-flush)" if args.no_flush else
-                              "flushed between timed steps (256 MB write)"), "timing": graph_note,
-                       "parallelism": f"dp{world}"},
-            "gpu_launches": st.launches_per_step * reps,
-            "roofline": {"bound": "tensor", "kernel": "sparse_conv3x3_tc_kernel (level %d)" % dom["level"],
-                         "achieved": round(achieved, 2), "peak": tc_peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / tc_peak, 4), "peak_kind": f"{peak_kind} bf16 burst",
-                         "frac_sustained": round(achieved / tc_sust, 4) if tc_sust else None,
-                         "traffic": traffic, "traffic_unit": "bytes per launch (dram read+write)",
-                         "traffic_source": traffic_src, "all_convs_tflops": round(all_conv_tflops, 2),
-                         "conv_share_of_step": round(conv_total_ms / ms_all, 4)},
+                              "flushed between timed steps (256 MB write)"), "timing": timing_note,
+                       "parallelism": f"dp{world} (frame sharding)"},
+            "gpu_launches": (st.launches_per_step * reps if world == 1 else None),
+            "roofline": roof,
             "conv_levels": per_level,
-            "conv_isolated_ms": iso,
-            "dense_step": (dict(dense, speedup_of_step=round(dense["ms"] / ms_all, 3)) if dense else None),
-            "memory_kernels": mem,
-            "resblock (NEXT-3)": rblk,
-            "temporal_attention (NEXT-4)": tblk,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "density_sweep": sweep,
-            "paper_context": "1.8x average end-to-end speedup vs diffusion-only on 4x A40 (P:34, P:445); "
-                             "context only, not this metric",
+            "multi_gpu": multi,
+            "wall_s_timed_steps": round(wall_s, 4),
+            "paper_context": "1.8x average end-to-end speedup vs diffusion-only on 4x A40 (P:34, P:445); context "
+                             "only, not this metric",
             "clocks": summarize_clocks(clk_lines),
         }
+        if world > 1:
+            line["gpu_launches"] = None
+            line["gpu_launches_note"] = "eager multi-rank step: per rank ~%d sphinx kernels + NCCL" % (
+                st.launches_per_step + 4 * L)
+        line.update(extras)
+        line["e2e"] = extras.get("e2e")
+        line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def run_profile():
+def run_profile(args):
     """Minimal run for ncu: the captured step graph replayed twice; only the step's kernels
     (and the graph-capture warm-up's) appear in the launch list."""
     import torch
+    import paper_2511_18672_b200 as sp
+    from paper_2511_18672_b200.step import RefinementStep
     torch.cuda.set_device(0)
-    st = GpuStep(make_request("r0"), torch.device("cuda", 0))
+    cfg = step_config(WORKLOADS[args.workload]["means"])
+    st = RefinementStep(cfg, make_batch(args.workload), torch.device("cuda", 0), sp)
     g, _ = capture_step(torch, st, with_conv_events=False)
     torch.cuda.synchronize()
     for _ in range(2):
         g.replay()
     torch.cuda.synchronize()
-    print(json.dumps({"profile": "done", "launches_per_step": st.launches_per_step}))
+    print(json.dumps({"profile": "done", "workload": args.workload, "launches_per_step": st.launches_per_step}))
 
 
-def run_e2e(torch, st, g, req, dev, args, flops):
+def run_e2e(torch, st, g, batch, dev, args, flops):
     """Same step through the public API with HOST buffers: every step copies its inputs from
-    pinned host memory (H2D) and reads its outputs back (D2H), all inside the timed region."""
-    in_keys = ["O", "U", "tau_u", "q", "c0", "c1", "t", "x0", "eps", "lid", "lat_cache", "feat0", "feat1",
-               "feat2"]
-    host = {k: torch.from_numpy(np.ascontiguousarray(req[k].view(np.int16) if req[k].dtype == np.uint16
-                                                     else req[k])).pin_memory() for k in in_keys}
-    # the step's result is the refined latent (a6's output); the feature maps are intermediates of
-    # the UNet levels and stay on the device for the next layer
-    outs = [st.lat_out]
-    out_host = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
+    pinned host memory (H2D) and reads its result back (D2H), all inside the timed region."""
+    from paper_2511_18672_b200.step import RefinementStep
+    in_keys = ["O", "U", "tau_u", "q", "c0", "c1", "t", "x0", "eps", "lid", "lat_cache"] + \
+              [f"feat{l}" for l in range(st.cfg.L)]
+    host = {k: torch.from_numpy(np.ascontiguousarray(batch[k].view(np.int16) if batch[k].dtype == np.uint16
+                                                     else batch[k])).pin_memory() for k in in_keys}
+    out_host = torch.empty(st.lat_out.shape, dtype=st.lat_out.dtype).pin_memory()
     h2d = sum(h.numel() * h.element_size() for h in host.values())
-    d2h = sum(o.numel() * o.element_size() for o in out_host)
+    d2h = out_host.numel() * out_host.element_size()
+
+    def copy_in(s_):
+        for k, h in host.items():
+            dst = s_.d[k]
+            (dst.view(torch.int16) if dst.dtype == torch.bfloat16 else dst).copy_(h, non_blocking=True)
 
     def step():
-        for k, h in host.items():
-            dst = st.d[k]
-            if dst.dtype == torch.bfloat16:
-                dst.view(torch.int16).copy_(h, non_blocking=True)
-            else:
-                dst.copy_(h, non_blocking=True)
+        copy_in(st)
         g.replay()
-        for o, oh in zip(outs, out_host):
-            oh.copy_(o, non_blocking=True)
+        out_host.copy_(st.lat_out, non_blocking=True)
 
     for _ in range(2):
         step()
@@ -718,16 +758,16 @@ def run_e2e(torch, st, g, req, dev, args, flops):
     torch.cuda.synchronize()
     ms_serial = e0.elapsed_time(e1) / reps
 
-    # serving loop: two input/output sets (a second GpuStep over the same model state and its own
-    # graph); step j's H2D runs on a copy stream while step j-1 computes, the result D2H on a third
-    # stream (PCIe is full duplex).  Every step still copies all its inputs and reads its result.
-    st2 = GpuStep(req, dev)
+    # serving loop: two input/output sets (a second step over the same model state, its own
+    # graph); step j's H2D runs on a copy stream while step j-1 computes, the result D2H on a
+    # third stream (PCIe is full duplex).  Every step still copies all its inputs and reads its result.
+    st2 = RefinementStep(st.cfg, batch, dev, st.ops)
     g2, _ = capture_step(torch, st2, with_conv_events=False)
-    sets = [(st, g, out_host[0]), (st2, g2, torch.empty_like(out_host[0]).pin_memory())]
+    sets = [(st, g, out_host), (st2, g2, torch.empty_like(out_host).pin_memory())]
     main = torch.cuda.current_stream()
     cs, ds = torch.cuda.Stream(), torch.cuda.Stream()
-    freed = [torch.cuda.Event(), torch.cuda.Event()]    # set's compute done: inputs may be overwritten
-    read = [torch.cuda.Event(), torch.cuda.Event()]     # set's result read back: outputs may be rewritten
+    freed = [torch.cuda.Event(), torch.cuda.Event()]
+    read = [torch.cuda.Event(), torch.cuda.Event()]
     start = torch.cuda.Event()
 
     def pipelined(n):
@@ -737,9 +777,7 @@ def run_e2e(torch, st, g, req, dev, args, flops):
             s_, g_, oh = sets[j % 2]
             cs.wait_event(freed[j % 2])
             with torch.cuda.stream(cs):
-                for k, h in host.items():
-                    dst = s_.d[k]
-                    (dst.view(torch.int16) if dst.dtype == torch.bfloat16 else dst).copy_(h, non_blocking=True)
+                copy_in(s_)
             landed = torch.cuda.Event()
             landed.record(cs)
             main.wait_event(landed)
@@ -765,86 +803,106 @@ def run_e2e(torch, st, g, req, dev, args, flops):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps_timed": n_pipe, "serial_ms_per_step": round(ms_serial, 4),
             "h2d_gbs": round(h2d / (ms * 1e-3) / 1e9, 1),
-            "note": "serving loop, two input sets: step j's H2D (copy stream) overlaps step j-1's compute, "
-                    "the result D2H on a third stream; serial_ms_per_step = copy, compute, read back one after "
-                    "the other.  Conv weights resident on device (model state); per-step opacity/uncertainty "
-                    "maps, level input features and latents H2D; the refined latent (the step's result) D2H"}
+            "note": "serving loop, two input sets: step j's H2D (copy stream) overlaps step j-1's compute, the "
+                    "result D2H on a third stream; serial_ms_per_step = copy, compute, read back one after the "
+                    "other.  Conv weights resident (model state); per-step opacity/uncertainty maps, level input "
+                    "features and latents H2D; the refined latent (the step's result) D2H"}
 
 
 # ----------------------------------------------------------------- CPU oracle arm
 
-def oracle_step_sample(req, max_blocks_per_level):
-    """The same step on the CPU oracle, bounded: masks/start steps/compaction/noise on the
-    whole request, convs on the first max_blocks_per_level active blocks of each level.
-    Returns (seconds, conv FLOPs computed, description)."""
+def oracle_step_sample(batch, cfg, max_blocks_per_level):
+    """The same step on the CPU oracle, bounded: masks/start steps/compaction/noise/scatter on
+    the whole batch, one conv per level on the first max_blocks_per_level active blocks.
+    Returns (seconds, conv FLOPs computed)."""
     import oracle
     t0 = time.perf_counter()
-    lg = oracle.make_klogic(syn.SPEC_KLOGIC["thr"], syn.SPEC_KLOGIC["steps"])
-    masks, counts = oracle.block_mask(req["O"], req["U"], req["tau_u"], 0.5, F, B, 3)
-    k = oracle.start_step(req["q"], req["c0"], req["c1"], req["t"], GAMMA, [lg], logic_id=req["lid"])
-    ids = [oracle.compact(masks[l], k, U_STEP) for l in range(3)]
-    inact = oracle.compact(None, k, U_STEP, oracle.SELECT_INACTIVE_FRAMES, shape=masks[0].shape)
-    z = oracle.noise(req["x0"], req["eps"], req["x0"], B, ids[0], k, req["abar"])
-    z = oracle.noise(req["x0"], req["eps"], z.astype(np.float32), B, inact,
-                     np.full(N_FRAMES, U_STEP + 1, np.int32), req["abar"])
-    oracle.scatter(z.astype(np.float32), req["lat_cache"], B, mask=masks[0], k=k, u=U_STEP)
+    kl = batch["klogic"]
+    lg = oracle.make_klogic(kl["thr"], kl["steps"], kl["fallback_k"], kl["k_max"])
+    masks, counts = oracle.block_mask(batch["O"], batch["U"], batch["tau_u"], cfg.tau_o, cfg.f, cfg.b, cfg.L)
+    k = oracle.start_step(batch["q"], batch["c0"], batch["c1"], batch["t"], cfg.gamma, [lg], logic_id=batch["lid"])
+    ids = [oracle.compact(masks[l], k, cfg.u) for l in range(cfg.L)]
+    inact = oracle.compact(None, k, cfg.u, oracle.SELECT_INACTIVE_FRAMES, shape=masks[0].shape)
+    z = oracle.noise(batch["x0"], batch["eps"], batch["x0"], cfg.b, ids[0], k, batch["abar"])
+    z = oracle.noise(batch["x0"], batch["eps"], z.astype(np.float32), cfg.b, inact,
+                     np.full(cfg.n_frames, cfg.u + 1, np.int32), batch["abar"])
+    oracle.scatter(z.astype(np.float32), batch["lat_cache"], cfg.b, mask=masks[0], k=k, u=cfg.u)
     flops = 0
-    for l, (h, c) in enumerate(LEVELS):
+    for l, (h, c) in enumerate(cfg.levels):
         sub = ids[l][:max_blocks_per_level]
-        y, _ = oracle.conv3x3_blocks(req[f"feat{l}"], req[f"w{l}0"], req[f"b{l}0"], B, sub, n_threads=0)
-        hb = -(-h // B)
-        r = sub % (hb * hb)
-        px = int((np.minimum(B, h - (r // hb) * B) * np.minimum(B, h - (r % hb) * B)).sum())
-        flops += px * 2 * 9 * c * c
+        oracle.conv3x3_blocks(batch[f"feat{l}"], batch[f"w{l}0"], batch[f"b{l}0"], cfg.b, sub, n_threads=0)
+        flops += cfg.real_px(l, sub) * 2 * 9 * c * c
     return time.perf_counter() - t0, flops
 
 
-def calibrate_blocks(req, seconds):
+def calibrate_blocks(batch, cfg, seconds):
     """Blocks per level so that one oracle step sample takes about `seconds`."""
-    t1, _ = oracle_step_sample(req, 1)
-    t3, _ = oracle_step_sample(req, 3)
+    t1, _ = oracle_step_sample(batch, cfg, 1)
+    t3, _ = oracle_step_sample(batch, cfg, 3)
     slope = max((t3 - t1) / 2, 1e-3)
     return int(max(1, min(4000, 1 + (seconds - t1) / slope)))
 
 
-def cpu_baseline(req, bounded_s=15.0):
+def cpu_baseline(batch, cfg, bounded_s=15.0):
     cores = os.cpu_count()
-    nb = calibrate_blocks(req, bounded_s)
-    t, f = oracle_step_sample(req, nb)
+    nb = calibrate_blocks(batch, cfg, bounded_s)
+    t, f = oracle_step_sample(batch, cfg, nb)
     return {"value": round(f / t / 1e12, 8), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
             "seconds": round(t, 2),
-            "sample": f"one configs[2] request: full mask/start-step/compaction/noise/scatter, one conv on the "
-                      f"first {nb} active blocks of each level (fp64 direct conv, OpenMP {cores} threads)"}
+            "sample": f"the {cfg.n_frames}-frame batch: full mask/start-step/compaction/noise/scatter, one conv on "
+                      f"the first {nb} active blocks of each level (fp64 direct conv, OpenMP {cores} threads)"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    req = make_request("r0")
+    name = args.workload
+    cfg = step_config(WORKLOADS[name]["means"])
+    batch = make_batch(name)
     cores = os.cpu_count()
-    nb = calibrate_blocks(req, 150.0 / max(1, args.steps + args.warmup))
+    nb = calibrate_blocks(batch, cfg, 150.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        oracle_step_sample(req, nb)
+        oracle_step_sample(batch, cfg, nb)
     ts, fl = [], 0
     for _ in range(args.steps):
-        t, f = oracle_step_sample(req, nb)
+        t, f = oracle_step_sample(batch, cfg, nb)
         ts.append(t)
         fl = f
     ms = statistics.mean(ts) * 1e3
     value = fl / (ms * 1e-3) / 1e12
-    sample = (f"bounded sample of configs[2]: full mask/start-step/compaction/noise/scatter, conv on the first "
-              f"{nb} active blocks per level")
+    sample = (f"bounded sample of {name}: full mask/start-step/compaction/noise/scatter over the {cfg.n_frames} "
+              f"frames, conv on the first {nb} active blocks per level")
     print(json.dumps({
-        "impl": "reference", "metric": "block-sparse conv effective TFLOP/s & speedup vs dense at 10/25/50% density",
-        "value": round(value, 8), "unit": "TFLOP/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "configs[2] (bounded oracle sample)", "frames_per_rank": N_FRAMES},
+        "impl": "reference", "metric": METRIC, "value": round(value, 8), "unit": "TFLOP/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[name]["desc"] + " (bounded oracle sample)", "frames": cfg.n_frames},
         "cpu_baseline": {"value": round(value, 8), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": round(value, 8), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: re-execute under torch.distributed.run, one
+    process per GPU on this node; rank 0 prints the JSON line."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    env.setdefault("NCCL_DEBUG_FILE", "/tmp/sphinx_nccl.%h.%p.log")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -853,8 +911,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="configs3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-extras", action="store_true", help="headline workload only")
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-resblock", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -865,8 +924,14 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     elif args.profile:
-        run_profile()
+        run_profile(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     else:
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/sphinx_nccl.%h.%p.log")
         run_gpu(args)
 
 

@@ -107,7 +107,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 7
+#define SPHINX_ABI_VERSION 8
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -294,6 +294,33 @@ SPHINX_API sphinx_status sphinx_scatter_cached(const void* src, sphinx_src_layou
                                     const uint8_t* block_mask, const int32_t* start_step,
                                     int32_t step_u, const int32_t* block_ids, const int32_t* count,
                                     sphinx_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
+ * Multi-GPU data plane: pack / unpack of listed blocks.  P:352 "batched
+ * convolution over selected blocks", "latent scatter-gather operations": refined blocks
+ * computed on one GPU travel to the GPU owning the frame's request as a COMPACT array in list
+ * order, then land at their NHWC positions.  Bit copies (NaN payloads, -0 preserved).
+ *
+ * sphinx_gather_blocks:  dst[j][py][px][:] = src[n, by*b+py, bx*b+px, :] for list entry j
+ *                        (id = (n*Hb+by)*Wb+bx), real pixels only; dst's padding pixels of
+ *                        truncated edge blocks are left untouched.
+ * sphinx_scatter_blocks: out[n, by*b+py, bx*b+px, :] = src[j][py][px][:] for list entry j, real
+ *                        pixels only; every other pixel of out is untouched.  The list may be in
+ *                        any order (e.g. several senders' segments concatenated); duplicate ids
+ *                        give an unspecified winner.
+ * src/dst/out  device, 16-byte aligned; NHWC [N][h][w][c] on the map side, [capacity][b][b][c]
+ *              on the compact side; dtype gives the element width; c * elem_size % 16 == 0
+ *              (else SPHINX_ERR_UNSUPPORTED); src must not alias dst/out.
+ * block_ids/count/capacity  device list (count <= capacity <= N*Hb*Wb; count read on device).
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_gather_blocks(const void* src, void* dst, sphinx_dtype dtype, int32_t n,
+                                              int32_t h, int32_t w, int32_t c, int32_t block,
+                                              const int32_t* block_ids, const int32_t* count,
+                                              int32_t capacity, sphinx_stream_t stream);
+SPHINX_API sphinx_status sphinx_scatter_blocks(const void* src, void* out, sphinx_dtype dtype, int32_t n,
+                                               int32_t h, int32_t w, int32_t c, int32_t block,
+                                               const int32_t* block_ids, const int32_t* count,
+                                               int32_t capacity, sphinx_stream_t stream);
 
 /* ---------------------------------------------------------------------------------
  * NEXT-1. Partial-step latent update (Alg1 line 18; deterministic DDIM, eta = 0):

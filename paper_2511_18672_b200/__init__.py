@@ -29,7 +29,7 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 7
+ABI_VERSION = 8
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
@@ -39,7 +39,8 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_sparse_pointwise", "sphinx_temporal_attention_workspace_size",
            "sphinx_temporal_attention", "sphinx_temporal_block", "sphinx_gn_scale_shift",
            "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex",
-           "sphinx_sparse_resblock_ex", "sphinx_temporal_attention_ex",
+           "sphinx_sparse_resblock_ex", "sphinx_temporal_attention_ex", "sphinx_gather_blocks",
+           "sphinx_scatter_blocks",
            "sphinx_conv_edge_plan")
 
 _lib = None
@@ -129,6 +130,8 @@ def load(path=SO_PATH):
         "sphinx_sparse_resblock_ex": ([P, P, P, P, P, P, P, P, P, I, F, P, P, P, P, I, P,
                                        I, I, I, I, I, P, P, I, P, Z, I, P], I),
         "sphinx_sparse_pointwise": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
+        "sphinx_gather_blocks": ([P, P, I, I, I, I, I, I, P, P, I, P], I),
+        "sphinx_scatter_blocks": ([P, P, I, I, I, I, I, I, P, P, I, P], I),
         "sphinx_gn_scale_shift": ([P, P, P, F, I, I, I, I, I, I, P, P], I),
         "sphinx_compact_blocks_batch": ([P, I, P], I),
         "sphinx_conv_edge_plan": ([P, P, I, I, I, I, I, P, Z, P], I),
@@ -349,6 +352,32 @@ def sphinx_conv_edge_plan(block_ids, count, n, h, w, block, c_out, capacity=None
     rc = load().sphinx_conv_edge_plan(_ptr(block_ids), _ptr(count), int(n), int(h), int(w), int(block), int(cap),
                                       _ptr(workspace), workspace.numel(), _stream(stream))
     _chk("sphinx_conv_edge_plan", rc)
+
+
+def _block_copy(fn, src, dst, block, block_ids, count, capacity, stream, map_side):
+    import torch
+    if src.dtype not in (torch.bfloat16, torch.float32) or dst.dtype != src.dtype:
+        raise ValueError("src/dst: same dtype, bf16 or fp32")
+    for t, nm in ((src, "src"), (dst, "dst")):
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError(f"{nm}: contiguous CUDA tensor")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, h, w, c = map_side.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = getattr(load(), fn)(_ptr(src), _ptr(dst), F32 if src.dtype == torch.float32 else BF16, n, h, w, c,
+                             int(block), _ptr(block_ids), _ptr(count), int(cap), _stream(stream))
+    _chk(fn, rc)
+
+
+def sphinx_gather_blocks(src, dst, block, block_ids, count, capacity=None, stream=None):
+    """Data plane pack: dst [cap,b,b,C] <- listed blocks of the NHWC map src [N,H,W,C]."""
+    _block_copy("sphinx_gather_blocks", src, dst, block, block_ids, count, capacity, stream, src)
+
+
+def sphinx_scatter_blocks(src, out, block, block_ids, count, capacity=None, stream=None):
+    """Data plane unpack: listed blocks of the NHWC map out [N,H,W,C] <- compact src [cap,b,b,C]."""
+    _block_copy("sphinx_scatter_blocks", src, out, block, block_ids, count, capacity, stream, out)
 
 
 def sphinx_scatter_cached(src, cache, out, block, block_mask=None, start_step=None, step_u=0,

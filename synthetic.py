@@ -28,11 +28,13 @@ def rng(*names):
 def to_bf16_bits(a):
     """float32 -> bf16 bit patterns (round to nearest even), as uint16."""
     a = np.ascontiguousarray(a, dtype=np.float32)
-    u = a.view(np.uint32).astype(np.uint64)
-    rounded = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
-    nan = np.isnan(a)
-    out = rounded.astype(np.uint16)
-    out[nan] = 0x7FC0
+    u = a.view(np.uint32)
+    r = (u >> 16) & 1                 # uint32 arithmetic: no finite value overflows 2^32
+    r += 0x7FFF
+    r += u
+    r >>= 16
+    out = r.astype(np.uint16)
+    out[np.isnan(a)] = 0x7FC0
     return out
 
 
@@ -126,8 +128,28 @@ def uncertainty_maps(n, hp, wp, cell_px, cells, frac_blobs=0.3, tag="uncert"):
 
 # ------------------------------------------------------------ tensors -------
 
+def _chunked_bf16_normal(shape, names, frames_per_chunk=8):
+    """N(0,1) -> bf16 bits for a large frame-major tensor: frame chunks drawn from independent
+    streams rng(*names, chunk) on a thread pool (numpy releases the GIL), same values whatever
+    the thread count."""
+    from concurrent.futures import ThreadPoolExecutor
+    out = np.empty(shape, np.uint16)
+    starts = list(range(0, shape[0], frames_per_chunk))
+
+    def one(i):
+        s0 = starts[i]
+        sub = (min(frames_per_chunk, shape[0] - s0),) + tuple(shape[1:])
+        out[s0:s0 + sub[0]] = to_bf16_bits(rng(*names, i).standard_normal(sub, dtype=np.float32))
+    with ThreadPoolExecutor(8) as ex:
+        list(ex.map(one, range(len(starts))))
+    return out
+
+
 def features_bf16(shape, tag):
-    """x ~ N(0,1) rounded to bf16 (bit patterns)."""
+    """x ~ N(0,1) rounded to bf16 (bit patterns).  Batches of more than one request (> 21
+    frames) are drawn in independent 8-frame chunks in parallel."""
+    if len(shape) == 4 and shape[0] > 21:
+        return _chunked_bf16_normal(shape, ("feat-chunk", tag, shape))
     return to_bf16_bits(rng("feat", tag, shape).standard_normal(shape, dtype=np.float32))
 
 
@@ -268,3 +290,52 @@ def sparse_pixel_maps(n, hp, wp, cell_px, n_px, tag="sparse-px"):
         else:
             U[i, y[2], x[2]] = np.nan
     return O, U, tau_u
+
+
+# ------------------------------------------------------------ request batches ---
+
+UNET_LEVELS = ((72, 320), (36, 640), (18, 1280))     # BASELINE configs[2]
+CONFIG3_REQUEST_DENSITIES = (0.05, 0.10, 0.25, 0.50, 0.75, 0.25, 0.10, 0.05)  # BASELINE configs[3]
+
+
+def make_batch(request_means, tag="r0", hp=576, f=8, b=8, levels=UNET_LEVELS, convs_per_level=2,
+               frames_per_request=21, pattern="clustered", c_lat=4, S=50, lo=None, hi=None):
+    """Host inputs of a batch of requests (DESIGN.md input recipe): per request, per-frame
+    level-0 densities U-shaped around the request's mean (request_densities), toy-disocclusion
+    opacity + uncertainty maps, U-shaped scores; frames 0 and n-1 of every request are its
+    conditioning inputs (logic_id -1, R-14); latents, level features, caches, conv weights.
+    With one request and tag 'r0' this is exactly the round-1 configs[2] request."""
+    n_req = len(request_means)
+    fpr = frames_per_request
+    one = n_req == 1
+    O, U, tau, q, c0, c1, t, lid = [], [], [], [], [], [], [], []
+    for r, mean in enumerate(request_means):
+        rt = tag if one else f"{tag}.{r}"
+        kw = {}
+        if lo is not None or not one:
+            kw["lo"] = lo if lo is not None else 1.0 / ((hp // f // b) ** 2)
+        if hi is not None or not one:
+            kw["hi"] = hi if hi is not None else 1.0
+        dens = request_densities(fpr, mean, **kw)
+        o, cells = opacity_maps(fpr, hp, hp, b * f, dens, pattern, tag=f"O{rt}")
+        uu, tu = uncertainty_maps(fpr, hp, hp, b * f, cells, tag=f"U{rt}")
+        qq, a0, a1, tt = request_scores(fpr, tag=f"q{rt}")
+        li = np.zeros(fpr, np.int32)
+        li[0] = li[-1] = -1
+        for lst, v in ((O, o), (U, uu), (tau, tu), (q, qq), (c0, a0), (c1, a1), (t, tt), (lid, li)):
+            lst.append(v)
+    cat = np.concatenate
+    F = n_req * fpr
+    h0 = hp // f
+    batch = dict(O=cat(O), U=cat(U), tau_u=cat(tau), q=cat(q), c0=cat(c0), c1=cat(c1), t=cat(t), lid=cat(lid),
+                 abar=abar_cosine(S), klogic=dict(SPEC_KLOGIC))
+    batch["x0"] = latents_f32((F, h0, h0, c_lat), f"x0{tag}")
+    batch["eps"] = latents_f32((F, h0, h0, c_lat), f"eps{tag}")
+    batch["lat_cache"] = latents_f32((F, h0, h0, c_lat), f"lc{tag}")
+    for l, (h, c) in enumerate(levels):
+        batch[f"feat{l}"] = features_bf16((F, h, h, c), f"x{l}{tag}")
+        batch[f"cache{l}"] = features_bf16((F, h, h, c), f"c{l}{tag}")
+        for j in range(convs_per_level):
+            batch[f"w{l}{j}"] = weights_bf16(c, c, f"w{l}{j}")
+            batch[f"b{l}{j}"] = bias_f32(c, f"b{l}{j}")
+    return batch

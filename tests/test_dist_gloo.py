@@ -8,6 +8,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+sys_path_tests = os.path.dirname(os.path.abspath(__file__))
+
 from paper_2511_18672_b200 import dist as sdist
 
 
@@ -82,3 +84,85 @@ def test_frame_costs_weighting():
     # a level-2 block (1280 ch) costs 16x a level-0 block (320 ch)
     c = sdist.frame_costs([[1, 0, 0], [0, 0, 1]], [320, 640, 1280])
     assert c[1] == 16 * c[0]
+
+
+# ------------------------------------------------------------------ the sharded step
+
+def _small_cfg():
+    from paper_2511_18672_b200.step import StepConfig
+    # 4 requests x 6 frames of 48x48 images, f=4 -> 12x12 latent; levels 12/6/3 with 4x4 blocks
+    # (ragged edge blocks at 6 and 3)
+    return StepConfig(hp=48, f=4, b=4, levels=((12, 16), (6, 32), (3, 32)), convs_per_level=2,
+                      frames_per_request=6, n_requests=4, u=25, gamma=0.5)
+
+
+def _small_batch():
+    import synthetic as syn
+    cfg = _small_cfg()
+    return syn.make_batch([0.3, 0.9, 0.1, 0.6], tag="gloo-step", hp=cfg.hp, f=cfg.f, b=cfg.b, levels=cfg.levels,
+                          convs_per_level=cfg.convs_per_level, frames_per_request=cfg.frames_per_request)
+
+
+def _step_outputs(st):
+    cfg = st.cfg
+    outs = [st.out(l).view(torch.int16).numpy().copy() for l in range(cfg.L)]
+    return outs, st.lat_out.numpy().copy()
+
+
+def _step_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, sys_path_tests)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle_ops
+        from paper_2511_18672_b200.step import RefinementStep
+        cfg = _small_cfg()
+        st = RefinementStep(cfg, _small_batch(), "cpu", oracle_ops, rank=rank, world=world)
+        for _ in range(2):  # two steps: persistent buffers and the plan are reused across steps
+            st.run()
+        outs, lat = _step_outputs(st)
+        q.put((rank, outs, lat, st.plan["rank_of"].tolist(), st.bytes_sent, st.k_mine.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_sharded_step_matches_single_rank(world):
+    """The whole data plane at world 2 and 4 (gloo, CPU, oracle compute): mask slices, the
+    mask/start-step all-gather, the LPT plan, compaction over assigned frames and the owner
+    gather of refined blocks.  Every owner's buffers (the last conv of every level and the
+    latent) equal a single-rank step over the whole batch bit for bit, for its requests' frames."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    import oracle_ops
+    from paper_2511_18672_b200.step import RefinementStep
+    cfg = _small_cfg()
+    ref = RefinementStep(cfg, _small_batch(), "cpu", oracle_ops)
+    ref.run()
+    ref.run()
+    want_outs, want_lat = _step_outputs(ref)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    owner = cfg.owner_of_frame(world)
+    plans = [r[3] for r in res]
+    assert all(p == plans[0] for p in plans)              # every rank derived the same plan
+    rank_of = np.array(plans[0])
+    assert (rank_of != owner).any()                       # some frames are computed off-owner
+    assert sum(r[4] for r in res) > 0                     # ... so refined blocks moved
+    for rank, outs, lat, _, _, kmine in res:
+        mine = owner == rank
+        for l in range(cfg.L):
+            assert np.array_equal(outs[l][mine], want_outs[l][mine]), (rank, l)
+        assert np.array_equal(lat[mine].view(np.uint32), want_lat[mine].view(np.uint32)), rank
+        # this rank compacted exactly the frames assigned to it
+        assert all((kmine[n] == -1) == (rank_of[n] != rank or ref.k[n].item() == -1) for n in range(cfg.n_frames))

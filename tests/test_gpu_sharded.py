@@ -1,0 +1,133 @@
+"""GPU test of the multi-rank data plane with the real kernels: 2 and 4 ranks share
+the one GPU of the test box (gloo transport staged through host memory -- NCCL refuses two ranks
+on one device; on an 8-GPU box the same code moves device tensors with NCCL).  Every owner's
+buffers after a sharded step equal a single-rank step over the whole batch bit for bit for its
+requests' frames: every block is computed by exactly one rank with the same kernels, and
+sphinx_gather_blocks / sphinx_scatter_blocks are bit copies."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+
+
+def _cfg():
+    from paper_2511_18672_b200.step import StepConfig
+    # 4 requests x 6 frames at the paper's geometry (576x576 -> 72/36/18, 320/640/1280 channels)
+    return StepConfig(frames_per_request=6, n_requests=4)
+
+
+def _batch():
+    import synthetic as syn
+    cfg = _cfg()
+    return syn.make_batch([0.3, 0.75, 0.1, 0.5], tag="gpu-shard", frames_per_request=cfg.frames_per_request)
+
+
+def _outs(st):
+    torch.cuda.synchronize()
+    return ([st.out(l).view(torch.int16).cpu().numpy() for l in range(st.cfg.L)], st.lat_out.cpu().numpy(),
+            [st.y[l].view(torch.int16).cpu().numpy() for l in range(st.cfg.L)])
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2511_18672_b200 as sp
+        from paper_2511_18672_b200.step import RefinementStep
+        sp.load()
+        st = RefinementStep(_cfg(), _batch(), torch.device("cuda", 0), sp, rank=rank, world=world)
+        for _ in range(2):
+            st.run()
+        outs, lat, _ = _outs(st)
+        q.put((rank, outs, lat, st.plan["rank_of"].tolist(), st.bytes_sent))
+    finally:
+        dist.destroy_process_group()
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_step_matches_single_rank_on_gpu(sphinx, world):
+    import torch.multiprocessing as mp
+    from paper_2511_18672_b200.step import RefinementStep
+    cfg = _cfg()
+    ref = RefinementStep(cfg, _batch(), torch.device("cuda", 0), sphinx)
+    ref.run()
+    ref.run()
+    want, want_lat, _ = _outs(ref)
+    del ref
+    torch.cuda.empty_cache()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    owner = cfg.owner_of_frame(world)
+    rank_of = np.array(res[0][3])
+    assert all(r[3] == res[0][3] for r in res)
+    assert (rank_of != owner).any() and sum(r[4] for r in res) > 0
+    for rank, outs, lat, _, _ in res:
+        mine = owner == rank
+        for l in range(cfg.L):
+            assert np.array_equal(outs[l][mine], want[l][mine]), (rank, l)
+        assert np.array_equal(lat[mine].view(np.uint32), want_lat[mine].view(np.uint32)), rank
+
+
+def test_gather_scatter_blocks_bit_copy(sphinx):
+    """sphinx_gather_blocks / sphinx_scatter_blocks: bit copies of listed blocks (NaN payloads and
+    -0 kept), truncated edge blocks, unlisted pixels untouched, any list order."""
+    import synthetic as syn
+    rg = np.random.default_rng(3)
+    for (n, h, w, c, b, dt) in [(3, 18, 18, 1280, 8, torch.bfloat16), (2, 36, 36, 640, 8, torch.bfloat16),
+                                (4, 72, 72, 4, 8, torch.float32), (2, 13, 7, 8, 4, torch.bfloat16)]:
+        hb, wb = -(-h // b), -(-w // b)
+        src = torch.from_numpy(rg.integers(-2 ** 15, 2 ** 15, size=(n, h, w, c * (2 if dt == torch.float32 else 1)),
+                                           dtype=np.int64).astype(np.int16)).view(dt).cuda()
+        src.view(torch.int16)[0, 0, 0, :2] = torch.tensor([0x7FC1, -32768], dtype=torch.int16)  # NaN payload, -0
+        ids_np = np.sort(rg.choice(n * hb * wb, size=max(1, n * hb * wb // 2), replace=False)).astype(np.int32)
+        ids_np = np.concatenate([[0], ids_np[ids_np != 0]]).astype(np.int32)
+        perm = rg.permutation(len(ids_np))
+        for order in (np.arange(len(ids_np)), perm):
+            ids = torch.from_numpy(ids_np[order]).cuda()
+            cnt = torch.tensor([len(ids_np)], dtype=torch.int32).cuda()
+            pay = torch.zeros((len(ids_np), b, b, src.shape[-1]), dtype=dt, device="cuda")
+            sphinx.sphinx_gather_blocks(src, pay, b, ids, cnt)
+            out = torch.zeros_like(src)
+            out.view(torch.int16).fill_(0x1234)
+            sphinx.sphinx_scatter_blocks(pay, out, b, ids, cnt)
+            torch.cuda.synchronize()
+            s16 = src.view(torch.int16).cpu().numpy()
+            o16 = out.view(torch.int16).cpu().numpy()
+            p16 = pay.view(torch.int16).cpu().numpy()
+            listed = np.zeros((n, h, w), bool)
+            for j, id_ in enumerate(ids_np[order]):
+                f, r = divmod(int(id_), hb * wb)
+                by, bx = divmod(r, wb)
+                ry, rx = min(b, h - by * b), min(b, w - bx * b)
+                listed[f, by * b:by * b + ry, bx * b:bx * b + rx] = True
+                assert np.array_equal(p16[j, :ry, :rx], s16[f, by * b:by * b + ry, bx * b:bx * b + rx])
+            assert np.array_equal(o16[listed], s16[listed])
+            assert np.all(o16[~listed] == 0x1234)
