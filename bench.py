@@ -356,8 +356,8 @@ def memory_kernels(torch, st, reps=10):
     ms = timed(lambda: sp.sphinx_gather_blocks(st.z[0], pay, cfg.b, st.ids[0], st.cnt[0]))
     row("gather_blocks_level0 (data plane pack)", ms, 2 * cnt * 64 * 320 * 2, "2 x listed block bytes")
     zo = torch.empty_like(st.zt)
-    ms = timed(lambda: sp.sphinx_ddim_step(st.zt, d["x0"], zo, cfg.b, st.ids[0], st.cnt[0], cfg.u,
-                                           d["abar"].cpu().numpy()))
+    abar_h = d["abar"].cpu().numpy()  # host table (the step u is a loop scalar)
+    ms = timed(lambda: sp.sphinx_ddim_step(st.zt, d["x0"], zo, cfg.b, st.ids[0], st.cnt[0], cfg.u, abar_h))
     row("ddim_step (NEXT-1)", ms, cnt * 64 * cfg.c_lat * 12, "12 B per active latent element (z, x0_hat in; z' out)")
     nu = min(n, 21)
     rgb = torch.rand((nu, hp, hp, 3), device=dev, dtype=torch.float32)
