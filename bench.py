@@ -583,11 +583,16 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.share_gpu:  # functional check of the N-rank path on a 1-GPU box (timings meaningless)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     sp.load()
     hbm, tc_peak, tc_sust, peak_kind = peaks()
     name = args.workload
@@ -640,21 +645,28 @@ def run_gpu(args):
         ms_min = -sdist.reduce_step(-ms, 0.0, device=dev)[0]
         sent = torch.tensor([float(st.bytes_sent)], dtype=torch.float64, device=dev)
         dist.all_reduce(sent)
+        comm_max, _ = sdist.reduce_step(st.comm_ms(), 0.0, device=dev)
+        e2e_sh = None if args.no_e2e else run_e2e_sharded(torch, st, batch, dev, args, flops, world)
         p = st.plan
         multi = {"ranks": world, "partition": "LPT over frames by executed MMA work (sum_l count*C_l^2) at u",
                  "plan_imbalance_max_over_mean": round(p["imbalance"], 4),
                  "step_ms_max": round(ms_all, 5), "step_ms_min": round(ms_min, 5),
                  "bytes_moved_per_step": int(sent.item()),
+                 "comm_ms_max": round(comm_max, 5),
+                 "comm_note": "device time of the owner-gather sections (pack + grouped send/recv + unpack) "
+                              "on the communication stream, summed over levels, max over ranks; it overlaps "
+                              "the next level's convs",
                  "owner": "request j -> rank j*N//R", "nccl": nccl_summary() if rank == 0 else None}
     else:
         ms_all = ms
+        e2e_sh = None
     value = flops / (ms_all * 1e-3) / 1e12
     per_level, roof = conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms)
 
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
         extras["conv_warm_cold"] = warm_cold_conv(torch, st, flush)
-        extras["e2e"] = run_e2e(torch, st, g, batch, dev, args, flops)
+        extras["e2e"] = None if args.no_e2e else run_e2e(torch, st, g, batch, dev, args, flops)
         extras["memory_kernels"] = memory_kernels(torch, st)
         extras["configs2"] = single_rank_workload(torch, sp, "configs2", dev, flush, args, tc_peak, tc_sust)
         del g, g_ev
@@ -699,7 +711,7 @@ def run_gpu(args):
             line["gpu_launches_note"] = "eager multi-rank step: per rank ~%d sphinx kernels + NCCL" % (
                 st.launches_per_step + 4 * L)
         line.update(extras)
-        line["e2e"] = extras.get("e2e")
+        line["e2e"] = extras.get("e2e") if world == 1 else e2e_sh
         line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -809,6 +821,79 @@ def run_e2e(torch, st, g, batch, dev, args, flops):
                     "features and latents H2D; the refined latent (the step's result) D2H"}
 
 
+def run_e2e_sharded(torch, st, batch, dev, args, flops, world):
+    """e2e at N > 1 through the same public call: every step each rank copies from pinned host
+    memory the maps of its mask slice and the latents + level features of the frames the plan
+    assigned to it (stable across steps: same masks, same u), runs the sharded step, and reads
+    back the refined latent of the frames it owns.  Device time of the whole loop, max over ranks."""
+    from paper_2511_18672_b200 import dist as sdist
+    cfg = st.cfg
+    mine = np.flatnonzero(st.plan["rank_of"] == st.rank)
+    own = np.flatnonzero(st.owner == st.rank)
+    sl = st.slice
+    maps = ["O", "U", "tau_u", "q", "c0", "c1", "t", "lid"]
+    frame_keys = ["x0", "eps", "lat_cache"] + [f"feat{l}" for l in range(cfg.L)]
+
+    def pin(a):
+        a = np.ascontiguousarray(a.view(np.int16) if a.dtype == np.uint16 else a)
+        return torch.from_numpy(a).pin_memory()
+    host_maps = {k: pin(batch[k][sl]) for k in maps}
+    host_frames = {k: pin(batch[k][mine]) for k in frame_keys}
+    out_host = torch.empty((len(own),) + tuple(st.lat_out.shape[1:]), dtype=torch.float32).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in list(host_maps.values()) + list(host_frames.values()))
+    d2h = out_host.numel() * 4
+    runs = [(int(a), int(b)) for a, b in _runs(mine)]
+
+    def dev_view(k):
+        t = st.d[k]
+        return t.view(torch.int16) if t.dtype == torch.bfloat16 else t
+
+    def step():
+        for k, h in host_maps.items():
+            dev_view(k)[sl].copy_(h, non_blocking=True)
+        for k, h in host_frames.items():
+            dv, off = dev_view(k), 0
+            for a, b in runs:  # contiguous frame runs of this rank's assignment
+                dv[a:b].copy_(h[off:off + b - a], non_blocking=True)
+                off += b - a
+        st.run()
+        o0 = int(own[0])
+        out_host.copy_(st.lat_out[o0:o0 + len(own)], non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    reps = max(1, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms, _ = sdist.reduce_step(e0.elapsed_time(e1) / reps, 0.0, device=dev)
+    tot = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+    import torch.distributed as dist
+    dist.all_reduce(tot)
+    return {"value": round(flops / (ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
+            "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item()),
+            "steps_timed": reps,
+            "note": "serial loop per rank: H2D of the rank's mask-slice maps and its assigned frames' latents and "
+                    "level features, the sharded step, D2H of the owned frames' refined latent; bytes summed over "
+                    "ranks, time max over ranks"}
+
+
+def _runs(idx):
+    """Contiguous runs [a, b) of a sorted index array."""
+    idx = list(idx)
+    out = []
+    for i in idx:
+        if out and out[-1][1] == i:
+            out[-1][1] = i + 1
+        else:
+            out.append([i, i + 1])
+    return out
+
+
 # ----------------------------------------------------------------- CPU oracle arm
 
 def oracle_step_sample(batch, cfg, max_blocks_per_level):
@@ -916,6 +1001,10 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-resblock", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo + --share-gpu: exercise the multi-rank path with every rank on cuda:0")
+    ap.add_argument("--share-gpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-flush", action="store_true", help="diagnostic: keep L2 warm between steps")
     ap.add_argument("--profile", action="store_true",

@@ -88,6 +88,8 @@ struct ConvParams {
   int taps;       // 9 = 3x3 conv; 1 = pointwise (1x1) projection (NEXT-4), per-tap path only
   int n_tiles_n;  // tiles along C_out
   int n_last;     // width of the last C_out tile (== BN: C_out is tiled in equal widths)
+  int tma_y;      // per-tap mode, bf16 y: the epilogue stages each 32-column chunk in shared memory
+                  // and writes it with one TMA tensor store per block (tmY)
   int bpt;        // blocks per 128-row tile = 128 / b^2
   // split-K workspace (NULL = never split): per-(tile, split) fp32 partial tiles and one
   // arrival counter per (tile, CTA of the pair); counters are zero between launches.
@@ -153,8 +155,9 @@ struct ConvCfg {
   static constexpr int kBarBytes = 512 + kBM * 8 + 2 * 256 * 4 + (NORM ? 8 * 8 * 20 * 4 + 512 : 0);
   static constexpr int kMaxSmem = 232448;          // 227 KB opt-in per CTA
   static constexpr int kAvail = kMaxSmem - 1024 - kBarBytes;
-  // per-tap mode
-  static constexpr int kStagesFit = kAvail / kStageBytes;
+  // per-tap mode: + the TMA-store staging of the epilogue (2 halves x 2 buffers x 128 rows x 64 B)
+  static constexpr int kStoreBytes = HALO ? 0 : 2 * 2 * kBM * 64;
+  static constexpr int kStagesFit = (kAvail - kStoreBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   // halo mode (BPT = 2 blocks of 8x8)
   static constexpr int kHaloRow = 1280;
@@ -171,7 +174,7 @@ struct ConvCfg {
   static constexpr int kNumBars = HALO ? kANum + kBNum : kStages;
   static constexpr uint32_t kTmemCols = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int kSmem = 1024 + kRingBytes + kBarBytes;
+  static constexpr int kSmem = 1024 + kRingBytes + kStoreBytes + kBarBytes;
   static_assert(HALO ? kBNum >= 3 : kStages >= 3, "pipeline too shallow");
   static_assert((2 * kNumBars + 5 + 3) * 8 <= 512, "barrier area");
   // stream-K owner staging: 2 buffers x kMaxParts parts x (32 cols x 128 rows fp32)
@@ -392,6 +395,57 @@ __device__ __forceinline__ HaloTile halo_tile(int mt, int rank, int nF, int nB, 
   return g;
 }
 
+// Per-tap mode, bf16 y: one 32-column chunk of the tile (this thread = tile row `row`) -> bias
+// (+ residual) -> bf16 -> the half's staging buffer (row-major 64 B rows, SW64 swizzle), then one
+// TMA tensor store per listed block of the tile (box {32 ch, BLK, BLK, 1}; out-of-image pixels
+// of edge blocks and channels beyond C_out are clipped by the TMA unit).  Rows are block-major,
+// so row r sits at byte r * 64 = (block, pixel) of the box layout.  Two buffers per half: the
+// issuing thread (row 0) waits until the store that last read a buffer has read it.
+template <int BLK, int BPT>
+__device__ __forceinline__ void stage_chunk_tma(const ConvParams& p, const CUtensorMap& tmY, uint8_t* buf,
+                                                int row, int half, size_t pix, bool valid, int co,
+                                                float (&v)[32], const float* sb, int j0, int count) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 b4 = *reinterpret_cast<const float4*>(sb + i);
+    v[i] += b4.x;
+    v[i + 1] += b4.y;
+    v[i + 2] += b4.z;
+    v[i + 3] += b4.w;
+  }
+  if (p.res && valid) add_residual<32>(p, pix, co, v);
+  if (row == 0) bulk_wait_group_read<1>();
+  named_bar_sync(4 + half, 128);
+  const uint32_t base = smem_u32(buf) + (uint32_t)row * 64u;
+  const uint32_t sw = ((uint32_t)row >> 1) & 3u;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint4 pk;
+    __nv_bfloat162 t0 = __floats2bfloat162_rn(v[8 * g + 0], v[8 * g + 1]);
+    __nv_bfloat162 t1 = __floats2bfloat162_rn(v[8 * g + 2], v[8 * g + 3]);
+    __nv_bfloat162 t2 = __floats2bfloat162_rn(v[8 * g + 4], v[8 * g + 5]);
+    __nv_bfloat162 t3 = __floats2bfloat162_rn(v[8 * g + 6], v[8 * g + 7]);
+    pk.x = *reinterpret_cast<uint32_t*>(&t0);
+    pk.y = *reinterpret_cast<uint32_t*>(&t1);
+    pk.z = *reinterpret_cast<uint32_t*>(&t2);
+    pk.w = *reinterpret_cast<uint32_t*>(&t3);
+    sts128(base + (((uint32_t)g ^ sw) << 4), pk);
+  }
+  fence_proxy_async_shared();
+  named_bar_sync(4 + half, 128);
+  if (row == 0) {
+#pragma unroll 1
+    for (int bi = 0; bi < BPT; ++bi) {
+      const int j = j0 + bi;
+      if (j >= count) break;  // a short last tile's padding blocks are computed, never stored
+      int n, by, bx;
+      decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
+      tma_store_4d(&tmY, buf + bi * (BLK * BLK * 64), co, bx * BLK, by * BLK, n);
+    }
+    bulk_commit_group();
+  }
+}
+
 // CG = 1: one CTA per 128 x BN tile, tcgen05.mma.cta_group::1 (M = 128).
 // CG = 2: a CTA pair (cluster of 2) per 256 x BN tile, tcgen05.mma.cta_group::2 (M = 256):
 //   each CTA TMA-loads its own 128 rows of A and its half (BN/2 rows) of B; the leader
@@ -403,7 +457,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
     sparse_conv3x3_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                              const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmC,
-                             const __grid_constant__ CUtensorMap tmB2, const ConvParams p) {
+                             const __grid_constant__ CUtensorMap tmY, const ConvParams p) {
   using Cfg = ConvCfg<BN, CG, HALO, EDGE, NORM>;
   static_assert(!NORM || HALO, "the fused GN+SiLU transform works on halo slots");
   static_assert(!EDGE || HALO, "edge packing is a halo-mode feature");
@@ -415,7 +469,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + (HALO ? Cfg::kARing : S * kStageA);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes);
+  uint8_t* s_store = smem + Cfg::kRingBytes;  // per-tap mode: [half][buf][128 rows x 64 B], SW64
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes + Cfg::kStoreBytes);
   uint64_t* empty = full + NB;
   uint64_t* tfull = empty + NB;
   uint64_t* tempty = tfull + 2;
@@ -640,11 +695,9 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
             if (cb.it.x != b_seg) {
               b_seg = cb.it.x;
               const int ntb = cb.g.t - (cb.g.t / p.n_tiles_n) * p.n_tiles_n;
-              // ragged last C_out tile: narrower weight box (second tensor map), fewer bytes
-              const bool nar = ntb == p.n_tiles_n - 1 && p.n_last < BN;
-              b_n0 = ntb * BN + rank * (nar ? p.n_last / CG : Cfg::kBNc);
-              b_bytes = nar ? (uint32_t)(p.n_last / CG) * kBK * 2 : (uint32_t)Cfg::kStageB;
-              b_tm = nar ? &tmB2 : &tmB;
+              b_n0 = ntb * BN + rank * Cfg::kBNc;
+              b_bytes = (uint32_t)Cfg::kStageB;
+              b_tm = &tmB;
             }
             const int n0 = b_n0;
             for (int tap = 0; tap < 9; ++tap) {
@@ -694,11 +747,9 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
           cy[i] = by * BLK - 1;
           cx[i] = bx * BLK - 1;
         }
-        const bool nar = nt == p.n_tiles_n - 1 && p.n_last < BN;
-        const int n0 = nt * BN + rank * (nar ? p.n_last / CG : Cfg::kBNc);
-        const uint32_t stage_bytes = (uint32_t)kStageA + (nar ? (uint32_t)(p.n_last / CG) * kBK * 2
-                                                              : (uint32_t)Cfg::kStageB);
-        const CUtensorMap* b_tm = nar ? &tmB2 : &tmB;
+        const int n0 = nt * BN + rank * Cfg::kBNc;
+        const uint32_t stage_bytes = (uint32_t)kStageA + (uint32_t)Cfg::kStageB;
+        const CUtensorMap* b_tm = &tmB;
         int tap = ks0 / p.kc, kc = ks0 - (ks0 / p.kc) * p.kc;
         for (int ks = ks0; ks < ks1; ++ks) {
           {
@@ -865,6 +916,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     const int erow = half * kBM + row;  // epilogue thread index
+    int st_cnt = 0;                      // staged chunks (TMA-store path): buffer = st_cnt & 1
     int acc = 0;
     uint32_t acc_phase = 0;
     SegIter it = it0;
@@ -978,6 +1030,8 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         // a ragged last C_out tile only has p.n_last valid accumulator columns (the rest are
         // beyond C_out: never stored, so they need not be drained or parked either)
         const int width = (nt == p.n_tiles_n - 1 && p.n_last < BN) ? p.n_last : BN;
+        // per-tap mode, bf16 y: staged TMA stores (one 4-D box per block and 32-column chunk)
+        const bool staged = !HALO && p.tma_y && ns == 1 && sg.role != kPart;
         for (int c0 = half * 32; c0 < width; c0 += 32 * kHalves) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
@@ -989,6 +1043,19 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
             // split-K: park this split's fp32 partial (column-major, coalesced)
 #pragma unroll
             for (int i = 0; i < 32; ++i) __stcg(part + (size_t)(c0 + i) * kBM, __uint_as_float(r[i]));
+          } else if (staged) {
+            if constexpr (!HALO) {
+              // Row r of the tile is pixel (ry, rx) of block bi (block-major rows), i.e. byte r*64
+              // of the staging buffer is exactly where the box {32 ch, BLK, BLK, 1} of block bi
+              // expects it; the 16-B chunks are SW64-swizzled (chunk ^= (r >> 1) & 3) to match the
+              // tensor map and keep the warp's shared stores conflict-free.
+              float v[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+              stage_chunk_tma<BLK, BPT>(p, tmY, s_store + (half * 2 + (st_cnt & 1)) * (kBM * 64), row, half, pix,
+                              valid, nt * BN + c0, v, sbt + c0, mt * bpt_pair + rank * BPT, count);
+              ++st_cnt;
+            }
           } else if (valid) {
             float v[32];
 #pragma unroll
@@ -1115,6 +1182,9 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         }
       }
     }
+    // staged TMA stores: complete before the CTA exits (shared memory must outlive their reads)
+    if constexpr (!HALO)
+      if (p.tma_y && row == 0) bulk_wait_group_all();
   } else if constexpr (NORM) {
     if (warp >= kXWarp) {
       // ============ fused GroupNorm + SiLU (NEXT-3): transform warps 7..14, both CTAs ============
@@ -1477,11 +1547,22 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
-    const cuuint32_t box2[3] = {(cuuint32_t)kBK, 1, (cuuint32_t)(bn / cg)};
-    r = enc(&tb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides, box2, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  // per-tap mode with bf16 y: the epilogue writes each 32-column chunk of a block with one TMA
+  // tensor store (box {32 ch, b, b, 1} of the NHWC map; SW64 staging layout)
+  const int tma_y = (!halo && y_dtype == SPHINX_BF16 && !norm_tab && c_out >= 32) ? 1 : 0;
+  if (tma_y) {
+    const cuuint64_t dims[4] = {(cuuint64_t)c_out, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
+    const cuuint64_t strides[3] = {(cuuint64_t)c_out * 2, (cuuint64_t)w_ * c_out * 2,
+                                   (cuuint64_t)h * w_ * c_out * 2};
+    const cuuint32_t box[4] = {32, (cuuint32_t)block, (cuuint32_t)block, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(&tb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return SPHINX_ERR_UNSUPPORTED;
+  } else {
+    tb2 = tb;  // unused
   }
   ConvParams p;
   p.ids = block_ids;
@@ -1502,6 +1583,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   p.taps = taps;
   p.n_tiles_n = cdiv(c_out, bn);
   p.n_last = bn;
+  p.tma_y = tma_y;
   p.bpt = kBM / (block * block);
   p.halo = halo;
   p.trace = 0;

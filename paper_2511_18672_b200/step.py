@@ -328,6 +328,8 @@ class RefinementStep:
             ev.record()
             self.comm_stream.wait_event(ev)
             ctx = torch.cuda.stream(self.comm_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(self.comm_stream)
         with ctx:
             n_mine = int(pair[me].sum())
             items = [(self.out(l), c, torch.bfloat16, "f")]
@@ -364,17 +366,26 @@ class RefinementStep:
                     ops.sphinx_scatter_blocks(rpay, mp, b, self.recv_ids[l], self.recv_cnt[l:l + 1],
                                               capacity=n_recv)
             self.bytes_sent += sum(t.numel() for _, t in sends)
+        if self.cuda:
+            e1.record(self.comm_stream)
+            self.comm_events.append((e0, e1))
 
     # ------------------------------------------------------------------ the step
     def run(self, conv_events=None):
         """One refinement step (all of SURVEY 8(a)) on this rank's share of the batch."""
         self.bytes_sent = 0
+        self.comm_events = []
         self._masks()
         if self.world > 1:
             self._plan_step()
         self._compute(conv_events)
         if self.world > 1 and self.cuda:
             self.torch.cuda.current_stream().wait_stream(self.comm_stream)
+
+    def comm_ms(self):
+        """Device time of the last step's owner-gather sections (pack, grouped send/recv, unpack)
+        on the communication stream, summed over levels (call after synchronising)."""
+        return sum(a.elapsed_time(b) for a, b in getattr(self, "comm_events", []))
 
     def active_stats(self):
         """Algorithmic conv FLOPs of the step over the WHOLE batch (real active pixels of every

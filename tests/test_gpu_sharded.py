@@ -1,9 +1,14 @@
 """GPU test of the multi-rank data plane with the real kernels: 2 and 4 ranks share
 the one GPU of the test box (gloo transport staged through host memory -- NCCL refuses two ranks
-on one device; on an 8-GPU box the same code moves device tensors with NCCL).  Every owner's
-buffers after a sharded step equal a single-rank step over the whole batch bit for bit for its
-requests' frames: every block is computed by exactly one rank with the same kernels, and
-sphinx_gather_blocks / sphinx_scatter_blocks are bit copies."""
+on one device; on an 8-GPU box the same code moves device tensors with NCCL).
+
+* Data plane, bit for bit: after a sharded step every owner's buffers hold, for each of its
+  requests' frames, exactly the values the rank that computed the frame produced (pack, transfer
+  and unpack are bit copies; every frame is computed by exactly one rank).
+* Against a single-rank step over the whole batch: equal within the conv bar.  Not bitwise: the
+  device picks tail split-K from the list length (tiles of the last partial wave are split along
+  K and reduced in a fixed order), and a rank's list is a subset of the batch's, so a block may
+  be summed in a different (equally exact) order.  The latent path (noise, scatter) is bitwise."""
 import os
 import socket
 import sys
@@ -51,7 +56,9 @@ def _worker(rank, world, port, q):
         for _ in range(2):
             st.run()
         outs, lat, _ = _outs(st)
-        q.put((rank, outs, lat, st.plan["rank_of"].tolist(), st.bytes_sent))
+        keep = (st.plan["rank_of"] == rank) | (st.owner == rank)
+        q.put((rank, {int(n): [o[n] for o in outs] + [lat[n]] for n in np.flatnonzero(keep)},
+               st.plan["rank_of"].tolist(), st.bytes_sent))
     finally:
         dist.destroy_process_group()
 
@@ -86,14 +93,25 @@ def test_sharded_step_matches_single_rank_on_gpu(sphinx, world):
         p.join(timeout=120)
         assert p.exitcode == 0
     owner = cfg.owner_of_frame(world)
-    rank_of = np.array(res[0][3])
-    assert all(r[3] == res[0][3] for r in res)
-    assert (rank_of != owner).any() and sum(r[4] for r in res) > 0
-    for rank, outs, lat, _, _ in res:
-        mine = owner == rank
+    rank_of = np.array(res[0][2])
+    assert all(r[2] == res[0][2] for r in res)
+    assert (rank_of != owner).any() and sum(r[3] for r in res) > 0
+    frames = {r[0]: r[1] for r in res}
+    for n in range(cfg.n_frames):
+        got = frames[owner[n]][n]          # the owner's buffers after the step
+        comp = frames[rank_of[n]][n]       # what the computing rank produced
         for l in range(cfg.L):
-            assert np.array_equal(outs[l][mine], want[l][mine]), (rank, l)
-        assert np.array_equal(lat[mine].view(np.uint32), want_lat[mine].view(np.uint32)), rank
+            assert np.array_equal(got[l], comp[l]), (n, l)
+            g = got[l].view(np.uint16)
+            w = want[l][n].view(np.uint16)
+            gf = (g.astype(np.uint32) << 16).view(np.float32)
+            wf = (w.astype(np.uint32) << 16).view(np.float32)
+            # both are within the conv bar of the exact value: differences are rare and small
+            d = np.abs(gf - wf)
+            assert d.max() <= 2.0 ** -6 * np.abs(wf).max() + 1e-6, (n, l)
+            assert (d > 0).mean() < 0.05, (n, l)
+        assert np.array_equal(got[cfg.L], comp[cfg.L])
+        assert np.array_equal(got[cfg.L].view(np.uint32), want_lat[n].view(np.uint32)), n
 
 
 def test_gather_scatter_blocks_bit_copy(sphinx):

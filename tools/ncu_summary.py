@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--rep")
     ap.add_argument("--bench")
+    ap.add_argument("--mem", help="ncu --set full capture of the HBM-bound kernels")
     a = ap.parse_args()
     print(f"# ncu summary — {a.tag}\n")
     if a.bench:
@@ -90,6 +91,22 @@ def main():
             vals = [d.get(k, "") for k, _ in keys]
             print(f"| `{d.get('Kernel Name','')[:60]}` | {d.get('Grid Size','')} | " + " | ".join(vals) + " |")
         print("\n(dram bytes in the unit ncu reports; `traffic` = read + write per launch)")
+    if a.mem:
+        rows = full(a.mem)
+        keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+                "launch__grid_size"]
+        print("\n## HBM-bound kernels of the step (`ncu --set full --clock-control none`)\n")
+        print("| kernel | " + " | ".join(k.split('.')[0].replace('__', ' ') for k in keys) + " | achieved GB/s |")
+        print("|---" * (len(keys) + 2) + "|")
+        for d in rows:
+            def num(k):
+                v = d.get(k, "0 ").split()
+                x = float(v[0].replace(",", ""))
+                u = v[1] if len(v) > 1 else ""
+                return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9}.get(u, 1)
+            gbs = (num("dram__bytes_read.sum") + num("dram__bytes_write.sum")) / max(num("gpu__time_duration.sum"), 1e-12) / 1e9
+            print(f"| `{d.get('Kernel Name','')[:50]}` | " + " | ".join(d.get(k, "") for k in keys) + f" | {gbs:.0f} |")
 
 
 if __name__ == "__main__":
