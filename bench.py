@@ -661,7 +661,16 @@ def run_gpu(args):
         ms_all = ms
         e2e_sh = None
     value = flops / (ms_all * 1e-3) / 1e12
-    per_level, roof = conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms)
+    if world > 1:  # the conv launches of THIS rank process its own lists (its share of the batch)
+        my_px, my_blocks = [], []
+        for l in range(L):
+            ids = st.ids[l][: int(st.cnt[l].item())].cpu().numpy()
+            my_px.append(cfg.real_px(l, ids))
+            my_blocks.append(len(ids))
+        per_level, roof = conv_level_stats(st, conv_ms, my_px, my_blocks, tc_peak, tc_sust, ms)
+        roof["scope"] = "rank 0's own conv launches (its share of the batch)"
+    else:
+        per_level, roof = conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms)
 
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:

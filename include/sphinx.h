@@ -74,7 +74,9 @@ typedef enum { SPHINX_BF16 = 0, SPHINX_F32 = 1 } sphinx_dtype;
 typedef enum {
   SPHINX_SELECT_ACTIVE = 0,          /* mask == 1 and 0 <= k[n] <= u: A_u = 1[k <= u] (Alg1 line 17) */
   SPHINX_SELECT_INACTIVE_FRAMES = 1, /* every block of frames with k[n] > u: resampled (Alg1 line 19) */
-  SPHINX_SELECT_ALL = 2              /* every block of frames with k[n] >= 0 (or all if k == NULL) */
+  SPHINX_SELECT_ALL = 2,             /* every block of frames with k[n] >= 0 (or all if k == NULL) */
+  SPHINX_SELECT_NOISE = 3            /* ACTIVE | INACTIVE_FRAMES: every block the step's noise pass
+                                        touches (Alg1 lines 12 and 19 in one list); needs mask and k */
 } sphinx_select;
 
 typedef enum { SPHINX_SRC_FULL = 0, SPHINX_SRC_COMPACT = 1 } sphinx_src_layout;
@@ -107,7 +109,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 8
+#define SPHINX_ABI_VERSION 9
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -192,6 +194,17 @@ SPHINX_API sphinx_status sphinx_noise_inject(const float* x0, const float* eps, 
                                   const int32_t* block_ids, const int32_t* count, int32_t capacity,
                                   const int32_t* step, const float* abar, int32_t total_steps,
                                   sphinx_stream_t stream);
+/* The step's whole noise pass in one launch (Alg1 line 12 for active frames, line 19 for inactive
+ * ones): for every listed block of frame n, u_n = start_step[n] if 0 <= start_step[n] <= step_u
+ * (active: noised to its start step k) and u_n = step_u + 1 if start_step[n] > step_u (inactive:
+ * resampled); frames with start_step < 0 are untouched.  Use with a SPHINX_SELECT_NOISE list.
+ * Same arguments and results as two sphinx_noise_inject calls over the ACTIVE and
+ * INACTIVE_FRAMES lists with those steps; step_u + 1 <= total_steps. */
+SPHINX_API sphinx_status sphinx_noise_inject_step(const float* x0, const float* eps, float* x_t,
+                                       int32_t n, int32_t h, int32_t w, int32_t c, int32_t block,
+                                       const int32_t* block_ids, const int32_t* count, int32_t capacity,
+                                       const int32_t* start_step, int32_t step_u, const float* abar,
+                                       int32_t total_steps, sphinx_stream_t stream);
 
 /* ---------------------------------------------------------------------------------
  * (4) Block-sparse 3x3 convolution ("tiles the feature maps into blocks ...

@@ -184,9 +184,9 @@ int oracle_start_step(const float* q, const float* c0, const float* c1, const fl
 int oracle_compact(const uint8_t* mask, int n, int hb, int wb, const int32_t* k, int u,
                    int select, int32_t* ids, int32_t* count) {
   if (!ids || !count || n <= 0 || hb <= 0 || wb <= 0) return BAD;
-  if (select < 0 || select > 2) return BAD;
-  if (select == 0 && !mask) return BAD;
-  if (select == 1 && !k) return BAD;
+  if (select < 0 || select > 3) return BAD;
+  if ((select == 0 || select == 3) && !mask) return BAD;
+  if ((select == 1 || select == 3) && !k) return BAD;
   int32_t c = 0;
   for (int i = 0; i < n; ++i)
     for (int by = 0; by < hb; ++by)
@@ -197,6 +197,8 @@ int oracle_compact(const uint8_t* mask, int n, int hb, int wb, const int32_t* k,
           take = mask[id] && (!k || (k[i] >= 0 && k[i] <= u));
         else if (select == 1) /* frames not in A_u are resampled (Alg1 line 19) */
           take = k[i] > u;
+        else if (select == 3) /* the step's noise pass: line 12's blocks or line 19's frames */
+          take = (mask[id] && k[i] >= 0 && k[i] <= u) || k[i] > u;
         else
           take = !k || k[i] >= 0;
         if (take) ids[c++] = id;

@@ -26,10 +26,10 @@ SO_PATH = os.path.join(HERE, "libsphinx.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_DEVICE = 0, 1, 2, 3, 4
 BF16, F32 = 0, 1
-SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
+SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL, SELECT_NOISE = 0, 1, 2, 3
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 8
+ABI_VERSION = 9
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
@@ -40,7 +40,7 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_temporal_attention", "sphinx_temporal_block", "sphinx_gn_scale_shift",
            "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex",
            "sphinx_sparse_resblock_ex", "sphinx_temporal_attention_ex", "sphinx_gather_blocks",
-           "sphinx_scatter_blocks",
+           "sphinx_scatter_blocks", "sphinx_noise_inject_step",
            "sphinx_conv_edge_plan")
 
 _lib = None
@@ -131,6 +131,7 @@ def load(path=SO_PATH):
                                        I, I, I, I, I, P, P, I, P, Z, I, P], I),
         "sphinx_sparse_pointwise": ([P, P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_gather_blocks": ([P, P, I, I, I, I, I, I, P, P, I, P], I),
+        "sphinx_noise_inject_step": ([P, P, P, I, I, I, I, I, P, P, I, P, I, P, I, P], I),
         "sphinx_scatter_blocks": ([P, P, I, I, I, I, I, I, P, P, I, P], I),
         "sphinx_gn_scale_shift": ([P, P, P, F, I, I, I, I, I, I, P, P], I),
         "sphinx_compact_blocks_batch": ([P, I, P], I),
@@ -266,6 +267,24 @@ def sphinx_noise_inject(x0, eps, x_t, block, block_ids, count, step, abar, capac
                                     _ptr(block_ids), _ptr(count), int(cap), _ptr(step), _ptr(abar),
                                     abar.numel() - 1, _stream(stream))
     _chk("sphinx_noise_inject", rc)
+
+
+def sphinx_noise_inject_step(x0, eps, x_t, block, block_ids, count, start_step, step_u, abar, capacity=None,
+                             stream=None):
+    """Step 3, the step's whole noise pass (Alg1 lines 12 + 19): listed blocks of frames with
+    0 <= k <= u to their start step k, of frames with k > u to u + 1 (SELECT_NOISE list)."""
+    import torch
+    for t, nm in ((x0, "x0"), (eps, "eps"), (x_t, "x_t"), (abar, "abar")):
+        _dev(t, torch.float32, nm)
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    _dev(start_step, torch.int32, "start_step")
+    n, h, w, c = x0.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = load().sphinx_noise_inject_step(_ptr(x0), _ptr(eps), _ptr(x_t), n, h, w, c, int(block),
+                                         _ptr(block_ids), _ptr(count), int(cap), _ptr(start_step), int(step_u),
+                                         _ptr(abar), abar.numel() - 1, _stream(stream))
+    _chk("sphinx_noise_inject_step", rc)
 
 
 _ws_cache = {}

@@ -21,7 +21,8 @@ __global__ void __launch_bounds__(256) noise_kernel(const float* __restrict__ x0
                                                     const int32_t* __restrict__ ids,
                                                     const int32_t* __restrict__ count,
                                                     const int32_t* __restrict__ step,
-                                                    const float* __restrict__ abar, int S) {
+                                                    const float* __restrict__ abar, int S,
+                                                    int step_u) {
   pdl_wait();
   pdl_trigger();
   const int cnt = *count;
@@ -38,7 +39,8 @@ __global__ void __launch_bounds__(256) noise_kernel(const float* __restrict__ x0
     const int by = rem / wb, bx = rem - by * wb;
     const int y = by * b + p / b, x = bx * b + p % b;
     if (y >= h || x >= w) continue;  // truncated edge block
-    const int u = __ldg(step + fr);
+    int u = __ldg(step + fr);
+    if (step_u >= 0) u = u > step_u ? step_u + 1 : u;  // step = start steps: active k, inactive u+1
     if (u < 0 || u > S) continue;
     const float ab = __ldg(abar + u);
     const float a = sqrtf(ab), s = sqrtf(1.0f - ab);
@@ -62,12 +64,11 @@ __global__ void __launch_bounds__(256) noise_kernel(const float* __restrict__ x0
 
 using namespace sphinx;
 
-extern "C" sphinx_status sphinx_noise_inject(const float* x0, const float* eps, float* x_t,
-                                             int32_t n, int32_t h, int32_t w, int32_t c,
-                                             int32_t b, const int32_t* block_ids,
-                                             const int32_t* count, int32_t capacity,
-                                             const int32_t* step, const float* abar,
-                                             int32_t total_steps, sphinx_stream_t stream) {
+static sphinx_status noise_impl(const float* x0, const float* eps, float* x_t, int32_t n, int32_t h,
+                                int32_t w, int32_t c, int32_t b, const int32_t* block_ids,
+                                const int32_t* count, int32_t capacity, const int32_t* step,
+                                const float* abar, int32_t total_steps, int32_t step_u,
+                                sphinx_stream_t stream) {
   if (!x0 || !eps || !x_t || !block_ids || !count || !step || !abar)
     return SPHINX_ERR_INVALID_ARGUMENT;
   if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || b <= 0 || capacity < 0 || total_steps < 2)
@@ -90,7 +91,29 @@ extern "C" sphinx_status sphinx_noise_inject(const float* x0, const float* eps, 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = launch_k(vec ? noise_kernel<4> : noise_kernel<1>, dim3((unsigned)blocks), dim3(256),
                            0, s, x0, eps, x_t, (int)h, (int)w, (int)c, (int)b, hb, wb, block_ids,
-                           count, step, abar, (int)total_steps);
+                           count, step, abar, (int)total_steps, (int)step_u);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
+}
+
+extern "C" sphinx_status sphinx_noise_inject(const float* x0, const float* eps, float* x_t,
+                                             int32_t n, int32_t h, int32_t w, int32_t c,
+                                             int32_t b, const int32_t* block_ids,
+                                             const int32_t* count, int32_t capacity,
+                                             const int32_t* step, const float* abar,
+                                             int32_t total_steps, sphinx_stream_t stream) {
+  return noise_impl(x0, eps, x_t, n, h, w, c, b, block_ids, count, capacity, step, abar, total_steps, -1,
+                    stream);
+}
+
+extern "C" sphinx_status sphinx_noise_inject_step(const float* x0, const float* eps, float* x_t,
+                                                  int32_t n, int32_t h, int32_t w, int32_t c,
+                                                  int32_t b, const int32_t* block_ids,
+                                                  const int32_t* count, int32_t capacity,
+                                                  const int32_t* start_step, int32_t step_u,
+                                                  const float* abar, int32_t total_steps,
+                                                  sphinx_stream_t stream) {
+  if (step_u < 0 || step_u + 1 > total_steps) return SPHINX_ERR_INVALID_ARGUMENT;
+  return noise_impl(x0, eps, x_t, n, h, w, c, b, block_ids, count, capacity, start_step, abar, total_steps,
+                    step_u, stream);
 }

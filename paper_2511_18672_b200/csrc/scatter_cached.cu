@@ -2,8 +2,8 @@
 //
 // P:352 "reuses cached latents from the last full denoising step for unrefined
 // regions".  HBM-bound copy, 2 x map bytes (read src-or-cache, write out).
-// FULL layout: a flat grid-stride loop over the 16-byte words of the NHWC map (coalesced for
-// any C); COMPACT layout: one CTA per (frame, pixel row), each block's row segment taken from
+// FULL layout: CTAs of 256 threads over (pixel rows x 16-byte words of a row), coalesced for
+// any C; COMPACT layout: one CTA per (frame, pixel row), each block's row segment taken from
 // its compact slot (binary search of the ascending list) or from the cache.  The element
 // type never passes through a float conversion (NaN payloads, -0 kept).
 #include "common.cuh"
@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(256) scatter_full_kernel(
   pdl_trigger();
   const int row_vec = w * px_vec;
   const float inv_pv = 1.0f / (float)px_vec;  // exact floor((xv + 0.5) / px_vec) for xv < 2^20
-  for (int row = blockIdx.y; row < rows; row += gridDim.y) {
+  // blockDim.y pixel rows per CTA: short rows (the 4-channel fp32 latent is 72 words) still
+  // give every warp a full row segment
+  for (int row = blockIdx.y * blockDim.y + threadIdx.y; row < rows; row += gridDim.y * blockDim.y) {
     const int n = row / h, y = row - n * h;
     const int kf = k ? __ldg(k + n) : 0;
     const bool frame_ok = !k || (kf >= 0 && kf <= u);
@@ -118,9 +120,16 @@ extern "C" sphinx_status sphinx_scatter_cached(const void* src, sphinx_src_layou
     check_device(&sms);
     if ((long long)w * px_vec >= (1 << 20)) return SPHINX_ERR_UNSUPPORTED;  // row index math
     const int rows = n * h, row_vec = w * px_vec;
-    const int gx = cdiv(row_vec, 256 * 4);
-    const int gy = rows < 65535 ? rows : 65535;
-    cudaError_t e = launch_k(scatter_full_kernel, dim3(gx, gy), dim3(256), 0, s,
+    // threads along the row's 16-byte words, 4 words in flight each (a multiple of 32, <= 256);
+    // the rest of the 256 threads over rows
+    int bdx = (cdiv(row_vec, 4) + 31) / 32 * 32;
+    bdx = bdx < 32 ? 32 : (bdx > 256 ? 256 : bdx);
+    while (256 % bdx) bdx += 32;
+    const int bdy = 256 / bdx;
+    const int gx = cdiv(row_vec, bdx * 4);
+    const int gyr = cdiv(rows, bdy);
+    const int gy = gyr < 65535 ? gyr : 65535;
+    cudaError_t e = launch_k(scatter_full_kernel, dim3(gx, gy), dim3(bdx, bdy), 0, s,
                              static_cast<const int4*>(src), static_cast<const int4*>(cache),
                              static_cast<int4*>(out), (int)h, (int)w, px_vec, (int)b, hb, wb,
                              block_mask, start_step, (int)step_u, out == src ? 1 : 0, rows);

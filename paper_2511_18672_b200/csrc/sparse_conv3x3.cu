@@ -88,6 +88,7 @@ struct ConvParams {
   int taps;       // 9 = 3x3 conv; 1 = pointwise (1x1) projection (NEXT-4), per-tap path only
   int n_tiles_n;  // tiles along C_out
   int n_last;     // width of the last C_out tile (== BN: C_out is tiled in equal widths)
+  int ring_bytes; // operand-ring bytes of the launched configuration (split-K staging bound)
   int tma_y;      // per-tap mode, bf16 y: the epilogue stages each 32-column chunk in shared memory
                   // and writes it with one TMA tensor store per block (tmY)
   int bpt;        // blocks per 128-row tile = 128 / b^2
@@ -128,6 +129,8 @@ __device__ __forceinline__ int choose_split(int tiles, int n_clusters, int kstep
   int best = 1, best_cost = ksteps * 1000;
   for (int sk = 2; sk <= kMaxSplit; ++sk) {
     if (ksteps / sk < kMinSteps || tiles * sk > n_clusters || tiles * sk > p.ws_slots) break;
+    // the reducing unit stages sk column slices of every part in the operand ring
+    if ((long long)sk * ((p.n_last / 8 + sk - 1) / sk) * 8 * kBM * 4 > p.ring_bytes) break;
     const int cost = ksteps * 1000 / sk + kRedCost * 1000;
     if (cost < best_cost) {
       best_cost = cost;
@@ -1407,7 +1410,9 @@ static sphinx_status launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, con
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tb2, p);
+  ConvParams pk = p;
+  pk.ring_bytes = Cfg::kRingBytes;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tb2, pk);
   if (e != cudaSuccess) return cuda_fail(e);
   return SPHINX_OK;
 }

@@ -9,9 +9,9 @@ kernels behind the C ABI (include/sphinx.h), reached through ``ops`` (the
 
 Single rank (world = 1): one stream, every launch PDL-chained, CUDA-graph capturable:
     sphinx_block_mask (a1 + a2) -> sphinx_compact_blocks_batch (a3: the L levels' ACTIVE lists at
-    u + the INACTIVE_FRAMES list) -> sphinx_conv_edge_plan (ragged levels) -> sphinx_noise_inject
-    x2 (a4: active latent blocks to their start step k, Alg1 line 12; inactive frames resampled
-    to u+1, line 19) -> per level `convs_per_level` x sphinx_sparse_conv3x3 C->C in persistent-
+    u + the NOISE list) -> sphinx_conv_edge_plan (ragged levels) -> sphinx_noise_inject_step
+    (a4: active latent blocks to their start step k, Alg1 line 12, and inactive frames resampled
+    to u+1, line 19, in one pass) -> per level `convs_per_level` x sphinx_sparse_conv3x3 C->C in persistent-
     buffer mode (a5; the feature-level scatter a6 fused into the epilogue, R-17) ->
     sphinx_scatter_cached of the latent (a6 at latent resolution, P:352 latent reuse).
 
@@ -174,9 +174,9 @@ class RefinementStep:
         self.k_mine = self.k if world == 1 else torch.full((F,), -1, dtype=i32, device=self.dev)
         self.ids = [torch.zeros((F * hb * hb,), dtype=i32, device=self.dev) for hb in cfg.hb]
         self.cnt = [torch.zeros((1,), dtype=i32, device=self.dev) for _ in range(L)]
-        self.ids_in = torch.zeros((F * cfg.hb[0] ** 2,), dtype=i32, device=self.dev)
-        self.cnt_in = torch.zeros((1,), dtype=i32, device=self.dev)
-        self.step_u1 = torch.full((F,), cfg.u + 1, dtype=i32, device=self.dev)
+        # the noise pass's list: active blocks of active frames + every block of inactive frames
+        self.ids_noise = torch.zeros((F * cfg.hb[0] ** 2,), dtype=i32, device=self.dev)
+        self.cnt_noise = torch.zeros((1,), dtype=i32, device=self.dev)
         self.zt = self.d["x0"].clone()
         # persistent buffers (R-17): pre-filled with the cache once (the full step's job); the conv
         # epilogue then writes only listed blocks, i.e. the feature-level scatter is fused
@@ -188,9 +188,9 @@ class RefinementStep:
         for (h, c) in cfg.levels:
             nb = int(ops.load().sphinx_conv_workspace_size(F, h, h, c, c, b)) if self.cuda else 0
             self.ws.append(torch.zeros(max(nb, 256), dtype=u8, device=self.dev))
-        # launches per step (single rank): mask 2 + compaction 1 + edge plans + noise 2 + convs + scatter 1
+        # launches per step (single rank): mask 2 + compaction 1 + edge plans + noise 1 + convs + scatter 1
         n_edge = sum(1 for (h, _) in cfg.levels if h % b)
-        self.launches_per_step = 2 + 1 + n_edge + 2 + L * cfg.convs_per_level + 1
+        self.launches_per_step = 2 + 1 + n_edge + 1 + L * cfg.convs_per_level + 1
         self.conv_events = None
         self.comm = None
         if world > 1:
@@ -267,17 +267,18 @@ class RefinementStep:
         ops.sphinx_compact_blocks_batch(
             [dict(block_mask=self.masks[l], start_step=kk, step_u=cfg.u, select=ops.SELECT_ACTIVE,
                   block_ids=self.ids[l], count=self.cnt[l]) for l in range(L)] +
-            [dict(block_mask=None, start_step=kk, step_u=cfg.u, select=ops.SELECT_INACTIVE_FRAMES,
-                  block_ids=self.ids_in, count=self.cnt_in, shape=tuple(self.masks[0].shape))])
+            [dict(block_mask=self.masks[0], start_step=kk, step_u=cfg.u, select=ops.SELECT_NOISE,
+                  block_ids=self.ids_noise, count=self.cnt_noise)])
         # edge-class plans of the ragged levels right after compaction, so every conv of the step
         # reuses its level's plan and may start before its predecessor ends
         for l, (h, c) in enumerate(cfg.levels):
             if h % cfg.b:
                 ops.sphinx_conv_edge_plan(self.ids[l], self.cnt[l], cfg.n_frames, h, h, cfg.b, c,
                                           workspace=self.ws[l])
-        ops.sphinx_noise_inject(d["x0"], d["eps"], self.zt, cfg.b, self.ids[0], self.cnt[0], kk, d["abar"])
-        ops.sphinx_noise_inject(d["x0"], d["eps"], self.zt, cfg.b, self.ids_in, self.cnt_in, self.step_u1,
-                                d["abar"])
+        # Alg1 line 12 (active latent blocks noised to their start step k) and line 19 (inactive
+        # frames resampled to u+1) in one pass over the NOISE list
+        ops.sphinx_noise_inject_step(d["x0"], d["eps"], self.zt, cfg.b, self.ids_noise, self.cnt_noise, kk, cfg.u,
+                                     d["abar"])
         for l in range(L):
             src = d[f"feat{l}"]
             for j in range(cfg.convs_per_level):

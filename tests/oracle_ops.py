@@ -9,7 +9,7 @@ import torch
 import oracle
 import synthetic as syn
 
-SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL = 0, 1, 2
+SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL, SELECT_NOISE = 0, 1, 2, 3
 
 
 def _np(t):
@@ -57,6 +57,12 @@ def sphinx_noise_inject(x0, eps, x_t, b, ids, cnt, step, abar):
     n = int(cnt.item())
     z = oracle.noise(_np(x0), _np(eps), _np(x_t).copy(), b, _np(ids)[:n], _np(step), _np(abar))
     x_t.copy_(torch.from_numpy(z.astype(np.float32)))
+
+
+def sphinx_noise_inject_step(x0, eps, x_t, b, ids, cnt, start_step, u, abar):
+    k = _np(start_step)
+    step = np.where((k >= 0) & (k <= u), k, np.where(k > u, u + 1, -1)).astype(np.int32)
+    sphinx_noise_inject(x0, eps, x_t, b, ids, cnt, torch.from_numpy(step), abar)
 
 
 def sphinx_sparse_conv3x3(x, w, bias, y, b, ids, cnt, **kw):

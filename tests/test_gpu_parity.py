@@ -218,8 +218,11 @@ def test_compact_vs_oracle(sphinx):
             m = (rg.random((n, hb, wb)) < dens).astype(np.uint8)
             k = rg.integers(-1, 45, size=n).astype(np.int32)
             for u in (0, 25, 49):
-                for sel in (0, 1, 2):
-                    if sel == 0:
+                for sel in (0, 1, 2, 3):
+                    if sel == 3:  # NOISE = ACTIVE | INACTIVE_FRAMES
+                        _, _, got = gpu_compact(sphinx, m, k, u, sel)
+                        assert np.array_equal(got, oracle.compact(m, k, u, sel))
+                    elif sel == 0:
                         for kk in (k, None):
                             _, _, got = gpu_compact(sphinx, m, kk, u, sel)
                             assert np.array_equal(got, oracle.compact(m, kk, u, sel))
@@ -259,6 +262,33 @@ def test_noise_vs_oracle(sphinx, shape, b):
     sphinx.sphinx_noise_inject(inplace, T(eps), inplace, b, g_ids, g_cnt, T(step), T(abar))
     want2 = oracle.noise(x0, eps, x0, b, ids, step, abar)
     assert np.all(np.abs(inplace.cpu().numpy() - want2) <= 1e-6 * scale + 1e-30)
+
+
+@pytest.mark.parametrize("shape,b", [((21, 72, 72, 4), 8), ((5, 20, 13, 8), 4)])
+def test_noise_step_fused_vs_oracle(sphinx, shape, b):
+    """sphinx_noise_inject_step over a SELECT_NOISE list == Alg1 line 12 (active blocks at their
+    start step k) and line 19 (inactive frames at u+1) in one pass; conditioning frames (k = -1)
+    untouched; within 1e-6 of |a x0| + |s eps| (R-3)."""
+    n, h, w, c = shape
+    hb, wb = -(-h // b), -(-w // b)
+    rg = syn.rng("gpu-noise-step", shape)
+    m = (rg.random((n, hb, wb)) < 0.4).astype(np.uint8)
+    k = rg.integers(-1, 45, size=n).astype(np.int32)
+    u = 25
+    abar = syn.abar_cosine(50)
+    x0, eps, xt = (syn.latents_f32(shape, f"gns{j}") for j in range(3))
+    step = np.where((k >= 0) & (k <= u), k, np.where(k > u, u + 1, -1)).astype(np.int32)
+    want = oracle.noise(x0, eps, xt, b, oracle.compact(m, k, u, oracle.SELECT_NOISE), step, abar)
+    g_ids, g_cnt, _ = gpu_compact(sphinx, m, k, u, 3)
+    out = T(xt)
+    sphinx.sphinx_noise_inject_step(T(x0), T(eps), out, b, g_ids, g_cnt, T(k), u, T(abar))
+    got = out.cpu().numpy()
+    touched = want != xt.astype(np.float64)
+    assert touched.any() and np.array_equal(got[~touched], xt[~touched])
+    uu = np.clip(step, 0, 50)
+    a = np.sqrt(abar[uu].astype(np.float64))[:, None, None, None]
+    s_ = np.sqrt(1.0 - abar[uu].astype(np.float64))[:, None, None, None]
+    assert np.all(np.abs(got - want) <= 1e-6 * (np.abs(a * x0) + np.abs(s_ * eps)) + 1e-30)
 
 
 # ----------------------------------------------------------------- step 4

@@ -70,8 +70,8 @@ def test_step_masks_ids_start_steps_exact(step_run):
         assert np.array_equal(st.ids[l][:c].cpu().numpy(), ids)
     assert np.array_equal(st.counts.cpu().numpy(), counts)
     assert np.array_equal(st.k.cpu().numpy(), k)
-    inact = oracle.compact(None, k, cfg.u, oracle.SELECT_INACTIVE_FRAMES, shape=masks[0].shape)
-    assert np.array_equal(st.ids_in[:int(st.cnt_in.item())].cpu().numpy(), inact)
+    noise = oracle.compact(masks[0], k, cfg.u, oracle.SELECT_NOISE)
+    assert np.array_equal(st.ids_noise[:int(st.cnt_noise.item())].cpu().numpy(), noise)
     if name == "configs3":  # the mixed densities reach the batch (8 requests, 5..75% means)
         d0 = masks[0].reshape(8, -1).mean(1)
         assert d0.min() < 0.12 and d0.max() > 0.6

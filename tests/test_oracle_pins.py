@@ -262,6 +262,8 @@ def test_compact_brute_force_and_selections():
         assert np.array_equal(inact, np.flatnonzero(np.repeat(k > u, hb * wb)))
         allb = oracle.compact(None, k, u, oracle.SELECT_ALL, shape=(n, hb, wb))
         assert np.array_equal(allb, np.flatnonzero(np.repeat(k >= 0, hb * wb)))
+        noise = oracle.compact(m, k, u, oracle.SELECT_NOISE)               # lines 12 + 19 together
+        assert np.array_equal(noise, np.union1d(want, np.flatnonzero(np.repeat(k > u, hb * wb))))
     m = np.ones((3, 5, 5), np.uint8)
     assert np.array_equal(oracle.compact(m), np.arange(75))                 # density 1 -> identity
     assert len(oracle.compact(0 * m)) == 0                                  # density 0 -> empty
