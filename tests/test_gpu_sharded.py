@@ -80,6 +80,14 @@ def test_sharded_step_matches_single_rank_on_gpu(sphinx, world):
     ref.run()
     ref.run()
     want, want_lat, _ = _outs(ref)
+    # A2[l] = sum |W2| * |y1| (fp32, per output element): the scale of the conv bar of the level's
+    # second conv, whose input y1 is the single-rank step's first-conv output
+    import torch.nn.functional as F_
+    a2 = []
+    for l in range(cfg.L):
+        y1 = ref.y[l].float().abs().permute(0, 3, 1, 2)
+        w2 = ref.d[f"w{l}1"].float().abs().permute(0, 3, 1, 2)
+        a2.append(F_.conv2d(y1, w2, padding=1).permute(0, 2, 3, 1).cpu().numpy())
     del ref
     torch.cuda.empty_cache()
     ctx = mp.get_context("spawn")
@@ -106,10 +114,13 @@ def test_sharded_step_matches_single_rank_on_gpu(sphinx, world):
             w = want[l][n].view(np.uint16)
             gf = (g.astype(np.uint32) << 16).view(np.float32)
             wf = (w.astype(np.uint32) << 16).view(np.float32)
-            # both are within the conv bar of the exact value: differences are rare and small
+            # Each output is within the conv bar (1e-3 * A2 + 1e-6) of the exact conv of its own
+            # input; the two inputs (first-conv outputs, bf16) differ by at most one bf16 ulp
+            # (<= 2^-7 |y1|) per element, which moves the exact output by at most 2^-7 * A2.
+            # Differences compound through the two convs, so they are not rare at 1280 channels.
             d = np.abs(gf - wf)
-            assert d.max() <= 2.0 ** -6 * np.abs(wf).max() + 1e-6, (n, l)
-            assert (d > 0).mean() < 0.05, (n, l)
+            bar = 2e-3 * a2[l][n] + 2.0 ** -7 * a2[l][n] + 2e-6
+            assert (d <= bar).all(), (n, l, float((d / bar).max()), float((d > 0).mean()))
         assert np.array_equal(got[cfg.L], comp[cfg.L])
         assert np.array_equal(got[cfg.L].view(np.uint32), want_lat[n].view(np.uint32)), n
 
