@@ -49,8 +49,10 @@ class StepConfig:
     pixels per level-0 cell), UNet `levels` [(H_l, C_l)], b x b blocks, step u."""
 
     def __init__(self, hp=576, f=8, b=8, levels=((72, 320), (36, 640), (18, 1280)), convs_per_level=2,
-                 frames_per_request=21, n_requests=1, u=25, gamma=0.5, tau_o=0.5, c_lat=4):
+                 frames_per_request=21, n_requests=1, u=25, gamma=0.5, tau_o=0.5, c_lat=4,
+                 interleave_levels=True):
         self.hp, self.f, self.b = hp, f, b
+        self.interleave_levels = interleave_levels  # conv launch order (RefinementStep.conv_order)
         self.levels = [tuple(x) for x in levels]
         self.convs_per_level = convs_per_level
         self.frames_per_request, self.n_requests = frames_per_request, n_requests
@@ -279,25 +281,42 @@ class RefinementStep:
         # frames resampled to u+1) in one pass over the NOISE list
         ops.sphinx_noise_inject_step(d["x0"], d["eps"], self.zt, cfg.b, self.ids_noise, self.cnt_noise, kk, cfg.u,
                                      d["abar"])
-        for l in range(L):
-            src = d[f"feat{l}"]
-            for j in range(cfg.convs_per_level):
-                dst = self.y[l] if j % 2 == 0 else self.z[l]
-                if conv_events is not None:
-                    conv_events[l][j][0].record()
-                ops.sphinx_sparse_conv3x3(src, d[f"w{l}{j}"], d[f"b{l}{j}"], dst, cfg.b, self.ids[l], self.cnt[l],
-                                          workspace=self.ws[l], reuse_plan=True, list_ready=True,
-                                          input_ready=j == 0)  # a level's input features are step inputs
-                if conv_events is not None:
-                    conv_events[l][j][1].record()
-                src = dst
-            if l == 0:
-                # step 5 at latent resolution: refined latent blocks from this step, the latent
-                # cache of the last full step everywhere else (P:352 spatial latent reuse)
-                ops.sphinx_scatter_cached(self.zt, d["lat_cache"], self.lat_out, cfg.b, block_mask=self.masks[0],
-                                          start_step=kk, step_u=cfg.u)
-            if self.world > 1:
-                self._exchange_level(l, src)
+        # step 5 at latent resolution: refined latent blocks from this step, the latent cache of
+        # the last full step everywhere else (P:352 spatial latent reuse); depends on the noise
+        # pass only, so it runs before the convs and does not drain the conv chain
+        ops.sphinx_scatter_cached(self.zt, d["lat_cache"], self.lat_out, cfg.b, block_mask=self.masks[0],
+                                  start_step=kk, step_u=cfg.u)
+        src = [d[f"feat{l}"] for l in range(L)]
+        prev = None
+        for (l, j) in self.conv_order():
+            dst = self.y[l] if j % 2 == 0 else self.z[l]
+            if conv_events is not None:
+                conv_events[l][j][0].record()
+            # INPUT_READY unless the input was written by the kernel right before: a level's input
+            # features are step inputs, and with several levels conv j's input (conv j-1's output)
+            # is at least two launches back in conv_order(), so the loads and MMAs may overlap the
+            # preceding conv's tail
+            ops.sphinx_sparse_conv3x3(src[l], d[f"w{l}{j}"], d[f"b{l}{j}"], dst, cfg.b, self.ids[l], self.cnt[l],
+                                      workspace=self.ws[l], reuse_plan=True, list_ready=True,
+                                      input_ready=(j == 0 or prev != (l, j - 1)))
+            if conv_events is not None:
+                conv_events[l][j][1].record()
+            src[l] = dst
+            prev = (l, j)
+            if self.world > 1 and j == cfg.convs_per_level - 1:
+                self._exchange_level(l, dst)
+
+    def conv_order(self):
+        """Launch order of the step's convs (level l, index j): anti-diagonals d = l + j, levels
+        descending within one, e.g. (0,0) (1,0) (0,1) (2,0) (1,1) (2,1).  Consecutive convs are
+        of different levels, so no conv's input was written by the kernel right before it: each
+        conv is launched with INPUT_READY and its main loop fills its predecessor's tail (the
+        predecessor does not feed it).  A single level runs in order (its convs are dependent)."""
+        L, C = self.cfg.L, self.cfg.convs_per_level
+        if not self.cfg.interleave_levels:  # level by level (A/B reference)
+            return [(l, j) for l in range(L) for j in range(C)]
+        order = [(l, dd - l) for dd in range(L + C - 1) for l in range(L - 1, -1, -1) if 0 <= dd - l < C]
+        return order
 
     def out(self, l):
         """The level-l output map of the step (the last conv's persistent buffer)."""
