@@ -694,6 +694,12 @@ def run_gpu(args):
 
     if rank == 0:
         cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(batch, cfg, bounded_s=args.cpu_seconds)
+        if cpu is not None:
+            fl_cfg = {name: flops}
+            for k in ("configs2", "configs4"):
+                if extras.get(k):
+                    fl_cfg[k] = extras[k]["value_tflops"] * 1e12 * extras[k]["ms_per_step"] * 1e-3
+            cpu["oracle_configs"] = oracle_record(fl_cfg, cpu["value"] * 1e12)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": reps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_all, 5), "higher_is_better": True,
@@ -945,6 +951,71 @@ def cpu_baseline(batch, cfg, bounded_s=15.0):
             "seconds": round(t, 2),
             "sample": f"the {cfg.n_frames}-frame batch: full mask/start-step/compaction/noise/scatter, one conv on "
                       f"the first {nb} active blocks of each level (fp64 direct conv, OpenMP {cores} threads)"}
+
+
+def oracle_record(conv_flops_by_config, rate_all_cores, seconds_1core=8.0):
+    """SURVEY 8(d) "oracle timing beside it": the oracle as it stands on this box's host cores.
+    configs[0] (1 frame 16x16x32, b 4, 4 of 16 blocks): the whole path on one thread.
+    configs[1] (1 frame 72x72x320, b 8): the conv at 10% (8 blocks) on one thread and on all
+    cores (OpenMP over blocks, 16 per chunk: 8 blocks keep one thread busy).
+    configs[2..4]: their full steps' conv FLOPs (from the GPU run) at the one-thread rate and at
+    rate_all_cores (the cpu_baseline sample's measured all-core rate, FLOP/s), labelled
+    extrapolated (the full runs are minutes to hours of CPU time)."""
+    import oracle
+    cores = os.cpu_count()
+    out = {"cores": cores, "kind": "oracle"}
+    # configs[0], everything on one thread (the conv's OpenMP pinned to 1)
+    n, hp, b, c, S, u = 1, 16, 4, 32, 50, 25
+    O, _ = syn.opacity_maps(n, hp, hp, b, [0.25], "scattered", tag="smoke")
+    q, c0, c1, t = (np.float32([61.75]), np.float32([60]), np.float32([70]), np.float32([0.25]))
+    lg = oracle.make_klogic(syn.SPEC_KLOGIC["thr"], syn.SPEC_KLOGIC["steps"])
+    abar = syn.abar_cosine(S)
+    x0 = syn.latents_f32((n, hp, hp, c), "smoke-x0")
+    eps = syn.latents_f32((n, hp, hp, c), "smoke-eps")
+    w = syn.weights_bf16(c, c, "smoke")
+    bias = syn.bias_f32(c, "smoke")
+    cache = syn.latents_f32((n, hp, hp, c), "smoke-cache")
+    t0 = time.perf_counter()
+    om, _ = oracle.block_mask(O, None, None, 0.5, 1, b, 1)
+    ok = oracle.start_step(q, c0, c1, t, 0.5, [lg])
+    oids = oracle.compact(om[0], ok, u)
+    xt = oracle.noise(x0, eps, x0, b, oids, ok, abar).astype(np.float32)
+    xbits = syn.to_bf16_bits(xt)
+    oy, _ = oracle.conv3x3_blocks(xbits, w, bias, b, oids, n_threads=1, y_init=cache.astype(np.float64))
+    oracle.scatter(oy.astype(np.float32), cache, b, mask=om[0], k=ok, u=u)
+    t_c0 = time.perf_counter() - t0
+    out["configs0_path_1thread_s"] = round(t_c0, 5)
+    out["configs0_conv_flops"] = int(len(oids) * b * b * 2 * 9 * c * c)
+    # configs[1]: 8 of 81 blocks of one 72x72x320 frame
+    h, c = 72, 320
+    x = syn.features_bf16((1, h, h, c), "sweep")
+    w = syn.weights_bf16(c, c, "sweep")
+    rg = syn.rng("sweep-mask", 1, 0.10)
+    ids = np.flatnonzero(syn.choose_cells(rg, 9, 9, 8, "clustered").ravel()).astype(np.int32)
+    fl = len(ids) * 64 * 2 * 9 * c * c
+    t0 = time.perf_counter()
+    oracle.conv3x3_blocks(x, w, None, 8, ids[:1], n_threads=1)
+    t1 = time.perf_counter() - t0
+    nb1 = int(max(1, min(len(ids), seconds_1core / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.conv3x3_blocks(x, w, None, 8, ids[:nb1], n_threads=1)
+    t1 = time.perf_counter() - t0
+    rate1 = nb1 * 64 * 2 * 9 * c * c / t1
+    t0 = time.perf_counter()
+    oracle.conv3x3_blocks(x, w, None, 8, ids, n_threads=cores)  # (also restores the thread count)
+    tall = time.perf_counter() - t0
+    out["configs1_conv_10pct"] = {"blocks": int(len(ids)), "gflop": round(fl / 1e9, 4),
+                                  "s_1thread": round(t1 * len(ids) / nb1, 4),
+                                  "s_1thread_note": f"measured on {nb1} of {len(ids)} blocks, scaled by block count",
+                                  "s_all_cores": round(tall, 4),
+                                  "gflops_1thread": round(rate1 / 1e9, 4)}
+    out["extrapolated"] = {k: {"conv_gflop": round(v / 1e9, 1), "s_all_cores": round(v / rate_all_cores, 1),
+                               "s_1thread": round(v / rate1, 1)}
+                           for k, v in conv_flops_by_config.items()}
+    out["extrapolated_note"] = ("full-step conv FLOPs from the GPU run / the measured fp64 direct-conv rate: one "
+                                "thread (configs[1] above), all cores (the cpu_baseline sample's rate, "
+                                f"{rate_all_cores / 1e9:.2f} GFLOP/s, mask/compaction/noise/scatter included)")
+    return out
 
 
 def run_reference(args):
