@@ -360,7 +360,7 @@ def memory_kernels(torch, st, reps=10):
     ms = timed(lambda: sp.sphinx_ddim_step(st.zt, d["x0"], zo, cfg.b, st.ids[0], st.cnt[0], cfg.u, abar_h))
     row("ddim_step (NEXT-1)", ms, cnt * 64 * cfg.c_lat * 12, "12 B per active latent element (z, x0_hat in; z' out)")
     nu = min(n, 21)
-    rgb = torch.rand((nu, hp, hp, 3), device=dev, dtype=torch.float32)
+    rgb = torch.from_numpy(syn.rgb_frames(nu, hp, hp, "bench")).to(dev)  # textured frames with flat patches
     U = torch.empty((nu, hp, hp), device=dev, dtype=torch.float32)
     tau = torch.empty((nu,), device=dev, dtype=torch.float32)
     ms = timed(lambda: sp.sphinx_uncertainty_map(rgb, U, tau))

@@ -68,9 +68,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                   \
     if (p.trace) g_conv_trace[blockIdx.x * 24 + (k)] = (v); \
   } while (0)
+// accumulate the time spent in `stmt` (a barrier wait) into slot k (20: operand full, 21: accumulator
+// empty, 22: A-resident region full, 23: epilogue waiting for the accumulator)
+// (only with dbg bit 8: the global read-modify-write per wait perturbs the loop it measures)
+#define TWAIT(k, stmt)                                                                \
+  do {                                                                                \
+    const bool _on = p.trace && (p.dbg & 8);                                          \
+    const unsigned long long _t0 = _on ? gtimer() : 0ull;                             \
+    stmt;                                                                             \
+    if (_on) g_conv_trace[blockIdx.x * 24 + (k)] += gtimer() - _t0;                   \
+  } while (0)
 #else
 #define CONV_TRACE(k, v) \
   do {                   \
+  } while (0)
+#define TWAIT(k, stmt) \
+  do {                 \
+    stmt;              \
   } while (0)
 #endif
 
@@ -158,7 +172,7 @@ struct ConvCfg {
   static constexpr int kBarBytes = 512 + kBM * 8 + 2 * 256 * 4 + (NORM ? 8 * 8 * 20 * 4 + 512 : 0);
   static constexpr int kMaxSmem = 232448;          // 227 KB opt-in per CTA
   static constexpr int kAvail = kMaxSmem - 1024 - kBarBytes;
-  // per-tap mode: + the TMA-store staging of the epilogue (2 halves x 2 buffers x 128 rows x 64 B)
+  // per-tap mode: + the TMA-store staging of the epilogue (8 warps x 2 buffers x 32 rows x 64 B)
   static constexpr int kStoreBytes = HALO ? 0 : 2 * 2 * kBM * 64;
   static constexpr int kStagesFit = (kAvail - kStoreBytes) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
@@ -260,13 +274,15 @@ __device__ __forceinline__ void store_row_chunk(const ConvParams& p, size_t pix,
                                                 const float* sb) {
   // sb: this chunk's 32 bias values in shared memory (zero-padded): broadcast LDS.128, no
   // predicated global loads queued behind the previous chunk's stores
+  if (sb) {  // (nullptr: bias already added)
 #pragma unroll
-  for (int i = 0; i < 32; i += 4) {
-    const float4 b4 = *reinterpret_cast<const float4*>(sb + i);
-    v[i] += b4.x;
-    v[i + 1] += b4.y;
-    v[i + 2] += b4.z;
-    v[i + 3] += b4.w;
+    for (int i = 0; i < 32; i += 4) {
+      const float4 b4 = *reinterpret_cast<const float4*>(sb + i);
+      v[i] += b4.x;
+      v[i + 1] += b4.y;
+      v[i + 2] += b4.z;
+      v[i + 3] += b4.w;
+    }
   }
   if (p.res) add_residual<32>(p, pix, co, v);
 #ifdef SPHINX_TRACE
@@ -398,29 +414,23 @@ __device__ __forceinline__ HaloTile halo_tile(int mt, int rank, int nF, int nB, 
   return g;
 }
 
-// Per-tap mode, bf16 y: one 32-column chunk of the tile (this thread = tile row `row`) -> bias
-// (+ residual) -> bf16 -> the half's staging buffer (row-major 64 B rows, SW64 swizzle), then one
-// TMA tensor store per listed block of the tile (box {32 ch, BLK, BLK, 1}; out-of-image pixels
-// of edge blocks and channels beyond C_out are clipped by the TMA unit).  Rows are block-major,
-// so row r sits at byte r * 64 = (block, pixel) of the box layout.  Two buffers per half: the
-// issuing thread (row 0) waits until the store that last read a buffer has read it.
-template <int BLK, int BPT>
-__device__ __forceinline__ void stage_chunk_tma(const ConvParams& p, const CUtensorMap& tmY, uint8_t* buf,
-                                                int row, int half, size_t pix, bool valid, int co,
-                                                float (&v)[32], const float* sb, int j0, int count) {
-#pragma unroll
-  for (int i = 0; i < 32; i += 4) {
-    const float4 b4 = *reinterpret_cast<const float4*>(sb + i);
-    v[i] += b4.x;
-    v[i + 1] += b4.y;
-    v[i + 2] += b4.z;
-    v[i + 3] += b4.w;
-  }
+// Per-tap mode, bf16 y: one 32-column chunk of this WARP's 32 tile rows -> (bias already added,
+// + residual) -> bf16 -> the warp's own staging buffer (32 rows of 64 B, SW64 swizzle), then one
+// TMA tensor store per block quarter the warp covers (box {32 ch, BLK, 4, 1}: b = 8 -> rows
+// [4(q&1), 4(q&1)+4) of block q/2; b = 4 -> two whole 4x4 blocks).  Out-of-image pixels of edge
+// blocks and channels beyond C_out are clipped by the TMA unit; a short tile's padding blocks are
+// skipped.  Warp-local: no barrier with the other epilogue warps.  Two buffers per warp: lane 0
+// waits until the store that last read a buffer has read it.  Row r of the warp sits at byte
+// r * 64 = (y, x) of the box layout (tile rows are block-major).
+template <int BLK>
+__device__ __forceinline__ void stage_chunk_tma_warp(const ConvParams& p, const CUtensorMap& tmY, uint8_t* buf,
+                                                     int lane, int q, size_t pix, bool valid, int co,
+                                                     float (&v)[32], int bn, int by, int bx, bool listed) {
   if (p.res && valid) add_residual<32>(p, pix, co, v);
-  if (row == 0) bulk_wait_group_read<1>();
-  named_bar_sync(4 + half, 128);
-  const uint32_t base = smem_u32(buf) + (uint32_t)row * 64u;
-  const uint32_t sw = ((uint32_t)row >> 1) & 3u;
+  if (lane == 0) bulk_wait_group_read<1>();
+  __syncwarp();
+  const uint32_t base = smem_u32(buf) + (uint32_t)lane * 64u;
+  const uint32_t sw = ((uint32_t)lane >> 1) & 3u;
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     uint4 pk;
@@ -435,15 +445,20 @@ __device__ __forceinline__ void stage_chunk_tma(const ConvParams& p, const CUten
     sts128(base + (((uint32_t)g ^ sw) << 4), pk);
   }
   fence_proxy_async_shared();
-  named_bar_sync(4 + half, 128);
-  if (row == 0) {
-#pragma unroll 1
-    for (int bi = 0; bi < BPT; ++bi) {
-      const int j = j0 + bi;
-      if (j >= count) break;  // a short last tile's padding blocks are computed, never stored
-      int n, by, bx;
-      decode_block(__ldg(p.ids + j), p.hb, p.wb, n, by, bx);
-      tma_store_4d(&tmY, buf + bi * (BLK * BLK * 64), co, bx * BLK, by * BLK, n);
+  __syncwarp();
+  // block coordinates of the (up to two) blocks of this warp's rows: lane 0's and lane 16's
+  const int n1 = __shfl_sync(0xffffffffu, bn, 16), by1 = __shfl_sync(0xffffffffu, by, 16),
+            bx1 = __shfl_sync(0xffffffffu, bx, 16);
+  const bool l1 = __shfl_sync(0xffffffffu, listed ? 1 : 0, 16) != 0;
+#ifdef SPHINX_TRACE
+  if (p.dbg & 1) return;  // timing probe: stage, but issue no store
+#endif
+  if (lane == 0) {
+    if constexpr (BLK == 8) {
+      if (listed) tma_store_4d(&tmY, buf, co, bx * BLK, by * BLK + (q & 1) * 4, bn);
+    } else {
+      if (listed) tma_store_4d(&tmY, buf, co, bx * BLK, by * BLK, bn);
+      if (l1) tma_store_4d(&tmY, buf + 1024, co, bx1 * BLK, by1 * BLK, n1);
     }
     bulk_commit_group();
   }
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + (HALO ? Cfg::kARing : S * kStageA);
-  uint8_t* s_store = smem + Cfg::kRingBytes;  // per-tap mode: [half][buf][128 rows x 64 B], SW64
+  uint8_t* s_store = smem + Cfg::kRingBytes;  // per-tap mode: [warp][buf][32 rows x 64 B], SW64
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes + Cfg::kStoreBytes);
   uint64_t* empty = full + NB;
   uint64_t* tfull = empty + NB;
@@ -879,11 +894,11 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         const int ks0 = U.sk * ksteps / U.ns, ks1 = (U.sk + 1) * ksteps / U.ns;
         const bool nar = U.t % p.n_tiles_n == p.n_tiles_n - 1 && p.n_last < BN;
         const uint32_t idesc_t = nar ? idesc_bf16_f32(kBM * CG, p.n_last) : idesc;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        TWAIT(21, mbar_wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int ks = ks0; ks < ks1; ++ks) {
-          mbar_wait(&full[stage], phase);
+          TWAIT(20, mbar_wait(&full[stage], phase));
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * kStageA);
           const uint32_t b_addr = smem_u32(sB + stage * Cfg::kStageB);
@@ -922,16 +937,9 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
     int st_cnt = 0;                      // staged chunks (TMA-store path): buffer = st_cnt & 1
     int acc = 0;
     uint32_t acc_phase = 0;
-    SegIter it = it0;
-    Seg sg;
-    for (; it.get(sg); it.next(sg)) {
-      const int t = sg.t, sk = sg.sk, ns = sg.ns;
-      const Unit U{sg.t, sg.sk, sg.ns, sg.slot};
-      const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
-      // tile row -> (block, pixel): per-tap mode rows are block-major (b^2 rows per block);
-      // halo mode rows are [line q][block][8 px along the line] (group = q * bpt + block)
-      int bi, ry, rx, j, nblk;
-      const int32_t* lst;
+    // tile row -> (block, pixel): per-tap mode rows are block-major (b^2 rows per block);
+    // halo mode rows are [line q][block][8 px along the line] (group = q * bpt + block)
+    auto tile_geom = [&](int mt, int& bi, int& ry, int& rx, int& j, int& nblk, const int32_t*& lst) {
       if constexpr (HALO) {
         const HaloTile g = halo_tile<CG>(mt, rank, nF, nB, list, nR, p);
         bi = (row >> 3) % g.bpt;
@@ -949,31 +957,75 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         nblk = count;
         lst = p.ids;
       }
+    };
+    // One tile ahead: the next tile's block id and (per-tap unsplit tiles) bias columns are loaded
+    // while this tile drains, so their global-load latency is off the epilogue's critical path.
+    int pf_id = 0;
+    float pf_b[4] = {0.f, 0.f, 0.f, 0.f};
+    auto prefetch = [&](const Seg& g) {
+      const int mt = g.t / p.n_tiles_n, nt = g.t - mt * p.n_tiles_n;
+      int bi, ry, rx, j, nblk;
+      const int32_t* lst;
+      tile_geom(mt, bi, ry, rx, j, nblk, lst);
+      pf_id = (bi < (HALO ? 8 : BPT) && j < nblk) ? __ldg(lst + j) : 0;
+      if (!HALO && g.ns == 1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = half * 32 + k * 64 + lane, co = nt * BN + c;
+          pf_b[k] = (p.bias && c < BN && co < p.cout) ? __ldg(p.bias + co) : 0.f;
+        }
+      }
+    };
+    SegIter it = it0;
+    Seg sg;
+    bool have = it.get(sg);
+    if (have) prefetch(sg);
+    while (have) {
+      const int t = sg.t, sk = sg.sk, ns = sg.ns;
+      const Unit U{sg.t, sg.sk, sg.ns, sg.slot};
+      const int mt = t / p.n_tiles_n, nt = t - mt * p.n_tiles_n;
+      const int my_id = pf_id;
+      float b_reg[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b_reg[k] = pf_b[k];
+      SegIter nit = it;
+      nit.next(sg);
+      Seg nsg;
+      const bool nhave = nit.get(nsg);
+      if (nhave) prefetch(nsg);
+      int bi, ry, rx, j, nblk;
+      const int32_t* lst;
+      tile_geom(mt, bi, ry, rx, j, nblk, lst);
       bool valid = (bi < (HALO ? 8 : BPT)) && (j < nblk);
       size_t pix = 0;
+      int n = 0, by = 0, bx = 0;
       if (valid) {
-        int n, by, bx;
-        decode_block(__ldg(lst + j), p.hb, p.wb, n, by, bx);
+        decode_block(my_id, p.hb, p.wb, n, by, bx);
         const int yy = by * BLK + ry, xx = bx * BLK + rx;
         valid = (yy < p.h) && (xx < p.w);
         pix = (((size_t)n * p.h + yy) * p.w + xx) * p.cout;
       }
+      const bool listed = (bi < (HALO ? 8 : BPT)) && (j < nblk);
       // split-K part: column-major [BN][128] (lanes = consecutive rows: coalesced)
       float* part = nullptr;
       if (ns > 1) part = p.ws_part + ((size_t)(U.slot * ns + sk) * CG + rank) * kBM * BN + row;
       // stream-K part: column-major [BN][128] slot of this cluster (coalesced per column)
       float* skpart = (sg.role == kPart)
                           ? p.ws_part + ((size_t)cluster_id * CG + rank) * kBM * BN + row : nullptr;
-      {
-        // this tile's bias slice -> s_bias[acc] (the slot was last read two tiles ago, before
-        // the previous tile's barrier below)
+      // per-tap unsplit tiles: each warp holds its chunks' bias in registers (lane l: column
+      // c0 + l of chunk k, c0 = half*32 + k*64) -- no barrier across the epilogue warps
+      const bool regbias = !HALO && ns == 1;
+      if (!regbias) {
+        // this tile's bias slice -> s_bias[acc] (the slot was last read by a tile that used it
+        // two or more tiles ago, before a barrier 1 every thread has passed since)
         float* sb = s_bias + acc * 256;
         const int nb = p.bias ? min(BN, p.cout - nt * BN) : 0;
         for (int c = erow; c < BN; c += kEpiT) sb[c] = c < nb ? __ldg(p.bias + nt * BN + c) : 0.f;
         named_bar_sync(1, kEpiT);
       }
       const float* sbt = s_bias + acc * 256;
-      mbar_wait(&tfull[acc], acc_phase);
+      if (warp == 2 && lane == 0) TWAIT(23, mbar_wait(&tfull[acc], acc_phase));
+      else mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #ifdef SPHINX_TRACE
       if (warp == 2 && lane == 0) {
@@ -1029,12 +1081,47 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
         }
         if (row == 0) cnt[0] = 0;  // leave the counter zeroed for the next launch
        }
+      } else if (regbias) {
+        if constexpr (!HALO) {
+          // per-tap unsplit tile: double-buffered TMEM drain (chunk k+1's tcgen05.ld is in flight
+          // while chunk k is converted and stored), bias from registers, and with bf16 y a
+          // warp-local staged TMA store per chunk
+          int width = (nt == p.n_tiles_n - 1 && p.n_last < BN) ? p.n_last : BN;
+#ifdef SPHINX_TRACE
+          if (p.dbg & 4) width = 0;  // timing probe: release the accumulator without draining it
+#endif
+          uint8_t* wbuf = s_store + (size_t)((half * 4 + q) * 2) * 2048;
+          uint32_t ra[32], rb[32];
+          const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+          if (half * 32 < width) {
+            tmem_ld_32x32b_x32(tbase + (uint32_t)(half * 32), ra);
+            tc_wait_ld_dep(ra);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int c0 = half * 32 + k * 64;
+            if (c0 >= width) break;
+            uint32_t(&cur)[32] = (k & 1) ? rb : ra;
+            uint32_t(&nxt)[32] = (k & 1) ? ra : rb;
+            const bool more = c0 + 64 < width;
+            if (more) tmem_ld_32x32b_x32(tbase + (uint32_t)(c0 + 64), nxt);
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(cur[i]) + __shfl_sync(0xffffffffu, b_reg[k], i);
+            if (p.tma_y) {
+              stage_chunk_tma_warp<BLK>(p, tmY, wbuf + (st_cnt & 1) * 2048, lane, q, pix, valid, nt * BN + c0, v,
+                                        n, by, bx, listed);
+              ++st_cnt;
+            } else if (valid) {
+              store_row_chunk(p, pix, nt * BN + c0, v, nullptr);
+            }
+            if (more) tc_wait_ld_dep(nxt);
+          }
+        }
       } else {
         // a ragged last C_out tile only has p.n_last valid accumulator columns (the rest are
         // beyond C_out: never stored, so they need not be drained or parked either)
         const int width = (nt == p.n_tiles_n - 1 && p.n_last < BN) ? p.n_last : BN;
-        // per-tap mode, bf16 y: staged TMA stores (one 4-D box per block and 32-column chunk)
-        const bool staged = !HALO && p.tma_y && ns == 1 && sg.role != kPart;
         for (int c0 = half * 32; c0 < width; c0 += 32 * kHalves) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), r);
@@ -1046,19 +1133,6 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
             // split-K: park this split's fp32 partial (column-major, coalesced)
 #pragma unroll
             for (int i = 0; i < 32; ++i) __stcg(part + (size_t)(c0 + i) * kBM, __uint_as_float(r[i]));
-          } else if (staged) {
-            if constexpr (!HALO) {
-              // Row r of the tile is pixel (ry, rx) of block bi (block-major rows), i.e. byte r*64
-              // of the staging buffer is exactly where the box {32 ch, BLK, BLK, 1} of block bi
-              // expects it; the 16-B chunks are SW64-swizzled (chunk ^= (r >> 1) & 3) to match the
-              // tensor map and keep the warp's shared stores conflict-free.
-              float v[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-              stage_chunk_tma<BLK, BPT>(p, tmY, s_store + (half * 2 + (st_cnt & 1)) * (kBM * 64), row, half, pix,
-                              valid, nt * BN + c0, v, sbt + c0, mt * bpt_pair + rank * BPT, count);
-              ++st_cnt;
-            }
           } else if (valid) {
             float v[32];
 #pragma unroll
@@ -1184,10 +1258,13 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
           }
         }
       }
+      it = nit;
+      sg = nsg;
+      have = nhave;
     }
     // staged TMA stores: complete before the CTA exits (shared memory must outlive their reads)
     if constexpr (!HALO)
-      if (p.tma_y && row == 0) bulk_wait_group_all();
+      if (p.tma_y && lane == 0) bulk_wait_group_all();
   } else if constexpr (NORM) {
     if (warp >= kXWarp) {
       // ============ fused GroupNorm + SiLU (NEXT-3): transform warps 7..14, both CTAs ============
@@ -1502,7 +1579,17 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   PFN_encodeTiled_t enc = get_encode_tiled();
   if (!enc) return cuda_fail(cudaErrorNotSupported);
 
-  const int bn = pick_bn(c_out);
+  int bn = pick_bn(c_out);
+  // pointwise projections (K = C_in only: 5 K-steps per tile at C_in = 320) issue many short
+  // tiles; the 256-wide tile needs 1/3 fewer MMA instructions and tiles per output column than
+  // the 160-wide one, worth up to 1/15 padded columns (q|k|v 960 -> 1024: 23.3 vs 25.5 us, §6.9)
+  if (taps == 1 && bn != 256 && cdiv(c_out, 256) * 256 * 15 <= c_out * 16) bn = 256;
+#ifdef SPHINX_DEV_KNOBS
+  if (const char* env = getenv("SPHINX_BN")) {  // dev build A/B: force the C_out tile width
+    const int v = atoi(env);
+    if (v == 32 || v == 64 || v == 128 || v == 160 || v == 256) bn = v;
+  }
+#endif
   // CTA-pair (cta_group::2) unless the caller forces the 1-SM kernel: halves the weight traffic
   // per SM
   int cg = (flags & SPHINX_CONV_FORCE_CG1) ? 1 : 2;
@@ -1560,7 +1647,7 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     const cuuint64_t dims[4] = {(cuuint64_t)c_out, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
     const cuuint64_t strides[3] = {(cuuint64_t)c_out * 2, (cuuint64_t)w_ * c_out * 2,
                                    (cuuint64_t)h * w_ * c_out * 2};
-    const cuuint32_t box[4] = {32, (cuuint32_t)block, (cuuint32_t)block, 1};
+    const cuuint32_t box[4] = {32, (cuuint32_t)block, 4, 1};  // one warp's 32 rows (stage_chunk_tma_warp)
     const cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(&tb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, y, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -240,10 +240,20 @@ __global__ void __launch_bounds__(256) normalize_hist_kernel(float* U, int plane
   const float lo = __int_as_float(minmax[2 * n]), hi = __int_as_float(minmax[2 * n + 1]);
   const float range = hi - lo;
   float* u = U + (size_t)n * plane;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < plane; p += gridDim.x * blockDim.x) {
-    const float v = range > 0.0f ? 1.0f - (u[p] - lo) / range : 1.0f;  // normalise + invert
-    u[p] = v;
-    atomicAdd(&sh[u_bin(v)], 1);
+  // flat (blurry) regions put most pixels of a frame in a few bins: warp-aggregated increments
+  // (one shared atomic per distinct bin of the warp) instead of up to 32-way same-address ones
+  const int lane = threadIdx.x & 31;
+  for (int p0 = blockIdx.x * blockDim.x; p0 < plane; p0 += gridDim.x * blockDim.x) {
+    const int p = p0 + threadIdx.x;
+    const bool in = p < plane;
+    float v = 0.0f;
+    if (in) {
+      v = range > 0.0f ? 1.0f - (u[p] - lo) / range : 1.0f;  // normalise + invert
+      u[p] = v;
+    }
+    const int bin = in ? u_bin(v) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (in && lane == __ffs(peers) - 1) atomicAdd(&sh[bin], __popc(peers));
   }
   __syncthreads();
   if (sh[threadIdx.x]) atomicAdd(hist + 256 * n + threadIdx.x, sh[threadIdx.x]);

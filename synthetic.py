@@ -339,3 +339,21 @@ def make_batch(request_means, tag="r0", hp=576, f=8, b=8, levels=UNET_LEVELS, co
             batch[f"w{l}{j}"] = weights_bf16(c, c, f"w{l}{j}")
             batch[f"b{l}{j}"] = bias_f32(c, f"b{l}{j}")
     return batch
+
+
+def rgb_frames(n, h, w, tag):
+    """Regression-output-like RGB frames in [0,1] (NEXT-2 input): smooth gradients with sharp
+    texture everywhere except a few flat disc-shaped patches (the blurry regions Otsu separates)."""
+    rg = rng("gpu-rgb", tag, n, h, w)
+    yy, xx = np.mgrid[0:h, 0:w].astype(np.float32)
+    out = np.empty((n, h, w, 3), np.float32)
+    for i in range(n):
+        base = 0.5 + 0.3 * np.sin(yy / (7 + i)) * np.cos(xx / (11 + i))
+        tex = rg.random((h, w)).astype(np.float32) * 0.4
+        blur = np.zeros((h, w), bool)
+        for _ in range(3):
+            cy, cx, r = rg.integers(0, h), rg.integers(0, w), rg.integers(h // 10 + 2, h // 4 + 3)
+            blur |= (yy - cy) ** 2 + (xx - cx) ** 2 < r * r
+        img = np.where(blur, base, base + tex - 0.2)
+        out[i] = np.clip(np.stack([img, img * 0.9, img * 1.1], -1), 0, 1)
+    return out

@@ -506,19 +506,7 @@ def test_ddim_step_vs_oracle(sphinx, shape, b, u):
 
 def _rgb_frames(n, h, w, tag):
     """Synthetic regression frames: smooth gradients + sharp texture + flat (blurry) patches."""
-    rg = syn.rng("gpu-rgb", tag, n, h, w)
-    yy, xx = np.mgrid[0:h, 0:w].astype(np.float32)
-    out = np.empty((n, h, w, 3), np.float32)
-    for i in range(n):
-        base = 0.5 + 0.3 * np.sin(yy / (7 + i)) * np.cos(xx / (11 + i))
-        tex = rg.random((h, w)).astype(np.float32) * 0.4
-        blur = np.zeros((h, w), bool)
-        for _ in range(3):
-            cy, cx, r = rg.integers(0, h), rg.integers(0, w), rg.integers(h // 10 + 2, h // 4 + 3)
-            blur |= (yy - cy) ** 2 + (xx - cx) ** 2 < r * r
-        img = np.where(blur, base, base + tex - 0.2)
-        out[i] = np.clip(np.stack([img, img * 0.9, img * 1.1], -1), 0, 1)
-    return out
+    return syn.rgb_frames(n, h, w, tag)
 
 
 @pytest.mark.parametrize("n,h,w,win,sm", [(2, 64, 64, 7, 5), (3, 576, 576, 7, 5), (2, 37, 53, 3, 1),
