@@ -21,7 +21,8 @@ from paper_2511_18672_b200.step import RefinementStep  # noqa: E402
 
 
 def main():
-    sp.load()
+    # SPHINX_LIB: time another build of the library (same-box A/B of compile-time variants)
+    sp.load(os.environ["SPHINX_LIB"]) if os.environ.get("SPHINX_LIB") else sp.load()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
