@@ -10,217 +10,221 @@
 //   tau[n] = Otsu over a 256-bin histogram of U (bin i = (i/256, (i+1)/256]), exact argmax.
 // U and tau are exactly the (uncertainty, tau_u) inputs of sphinx_block_mask (U > tau blurry).
 //
-// Kernels: (1) fused stencil per 32x32 tile: Y, L, V (separable fp64 window sums), S
-// (separable box) staged in shared memory over the tile + halo (radius 1 + window/2 +
-// smooth/2), S written to the output buffer and per-frame min/max folded with integer
-// atomics (S >= 0, so float bits order as ints); (2) normalise +
-// invert in place and a per-CTA shared histogram folded into the per-frame histogram
-// (integer atomics: deterministic); (3) one CTA per frame: the exact Otsu argmax.
+// Kernels: (1) fused stencil, one column-sweep CTA per 116-column x 64-row strip: Y, L, the
+// window sums of L and L^2 -> V, the box sums -> S, each stage one row behind the previous (see
+// below); S written to the output buffer and per-frame min/max folded with integer atomics
+// (S >= 0, so float bits order as ints); (2) normalise + invert in place and a per-CTA shared
+// histogram (run-length + warp-aggregated increments) folded into the per-frame histogram (integer
+// atomics: deterministic); (3) one CTA per frame: scans of the histogram and the exact Otsu argmax.
 #include "common.cuh"
 
 namespace sphinx {
 
-constexpr int kUT = 32;  // output tile edge
+// ---------------------------------------------------------------- (1) fused stencil
+// Column sweep: a CTA of kSW threads owns a strip of kSW image columns (thread i = column
+// x0 - R + i, R = rv + rs + 1 halo columns each side, kSW - 2R output columns) and walks its
+// kSH output rows (+ R halo rows above and below) top to bottom; per row, four stages behind one
+// another, each one row behind the stage it reads:
+//   Y (row yY)         luminance of the row (shared ring of 4 rows)
+//   L (row yY - 1)     3x3 Laplacian from the Y ring (shared row, double-buffered)
+//   H, V (rows yL, yL - rv)  horizontal window sums of L and L^2 (thread-private ring of 16 rows
+//                      in shared memory), then the vertical window sums -> V (shared row)
+//   T, S (rows yV, yV - rs)  horizontal box sums of V (thread-private ring), vertical -> S
+// Every stage's input is edge-replicated: reads use image-clamped rows and columns (a stage's
+// rows outside the image are never produced; the clamped row always is, and is still in its
+// ring).  Three barriers per row; the window sums are plain sums in a fixed order.
+constexpr int kSW = 128;   // threads = strip columns
+constexpr int kSH = 64;    // output rows per CTA
+constexpr int kRing = 16;  // thread-private row rings (radius <= 7)
 
-__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+template <bool RINGS>  // shared row rings only for runtime radii (compile-time radii: registers)
+struct SweepSmem {
+  static constexpr int kR = RINGS ? kRing : 1;
+  float Ys[4][kSW];
+  float Ls[2][kSW];
+  float Vs[2][kSW];
+  float H1[kR][kSW], H2[kR][kSW], Ts[kR][kSW];
+};
 
-// Every stage works on the in-image rectangle its consumer needs and reads the previous stage
-// with image-clamped coordinates (edge replication of each stage's input, exactly as defined):
-//   S rows [sy0, sy1)  <- V rows [vy0, vy1) = [max(0, sy0-rs), min(h, sy1+rs))
-//   V rows [vy0, vy1)  <- L rows [ly0, ly1) = [max(0, vy0-rv), min(h, vy1+rv))
-//   L rows [ly0, ly1)  <- Y rows [yy0, yy1) = [max(0, ly0-1), min(h, ly1+1))      (same in x)
-// The window variance uses separable fp32 row/column sums of L and L^2:
-//   V = E[L^2] - E[L]^2 over the (2rv+1)^2 window.  The cancellation error is
-//   ~ 2^-23 E[L^2]; for images in [0,1] the Laplacian of a window with small variance but a
-//   large mean (constant curvature) is itself small, so after min-max normalisation the error
-//   stays ~1e-6 (parity tolerance 1e-4 vs the fp64 two-pass oracle, tests/test_gpu_parity).
-// RV, RS > 0: compile-time radii (the SPEC defaults 3 / 2): the window loops unroll and taps away
-// from the image border skip the clamp (measured ncu: the generic version was issue-bound at 88%
-// SM throughput on index arithmetic).  RV = RS = 0: runtime radii.
-// INT: the tile's whole halo lies inside the image (about 79% of the 576x576 tiles), so no tap
-// needs an edge-replication clamp or a per-element border test.
 template <int RV, int RS, bool INT>
-__device__ __forceinline__ void lapvar_body(const float* __restrict__ rgb, int h, int w, int rv_rt,
-                                            int rs_rt, float* __restrict__ S_out, int* __restrict__ minmax,
-                                            unsigned char* smraw) {
-  const int rv = RV > 0 ? RV : rv_rt, rs = RS > 0 ? RS : rs_rt;
-  const int n = blockIdx.z;
-  const int sy0 = blockIdx.y * kUT, sx0 = blockIdx.x * kUT;
-  const int sy1 = min(h, sy0 + kUT), sx1 = min(w, sx0 + kUT);
-  const int vy0 = max(0, sy0 - rs), vy1 = min(h, sy1 + rs), vx0 = max(0, sx0 - rs), vx1 = min(w, sx1 + rs);
-  const int ly0 = max(0, vy0 - rv), ly1 = min(h, vy1 + rv), lx0 = max(0, vx0 - rv), lx1 = min(w, vx1 + rv);
-  const int yy0 = max(0, ly0 - 1), yy1 = min(h, ly1 + 1), yx0 = max(0, lx0 - 1), yx1 = min(w, lx1 + 1);
-  const int YW = yx1 - yx0, LW = lx1 - lx0, VW = vx1 - vx0, SW = sx1 - sx0;
-  const int YH = yy1 - yy0, LH = ly1 - ly0, VH = vy1 - vy0, SH = sy1 - sy0;
-  // smem carve-up (max extents for T=32, r<=7: Y 62x62, L 60x60, rowsums 60x46 x2 fp64, V 46x46,
-  // S-rowsums 46x32)
-  float* R1 = reinterpret_cast<float*>(smraw);              // [LH][VW] sum_dx L
-  float* R2 = R1 + LH * VW;                                 // [LH][VW] sum_dx L^2
-  float* Ys = reinterpret_cast<float*>(R2 + LH * VW);       // [YH][YW]
-  float* Ls = Ys + YH * YW;                                 // [LH][LW]
-  float* Vs = Ls + LH * LW;                                 // [VH][VW]
-  float* Ts = Vs + VH * VW;                                 // [VH][SW] sum_dx V (box rows)
+__device__ __forceinline__ void lapvar_sweep_body(const float* __restrict__ rgb, int h, int w, int rv_rt,
+                                                  int rs_rt, float* __restrict__ S_out,
+                                                  int* __restrict__ minmax, SweepSmem<RV == 0>& sm) {
+  auto& Ys = sm.Ys;
+  auto& Ls = sm.Ls;
+  auto& Vs = sm.Vs;
+  auto& H1 = sm.H1;
+  auto& H2 = sm.H2;
+  auto& Ts = sm.Ts;
+  const int rv = RV > 0 ? RV : rv_rt, rs = RS > 0 ? RS : rs_rt, R = rv + rs + 1;
+  const int TW = kSW - 2 * R;
+  const int n = blockIdx.z, i = threadIdx.x;
+  const int x0 = blockIdx.x * TW, x1 = min(w, x0 + TW);
+  const int y0 = blockIdx.y * kSH, y1 = min(h, y0 + kSH);
+  const int xb = x0 - R;  // image column of smem column 0
+  const int g = xb + i;   // this thread's column
+  // image-clamped column -> smem column (interior strips: no clamp)
+  auto cix = [&](int x) { return (INT ? x : min(max(x, 0), w - 1)) - xb; };
+  auto crow = [&](int y) { return INT ? y : min(max(y, 0), h - 1); };
+  const bool in_img = g >= 0 && g < w;
+  const bool l_ok = in_img && g >= x0 - rs - rv && g < x1 + rs + rv;
+  const bool h_ok = in_img && g >= x0 - rs && g < x1 + rs;
+  const bool t_ok = g >= x0 && g < x1;
+  const int yY_lo = max(0, y0 - R), yY_hi = min(h, y1 + R);
+  const int yL_lo = max(0, y0 - rs - rv), yL_hi = min(h, y1 + rs + rv);
+  const int yV_lo = max(0, y0 - rs), yV_hi = min(h, y1 + rs);
   const size_t plane = (size_t)h * w;
   const float* img = rgb + (size_t)n * plane * 3;
-  // luminance of the tile + halo: 8 pixels (24 independent loads) in flight per thread (one
-  // pixel per iteration left each warp ~11 serial load latencies: ncu's top stall)
-  {
-    const int ny = YH * YW;
-    for (int e0 = threadIdx.x; e0 < ny; e0 += 8 * 256) {
-      float v[8][3];
+  const float inv_cnt = 1.0f / (float)((2 * rv + 1) * (2 * rv + 1));
+  const float inv_box = 1.0f / (float)((2 * rs + 1) * (2 * rs + 1));
+  float lo = 3.0e38f, hi = 0.0f;
+  // compile-time radii: the vertical windows live in registers (virtual rows, oldest first)
+  float rh1[2 * (RV > 0 ? RV : 0) + 1], rh2[2 * (RV > 0 ? RV : 0) + 1], rt[2 * (RS > 0 ? RS : 0) + 1];
+  // the next Y row's pixel, loaded one iteration ahead
+  float pr = 0.f, pg = 0.f, pb = 0.f;
+  auto load_px = [&](int y) {
+    if (in_img && y >= yY_lo && y < yY_hi) {
+      const float* px = img + ((size_t)y * w + g) * 3;
+      pr = __ldg(px);
+      pg = __ldg(px + 1);
+      pb = __ldg(px + 2);
+    }
+  };
+  load_px(y0 - R);
+  const int T = (y1 - y0) + 2 * R;
+  for (int t = 0; t < T; ++t) {
+    const int yY = y0 - R + t, yL = yY - 1, yV = yL - rv, yS = yV - rs;
+    // ---- Y
+    if (in_img && yY >= yY_lo && yY < yY_hi) Ys[yY & 3][i] = 0.299f * pr + 0.587f * pg + 0.114f * pb;
+    load_px(yY + 1);
+    __syncthreads();
+    // ---- L (same operation order as the oracle: up + down + left + right - 4 centre)
+    if (l_ok && yL >= yL_lo && yL < yL_hi) {
+      const float* yc = Ys[yL & 3];
+      const float up = Ys[crow(yL - 1) & 3][i], dn = Ys[crow(yL + 1) & 3][i];
+      Ls[yL & 1][i] = up + dn + yc[cix(g - 1)] + yc[cix(g + 1)] - 4.0f * yc[i];
+    }
+    __syncthreads();
+    // ---- H (row yL) and V (row yV)
+    if (h_ok) {
+      if (yL >= yL_lo && yL < yL_hi) {
+        const float* lr = Ls[yL & 1];
+        float s1 = 0.0f, s2 = 0.0f;
+        if constexpr (RV > 0) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int e = e0 + k * 256;
-        if (e < ny) {
-          const int a = e / YW, c = e - a * YW;
-          const float* px = img + ((size_t)(yy0 + a) * w + (yx0 + c)) * 3;
-          v[k][0] = __ldg(px);
-          v[k][1] = __ldg(px + 1);
-          v[k][2] = __ldg(px + 2);
+          for (int d = -RV; d <= RV; ++d) {
+            const float l = lr[cix(g + d)];
+            s1 += l;
+            s2 = fmaf(l, l, s2);
+          }
+          // register ring of the last 2RV+1 virtual rows; the image's first row also stands for
+          // the rows above it (edge replication)
+          const bool fill = yL == 0 && y0 - rs - rv < 0;
+#pragma unroll
+          for (int k = 0; k < 2 * RV; ++k) {
+            rh1[k] = fill ? s1 : rh1[k + 1];
+            rh2[k] = fill ? s2 : rh2[k + 1];
+          }
+          rh1[2 * RV] = s1;
+          rh2[2 * RV] = s2;
+        } else {
+          for (int d = -rv; d <= rv; ++d) {
+            const float l = lr[cix(g + d)];
+            s1 += l;
+            s2 = fmaf(l, l, s2);
+          }
+          H1[yL & (kRing - 1)][i] = s1;
+          H2[yL & (kRing - 1)][i] = s2;
+        }
+      } else if constexpr (RV > 0) {
+        if (yL >= h) {  // below the image: the last row stands for the rows below it
+#pragma unroll
+          for (int k = 0; k < 2 * RV; ++k) {
+            rh1[k] = rh1[k + 1];
+            rh2[k] = rh2[k + 1];
+          }
         }
       }
+      if (yV >= yV_lo && yV < yV_hi) {
+        float a = 0.0f, b = 0.0f;
+        if constexpr (RV > 0) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int e = e0 + k * 256;
-        if (e < ny) Ys[e] = 0.299f * v[k][0] + 0.587f * v[k][1] + 0.114f * v[k][2];
+          for (int k = 0; k <= 2 * RV; ++k) {
+            a += rh1[k];
+            b += rh2[k];
+          }
+        } else {
+          for (int d = -rv; d <= rv; ++d) {
+            const int r = crow(yV + d) & (kRing - 1);
+            a += H1[r][i];
+            b += H2[r][i];
+          }
+        }
+        const float m = a * inv_cnt;
+        Vs[yV & 1][i] = fmaxf(fmaf(-m, m, b * inv_cnt), 0.0f);
+      }
+    }
+    __syncthreads();
+    // ---- T (row yV) and S (row yS)
+    if (t_ok) {
+      if (yV >= yV_lo && yV < yV_hi) {
+        const float* vr = Vs[yV & 1];
+        float s1 = 0.0f;
+        if constexpr (RS > 0) {
+#pragma unroll
+          for (int d = -RS; d <= RS; ++d) s1 += vr[cix(g + d)];
+          const bool fill = yV == 0 && y0 - rs < 0;
+#pragma unroll
+          for (int k = 0; k < 2 * RS; ++k) rt[k] = fill ? s1 : rt[k + 1];
+          rt[2 * RS] = s1;
+        } else {
+          for (int d = -rs; d <= rs; ++d) s1 += vr[cix(g + d)];
+          Ts[yV & (kRing - 1)][i] = s1;
+        }
+      } else if constexpr (RS > 0) {
+        if (yV >= h) {
+#pragma unroll
+          for (int k = 0; k < 2 * RS; ++k) rt[k] = rt[k + 1];
+        }
+      }
+      if (yS >= y0 && yS < y1) {
+        float s1 = 0.0f;
+        if constexpr (RS > 0) {
+#pragma unroll
+          for (int k = 0; k <= 2 * RS; ++k) s1 += rt[k];
+        } else {
+          for (int d = -rs; d <= rs; ++d) s1 += Ts[crow(yS + d) & (kRing - 1)][i];
+        }
+        const float sv = s1 * inv_box;
+        S_out[(size_t)n * plane + (size_t)yS * w + g] = sv;
+        lo = fminf(lo, sv);
+        hi = fmaxf(hi, sv);
       }
     }
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < LH * LW; e += blockDim.x) {
-   const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)LW)), c = e - a * LW;
-    const int i = a * LW + c;
-    const int py = ly0 + a, px = lx0 + c;  // in-image position; neighbours clamped to the image
-    const int cy = py - yy0, cx = px - yx0;
-    const int uy = (INT ? py - 1 : max(py - 1, 0)) - yy0, dy = (INT ? py + 1 : min(py + 1, h - 1)) - yy0;
-    const int lx = (INT ? px - 1 : max(px - 1, 0)) - yx0, rx = (INT ? px + 1 : min(px + 1, w - 1)) - yx0;
-    Ls[i] = Ys[uy * YW + cx] + Ys[dy * YW + cx] + Ys[cy * YW + lx] + Ys[cy * YW + rx] - 4.0f * Ys[cy * YW + cx];
-   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < LH * VW; e += blockDim.x) {  // horizontal window sums of L and L^2
-    const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)VW)), c = e - a * VW;
-      const int px = vx0 + c;
-      float s1 = 0.0f, s2 = 0.0f;
-      if (INT || (px - rv >= 0 && px + rv < w)) {
-        const float* lr = Ls + a * LW + (px - lx0);
-        if constexpr (RV > 0) {
-#pragma unroll
-          for (int d = -RV; d <= RV; ++d) {
-            const float l = lr[d];
-            s1 += l;
-            s2 = fmaf(l, l, s2);
-          }
-        } else {
-          for (int d = -rv; d <= rv; ++d) {
-            const float l = lr[d];
-            s1 += l;
-            s2 = fmaf(l, l, s2);
-          }
-        }
-      } else {
-        for (int d = -rv; d <= rv; ++d) {
-          const float l = Ls[a * LW + min(max(px + d, 0), w - 1) - lx0];
-          s1 += l;
-          s2 = fmaf(l, l, s2);
-        }
-      }
-      R1[a * VW + c] = s1;
-      R2[a * VW + c] = s2;
-    }
-  __syncthreads();
-  const float inv_cnt = 1.0f / (float)((2 * rv + 1) * (2 * rv + 1));
-  for (int e = threadIdx.x; e < VH * VW; e += blockDim.x) {  // vertical window sums -> variance
-    const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)VW)), c = e - a * VW;
-      const int py = vy0 + a;
-      float s1 = 0.0f, s2 = 0.0f;
-      if (INT || (py - rv >= 0 && py + rv < h)) {
-        const float* r1 = R1 + (py - ly0) * VW + c;
-        const float* r2 = R2 + (py - ly0) * VW + c;
-        if constexpr (RV > 0) {
-#pragma unroll
-          for (int d = -RV; d <= RV; ++d) {
-            s1 += r1[d * VW];
-            s2 += r2[d * VW];
-          }
-        } else {
-          for (int d = -rv; d <= rv; ++d) {
-            s1 += r1[d * VW];
-            s2 += r2[d * VW];
-          }
-        }
-      } else {
-        for (int d = -rv; d <= rv; ++d) {
-          const int r = min(max(py + d, 0), h - 1) - ly0;
-          s1 += R1[r * VW + c];
-          s2 += R2[r * VW + c];
-        }
-      }
-      const float m = s1 * inv_cnt;
-      Vs[a * VW + c] = fmaxf(fmaf(-m, m, s2 * inv_cnt), 0.0f);
-    }
-  __syncthreads();
-  for (int e = threadIdx.x; e < VH * SW; e += blockDim.x) {  // box: horizontal sums of V
-    const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)SW)), c = e - a * SW;
-      const int px = sx0 + c;
-      float s1 = 0.0f;
-      if (INT || (px - rs >= 0 && px + rs < w)) {
-        const float* vr = Vs + a * VW + (px - vx0);
-        if constexpr (RS > 0) {
-#pragma unroll
-          for (int d = -RS; d <= RS; ++d) s1 += vr[d];
-        } else {
-          for (int d = -rs; d <= rs; ++d) s1 += vr[d];
-        }
-      } else {
-        for (int d = -rs; d <= rs; ++d) s1 += Vs[a * VW + min(max(px + d, 0), w - 1) - vx0];
-      }
-      Ts[a * SW + c] = s1;
-    }
-  __syncthreads();
-  const float inv_box = 1.0f / (float)((2 * rs + 1) * (2 * rs + 1));
-  float lo = 3.0e38f, hi = 0.0f;
-  for (int e = threadIdx.x; e < SH * SW; e += blockDim.x) {  // box: vertical sums -> S
-   const int a = __float2int_rz(((float)e + 0.5f) * (1.0f / (float)SW)), c = e - a * SW;
-    const int py = sy0 + a;
-    float s1 = 0.0f;
-    if (INT || (py - rs >= 0 && py + rs < h)) {
-      const float* tr = Ts + (py - vy0) * SW + c;
-      if constexpr (RS > 0) {
-#pragma unroll
-        for (int d = -RS; d <= RS; ++d) s1 += tr[d * SW];
-      } else {
-        for (int d = -rs; d <= rs; ++d) s1 += tr[d * SW];
-      }
-    } else {
-      for (int d = -rs; d <= rs; ++d) s1 += Ts[(min(max(py + d, 0), h - 1) - vy0) * SW + c];
-    }
-    const float sv = s1 * inv_box;
-    S_out[(size_t)n * plane + (size_t)py * w + sx0 + c] = sv;
-    lo = fminf(lo, sv);
-    hi = fmaxf(hi, sv);
-   }
   for (int d = 16; d > 0; d >>= 1) {
     lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, d));
     hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, d));
   }
-  if ((threadIdx.x & 31) == 0) {
+  if ((threadIdx.x & 31) == 0 && hi >= lo) {
     atomicMin(minmax + 2 * n, __float_as_int(lo));  // S >= +0: float order == int order
     atomicMax(minmax + 2 * n + 1, __float_as_int(hi));
   }
 }
 
 template <int RV, int RS>
-__global__ void __launch_bounds__(256) lapvar_smooth_kernel(const float* __restrict__ rgb, int h, int w,
-                                                            int rv_rt, int rs_rt, float* __restrict__ S_out,
-                                                            int* __restrict__ minmax) {
+__global__ void __launch_bounds__(kSW) lapvar_sweep_kernel(const float* __restrict__ rgb, int h, int w,
+                                                           int rv_rt, int rs_rt, float* __restrict__ S_out,
+                                                           int* __restrict__ minmax) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) unsigned char smraw[];
   const int rv = RV > 0 ? RV : rv_rt, rs = RS > 0 ? RS : rs_rt, R = rv + rs + 1;
-  const int sy0 = blockIdx.y * kUT, sx0 = blockIdx.x * kUT;
-  const bool interior = sy0 - R >= 0 && sx0 - R >= 0 && sy0 + kUT + R <= h && sx0 + kUT + R <= w;
-  if (interior) lapvar_body<RV, RS, true>(rgb, h, w, rv_rt, rs_rt, S_out, minmax, smraw);
-  else lapvar_body<RV, RS, false>(rgb, h, w, rv_rt, rs_rt, S_out, minmax, smraw);
+  const int x0 = blockIdx.x * (kSW - 2 * R), y0 = blockIdx.y * kSH;
+  // every column and row the strip touches (with its halo) lies inside the image: no clamps
+  const bool interior = x0 - R >= 0 && x0 - R + kSW <= w && y0 - R >= 0 && y0 + kSH + R <= h;
+  __shared__ SweepSmem<RV == 0> sm;
+  if (interior) lapvar_sweep_body<RV, RS, true>(rgb, h, w, rv_rt, rs_rt, S_out, minmax, sm);
+  else lapvar_sweep_body<RV, RS, false>(rgb, h, w, rv_rt, rs_rt, S_out, minmax, sm);
 }
 
 __device__ __forceinline__ int u_bin(float v) {
@@ -228,6 +232,13 @@ __device__ __forceinline__ int u_bin(float v) {
   int t = (int)ceilf(v * 256.0f) - 1;
   return t < 0 ? 0 : (t > 255 ? 255 : t);
 }
+
+// ---------------------------------------------------------------- (2) normalise + histogram
+// Each thread normalises 8 consecutive pixels (two 16-byte loads and stores when the frame is
+// 16-byte aligned) and counts runs of equal bins in a register: flat, blurry regions put long runs
+// in one bin, so a shared increment is issued only when the bin changes (and once at the end).
+// The CTA histogram is folded into the frame's with integer atomics (deterministic).
+constexpr int kNormPx = 8;
 
 __global__ void __launch_bounds__(256) normalize_hist_kernel(float* U, int plane, const int* __restrict__ minmax,
                                                              int* __restrict__ hist) {
@@ -240,20 +251,41 @@ __global__ void __launch_bounds__(256) normalize_hist_kernel(float* U, int plane
   const float lo = __int_as_float(minmax[2 * n]), hi = __int_as_float(minmax[2 * n + 1]);
   const float range = hi - lo;
   float* u = U + (size_t)n * plane;
-  // flat (blurry) regions put most pixels of a frame in a few bins: warp-aggregated increments
-  // (one shared atomic per distinct bin of the warp) instead of up to 32-way same-address ones
-  const int lane = threadIdx.x & 31;
-  for (int p0 = blockIdx.x * blockDim.x; p0 < plane; p0 += gridDim.x * blockDim.x) {
-    const int p = p0 + threadIdx.x;
-    const bool in = p < plane;
-    float v = 0.0f;
-    if (in) {
-      v = range > 0.0f ? 1.0f - (u[p] - lo) / range : 1.0f;  // normalise + invert
-      u[p] = v;
+  // 16-byte vectors when every frame starts 16-byte aligned
+  const bool vec = (plane & 3) == 0 && (reinterpret_cast<uintptr_t>(U) & 15) == 0;
+  const int step = gridDim.x * blockDim.x * kNormPx;
+  for (int pb = (blockIdx.x * blockDim.x + threadIdx.x) * kNormPx; pb < plane; pb += step) {
+    float v[kNormPx];
+    const int np = min(kNormPx, plane - pb);
+    if (vec && np == kNormPx) {
+      const float4 a = *reinterpret_cast<const float4*>(u + pb), b = *reinterpret_cast<const float4*>(u + pb + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kNormPx; ++k) v[k] = k < np ? u[pb + k] : 0.0f;
     }
-    const int bin = in ? u_bin(v) : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    if (in && lane == __ffs(peers) - 1) atomicAdd(&sh[bin], __popc(peers));
+#pragma unroll
+    for (int k = 0; k < kNormPx; ++k) v[k] = range > 0.0f ? 1.0f - (v[k] - lo) / range : 1.0f;  // normalise + invert
+    if (vec && np == kNormPx) {
+      *reinterpret_cast<float4*>(u + pb) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(u + pb + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+      for (int k = 0; k < np; ++k) u[pb + k] = v[k];
+    }
+    int run_bin = u_bin(v[0]), run = 1;
+#pragma unroll
+    for (int k = 1; k < kNormPx; ++k) {
+      if (k >= np) break;
+      const int bin = u_bin(v[k]);
+      if (bin == run_bin) {
+        ++run;
+      } else {
+        atomicAdd(&sh[run_bin], run);
+        run_bin = bin;
+        run = 1;
+      }
+    }
+    atomicAdd(&sh[run_bin], run);
   }
   __syncthreads();
   if (sh[threadIdx.x]) atomicAdd(hist + 256 * n + threadIdx.x, sh[threadIdx.x]);
@@ -267,22 +299,22 @@ typedef unsigned __int128 u128;
 __global__ void __launch_bounds__(256) otsu_kernel(const int* __restrict__ hist, float* __restrict__ tau) {
   pdl_wait();
   pdl_trigger();
-  __shared__ long long h[256];
+  __shared__ long long h[256], hs[256];
   __shared__ u128 sq[256], sr[256], sd[256];
   const int n = blockIdx.x, k = threadIdx.x;
-  h[k] = hist[256 * n + k];
-  __syncthreads();
-  long long N = 0, S = 0, n0 = 0, s0 = 0;
-  int nonempty = 0;
-  for (int i = 0; i < 256; ++i) {
-    N += h[i];
-    S += (long long)i * h[i];
-    nonempty += h[i] > 0;
-    if (i <= k) {
-      n0 += h[i];
-      s0 += (long long)i * h[i];
-    }
+  const long long hk = hist[256 * n + k];
+  h[k] = hk;
+  hs[k] = (long long)k * hk;
+  const int nonempty = __syncthreads_count(hk > 0);
+  // inclusive scans of the counts and of the bin-index sums (Hillis-Steele, 8 steps)
+  for (int off = 1; off < 256; off <<= 1) {
+    const long long a = k >= off ? h[k - off] : 0, b = k >= off ? hs[k - off] : 0;
+    __syncthreads();
+    h[k] += a;
+    hs[k] += b;
+    __syncthreads();
   }
+  const long long n0 = h[k], s0 = hs[k], N = h[255], S = hs[255];
   const long long n1 = N - n0;
   if (k < 255 && n0 > 0 && n1 > 0) {
     const __int128 d = (__int128)n0 * S - (__int128)N * s0;
@@ -344,23 +376,13 @@ extern "C" sphinx_status sphinx_uncertainty_map(const float* rgb, int32_t n, int
   e = cudaMemset2DAsync(minmax + 1, 2 * sizeof(int), 0, sizeof(int), (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
   const int rv = window / 2, rs = smooth / 2, R = rs + rv + 1;
-  const int NY = kUT + 2 * R, NL = kUT + 2 * (rs + rv), NV = kUT + 2 * rs;
-  const size_t smem = (size_t)NL * NV * 2 * sizeof(float) +
-                      (size_t)(NY * NY + NL * NL + NV * NV + NV * kUT) * sizeof(float);
-  static bool attr_set = false;
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(lapvar_smooth_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(lapvar_smooth_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e != cudaSuccess) return cuda_fail(e);
-    attr_set = true;
-  }
-  e = launch_k((rv == 3 && rs == 2) ? lapvar_smooth_kernel<3, 2> : lapvar_smooth_kernel<0, 0>,
-               dim3(cdiv(w, kUT), cdiv(h, kUT), n), dim3(256), smem, s, rgb, (int)h, (int)w, rv, rs,
+  const int TW = kSW - 2 * R;  // output columns per strip
+  e = launch_k((rv == 3 && rs == 2) ? lapvar_sweep_kernel<3, 2> : lapvar_sweep_kernel<0, 0>,
+               dim3(cdiv(w, TW), cdiv(h, kSH), n), dim3(kSW), 0, s, rgb, (int)h, (int)w, rv, rs,
                uncertainty, minmax);
   if (e != cudaSuccess) return cuda_fail(e);
   const int plane = h * w;
-  e = launch_k(normalize_hist_kernel, dim3(cdiv(plane, 256 * 8), n), dim3(256), 0, s, uncertainty, plane,
+  e = launch_k(normalize_hist_kernel, dim3(cdiv(plane, 256 * kNormPx), n), dim3(256), 0, s, uncertainty, plane,
                static_cast<const int*>(minmax), hist);
   if (e != cudaSuccess) return cuda_fail(e);
   e = launch_k(otsu_kernel, dim3(n), dim3(256), 0, s, static_cast<const int*>(hist), tau_u);
