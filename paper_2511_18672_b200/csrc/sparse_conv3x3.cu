@@ -1602,9 +1602,14 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     // At most one wave of tiles even if every capacity block is listed (e.g. a single frame):
     // the problem is latency-bound, and the per-tap path's split-K over (tap, chunk) K-steps
     // (halo mode splits only at 64-channel chunks) fills more of the GPU.  Measured on one
-    // 72x72x320 frame: 9.5 vs 12.6 us at 5% density, 15.5 vs 17.8 us dense.
+    // 72x72x320 frame: 9.5 vs 12.6 us at 5% density, 15.5 vs 17.8 us dense.  With C_in <= 320
+    // (per-tap A traffic = 9 shifted windows of 64 channels per chunk) the per-tap path also wins
+    // up to ~16 waves at capacity: its (tap, chunk) tails are finer and, since the round-2 per-tap
+    // epilogue, its tiles drain as fast (21 x 72x72x320, same box: 22.5 vs 25.8 us at 10%, 37.2 vs
+    // 40.6 at 25%, 73.2 vs 73.9 at 50%, 148.0 vs 148.4 dense; the configs[2] step -1%; the
+    // configs[3] level 0 (92 waves at capacity) stays in halo mode)
     const long long max_tiles = (long long)cdiv(capacity, (kBM / (block * block)) * 2) * cdiv(c_out, pick_bn(c_out));
-    if (max_tiles <= sms / 2) halo = 0;
+    if (max_tiles <= sms / 2 || (c_in <= 320 && max_tiles <= 16LL * (sms / 2))) halo = 0;
   }
   if (norm_tab) {
     if (!halo) return SPHINX_ERR_UNSUPPORTED;  // the transform works on halo slots (b = 8, 3x3)

@@ -50,8 +50,11 @@ class StepConfig:
 
     def __init__(self, hp=576, f=8, b=8, levels=((72, 320), (36, 640), (18, 1280)), convs_per_level=2,
                  frames_per_request=21, n_requests=1, u=25, gamma=0.5, tau_o=0.5, c_lat=4,
-                 interleave_levels=True):
+                 interleave_levels=True, conv_variant=None):
         self.hp, self.f, self.b = hp, f, b
+        # per-level kernel-variant flags of sphinx_sparse_conv3x3_ex (A/B and tests; None = the
+        # library's default choice)
+        self.conv_variant = conv_variant
         self.interleave_levels = interleave_levels  # conv launch order (RefinementStep.conv_order)
         self.levels = [tuple(x) for x in levels]
         self.convs_per_level = convs_per_level
@@ -298,7 +301,8 @@ class RefinementStep:
             # preceding conv's tail
             ops.sphinx_sparse_conv3x3(src[l], d[f"w{l}{j}"], d[f"b{l}{j}"], dst, cfg.b, self.ids[l], self.cnt[l],
                                       workspace=self.ws[l], reuse_plan=True, list_ready=True,
-                                      input_ready=(j == 0 or prev != (l, j - 1)))
+                                      input_ready=(j == 0 or prev != (l, j - 1)),
+                                      variant=(cfg.conv_variant[l] if cfg.conv_variant else 0))
             if conv_events is not None:
                 conv_events[l][j][1].record()
             src[l] = dst

@@ -134,8 +134,9 @@ def run_pointwise(trace):
                               "tflops": round(fl / t / 1e9, 1)}), flush=True)
 
 
-def run_single(trace):
-    """configs[1]: one 72x72x320 frame, 3x3 conv, the density sweep's lists (default kernel choice)."""
+def run_single(trace, nf=1):
+    """configs[1]: one 72x72x320 frame (nf = 21: the sweep's 21-frame variant), 3x3 conv, the
+    density sweep's lists (default kernel choice; dev build: variant flags A/B)."""
     import torch
     import paper_2511_18672_b200 as sp
     import synthetic as syn
@@ -143,7 +144,7 @@ def run_single(trace):
     lib = sp.load(os.path.join(ROOT, "paper_2511_18672_b200", "libsphinx_trace.so" if trace else "libsphinx.so"))
     dev = torch.device("cuda", 0)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    h, c, nf = 72, 320, 1
+    h, c = 72, 320
     x = torch.from_numpy(syn.features_bf16((nf, h, h, c), "sweep").view(np.int16)).view(torch.bfloat16).to(dev)
     w = torch.from_numpy(syn.weights_bf16(c, c, "sweep").view(np.int16)).view(torch.bfloat16).to(dev)
     y = torch.zeros((nf, h, h, c), dtype=torch.bfloat16, device=dev)
@@ -165,13 +166,14 @@ def run_single(trace):
             f()
             launch += 1
             torch.cuda.synchronize()
-            show(lib, sms, f"single frame, {len(ids_np)} blocks")
+            show(lib, sms, f"{nf} frame(s), {len(ids_np)} blocks")
             os.environ["SPHINX_TRACE_LAUNCH"] = "-1"
-            for bn in ("64", "128", "160"):  # dev build: C_out tile width A/B
-                os.environ["SPHINX_BN"] = bn
-                t = bench.graph_time(torch, f)
-                print(json.dumps({"time": f"single frame {len(ids_np)} blocks, BN {bn} (dev build)", "ms": round(t, 5)}))
-                del os.environ["SPHINX_BN"]
+            for name, fl in (("default", 0), ("no split", sp.CONV_NO_SPLIT), ("no stream-K", sp.CONV_NO_STREAMK),
+                             ("force stream-K", sp.CONV_FORCE_STREAMK), ("per-tap", sp.CONV_FORCE_PERTAP),
+                             ("halo", sp.CONV_FORCE_HALO)):
+                g_ = lambda: sp.sphinx_sparse_conv3x3(x, w, None, y, 8, ids, cnt, workspace=ws, variant=fl)
+                t = bench.graph_time(torch, g_)
+                print(json.dumps({"time": f"{nf} frame(s) {len(ids_np)} blocks, {name}", "ms": round(t, 5)}))
         else:
             t = bench.graph_time(torch, f)
             print(json.dumps({"time": f"single frame {len(ids_np)} blocks", "ms": round(t, 5)}), flush=True)
@@ -204,12 +206,13 @@ def run_step(name, trace):
 
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "step"
-    if what == "single":
+    if what in ("single", "sweep21"):
+        nf = 1 if what == "single" else 21
         if "--trace" in sys.argv:
-            run_single(True)
+            run_single(True, nf)
         else:
-            run_single(False)
-            subprocess.check_call([sys.executable, __file__, "single", "--trace"])
+            run_single(False, nf)
+            subprocess.check_call([sys.executable, __file__, what, "--trace"])
     elif what == "pointwise":
         if "--trace" in sys.argv:
             run_pointwise(True)

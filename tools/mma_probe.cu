@@ -14,8 +14,19 @@ using namespace sphinx;
 
 constexpr int ITER = 2048;
 
-// WAIT (bits): every 4 MMAs also 1 = wait on an already-complete mbarrier phase, 2 = fence
+// WAIT (bits): every 4 MMAs also 1 = wait on an already-complete mbarrier phase, 2 = fence,
+// 4 = the wait uses mbarrier.test_wait (non-blocking probe) in a spin instead of try_wait
 // (the shape of the conv kernels' per-(tap, chunk) loop: wait operands, fence, 4 MMAs, commit)
+__device__ __forceinline__ void mbar_wait_test(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "TW_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra TW_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
 template <int N, int ISSUERS, int COMMIT_EVERY, int WAIT = 0>
 __global__ void __launch_bounds__(128, 1) probe(unsigned long long* out) {
   extern __shared__ uint8_t raw[];
@@ -48,7 +59,10 @@ __global__ void __launch_bounds__(128, 1) probe(unsigned long long* out) {
     for (int i = 0; i < ITER; ++i) {
       const int k = i & 3;
       if (WAIT && k == 0) {
-        if (WAIT & 1) mbar_wait(&bars[4 + warp], 0);
+        if (WAIT & 1) {
+          if (WAIT & 4) mbar_wait_test(&bars[4 + warp], 0);
+          else mbar_wait(&bars[4 + warp], 0);
+        }
         if (WAIT & 2) tc_fence_after();
       }
       tc_mma_bf16(d, umma_desc_sw128(a + k * 32, 1024, 0), umma_desc_sw128(b + k * 32, 1024, 0), idesc,
@@ -102,9 +116,9 @@ int main() {
   run<160, 1, 4, 3>(1);
   run<160, 1, 4, 1>(1);
   run<160, 1, 4, 2>(1);
-  run<256, 1, 4, 3>(1);
+  run<160, 1, 4, 7>(1);
+  run<160, 1, 4, 5>(1);
   run<128, 1, 4, 3>(1);
-  run<128, 1, 4, 1>(1);
-  run<128, 1, 4, 2>(1);
+  run<128, 1, 4, 7>(1);
   return 0;
 }
