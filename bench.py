@@ -691,6 +691,12 @@ def run_gpu(args):
             del st2
         if not args.no_sweep:
             extras["density_sweep"] = density_sweep(torch, sp, dev)
+            # the metric's second half at a glance: speedup over the best dense launch (own or cuDNN)
+            # at 10 / 25 / 50% density, per batch size of the sweep (configs[1] = 1 frame)
+            extras["speedup_vs_dense"] = {
+                f"{sw['frames']}_frames": {f"{int(round(r['density'] * 100 / 5) * 5)}%": r["speedup_vs_dense"]
+                                           for r in sw["rows"] if 0.08 < r["density"] < 0.6}
+                for sw in extras["density_sweep"]}
 
     if rank == 0:
         cpu = None if (world > 1 or args.no_cpu) else cpu_baseline(batch, cfg, bounded_s=args.cpu_seconds)
