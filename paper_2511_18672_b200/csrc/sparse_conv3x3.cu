@@ -1647,7 +1647,10 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
   }
   // per-tap mode with bf16 y: the epilogue writes each 32-column chunk of a block with one TMA
   // tensor store (box {32 ch, b, b, 1} of the NHWC map; SW64 staging layout)
-  const int tma_y = (!halo && y_dtype == SPHINX_BF16 && !norm_tab && c_out >= 32) ? 1 : 0;
+  int tma_y = (!halo && y_dtype == SPHINX_BF16 && !norm_tab && c_out >= 32) ? 1 : 0;
+#ifdef SPHINX_DEV_KNOBS
+  if (getenv("SPHINX_NO_TMA_Y")) tma_y = 0;  // dev build A/B: direct 16-byte stores instead
+#endif
   if (tma_y) {
     const cuuint64_t dims[4] = {(cuuint64_t)c_out, (cuuint64_t)w_, (cuuint64_t)h, (cuuint64_t)n};
     const cuuint64_t strides[3] = {(cuuint64_t)c_out * 2, (cuuint64_t)w_ * c_out * 2,

@@ -122,10 +122,15 @@ def run_pointwise(trace):
                 import bench
                 os.environ["SPHINX_TRACE_LAUNCH"] = "-1"
                 for bn in ("160", "256", "128"):  # dev build: C_out tile width A/B
-                    os.environ["SPHINX_BN"] = bn
-                    t = bench.graph_time(torch, f)
-                    print(json.dumps({"time": f"pointwise level 0, BN {bn} (dev build)", "ms": round(t, 5)}))
-                    del os.environ["SPHINX_BN"]
+                    for tmay in (True, False):
+                        os.environ["SPHINX_BN"] = bn
+                        if not tmay:
+                            os.environ["SPHINX_NO_TMA_Y"] = "1"
+                        t = bench.graph_time(torch, f)
+                        print(json.dumps({"time": f"pointwise level 0, BN {bn}, TMA-store {tmay} (dev build)",
+                                          "ms": round(t, 5)}))
+                        os.environ.pop("SPHINX_NO_TMA_Y", None)
+                        del os.environ["SPHINX_BN"]
         else:
             import bench
             t = bench.graph_time(torch, f)
@@ -170,9 +175,12 @@ def run_single(trace, nf=1):
             os.environ["SPHINX_TRACE_LAUNCH"] = "-1"
             for name, fl in (("default", 0), ("no split", sp.CONV_NO_SPLIT), ("no stream-K", sp.CONV_NO_STREAMK),
                              ("force stream-K", sp.CONV_FORCE_STREAMK), ("per-tap", sp.CONV_FORCE_PERTAP),
-                             ("halo", sp.CONV_FORCE_HALO)):
+                             ("halo", sp.CONV_FORCE_HALO), ("per-tap, direct stores", sp.CONV_FORCE_PERTAP)):
+                if "direct" in name:
+                    os.environ["SPHINX_NO_TMA_Y"] = "1"
                 g_ = lambda: sp.sphinx_sparse_conv3x3(x, w, None, y, 8, ids, cnt, workspace=ws, variant=fl)
                 t = bench.graph_time(torch, g_)
+                os.environ.pop("SPHINX_NO_TMA_Y", None)
                 print(json.dumps({"time": f"{nf} frame(s) {len(ids_np)} blocks, {name}", "ms": round(t, 5)}))
         else:
             t = bench.graph_time(torch, f)
