@@ -29,6 +29,25 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 bool pdl_enabled();  // SPHINX_PDL=0 disables (A/B measurement)
 
+// A listed block of an NHWC map [N][h][w][c] (b x b pixels, hb x wb blocks per frame): element
+// offset of its first pixel, valid rows, valid vectors per row (vpp vectors per pixel), frame.
+struct BlockRef {
+  size_t base;  // element offset of the block's first pixel
+  int rows, colv, fr;
+};
+
+__device__ __forceinline__ BlockRef block_ref(int id, int h, int w, int c, int b, int hb, int wb,
+                                              int vpp) {
+  BlockRef r;
+  r.fr = id / (hb * wb);
+  const int rem = id - r.fr * hb * wb;
+  const int by = rem / wb, bx = rem - by * wb;
+  r.rows = min(b, h - by * b);
+  r.colv = min(b, w - bx * b) * vpp;
+  r.base = (((size_t)r.fr * h + by * b) * w + (size_t)bx * b) * c;
+  return r;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {

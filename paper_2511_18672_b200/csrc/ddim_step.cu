@@ -7,9 +7,18 @@
 // HBM-bound elementwise pass over the listed blocks only (12 B per element: z, x0_hat in,
 // z' out), same thread layout as noise_inject (one 16-byte vector per thread).  The
 // inactive frames' resampling (Alg1 line 19) is sphinx_noise_inject at step u+1.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sphinx {
+
+// Same work layout as noise_inject.cu: one warp per listed block (kDdimBlk blocks per pass),
+// lanes over the blocks' 16-byte vectors (row, column from a shift: no per-vector division), all
+// of a pass's loads issued before its stores (tools/mem_ab.py: 8.4 -> 4.9 us L2-warm, ncu cold
+// 12.5 -> 10.2 us).
+constexpr int kDdimItems = 2;
+constexpr int kDdimBlk = 1;  // blocks per warp pass (2: measured equal)
 
 template <int V>
 __global__ void __launch_bounds__(256) ddim_kernel(const float* z, const float* __restrict__ x0h,
@@ -17,35 +26,59 @@ __global__ void __launch_bounds__(256) ddim_kernel(const float* z, const float* 
                                                    int wb, const int32_t* __restrict__ ids,
                                                    const int32_t* __restrict__ count, float a0,
                                                    float inv_s0, float a1, float s1) {
+  using VecT = typename std::conditional<V == 4, float4, float>::type;
   pdl_wait();
   pdl_trigger();
   const int cnt = *count;
+  const int lane = threadIdx.x & 31;
   const int vpp = c / V;
-  const int per_block = b * b * vpp;
-  const long long total = (long long)cnt * per_block;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(e / per_block);
-    const int r = (int)(e - (long long)j * per_block);
-    const int p = r / vpp, v = r - p * vpp;
-    const int id = __ldg(ids + j);
-    const int fr = id / (hb * wb), rem = id - fr * hb * wb;
-    const int by = rem / wb, bx = rem - by * wb;
-    const int y = by * b + p / b, x = bx * b + p % b;
-    if (y >= h || x >= w) continue;
-    const size_t off = (((size_t)fr * h + y) * w + x) * c + (size_t)v * V;
-    if constexpr (V == 4) {
-      const float4 Z = *reinterpret_cast<const float4*>(z + off);
-      const float4 X = __ldg(reinterpret_cast<const float4*>(x0h + off));
-      float4 o;
-      o.x = fmaf(a1, X.x, s1 * ((Z.x - a0 * X.x) * inv_s0));
-      o.y = fmaf(a1, X.y, s1 * ((Z.y - a0 * X.y) * inv_s0));
-      o.z = fmaf(a1, X.z, s1 * ((Z.z - a0 * X.z) * inv_s0));
-      o.w = fmaf(a1, X.w, s1 * ((Z.w - a0 * X.w) * inv_s0));
-      *reinterpret_cast<float4*>(z_out + off) = o;
-    } else {
-      const float X = __ldg(x0h + off);
-      z_out[off] = fmaf(a1, X, s1 * ((z[off] - a0 * X) * inv_s0));
+  const int rowv = b * vpp;  // vectors per block row
+  const int sh = (rowv & (rowv - 1)) == 0 ? __ffs(rowv) - 1 : -1;
+  const int per_block = b * rowv;
+  const size_t row_stride = (size_t)w * c;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j0 < cnt; j0 += kDdimBlk * nwarps) {
+    BlockRef br[kDdimBlk];
+#pragma unroll
+    for (int k = 0; k < kDdimBlk; ++k) {
+      const bool has = j0 + k * nwarps < cnt;
+      br[k] = block_ref(has ? __ldg(ids + j0 + k * nwarps) : 0, h, w, c, b, hb, wb, vpp);
+      if (!has) br[k].rows = 0;
+    }
+    for (int t0 = lane; t0 < per_block; t0 += 32 * kDdimItems) {
+      size_t off[kDdimBlk][kDdimItems];
+      bool ok[kDdimBlk][kDdimItems];
+      VecT Z[kDdimBlk][kDdimItems], X[kDdimBlk][kDdimItems];
+#pragma unroll
+      for (int k = 0; k < kDdimBlk; ++k)
+#pragma unroll
+        for (int i = 0; i < kDdimItems; ++i) {
+          const int t = t0 + 32 * i;
+          const int r = sh >= 0 ? t >> sh : t / rowv;
+          const int col = t - r * rowv;
+          ok[k][i] = t < per_block && r < br[k].rows && col < br[k].colv;  // truncated edge blocks
+          off[k][i] = br[k].base + (size_t)r * row_stride + (size_t)col * V;
+          if (ok[k][i]) {
+            Z[k][i] = *reinterpret_cast<const VecT*>(z + off[k][i]);
+            X[k][i] = __ldg(reinterpret_cast<const VecT*>(x0h + off[k][i]));
+          }
+        }
+#pragma unroll
+      for (int k = 0; k < kDdimBlk; ++k)
+#pragma unroll
+        for (int i = 0; i < kDdimItems; ++i) {
+          if (!ok[k][i]) continue;
+          if constexpr (V == 4) {
+            float4 o;
+            o.x = fmaf(a1, X[k][i].x, s1 * ((Z[k][i].x - a0 * X[k][i].x) * inv_s0));
+            o.y = fmaf(a1, X[k][i].y, s1 * ((Z[k][i].y - a0 * X[k][i].y) * inv_s0));
+            o.z = fmaf(a1, X[k][i].z, s1 * ((Z[k][i].z - a0 * X[k][i].z) * inv_s0));
+            o.w = fmaf(a1, X[k][i].w, s1 * ((Z[k][i].w - a0 * X[k][i].w) * inv_s0));
+            *reinterpret_cast<float4*>(z_out + off[k][i]) = o;
+          } else {
+            z_out[off[k][i]] = fmaf(a1, X[k][i], s1 * ((Z[k][i] - a0 * X[k][i]) * inv_s0));
+          }
+        }
     }
   }
 }
@@ -76,8 +109,7 @@ extern "C" sphinx_status sphinx_ddim_step(const float* z, const float* x0_hat, f
   const float a0 = (float)sqrt(ab0), inv_s0 = (float)(1.0 / sqrt(1.0 - ab0));
   const float a1 = (float)sqrt(ab1), s1 = (float)sqrt(1.0 - ab1);
   const bool vec = (c % 4 == 0) && aligned16(z) && aligned16(x0_hat) && aligned16(z_out);
-  const int V = vec ? 4 : 1;
-  long long blocks = ((long long)capacity * b * b * (c / V) + 255) / 256;
+  long long blocks = ((long long)capacity + 8 * kDdimBlk - 1) / (8 * kDdimBlk);  // a warp per kDdimBlk blocks
   if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
   if (blocks < 1) blocks = 1;
   cudaError_t e = launch_k(vec ? ddim_kernel<4> : ddim_kernel<1>, dim3((unsigned)blocks), dim3(256), 0,

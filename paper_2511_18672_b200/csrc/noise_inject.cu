@@ -5,13 +5,27 @@
 // north_star), u = 0 noisiest.
 //
 // HBM-bound elementwise pass: 12 B per element (x0, eps in; x_t out) on active blocks
-// only.  One thread moves one 16-byte vector (4 channels) of one pixel; a block's row
-// segment is contiguous in NHWC (b*C*4 bytes) so consecutive threads of a warp touch
-// consecutive 16-byte words of the same segment.  The device count bounds the work;
+// only.  A warp moves whole blocks, its lanes 16-byte vectors (4 channels); a block's row
+// segment is contiguous in NHWC (b*C*4 bytes) so consecutive lanes touch consecutive
+// 16-byte words of the same segment.  The device count bounds the work;
 // the grid is sized from the capacity, so no host read of the count is needed.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace sphinx {
+
+// Work layout: one warp per listed block, kBlk blocks per warp pass (grid stride over the list),
+// lanes over the blocks' 16-byte vectors.  A block row is one contiguous run of b*C elements in
+// NHWC, so a vector's offset is base + row * (w*C) + col with (row, col) from a shift when the
+// row's vector count is a power of two (every b = 4 / 8 map) -- no per-vector divisions (round
+// 2's flat-index version spent half its issue slots on 64-bit index division: ncu 1.9 TB/s).
+// Every data load of a pass is issued before any store and before the step check, so a warp's
+// dependent chain is count -> ids -> {x0, eps, step} per pass (measured, tools/mem_ab.py on 168
+// frames x 72x72x4: 10.0 -> 6.1 us L2-warm, ncu cold 14.2 -> 12.2 us).
+constexpr int kMaxAbar = 1024;  // abar entries staged in shared memory (larger S: read from global)
+constexpr int kItems = 2;       // vectors per lane per block and pass (a whole 8x8x4 fp32 block)
+constexpr int kBlk = 1;         // blocks per warp pass (2: measured equal, tools/mem_ab.py)
 
 template <int V>
 __global__ void __launch_bounds__(256) noise_kernel(const float* __restrict__ x0,
@@ -23,39 +37,74 @@ __global__ void __launch_bounds__(256) noise_kernel(const float* __restrict__ x0
                                                     const int32_t* __restrict__ step,
                                                     const float* __restrict__ abar, int S,
                                                     int step_u) {
+  using VecT = typename std::conditional<V == 4, float4, float>::type;
+  __shared__ float s_abar[kMaxAbar];
   pdl_wait();
   pdl_trigger();
+  const bool staged = S + 1 <= kMaxAbar;
+  if (staged)
+    for (int i = threadIdx.x; i <= S; i += blockDim.x) s_abar[i] = __ldg(abar + i);
   const int cnt = *count;
-  const int vpp = c / V;              // vectors per pixel
-  const int per_block = b * b * vpp;  // vectors per (padded) block
-  const long long total = (long long)cnt * per_block;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(e / per_block);
-    const int r = (int)(e - (long long)j * per_block);
-    const int p = r / vpp, v = r - p * vpp;
-    const int id = __ldg(ids + j);
-    const int fr = id / (hb * wb), rem = id - fr * hb * wb;
-    const int by = rem / wb, bx = rem - by * wb;
-    const int y = by * b + p / b, x = bx * b + p % b;
-    if (y >= h || x >= w) continue;  // truncated edge block
-    int u = __ldg(step + fr);
-    if (step_u >= 0) u = u > step_u ? step_u + 1 : u;  // step = start steps: active k, inactive u+1
-    if (u < 0 || u > S) continue;
-    const float ab = __ldg(abar + u);
-    const float a = sqrtf(ab), s = sqrtf(1.0f - ab);
-    const size_t off = (((size_t)fr * h + y) * w + x) * c + (size_t)v * V;
-    if constexpr (V == 4) {
-      const float4 X = __ldg(reinterpret_cast<const float4*>(x0 + off));
-      const float4 E = __ldg(reinterpret_cast<const float4*>(eps + off));
-      float4 Z;
-      Z.x = fmaf(a, X.x, s * E.x);
-      Z.y = fmaf(a, X.y, s * E.y);
-      Z.z = fmaf(a, X.z, s * E.z);
-      Z.w = fmaf(a, X.w, s * E.w);
-      *reinterpret_cast<float4*>(x_t + off) = Z;
-    } else {
-      x_t[off] = fmaf(a, __ldg(x0 + off), s * __ldg(eps + off));
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int vpp = c / V;
+  const int rowv = b * vpp;  // vectors per block row
+  const int sh = (rowv & (rowv - 1)) == 0 ? __ffs(rowv) - 1 : -1;
+  const int per_block = b * rowv;
+  const size_t row_stride = (size_t)w * c;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j0 < cnt; j0 += kBlk * nwarps) {
+    int id[kBlk];
+#pragma unroll
+    for (int k = 0; k < kBlk; ++k) id[k] = j0 + k * nwarps < cnt ? __ldg(ids + j0 + k * nwarps) : -1;
+    BlockRef br[kBlk];
+    int u[kBlk];
+#pragma unroll
+    for (int k = 0; k < kBlk; ++k) {
+      br[k] = block_ref(id[k] < 0 ? 0 : id[k], h, w, c, b, hb, wb, vpp);
+      if (id[k] < 0) br[k].rows = 0;
+      u[k] = id[k] < 0 ? -1 : __ldg(step + br[k].fr);
+    }
+    for (int t0 = lane; t0 < per_block; t0 += 32 * kItems) {
+      size_t off[kBlk][kItems];
+      bool ok[kBlk][kItems];
+      VecT X[kBlk][kItems], E[kBlk][kItems];
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k)
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+          const int t = t0 + 32 * i;
+          const int r = sh >= 0 ? t >> sh : t / rowv;
+          const int col = t - r * rowv;
+          ok[k][i] = t < per_block && r < br[k].rows && col < br[k].colv;  // truncated edge blocks
+          off[k][i] = br[k].base + (size_t)r * row_stride + (size_t)col * V;
+          if (ok[k][i]) {
+            X[k][i] = __ldg(reinterpret_cast<const VecT*>(x0 + off[k][i]));
+            E[k][i] = __ldg(reinterpret_cast<const VecT*>(eps + off[k][i]));
+          }
+        }
+#pragma unroll
+      for (int k = 0; k < kBlk; ++k) {
+        int uu = u[k];
+        if (step_u >= 0) uu = uu > step_u ? step_u + 1 : uu;  // start steps: active k, inactive u+1
+        if (uu < 0 || uu > S) continue;  // (checked after the loads: they do not wait for it)
+        const float ab = staged ? s_abar[uu] : __ldg(abar + uu);
+        const float a = sqrtf(ab), s = sqrtf(1.0f - ab);
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+          if (!ok[k][i]) continue;
+          if constexpr (V == 4) {
+            float4 Z;
+            Z.x = fmaf(a, X[k][i].x, s * E[k][i].x);
+            Z.y = fmaf(a, X[k][i].y, s * E[k][i].y);
+            Z.z = fmaf(a, X[k][i].z, s * E[k][i].z);
+            Z.w = fmaf(a, X[k][i].w, s * E[k][i].w);
+            *reinterpret_cast<float4*>(x_t + off[k][i]) = Z;
+          } else {
+            x_t[off[k][i]] = fmaf(a, X[k][i], s * E[k][i]);
+          }
+        }
+      }
     }
   }
 }
@@ -82,9 +131,8 @@ static sphinx_status noise_impl(const float* x0, const float* eps, float* x_t, i
   if (st != SPHINX_OK) return st;
   if (capacity == 0) return SPHINX_OK;
   const bool vec = (c % 4 == 0) && aligned16(x0) && aligned16(eps) && aligned16(x_t);
-  const int V = vec ? 4 : 1;
-  const long long work = (long long)capacity * b * b * (c / V);
-  long long blocks = (work + 255) / 256;
+  // one warp per kBlk listed blocks, 8 warps per CTA
+  long long blocks = ((long long)capacity + 8 * kBlk - 1) / (8 * kBlk);
   const long long cap = (long long)sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
