@@ -4,7 +4,7 @@ library builds, on configs[3]-sized latents (168 x 72x72x4 fp32, a 13 608-entry 
     SPHINX_LIB=<path> python tools/mem_ab.py
 
 warm: CUDA-graph replay of 20 launches (L2-warm); cold: one launch in a graph replayed right
-behind a 256 MB L2 flush (bench.py memory_kernels' protocol)."""
+behind a 256 MB write + 256 MB read L2 flush (bench.py memory_kernels' protocol)."""
 import json
 import os
 import statistics
@@ -21,7 +21,7 @@ import paper_2511_18672_b200 as sp  # noqa: E402
 import synthetic as syn  # noqa: E402
 
 
-def cold(fn, flush, reps=12):
+def cold(fn, flush, reps=12, flush_r=[]):
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
@@ -33,6 +33,9 @@ def cold(fn, flush, reps=12):
     ts = []
     for i in range(reps):
         flush.fill_(0.0)
+        if not flush_r:
+            flush_r.append(torch.zeros_like(flush))
+        flush_r[0].amax()  # clean L2 (bench.py memory_kernels' protocol)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         g.replay()
@@ -67,6 +70,18 @@ def main():
     for name, f in (("noise", f_noise), ("ddim", f_ddim)):
         out[name + "_warm_us"] = round(bench.graph_time(torch, f) * 1e3, 2)
         out[name + "_cold_us"] = round(cold(f, flush) * 1e3, 2)
+    # step 1 (block mask + counts + start steps) at the configs[2] and configs[3] frame counts
+    for nf in (21, 168):
+        O, cells = syn.opacity_maps(nf, 576, 576, 64, list(syn.request_densities(nf)), "clustered", tag="memab")
+        U, tau = syn.uncertainty_maps(nf, 576, 576, 64, cells, tag="memab")
+        Od, Ud, taud = (torch.from_numpy(a).to(dev) for a in (O, U, tau))
+        masks = [torch.empty((nf, 9 >> l if l == 0 else -(-9 // (1 << l)), 9 if l == 0 else -(-9 // (1 << l))),
+                             dtype=torch.uint8, device=dev) for l in range(3)]
+        counts = torch.empty((nf, 3), dtype=torch.int32, device=dev)
+        f_mask = lambda: sp.sphinx_block_mask(Od, Ud, taud, 0.5, 8, 8, masks, counts, None, None)
+        out[f"mask{nf}_mbytes"] = round(nf * 576 * 576 * 8 / 1e6, 1)
+        out[f"mask{nf}_warm_us"] = round(bench.graph_time(torch, f_mask) * 1e3, 2)
+        out[f"mask{nf}_cold_us"] = round(cold(f_mask, flush) * 1e3, 2)
     print(json.dumps(out), flush=True)
 
 
