@@ -12,6 +12,8 @@ so frames (and whole requests) are independent units.  Two schemes are supported
   executed MMA work cost_n = sum_l count[n,l] * C_l^2 (a level-l block costs (C_l/C_0)^2
   level-0 blocks of work).
 """
+import heapq
+
 import numpy as np
 
 
@@ -27,16 +29,24 @@ def lpt_assign(costs, world):
     """Longest-processing-time-first: frames sorted by cost descending (ties: lower frame id
     first) go to the currently least-loaded rank (ties: lowest rank).  Deterministic, so
     every rank computes the same plan from the same gathered counts.
-    Returns (list of frame-id arrays per rank, int64 load per rank)."""
+    Returns (list of frame-id arrays per rank, int64 load per rank).
+    (Runs once per sharded step on every rank, between the mask all-gather and the compaction:
+    plain Python ints and a (load, rank) heap -- the heap order is exactly "least loaded, then
+    lowest rank" -- keep it at ~0.1 ms for 168 frames; a numpy-scalar loop took ~0.9 ms.)"""
     costs = np.asarray(costs, dtype=np.int64)
-    order = sorted(range(len(costs)), key=lambda i: (-int(costs[i]), i))
-    load = np.zeros(world, dtype=np.int64)
-    assign = [[] for _ in range(world)]
+    order = np.lexsort((np.arange(len(costs)), -costs)).tolist()  # cost desc, then frame id
+    cl = costs.tolist()
+    heap = [(0, r) for r in range(world)]  # already a heap
+    rank_of = [0] * len(cl)
     for i in order:
-        r = int(np.argmin(load))  # argmin returns the lowest index among ties
-        assign[r].append(i)
-        load[r] += costs[i]
-    return [np.array(sorted(a), dtype=np.int64) for a in assign], load
+        ld, r = heap[0]
+        rank_of[i] = r
+        heapq.heapreplace(heap, (ld + cl[i], r))
+    rank_of = np.asarray(rank_of, dtype=np.int64)
+    load = np.bincount(rank_of, weights=costs, minlength=world).astype(np.int64) if len(cl) else \
+        np.zeros(world, dtype=np.int64)
+    idx = np.arange(len(cl), dtype=np.int64)
+    return [idx[rank_of == r] for r in range(world)], load
 
 
 def round_robin(n, world, rank):

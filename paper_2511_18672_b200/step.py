@@ -205,6 +205,7 @@ class RefinementStep:
             self.comm_stream = torch.cuda.Stream(device=self.dev) if self.cuda else None
             self.h_k = torch.zeros((F,), dtype=i32).pin_memory() if self.cuda else torch.zeros((F,), dtype=i32)
             self.plan = None
+            self.h_plan_in = None
             self.recv_ids = [torch.zeros((F * hb * hb,), dtype=i32, device=self.dev) for hb in cfg.hb]
             self.recv_cnt = torch.zeros((L,), dtype=i32, device=self.dev)
             self.h_recv_cnt = torch.zeros((L,), dtype=i32).pin_memory() if self.cuda else torch.zeros((L,), dtype=i32)
@@ -244,19 +245,25 @@ class RefinementStep:
         for r, fr in enumerate(assign):
             rank_of[fr] = r
         # blocks of level l computed by s for frames owned by o: pair[l][s, o]
-        pair = np.zeros((L, world, world), np.int64)
-        for l in range(L):
-            np.add.at(pair[l], (rank_of, self.owner), cnt[:, l])
+        cell = rank_of * world + self.owner
+        pair = np.stack([np.bincount(cell, weights=cnt[:, l], minlength=world * world)
+                         for l in range(L)]).astype(np.int64).reshape(L, world, world)
         return dict(rank_of=rank_of, load=load, cnt=cnt, pair=pair,
                     imbalance=float(load.max() / max(load.mean(), 1e-9)))
 
     def _plan_step(self):
         """D2H of the gathered masks and k, host plan, H2D of this rank's k (others' frames -1)."""
         torch = self.torch
+        # one D2H of the gathered masks and k into pinned buffers, one sync
+        if self.h_plan_in is None:
+            self.h_plan_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=self.cuda)
+                              for t in self.masks + [self.k]]
+        for h, t in zip(self.h_plan_in, self.masks + [self.k]):
+            h.copy_(t, non_blocking=self.cuda)
         if self.cuda:
             torch.cuda.current_stream().synchronize()
-        masks = [m.cpu().numpy() for m in self.masks]
-        k = self.k.cpu().numpy()
+        masks = [h.numpy() for h in self.h_plan_in[:-1]]
+        k = self.h_plan_in[-1].numpy()
         self.plan = p = self.make_plan(masks, k)
         mine = np.where(p["rank_of"] == self.rank, k, -1).astype(np.int32)
         self.h_k.copy_(torch.from_numpy(mine))

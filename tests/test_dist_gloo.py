@@ -80,6 +80,32 @@ def test_lpt_balance_and_determinism():
     assert a[0].tolist() == [0, 2] and a[1].tolist() == [1, 3]
 
 
+def _lpt_reference(costs, world):
+    """The LPT rule written out literally (the definition dist.lpt_assign implements): frames by
+    cost descending, ties by lower frame id; each goes to the least-loaded rank, ties lowest rank."""
+    costs = [int(c) for c in costs]
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    load = [0] * world
+    assign = [[] for _ in range(world)]
+    for i in order:
+        r = min(range(world), key=lambda j: (load[j], j))
+        assign[r].append(i)
+        load[r] += costs[i]
+    return [sorted(a) for a in assign], load
+
+
+def test_lpt_matches_the_rule():
+    rg = np.random.default_rng(3)
+    cases = [rg.integers(0, 10_000, size=168), rg.integers(0, 4, size=168),  # tie-heavy
+             np.zeros(21, np.int64), rg.integers(0, 2**40, size=200), np.array([7]), np.array([], np.int64)]
+    for costs in cases:
+        for world in (1, 2, 3, 4, 8):
+            assign, load = sdist.lpt_assign(costs, world)
+            want_a, want_l = _lpt_reference(costs, world)
+            assert [a.tolist() for a in assign] == want_a
+            assert load.tolist() == want_l
+
+
 def test_frame_costs_weighting():
     # a level-2 block (1280 ch) costs 16x a level-0 block (320 ch)
     c = sdist.frame_costs([[1, 0, 0], [0, 0, 1]], [320, 640, 1280])
