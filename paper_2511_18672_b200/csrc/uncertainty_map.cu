@@ -34,7 +34,10 @@ namespace sphinx {
 // rows outside the image are never produced; the clamped row always is, and is still in its
 // ring).  Three barriers per row; the window sums are plain sums in a fixed order.
 constexpr int kSW = 128;   // threads = strip columns
-constexpr int kSH = 64;    // output rows per CTA
+#ifndef SPHINX_UNC_KSH
+#define SPHINX_UNC_KSH 32
+#endif
+constexpr int kSH = SPHINX_UNC_KSH;  // output rows per CTA
 constexpr int kRing = 16;  // thread-private row rings (radius <= 7)
 
 template <bool RINGS>  // shared row rings only for runtime radii (compile-time radii: registers)
