@@ -510,6 +510,18 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
 #endif
   const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
   const int cluster_id = blockIdx.x / CG, n_clusters = gridDim.x / CG;
+  // early_list: the count and the plan's class counts are valid at launch, so their loads are
+  // issued here and their latency hides under the setup below (asm with memory clobbers keeps the
+  // compiler from sinking them)
+  int e_count = 0, e_nF = 0, e_nB = 0, e_nR = 0;
+  if (p.early_list) {
+    e_count = __ldg(p.count);
+    if (EDGE && p.plan_ids) {
+      e_nF = __ldg(p.plan_meta + 0);
+      e_nB = __ldg(p.plan_meta + 1);
+      e_nR = __ldg(p.plan_meta + 2);
+    }
+  }
   // ---- setup that needs no upstream data (overlaps the previous kernel's tail under PDL)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -548,15 +560,16 @@ __global__ void __launch_bounds__(NORM ? kThreadsNorm : kThreadsEpi8, 1)
 #ifdef SPHINX_TRACE
   if (threadIdx.x == 0) CONV_TRACE(1, gtimer());
 #endif
-  const int count = *p.count;
+  const int count = p.early_list ? e_count : *p.count;
   constexpr int BPT = kBM / (BLK * BLK);  // blocks per CTA tile (2 at b=8, 8 at b=4)
   constexpr int bb = BLK * BLK;
   const int bpt_pair = BPT * CG;  // blocks per (pair) tile
   // class counts (edge packing) -- without a plan every listed block is a "full" block
   const int32_t* list = (EDGE && p.plan_ids) ? p.plan_ids : p.ids;
-  const int nF = (EDGE && p.plan_ids) ? __ldg(p.plan_meta + 0) : count;
-  const int nB = (EDGE && p.plan_ids) ? __ldg(p.plan_meta + 1) : 0;
-  const int nR = (EDGE && p.plan_ids) ? __ldg(p.plan_meta + 2) : 0;
+  const bool planned = EDGE && p.plan_ids;
+  const int nF = planned ? (p.early_list ? e_nF : __ldg(p.plan_meta + 0)) : count;
+  const int nB = planned ? (p.early_list ? e_nB : __ldg(p.plan_meta + 1)) : 0;
+  const int nR = planned ? (p.early_list ? e_nR : __ldg(p.plan_meta + 2)) : 0;
   const int m_tiles = HALO ? (nF + 2 * CG - 1) / (2 * CG) +
                                  (nB + p.bpt_b * CG - 1) / (p.bpt_b * CG) +
                                  (nR + p.bpt_r * CG - 1) / (p.bpt_r * CG)

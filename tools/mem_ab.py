@@ -82,6 +82,18 @@ def main():
         out[f"mask{nf}_mbytes"] = round(nf * 576 * 576 * 8 / 1e6, 1)
         out[f"mask{nf}_warm_us"] = round(bench.graph_time(torch, f_mask) * 1e3, 2)
         out[f"mask{nf}_cold_us"] = round(cold(f_mask, flush) * 1e3, 2)
+        # step 2: the step's batched compaction (3 ACTIVE lists + the NOISE list) over these masks
+        kk = torch.from_numpy(rg.integers(0, 40, nf).astype(np.int32)).to(dev)
+        f_mask()
+        lists = [(torch.empty((nf * m.shape[1] * m.shape[2],), dtype=torch.int32, device=dev),
+                  torch.empty((1,), dtype=torch.int32, device=dev)) for m in masks + masks[:1]]
+        jobs = [dict(block_mask=masks[l], start_step=kk, step_u=25, select=sp.SELECT_ACTIVE, block_ids=lists[l][0],
+                     count=lists[l][1]) for l in range(3)] + \
+               [dict(block_mask=masks[0], start_step=kk, step_u=25, select=sp.SELECT_NOISE, block_ids=lists[3][0],
+                     count=lists[3][1])]
+        f_comp = lambda: sp.sphinx_compact_blocks_batch(jobs)
+        out[f"compact{nf}_warm_us"] = round(bench.graph_time(torch, f_comp) * 1e3, 2)
+        out[f"compact{nf}_cold_us"] = round(cold(f_comp, flush) * 1e3, 2)
     print(json.dumps(out), flush=True)
 
 

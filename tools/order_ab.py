@@ -4,6 +4,7 @@ interleaved anti-diagonal order (RefinementStep.conv_order).  Outputs must be bi
 A and B rounds so clock drift hits both.
 
     python tools/order_ab.py [configs2 configs3 ...]
+    AB_KNOB=fused_compaction python tools/order_ab.py ...   # another boolean StepConfig knob
 """
 import json
 import os
@@ -27,12 +28,13 @@ def main():
     torch.cuda.set_device(dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     res = {}
+    knob = os.environ.get("AB_KNOB", "interleave_levels")
     for name in (sys.argv[1:] or ["configs2", "configs3"]):
         batch = bench.make_batch(name)
         steps, graphs = {}, {}
         for il in (False, True):
             cfg = bench.step_config(bench.WORKLOADS[name]["means"])
-            cfg.interleave_levels = il
+            setattr(cfg, knob, il)
             st = RefinementStep(cfg, batch, dev, sp)
             g, _ = bench.capture_step(torch, st, with_conv_events=False)
             steps[il], graphs[il] = st, g
@@ -55,8 +57,11 @@ def main():
                     flush.fill_(1.0)
                     torch.cuda.synchronize()
                     ms[il].append(e0.elapsed_time(e1))
-        res[name] = {"level_order_ms": float(np.median(ms[False])), "interleaved_ms": float(np.median(ms[True])),
-                     "order": steps[True].conv_order()}
+        if knob == "interleave_levels":
+            res[name] = {"level_order_ms": float(np.median(ms[False])), "interleaved_ms": float(np.median(ms[True])),
+                         "order": steps[True].conv_order()}
+        else:
+            res[name] = {f"{knob}=False_ms": float(np.median(ms[False])), f"{knob}=True_ms": float(np.median(ms[True]))}
         print(json.dumps({name: res[name]}), flush=True)
         del steps, graphs
         torch.cuda.empty_cache()
