@@ -747,9 +747,13 @@ def run_gpu(args):
             "clocks": summarize_clocks(clk_lines),
         }
         if world > 1:
-            line["gpu_launches"] = None
-            line["gpu_launches_note"] = "eager multi-rank step: per rank ~%d sphinx kernels + NCCL" % (
-                st.launches_per_step + 4 * L)
+            # rank 0's own kernels in the timed steps (every rank launches its own share): the step's
+            # kernels on its frames plus the owner-gather pack / unpack kernels of its exchanges
+            line["gpu_launches"] = int((st.launches_per_step + st.exchange_launches) * reps)
+            line["gpu_launches_note"] = ("rank 0: %d sphinx kernels per step (%d step + %d owner-gather pack/"
+                                         "unpack), eager multi-rank step; NCCL kernels not counted" % (
+                                             st.launches_per_step + st.exchange_launches, st.launches_per_step,
+                                             st.exchange_launches))
         line.update(extras)
         line["e2e"] = extras.get("e2e") if world == 1 else e2e_sh
         line["cpu_baseline"] = cpu

@@ -371,6 +371,7 @@ class RefinementStep:
             for mp, ch, dt, tag in items:
                 pay = self._payload((tag, l, "s"), (n_mine, b, b, ch), dt)
                 ops.sphinx_gather_blocks(mp, pay, b, self.ids[l], self.cnt[l])
+                self.exchange_launches += 1
                 rpay = self._payload((tag, l, "r"), (n_recv, b, b, ch), dt)
                 off = 0
                 for o, n in sends_n:
@@ -396,6 +397,7 @@ class RefinementStep:
                 for rpay, mp in unpack:
                     ops.sphinx_scatter_blocks(rpay, mp, b, self.recv_ids[l], self.recv_cnt[l:l + 1],
                                               capacity=n_recv)
+                    self.exchange_launches += 1
             self.bytes_sent += sum(t.numel() for _, t in sends)
         if self.cuda:
             e1.record(self.comm_stream)
@@ -405,6 +407,7 @@ class RefinementStep:
     def run(self, conv_events=None):
         """One refinement step (all of SURVEY 8(a)) on this rank's share of the batch."""
         self.bytes_sent = 0
+        self.exchange_launches = 0  # pack / unpack kernels of the owner gather this step (N > 1)
         self.comm_events = []
         self._masks()
         if self.world > 1:
