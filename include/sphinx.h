@@ -109,7 +109,7 @@ typedef struct {
 
 SPHINX_API int32_t sphinx_abi_version(void);      /* returns SPHINX_ABI_VERSION */
 SPHINX_API int32_t sphinx_last_cuda_error(void);  /* cudaError_t of the last SPHINX_ERR_CUDA on this thread */
-#define SPHINX_ABI_VERSION 9
+#define SPHINX_ABI_VERSION 10
 
 /* ---------------------------------------------------------------------------------
  * (1) Block mask + start step.
@@ -176,6 +176,33 @@ typedef struct {
 } sphinx_compact_job;
 SPHINX_API sphinx_status sphinx_compact_blocks_batch(const sphinx_compact_job* jobs, int32_t n_jobs,
                                                      sphinx_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
+ * Multi-GPU data plane (P:333 frames are the independent units; north_star "balanced
+ * by active-block count"): the frame -> rank plan, computed on the device by every rank from the
+ * all-gathered masks and start steps, identical on every rank (deterministic):
+ *   cost[f] = sum_l count_l[f] * C_l^2, count_l[f] = blocks with mask 1 in frame f at level l if
+ *             0 <= k[f] <= u, else 0 (the executed MMA work of frame f at this step);
+ *   frames by cost descending (frame id ascending on ties) each go to the least-loaded rank
+ *   (lowest rank on ties): longest processing time first.
+ * block_mask        HOST array of n_levels DEVICE pointers, u8 [n][blocks_per_frame[l]].
+ * blocks_per_frame  HOST [n_levels]: hb_l * wb_l.      channels  HOST [n_levels]: C_l.
+ * start_step        int32 [n] device (all ranks' frames).   step_u  u of Alg1's loop.
+ * owner             int32 [n] device: the rank that owns frame f's request (receives its blocks).
+ * world, rank       ranks and this rank (1 <= world <= 32; n <= 4096).
+ * Outputs (device): k_mine int32 [n] = start_step of this rank's frames, -1 elsewhere (the input of
+ * this rank's compaction); rank_of int32 [n]; load int64 [world] (sum of the ranks' costs);
+ * pair int32 [n_levels][world][world] = level-l blocks rank s computes for frames rank o owns;
+ * recv int32 [n_levels] = blocks this rank receives per level (sum over s != rank of pair[l][s][rank]).
+ * One 1024-thread CTA; no host synchronisation (the host reads pair back only to size the NCCL
+ * send / recv of the owner gather).
+ * ------------------------------------------------------------------------------- */
+SPHINX_API sphinx_status sphinx_shard_plan(uint8_t* const* block_mask, const int32_t* blocks_per_frame,
+                                           const int32_t* channels, int32_t n_levels, int32_t n,
+                                           const int32_t* start_step, int32_t step_u, const int32_t* owner,
+                                           int32_t world, int32_t rank, int32_t* k_mine, int32_t* rank_of,
+                                           int64_t* load, int32_t* pair, int32_t* recv,
+                                           sphinx_stream_t stream);
 
 /* ---------------------------------------------------------------------------------
  * (3) Forward noise on listed blocks (Alg1 line 12 add_noise(Z0, k_min); line 19

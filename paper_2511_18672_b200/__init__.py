@@ -29,7 +29,7 @@ BF16, F32 = 0, 1
 SELECT_ACTIVE, SELECT_INACTIVE_FRAMES, SELECT_ALL, SELECT_NOISE = 0, 1, 2, 3
 SRC_FULL, SRC_COMPACT = 0, 1
 MAX_LOGICS = 8
-ABI_VERSION = 9
+ABI_VERSION = 10
 EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_compact_blocks", "sphinx_noise_inject", "sphinx_sparse_conv3x3",
            "sphinx_conv_workspace_size", "sphinx_scatter_cached", "sphinx_ddim_step",
@@ -41,7 +41,7 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex",
            "sphinx_sparse_resblock_ex", "sphinx_temporal_attention_ex", "sphinx_gather_blocks",
            "sphinx_scatter_blocks", "sphinx_noise_inject_step",
-           "sphinx_conv_edge_plan")
+           "sphinx_conv_edge_plan", "sphinx_shard_plan")
 
 _lib = None
 
@@ -114,6 +114,7 @@ def load(path=SO_PATH):
         "sphinx_last_cuda_error": ([], I),
         "sphinx_block_mask": ([P, P, P, F, I, I, I, I, I, I, P, P, P, P, P], I),
         "sphinx_compact_blocks": ([P, I, I, I, P, I, I, P, P, P], I),
+        "sphinx_shard_plan": ([P, P, P, I, I, P, I, P, I, I, P, P, P, P, P, P], I),
         "sphinx_noise_inject": ([P, P, P, I, I, I, I, I, P, P, I, P, P, I, P], I),
         "sphinx_sparse_conv3x3": ([P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_conv_workspace_size": ([I, I, I, I, I, I], Z),
@@ -250,6 +251,30 @@ def sphinx_compact_blocks_batch(jobs, stream=None):
                             jb["count"].data_ptr())
     rc = load().sphinx_compact_blocks_batch(ctypes.cast(arr, ctypes.c_void_p), len(jobs), _stream(stream))
     _chk("sphinx_compact_blocks_batch", rc)
+
+
+def sphinx_shard_plan(block_masks, channels, start_step, step_u, owner, world, rank, k_mine, rank_of, rank_load,
+                      pair, recv, stream=None):
+    """§8(e) frame -> rank LPT plan on the device (sphinx.h).  block_masks: list of u8 [N,Hb_l,Wb_l];
+    channels: host ints C_l; start_step/owner/k_mine/rank_of int32 [N]; rank_load int64 [world];
+    pair int32 [L,world,world]; recv int32 [L]."""
+    import torch
+    L = len(block_masks)
+    for m in block_masks:
+        _dev(m, torch.uint8, "block_mask")
+    for t, nm in ((start_step, "start_step"), (owner, "owner"), (k_mine, "k_mine"), (rank_of, "rank_of"),
+                  (pair, "pair"), (recv, "recv")):
+        _dev(t, torch.int32, nm)
+    _dev(rank_load, torch.int64, "rank_load")
+    n = block_masks[0].shape[0]
+    masks = (ctypes.c_void_p * L)(*[m.data_ptr() for m in block_masks])
+    bpf = (ctypes.c_int32 * L)(*[int(m.shape[1] * m.shape[2]) for m in block_masks])
+    ch = (ctypes.c_int32 * L)(*[int(c) for c in channels])
+    rc = load().sphinx_shard_plan(ctypes.cast(masks, ctypes.c_void_p), ctypes.cast(bpf, ctypes.c_void_p),
+                                      ctypes.cast(ch, ctypes.c_void_p), L, int(n), _ptr(start_step), int(step_u),
+                                      _ptr(owner), int(world), int(rank), _ptr(k_mine), _ptr(rank_of), _ptr(rank_load),
+                                      _ptr(pair), _ptr(recv), _stream(stream))
+    _chk("sphinx_shard_plan", rc)
 
 
 def sphinx_noise_inject(x0, eps, x_t, block, block_ids, count, step, abar, capacity=None,

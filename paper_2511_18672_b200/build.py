@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libsphinx.so")
 SOURCES = ["abi.cu", "block_mask.cu", "compact.cu", "noise_inject.cu", "sparse_conv3x3.cu",
            "scatter_cached.cu", "ddim_step.cu",
-           "uncertainty_map.cu", "group_norm.cu", "temporal_attn.cu", "block_copy.cu"]
+           "uncertainty_map.cu", "group_norm.cu", "temporal_attn.cu", "block_copy.cu", "shard_plan.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
               "-cudart", "static"]

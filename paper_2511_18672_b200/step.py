@@ -19,8 +19,10 @@ Sharded (world = N > 1; "spatial ResNet layers ... per frame", SURVEY 8(e)
     1. every rank runs sphinx_block_mask on its contiguous slice of F/N frames;
     2. C1: NCCL all-gather of the slices' block masks and start steps (the per-frame active
        counts follow from them), so every rank holds the whole batch's masks;
-    3. every rank computes the SAME deterministic LPT plan on the host (dist.lpt_assign, frames
-       weighted by executed MMA work sum_l count[n,l] C_l^2 at this u) -- one small D2H per step;
+    3. every rank computes the SAME deterministic LPT plan ON THE DEVICE (sphinx_shard_plan, frames
+       weighted by executed MMA work sum_l count[n,l] C_l^2 at this u; the host twin is make_plan /
+       dist.lpt_assign); the host reads the exchange sizes back only when it issues the exchange,
+       after the convs are queued;
     4. compaction over the frames assigned to this rank (k of other frames masked to -1), then
        noise, convs and the latent scatter exactly as on one rank;
     5. C2: after each level, the refined blocks of frames owned by another rank (request j is
@@ -198,17 +200,26 @@ class RefinementStep:
         self.launches_per_step = 2 + 1 + n_edge + 1 + L * cfg.convs_per_level + 1
         self.conv_events = None
         self.comm = None
+        self._plan, self._plan_pending = None, False
         if world > 1:
             self.tp = _Transport(group)
             self.slice = slice(rank * F // world, (rank + 1) * F // world)
             self.owner = cfg.owner_of_frame(world)
             self.comm_stream = torch.cuda.Stream(device=self.dev) if self.cuda else None
-            self.h_k = torch.zeros((F,), dtype=i32).pin_memory() if self.cuda else torch.zeros((F,), dtype=i32)
-            self.plan = None
-            self.h_plan_in = None
+            # the frame -> rank plan lives on the device (sphinx_shard_plan); the host reads back only
+            # what sizes the owner gather, when it issues it
+            self.owner_d = torch.from_numpy(self.owner.astype(np.int32)).to(self.dev)
+            self.rank_of_d = torch.zeros((F,), dtype=i32, device=self.dev)
+            self.load_d = torch.zeros((world,), dtype=torch.int64, device=self.dev)
+            self.pair_d = torch.zeros((L, world, world), dtype=i32, device=self.dev)
+            pin = dict(pin_memory=True) if self.cuda else {}
+            self.h_rank_of = torch.zeros((F,), dtype=i32, **pin)
+            self.h_load = torch.zeros((world,), dtype=torch.int64, **pin)
+            self.h_pair = torch.zeros((L, world, world), dtype=i32, **pin)
+            self.plan_ev = torch.cuda.Event() if self.cuda else None
+            self._plan, self._plan_pending = None, False
             self.recv_ids = [torch.zeros((F * hb * hb,), dtype=i32, device=self.dev) for hb in cfg.hb]
             self.recv_cnt = torch.zeros((L,), dtype=i32, device=self.dev)
-            self.h_recv_cnt = torch.zeros((L,), dtype=i32).pin_memory() if self.cuda else torch.zeros((L,), dtype=i32)
             self._pay = {}
 
     # ------------------------------------------------------------------ pieces of the step
@@ -251,26 +262,33 @@ class RefinementStep:
         return dict(rank_of=rank_of, load=load, cnt=cnt, pair=pair,
                     imbalance=float(load.max() / max(load.mean(), 1e-9)))
 
-    def _plan_step(self):
-        """D2H of the gathered masks and k, host plan, H2D of this rank's k (others' frames -1)."""
-        torch = self.torch
-        # one D2H of the gathered masks and k into pinned buffers, one sync
-        if self.h_plan_in is None:
-            self.h_plan_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=self.cuda)
-                              for t in self.masks + [self.k]]
-        for h, t in zip(self.h_plan_in, self.masks + [self.k]):
+    def _plan_device(self):
+        """The LPT plan on the device from the gathered masks and k (sphinx_shard_plan: the same rule
+        as make_plan, on every rank): this rank's k_mine and the receive counts stay on the device;
+        the exchange sizes, loads and assignment are copied back asynchronously."""
+        cfg = self.cfg
+        self.ops.sphinx_shard_plan(self.masks, [c for (_, c) in cfg.levels], self.k, cfg.u, self.owner_d,
+                                   self.world, self.rank, self.k_mine, self.rank_of_d, self.load_d, self.pair_d,
+                                   self.recv_cnt)
+        for h, t in ((self.h_pair, self.pair_d), (self.h_load, self.load_d), (self.h_rank_of, self.rank_of_d)):
             h.copy_(t, non_blocking=self.cuda)
         if self.cuda:
-            torch.cuda.current_stream().synchronize()
-        masks = [h.numpy() for h in self.h_plan_in[:-1]]
-        k = self.h_plan_in[-1].numpy()
-        self.plan = p = self.make_plan(masks, k)
-        mine = np.where(p["rank_of"] == self.rank, k, -1).astype(np.int32)
-        self.h_k.copy_(torch.from_numpy(mine))
-        recv = p["pair"][:, :, self.rank].sum(1) - p["pair"][:, self.rank, self.rank]
-        self.h_recv_cnt.copy_(torch.from_numpy(recv.astype(np.int32)))
-        self.k_mine.copy_(self.h_k, non_blocking=True)
-        self.recv_cnt.copy_(self.h_recv_cnt, non_blocking=True)
+            self.plan_ev.record()
+        self._plan, self._plan_pending = None, True
+
+    @property
+    def plan(self):
+        """The step's plan on the host (rank_of, load, pair [L][sender][owner], imbalance); waits for
+        the read-back of sphinx_shard_plan's outputs the first time it is needed in a step."""
+        if self._plan_pending:
+            if self.cuda:
+                self.plan_ev.synchronize()
+            load = self.h_load.numpy().astype(np.int64)
+            self._plan = dict(rank_of=self.h_rank_of.numpy().astype(np.int64), load=load,
+                              pair=self.h_pair.numpy().astype(np.int64),
+                              imbalance=float(load.max() / max(load.mean(), 1e-9)))
+            self._plan_pending = False
+        return self._plan
 
     def _compute(self, conv_events=None):
         cfg, ops, d = self.cfg, self.ops, self.d
@@ -411,7 +429,7 @@ class RefinementStep:
         self.comm_events = []
         self._masks()
         if self.world > 1:
-            self._plan_step()
+            self._plan_device()
         self._compute(conv_events)
         if self.world > 1 and self.cuda:
             self.torch.cuda.current_stream().wait_stream(self.comm_stream)

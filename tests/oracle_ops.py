@@ -49,6 +49,28 @@ def sphinx_compact_blocks_batch(jobs):
         j["count"].fill_(len(ids))
 
 
+def sphinx_shard_plan(masks, channels, k, u, owner, world, rank, k_mine, rank_of, rank_load, pair, recv):
+    """Host twin of the device plan (the rule of sphinx.h / dist.lpt_assign) on CPU tensors."""
+    from paper_2511_18672_b200 import dist as sdist
+    kk = _np(k)
+    act = (kk >= 0) & (kk <= u)
+    F = len(kk)
+    cnt = np.stack([_np(m).reshape(F, -1).astype(np.int64).sum(1) * act for m in masks], 1)
+    assign, load = sdist.lpt_assign(sdist.frame_costs(cnt, channels), world)
+    ro = np.zeros(F, np.int64)
+    for r, fr in enumerate(assign):
+        ro[fr] = r
+    own = _np(owner).astype(np.int64)
+    pr = np.zeros((len(masks), world, world), np.int64)
+    for l in range(len(masks)):
+        np.add.at(pr[l], (ro, own), cnt[:, l])
+    rank_of.copy_(torch.from_numpy(ro.astype(np.int32)))
+    rank_load.copy_(torch.from_numpy(load.astype(np.int64)))
+    pair.copy_(torch.from_numpy(pr.astype(np.int32)))
+    k_mine.copy_(torch.from_numpy(np.where(ro == rank, kk, -1).astype(np.int32)))
+    recv.copy_(torch.from_numpy((pr[:, :, rank].sum(1) - pr[:, rank, rank]).astype(np.int32)))
+
+
 def sphinx_conv_edge_plan(*a, **k):
     pass
 

@@ -160,3 +160,42 @@ def test_gather_scatter_blocks_bit_copy(sphinx):
                 assert np.array_equal(p16[j, :ry, :rx], s16[f, by * b:by * b + ry, bx * b:bx * b + rx])
             assert np.array_equal(o16[listed], s16[listed])
             assert np.all(o16[~listed] == 0x1234)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_plan_device_equals_host_rule(sphinx, world):
+    """sphinx_shard_plan on the device = the LPT rule on the host (dist.lpt_assign over
+    sum_l count*C_l^2 of the frames active at u), for every rank: assignment, loads, exchange
+    matrix, k_mine and receive counts; random masks with many equal costs (ties), excluded frames
+    (k < 0, k > u), 168 frames."""
+    from paper_2511_18672_b200 import dist as sdist
+    rg = np.random.default_rng(world)
+    F, u, chans, hbs = 168, 25, [320, 640, 1280], [9, 5, 3]
+    for rnd in range(3):
+        masks = [(rg.random((F, hb, hb)) < (0.05 if rnd == 2 else 0.3)).astype(np.uint8) for hb in hbs]
+        k = rg.integers(-1, 40, F).astype(np.int32)
+        owner = ((np.arange(F) // 21) * world // 8).astype(np.int32)
+        act = (k >= 0) & (k <= u)
+        cnt = np.stack([m.reshape(F, -1).astype(np.int64).sum(1) * act for m in masks], 1)
+        assign, load = sdist.lpt_assign(sdist.frame_costs(cnt, chans), world)
+        ro = np.zeros(F, np.int64)
+        for r, fr in enumerate(assign):
+            ro[fr] = r
+        pr = np.zeros((3, world, world), np.int64)
+        for l in range(3):
+            np.add.at(pr[l], (ro, owner), cnt[:, l])
+        md = [torch.from_numpy(m).cuda() for m in masks]
+        kd, od = torch.from_numpy(k).cuda(), torch.from_numpy(owner).cuda()
+        for rank in range(world):
+            out = dict(k_mine=torch.full((F,), 9, dtype=torch.int32, device="cuda"),
+                       rank_of=torch.full((F,), 9, dtype=torch.int32, device="cuda"),
+                       rank_load=torch.full((world,), 9, dtype=torch.int64, device="cuda"),
+                       pair=torch.full((3, world, world), 9, dtype=torch.int32, device="cuda"),
+                       recv=torch.full((3,), 9, dtype=torch.int32, device="cuda"))
+            sphinx.sphinx_shard_plan(md, chans, kd, u, od, world, rank, **out)
+            torch.cuda.synchronize()
+            assert np.array_equal(out["rank_of"].cpu().numpy(), ro)
+            assert np.array_equal(out["rank_load"].cpu().numpy(), load)
+            assert np.array_equal(out["pair"].cpu().numpy(), pr)
+            assert np.array_equal(out["k_mine"].cpu().numpy(), np.where(ro == rank, k, -1))
+            assert np.array_equal(out["recv"].cpu().numpy(), pr[:, :, rank].sum(1) - pr[:, rank, rank])
