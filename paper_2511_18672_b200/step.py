@@ -129,6 +129,11 @@ class _Transport:
                 t.copy_(h)
 
 
+def torch_int32():
+    import torch
+    return torch.int32
+
+
 def torch_cat(parts):
     import torch
     return torch.cat(parts)
@@ -218,6 +223,15 @@ class RefinementStep:
             self.h_pair = torch.zeros((L, world, world), dtype=i32, **pin)
             self.plan_ev = torch.cuda.Event() if self.cuda else None
             self._plan, self._plan_pending = None, False
+            # packed C1 buffer: row r = rank r's slice [mask level 0 | ... | mask level L-1 | k (int32)]
+            fs = F // world
+            off, self.gath_lv = 0, []
+            for hb in cfg.hb:
+                self.gath_lv.append((off, fs * hb * hb, (fs, hb, hb)))
+                off += fs * hb * hb
+            off = (off + 15) // 16 * 16
+            self.gath_k = (off, 4 * fs)
+            self.gath = torch.zeros((world, (off + 4 * fs + 15) // 16 * 16), dtype=u8, device=self.dev)
             self.recv_ids = [torch.zeros((F * hb * hb,), dtype=i32, device=self.dev) for hb in cfg.hb]
             self.recv_cnt = torch.zeros((L,), dtype=i32, device=self.dev)
             self._pay = {}
@@ -235,12 +249,20 @@ class RefinementStep:
                                   self._start_args(), self.k)
             return
         sl = self.slice
-        ops.sphinx_block_mask(d["O"][sl], d["U"][sl], d["tau_u"][sl], cfg.tau_o, cfg.f, cfg.b,
-                              [m[sl] for m in self.masks], self.counts[sl], self._start_args(sl), self.k[sl])
+        # the slice's masks and start steps are written straight into this rank's row of one packed
+        # buffer [world][level masks | k], so C1 is ONE all-gather (not one per level + one for k)
+        mine = self.gath[self.rank]
+        views = [mine[o:o + n].view(shp) for (o, n, shp) in self.gath_lv]
+        ko, kn = self.gath_k
+        kv = mine[ko:ko + kn].view(torch_int32())
+        ops.sphinx_block_mask(d["O"][sl], d["U"][sl], d["tau_u"][sl], cfg.tau_o, cfg.f, cfg.b, views,
+                              self.counts[sl], self._start_args(sl), kv)
         # C1: every rank gets the whole batch's masks and start steps
-        for m in self.masks:
-            self.tp.all_gather_into(m, m[sl])
-        self.tp.all_gather_into(self.k, self.k[sl])
+        self.tp.all_gather_into(self.gath.view(-1), mine)
+        w = self.world
+        for m, (o, n, _) in zip(self.masks, self.gath_lv):
+            m.view(w, n).copy_(self.gath[:, o:o + n])
+        self.k.view(w, kn // 4).copy_(self.gath[:, ko:ko + kn].view(torch_int32()))
 
     def make_plan(self, masks, k):
         """Host plan from the batch's masks [L][F,Hb,Wb] and start steps k [F] (numpy): LPT
