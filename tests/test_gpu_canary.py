@@ -154,3 +154,18 @@ def test_canary_gather_scatter_and_uncertainty(sphinx):
     sphinx.sphinx_uncertainty_map(rgb, U.t, tau.t)
     U.check("uncertainty map")
     tau.check("tau_u")
+
+
+def test_canary_shard_plan(sphinx):
+    """sphinx_shard_plan writes exactly its five outputs (k_mine, rank_of, load, pair, recv)."""
+    rg = np.random.default_rng(5)
+    F, world, u = 50, 4, 25
+    masks = [T((rg.random((F, hb, hb)) < 0.3).astype(np.uint8)) for hb in (9, 5, 3)]
+    k = T(rg.integers(-1, 40, F).astype(np.int32))
+    owner = T((np.arange(F) * world // F).astype(np.int32))
+    outs = dict(k_mine=Guarded((F,), torch.int32), rank_of=Guarded((F,), torch.int32),
+                rank_load=Guarded((world,), torch.int64), pair=Guarded((3, world, world), torch.int32),
+                recv=Guarded((3,), torch.int32))
+    sphinx.sphinx_shard_plan(masks, [320, 640, 1280], k, u, owner, world, 1, **{k_: g.t for k_, g in outs.items()})
+    for k_, g in outs.items():
+        g.check(f"shard_plan {k_}")
