@@ -75,6 +75,26 @@ def make_batch(name):
 
 # ----------------------------------------------------------------- measurement helpers
 
+def ncu_tensor_pct(kernel_sig):
+    """Mean ncu sm__pipe_tensor_cycles_active (% of peak, elapsed) of the conv launches whose name
+    contains kernel_sig, from the newest committed `ncu --set full` capture of the configs[3] step
+    (profiles/*_conv_full_raw.csv).  Returns (percent or None, source file)."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_conv_full_raw.csv")))
+    if not files:
+        return None, None
+    rows = list(csv.reader(open(files[-1])))
+    if len(rows) < 3:
+        return None, None
+    idx = {h: i for i, h in enumerate(rows[0])}
+    m = "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"
+    if m not in idx:
+        return None, os.path.basename(files[-1])
+    vals = [float(r[idx[m]].replace(",", "")) for r in rows[2:] if kernel_sig in r[idx["Kernel Name"]]]
+    return (round(sum(vals) / len(vals), 2) if vals else None), os.path.basename(files[-1])
+
+
 def ncu_traffic(kernel_sig):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes) of the conv launches whose
     name contains kernel_sig, from the newest committed `ncu --set full` capture
@@ -490,7 +510,9 @@ def temporal_levels(torch, st, reps=20):
 
 # ----------------------------------------------------------------- GPU arm
 
-def conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms_all):
+def conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms_all, with_ncu=False):
+    """Per-level conv times and rates; with_ncu (the configs[3] headline, the workload the committed
+    ncu capture profiles): each level's ncu tensor-pipe activity from that capture."""
     cfg = st.cfg
     per_level = []
     for l, (h, c) in enumerate(cfg.levels):
@@ -502,6 +524,11 @@ def conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms_all):
                           "conv_ms_each": [round(statistics.mean(conv_ms[l][j]), 5) for j in range(CONVS_PER_LEVEL)],
                           "tflops": round(f_l / (t_l * 1e-3) / 1e12, 2),
                           "frac_burst": round(f_l / (t_l * 1e-3) / 1e12 / tc_peak, 4)})
+        if with_ncu:
+            bn_l = 256 if c % 256 == 0 and c > 640 else 160
+            pct, src = ncu_tensor_pct(f"<{bn_l}, 2, 8, 1, {1 if h % cfg.b else 0}, 0>")
+            per_level[-1]["ncu_tensor_pipe_pct"] = pct
+            per_level[-1]["ncu_source"] = src
     conv_total_ms = sum(p["conv_ms"] for p in per_level) * CONVS_PER_LEVEL
     dom = max(per_level, key=lambda p: p["conv_ms"])
     dom_flops = dom["real_px"] * 2 * 9 * cfg.levels[dom["level"]][1] ** 2
@@ -689,7 +716,8 @@ def run_gpu(args):
         per_level, roof = conv_level_stats(st, conv_ms, my_px, my_blocks, tc_peak, tc_sust, ms)
         roof["scope"] = "rank 0's own conv launches (its share of the batch)"
     else:
-        per_level, roof = conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms)
+        per_level, roof = conv_level_stats(st, conv_ms, px_l, blocks_l, tc_peak, tc_sust, ms,
+                                           with_ncu=(name == "configs3"))
 
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
