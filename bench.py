@@ -367,21 +367,25 @@ def memory_kernels(torch, st, reps=10):
             torch.cuda.synchronize()
             if i >= 2:
                 ts.append(e0.elapsed_time(e1))
+        warm.append(graph_time(torch, fn))  # warm as well (back-to-back launches, L2-warm)
         return statistics.median(ts)
 
     out = {}
+    warm = []
 
     def row(name, ms, nbytes, note):
         out[name] = {"ms": round(ms, 5), "algorithmic_bytes": int(nbytes),
                      "gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
-                     "hbm_frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": note}
+                     "hbm_frac": round(nbytes / (ms * 1e-3) / 1e9 / hbm, 4), "bytes": note,
+                     "warm_ms": round(warm[-1], 5), "warm_gbs": round(nbytes / (warm[-1] * 1e-3) / 1e9, 1)}
     n, hp = cfg.n_frames, cfg.hp
     ms = timed(lambda: sp.sphinx_block_mask(d["O"], d["U"], d["tau_u"], cfg.tau_o, cfg.f, cfg.b, st.masks,
                                             st.counts, st._start_args(), st.k))
     row("block_mask", ms, n * hp * hp * 8, "two fp32 maps read (8 B/px)")
     cnt = int(st.cnt[0].item())
     ms = timed(lambda: sp.sphinx_compact_blocks(st.masks[0], st.k, cfg.u, sp.SELECT_ACTIVE, st.ids[0], st.cnt[0]))
-    out["compact_blocks"] = {"ms": round(ms, 5), "entries": n * cfg.hb[0] ** 2, "bound": "latency (one CTA)"}
+    out["compact_blocks"] = {"ms": round(ms, 5), "entries": n * cfg.hb[0] ** 2, "bound": "latency (one CTA)",
+                             "warm_ms": round(warm[-1], 5)}
     ms = timed(lambda: sp.sphinx_noise_inject(d["x0"], d["eps"], st.zt, cfg.b, st.ids[0], st.cnt[0], st.k,
                                               d["abar"]))
     row("noise_inject", ms, cnt * 64 * cfg.c_lat * 12, "12 B per active latent element (x0, eps in; x_t out)")
@@ -402,8 +406,9 @@ def memory_kernels(torch, st, reps=10):
     tau = torch.empty((nu,), device=dev, dtype=torch.float32)
     ms = timed(lambda: sp.sphinx_uncertainty_map(rgb, U, tau))
     row("uncertainty_map (NEXT-2, 21 frames)", ms, nu * hp * hp * 16, "rgb read 12 B/px + U write 4 B/px")
-    out["timing"] = ("one launch per sample in a CUDA graph replayed behind a 256 MB write + 256 MB read "
-                     "L2 flush (clean cold L2), median of 10")
+    out["timing"] = ("ms: one launch per sample in a CUDA graph replayed behind a 256 MB write + 256 MB read "
+                     "L2 flush (clean cold L2), median of 10; warm_ms: CUDA graph of 20 back-to-back launches "
+                     "(L2-warm), per launch, median of 5 replays")
     return out
 
 
