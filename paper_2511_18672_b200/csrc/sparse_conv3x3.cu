@@ -1738,7 +1738,13 @@ static sphinx_status conv_impl(const void* x, const void* w, const float* bias, 
     p.ws_tiles = (int)(kCntBytes / (2 * sizeof(int32_t))) / cg;
   }
   const long long max_tiles = (long long)cdiv(capacity, p.bpt * cg) * p.n_tiles_n;
-  const int max_clusters = sms / cg;
+  int max_clusters = sms / cg;
+#ifdef SPHINX_DEV_KNOBS
+  if (const char* env = getenv("SPHINX_GRID_CAP")) {  // dev build: fewer SMs (ingress-limit probe)
+    const int v = atoi(env) / cg;
+    if (v >= 1 && v < max_clusters) max_clusters = v;
+  }
+#endif
   const long long want = p.ws_part ? max_tiles * 16 : max_tiles;  // split-K may multiply units
   const int grid = cg * (int)(want < max_clusters ? want : max_clusters);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
