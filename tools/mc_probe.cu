@@ -26,9 +26,10 @@ __device__ __forceinline__ void tma_load_3d_mc(const CUtensorMap* m, uint64_t* b
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32) probe(const __grid_constant__ CUtensorMap tm,
-                                                                       int rounds, int slots, int rows, int mc) {
+                                                                       int rounds, int slots, int rows, int mc,
+                                                                       int box, int strided) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + slots * kBox);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + slots * kBox);  // slots hold up to kBox bytes
   uint64_t* empty = bar + slots;
   const uint32_t rank = cluster_ctarank();
   if (threadIdx.x == 0) {
@@ -37,7 +38,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32) probe(const __gr
       mbar_init(&empty[s], 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < slots; ++s) mbar_arrive_expect_tx(&bar[s], kBox);
+    for (int s = 0; s < slots; ++s) mbar_arrive_expect_tx(&bar[s], box);
   }
   __syncwarp();
   cluster_sync();
@@ -46,7 +47,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32) probe(const __gr
     for (int s = 0; s < slots; ++s) {
       st = st * 6364136223846793005ull + 1442695040888963407ull;
       const int row = (int)((st >> 33) & (uint64_t)(rows - 1));
-      if (!mc) {
+      if (strided) {  // weight tile: (tap, chunk) index and a block of 80 output channels
+        tma_load_3d(&tm, &bar[s], smem + s * kBox, 0, (int)((st >> 40) % 45), 80 * (int)((st >> 50) & 3),
+                    policy_evict_normal());
+      } else if (!mc) {
         tma_load_3d(&tm, &bar[s], smem + s * kBox, 0, 0, row, policy_evict_normal());
       } else if ((uint32_t)(s & 1) == rank) {
         if (k > 0) mbar_wait(&empty[s], (uint32_t)((k - 1) & 1));
@@ -55,7 +59,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32) probe(const __gr
     }
     for (int s = 0; s < slots; ++s) {
       mbar_wait(&bar[s], (uint32_t)(k & 1));
-      if (k + 1 < rounds) mbar_arrive_expect_tx(&bar[s], kBox);
+      if (k + 1 < rounds) mbar_arrive_expect_tx(&bar[s], box);
       if (mc) {
         uint32_t r;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(&empty[s])), "r"((uint32_t)(s & 1)));
@@ -93,21 +97,35 @@ int main() {
     printf("encode fail\n");
     return 1;
   }
+  // strided variant: the conv's weight tiles, 80 rows of 128 B (64 channels of one output channel
+  // and tap) with a row stride of 9 * 320 * 2 = 5760 B (OHWI weights, C_in = 320), 10 KB per box
+  CUtensorMap tms;
+  {
+    cuuint64_t d2[3] = {64, 45, 320};  // [C_out = 320][45 (tap, chunk)][64 ch]
+    cuuint64_t s2[2] = {128, 5760};
+    cuuint32_t b2[3] = {64, 1, 80};
+    if (enc(&tms, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, d2, s2, b2, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS) {
+      printf("encode fail (strided)\n");
+      return 1;
+    }
+  }
   const int slots = 8;  // 128 KB in flight per CTA
   const int smem = slots * kBox + 2 * slots * 8 + 64;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   printf("mode,ctas,GBps_landed,GBps_per_SM_landed,GBps_per_SM_issued\n");
   for (int ctas = 16; ctas <= sms; ctas *= 2) {
     const int g = ctas > sms ? sms : ctas;
-    for (int mc = 0; mc < 2; ++mc) {
-      const int rounds = 400;
+    for (int mode = 0; mode < 3; ++mode) {  // 0 unicast, 1 multicast (16 KB contiguous), 2 unicast strided
+      const int rounds = 400, mc = mode == 1, strided = mode == 2, box = strided ? 10240 : kBox;
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       float ms = 0;
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(a);
-        probe<<<g - (g & 1), 32, smem>>>(tm, rounds, slots, rows, mc);
+        probe<<<g - (g & 1), 32, smem>>>(strided ? tms : tm, rounds, slots, rows, mc, box, strided);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         cudaEventElapsedTime(&ms, a, b);
@@ -117,8 +135,9 @@ int main() {
         return 1;
       }
       const int n = g - (g & 1);
-      const double landed = (double)rounds * slots * kBox * n;  // every CTA receives every slot each round
-      printf("%s,%d,%.0f,%.1f,%.1f\n", mc ? "multicast" : "unicast", n, landed / ms / 1e6, landed / ms / 1e6 / n,
+      const double landed = (double)rounds * slots * box * n;  // every CTA receives every slot each round
+      const char* nm = mode == 0 ? "unicast" : (mode == 1 ? "multicast" : "unicast_weight_tiles");
+      printf("%s,%d,%.0f,%.1f,%.1f\n", nm, n, landed / ms / 1e6, landed / ms / 1e6 / n,
              landed / ms / 1e6 / n / (mc ? 2 : 1));
     }
     if (ctas * 2 > sms && ctas < sms) ctas = sms / 2;
