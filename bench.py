@@ -778,6 +778,8 @@ def run_gpu(args):
             "paper_context": "1.8x average end-to-end speedup vs diffusion-only on 4x A40 (P:34, P:445); context "
                              "only, not this metric",
             "clocks": summarize_clocks(clk_lines),
+            # the spread of the timed steps (this rank's), beside the mean above
+            "step_ms_p10_p50_p90": [round(float(np.percentile(step_ms, q)), 5) for q in (10, 50, 90)],
         }
         if world > 1:
             # rank 0's own kernels in the timed steps (every rank launches its own share): the step's
