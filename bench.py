@@ -817,14 +817,17 @@ def run_profile(args):
 
 def run_e2e(torch, st, g, batch, dev, args, flops):
     """Same step through the public API with HOST buffers: every step copies its inputs from
-    pinned host memory (H2D) and reads its result back (D2H), all inside the timed region."""
+    pinned host memory (H2D) and reads its result back (D2H), all inside the timed region.  The
+    level input features stay in pinned host memory and each step moves only the halo windows of its
+    listed blocks (RefinementStep host_features: sphinx_gather_halo_windows reads them over PCIe);
+    maps, scores and latents are copied whole."""
     from paper_2511_18672_b200.step import RefinementStep
-    in_keys = ["O", "U", "tau_u", "q", "c0", "c1", "t", "x0", "eps", "lid", "lat_cache"] + \
-              [f"feat{l}" for l in range(st.cfg.L)]
+    in_keys = ["O", "U", "tau_u", "q", "c0", "c1", "t", "x0", "eps", "lid", "lat_cache"]
     host = {k: torch.from_numpy(np.ascontiguousarray(batch[k].view(np.int16) if batch[k].dtype == np.uint16
                                                      else batch[k])).pin_memory() for k in in_keys}
+    hfeat = {l: torch.from_numpy(np.ascontiguousarray(batch[f"feat{l}"]).view(np.int16)).pin_memory()
+             .view(torch.bfloat16) for l in range(st.cfg.L)}
     out_host = torch.empty(st.lat_out.shape, dtype=st.lat_out.dtype).pin_memory()
-    h2d = sum(h.numel() * h.element_size() for h in host.values())
     d2h = out_host.numel() * out_host.element_size()
 
     def copy_in(s_):
@@ -832,10 +835,17 @@ def run_e2e(torch, st, g, batch, dev, args, flops):
             dst = s_.d[k]
             (dst.view(torch.int16) if dst.dtype == torch.bfloat16 else dst).copy_(h, non_blocking=True)
 
+    # two input/output sets (one model state each), features read from the same pinned host maps
+    sts = [RefinementStep(st.cfg, batch, dev, st.ops, host_features=hfeat) for _ in range(2)]
+    graphs = [capture_step(torch, s_, with_conv_events=False)[0] for s_ in sts]
+    torch.cuda.synchronize()
+    h2d = sum(h.numel() * h.element_size() for h in host.values()) + sts[0].window_bytes()
+    full_feat = sum(h.numel() * h.element_size() for h in hfeat.values())
+
     def step():
-        copy_in(st)
-        g.replay()
-        out_host.copy_(st.lat_out, non_blocking=True)
+        copy_in(sts[0])
+        graphs[0].replay()
+        out_host.copy_(sts[0].lat_out, non_blocking=True)
 
     for _ in range(2):
         step()
@@ -849,12 +859,10 @@ def run_e2e(torch, st, g, batch, dev, args, flops):
     torch.cuda.synchronize()
     ms_serial = e0.elapsed_time(e1) / reps
 
-    # serving loop: two input/output sets (a second step over the same model state, its own
-    # graph); step j's H2D runs on a copy stream while step j-1 computes, the result D2H on a
-    # third stream (PCIe is full duplex).  Every step still copies all its inputs and reads its result.
-    st2 = RefinementStep(st.cfg, batch, dev, st.ops)
-    g2, _ = capture_step(torch, st2, with_conv_events=False)
-    sets = [(st, g, out_host), (st2, g2, torch.empty_like(out_host).pin_memory())]
+    # serving loop: step j's H2D runs on a copy stream while step j-1 computes (its feature windows
+    # cross PCIe inside its compute), the result D2H on a third stream.  Every step still moves all
+    # its inputs and reads its result.
+    sets = [(sts[0], graphs[0], out_host), (sts[1], graphs[1], torch.empty_like(out_host).pin_memory())]
     main = torch.cuda.current_stream()
     cs, ds = torch.cuda.Stream(), torch.cuda.Stream()
     freed = [torch.cuda.Event(), torch.cuda.Event()]
@@ -889,15 +897,18 @@ def run_e2e(torch, st, g, batch, dev, args, flops):
     e1.record(main)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n_pipe
-    del st2, g2
+    del sts, graphs
     return {"value": round(flops / (ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s", "ms_per_step": round(ms, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "feature_bytes_moved_vs_whole_maps": [int(h2d - sum(h.numel() * h.element_size()
+                                                               for h in host.values())), int(full_feat)],
             "steps_timed": n_pipe, "serial_ms_per_step": round(ms_serial, 4),
             "h2d_gbs": round(h2d / (ms * 1e-3) / 1e9, 1),
             "note": "serving loop, two input sets: step j's H2D (copy stream) overlaps step j-1's compute, the "
                     "result D2H on a third stream; serial_ms_per_step = copy, compute, read back one after the "
-                    "other.  Conv weights resident (model state); per-step opacity/uncertainty maps, level input "
-                    "features and latents H2D; the refined latent (the step's result) D2H"}
+                    "other.  Conv weights resident (model state); per step: opacity/uncertainty maps, scores and "
+                    "latents H2D whole, level input features as the halo windows of the listed blocks read from "
+                    "pinned host memory by sphinx_gather_halo_windows; the refined latent (the step's result) D2H"}
 
 
 def run_e2e_sharded(torch, st, batch, dev, args, flops, world):

@@ -197,6 +197,19 @@ SPHINX_API sphinx_status sphinx_compact_blocks_batch(const sphinx_compact_job* j
  * One 1024-thread CTA; no host synchronisation (the host reads pair back only to size the NCCL
  * send / recv of the owner gather).
  * ------------------------------------------------------------------------------- */
+/* Halo windows of listed blocks, copied map to map (same NHWC geometry [n][h][w][c], bf16 or fp32):
+ * for every listed block the pixels a 3x3 conv over it reads -- rows [by*b-1, by*b+b+1) x columns
+ * [bx*b-1, bx*b+b+1), clipped to the image, all channels -- go from src to dst; nothing else of dst
+ * is written.  src may be PINNED HOST memory (read by the GPU over PCIe through unified addressing):
+ * a serving loop whose level features arrive from the host then moves only what its convs read
+ * (refinement touches the selected blocks; their 1-pixel ring is the conv's halo).
+ * block_ids/count/capacity: a list of this geometry (device).  c * elem % 16 == 0; src, dst 16-B
+ * aligned.  Bit copy. */
+SPHINX_API sphinx_status sphinx_gather_halo_windows(const void* src, void* dst, sphinx_dtype dtype, int32_t n,
+                                                    int32_t h, int32_t w, int32_t c, int32_t block,
+                                                    const int32_t* block_ids, const int32_t* count,
+                                                    int32_t capacity, sphinx_stream_t stream);
+
 SPHINX_API sphinx_status sphinx_shard_plan(uint8_t* const* block_mask, const int32_t* blocks_per_frame,
                                            const int32_t* channels, int32_t n_levels, int32_t n,
                                            const int32_t* start_step, int32_t step_u, const int32_t* owner,

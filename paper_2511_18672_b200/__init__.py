@@ -41,7 +41,7 @@ EXPORTS = ("sphinx_abi_version", "sphinx_last_cuda_error", "sphinx_block_mask",
            "sphinx_sparse_conv3x3_gn_silu", "sphinx_compact_blocks_batch", "sphinx_sparse_conv3x3_ex",
            "sphinx_sparse_resblock_ex", "sphinx_temporal_attention_ex", "sphinx_gather_blocks",
            "sphinx_scatter_blocks", "sphinx_noise_inject_step",
-           "sphinx_conv_edge_plan", "sphinx_shard_plan")
+           "sphinx_conv_edge_plan", "sphinx_shard_plan", "sphinx_gather_halo_windows")
 
 _lib = None
 
@@ -115,6 +115,7 @@ def load(path=SO_PATH):
         "sphinx_block_mask": ([P, P, P, F, I, I, I, I, I, I, P, P, P, P, P], I),
         "sphinx_compact_blocks": ([P, I, I, I, P, I, I, P, P, P], I),
         "sphinx_shard_plan": ([P, P, P, I, I, P, I, P, I, I, P, P, P, P, P, P], I),
+        "sphinx_gather_halo_windows": ([P, P, I, I, I, I, I, I, P, P, I, P], I),
         "sphinx_noise_inject": ([P, P, P, I, I, I, I, I, P, P, I, P, P, I, P], I),
         "sphinx_sparse_conv3x3": ([P, P, P, P, I, I, I, I, I, I, I, P, P, I, P, Z, P], I),
         "sphinx_conv_workspace_size": ([I, I, I, I, I, I], Z),
@@ -412,6 +413,25 @@ def _block_copy(fn, src, dst, block, block_ids, count, capacity, stream, map_sid
     rc = getattr(load(), fn)(_ptr(src), _ptr(dst), F32 if src.dtype == torch.float32 else BF16, n, h, w, c,
                              int(block), _ptr(block_ids), _ptr(count), int(cap), _stream(stream))
     _chk(fn, rc)
+
+
+def sphinx_gather_halo_windows(src, dst, block, block_ids, count, capacity=None, stream=None):
+    """dst [N,H,W,C] <- the halo windows of the listed blocks of src (same shape and dtype); src may
+    be a PINNED host tensor, read by the GPU over PCIe (sphinx.h)."""
+    import torch
+    if src.dtype not in (torch.bfloat16, torch.float32) or dst.dtype != src.dtype or src.shape != dst.shape:
+        raise ValueError("src/dst: same shape and dtype, bf16 or fp32")
+    if not (src.is_contiguous() and (src.is_cuda or src.is_pinned())):
+        raise ValueError("src: contiguous CUDA or pinned host tensor")
+    if not (dst.is_cuda and dst.is_contiguous()):
+        raise ValueError("dst: contiguous CUDA tensor")
+    _dev(block_ids, torch.int32, "block_ids")
+    _dev(count, torch.int32, "count")
+    n, h, w, c = dst.shape
+    cap = block_ids.numel() if capacity is None else capacity
+    rc = load().sphinx_gather_halo_windows(_ptr(src), _ptr(dst), F32 if src.dtype == torch.float32 else BF16, n, h,
+                                           w, c, int(block), _ptr(block_ids), _ptr(count), int(cap), _stream(stream))
+    _chk("sphinx_gather_halo_windows", rc)
 
 
 def sphinx_gather_blocks(src, dst, block, block_ids, count, capacity=None, stream=None):

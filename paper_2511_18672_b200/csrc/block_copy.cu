@@ -69,7 +69,73 @@ static sphinx_status block_copy(bool pack, const void* src, void* dst, sphinx_dt
   return SPHINX_OK;
 }
 
+// Halo windows of listed blocks, map to map (same NHWC geometry): for every listed block, the pixels
+// a 3x3 conv over it reads -- rows [by*b - 1, by*b + b + 1) x columns [bx*b - 1, bx*b + b + 1),
+// clipped to the image -- are copied from src to dst.  src may be pinned host memory (read by the
+// GPU over PCIe through unified addressing): a serving loop then moves only the features its convs
+// read instead of whole maps.  One CTA task per (block, window row); each thread keeps 4 16-byte
+// loads in flight.  Overlapping windows of neighbouring blocks write identical bits.
+__global__ void __launch_bounds__(256) halo_window_kernel(const int4* __restrict__ src, int4* __restrict__ dst,
+                                                          int h, int w, int px_vec, int b, int hb, int wb,
+                                                          const int32_t* __restrict__ ids,
+                                                          const int32_t* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
+  const int cnt = *count;
+  const long long tasks = (long long)cnt * (b + 2);
+  for (long long t = blockIdx.x; t < tasks; t += gridDim.x) {
+    const int j = (int)(t / (b + 2)), r = (int)(t - (long long)j * (b + 2));
+    const int id = __ldg(ids + j);
+    const int n = id / (hb * wb), rem = id - n * (hb * wb);
+    const int by = rem / wb, bx = rem - by * wb;
+    const int y = by * b - 1 + r;
+    if (y < 0 || y >= h) continue;
+    const int x0 = max(bx * b - 1, 0), x1 = min(bx * b + b + 1, w);
+    const int words = (x1 - x0) * px_vec;
+    const size_t base = (((size_t)n * h + y) * w + x0) * px_vec;
+    for (int i0 = threadIdx.x; i0 < words; i0 += 4 * blockDim.x) {
+      int4 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q * blockDim.x;
+        if (i < words) v[q] = src[base + i];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q * blockDim.x;
+        if (i < words) dst[base + i] = v[q];
+      }
+    }
+  }
+}
+
 }  // namespace sphinx
+
+extern "C" sphinx_status sphinx_gather_halo_windows(const void* src, void* dst, sphinx_dtype dtype, int32_t n,
+                                                    int32_t h, int32_t w, int32_t c, int32_t block,
+                                                    const int32_t* block_ids, const int32_t* count,
+                                                    int32_t capacity, sphinx_stream_t stream) {
+  using namespace sphinx;
+  if (!src || !dst || !block_ids || !count || src == dst) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (n <= 0 || h <= 0 || w <= 0 || c <= 0 || block <= 0 || capacity < 0) return SPHINX_ERR_INVALID_ARGUMENT;
+  if (dtype != SPHINX_BF16 && dtype != SPHINX_F32) return SPHINX_ERR_INVALID_ARGUMENT;
+  const int hb = cdiv(h, block), wb = cdiv(w, block);
+  if ((int64_t)capacity > (int64_t)n * hb * wb) return SPHINX_ERR_INVALID_ARGUMENT;
+  const int elem = dtype == SPHINX_BF16 ? 2 : 4;
+  if (((int64_t)c * elem) % 16 != 0 || !aligned16(src) || !aligned16(dst)) return SPHINX_ERR_UNSUPPORTED;
+  int sms = 148;
+  sphinx_status st = check_device(&sms);
+  if (st != SPHINX_OK) return st;
+  if (capacity == 0) return SPHINX_OK;
+  const int px_vec = (int)((int64_t)c * elem / 16);
+  const long long tasks = (long long)capacity * (block + 2);
+  const int grid = (int)(tasks < (long long)sms * 16 ? tasks : (long long)sms * 16);
+  cudaError_t e = launch_k(halo_window_kernel, dim3(grid), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+                           static_cast<const int4*>(src), static_cast<int4*>(dst), (int)h, (int)w, px_vec,
+                           (int)block, hb, wb, block_ids, count);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return SPHINX_OK;
+}
 
 extern "C" sphinx_status sphinx_gather_blocks(const void* src, void* dst, sphinx_dtype dtype, int32_t n,
                                               int32_t h, int32_t w, int32_t c, int32_t block,

@@ -159,9 +159,14 @@ class RefinementStep:
     ops: the binding module (or a stand-in exposing the same calls).  group: torch.distributed
     process group or None (single rank)."""
 
-    def __init__(self, cfg, inputs, device, ops, group=None, rank=0, world=1):
+    def __init__(self, cfg, inputs, device, ops, group=None, rank=0, world=1, host_features=None):
+        """host_features: None (the level input features feat{l} are device-resident step inputs) or
+        {l: pinned host bf16 tensor [F,H_l,H_l,C_l]}: each step then moves only the halo windows of
+        its listed blocks over PCIe into the device maps (sphinx_gather_halo_windows), i.e. exactly
+        what the level's first conv reads."""
         import torch
         self.cfg, self.ops, self.torch = cfg, ops, torch
+        self.host_features = host_features
         self.dev = torch.device(device)
         self.rank, self.world = rank, world
         self.cuda = self.dev.type == "cuda"
@@ -202,7 +207,8 @@ class RefinementStep:
             self.ws.append(torch.zeros(max(nb, 256), dtype=u8, device=self.dev))
         # launches per step (single rank): mask 2 + compaction 1 + edge plans + noise 1 + convs + scatter 1
         n_edge = sum(1 for (h, _) in cfg.levels if h % b)
-        self.launches_per_step = 2 + 1 + n_edge + 1 + L * cfg.convs_per_level + 1
+        self.launches_per_step = 2 + 1 + n_edge + 1 + L * cfg.convs_per_level + 1 + \
+            (L if host_features is not None else 0)
         self.conv_events = None
         self.comm = None
         self._plan, self._plan_pending = None, False
@@ -321,6 +327,11 @@ class RefinementStep:
                   block_ids=self.ids[l], count=self.cnt[l]) for l in range(L)] +
             [dict(block_mask=self.masks[0], start_step=kk, step_u=cfg.u, select=ops.SELECT_NOISE,
                   block_ids=self.ids_noise, count=self.cnt_noise)])
+        if self.host_features is not None:
+            # features from the host: only the listed blocks' halo windows cross PCIe (well ahead of the
+            # convs, so each conv may still start INPUT_READY)
+            for l in range(L):
+                ops.sphinx_gather_halo_windows(self.host_features[l], d[f"feat{l}"], cfg.b, self.ids[l], self.cnt[l])
         # edge-class plans of the ragged levels right after compaction, so every conv of the step
         # reuses its level's plan and may start before its predecessor ends
         for l, (h, c) in enumerate(cfg.levels):
@@ -460,6 +471,17 @@ class RefinementStep:
         """Device time of the last step's owner-gather sections (pack, grouped send/recv, unpack)
         on the communication stream, summed over levels (call after synchronising)."""
         return sum(a.elapsed_time(b) for a, b in getattr(self, "comm_events", []))
+
+    def window_bytes(self):
+        """Bytes the halo-window gathers of the last step moved per level's list (host features)."""
+        cfg, out = self.cfg, 0
+        for l, (h, c) in enumerate(cfg.levels):
+            ids = self.ids[l][: int(self.cnt[l].item())].cpu().numpy() % (cfg.hb[l] ** 2)
+            by, bx = ids // cfg.hb[l], ids % cfg.hb[l]
+            rows = np.minimum(by * cfg.b + cfg.b + 1, h) - np.maximum(by * cfg.b - 1, 0)
+            cols = np.minimum(bx * cfg.b + cfg.b + 1, h) - np.maximum(bx * cfg.b - 1, 0)
+            out += int((rows * cols).sum()) * c * 2
+        return out
 
     def active_stats(self):
         """Algorithmic conv FLOPs of the step over the WHOLE batch (real active pixels of every
