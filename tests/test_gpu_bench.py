@@ -45,9 +45,9 @@ def test_bench_line_one_gpu():
 
 
 def test_bench_two_ranks_self_launch():
-    d = _run(["--gpus", "2", "--dist-backend", "gloo", "--share-gpu", "--steps", "2", "--warmup", "3",
-              "--no-e2e"])
+    d = _run(["--gpus", "2", "--dist-backend", "gloo", "--share-gpu", "--steps", "2", "--warmup", "3"])
     assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     m = d["multi_gpu"]
     assert m["ranks"] == 2 and m["plan_imbalance_max_over_mean"] >= 1.0 and m["bytes_moved_per_step"] > 0
     assert isinstance(d["gpu_launches"], int) and d["gpu_launches"] > 0
