@@ -71,10 +71,41 @@ static sphinx_status block_copy(bool pack, const void* src, void* dst, sphinx_dt
 
 // Halo windows of listed blocks, map to map (same NHWC geometry): for every listed block, the pixels
 // a 3x3 conv over it reads -- rows [by*b - 1, by*b + b + 1) x columns [bx*b - 1, bx*b + b + 1),
-// clipped to the image -- are copied from src to dst.  src may be pinned host memory (read by the
+// clipped to the image -- end up copied from src to dst.  src may be pinned host memory (read by the
 // GPU over PCIe through unified addressing): a serving loop then moves only the features its convs
-// read instead of whole maps.  One CTA task per (block, window row); each thread keeps 4 16-byte
-// loads in flight.  Overlapping windows of neighbouring blocks write identical bits.
+// read instead of whole maps.  Each block copies its own pixels and the parts of its 1-pixel ring that
+// belong to UNLISTED neighbours (a listed neighbour copies those pixels as its own), so every needed
+// pixel crosses once (a binary search of the ascending list tells listed from unlisted).  One CTA
+// task per (block, window row); each thread keeps 4 16-byte loads in flight.
+__device__ __forceinline__ bool listed(const int32_t* __restrict__ ids, int cnt, int id) {
+  int lo = 0, hi = cnt - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int v = __ldg(ids + mid);
+    if (v == id) return true;
+    if (v < id) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void copy_run(const int4* __restrict__ src, int4* __restrict__ dst, size_t base,
+                                         int words) {
+  for (int i0 = threadIdx.x; i0 < words; i0 += 4 * blockDim.x) {
+    int4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * blockDim.x;
+      if (i < words) v[q] = src[base + i];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * blockDim.x;
+      if (i < words) dst[base + i] = v[q];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) halo_window_kernel(const int4* __restrict__ src, int4* __restrict__ dst,
                                                           int h, int w, int px_vec, int b, int hb, int wb,
                                                           const int32_t* __restrict__ ids,
@@ -83,29 +114,34 @@ __global__ void __launch_bounds__(256) halo_window_kernel(const int4* __restrict
   pdl_trigger();
   const int cnt = *count;
   const long long tasks = (long long)cnt * (b + 2);
+  __shared__ int s_keep[3];  // this row's left ring pixel / middle run / right ring pixel: copy?
   for (long long t = blockIdx.x; t < tasks; t += gridDim.x) {
     const int j = (int)(t / (b + 2)), r = (int)(t - (long long)j * (b + 2));
     const int id = __ldg(ids + j);
     const int n = id / (hb * wb), rem = id - n * (hb * wb);
     const int by = rem / wb, bx = rem - by * wb;
     const int y = by * b - 1 + r;
-    if (y < 0 || y >= h) continue;
-    const int x0 = max(bx * b - 1, 0), x1 = min(bx * b + b + 1, w);
-    const int words = (x1 - x0) * px_vec;
-    const size_t base = (((size_t)n * h + y) * w + x0) * px_vec;
-    for (int i0 = threadIdx.x; i0 < words; i0 += 4 * blockDim.x) {
-      int4 v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + q * blockDim.x;
-        if (i < words) v[q] = src[base + i];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + q * blockDim.x;
-        if (i < words) dst[base + i] = v[q];
-      }
+    if (y < 0 || y >= h) continue;  // (uniform across the CTA)
+    // the block row owning pixel row y: by - 1 (top ring), by, or by + 1 (bottom ring)
+    const int oy = r == 0 ? by - 1 : (r == b + 1 ? by + 1 : by);
+    if (threadIdx.x < 3) {
+      const int ox = bx - 1 + (int)threadIdx.x;
+      bool keep;
+      if (ox < 0 || ox >= wb) keep = false;  // outside the image (clipped anyway)
+      else if (oy == by && ox == bx) keep = true;  // the block's own pixels
+      else keep = !listed(ids, cnt, (n * hb + oy) * wb + ox);
+      s_keep[threadIdx.x] = keep;
     }
+    __syncthreads();
+    const size_t row = ((size_t)n * h + y) * w;
+    // left ring pixel, middle run (b pixels, clipped), right ring pixel
+    const int xs[3] = {bx * b - 1, bx * b, bx * b + b};
+    const int xe[3] = {bx * b, min(bx * b + b, w), bx * b + b + 1};
+    for (int part = 0; part < 3; ++part) {
+      const int x0 = max(xs[part], 0), x1 = min(xe[part], w);
+      if (s_keep[part] && x1 > x0) copy_run(src, dst, (row + x0) * px_vec, (x1 - x0) * px_vec);
+    }
+    __syncthreads();  // s_keep is rewritten by the next task
   }
 }
 

@@ -473,14 +473,30 @@ class RefinementStep:
         return sum(a.elapsed_time(b) for a, b in getattr(self, "comm_events", []))
 
     def window_bytes(self):
-        """Bytes the halo-window gathers of the last step moved per level's list (host features)."""
+        """Bytes the halo-window gathers of the last step moved (host features): each listed block's
+        own pixels plus the parts of its 1-pixel ring owned by UNLISTED neighbour blocks (the rule of
+        sphinx_gather_halo_windows)."""
         cfg, out = self.cfg, 0
         for l, (h, c) in enumerate(cfg.levels):
-            ids = self.ids[l][: int(self.cnt[l].item())].cpu().numpy() % (cfg.hb[l] ** 2)
-            by, bx = ids // cfg.hb[l], ids % cfg.hb[l]
-            rows = np.minimum(by * cfg.b + cfg.b + 1, h) - np.maximum(by * cfg.b - 1, 0)
-            cols = np.minimum(bx * cfg.b + cfg.b + 1, h) - np.maximum(bx * cfg.b - 1, 0)
-            out += int((rows * cols).sum()) * c * 2
+            hb, b = cfg.hb[l], cfg.b
+            ids = self.ids[l][: int(self.cnt[l].item())].cpu().numpy().astype(np.int64)
+            is_listed = np.zeros(cfg.n_frames * hb * hb, bool)
+            is_listed[ids] = True
+            n, r = ids // (hb * hb), ids % (hb * hb)
+            by, bx = r // hb, r % hb
+            for rr in range(b + 2):
+                y = by * b - 1 + rr
+                oy = by - 1 if rr == 0 else (by + 1 if rr == b + 1 else by)
+                yok = (y >= 0) & (y < h)
+                for part, (xs, xe) in enumerate(((bx * b - 1, bx * b), (bx * b, np.minimum(bx * b + b, h)),
+                                                 (bx * b + b, bx * b + b + 1))):
+                    ox = bx - 1 + part
+                    inside = (ox >= 0) & (ox < hb) & (oy >= 0) & (oy < hb)
+                    own = (oy == by) & (ox == bx)
+                    nb = (n * hb + np.clip(oy, 0, hb - 1)) * hb + np.clip(ox, 0, hb - 1)
+                    keep = inside & (own | ~is_listed[nb])
+                    width = np.clip(np.minimum(xe, h) - np.maximum(xs, 0), 0, None)
+                    out += int((width * (keep & yok)).sum()) * c * 2
         return out
 
     def active_stats(self):
